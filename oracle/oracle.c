@@ -1,0 +1,535 @@
+/*
+ * oracle/oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of the online local
+ * Information Distribution (ID) of arxiv 2503.22588 (section III,
+ * P:127-222) and of the IDW query of Eq. 4.  It exists to prove the
+ * CUDA path right.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load it; the product library
+ * (paper_2503_22588_b200/, libnbt.so) never links, includes or calls it, and the
+ * two share no code, headers, tables or constants.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n, "S:n" = SPEC.md line n,
+ * "Qn" = the reading numbered n in DESIGN.md (paper silent / ambiguous).
+ * Everything is IEEE double, round-to-nearest, compiled with
+ * -ffp-contract=off (no FMA contraction), so each written operation is
+ * rounded exactly once.  Integer work uses int64 / __int128 so that no
+ * overflow reasoning is needed to read it.
+ *
+ * Parity status per function:
+ *   orc_trace_ray          pinned  (hand-traced rays, closed form, exact rational brute force)
+ *   orc_frame_q16          pinned  (orthonormality, centre/corner rays, d_h worked examples)
+ *   orc_id_compute         pinned  (SPEC worked examples, closed forms, invariants)
+ *                          absolute g_P values on a real scene: "parity unpinned" (paper prints none, T25)
+ *   orc_idw_query          pinned  (SPEC worked examples, convexity, H_NB identity)
+ *   orc_sample_perspectives pinned (forced-sample example, radius bounds, radial CDF)
+ *   orc_classify           pinned  (S:69-74 threshold rule examples)
+ *   orc_philox4x32         pinned  (published Random123 known-answer vectors)
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_OK 0
+#define ORC_ERR_INVALID_ARG 1
+#define ORC_ERR_DEGENERATE 2
+#define ORC_ERR_EMPTY 3
+#define ORC_ERR_SELFCHECK 9
+
+#define Q 65536            /* Q16: one voxel = 65536 units (Q19) */
+#define QLIM 1073741824LL  /* |coordinate| must stay below 2^30 (Q19) */
+
+/* ------------------------------------------------------------------ map (O-1) */
+
+typedef struct {
+    int32_t nx, ny, nz;
+    double voxel_size;       /* s_Vox */
+    double origin[3];        /* world position of voxel (0,0,0)'s min corner */
+    double gain[3];          /* g[U], g[F], g[O]  (Eq. 2, Q15) */
+    int32_t outside_policy;  /* 0 = outside counts as Unknown, 1 = clip */
+    const uint8_t *codes;    /* x fastest, nx*ny*nz */
+} orc_map;
+
+/* code of voxel (x,y,z); -1 if outside the grid */
+static int code_at(const orc_map *m, int64_t x, int64_t y, int64_t z)
+{
+    if (x < 0 || y < 0 || z < 0 || x >= m->nx || y >= m->ny || z >= m->nz) return -1;
+    return m->codes[x + (int64_t)m->nx * (y + (int64_t)m->ny * z)];
+}
+
+/* ---------------------------------------------------------------- camera (a5) */
+
+typedef struct {
+    int32_t width, height;           /* ray lattice W x H */
+    double fx, fy, cx, cy;           /* pinhole intrinsics in pixel units; 2cx = W-1, 2cy = H-1 */
+    int32_t add_corners;             /* append the 4 far-plane corner rays */
+    double tan_half_fov_h, tan_half_fov_v;
+} orc_camera;
+
+/* Corner-inclusive W x H lattice: pixel 0 and W-1 sit on the frustum borders
+ * d_h = d_Cam tan(FoV_h/2), d_v = d_Cam tan(FoV_v/2). */
+int orc_camera_from_fov(double fov_h, double fov_v, int32_t w, int32_t h, orc_camera *out)
+{
+    if (!out || w < 1 || h < 1 || !(fov_h > 0 && fov_h < M_PI) || !(fov_v > 0 && fov_v < M_PI))
+        return ORC_ERR_INVALID_ARG;
+    out->width = w;
+    out->height = h;
+    out->tan_half_fov_h = tan(fov_h / 2.0);
+    out->tan_half_fov_v = tan(fov_v / 2.0);
+    out->cx = (w - 1) / 2.0;
+    out->cy = (h - 1) / 2.0;
+    out->fx = (w > 1) ? (w - 1) / (2.0 * out->tan_half_fov_h) : 1.0;
+    out->fy = (h > 1) ? (h - 1) / (2.0 * out->tan_half_fov_v) : 1.0;
+    out->add_corners = 0;
+    return ORC_OK;
+}
+
+/* The paper's s_G lattice (Q6-Q8): spacing s_G * s_Vox on the far
+ * plane, centred on the axis, plus the 4 corner rays unless they coincide with
+ * lattice points (Q9). */
+int orc_camera_from_grid_scaling(double fov_h, double fov_v, double range, double voxel_size,
+                                 double s_g, orc_camera *out)
+{
+    if (!out || !(range > 0) || !(voxel_size > 0) || !(s_g >= 1.0) ||
+        !(fov_h > 0 && fov_h < M_PI) || !(fov_v > 0 && fov_v < M_PI))
+        return ORC_ERR_INVALID_ARG;
+    double delta = s_g * voxel_size;
+    double th = tan(fov_h / 2.0), tv = tan(fov_v / 2.0);
+    double d_h = range * th, d_v = range * tv;
+    /* lattice offsets m*delta with |m*delta| <= d_h, judged with a 1e-9 relative
+     * tolerance so that tan(pi/4) = 0.9999999999999999 still yields the border point */
+    double rh = d_h / delta, rv = d_v / delta;
+    double mh = floor(rh + 1e-9), mv = floor(rv + 1e-9);
+    if (mh > 100000 || mv > 100000) return ORC_ERR_INVALID_ARG;
+    out->width = 2 * (int32_t)mh + 1;
+    out->height = 2 * (int32_t)mv + 1;
+    out->cx = mh;
+    out->cy = mv;
+    out->fx = range / delta;
+    out->fy = range / delta;
+    out->tan_half_fov_h = th;
+    out->tan_half_fov_v = tv;
+    out->add_corners = !(fabs(rh - mh) <= 1e-9 && fabs(rv - mv) <= 1e-9);
+    return ORC_OK;
+}
+
+int32_t orc_camera_num_rays(const orc_camera *cam)
+{
+    return cam->width * cam->height + (cam->add_corners ? 4 : 0);
+}
+
+/* -------------------------------------------------- frame + Q16 (a4, O-2, O-3) */
+
+typedef struct {
+    int32_t o[3];     /* origin p_P in Q16 voxel coordinates */
+    int32_t a[3];     /* axis: (range/s) * fwd */
+    int32_t rh[3];    /* half-pixel step along right */
+    int32_t uh[3];    /* half-pixel step along up */
+    int32_t rc[3];    /* corner offset along right (range/s * tan_h) */
+    int32_t uc[3];    /* corner offset along up */
+} orc_frame;
+
+static int rne_q16(double v, int32_t *out)
+{
+    double q = v * 65536.0;                 /* exact: power of two */
+    if (!(fabs(q) < (double)QLIM)) return ORC_ERR_INVALID_ARG;
+    *out = (int32_t)nearbyint(q);           /* round half to even (default mode) */
+    return ORC_OK;
+}
+
+/* Orientation: the view axis points from p_P to the PoI; roll fixed by
+ * up-hint +z, fallback +x (Q4); far plane flat at d_Cam (Q5). */
+int orc_frame_q16(const orc_map *m, const double poi[3], const double p[3], const orc_camera *cam,
+                  double range, orc_frame *f, double fwd_out[3], double right_out[3], double up_out[3])
+{
+    double d[3] = {poi[0] - p[0], poi[1] - p[1], poi[2] - p[2]};
+    if (d[0] == 0.0 && d[1] == 0.0 && d[2] == 0.0) return ORC_ERR_DEGENERATE;   /* Q18 */
+    double n = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+    double fwd[3] = {d[0] / n, d[1] / n, d[2] / n};
+    double c[3] = {fwd[1], -fwd[0], 0.0};                      /* fwd x z */
+    double nc = sqrt((c[0] * c[0] + c[1] * c[1]) + c[2] * c[2]);
+    if (nc < 1e-6) {
+        c[0] = 0.0; c[1] = fwd[2]; c[2] = -fwd[1];              /* fwd x x */
+        nc = sqrt((c[0] * c[0] + c[1] * c[1]) + c[2] * c[2]);
+    }
+    double right[3] = {c[0] / nc, c[1] / nc, c[2] / nc};
+    double up[3] = {right[1] * fwd[2] - right[2] * fwd[1],
+                    right[2] * fwd[0] - right[0] * fwd[2],
+                    right[0] * fwd[1] - right[1] * fwd[0]};
+    double s = m->voxel_size;
+    double rs = range / s;
+    double hx = rs / (2.0 * cam->fx);
+    double hy = rs / (2.0 * cam->fy);
+    double ch = rs * cam->tan_half_fov_h;
+    double cv = rs * cam->tan_half_fov_v;
+    int st = ORC_OK;
+    for (int k = 0; k < 3; ++k) {
+        st |= rne_q16((p[k] - m->origin[k]) / s, &f->o[k]);
+        st |= rne_q16(rs * fwd[k], &f->a[k]);
+        st |= rne_q16(hx * right[k], &f->rh[k]);
+        st |= rne_q16(hy * up[k], &f->uh[k]);
+        st |= rne_q16(ch * right[k], &f->rc[k]);
+        st |= rne_q16(cv * up[k], &f->uc[k]);
+    }
+    if (fwd_out) memcpy(fwd_out, fwd, sizeof fwd);
+    if (right_out) memcpy(right_out, right, sizeof right);
+    if (up_out) memcpy(up_out, up, sizeof up);
+    return st ? ORC_ERR_INVALID_ARG : ORC_OK;
+}
+
+/* Endpoint of ray k (O-4): k runs row-major over (row kk, column i); corner rays
+ * follow in the order (-,-), (+,-), (-,+), (+,+).  Returns INVALID_ARG if any
+ * coordinate leaves (-2^30, 2^30). */
+static int ray_endpoint(const orc_frame *f, const orc_camera *cam, int32_t k, int32_t e[3])
+{
+    int64_t v[3];
+    int32_t nlat = cam->width * cam->height;
+    if (k < nlat) {
+        int64_t i = k % cam->width, kk = k / cam->width;
+        int64_t mi = 2 * i - (cam->width - 1), mk = 2 * kk - (cam->height - 1);
+        for (int c = 0; c < 3; ++c)
+            v[c] = (int64_t)f->o[c] + f->a[c] + mi * f->rh[c] + mk * f->uh[c];
+    } else {
+        int32_t q = k - nlat;
+        int64_t sr = (q & 1) ? 1 : -1, su = (q & 2) ? 1 : -1;
+        for (int c = 0; c < 3; ++c)
+            v[c] = (int64_t)f->o[c] + f->a[c] + sr * f->rc[c] + su * f->uc[c];
+    }
+    for (int c = 0; c < 3; ++c) {
+        if (v[c] <= -QLIM || v[c] >= QLIM) return ORC_ERR_INVALID_ARG;
+        e[c] = (int32_t)v[c];
+    }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------ exact DDA (a6, O-5, Q13) */
+
+typedef struct {
+    int64_t n_u, n_f, n_o;   /* per-state counts of the N_O counted voxels (Eq. 2) */
+    int64_t lookups;         /* in-grid visits (memory-touching subset) */
+    int64_t visits;          /* voxels visited including uncounted (clipped) ones */
+    double g;                /* g_R = sum of g(v_i) over the counted voxels, in visit order */
+    int32_t stop;            /* 0 = reached the endpoint voxel, 1 = stopped on Occupied */
+} orc_ray;
+
+static int64_t floor_div_q(int64_t a) { return (a >= 0) ? a / Q : -((-a + Q - 1) / Q); }
+
+/*
+ * Walk the voxels of the segment O -> E (Q16 voxel coordinates).
+ *
+ * Definition followed: the point P(t) = O + t (E - O), t in [0,1], lies in voxel
+ * floor(P(t)) (half-open voxels, O-1).  Moving in +a the index changes AT the
+ * boundary parameter; moving in -a it changes just AFTER it.  Events are
+ * therefore ordered by (t, positive-before-negative, axis x<y<z); same-sign
+ * simultaneous crossings (edges/corners) are taken one axis at a time in axis
+ * order, which keeps the path 6-connected (Q13).  The walk visits exactly
+ * 1 + sum_a |floor(E_a) - floor(O_a)| voxels when it does not stop early.
+ *
+ * Each visited voxel is scored by its state (Eq. 2): outside the
+ * grid is Unknown (Q14) unless the clip policy is set; the walk stops
+ * after the first Occupied voxel, which is counted (Q11); the origin
+ * voxel is counted (Q12).  If ijk_out != NULL the visited voxels (up to
+ * max_visits) are written there and their codes (0/1/2, 255 = outside) to
+ * code_out.
+ */
+int orc_trace_ray(const orc_map *m, const int32_t o[3], const int32_t e[3], int32_t max_visits,
+                  int32_t *ijk_out, uint8_t *code_out, int32_t *len_out, orc_ray *r)
+{
+    int64_t v[3], ve[3], D[3], N[3];
+    int neg[3];
+    int64_t nsteps = 0;
+    for (int a = 0; a < 3; ++a) {
+        if (o[a] <= -QLIM || o[a] >= QLIM || e[a] <= -QLIM || e[a] >= QLIM) return ORC_ERR_INVALID_ARG;
+        v[a] = floor_div_q(o[a]);
+        ve[a] = floor_div_q(e[a]);
+        D[a] = (int64_t)e[a] - o[a];
+        neg[a] = D[a] < 0;
+        /* distance (in Q16 units) from O to the next boundary crossed along a */
+        N[a] = neg[a] ? (int64_t)o[a] - v[a] * Q : (v[a] + 1) * Q - o[a];
+        nsteps += llabs(ve[a] - v[a]);
+    }
+    memset(r, 0, sizeof *r);
+    int32_t len = 0;
+    for (int64_t s = 0;; ++s) {
+        /* visit v */
+        int code = code_at(m, v[0], v[1], v[2]);
+        if (ijk_out && len < max_visits) {
+            ijk_out[3 * len + 0] = (int32_t)v[0];
+            ijk_out[3 * len + 1] = (int32_t)v[1];
+            ijk_out[3 * len + 2] = (int32_t)v[2];
+            code_out[len] = (code < 0) ? 255 : (uint8_t)code;
+        }
+        ++len;
+        r->visits++;
+        if (code >= 0) r->lookups++;
+        if (code < 0 && m->outside_policy == 1) {
+            /* clipped: not counted */
+        } else {
+            int c = code < 0 ? 0 : code;
+            r->g += m->gain[c];
+            if (c == 0) r->n_u++;
+            else if (c == 1) r->n_f++;
+            else { r->n_o++; r->stop = 1; break; }
+        }
+        if (s == nsteps) break;
+        /* next event: active axis with the smallest (N_a/|D_a|, neg_a, a) */
+        int best = -1;
+        for (int a = 0; a < 3; ++a) {
+            if (D[a] == 0) continue;
+            if (best < 0) { best = a; continue; }
+            __int128 lhs = (__int128)N[a] * (D[best] < 0 ? -D[best] : D[best]);
+            __int128 rhs = (__int128)N[best] * (D[a] < 0 ? -D[a] : D[a]);
+            if (lhs < rhs || (lhs == rhs && neg[a] < neg[best])) best = a;
+        }
+        v[best] += neg[best] ? -1 : 1;
+        N[best] += Q;
+    }
+    if (len_out) *len_out = len;
+    return ORC_OK;
+}
+
+/* ---------------------------------------------- ID per perspective (a7, a8, O-6) */
+
+typedef struct {
+    double xyz[3];
+    double gain;                  /* g_P,j */
+    int64_t t_u, t_f, t_o, lookups;
+} orc_persp_out;
+
+/* g_P,j for perspective j = (1/N_E) sum_k g_R,k,j with
+ * g_R,k,j = sum over the N_O counted voxels of g(v_i) (Eq. 2).
+ * Canonical form (Q26): ((T_U g_U + T_F g_F) + T_O g_O) / N_E from integer
+ * per-state totals.  The direct ray-order sum is also computed and must agree
+ * within 1e-12 relative (self-check of the two readings of P:214). */
+static int one_perspective(const orc_map *m, const double poi[3], const double p[3],
+                           const orc_camera *cam, double range, orc_persp_out *out)
+{
+    orc_frame f;
+    int st = orc_frame_q16(m, poi, p, cam, range, &f, NULL, NULL, NULL);
+    if (st) return st;
+    int32_t ne = orc_camera_num_rays(cam);
+    int64_t tu = 0, tf = 0, to = 0, tl = 0;
+    double direct = 0.0;
+    for (int32_t k = 0; k < ne; ++k) {
+        int32_t e[3];
+        if ((st = ray_endpoint(&f, cam, k, e))) return st;
+        orc_ray r;
+        if ((st = orc_trace_ray(m, f.o, e, 0, NULL, NULL, NULL, &r))) return st;
+        direct += r.g;
+        tu += r.n_u; tf += r.n_f; to += r.n_o; tl += r.lookups;
+    }
+    double canon = (((double)tu * m->gain[0] + (double)tf * m->gain[1]) + (double)to * m->gain[2]) / (double)ne;
+    direct = direct / (double)ne;
+    double scale = fabs(canon) > 1.0 ? fabs(canon) : 1.0;
+    if (fabs(direct - canon) > 1e-12 * scale) return ORC_ERR_SELFCHECK;
+    memcpy(out->xyz, p, 3 * sizeof(double));
+    out->gain = canon;
+    out->t_u = tu; out->t_f = tf; out->t_o = to; out->lookups = tl;
+    return ORC_OK;
+}
+
+/* The whole ID: every perspective j of the set, in input order (O-7).
+ * Perspectives are independent; nthreads > 1 only spreads them over host
+ * cores (each perspective is still evaluated by the same sequential loop).
+ * Returns the first failing perspective's index in *bad_index. */
+int orc_id_compute(const orc_map *m, const double poi[3], const double *persp, int32_t n_persp,
+                   const orc_camera *cam, double range, int32_t nthreads,
+                   double *xyz_out, double *gain_out, int64_t *counts_out, int32_t *bad_index)
+{
+    if (!m || !poi || !persp || !cam || n_persp < 0 || !(range > 0)) return ORC_ERR_INVALID_ARG;
+    if (cam->width < 1 || cam->height < 1) return ORC_ERR_INVALID_ARG;
+    int status = ORC_OK;
+    int32_t bad = -1;
+#ifdef _OPENMP
+    if (nthreads < 1) nthreads = 1;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+#endif
+    for (int32_t j = 0; j < n_persp; ++j) {
+        orc_persp_out o;
+        int st = one_perspective(m, poi, persp + 3 * (int64_t)j, cam, range, &o);
+        if (st) {
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+            {
+                if (bad < 0 || j < bad) { bad = j; status = st; }
+            }
+            continue;
+        }
+        if (xyz_out) memcpy(xyz_out + 3 * (int64_t)j, o.xyz, 3 * sizeof(double));
+        if (gain_out) gain_out[j] = o.gain;
+        if (counts_out) {
+            counts_out[4 * (int64_t)j + 0] = o.t_u;
+            counts_out[4 * (int64_t)j + 1] = o.t_f;
+            counts_out[4 * (int64_t)j + 2] = o.t_o;
+            counts_out[4 * (int64_t)j + 3] = o.lookups;
+        }
+    }
+    if (bad_index) *bad_index = bad;
+    return status;
+}
+
+/* Rays of one perspective, for per-ray parity: endpoints (Q16) and counts. */
+int orc_perspective_rays(const orc_map *m, const double poi[3], const double p[3],
+                         const orc_camera *cam, double range, int32_t *o_out, int32_t *e_out,
+                         int64_t *ray_counts_out /* ne x 5: U,F,O,lookups,stop */)
+{
+    orc_frame f;
+    int st = orc_frame_q16(m, poi, p, cam, range, &f, NULL, NULL, NULL);
+    if (st) return st;
+    int32_t ne = orc_camera_num_rays(cam);
+    if (o_out) memcpy(o_out, f.o, sizeof f.o);
+    for (int32_t k = 0; k < ne; ++k) {
+        int32_t e[3];
+        if ((st = ray_endpoint(&f, cam, k, e))) return st;
+        if (e_out) memcpy(e_out + 3 * (int64_t)k, e, sizeof e);
+        if (ray_counts_out) {
+            orc_ray r;
+            if ((st = orc_trace_ray(m, f.o, e, 0, NULL, NULL, NULL, &r))) return st;
+            int64_t *rc = ray_counts_out + 5 * (int64_t)k;
+            rc[0] = r.n_u; rc[1] = r.n_f; rc[2] = r.n_o; rc[3] = r.lookups; rc[4] = r.stop;
+        }
+    }
+    return ORC_OK;
+}
+
+/* Frame export for tests: o,a,rh,uh,rc,uc (18 int32) and fwd,right,up (9 doubles). */
+int orc_frame_export(const orc_map *m, const double poi[3], const double p[3], const orc_camera *cam,
+                     double range, int32_t *q16_out, double *axes_out)
+{
+    orc_frame f;
+    int st = orc_frame_q16(m, poi, p, cam, range, &f, axes_out, axes_out ? axes_out + 3 : NULL,
+                           axes_out ? axes_out + 6 : NULL);
+    if (st) return st;
+    if (q16_out) memcpy(q16_out, &f, sizeof f);
+    return ORC_OK;
+}
+
+/* ----------------------------------------------------- IDW query (a9, Eq. 4, O-8) */
+
+/* G(x) = sum_u w_u * v_u(x),  v_u = sum_j g_j d_j^-p / sum_j d_j^-p,
+ * over buffer entries u = 0 (oldest) .. m-1 (newest); w_u = 1/(m-u) so the
+ * newest entry weighs 1 (Q21); with a full buffer m = N_B this is the
+ * paper's 1/(N_B - u).  If a perspective is closer than zero_eps, v_u is the
+ * gain of the nearest one (lowest j among ties) (Q23).  Sums over all
+ * perspectives of the entry (Q22).  normalize != 0 divides by sum_u w_u. */
+int orc_idw_query(int32_t n_entries, const int32_t *entry_sizes, const double *const *entry_xyz,
+                  const double *const *entry_gain, const double *query_xyz, int32_t n_q,
+                  double power_p, double zero_eps, int32_t normalize, double *g_out)
+{
+    if (n_entries <= 0) return ORC_ERR_EMPTY;
+    for (int32_t e = 0; e < n_entries; ++e)
+        if (entry_sizes[e] <= 0) return ORC_ERR_INVALID_ARG;
+    for (int32_t q = 0; q < n_q; ++q) {
+        const double *x = query_xyz + 3 * (int64_t)q;
+        double g = 0.0, wsum = 0.0;
+        for (int32_t e = 0; e < n_entries; ++e) {
+            const double *P = entry_xyz[e];
+            const double *G = entry_gain[e];
+            int32_t np = entry_sizes[e];
+            int32_t nearest = -1;
+            double dmin = 0.0;
+            double num = 0.0, den = 0.0;
+            for (int32_t j = 0; j < np; ++j) {
+                double dx = x[0] - P[3 * j], dy = x[1] - P[3 * j + 1], dz = x[2] - P[3 * j + 2];
+                double d2 = (dx * dx + dy * dy) + dz * dz;
+                double d = sqrt(d2);
+                if (nearest < 0 || d < dmin) { nearest = j; dmin = d; }
+                double w = (power_p == 2.0) ? 1.0 / d2 : pow(d2, -power_p / 2.0);
+                num += G[j] * w;
+                den += w;
+            }
+            double v = (dmin < zero_eps) ? G[nearest] : num / den;
+            double wu = 1.0 / (double)(n_entries - e);
+            g += wu * v;
+            wsum += wu;
+        }
+        g_out[q] = normalize ? g / wsum : g;
+    }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------ sampler (a3, Eq. 1, O-9, Q1-Q3) */
+
+/* Philox4x32-10 (Salmon et al., Random123): counter-based, so the same draws
+ * can be reproduced anywhere from (seed, counter). */
+void orc_philox4x32(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+static double u01(uint32_t b) { return ((double)b + 0.5) * (1.0 / 4294967296.0); }
+
+/* p_P = p_POI + r_S X_R^{1/3} X / ||X||  (Eq. 1, P:149-151 with the PoI offset, Q2),
+ * X ~ N(0, I_3) by Box-Muller (Muller's method), X_R ~ U(0,1) (Q1);
+ * mode 1 ("surface") uses X_R = 1 (Q3).  Draw j, attempt a uses Philox counters
+ * (j, a, 0, 0) for the normals and (j, a, 1, 0) for X_R; ||X|| < 1e-12 is
+ * resampled with a+1. */
+int orc_sample_perspectives(const double poi[3], double r_s, int32_t n, uint64_t seed, int32_t mode,
+                            double *xyz_out)
+{
+    if (!poi || !xyz_out || n < 0 || !(r_s > 0) || (mode != 0 && mode != 1)) return ORC_ERR_INVALID_ARG;
+    const double two_pi = 6.283185307179586;
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int32_t j = 0; j < n; ++j) {
+        for (uint32_t attempt = 0;; ++attempt) {
+            uint32_t c0[4] = {(uint32_t)j, attempt, 0u, 0u}, b[4];
+            orc_philox4x32(c0, key, b);
+            double u0 = u01(b[0]), u1 = u01(b[1]), u2 = u01(b[2]), u3 = u01(b[3]);
+            double r01 = sqrt(-2.0 * log(u0)), r23 = sqrt(-2.0 * log(u2));
+            double X[3] = {r01 * cos(two_pi * u1), r01 * sin(two_pi * u1), r23 * cos(two_pi * u3)};
+            double nx = sqrt((X[0] * X[0] + X[1] * X[1]) + X[2] * X[2]);
+            if (nx < 1e-12) continue;
+            double xr = 1.0;
+            if (mode == 0) {
+                uint32_t c1[4] = {(uint32_t)j, attempt, 1u, 0u}, b1[4];
+                orc_philox4x32(c1, key, b1);
+                xr = u01(b1[0]);
+            }
+            double scale = r_s * cbrt(xr);
+            for (int k = 0; k < 3; ++k) xyz_out[3 * (int64_t)j + k] = poi[k] + scale * (X[k] / nx);
+            break;
+        }
+    }
+    return ORC_OK;
+}
+
+/* The Eq. 1 map applied to given draws (forced-sample pins). */
+void orc_eq1(const double poi[3], double r_s, const double X[3], double x_r, double out[3])
+{
+    double nx = sqrt((X[0] * X[0] + X[1] * X[1]) + X[2] * X[2]);
+    double scale = r_s * cbrt(x_r);
+    for (int k = 0; k < 3; ++k) out[k] = poi[k] + scale * (X[k] / nx);
+}
+
+/* ------------------------------------------------- classification (Q16) */
+
+/* unobserved -> Unknown; P >= t_occ -> Occupied; P <= t_free -> Free; else Unknown. */
+void orc_classify(const float *p, const uint8_t *observed, int64_t n, double t_occ, double t_free,
+                  uint8_t *codes_out)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        if (!observed[i]) codes_out[i] = 0;
+        else if ((double)p[i] >= t_occ) codes_out[i] = 2;
+        else if ((double)p[i] <= t_free) codes_out[i] = 1;
+        else codes_out[i] = 0;
+    }
+}
+
+int orc_version(void) { return 1; }
