@@ -1,0 +1,233 @@
+/*
+ * nbt.h -- C ABI of libnbt, the B200-native online local Information Distribution (ID)
+ * of arxiv 2503.22588 ("Next-Best-Trajectory planning ... GPU-parallel online local
+ * Information Distribution").  Citations: P:n = /root/reference/PAPER.md line n,
+ * S:n = SPEC.md line n, Qn = reading n in DESIGN.md section 2.
+ *
+ * The library computes, on one CUDA device (sm_100a):
+ *   * the voxel-map store (three states, 2-bit packed, L2-resident)
+ *   * perspective sampling by Eq. 1
+ *   * per-perspective frames and far-plane endpoint lattices
+ *   * raycasting with early stop + Eq. 2 scoring
+ *   * the per-perspective mean -> the IG point cloud
+ *   * the IDW query of Eq. 4 over the last N_B clouds
+ *
+ * Conventions for every function:
+ *   * Return codes only; nothing throws or aborts across the ABI.  On failure a
+ *     human-readable detail is available from nbt_last_error_message() (thread-local).
+ *   * OWNERSHIP: the library owns everything behind a handle; the caller creates and
+ *     destroys handles.  Input arrays are borrowed for the duration of the call only:
+ *     host inputs are copied (staged) before the call returns, so the caller may free
+ *     or reuse them immediately.  Output arrays are caller-owned.
+ *   * "on_device" flags say whether a pointer is device memory of the ctx's device (1)
+ *     or host memory (0).  Device pointers must stay valid until the enqueued work
+ *     completes.
+ *   * ASYNCHRONY: work is enqueued on the ctx stream.  Results written to device
+ *     buffers are valid after nbt_ctx_sync() or a sync of that stream.  Results written
+ *     to HOST buffers are valid when the call returns (the call synchronizes the
+ *     stream).  Calls on one ctx are executed in stream order, so nbt_map_update()
+ *     issued after nbt_id_compute() never changes what that compute reads (the
+ *     single-writer snapshot rule).
+ *   * Validation of host inputs happens before enqueueing and returns the error.
+ *     Validation of DEVICE inputs happens on the device: offending elements are
+ *     skipped / flagged and the error is returned by the next nbt_ctx_sync().
+ *   * A ctx is not thread-safe.  Distinct ctxs share nothing.
+ *   * Coordinates: world units (metres in the paper's experiments).  A map maps
+ *     world point w to voxel floor((w - origin) / voxel_size) (half-open voxels).
+ */
+#ifndef NBT_H_
+#define NBT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NBT_ABI_VERSION 1
+
+typedef enum {
+    NBT_OK = 0,
+    NBT_ERR_INVALID_ARG = 1,    /* null pointer, bad size, non-finite value, code >= 3, Q16 overflow */
+    NBT_ERR_DEGENERATE = 2,     /* a perspective coincides with the PoI (Q18) */
+    NBT_ERR_EMPTY = 3,          /* IDW query on an empty buffer ("no distribution available") */
+    NBT_ERR_OUT_OF_MEMORY = 4,
+    NBT_ERR_CUDA = 5,           /* a CUDA runtime error; the message names it */
+    NBT_ERR_NCCL = 6,           /* reserved for collective failures reported by the caller's layer */
+    NBT_ERR_STATE = 7           /* wrong handle state (e.g. map of another ctx) */
+} nbt_status;
+
+int         nbt_abi_version(void);
+const char *nbt_status_string(nbt_status s);
+const char *nbt_last_error_message(void);
+
+/* ---------------------------------------------------------------- context */
+
+typedef struct nbt_ctx_s *nbt_ctx;
+
+/* Bind to CUDA device `device`.  `cuda_stream` is a borrowed cudaStream_t (NULL = the
+ * ctx creates and owns a non-blocking stream).  The ctx owns scratch buffers that grow
+ * on demand. */
+nbt_status nbt_ctx_create(int device, void *cuda_stream, nbt_ctx *out);
+/* Replace the borrowed stream (e.g. torch.cuda.current_stream()).  NULL = own stream. */
+nbt_status nbt_ctx_set_stream(nbt_ctx ctx, void *cuda_stream);
+/* Wait for all enqueued work; returns the first device-side validation error recorded
+ * since the previous sync (and clears it), else NBT_OK. */
+nbt_status nbt_ctx_sync(nbt_ctx ctx);
+void       nbt_ctx_destroy(nbt_ctx ctx);
+/* Number of kernels libnbt has launched on this ctx since creation. */
+uint64_t   nbt_ctx_launch_count(nbt_ctx ctx);
+
+/* Optional per-kernel device timing with CUDA events recorded on the ctx stream around
+ * each launch of the named kernel family (used by bench.py for the roofline). */
+enum {
+    NBT_KERNEL_TRACE = 0,       /* k_id_trace: rows a5-a8, the hot loop */
+    NBT_KERNEL_FRAMES = 1,      /* k_persp_frames: row a4 */
+    NBT_KERNEL_FINALIZE = 2,    /* k_id_finalize: row a8 */
+    NBT_KERNEL_IDW = 3,         /* k_idw_query: row a9 */
+    NBT_KERNEL_SAMPLE = 4,      /* k_sample_perspectives: row a3 */
+    NBT_KERNEL_MAP_UPDATE = 5,  /* k_delta_keys + radix sort + k_delta_apply: row a2 */
+    NBT_KERNEL_COUNT = 6
+};
+nbt_status nbt_ctx_set_profiling(nbt_ctx ctx, int enable);
+/* Sum of the recorded durations (ms) and number of launches of `kernel` since the last
+ * reset; synchronizes the stream.  reset != 0 clears the record. */
+nbt_status nbt_ctx_profile_read(nbt_ctx ctx, int32_t kernel, double *total_ms, uint64_t *launches, int reset);
+
+/* ------------------------------------------------------- voxel map (row a1, a2) */
+
+enum { NBT_UNKNOWN = 0, NBT_FREE = 1, NBT_OCCUPIED = 2 };      /* three states (Eq. 2) */
+enum { NBT_OUTSIDE_UNKNOWN = 0, NBT_OUTSIDE_CLIP = 1 };        /* Q14 */
+
+typedef struct nbt_map_s *nbt_map;
+
+typedef struct {
+    int32_t nx, ny, nz;       /* voxels per axis, each >= 1; (nx+2)(ny+2)(nz+2) < 2^32 */
+    double  voxel_size;       /* s_Vox > 0 (1 cm) */
+    double  origin[3];        /* world position of voxel (0,0,0)'s min corner */
+    double  gain[3];          /* g[U], g[F], g[O] of Eq. 2 as per-state constants (Q15);
+                                 default {1.0, 0.12, 0.03}; each finite, >= 0 */
+    int32_t outside_policy;   /* NBT_OUTSIDE_UNKNOWN (default) or NBT_OUTSIDE_CLIP */
+} nbt_map_desc;
+
+/* Fill *desc with the defaults above for an nx*ny*nz grid of voxel_size at origin 0. */
+void nbt_map_desc_default(nbt_map_desc *desc, int32_t nx, int32_t ny, int32_t nz, double voxel_size);
+/* Create a map whose every voxel is Unknown (UFOMap's default). */
+nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out);
+/* Replace all voxels: codes[x + nx*(y + ny*z)] in {0,1,2}; n must equal nx*ny*nz.
+ * Synchronizes the ctx stream; a code >= 3 gives NBT_ERR_INVALID_ARG (map unchanged
+ * for host input; for device input the offending voxels become Unknown). */
+nbt_status nbt_map_upload(nbt_map map, const uint8_t *codes, size_t n, int on_device);
+/* Replace all voxels from occupancy probabilities (Q16): observed[i] == 0 ->
+ * Unknown; p[i] >= t_occ -> Occupied; p[i] <= t_free -> Free; else Unknown. */
+nbt_status nbt_map_upload_prob(nbt_map map, const float *p, const uint8_t *observed, size_t n,
+                               int on_device, double t_occ, double t_free);
+/* Apply n sparse deltas: voxel (ijk[3i], ijk[3i+1], ijk[3i+2]) := codes[i].  Indices must
+ * lie inside the grid and codes in {0,1,2}.  Duplicated voxels resolve to the LAST delta
+ * in array order (Q30).  Stream-ordered after earlier work on the ctx.  n == 0 is a no-op. */
+nbt_status nbt_map_update(nbt_map map, const int32_t *ijk, const uint8_t *codes, size_t n, int on_device);
+/* Device pointer and size of the packed store (for an in-place NCCL broadcast of a
+ * replica; every replica has the same layout for the same desc). */
+nbt_status nbt_map_device_buffer(nbt_map map, void **dev_ptr, size_t *bytes);
+/* Unpack to dense x-fastest uint8 codes (host buffer of n = nx*ny*nz bytes); syncs. */
+nbt_status nbt_map_download(nbt_map map, uint8_t *codes_out, size_t n);
+/* Copy of the descriptor. */
+nbt_status nbt_map_get_desc(nbt_map map, nbt_map_desc *out);
+void       nbt_map_destroy(nbt_map map);
+
+/* ------------------------------------------------------------ camera (row a5) */
+
+typedef struct {
+    int32_t width, height;          /* ray lattice W x H (>= 1 each) */
+    double  fx, fy, cx, cy;         /* pinhole intrinsics, pixel units; 2cx = W-1, 2cy = H-1 */
+    int32_t add_corners;            /* 1 = append the 4 far-plane corner rays (s_G mode) */
+    double  tan_half_fov_h, tan_half_fov_v;   /* tan(FoV/2), used for the corner rays */
+} nbt_camera;
+
+/* Corner-inclusive W x H lattice spanning the FoV on the far plane at d_Cam:
+ * ray (i, kk) ends at  p_P + d_Cam*fwd + (i-cx)/fx*d_Cam*right + (kk-cy)/fy*d_Cam*up,
+ * fx = (W-1)/(2 tan(FoV_h/2)) (1 if W = 1), so pixels 0 and W-1 lie on d_h. */
+nbt_status nbt_camera_from_fov(double fov_h, double fov_v, int32_t w, int32_t h, nbt_camera *out);
+/* The paper's s_G lattice: spacing s_G*voxel_size on the far plane, centred,
+ * plus the 4 corner rays unless they coincide with lattice points (Q6-Q9). */
+nbt_status nbt_camera_from_grid_scaling(double fov_h, double fov_v, double range, double voxel_size,
+                                        double s_g, nbt_camera *out);
+/* N_E = W*H (+4 with corners). */
+int32_t    nbt_camera_num_rays(const nbt_camera *cam);
+
+/* ------------------------------------------------------ perspectives (row a3) */
+
+enum { NBT_SAMPLE_BALL = 0, NBT_SAMPLE_SURFACE = 1 };
+/* Eq. 1 (Q1-Q3, Q29): n points p = poi + r_s * X_R^(1/3) * X/|X| written to
+ * xyz_out (n x 3 doubles, row-major), on the device (out_on_device = 1) or the host. */
+nbt_status nbt_sample_perspectives(nbt_ctx ctx, const double poi[3], double r_s, int32_t n, uint64_t seed,
+                                   int32_t mode, double *xyz_out, int out_on_device);
+
+/* ----------------------------------------- the Information Distribution (a4-a8) */
+
+typedef struct {
+    double   *xyz;        /* n x 3: the perspective origins p_P,j (copied from the input) */
+    double   *gain;       /* n: g_P,j, canonical form Q26 */
+    uint64_t *counts;     /* n x 4 or NULL: T_U, T_F, T_O (per-state visit totals over the
+                             perspective's rays) and L (in-grid lookups) */
+    int32_t   on_device;  /* 1: the three buffers are device memory of the ctx's device */
+} nbt_ig_cloud;
+
+/* The ID: for each perspective j of persp_xyz (n_persp x 3), cast the
+ * camera's N_E rays of length `range` (d_Cam, world units) towards the PoI through the
+ * map, stop each at its first Occupied voxel, score visited voxels by Eq. 2 and average
+ * per perspective.  Output row j belongs to input row j.  Errors: NBT_ERR_DEGENERATE if
+ * a host perspective equals the PoI (Q18); NBT_ERR_INVALID_ARG for non-finite inputs or
+ * a Q16 coordinate outside (-2^30, 2^30) (Q19).  n_persp == 0 is a no-op. */
+nbt_status nbt_id_compute(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz,
+                          int32_t n_persp, int persp_on_device, const nbt_camera *cam, double range,
+                          nbt_ig_cloud *out);
+/* Shard form for multi-GPU: computes only perspectives j = first + i*stride
+ * (i = 0, 1, ...) and writes them COMPACTLY to out rows i. */
+nbt_status nbt_id_compute_slice(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz,
+                                int32_t n_persp, int persp_on_device, int32_t first, int32_t stride,
+                                const nbt_camera *cam, double range, nbt_ig_cloud *out);
+
+/* -------------------------------------------- ID buffer + IDW query (row a9) */
+
+typedef struct nbt_idbuf_s *nbt_idbuf;
+
+/* Device ring buffer of the last `capacity_nb` IG clouds (N_B = 10 in P:310), each of
+ * at most max_persp perspectives. */
+nbt_status nbt_idbuf_create(nbt_ctx ctx, int32_t capacity_nb, int32_t max_persp, nbt_idbuf *out);
+/* Copy a cloud (n perspectives: xyz + gain) in as the NEWEST entry; evicts the oldest
+ * when full.  Stream-ordered. */
+nbt_status nbt_idbuf_push(nbt_idbuf buf, const nbt_ig_cloud *cloud, int32_t n);
+nbt_status nbt_idbuf_clear(nbt_idbuf buf);
+int32_t    nbt_idbuf_size(nbt_idbuf buf);
+/* Eq. 4 at n_q query positions (n_q x 3): G(x) = sum_u w_u v_u(x), entries u =
+ * oldest..newest, w_u = 1/(m-u) (newest 1, Q21), v_u = sum_j g_j d_j^-p / sum_j d_j^-p
+ * over entry u's perspectives (Q20, Q22), v_u = gain of the nearest perspective if its
+ * distance < zero_eps (Q23).  normalize_weights != 0 divides by sum_u w_u.  g_out has n_q
+ * doubles on the device (out_on_device = 1) or the host.  NBT_ERR_EMPTY if no entry. */
+nbt_status nbt_ig_query(nbt_idbuf buf, const double *query_xyz, int32_t n_q, int q_on_device,
+                        double power_p, double zero_eps, int32_t normalize_weights,
+                        double *g_out, int out_on_device);
+void       nbt_idbuf_destroy(nbt_idbuf buf);
+
+/* ----------------------------------------------------------- test hooks */
+
+/* Per-ray walk of explicit Q16 segments (host arrays, n_rays x 3 int32 each): the first
+ * max_visits visited voxels of ray r go to ijk_out[r*max_visits*3 ...], their codes
+ * (0/1/2; 255 = outside the grid) to code_out[r*max_visits ...]; len_out[r] = number of
+ * visited voxels (may exceed max_visits); counts_out[r*4 ...] = n_U, n_F, n_O, lookups.
+ * Uses the same device traversal as nbt_id_compute.  Synchronizes. */
+nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map map, const int32_t *o_q16, const int32_t *e_q16,
+                           int32_t n_rays, int32_t max_visits, int32_t *ijk_out, uint8_t *code_out,
+                           int32_t *len_out, uint32_t *counts_out);
+/* The device frames of n perspectives (host in/out): 18 int32 per perspective
+ * (O, A, Rh, Uh, Rc, Uc, each xyz) and a status per perspective (0 ok). Synchronizes. */
+nbt_status nbt_debug_frames(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz,
+                            int32_t n, const nbt_camera *cam, double range, int32_t *q16_out,
+                            int32_t *status_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NBT_H_ */

@@ -1,0 +1,413 @@
+"""Python binding of libnbt (include/nbt.h): argument marshalling only.
+
+Every step of the Information Distribution runs in libnbt's CUDA kernels; this module
+converts numpy arrays / torch tensors to pointers, calls the C ABI function of the same
+name and turns status codes into exceptions.  There is no CPU fallback: if libnbt.so is
+missing, or no CUDA device is present, calls raise.
+
+    import paper_2503_22588_b200 as nbt
+    ctx = nbt.Ctx(0)
+    m = nbt.Map(ctx, nbt.map_desc(256, 256, 256, 0.01)); m.upload(codes)
+    cam = nbt.camera_from_fov(fov_h, fov_v, 64, 48)
+    cloud = nbt.id_compute(ctx, m, poi, persp, cam, 1.5)    # -> IgCloud(xyz, gain, counts)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnbt.so")
+
+OK, ERR_INVALID_ARG, ERR_DEGENERATE, ERR_EMPTY, ERR_OUT_OF_MEMORY, ERR_CUDA, ERR_NCCL, ERR_STATE = range(8)
+UNKNOWN, FREE, OCCUPIED = 0, 1, 2
+OUTSIDE_UNKNOWN, OUTSIDE_CLIP = 0, 1
+SAMPLE_BALL, SAMPLE_SURFACE = 0, 1
+KERNEL_TRACE, KERNEL_FRAMES, KERNEL_FINALIZE, KERNEL_IDW, KERNEL_SAMPLE, KERNEL_MAP_UPDATE = range(6)
+
+# Every symbol include/nbt.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "nbt_abi_version", "nbt_status_string", "nbt_last_error_message",
+    "nbt_ctx_create", "nbt_ctx_set_stream", "nbt_ctx_sync", "nbt_ctx_destroy", "nbt_ctx_launch_count",
+    "nbt_ctx_set_profiling", "nbt_ctx_profile_read",
+    "nbt_map_desc_default", "nbt_map_create", "nbt_map_upload", "nbt_map_upload_prob", "nbt_map_update",
+    "nbt_map_device_buffer", "nbt_map_download", "nbt_map_get_desc", "nbt_map_destroy",
+    "nbt_camera_from_fov", "nbt_camera_from_grid_scaling", "nbt_camera_num_rays",
+    "nbt_sample_perspectives", "nbt_id_compute", "nbt_id_compute_slice",
+    "nbt_idbuf_create", "nbt_idbuf_push", "nbt_idbuf_clear", "nbt_idbuf_size", "nbt_ig_query", "nbt_idbuf_destroy",
+    "nbt_debug_trace", "nbt_debug_frames",
+]
+
+
+class NbtError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_status_name(status)}: {msg}")
+        self.status = status
+
+
+class MapDesc(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("voxel_size", C.c_double),
+                ("origin", C.c_double * 3), ("gain", C.c_double * 3), ("outside_policy", C.c_int32)]
+
+
+class Camera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("add_corners", C.c_int32),
+                ("tan_half_fov_h", C.c_double), ("tan_half_fov_v", C.c_double)]
+
+    @property
+    def num_rays(self):
+        return self.width * self.height + (4 if self.add_corners else 0)
+
+
+class IgCloudC(C.Structure):
+    _fields_ = [("xyz", C.c_void_p), ("gain", C.c_void_p), ("counts", C.c_void_p), ("on_device", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libnbt.so (raises if it has not been built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libnbt.so not built at {LIB_PATH}; run __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, dbl, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_uint64
+    sz = C.c_size_t
+    sig = {
+        "nbt_abi_version": ([], C.c_int),
+        "nbt_status_string": ([C.c_int], C.c_char_p),
+        "nbt_last_error_message": ([], C.c_char_p),
+        "nbt_ctx_create": ([C.c_int, vp, C.POINTER(vp)], C.c_int),
+        "nbt_ctx_set_stream": ([vp, vp], C.c_int),
+        "nbt_ctx_sync": ([vp], C.c_int),
+        "nbt_ctx_destroy": ([vp], None),
+        "nbt_ctx_launch_count": ([vp], u64),
+        "nbt_ctx_set_profiling": ([vp, C.c_int], C.c_int),
+        "nbt_ctx_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(u64), C.c_int], C.c_int),
+        "nbt_map_desc_default": ([C.POINTER(MapDesc), i32, i32, i32, dbl], None),
+        "nbt_map_create": ([vp, C.POINTER(MapDesc), C.POINTER(vp)], C.c_int),
+        "nbt_map_upload": ([vp, vp, sz, C.c_int], C.c_int),
+        "nbt_map_upload_prob": ([vp, vp, vp, sz, C.c_int, dbl, dbl], C.c_int),
+        "nbt_map_update": ([vp, vp, vp, sz, C.c_int], C.c_int),
+        "nbt_map_device_buffer": ([vp, C.POINTER(vp), C.POINTER(sz)], C.c_int),
+        "nbt_map_download": ([vp, vp, sz], C.c_int),
+        "nbt_map_get_desc": ([vp, C.POINTER(MapDesc)], C.c_int),
+        "nbt_map_destroy": ([vp], None),
+        "nbt_camera_from_fov": ([dbl, dbl, i32, i32, C.POINTER(Camera)], C.c_int),
+        "nbt_camera_from_grid_scaling": ([dbl, dbl, dbl, dbl, dbl, C.POINTER(Camera)], C.c_int),
+        "nbt_camera_num_rays": ([C.POINTER(Camera)], i32),
+        "nbt_sample_perspectives": ([vp, vp, dbl, i32, u64, i32, vp, C.c_int], C.c_int),
+        "nbt_id_compute": ([vp, vp, vp, vp, i32, C.c_int, C.POINTER(Camera), dbl, C.POINTER(IgCloudC)], C.c_int),
+        "nbt_id_compute_slice": ([vp, vp, vp, vp, i32, C.c_int, i32, i32, C.POINTER(Camera), dbl,
+                                  C.POINTER(IgCloudC)], C.c_int),
+        "nbt_idbuf_create": ([vp, i32, i32, C.POINTER(vp)], C.c_int),
+        "nbt_idbuf_push": ([vp, C.POINTER(IgCloudC), i32], C.c_int),
+        "nbt_idbuf_clear": ([vp], C.c_int),
+        "nbt_idbuf_size": ([vp], i32),
+        "nbt_ig_query": ([vp, vp, i32, C.c_int, dbl, dbl, i32, vp, C.c_int], C.c_int),
+        "nbt_idbuf_destroy": ([vp], None),
+        "nbt_debug_trace": ([vp, vp, vp, vp, i32, i32, vp, vp, vp, vp], C.c_int),
+        "nbt_debug_frames": ([vp, vp, vp, vp, i32, C.POINTER(Camera), dbl, vp, vp], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _status_name(s):
+    try:
+        return lib().nbt_status_string(int(s)).decode()
+    except Exception:  # noqa: BLE001 -- only used to format an error
+        return f"status {s}"
+
+
+def check(status):
+    if status != OK:
+        raise NbtError(status, lib().nbt_last_error_message().decode())
+
+
+# ------------------------------------------------------------------ marshalling
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+def _ptr(x, dtype):
+    """(pointer, on_device, keepalive) for a numpy array or torch tensor of `dtype`."""
+    if x is None:
+        return None, 0, None
+    if _is_torch(x):
+        import torch
+        tdt = {np.float64: torch.float64, np.float32: torch.float32, np.int32: torch.int32,
+               np.uint8: torch.uint8, np.uint64: torch.int64}[dtype]
+        if x.dtype != tdt or not x.is_contiguous():
+            raise TypeError(f"expected a contiguous {tdt} tensor")
+        return C.c_void_p(x.data_ptr()), int(x.is_cuda), x
+    a = np.ascontiguousarray(x, dtype=dtype)
+    return C.c_void_p(a.ctypes.data), 0, a
+
+
+def _poi(poi):
+    a = np.ascontiguousarray(poi, dtype=np.float64).reshape(3)
+    return C.c_void_p(a.ctypes.data), a
+
+
+# ------------------------------------------------------------------------ API
+
+def nbt_abi_version():
+    return lib().nbt_abi_version()
+
+
+class Ctx:
+    """nbt_ctx: one CUDA device + stream (a borrowed torch stream, or an owned one)."""
+
+    def __init__(self, device=0, stream=None):
+        h = C.c_void_p()
+        s = C.c_void_p(int(stream)) if stream is not None else None
+        check(lib().nbt_ctx_create(int(device), s, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def set_stream(self, stream):
+        check(lib().nbt_ctx_set_stream(self.h, C.c_void_p(int(stream)) if stream is not None else None))
+
+    def sync(self):
+        check(lib().nbt_ctx_sync(self.h))
+
+    @property
+    def launches(self):
+        return int(lib().nbt_ctx_launch_count(self.h))
+
+    def set_profiling(self, on=True):
+        check(lib().nbt_ctx_set_profiling(self.h, int(bool(on))))
+
+    def profile_read(self, kernel, reset=True):
+        """(total_ms, launches) of a kernel family since the last reset (syncs the stream)."""
+        ms, n = C.c_double(), C.c_uint64()
+        check(lib().nbt_ctx_profile_read(self.h, int(kernel), C.byref(ms), C.byref(n), int(bool(reset))))
+        return ms.value, int(n.value)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().nbt_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def map_desc(nx, ny, nz, voxel_size, origin=(0.0, 0.0, 0.0), gain=None, outside_policy=OUTSIDE_UNKNOWN):
+    d = MapDesc()
+    lib().nbt_map_desc_default(C.byref(d), int(nx), int(ny), int(nz), float(voxel_size))
+    d.origin[:] = [float(v) for v in origin]
+    if gain is not None:
+        d.gain[:] = [float(v) for v in gain]
+    d.outside_policy = int(outside_policy)
+    return d
+
+
+class Map:
+    """nbt_map: the device-resident 2-bit voxel store (row a1)."""
+
+    def __init__(self, ctx: Ctx, desc: MapDesc):
+        h = C.c_void_p()
+        check(lib().nbt_map_create(ctx.h, C.byref(desc), C.byref(h)))
+        self.h, self.ctx, self.desc = h, ctx, desc
+
+    @property
+    def shape(self):
+        return (self.desc.nz, self.desc.ny, self.desc.nx)
+
+    @property
+    def nvox(self):
+        return self.desc.nx * self.desc.ny * self.desc.nz
+
+    def upload(self, codes):
+        p, dev, keep = _ptr(codes, np.uint8)
+        check(lib().nbt_map_upload(self.h, p, self.nvox, dev))
+
+    def upload_prob(self, p, observed, t_occ=0.5, t_free=0.5):
+        pp, dev, k1 = _ptr(p, np.float32)
+        po, dev2, k2 = _ptr(observed, np.uint8)
+        if dev != dev2:
+            raise ValueError("p and observed must both be host or both device")
+        check(lib().nbt_map_upload_prob(self.h, pp, po, self.nvox, dev, float(t_occ), float(t_free)))
+
+    def update(self, ijk, codes):
+        pi, dev, k1 = _ptr(ijk, np.int32)
+        pc, dev2, k2 = _ptr(codes, np.uint8)
+        if dev != dev2:
+            raise ValueError("ijk and codes must both be host or both device")
+        n = (k2.numel() if _is_torch(k2) else k2.size) if k2 is not None else 0
+        check(lib().nbt_map_update(self.h, pi, pc, n, dev))
+
+    def device_buffer(self):
+        p, n = C.c_void_p(), C.c_size_t()
+        check(lib().nbt_map_device_buffer(self.h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def download(self):
+        out = np.empty(self.shape, np.uint8)
+        check(lib().nbt_map_download(self.h, C.c_void_p(out.ctypes.data), self.nvox))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().nbt_map_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def camera_from_fov(fov_h, fov_v, w, h) -> Camera:
+    cam = Camera()
+    check(lib().nbt_camera_from_fov(float(fov_h), float(fov_v), int(w), int(h), C.byref(cam)))
+    return cam
+
+
+def camera_from_grid_scaling(fov_h, fov_v, range_, voxel_size, s_g) -> Camera:
+    cam = Camera()
+    check(lib().nbt_camera_from_grid_scaling(float(fov_h), float(fov_v), float(range_), float(voxel_size),
+                                             float(s_g), C.byref(cam)))
+    return cam
+
+
+def sample_perspectives(ctx: Ctx, poi, r_s, n, seed, mode=SAMPLE_BALL, out=None):
+    """Eq. 1 on the device.  `out` may be a (n,3) float64 CUDA tensor; default: host numpy."""
+    pp, keep = _poi(poi)
+    if out is None:
+        out = np.empty((n, 3), np.float64)
+    po, dev, k = _ptr(out, np.float64)
+    check(lib().nbt_sample_perspectives(ctx.h, pp, float(r_s), int(n), int(seed) & (2 ** 64 - 1), int(mode), po, dev))
+    return out
+
+
+@dataclass
+class IgCloud:
+    xyz: object
+    gain: object
+    counts: object
+
+    def as_c(self):
+        px, dev, _ = _ptr(self.xyz, np.float64)
+        pg, _, _ = _ptr(self.gain, np.float64)
+        pc = _ptr(self.counts, np.uint64)[0] if self.counts is not None else None
+        return IgCloudC(px.value, pg.value, pc.value if pc is not None else None, dev)
+
+
+def empty_cloud(n, device=None, counts=True):
+    if device is None:
+        return IgCloud(np.empty((n, 3)), np.empty(n), np.empty((n, 4), np.uint64) if counts else None)
+    import torch
+    return IgCloud(torch.empty((n, 3), dtype=torch.float64, device=device),
+                   torch.empty(n, dtype=torch.float64, device=device),
+                   torch.empty((n, 4), dtype=torch.int64, device=device) if counts else None)
+
+
+def nbt_id_compute(ctx: Ctx, m: Map, poi, persp, cam: Camera, range_, out: IgCloud | None = None,
+                   first=0, stride=1):
+    """The ID (rows a4-a8).  persp: (n,3) float64 numpy (host) or CUDA tensor.  With first/stride
+    only rows first + i*stride are computed and written compactly (multi-GPU shards)."""
+    pp, keep = _poi(poi)
+    pper, dev, kp = _ptr(persp, np.float64)
+    n_src = (kp.shape[0] if kp is not None else 0)
+    n = max(0, (n_src - first + stride - 1) // stride) if first < n_src else 0
+    if out is None:
+        out = empty_cloud(n)
+    oc = out.as_c()
+    if (first, stride) == (0, 1):
+        check(lib().nbt_id_compute(ctx.h, m.h, pp, pper, int(n_src), dev, C.byref(cam), float(range_), C.byref(oc)))
+    else:
+        check(lib().nbt_id_compute_slice(ctx.h, m.h, pp, pper, int(n_src), dev, int(first), int(stride),
+                                         C.byref(cam), float(range_), C.byref(oc)))
+    return out
+
+
+id_compute = nbt_id_compute
+
+
+class IdBuffer:
+    """nbt_idbuf: device ring buffer of the last N_B IG clouds + the IDW query (row a9)."""
+
+    def __init__(self, ctx: Ctx, capacity_nb=10, max_persp=4096):
+        h = C.c_void_p()
+        check(lib().nbt_idbuf_create(ctx.h, int(capacity_nb), int(max_persp), C.byref(h)))
+        self.h, self.ctx = h, ctx
+
+    def push(self, cloud: IgCloud, n=None):
+        oc = cloud.as_c()
+        n = n if n is not None else (cloud.gain.shape[0])
+        check(lib().nbt_idbuf_push(self.h, C.byref(oc), int(n)))
+
+    def clear(self):
+        check(lib().nbt_idbuf_clear(self.h))
+
+    def __len__(self):
+        return int(lib().nbt_idbuf_size(self.h))
+
+    def query(self, xyz, power_p=2.0, zero_eps=1e-9, normalize=False, out=None):
+        pq, qdev, kq = _ptr(xyz, np.float64)
+        nq = kq.shape[0] if kq is not None else 0
+        if out is None:
+            out = np.empty(nq, np.float64)
+        po, odev, _ = _ptr(out, np.float64)
+        check(lib().nbt_ig_query(self.h, pq, int(nq), qdev, float(power_p), float(zero_eps), int(bool(normalize)),
+                                 po, odev))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().nbt_idbuf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def nbt_ig_query(buf: IdBuffer, xyz, power_p=2.0, zero_eps=1e-9, normalize=False, out=None):
+    return buf.query(xyz, power_p, zero_eps, normalize, out)
+
+
+def debug_trace(ctx: Ctx, m: Map, o_q16, e_q16, max_visits=1024):
+    """Per-ray device walks of explicit Q16 segments: (ijk [n,max,3], codes [n,max], len [n], counts [n,4])."""
+    o = np.ascontiguousarray(o_q16, dtype=np.int32).reshape(-1, 3)
+    e = np.ascontiguousarray(e_q16, dtype=np.int32).reshape(-1, 3)
+    n = o.shape[0]
+    ijk = np.zeros((n, max_visits, 3), np.int32)
+    codes = np.zeros((n, max_visits), np.uint8)
+    ln = np.zeros(n, np.int32)
+    cnt = np.zeros((n, 4), np.uint32)
+    check(lib().nbt_debug_trace(ctx.h, m.h, C.c_void_p(o.ctypes.data), C.c_void_p(e.ctypes.data), n, max_visits,
+                                C.c_void_p(ijk.ctypes.data), C.c_void_p(codes.ctypes.data),
+                                C.c_void_p(ln.ctypes.data), C.c_void_p(cnt.ctypes.data)))
+    return ijk, codes, ln, cnt
+
+
+def debug_frames(ctx: Ctx, m: Map, poi, persp, cam: Camera, range_):
+    pp, keep = _poi(poi)
+    P = np.ascontiguousarray(persp, dtype=np.float64).reshape(-1, 3)
+    q = np.zeros((P.shape[0], 18), np.int32)
+    st = np.zeros(P.shape[0], np.int32)
+    check(lib().nbt_debug_frames(ctx.h, m.h, pp, C.c_void_p(P.ctypes.data), P.shape[0], C.byref(cam),
+                                 float(range_), C.c_void_p(q.ctypes.data), C.c_void_p(st.ctypes.data)))
+    return q, st

@@ -1,0 +1,168 @@
+// Voxel-map store kernels.
+//
+// Layout in HBM: the nx*ny*nz grid is surrounded by a ring of
+// sentinel voxels (code 3 = "outside") and stored x-fastest, 2 bits per voxel, 16
+// voxels per 32-bit word: padded voxel (x+1, y+1, z+1) has linear index
+// i = (x+1) + px*((y+1) + py*(z+1)) and lives in bits 2*(i&15).. of word i>>4.
+// 256^3 -> 4.1 MiB, 512^3 -> 32.4 MiB: both stay resident in the 126 MB L2.
+// The sentinel ring lets the traversal detect leaving the grid with the same
+// "code >= 2" test that detects an Occupied voxel (no bounds check in the hot loop).
+#include <cub/cub.cuh>
+
+#include "nbt_internal.cuh"
+
+namespace nbt {
+namespace {
+
+constexpr uint32_t kOutside = 3u;
+
+// One thread per packed word (16 padded voxels).
+__global__ void k_map_pack(const uint8_t *__restrict__ codes, int nx, int ny, int nz, uint32_t px, uint32_t py,
+                           uint64_t nvox_pad, size_t nwords, uint32_t *__restrict__ words, int *err)
+{
+    size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (w >= nwords) return;
+    uint64_t i0 = (uint64_t)w * 16;
+    uint32_t x = (uint32_t)(i0 % px);
+    uint64_t r = i0 / px;
+    uint32_t y = (uint32_t)(r % py);
+    uint32_t z = (uint32_t)(r / py);
+    uint32_t out = 0;
+    bool bad = false;
+    for (int k = 0; k < 16; ++k) {
+        uint32_t c = kOutside;
+        if (i0 + k < nvox_pad) {
+            int gx = (int)x - 1, gy = (int)y - 1, gz = (int)z - 1;
+            if (gx >= 0 && gy >= 0 && gz >= 0 && gx < nx && gy < ny && gz < nz) {
+                c = codes[(size_t)gx + (size_t)nx * ((size_t)gy + (size_t)ny * gz)];
+                if (c > 2u) { bad = true; c = 0u; }
+            }
+        }
+        out |= c << (2 * k);
+        if (++x == px) { x = 0; if (++y == py) { y = 0; ++z; } }
+    }
+    words[w] = out;
+    if (bad) atomicCAS(err, 0, (int)NBT_ERR_INVALID_ARG);
+}
+
+// S:66-74 classification: unobserved -> U; P >= t_occ -> O; P <= t_free -> F; else U.
+__global__ void k_map_classify(const float *__restrict__ p, const uint8_t *__restrict__ obs, size_t n,
+                               double t_occ, double t_free, uint8_t *__restrict__ codes)
+{
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double v = (double)p[i];
+    uint8_t c = NBT_UNKNOWN;
+    if (obs[i]) c = (v >= t_occ) ? NBT_OCCUPIED : (v <= t_free ? NBT_FREE : NBT_UNKNOWN);
+    codes[i] = c;
+}
+
+// Delta keys: (linear voxel index << 32) | array position; invalid deltas sort last.
+__global__ void k_delta_keys(const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes, uint32_t n,
+                             int nx, int ny, int nz, unsigned long long *__restrict__ keys, int *err)
+{
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int x = ijk[3 * i], y = ijk[3 * i + 1], z = ijk[3 * i + 2];
+    bool ok = x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz && codes[i] <= 2;
+    if (!ok) {
+        keys[i] = ~0ull;
+        atomicCAS(err, 0, (int)NBT_ERR_INVALID_ARG);
+        return;
+    }
+    unsigned long long lin = (unsigned long long)x + (unsigned long long)nx * ((unsigned long long)y +
+                                                                             (unsigned long long)ny * z);
+    keys[i] = (lin << 32) | i;
+}
+
+// After sorting, the last key of each voxel run is the last delta in array order (Q30):
+// only that one writes.  Distinct voxels may share a word, so the 2-bit field is
+// changed with one atomicXor; the thread's own field is never touched by another thread.
+__global__ void k_delta_apply(const unsigned long long *__restrict__ keys, uint32_t n,
+                              const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes, uint32_t px,
+                              uint32_t py, uint32_t *words)
+{
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned long long k = keys[i];
+    if (k == ~0ull) return;
+    if (i + 1 < n && (keys[i + 1] >> 32) == (k >> 32)) return;
+    uint32_t pos = (uint32_t)(k & 0xffffffffu);
+    uint32_t x = (uint32_t)ijk[3 * pos] + 1, y = (uint32_t)ijk[3 * pos + 1] + 1, z = (uint32_t)ijk[3 * pos + 2] + 1;
+    uint64_t pi = (uint64_t)x + (uint64_t)px * ((uint64_t)y + (uint64_t)py * z);
+    uint32_t *w = words + (pi >> 4);
+    uint32_t sh = (uint32_t)(pi & 15) * 2;
+    uint32_t old = (*(volatile uint32_t *)w >> sh) & 3u;
+    uint32_t nw = codes[pos];
+    if (old != nw) atomicXor(w, (old ^ nw) << sh);
+}
+
+__global__ void k_map_unpack(const uint32_t *__restrict__ words, int nx, int ny, int nz, uint32_t px, uint32_t py,
+                             uint8_t *__restrict__ codes)
+{
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    size_t n = (size_t)nx * ny * nz;
+    if (i >= n) return;
+    uint32_t x = (uint32_t)(i % nx);
+    size_t r = i / nx;
+    uint32_t y = (uint32_t)(r % ny), z = (uint32_t)(r / ny);
+    uint64_t pi = (uint64_t)(x + 1) + (uint64_t)px * ((uint64_t)(y + 1) + (uint64_t)py * (z + 1));
+    codes[i] = (uint8_t)((words[pi >> 4] >> ((pi & 15) * 2)) & 3u);
+}
+
+inline unsigned blocks_for(size_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+nbt_status launch_map_pack(nbt_ctx ctx, nbt_map m, const uint8_t *d_codes)
+{
+    if (m->nwords == 0) return NBT_OK;
+    k_map_pack<<<blocks_for(m->nwords, 256), 256, 0, ctx->stream>>>(
+        d_codes, m->desc.nx, m->desc.ny, m->desc.nz, m->px, m->py, m->nvox_pad, m->nwords, m->d_words, ctx->d_err);
+    NBT_LAUNCHED(ctx);
+    return NBT_OK;
+}
+
+nbt_status launch_map_classify(nbt_ctx ctx, const float *d_p, const uint8_t *d_obs, size_t n, double t_occ,
+                               double t_free, uint8_t *d_codes_out)
+{
+    if (n == 0) return NBT_OK;
+    k_map_classify<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(d_p, d_obs, n, t_occ, t_free, d_codes_out);
+    NBT_LAUNCHED(ctx);
+    return NBT_OK;
+}
+
+nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const uint8_t *d_codes, size_t n)
+{
+    if (n == 0) return NBT_OK;
+    if (n >= (1ull << 31)) return fail(NBT_ERR_INVALID_ARG, "nbt_map_update: too many deltas");
+    uint32_t nn = (uint32_t)n;
+    ProfScope ps(ctx, NBT_KERNEL_MAP_UPDATE);
+    nbt_status st;
+    if ((st = ctx->keys.ensure(n * 8))) return st;
+    if ((st = ctx->keys_alt.ensure(n * 8))) return st;
+    auto *kin = ctx->keys.as<unsigned long long>();
+    auto *kout = ctx->keys_alt.as<unsigned long long>();
+    k_delta_keys<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(d_ijk, d_codes, nn, m->desc.nx, m->desc.ny,
+                                                              m->desc.nz, kin, ctx->d_err);
+    NBT_LAUNCHED(ctx);
+    size_t tmp = 0;
+    NBT_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kin, kout, (int)nn, 0, 64, ctx->stream));
+    if ((st = ctx->cub_tmp.ensure(tmp))) return st;
+    NBT_CUDA(cub::DeviceRadixSort::SortKeys(ctx->cub_tmp.p, tmp, kin, kout, (int)nn, 0, 64, ctx->stream));
+    k_delta_apply<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(kout, nn, d_ijk, d_codes, m->px, m->py,
+                                                               m->d_words);
+    NBT_LAUNCHED(ctx);
+    return NBT_OK;
+}
+
+nbt_status launch_map_unpack(nbt_ctx ctx, nbt_map m, uint8_t *d_codes_out)
+{
+    size_t n = (size_t)m->desc.nx * m->desc.ny * m->desc.nz;
+    k_map_unpack<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(m->d_words, m->desc.nx, m->desc.ny, m->desc.nz,
+                                                               m->px, m->py, d_codes_out);
+    NBT_LAUNCHED(ctx);
+    return NBT_OK;
+}
+
+}  // namespace nbt

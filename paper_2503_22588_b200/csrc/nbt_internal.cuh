@@ -1,0 +1,169 @@
+// Internal declarations shared by the libnbt translation units (product code only;
+// nothing here is visible across the C ABI).  Citations: P:n = PAPER.md line n.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "nbt.h"
+
+namespace nbt {
+
+// ----------------------------------------------------------------- errors
+
+void set_error(const std::string &msg);
+nbt_status fail(nbt_status s, const std::string &msg);
+nbt_status cuda_fail(cudaError_t e, const char *what);
+
+#define NBT_CUDA(call)                                                   \
+    do {                                                                 \
+        cudaError_t e_ = (call);                                         \
+        if (e_ != cudaSuccess) return ::nbt::cuda_fail(e_, #call);       \
+    } while (0)
+
+#define NBT_LAUNCHED(ctx)                                                \
+    do {                                                                 \
+        (ctx)->launches++;                                               \
+        cudaError_t e_ = cudaGetLastError();                             \
+        if (e_ != cudaSuccess) return ::nbt::cuda_fail(e_, "kernel launch"); \
+    } while (0)
+
+// Device error word bits (first error wins; read and cleared by nbt_ctx_sync).
+enum : int { DERR_NONE = 0 };
+
+// ----------------------------------------------------------- buffers
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    nbt_status ensure(size_t bytes);
+    void release();
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+// Pinned host staging area, reused after its last async copy completed.
+struct HostStage {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+    nbt_status acquire(size_t bytes);   // waits for the previous copy out of / into it
+    nbt_status mark(cudaStream_t s);    // record the copy just enqueued
+    void release();
+};
+
+// Per-kernel-family event timing (nbt_ctx_set_profiling).
+struct Profiler {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[NBT_KERNEL_COUNT];
+    double ms[NBT_KERNEL_COUNT] = {0};
+    uint64_t n[NBT_KERNEL_COUNT] = {0};
+    cudaEvent_t take();
+};
+
+// RAII: records a start event at construction and an end event at destruction when
+// profiling is on.
+struct ProfScope {
+    nbt_ctx ctx;
+    int kernel;
+    cudaEvent_t start = nullptr;
+    ProfScope(nbt_ctx c, int k);
+    ~ProfScope();
+};
+
+}  // namespace nbt
+
+// ----------------------------------------------------------------- handles
+
+struct nbt_ctx_s {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint64_t launches = 0;
+    int *d_err = nullptr;             // device-side validation status (nbt_status value)
+    int *h_err = nullptr;             // pinned mirror
+    int trace_blocks_per_sm = 0;      // cached occupancy of the trace kernel
+    // scratch
+    nbt::DevBuf persp;                // staged perspective origins (n x 3 f64)
+    nbt::DevBuf frames;               // per-perspective Q16 frames
+    nbt::DevBuf totals;               // per-perspective u64 totals (U, F, O, L)
+    nbt::DevBuf counter;              // work counter(s)
+    nbt::DevBuf out_tmp;              // device staging for host outputs
+    nbt::DevBuf deltas;               // staged map deltas
+    nbt::DevBuf keys, keys_alt, cub_tmp;
+    nbt::DevBuf queries, qout;
+    nbt::DevBuf dbg;                  // debug entry points
+    nbt::HostStage stage_in[3];
+    nbt::HostStage stage_out;
+    nbt::Profiler prof;
+};
+
+struct nbt_map_s {
+    nbt_ctx ctx = nullptr;
+    nbt_map_desc desc{};
+    uint32_t px = 0, py = 0, pz = 0;  // padded extents (one sentinel voxel each side)
+    uint64_t nvox_pad = 0;
+    size_t nwords = 0;
+    uint32_t *d_words = nullptr;      // 2-bit codes, 16 voxels per 32-bit word
+};
+
+struct nbt_idbuf_s {
+    nbt_ctx ctx = nullptr;
+    int32_t capacity = 0, max_persp = 0;
+    int32_t head = 0, count = 0;      // ring: slot of the oldest entry, number of entries
+    int32_t sizes[64] = {0};
+    double *d_xyz = nullptr;          // capacity x max_persp x 3
+    double *d_gain = nullptr;         // capacity x max_persp
+};
+
+// ------------------------------------------------------------- kernel API
+
+namespace nbt {
+
+// Map store (k_map.cu)
+nbt_status launch_map_pack(nbt_ctx ctx, nbt_map m, const uint8_t *d_codes);
+nbt_status launch_map_classify(nbt_ctx ctx, const float *d_p, const uint8_t *d_obs, size_t n, double t_occ,
+                               double t_free, uint8_t *d_codes_out);
+nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const uint8_t *d_codes, size_t n);
+nbt_status launch_map_unpack(nbt_ctx ctx, nbt_map m, uint8_t *d_codes_out);
+
+// Perspectives (k_sample.cu)
+nbt_status launch_sample(nbt_ctx ctx, const double poi[3], double r_s, int32_t n, uint64_t seed, int32_t mode,
+                         double *d_out);
+
+// The ID (k_id.cu)
+struct IdLaunch {
+    const double *d_persp;   // source perspective array (device)
+    int32_t n_src;           // rows in the source array
+    int32_t first, stride;   // computed rows: first + i*stride
+    int32_t n;               // number of computed rows
+    double poi[3];
+    nbt_camera cam;
+    double range;
+    double *d_xyz_out;       // n x 3
+    double *d_gain_out;      // n
+    uint64_t *d_counts_out;  // n x 4 or null
+};
+nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L);
+nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const int32_t *d_e, int32_t n_rays,
+                              int32_t max_visits, int32_t *d_ijk, uint8_t *d_code, int32_t *d_len,
+                              uint32_t *d_counts);
+nbt_status launch_debug_frames(nbt_ctx ctx, nbt_map m, const double poi[3], const double *d_persp, int32_t n,
+                               const nbt_camera &cam, double range, int32_t *d_frames);
+
+// IDW (k_idw.cu)
+struct IdwEntries {
+    int32_t m;               // entries, oldest first
+    int32_t slot[64];
+    int32_t size[64];
+};
+nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, const double *d_q, int32_t n_q,
+                      double power_p, double zero_eps, int32_t normalize, double *d_out);
+
+}  // namespace nbt

@@ -1,0 +1,845 @@
+// libnbt runtime: the C ABI of include/nbt.h (handles, validation, staging of host
+// inputs/outputs, stream ordering).  All arithmetic of the method runs in the kernels
+// of k_map.cu, k_sample.cu, k_id.cu and k_idw.cu; this file only moves data and checks
+// arguments.
+#include <math.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+
+#include "nbt_internal.cuh"
+
+namespace nbt {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+nbt_status fail(nbt_status s, const std::string &msg)
+{
+    g_last_error = msg;
+    return s;
+}
+
+nbt_status cuda_fail(cudaError_t e, const char *what)
+{
+    g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return e == cudaErrorMemoryAllocation ? NBT_ERR_OUT_OF_MEMORY : NBT_ERR_CUDA;
+}
+
+nbt_status DevBuf::ensure(size_t bytes)
+{
+    if (bytes <= cap && p) return NBT_OK;
+    size_t want = bytes < 256 ? 256 : bytes;
+    want = want + want / 4;
+    if (p) {
+        NBT_CUDA(cudaFree(p));   // implicit device synchronisation: no in-flight user
+        p = nullptr;
+        cap = 0;
+    }
+    NBT_CUDA(cudaMalloc(&p, want));
+    cap = want;
+    return NBT_OK;
+}
+
+void DevBuf::release()
+{
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+}
+
+nbt_status HostStage::acquire(size_t bytes)
+{
+    if (pending) {
+        NBT_CUDA(cudaEventSynchronize(ev));
+        pending = false;
+    }
+    if (!ev) NBT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (bytes <= cap && p) return NBT_OK;
+    if (p) NBT_CUDA(cudaFreeHost(p));
+    p = nullptr;
+    size_t want = bytes < 4096 ? 4096 : bytes + bytes / 4;
+    NBT_CUDA(cudaHostAlloc(&p, want, cudaHostAllocDefault));
+    cap = want;
+    return NBT_OK;
+}
+
+nbt_status HostStage::mark(cudaStream_t s)
+{
+    NBT_CUDA(cudaEventRecord(ev, s));
+    pending = true;
+    return NBT_OK;
+}
+
+void HostStage::release()
+{
+    if (pending && ev) cudaEventSynchronize(ev);
+    if (p) cudaFreeHost(p);
+    if (ev) cudaEventDestroy(ev);
+    p = nullptr;
+    ev = nullptr;
+    cap = 0;
+    pending = false;
+}
+
+// Copy a host array into device scratch through a pinned stage (async, stream-ordered).
+static nbt_status stage_h2d(nbt_ctx ctx, HostStage &st, DevBuf &dst, const void *src, size_t bytes)
+{
+    nbt_status s;
+    if ((s = dst.ensure(bytes))) return s;
+    if (bytes == 0) return NBT_OK;
+    if ((s = st.acquire(bytes))) return s;
+    memcpy(st.p, src, bytes);
+    NBT_CUDA(cudaMemcpyAsync(dst.p, st.p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return st.mark(ctx->stream);
+}
+
+// Copy device results to a host buffer (synchronises the stream).
+static nbt_status d2h_sync(nbt_ctx ctx, void *dst, const void *src, size_t bytes)
+{
+    if (bytes == 0) return NBT_OK;
+    nbt_status s;
+    if ((s = ctx->stage_out.acquire(bytes))) return s;
+    NBT_CUDA(cudaMemcpyAsync(ctx->stage_out.p, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaStreamSynchronize(ctx->stream));
+    memcpy(dst, ctx->stage_out.p, bytes);
+    return NBT_OK;
+}
+
+static nbt_status bind(nbt_ctx ctx)
+{
+    if (!ctx) return fail(NBT_ERR_INVALID_ARG, "null ctx");
+    NBT_CUDA(cudaSetDevice(ctx->device));
+    return NBT_OK;
+}
+
+// Device-side validation status recorded since the last sync.
+static nbt_status take_device_error(nbt_ctx ctx, const char *where)
+{
+    NBT_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaStreamSynchronize(ctx->stream));
+    int e = *ctx->h_err;
+    if (e != 0) {
+        NBT_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+        NBT_CUDA(cudaStreamSynchronize(ctx->stream));
+        return fail((nbt_status)e, std::string(where) + ": device-side validation failed (" +
+                                       nbt_status_string((nbt_status)e) + ")");
+    }
+    return NBT_OK;
+}
+
+cudaEvent_t Profiler::take()
+{
+    cudaEvent_t e = nullptr;
+    if (!pool.empty()) {
+        e = pool.back();
+        pool.pop_back();
+    } else if (cudaEventCreate(&e) != cudaSuccess) {
+        e = nullptr;
+    }
+    return e;
+}
+
+ProfScope::ProfScope(nbt_ctx c, int k) : ctx(c), kernel(k)
+{
+    if (ctx->prof.on) {
+        start = ctx->prof.take();
+        if (start) cudaEventRecord(start, ctx->stream);
+    }
+}
+
+ProfScope::~ProfScope()
+{
+    if (!start) return;
+    cudaEvent_t end = ctx->prof.take();
+    if (!end) {
+        ctx->prof.pool.push_back(start);
+        return;
+    }
+    cudaEventRecord(end, ctx->stream);
+    ctx->prof.pending[kernel].emplace_back(start, end);
+}
+
+static bool finite3(const double *p) { return isfinite(p[0]) && isfinite(p[1]) && isfinite(p[2]); }
+
+}  // namespace nbt
+
+using namespace nbt;
+
+extern "C" {
+
+int nbt_abi_version(void) { return NBT_ABI_VERSION; }
+
+const char *nbt_status_string(nbt_status s)
+{
+    switch (s) {
+    case NBT_OK: return "NBT_OK";
+    case NBT_ERR_INVALID_ARG: return "NBT_ERR_INVALID_ARG";
+    case NBT_ERR_DEGENERATE: return "NBT_ERR_DEGENERATE";
+    case NBT_ERR_EMPTY: return "NBT_ERR_EMPTY";
+    case NBT_ERR_OUT_OF_MEMORY: return "NBT_ERR_OUT_OF_MEMORY";
+    case NBT_ERR_CUDA: return "NBT_ERR_CUDA";
+    case NBT_ERR_NCCL: return "NBT_ERR_NCCL";
+    case NBT_ERR_STATE: return "NBT_ERR_STATE";
+    }
+    return "NBT_ERR_UNKNOWN";
+}
+
+const char *nbt_last_error_message(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------------ context
+
+nbt_status nbt_ctx_create(int device, void *cuda_stream, nbt_ctx *out)
+{
+    if (!out) return fail(NBT_ERR_INVALID_ARG, "nbt_ctx_create: null out");
+    *out = nullptr;
+    int ndev = 0;
+    NBT_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(NBT_ERR_INVALID_ARG, "nbt_ctx_create: no such device");
+    NBT_CUDA(cudaSetDevice(device));
+    nbt_ctx c = new (std::nothrow) nbt_ctx_s();
+    if (!c) return fail(NBT_ERR_OUT_OF_MEMORY, "nbt_ctx_create");
+    c->device = device;
+    cudaError_t e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess && cuda_stream) {
+        c->stream = (cudaStream_t)cuda_stream;
+    } else if (e == cudaSuccess) {
+        e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        c->own_stream = true;
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaHostAlloc(&c->h_err, sizeof(int), cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        nbt_ctx_destroy(c);
+        return cuda_fail(e, "nbt_ctx_create");
+    }
+    *out = c;
+    return NBT_OK;
+}
+
+nbt_status nbt_ctx_set_stream(nbt_ctx ctx, void *cuda_stream)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    NBT_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->own_stream) {
+        cudaStreamDestroy(ctx->stream);
+        ctx->own_stream = false;
+    }
+    if (cuda_stream) {
+        ctx->stream = (cudaStream_t)cuda_stream;
+    } else {
+        NBT_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    }
+    return NBT_OK;
+}
+
+nbt_status nbt_ctx_sync(nbt_ctx ctx)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    return take_device_error(ctx, "nbt_ctx_sync");
+}
+
+uint64_t nbt_ctx_launch_count(nbt_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+nbt_status nbt_ctx_set_profiling(nbt_ctx ctx, int enable)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    ctx->prof.on = enable != 0;
+    return NBT_OK;
+}
+
+nbt_status nbt_ctx_profile_read(nbt_ctx ctx, int32_t kernel, double *total_ms, uint64_t *launches, int reset)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (kernel < 0 || kernel >= NBT_KERNEL_COUNT || !total_ms || !launches)
+        return fail(NBT_ERR_INVALID_ARG, "nbt_ctx_profile_read: bad argument");
+    Profiler &P = ctx->prof;
+    NBT_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto &pr : P.pending[kernel]) {
+        float ms = 0.f;
+        NBT_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+        P.ms[kernel] += ms;
+        P.n[kernel] += 1;
+        P.pool.push_back(pr.first);
+        P.pool.push_back(pr.second);
+    }
+    P.pending[kernel].clear();
+    *total_ms = P.ms[kernel];
+    *launches = P.n[kernel];
+    if (reset) {
+        P.ms[kernel] = 0;
+        P.n[kernel] = 0;
+    }
+    return NBT_OK;
+}
+
+void nbt_ctx_destroy(nbt_ctx ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    DevBuf *bufs[] = {&ctx->persp, &ctx->frames, &ctx->totals, &ctx->counter, &ctx->out_tmp, &ctx->deltas,
+                      &ctx->keys, &ctx->keys_alt, &ctx->cub_tmp, &ctx->queries, &ctx->qout, &ctx->dbg};
+    for (DevBuf *b : bufs) b->release();
+    for (auto &st : ctx->stage_in) st.release();
+    for (auto &v : ctx->prof.pending)
+        for (auto &pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
+    ctx->stage_out.release();
+    if (ctx->d_err) cudaFree(ctx->d_err);
+    if (ctx->h_err) cudaFreeHost(ctx->h_err);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+// --------------------------------------------------------------------- map
+
+void nbt_map_desc_default(nbt_map_desc *d, int32_t nx, int32_t ny, int32_t nz, double voxel_size)
+{
+    if (!d) return;
+    memset(d, 0, sizeof *d);
+    d->nx = nx; d->ny = ny; d->nz = nz;
+    d->voxel_size = voxel_size;
+    d->gain[0] = 1.0;     // Unknown (Eq. 2)
+    d->gain[1] = 0.12;    // Free: P = P_min (S:92 clamp, Q15)
+    d->gain[2] = 0.03;    // Occupied: 1 - P_max (S:92 clamp, Q15)
+    d->outside_policy = NBT_OUTSIDE_UNKNOWN;
+}
+
+static nbt_status check_desc(const nbt_map_desc *d)
+{
+    if (!d) return fail(NBT_ERR_INVALID_ARG, "null map desc");
+    if (d->nx < 1 || d->ny < 1 || d->nz < 1 || d->nx > 16384 || d->ny > 16384 || d->nz > 16384)
+        return fail(NBT_ERR_INVALID_ARG, "map extents must be in [1, 16384]");
+    uint64_t pad = (uint64_t)(d->nx + 2) * (d->ny + 2) * (d->nz + 2);
+    if (pad >= (1ull << 32)) return fail(NBT_ERR_INVALID_ARG, "(nx+2)(ny+2)(nz+2) must be < 2^32");
+    if (!(d->voxel_size > 0) || !isfinite(d->voxel_size)) return fail(NBT_ERR_INVALID_ARG, "voxel_size must be > 0");
+    if (!finite3(d->origin)) return fail(NBT_ERR_INVALID_ARG, "origin must be finite");
+    for (int k = 0; k < 3; ++k)
+        if (!(d->gain[k] >= 0) || !isfinite(d->gain[k])) return fail(NBT_ERR_INVALID_ARG, "gain must be finite, >= 0");
+    if (d->outside_policy != NBT_OUTSIDE_UNKNOWN && d->outside_policy != NBT_OUTSIDE_CLIP)
+        return fail(NBT_ERR_INVALID_ARG, "bad outside_policy");
+    return NBT_OK;
+}
+
+nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
+{
+    nbt_status s;
+    if (!out) return fail(NBT_ERR_INVALID_ARG, "nbt_map_create: null out");
+    *out = nullptr;
+    if ((s = bind(ctx)) || (s = check_desc(desc))) return s;
+    nbt_map m = new (std::nothrow) nbt_map_s();
+    if (!m) return fail(NBT_ERR_OUT_OF_MEMORY, "nbt_map_create");
+    m->ctx = ctx;
+    m->desc = *desc;
+    m->px = desc->nx + 2; m->py = desc->ny + 2; m->pz = desc->nz + 2;
+    m->nvox_pad = (uint64_t)m->px * m->py * m->pz;
+    m->nwords = (size_t)((m->nvox_pad + 15) / 16);
+    cudaError_t e = cudaMalloc(&m->d_words, m->nwords * 4);
+    if (e != cudaSuccess) {
+        delete m;
+        return cuda_fail(e, "nbt_map_create: cudaMalloc");
+    }
+    // all Unknown inside, sentinel ring outside: pack from a null code array
+    DevBuf zeros;
+    size_t n = (size_t)desc->nx * desc->ny * desc->nz;
+    if ((s = zeros.ensure(n))) { nbt_map_destroy(m); return s; }
+    e = cudaMemsetAsync(zeros.p, 0, n, ctx->stream);
+    if (e == cudaSuccess) s = launch_map_pack(ctx, m, zeros.as<uint8_t>());
+    else s = cuda_fail(e, "nbt_map_create: memset");
+    if (s == NBT_OK) {
+        e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) s = cuda_fail(e, "nbt_map_create: sync");
+    }
+    zeros.release();
+    if (s) { nbt_map_destroy(m); return s; }
+    *out = m;
+    return NBT_OK;
+}
+
+static nbt_status map_nvox(nbt_map m, size_t n, const char *who)
+{
+    if (!m) return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": null map");
+    size_t want = (size_t)m->desc.nx * m->desc.ny * m->desc.nz;
+    if (n != want) return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": n must be nx*ny*nz");
+    return NBT_OK;
+}
+
+nbt_status nbt_map_upload(nbt_map m, const uint8_t *codes, size_t n, int on_device)
+{
+    nbt_status s;
+    if ((s = map_nvox(m, n, "nbt_map_upload"))) return s;
+    nbt_ctx ctx = m->ctx;
+    if ((s = bind(ctx))) return s;
+    if (!codes) return fail(NBT_ERR_INVALID_ARG, "nbt_map_upload: null codes");
+    if ((s = take_device_error(ctx, "nbt_map_upload (earlier work)"))) return s;
+    const uint8_t *src = codes;
+    DevBuf tmp;
+    if (!on_device) {
+        for (size_t i = 0; i < n; ++i)
+            if (codes[i] > 2) return fail(NBT_ERR_INVALID_ARG, "nbt_map_upload: code >= 3 at " + std::to_string(i));
+        if ((s = tmp.ensure(n))) return s;
+        cudaError_t e = cudaMemcpyAsync(tmp.p, codes, n, cudaMemcpyHostToDevice, ctx->stream);
+        if (e != cudaSuccess) { tmp.release(); return cuda_fail(e, "nbt_map_upload: H2D"); }
+        src = tmp.as<uint8_t>();
+    }
+    s = launch_map_pack(ctx, m, src);
+    if (s == NBT_OK) s = take_device_error(ctx, "nbt_map_upload");
+    tmp.release();
+    return s;
+}
+
+nbt_status nbt_map_upload_prob(nbt_map m, const float *p, const uint8_t *observed, size_t n, int on_device,
+                               double t_occ, double t_free)
+{
+    nbt_status s;
+    if ((s = map_nvox(m, n, "nbt_map_upload_prob"))) return s;
+    nbt_ctx ctx = m->ctx;
+    if ((s = bind(ctx))) return s;
+    if (!p || !observed) return fail(NBT_ERR_INVALID_ARG, "nbt_map_upload_prob: null input");
+    if (!isfinite(t_occ) || !isfinite(t_free)) return fail(NBT_ERR_INVALID_ARG, "thresholds must be finite");
+    DevBuf dp, dobs, codes;
+    const float *sp = p;
+    const uint8_t *so = observed;
+    cudaError_t e = cudaSuccess;
+    if (!on_device) {
+        if ((s = dp.ensure(n * 4)) || (s = dobs.ensure(n))) return s;
+        e = cudaMemcpyAsync(dp.p, p, n * 4, cudaMemcpyHostToDevice, ctx->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dobs.p, observed, n, cudaMemcpyHostToDevice, ctx->stream);
+        sp = dp.as<float>();
+        so = dobs.as<uint8_t>();
+    }
+    if (e == cudaSuccess && (s = codes.ensure(n)) == NBT_OK) {
+        s = launch_map_classify(ctx, sp, so, n, t_occ, t_free, codes.as<uint8_t>());
+        if (s == NBT_OK) s = launch_map_pack(ctx, m, codes.as<uint8_t>());
+        if (s == NBT_OK) s = take_device_error(ctx, "nbt_map_upload_prob");
+    } else if (e != cudaSuccess) {
+        s = cuda_fail(e, "nbt_map_upload_prob: H2D");
+    }
+    cudaStreamSynchronize(ctx->stream);
+    dp.release(); dobs.release(); codes.release();
+    return s;
+}
+
+nbt_status nbt_map_update(nbt_map m, const int32_t *ijk, const uint8_t *codes, size_t n, int on_device)
+{
+    if (!m) return fail(NBT_ERR_INVALID_ARG, "nbt_map_update: null map");
+    nbt_ctx ctx = m->ctx;
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (n == 0) return NBT_OK;
+    if (!ijk || !codes) return fail(NBT_ERR_INVALID_ARG, "nbt_map_update: null input");
+    const int32_t *dijk = ijk;
+    const uint8_t *dcodes = codes;
+    if (!on_device) {
+        for (size_t i = 0; i < n; ++i) {
+            const int32_t *v = ijk + 3 * i;
+            if (v[0] < 0 || v[1] < 0 || v[2] < 0 || v[0] >= m->desc.nx || v[1] >= m->desc.ny || v[2] >= m->desc.nz)
+                return fail(NBT_ERR_INVALID_ARG, "nbt_map_update: voxel outside the grid at " + std::to_string(i));
+            if (codes[i] > 2) return fail(NBT_ERR_INVALID_ARG, "nbt_map_update: code >= 3 at " + std::to_string(i));
+        }
+        // one staging area for [ijk | codes]
+        size_t bytes = n * 12 + n;
+        if ((s = ctx->deltas.ensure(bytes)) || (s = ctx->stage_in[1].acquire(bytes))) return s;
+        memcpy(ctx->stage_in[1].p, ijk, n * 12);
+        memcpy((char *)ctx->stage_in[1].p + n * 12, codes, n);
+        NBT_CUDA(cudaMemcpyAsync(ctx->deltas.p, ctx->stage_in[1].p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        if ((s = ctx->stage_in[1].mark(ctx->stream))) return s;
+        dijk = ctx->deltas.as<int32_t>();
+        dcodes = ctx->deltas.as<uint8_t>() + n * 12;
+    }
+    return launch_map_update(ctx, m, dijk, dcodes, n);
+}
+
+nbt_status nbt_map_device_buffer(nbt_map m, void **dev_ptr, size_t *bytes)
+{
+    if (!m || !dev_ptr || !bytes) return fail(NBT_ERR_INVALID_ARG, "nbt_map_device_buffer: null argument");
+    *dev_ptr = m->d_words;
+    *bytes = m->nwords * 4;
+    return NBT_OK;
+}
+
+nbt_status nbt_map_download(nbt_map m, uint8_t *codes_out, size_t n)
+{
+    nbt_status s;
+    if ((s = map_nvox(m, n, "nbt_map_download"))) return s;
+    if (!codes_out) return fail(NBT_ERR_INVALID_ARG, "nbt_map_download: null out");
+    nbt_ctx ctx = m->ctx;
+    if ((s = bind(ctx))) return s;
+    DevBuf tmp;
+    if ((s = tmp.ensure(n))) return s;
+    s = launch_map_unpack(ctx, m, tmp.as<uint8_t>());
+    if (s == NBT_OK) {
+        cudaError_t e = cudaMemcpyAsync(codes_out, tmp.p, n, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) s = cuda_fail(e, "nbt_map_download");
+    }
+    tmp.release();
+    return s;
+}
+
+nbt_status nbt_map_get_desc(nbt_map m, nbt_map_desc *out)
+{
+    if (!m || !out) return fail(NBT_ERR_INVALID_ARG, "nbt_map_get_desc: null argument");
+    *out = m->desc;
+    return NBT_OK;
+}
+
+void nbt_map_destroy(nbt_map m)
+{
+    if (!m) return;
+    cudaSetDevice(m->ctx->device);
+    cudaStreamSynchronize(m->ctx->stream);
+    if (m->d_words) cudaFree(m->d_words);
+    delete m;
+}
+
+// ------------------------------------------------------------------ camera
+
+nbt_status nbt_camera_from_fov(double fov_h, double fov_v, int32_t w, int32_t h, nbt_camera *out)
+{
+    if (!out || w < 1 || h < 1 || w > 65535 || h > 65535 || !(fov_h > 0 && fov_h < M_PI) || !(fov_v > 0 && fov_v < M_PI))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_camera_from_fov: need 0 < fov < pi and 1 <= w, h <= 65535");
+    out->width = w;
+    out->height = h;
+    out->tan_half_fov_h = tan(fov_h / 2.0);
+    out->tan_half_fov_v = tan(fov_v / 2.0);
+    out->cx = (w - 1) / 2.0;
+    out->cy = (h - 1) / 2.0;
+    out->fx = (w > 1) ? (w - 1) / (2.0 * out->tan_half_fov_h) : 1.0;
+    out->fy = (h > 1) ? (h - 1) / (2.0 * out->tan_half_fov_v) : 1.0;
+    out->add_corners = 0;
+    return NBT_OK;
+}
+
+nbt_status nbt_camera_from_grid_scaling(double fov_h, double fov_v, double range, double voxel_size, double s_g,
+                                        nbt_camera *out)
+{
+    if (!out || !(range > 0) || !(voxel_size > 0) || !(s_g >= 1.0) || !(fov_h > 0 && fov_h < M_PI) ||
+        !(fov_v > 0 && fov_v < M_PI))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_camera_from_grid_scaling: bad argument");
+    double delta = s_g * voxel_size;
+    double th = tan(fov_h / 2.0), tv = tan(fov_v / 2.0);
+    double rh = (range * th) / delta, rv = (range * tv) / delta;
+    double mh = floor(rh + 1e-9), mv = floor(rv + 1e-9);   // reading Q8: border point kept within 1e-9
+    if (mh > 30000 || mv > 30000) return fail(NBT_ERR_INVALID_ARG, "nbt_camera_from_grid_scaling: lattice too large");
+    out->width = 2 * (int32_t)mh + 1;
+    out->height = 2 * (int32_t)mv + 1;
+    out->cx = mh;
+    out->cy = mv;
+    out->fx = range / delta;
+    out->fy = range / delta;
+    out->tan_half_fov_h = th;
+    out->tan_half_fov_v = tv;
+    out->add_corners = !(fabs(rh - mh) <= 1e-9 && fabs(rv - mv) <= 1e-9);   // Q9 dedup
+    return NBT_OK;
+}
+
+int32_t nbt_camera_num_rays(const nbt_camera *cam)
+{
+    if (!cam) return 0;
+    return cam->width * cam->height + (cam->add_corners ? 4 : 0);
+}
+
+static nbt_status check_camera(const nbt_camera *cam)
+{
+    if (!cam) return fail(NBT_ERR_INVALID_ARG, "null camera");
+    if (cam->width < 1 || cam->height < 1 || cam->width > 65535 || cam->height > 65535)
+        return fail(NBT_ERR_INVALID_ARG, "camera lattice must be 1..65535 per axis");
+    if (!(cam->fx > 0) || !(cam->fy > 0) || !isfinite(cam->fx) || !isfinite(cam->fy))
+        return fail(NBT_ERR_INVALID_ARG, "camera fx, fy must be finite and > 0");
+    if (cam->cx * 2.0 != cam->width - 1 || cam->cy * 2.0 != cam->height - 1)
+        return fail(NBT_ERR_INVALID_ARG, "camera principal point must be the lattice centre (2cx = W-1)");
+    if (!isfinite(cam->tan_half_fov_h) || !isfinite(cam->tan_half_fov_v))
+        return fail(NBT_ERR_INVALID_ARG, "camera tan_half_fov must be finite");
+    if ((int64_t)cam->width * cam->height > (1ll << 30)) return fail(NBT_ERR_INVALID_ARG, "too many rays");
+    return NBT_OK;
+}
+
+// ------------------------------------------------------------ perspectives
+
+nbt_status nbt_sample_perspectives(nbt_ctx ctx, const double poi[3], double r_s, int32_t n, uint64_t seed,
+                                   int32_t mode, double *xyz_out, int out_on_device)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (!poi || !finite3(poi) || !(r_s > 0) || !isfinite(r_s) || n < 0 || (n > 0 && !xyz_out) ||
+        (mode != NBT_SAMPLE_BALL && mode != NBT_SAMPLE_SURFACE))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_sample_perspectives: bad argument");
+    if (n == 0) return NBT_OK;
+    double *dst = xyz_out;
+    if (!out_on_device) {
+        if ((s = ctx->out_tmp.ensure((size_t)n * 24))) return s;
+        dst = ctx->out_tmp.as<double>();
+    }
+    if ((s = launch_sample(ctx, poi, r_s, n, seed, mode, dst))) return s;
+    if (!out_on_device) return d2h_sync(ctx, xyz_out, dst, (size_t)n * 24);
+    return NBT_OK;
+}
+
+// ----------------------------------------------------------------- the ID
+
+static nbt_status id_common(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp, int32_t n_persp,
+                            int persp_on_device, int32_t first, int32_t stride, const nbt_camera *cam, double range,
+                            nbt_ig_cloud *out, const char *who)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (!m || m->ctx != ctx) return fail(NBT_ERR_STATE, std::string(who) + ": map belongs to another ctx");
+    if (!poi || !finite3(poi) || !out || n_persp < 0 || !(range > 0) || !isfinite(range))
+        return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": bad argument");
+    if ((s = check_camera(cam))) return s;
+    if (first < 0 || stride < 1) return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": bad first/stride");
+    int32_t n = (first < n_persp) ? (n_persp - first + stride - 1) / stride : 0;
+    if (n == 0) return NBT_OK;
+    if (!persp || !out->xyz || !out->gain) return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": null buffer");
+    const double *dpersp = persp;
+    if (!persp_on_device) {
+        for (int32_t i = 0; i < n; ++i) {
+            const double *p = persp + 3 * ((size_t)first + (size_t)i * stride);
+            if (!finite3(p)) return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": non-finite perspective " +
+                                                                   std::to_string(first + i * stride));
+            if (p[0] == poi[0] && p[1] == poi[1] && p[2] == poi[2])
+                return fail(NBT_ERR_DEGENERATE, std::string(who) + ": perspective " +
+                                                    std::to_string(first + i * stride) + " coincides with the PoI");
+        }
+        if ((s = stage_h2d(ctx, ctx->stage_in[0], ctx->persp, persp, (size_t)n_persp * 24))) return s;
+        dpersp = ctx->persp.as<double>();
+    }
+    IdLaunch L;
+    L.d_persp = dpersp;
+    L.n_src = n_persp;
+    L.first = first;
+    L.stride = stride;
+    L.n = n;
+    for (int k = 0; k < 3; ++k) L.poi[k] = poi[k];
+    L.cam = *cam;
+    L.range = range;
+    size_t xyz_b = (size_t)n * 24, gain_b = (size_t)n * 8, cnt_b = (size_t)n * 32;
+    if (out->on_device) {
+        L.d_xyz_out = out->xyz;
+        L.d_gain_out = out->gain;
+        L.d_counts_out = out->counts;
+        return launch_id(ctx, m, L);
+    }
+    if ((s = ctx->out_tmp.ensure(xyz_b + gain_b + cnt_b))) return s;
+    char *base = ctx->out_tmp.as<char>();
+    L.d_xyz_out = reinterpret_cast<double *>(base);
+    L.d_gain_out = reinterpret_cast<double *>(base + xyz_b);
+    L.d_counts_out = reinterpret_cast<uint64_t *>(base + xyz_b + gain_b);
+    if ((s = launch_id(ctx, m, L))) return s;
+    size_t total = xyz_b + gain_b + (out->counts ? cnt_b : 0);
+    if ((s = ctx->stage_out.acquire(total))) return s;
+    NBT_CUDA(cudaMemcpyAsync(ctx->stage_out.p, base, total, cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaStreamSynchronize(ctx->stream));
+    const char *h = static_cast<const char *>(ctx->stage_out.p);
+    memcpy(out->xyz, h, xyz_b);
+    memcpy(out->gain, h + xyz_b, gain_b);
+    if (out->counts) memcpy(out->counts, h + xyz_b + gain_b, cnt_b);
+    return take_device_error(ctx, who);
+}
+
+nbt_status nbt_id_compute(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp_xyz, int32_t n_persp,
+                          int persp_on_device, const nbt_camera *cam, double range, nbt_ig_cloud *out)
+{
+    return id_common(ctx, m, poi, persp_xyz, n_persp, persp_on_device, 0, 1, cam, range, out, "nbt_id_compute");
+}
+
+nbt_status nbt_id_compute_slice(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp_xyz,
+                                int32_t n_persp, int persp_on_device, int32_t first, int32_t stride,
+                                const nbt_camera *cam, double range, nbt_ig_cloud *out)
+{
+    return id_common(ctx, m, poi, persp_xyz, n_persp, persp_on_device, first, stride, cam, range, out,
+                     "nbt_id_compute_slice");
+}
+
+// ---------------------------------------------------------- ID buffer + IDW
+
+nbt_status nbt_idbuf_create(nbt_ctx ctx, int32_t capacity_nb, int32_t max_persp, nbt_idbuf *out)
+{
+    nbt_status s;
+    if (!out) return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_create: null out");
+    *out = nullptr;
+    if ((s = bind(ctx))) return s;
+    if (capacity_nb < 1 || capacity_nb > 64 || max_persp < 1)
+        return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_create: need 1 <= capacity <= 64 and max_persp >= 1");
+    nbt_idbuf b = new (std::nothrow) nbt_idbuf_s();
+    if (!b) return fail(NBT_ERR_OUT_OF_MEMORY, "nbt_idbuf_create");
+    b->ctx = ctx;
+    b->capacity = capacity_nb;
+    b->max_persp = max_persp;
+    cudaError_t e = cudaMalloc(&b->d_xyz, (size_t)capacity_nb * max_persp * 24);
+    if (e == cudaSuccess) e = cudaMalloc(&b->d_gain, (size_t)capacity_nb * max_persp * 8);
+    if (e != cudaSuccess) {
+        nbt_idbuf_destroy(b);
+        return cuda_fail(e, "nbt_idbuf_create");
+    }
+    *out = b;
+    return NBT_OK;
+}
+
+nbt_status nbt_idbuf_push(nbt_idbuf b, const nbt_ig_cloud *cloud, int32_t n)
+{
+    if (!b || !cloud) return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_push: null argument");
+    nbt_ctx ctx = b->ctx;
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (n < 1 || n > b->max_persp) return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_push: need 1 <= n <= max_persp");
+    if (!cloud->xyz || !cloud->gain) return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_push: null cloud buffers");
+    int32_t slot;
+    if (b->count < b->capacity) {
+        slot = (b->head + b->count) % b->capacity;
+        b->count++;
+    } else {
+        slot = b->head;                              // evict the oldest
+        b->head = (b->head + 1) % b->capacity;
+    }
+    b->sizes[slot] = n;
+    double *dx = b->d_xyz + (size_t)slot * b->max_persp * 3;
+    double *dg = b->d_gain + (size_t)slot * b->max_persp;
+    cudaMemcpyKind kind = cloud->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (cloud->on_device) {
+        NBT_CUDA(cudaMemcpyAsync(dx, cloud->xyz, (size_t)n * 24, kind, ctx->stream));
+        NBT_CUDA(cudaMemcpyAsync(dg, cloud->gain, (size_t)n * 8, kind, ctx->stream));
+        return NBT_OK;
+    }
+    HostStage &st = ctx->stage_in[2];
+    if ((s = st.acquire((size_t)n * 32))) return s;
+    memcpy(st.p, cloud->xyz, (size_t)n * 24);
+    memcpy((char *)st.p + (size_t)n * 24, cloud->gain, (size_t)n * 8);
+    NBT_CUDA(cudaMemcpyAsync(dx, st.p, (size_t)n * 24, kind, ctx->stream));
+    NBT_CUDA(cudaMemcpyAsync(dg, (char *)st.p + (size_t)n * 24, (size_t)n * 8, kind, ctx->stream));
+    return st.mark(ctx->stream);
+}
+
+nbt_status nbt_idbuf_clear(nbt_idbuf b)
+{
+    if (!b) return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_clear: null buffer");
+    b->head = 0;
+    b->count = 0;
+    return NBT_OK;
+}
+
+int32_t nbt_idbuf_size(nbt_idbuf b) { return b ? b->count : 0; }
+
+nbt_status nbt_ig_query(nbt_idbuf b, const double *query_xyz, int32_t n_q, int q_on_device, double power_p,
+                        double zero_eps, int32_t normalize_weights, double *g_out, int out_on_device)
+{
+    if (!b) return fail(NBT_ERR_INVALID_ARG, "nbt_ig_query: null buffer");
+    nbt_ctx ctx = b->ctx;
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (b->count == 0) return fail(NBT_ERR_EMPTY, "nbt_ig_query: no distribution available");
+    if (n_q < 0 || (n_q > 0 && (!query_xyz || !g_out)) || !(power_p >= 0) || !isfinite(power_p) ||
+        !(zero_eps >= 0) || !isfinite(zero_eps))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_ig_query: bad argument");
+    if (n_q == 0) return NBT_OK;
+    IdwEntries E;
+    E.m = b->count;
+    for (int e = 0; e < b->count; ++e) {
+        E.slot[e] = (b->head + e) % b->capacity;
+        E.size[e] = b->sizes[E.slot[e]];
+    }
+    const double *dq = query_xyz;
+    if (!q_on_device) {
+        for (int32_t i = 0; i < n_q; ++i)
+            if (!finite3(query_xyz + 3 * (size_t)i)) return fail(NBT_ERR_INVALID_ARG, "nbt_ig_query: non-finite query");
+        if ((s = stage_h2d(ctx, ctx->stage_in[2], ctx->queries, query_xyz, (size_t)n_q * 24))) return s;
+        dq = ctx->queries.as<double>();
+    }
+    double *dout = g_out;
+    if (!out_on_device) {
+        if ((s = ctx->qout.ensure((size_t)n_q * 8))) return s;
+        dout = ctx->qout.as<double>();
+    }
+    if ((s = launch_idw(ctx, b, E, dq, n_q, power_p, zero_eps, normalize_weights, dout))) return s;
+    if (!out_on_device) return d2h_sync(ctx, g_out, dout, (size_t)n_q * 8);
+    return NBT_OK;
+}
+
+void nbt_idbuf_destroy(nbt_idbuf b)
+{
+    if (!b) return;
+    cudaSetDevice(b->ctx->device);
+    cudaStreamSynchronize(b->ctx->stream);
+    if (b->d_xyz) cudaFree(b->d_xyz);
+    if (b->d_gain) cudaFree(b->d_gain);
+    delete b;
+}
+
+// -------------------------------------------------------------- test hooks
+
+nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *o_q16, const int32_t *e_q16, int32_t n_rays,
+                           int32_t max_visits, int32_t *ijk_out, uint8_t *code_out, int32_t *len_out,
+                           uint32_t *counts_out)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (!m || m->ctx != ctx) return fail(NBT_ERR_STATE, "nbt_debug_trace: map of another ctx");
+    if (n_rays < 0 || max_visits < 1 || (n_rays > 0 && (!o_q16 || !e_q16 || !ijk_out || !code_out || !len_out ||
+                                                        !counts_out)))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_debug_trace: bad argument");
+    if (n_rays == 0) return NBT_OK;
+    for (int32_t i = 0; i < 3 * n_rays; ++i)
+        if (o_q16[i] <= -(1 << 30) || o_q16[i] >= (1 << 30) || e_q16[i] <= -(1 << 30) || e_q16[i] >= (1 << 30))
+            return fail(NBT_ERR_INVALID_ARG, "nbt_debug_trace: coordinate outside (-2^30, 2^30)");
+    size_t nr = n_rays, mv = max_visits;
+    size_t b_in = nr * 12, b_ijk = nr * mv * 12, b_code = nr * mv, b_len = nr * 4, b_cnt = nr * 16;
+    size_t total = 2 * b_in + b_ijk + b_code + b_len + b_cnt + 64;
+    if ((s = ctx->dbg.ensure(total))) return s;
+    char *base = ctx->dbg.as<char>();
+    int32_t *d_o = (int32_t *)base, *d_e = (int32_t *)(base + b_in);
+    int32_t *d_ijk = (int32_t *)(base + 2 * b_in);
+    int32_t *d_len = (int32_t *)(base + 2 * b_in + b_ijk);
+    uint32_t *d_cnt = (uint32_t *)(base + 2 * b_in + b_ijk + b_len);
+    uint8_t *d_code = (uint8_t *)(base + 2 * b_in + b_ijk + b_len + b_cnt);
+    NBT_CUDA(cudaMemcpyAsync(d_o, o_q16, b_in, cudaMemcpyHostToDevice, ctx->stream));
+    NBT_CUDA(cudaMemcpyAsync(d_e, e_q16, b_in, cudaMemcpyHostToDevice, ctx->stream));
+    if ((s = launch_debug_trace(ctx, m, d_o, d_e, n_rays, max_visits, d_ijk, d_code, d_len, d_cnt))) return s;
+    NBT_CUDA(cudaMemcpyAsync(ijk_out, d_ijk, b_ijk, cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaMemcpyAsync(code_out, d_code, b_code, cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaMemcpyAsync(len_out, d_len, b_len, cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaMemcpyAsync(counts_out, d_cnt, b_cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return NBT_OK;
+}
+
+nbt_status nbt_debug_frames(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp_xyz, int32_t n,
+                            const nbt_camera *cam, double range, int32_t *q16_out, int32_t *status_out)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (!m || !poi || n < 0 || (n > 0 && (!persp_xyz || !q16_out || !status_out)))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_debug_frames: bad argument");
+    if ((s = check_camera(cam))) return s;
+    if (n == 0) return NBT_OK;
+    size_t b_in = (size_t)n * 24, b_out = (size_t)n * 19 * 4;
+    if ((s = ctx->dbg.ensure(b_in + b_out + 64))) return s;
+    double *d_p = ctx->dbg.as<double>();
+    int32_t *d_f = (int32_t *)(ctx->dbg.as<char>() + b_in);
+    NBT_CUDA(cudaMemcpyAsync(d_p, persp_xyz, b_in, cudaMemcpyHostToDevice, ctx->stream));
+    if ((s = launch_debug_frames(ctx, m, poi, d_p, n, *cam, range, d_f))) return s;
+    int32_t *h = new (std::nothrow) int32_t[(size_t)n * 19];
+    if (!h) return fail(NBT_ERR_OUT_OF_MEMORY, "nbt_debug_frames");
+    cudaError_t e = cudaMemcpyAsync(h, d_f, b_out, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess) {
+        for (int32_t i = 0; i < n; ++i) {
+            memcpy(q16_out + 18 * (size_t)i, h + 19 * (size_t)i, 18 * 4);
+            status_out[i] = h[19 * (size_t)i + 18];
+        }
+    }
+    delete[] h;
+    if (e != cudaSuccess) return cuda_fail(e, "nbt_debug_frames");
+    return NBT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,450 @@
+"""CUDA path (libnbt via its C ABI) vs the CPU oracle, element by element on the same seeded
+inputs.  Integer results (visited voxel sequences, per-state totals, lookups, map codes)
+must be bit-exact; g_P must be bit-exact too (same canonical fp64 expression, Q26); the
+sampler and IDW (different transcendental / summation order) within 1e-12 relative."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from nbt_inputs import CONFIGS, FOV_H, FOV_V, rand_map, random_segments_q16, tie_segments_q16, syn_map
+
+pytestmark = pytest.mark.gpu
+
+NTHREADS = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def nbt():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    from paper_2503_22588_b200 import _build
+    _build.build()
+    import paper_2503_22588_b200 as mod
+    return mod
+
+
+@pytest.fixture(scope="module")
+def ctx(nbt):
+    return nbt.Ctx(0)
+
+
+def make_map(nbt, ctx, codes, voxel_size=1.0, origin=(0.0, 0.0, 0.0), gain=None, policy=0):
+    nz, ny, nx = codes.shape
+    m = nbt.Map(ctx, nbt.map_desc(nx, ny, nz, voxel_size, origin, gain, policy))
+    m.upload(codes)
+    om = oracle.OracleMap(codes, voxel_size=voxel_size, origin=origin,
+                          gain=gain if gain is not None else (1.0, 0.12, 0.03), outside_policy=policy)
+    return m, om
+
+
+def run_both(nbt, ctx, m, om, poi, persp, w, h, range_, corners=False, grid=None):
+    if grid is None:
+        cam = nbt.camera_from_fov(FOV_H, FOV_V, w, h)
+        ocam = oracle.camera_from_fov(FOV_H, FOV_V, w, h)
+        cam.add_corners = ocam.add_corners = int(corners)
+    else:
+        cam = nbt.camera_from_grid_scaling(*grid)
+        ocam = oracle.camera_from_grid_scaling(*grid)
+    cloud = nbt.id_compute(ctx, m, poi, persp, cam, range_)
+    _, g, c = oracle.id_compute(om, poi, persp, ocam, range_, nthreads=NTHREADS)
+    return cloud, g, c
+
+
+def assert_cloud_equal(cloud, persp, g, c):
+    assert np.array_equal(np.asarray(cloud.xyz), np.asarray(persp))
+    assert np.array_equal(cloud.counts.astype(np.int64), c)
+    assert np.array_equal(cloud.gain, g)          # same canonical expression -> bit-exact
+
+
+# ------------------------------------------------------------------ map store
+
+def test_map_roundtrip_ragged(nbt, ctx):
+    codes = rand_map(0, seed=3, shape=(11, 23, 37))
+    m, _ = make_map(nbt, ctx, codes)
+    assert np.array_equal(m.download(), codes)
+    fresh = nbt.Map(ctx, nbt.map_desc(5, 6, 7, 1.0))
+    assert (fresh.download() == 0).all()          # created all Unknown
+
+
+def test_map_upload_rejects_bad_codes(nbt, ctx):
+    codes = rand_map(8, seed=1)
+    m, _ = make_map(nbt, ctx, codes)
+    bad = codes.copy(); bad[3, 4, 5] = 3
+    with pytest.raises(nbt.NbtError):
+        m.upload(bad)
+    assert np.array_equal(m.download(), codes)
+
+
+def test_map_upload_prob_matches_classify(nbt, ctx):
+    rng = np.random.default_rng(0)
+    p = rng.uniform(0, 1, (9, 10, 11)).astype(np.float32)
+    p[0, 0, :4] = [0.5, 0.3, 0.7, 0.12]
+    obs = (rng.uniform(size=p.shape) < 0.8).astype(np.uint8)
+    m = nbt.Map(ctx, nbt.map_desc(11, 10, 9, 1.0))
+    for t_occ, t_free in [(0.5, 0.5), (0.7, 0.3)]:
+        m.upload_prob(p, obs, t_occ, t_free)
+        want = oracle.classify(p, obs, t_occ, t_free).reshape(p.shape)
+        assert np.array_equal(m.download(), want)
+
+
+def _apply_in_order(codes, ijk, vals):
+    out = codes.copy()
+    for (x, y, z), v in zip(ijk, vals):
+        out[z, y, x] = v
+    return out
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_map_update_last_wins(nbt, ctx, on_device):
+    import torch
+    codes = rand_map(0, seed=5, shape=(13, 17, 19))
+    m, _ = make_map(nbt, ctx, codes)
+    rng = np.random.default_rng(2)
+    n = 5000
+    ijk = np.stack([rng.integers(0, 19, n), rng.integers(0, 17, n), rng.integers(0, 13, n)], 1).astype(np.int32)
+    ijk[n // 2:] = ijk[: n - n // 2]                  # many duplicates
+    vals = rng.integers(0, 3, n).astype(np.uint8)
+    if on_device:
+        m.update(torch.from_numpy(ijk).cuda(), torch.from_numpy(vals).cuda())
+    else:
+        m.update(ijk, vals)
+    ctx.sync()
+    assert np.array_equal(m.download(), _apply_in_order(codes, ijk, vals))
+
+
+def test_map_update_validation(nbt, ctx):
+    import torch
+    m, _ = make_map(nbt, ctx, rand_map(6, seed=1))
+    with pytest.raises(nbt.NbtError):
+        m.update(np.array([[6, 0, 0]], np.int32), np.array([1], np.uint8))
+    with pytest.raises(nbt.NbtError):
+        m.update(np.array([[0, 0, 0]], np.int32), np.array([3], np.uint8))
+    # device input: invalid entries are skipped and reported by the next sync
+    before = m.download()
+    m.update(torch.tensor([[0, 0, 0], [-1, 2, 2]], dtype=torch.int32, device="cuda"),
+             torch.tensor([2, 1], dtype=torch.uint8, device="cuda"))
+    with pytest.raises(nbt.NbtError):
+        ctx.sync()
+    after = before.copy(); after[0, 0, 0] = 2
+    assert np.array_equal(m.download(), after)
+    ctx.sync()                                        # error cleared
+
+
+# ------------------------------------------------------------ per-ray walks
+
+def _compare_walks(nbt, ctx, m, om, o, e, max_visits=256):
+    ijk, cd, ln, cnt = nbt.debug_trace(ctx, m, o, e, max_visits)
+    for r in range(len(o)):
+        w_ijk, w_cd, w = oracle.trace_ray(om, o[r], e[r], max_visits)
+        k = min(ln[r], max_visits)
+        assert ln[r] == w.visits
+        assert np.array_equal(ijk[r, :k], w_ijk[:k]), r
+        assert np.array_equal(cd[r, :k], w_cd[:k]), r
+        assert tuple(cnt[r]) == (w.n_u, w.n_f, w.n_o, w.lookups), r
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_walks_random_segments(nbt, ctx, policy):
+    """Every visited voxel of 3000 random rays, inside, leaving and outside the grid."""
+    codes = rand_map(12, 0.3, 0.68, 0.02, seed=7)
+    m, om = make_map(nbt, ctx, codes, policy=policy)
+    o, e = random_segments_q16(3000, -5.0, 17.0, seed=policy + 1)
+    _compare_walks(nbt, ctx, m, om, o, e)
+
+
+def test_walks_ties(nbt, ctx):
+    """Endpoints on faces, edges and corners (exact ties of the DDA)."""
+    codes = rand_map(8, 0.4, 0.6, 0.0, seed=2)
+    m, om = make_map(nbt, ctx, codes)
+    o, e = tie_segments_q16(4000, 9, seed=4)
+    o -= 65536
+    _compare_walks(nbt, ctx, m, om, o, e)
+
+
+def test_walks_hand_traced(nbt, ctx):
+    from conftest import read_golden
+    m, om = make_map(nbt, ctx, np.ones((4, 4, 4), np.uint8))
+    for row in read_golden("dda_hand_traced.txt"):
+        _, o, e, seq = [s.strip() for s in row.split("|")]
+        o = [int(round(float(v) * 65536)) for v in o.split()]
+        e = [int(round(float(v) * 65536)) for v in e.split()]
+        want = [tuple(int(t) for t in v.split()) for v in seq.split(";")]
+        ijk, _, ln, _ = nbt.debug_trace(ctx, m, [o], [e], 16)
+        assert [tuple(v) for v in ijk[0, :ln[0]]] == want
+
+
+def test_walks_long_rays(nbt, ctx):
+    """Long walks (1000+ voxels) through a sparse map: no drift of the decision terms."""
+    codes = rand_map(64, 0.5, 0.5, 0.0, seed=9)
+    m, om = make_map(nbt, ctx, codes)
+    o, e = random_segments_q16(200, -30.0, 94.0, seed=12)
+    _compare_walks(nbt, ctx, m, om, o, e, max_visits=400)
+
+
+# ---------------------------------------------------------------- frames
+
+def test_frames_bit_exact(nbt, ctx):
+    """T19: host (oracle) and device frame quantisation are bit-identical."""
+    m, om = make_map(nbt, ctx, np.zeros((4, 4, 4), np.uint8), voxel_size=0.01, origin=(-1.0, 0.5, 0.25))
+    rng = np.random.default_rng(0)
+    poi = np.array([0.3, 0.9, 0.6])
+    P = poi + rng.normal(size=(20000, 3)) * 0.7
+    P[:50] = poi + rng.normal(size=(50, 3)) * [1e-9, 1e-9, 1.0]       # near-vertical views (fallback axis)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 640, 480)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, 640, 480)
+    q, st = nbt.debug_frames(ctx, m, poi, P, cam, 1.5)
+    assert (st == 0).all()
+    for i in range(0, len(P), 7):
+        f = oracle.frame(om, poi, P[i], ocam, 1.5)
+        want = np.concatenate([f[k] for k in ("o", "a", "rh", "uh", "rc", "uc")])
+        assert np.array_equal(q[i], want), i
+
+
+# -------------------------------------------------------------- the ID
+
+def test_config_a_full(nbt, ctx):
+    cfg = CONFIGS["A"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)
+    cloud, g, c = run_both(nbt, ctx, m, om, cfg.poi, P, cfg.width, cfg.height, cfg.range_)
+    assert_cloud_equal(cloud, P, g, c)
+
+
+def test_config_a_every_ray(nbt, ctx):
+    """Per-ray parity for config A: device walks of the oracle's endpoints, all 12288 rays."""
+    cfg = CONFIGS["A"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    for p in P:
+        o, e, rc = oracle.perspective_rays(om, cfg.poi, p, ocam, cfg.range_)
+        _, _, _, cnt = nbt.debug_trace(ctx, m, np.repeat(o[None], len(e), 0), e, 4)
+        assert np.array_equal(cnt.astype(np.int64), rc[:, :4])
+
+
+def test_config_b_subset(nbt, ctx):
+    """Config B map, camera and range; every 8th of its 512 perspectives."""
+    cfg = CONFIGS["B"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)[::8]
+    cloud, g, c = run_both(nbt, ctx, m, om, cfg.poi, P, cfg.width, cfg.height, cfg.range_)
+    assert_cloud_equal(cloud, P, g, c)
+
+
+def test_config_c_two_full_resolution_perspectives(nbt, ctx):
+    """640x480 rays (config C) for two perspectives."""
+    cfg = CONFIGS["C"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)[[0, 101]]
+    cloud, g, c = run_both(nbt, ctx, m, om, cfg.poi, P, cfg.width, cfg.height, cfg.range_)
+    assert_cloud_equal(cloud, P, g, c)
+
+
+def test_config_d_subset(nbt, ctx):
+    """512^3 map (config D) at 160x120 rays, 6 of its 4096 perspectives."""
+    cfg = CONFIGS["D"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)[::700]
+    cloud, g, c = run_both(nbt, ctx, m, om, cfg.poi, P, cfg.width, cfg.height, cfg.range_)
+    assert_cloud_equal(cloud, P, g, c)
+
+
+@pytest.mark.parametrize("w,h,corners", [(1, 1, False), (1, 7, False), (9, 1, True), (13, 5, True), (37, 29, False)])
+def test_lattice_shapes(nbt, ctx, w, h, corners):
+    """Ragged lattices (not multiples of the 8x4 tile), single rows/columns, corner rays."""
+    codes = rand_map(24, 0.3, 0.66, 0.04, seed=w * 7 + h)
+    m, om = make_map(nbt, ctx, codes, 0.5, origin=(-1.0, -2.0, 0.5))
+    poi = np.array([5.1, 4.2, 6.7])
+    P = oracle.sample_perspectives(poi, 4.0, 33, seed=w + h)
+    cloud, g, c = run_both(nbt, ctx, m, om, poi, P, w, h, 9.0, corners=corners)
+    assert_cloud_equal(cloud, P, g, c)
+
+
+@pytest.mark.parametrize("s_g", [20, 40])
+def test_grid_scaling_camera(nbt, ctx, s_g):
+    cfg = CONFIGS["B"]
+    m, om = make_map(nbt, ctx, syn_map(96, 10.0, 4), 0.01)
+    poi = np.array([0.485, 0.485, 0.485])
+    P = oracle.sample_perspectives(poi, 0.3, 40, seed=s_g)
+    cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 0, 0, 0.6, grid=(FOV_H, FOV_V, 0.6, 0.01, float(s_g)))
+    assert_cloud_equal(cloud, P, g, c)
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_perspectives_outside_grid(nbt, ctx, policy):
+    """Origins outside the map (slow entry path), rays missing the map entirely, clip policy."""
+    codes = rand_map(16, 0.3, 0.69, 0.01, seed=11)
+    m, om = make_map(nbt, ctx, codes, 1.0, policy=policy)
+    poi = np.array([8.0, 8.0, 8.0])
+    rng = np.random.default_rng(1)
+    d = rng.normal(size=(40, 3)); d /= np.linalg.norm(d, axis=1, keepdims=True)
+    P = poi + d * rng.uniform(9, 30, (40, 1))
+    P[0] = [-20.0, 8.0, 8.0]
+    cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 16, 12, 40.0, corners=True)
+    assert_cloud_equal(cloud, P, g, c)
+
+
+def test_degenerate_and_special_maps(nbt, ctx):
+    poi = np.array([3.5, 3.5, 3.5])
+    m, om = make_map(nbt, ctx, np.full((7, 7, 7), 2, np.uint8), gain=(1.0, 0.12, 0.0))
+    P = np.array([[1.0, 1.0, 1.0], [6.0, 2.0, 3.0]])
+    cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 8, 6, 5.0)
+    assert_cloud_equal(cloud, P, g, c)
+    assert (cloud.gain == 0).all()
+    with pytest.raises(nbt.NbtError) as ei:
+        nbt.id_compute(ctx, m, poi, np.array([[1.0, 1.0, 1.0], poi]), nbt.camera_from_fov(1.0, 1.0, 4, 4), 3.0)
+    assert ei.value.status == nbt.ERR_DEGENERATE
+    with pytest.raises(nbt.NbtError):     # Q16 overflow: rays far beyond +-2^14 voxels
+        nbt.id_compute(ctx, m, poi, P, nbt.camera_from_fov(1.0, 1.0, 4, 4), 40000.0)
+    ctx.sync()
+    tiny, otiny = make_map(nbt, ctx, np.array([[[1]]], np.uint8))
+    cloud, g, c = run_both(nbt, ctx, tiny, otiny, np.array([0.5, 0.5, 0.5]), np.array([[0.5, 0.5, 2.5]]), 3, 3, 4.0)
+    assert_cloud_equal(cloud, np.array([[0.5, 0.5, 2.5]]), g, c)
+
+
+def test_voxel_face_origins(nbt, ctx):
+    """Perspectives and PoI exactly on voxel faces / corners (exact-tie starts)."""
+    codes = rand_map(20, 0.3, 0.7, 0.0, seed=3)
+    m, om = make_map(nbt, ctx, codes)
+    poi = np.array([10.0, 10.0, 10.0])
+    P = np.array([[2.0, 10.0, 10.0], [10.0, 3.0, 10.0], [4.0, 4.0, 4.0], [16.0, 4.0, 10.5], [10.0, 10.0, 2.0]])
+    cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 9, 9, 12.0, corners=True)
+    assert_cloud_equal(cloud, P, g, c)
+
+
+def test_slices_and_device_io(nbt, ctx):
+    """Shards (first, stride) equal rows of the full result; device in/out equals host in/out."""
+    import torch
+    cfg = CONFIGS["A"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, 20.0, 50, seed=3)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 24, 18)
+    full = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
+    for first, stride in [(0, 3), (2, 3), (5, 7), (49, 4)]:
+        part = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_, first=first, stride=stride)
+        assert np.array_equal(part.gain, full.gain[first::stride])
+        assert np.array_equal(part.counts, full.counts[first::stride])
+    dP = torch.from_numpy(P).cuda()
+    out = nbt.empty_cloud(50, device="cuda")
+    nbt.id_compute(ctx, m, cfg.poi, dP, cam, cfg.range_, out=out)
+    ctx.sync()
+    assert np.array_equal(out.gain.cpu().numpy(), full.gain)
+    assert np.array_equal(out.counts.cpu().numpy().astype(np.uint64), full.counts)
+
+
+def test_deterministic_and_permutation(nbt, ctx):
+    cfg = CONFIGS["A"]
+    m, _ = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, 20.0, 64, seed=8)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 32, 24)
+    a = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
+    b = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
+    perm = np.random.default_rng(0).permutation(64)
+    c = nbt.id_compute(ctx, m, cfg.poi, P[perm], cam, cfg.range_)
+    assert np.array_equal(a.gain, b.gain) and np.array_equal(a.counts, b.counts)
+    assert np.array_equal(a.gain[perm], c.gain)
+
+
+def test_update_then_compute_snapshot(nbt, ctx):
+    """Stream order: an update issued after a compute does not change what it read."""
+    import torch
+    cfg = CONFIGS["A"]
+    codes = cfg.map_codes()
+    m, om = make_map(nbt, ctx, codes, cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, 20.0, 16, seed=1)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 32, 24)
+    out = nbt.empty_cloud(16, device="cuda")
+    nbt.id_compute(ctx, m, cfg.poi, torch.from_numpy(P).cuda(), cam, cfg.range_, out=out)
+    ijk = np.argwhere(codes == 1)[:, ::-1].astype(np.int32)[:20000]
+    m.update(ijk, np.full(len(ijk), 2, np.uint8))
+    ctx.sync()
+    _, g, c = oracle.id_compute(om, cfg.poi, P, oracle.camera_from_fov(FOV_H, FOV_V, 32, 24), cfg.range_)
+    assert np.array_equal(out.counts.cpu().numpy().astype(np.int64), c)
+    after = _apply_in_order(codes, ijk, np.full(len(ijk), 2, np.uint8))
+    om2 = oracle.OracleMap(after, voxel_size=cfg.voxel_size)
+    cloud2 = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
+    _, g2, c2 = oracle.id_compute(om2, cfg.poi, P, oracle.camera_from_fov(FOV_H, FOV_V, 32, 24), cfg.range_)
+    assert np.array_equal(cloud2.counts.astype(np.int64), c2)
+
+
+# -------------------------------------------------------------- sampler
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_sampler_matches_oracle(nbt, ctx, mode):
+    poi = np.array([0.3, -0.2, 1.1])
+    want = oracle.sample_perspectives(poi, 1.0, 20000, seed=77, mode=mode)
+    got = nbt.sample_perspectives(ctx, poi, 1.0, 20000, seed=77, mode=mode)
+    assert np.abs(got - want).max() < 1e-12
+    import torch
+    dev = torch.empty((20000, 3), dtype=torch.float64, device="cuda")
+    nbt.sample_perspectives(ctx, poi, 1.0, 20000, seed=77, mode=mode, out=dev)
+    ctx.sync()
+    assert np.array_equal(dev.cpu().numpy(), got)
+
+
+# -------------------------------------------------------------- IDW
+
+@pytest.mark.parametrize("power_p,normalize", [(2.0, False), (3.0, False), (2.0, True), (1.0, False)])
+def test_idw_matches_oracle(nbt, ctx, power_p, normalize):
+    rng = np.random.default_rng(int(power_p * 10) + normalize)
+    buf = nbt.IdBuffer(ctx, 10, 700)
+    entries = []
+    for k in range(13):                               # more than N_B: the oldest 3 are evicted
+        n = int(rng.integers(1, 700))
+        xyz = rng.normal(size=(n, 3)); gain = rng.uniform(0, 4, n)
+        buf.push(nbt.IgCloud(xyz, gain, None))
+        entries.append((xyz, gain))
+    assert len(buf) == 10
+    q = rng.normal(size=(1984, 3)) * 1.2
+    q[:5] = entries[-1][0][:5]                        # zero distance to the newest entry
+    got = buf.query(q, power_p=power_p, normalize=normalize)
+    want = oracle.idw_query(entries[-10:], q, power_p=power_p, normalize=normalize)
+    assert np.allclose(got, want, rtol=1e-12, atol=0)
+
+
+def test_idw_empty_and_device(nbt, ctx):
+    import torch
+    buf = nbt.IdBuffer(ctx, 4, 16)
+    with pytest.raises(nbt.NbtError) as ei:
+        buf.query(np.zeros((1, 3)))
+    assert ei.value.status == nbt.ERR_EMPTY
+    xyz = torch.randn(16, 3, dtype=torch.float64, device="cuda")
+    gain = torch.rand(16, dtype=torch.float64, device="cuda")
+    buf.push(nbt.IgCloud(xyz, gain, None))
+    q = torch.randn(100, 3, dtype=torch.float64, device="cuda")
+    out = torch.empty(100, dtype=torch.float64, device="cuda")
+    buf.query(q, out=out)
+    ctx.sync()
+    want = oracle.idw_query([(xyz.cpu().numpy(), gain.cpu().numpy())], q.cpu().numpy())
+    assert np.allclose(out.cpu().numpy(), want, rtol=1e-12)
+
+
+# --------------------------------------------- full size, bench launch configuration
+
+def test_full_size_config_b_sampled(nbt, ctx):
+    """Config B at its full size (512 x 64x48, the bench workload and launch shape): every
+    perspective satisfies the closed-form/invariant bounds, and 24 sampled perspectives
+    are recomputed one by one by the oracle."""
+    import torch
+    cfg = CONFIGS["B"]
+    codes = cfg.map_codes()
+    m, om = make_map(nbt, ctx, codes, cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    out = nbt.empty_cloud(cfg.n_persp, device="cuda")
+    nbt.id_compute(ctx, m, cfg.poi, torch.from_numpy(P).cuda(), cam, cfg.range_, out=out)
+    ctx.sync()
+    counts = out.counts.cpu().numpy()
+    gain = out.gain.cpu().numpy()
+    ne = cam.num_rays
+    assert (counts[:, 2] <= ne).all() and (counts[:, 3] <= counts[:, :3].sum(1)).all()
+    assert (gain >= 0).all() and np.isfinite(gain).all()
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    idx = np.linspace(0, cfg.n_persp - 1, 24).astype(int)
+    _, g, c = oracle.id_compute(om, cfg.poi, P[idx], ocam, cfg.range_, nthreads=NTHREADS)
+    assert np.array_equal(counts[idx].astype(np.int64), c)
+    assert np.array_equal(gain[idx], g)
