@@ -81,6 +81,7 @@ def lib():
         L.orc_eq1.restype = None
         L.orc_classify.argtypes = [C.POINTER(C.c_float), u8p, C.c_int64, C.c_double, C.c_double, u8p]
         L.orc_classify.restype = None
+        L.orc_map_update.argtypes = [u8p, C.c_int32, C.c_int32, C.c_int32, ip, u8p, C.c_int64]
     return _lib
 
 
@@ -229,3 +230,13 @@ def classify(p, observed, t_occ=0.5, t_free=0.5):
     lib().orc_classify(_p(p, C.c_float), _p(obs, C.c_uint8), p.size, float(t_occ), float(t_free),
                        _p(out, C.c_uint8))
     return out
+
+
+def map_update(m: OracleMap, ijk, vals):
+    """Apply deltas in order to the oracle map's code array (in place)."""
+    ijk = np.ascontiguousarray(ijk, dtype=np.int32).reshape(-1, 3)
+    vals = np.ascontiguousarray(vals, dtype=np.uint8)
+    nz, ny, nx = m.codes.shape
+    st = lib().orc_map_update(_p(m.codes, C.c_uint8), nx, ny, nz, _p(ijk, C.c_int32), _p(vals, C.c_uint8), len(vals))
+    if st:
+        raise OracleError(st, "map_update")

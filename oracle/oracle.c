@@ -532,4 +532,16 @@ void orc_classify(const float *p, const uint8_t *observed, int64_t n, double t_o
     }
 }
 
+/* Map deltas (row a2): applied in array order, so the last delta of a voxel wins (Q30). */
+int orc_map_update(uint8_t *codes, int32_t nx, int32_t ny, int32_t nz, const int32_t *ijk, const uint8_t *vals,
+                   int64_t n)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t x = ijk[3 * i], y = ijk[3 * i + 1], z = ijk[3 * i + 2];
+        if (x < 0 || y < 0 || z < 0 || x >= nx || y >= ny || z >= nz || vals[i] > 2) return ORC_ERR_INVALID_ARG;
+        codes[x + (int64_t)nx * (y + (int64_t)ny * z)] = vals[i];
+    }
+    return ORC_OK;
+}
+
 int orc_version(void) { return 1; }

@@ -1,0 +1,148 @@
+"""Multi-GPU orchestration of the ID: one process per GPU, torch.distributed
+(NCCL over NVLink/NVSwitch on the B200 box; gloo for the CPU tests).
+
+Perspectives are independent, so the path shards across ranks with exactly two kinds of
+exchange, both real data movement of the method:
+
+* map replication -- the packed 2-bit store (4 MiB at 256^3, 32 MiB at 512^3) is
+  broadcast once from the rank that built it, and each cycle's map deltas (KB-scale)
+  are broadcast so every replica applies the same update (the single-writer rule,
+  S:97-98, holds per replica by stream order);
+* the IG point cloud -- each rank computes a strided slice of the perspective set
+  (perspective j -> rank j mod G, so cheap in-object and expensive open-space
+  perspectives spread evenly), and one all-gather assembles the cloud in input order on
+  every rank, where the IDW query runs.
+
+Integer per-state totals make the result bit-identical to a single-GPU run (the g_P of a
+perspective depends only on its own totals).  The arithmetic stays in libnbt; this module
+only moves tensors.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+
+def env_rank_world():
+    """(rank, world, local_rank) from the torchrun environment (1 process if absent)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def init_process_group(backend="nccl"):
+    import torch.distributed as dist
+    rank, world, local = env_rank_world()
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ shard logic
+
+def shard_count(n: int, rank: int, world: int) -> int:
+    """Number of perspectives j < n with j mod world == rank."""
+    return max(0, (n - rank + world - 1) // world) if rank < n else 0
+
+
+def rows_per_rank(n: int, world: int) -> int:
+    return (n + world - 1) // world
+
+
+def unstride(gathered, n: int, world: int):
+    """gathered: (world, R, ...) with rank r's rows r, r+W, r+2W, ... padded to R.
+    Returns the (n, ...) array in the original perspective order."""
+    R = gathered.shape[1]
+    tail = tuple(gathered.shape[2:])
+    if hasattr(gathered, "transpose") and not isinstance(gathered, np.ndarray):
+        flat = gathered.transpose(0, 1).reshape((world * R,) + tail)
+    else:
+        flat = np.swapaxes(gathered, 0, 1).reshape((world * R,) + tail)
+    return flat[:n]
+
+
+def pad_rows(t, rows: int):
+    """Pad a (k, ...) tensor to (rows, ...) with NaN / zeros (dropped after the gather)."""
+    import torch
+    k = t.shape[0]
+    if k == rows:
+        return t.contiguous()
+    fill = float("nan") if t.dtype.is_floating_point else 0
+    out = torch.full((rows,) + tuple(t.shape[1:]), fill, dtype=t.dtype, device=t.device)
+    out[:k] = t
+    return out
+
+
+# ------------------------------------------------------------------ collectives
+
+class _CudaBytes:
+    """__cuda_array_interface__ view of a raw device allocation (the packed map)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3}
+
+
+def map_tensor(m):
+    """A uint8 CUDA tensor aliasing the map's packed store (no copy)."""
+    import torch
+    ptr, nbytes = m.device_buffer()
+    return torch.as_tensor(_CudaBytes(ptr, nbytes), device=torch.device("cuda", m.ctx.device))
+
+
+def replicate_map(m, src: int = 0, group=None):
+    """Broadcast the packed store of `src`'s map into every rank's map (same desc)."""
+    import torch.distributed as dist
+    m.ctx.sync()
+    dist.broadcast(map_tensor(m), src=src, group=group)
+
+
+def broadcast_deltas(ijk, codes, src: int = 0, group=None):
+    """Broadcast one cycle's map deltas (device tensors of equal shape on every rank)."""
+    import torch.distributed as dist
+    dist.broadcast(ijk, src=src, group=group)
+    dist.broadcast(codes, src=src, group=group)
+
+
+def all_gather_rows(local, n_total: int, world: int, strided: bool = True, group=None):
+    """All-gather per-rank row blocks into the full (n_total, ...) array on every rank.
+    strided=True: rank r holds rows r, r+W, ... (shard_count rows); False: contiguous
+    equal blocks (weak scaling: rank r holds rows r*k .. r*k + k-1)."""
+    import torch
+    import torch.distributed as dist
+    R = rows_per_rank(n_total, world) if strided else local.shape[0]
+    loc = pad_rows(local, R)
+    out = torch.empty((world * R,) + tuple(loc.shape[1:]), dtype=loc.dtype, device=loc.device)
+    dist.all_gather_into_tensor(out, loc, group=group)
+    if not strided:
+        return out[:n_total]
+    return unstride(out.view((world, R) + tuple(loc.shape[1:])), n_total, world)
+
+
+def id_compute_sharded(nbt, ctx, m, poi, persp_dev, cam, range_, rank: int, world: int, group=None):
+    """The whole ID of `persp_dev` (n x 3 CUDA tensor, identical on every rank), sharded
+    j -> rank j mod world, gathered in input order on every rank: (xyz, gain, counts)."""
+    import torch
+    n = persp_dev.shape[0]
+    k = shard_count(n, rank, world)
+    dev = persp_dev.device
+    local = nbt.IgCloud(torch.empty((k, 3), dtype=torch.float64, device=dev),
+                        torch.empty(k, dtype=torch.float64, device=dev),
+                        torch.empty((k, 4), dtype=torch.int64, device=dev))
+    if k:
+        nbt.id_compute(ctx, m, poi, persp_dev, cam, range_, out=local, first=rank, stride=world)
+    if world == 1:
+        return local.xyz, local.gain, local.counts
+    xyz = all_gather_rows(local.xyz, n, world, group=group)
+    gain = all_gather_rows(local.gain, n, world, group=group)
+    counts = all_gather_rows(local.counts, n, world, group=group)
+    return xyz.contiguous(), gain.contiguous(), counts.contiguous()
