@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the online local Information Distribution on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config B]
+
+One STEP is one pass of the whole hot path for one MHP cycle
+on one batch of synthetic input (config B of BASELINE.json: 256^3 SYN map, 1 cm voxels,
+512 perspectives x 64x48 rays, range 1.5 m):
+  a2  apply this cycle's map deltas (nbt_map_update; broadcast from rank 0 when N > 1)
+  a3  sample the perspective set by Eq. 1 on the device
+  a4-a8  nbt_id_compute -> IG point cloud (frames, rays, exact DDA, scores, means)
+       (N > 1: all-gather of the cloud rows over NCCL)
+  a9  push the cloud into the N_B = 10 ring buffer and run 1984 IDW queries (Eq. 4)
+Map construction/upload is excluded.  Weak scaling: every rank computes its own
+512-perspective ID per step; `value` = rays of all ranks / max-over-ranks device time.
+Rank 0 prints one JSON line.  The L2 (126 MB) is flushed with a 256 MiB write before
+every timed step.  `--impl reference` times the CPU oracle (the only "reference" this
+paper-only build has) on the same workload, a bounded sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from nbt_inputs import CONFIGS, FOV_H, FOV_V, cycle_deltas, query_points  # noqa: E402
+
+N_QUERIES = 1984          # 64 trajectories x (K + 1 = 31) poses, K = 30
+N_B = 10                  # ID buffering
+POWER_P = 2.0             # IDW power
+N_DELTA_SETS = 8
+OPS_PER_LOOKUP = 13       # algorithmic int32 ops per in-grid voxel step
+INT_LANES_PER_SM_CLK = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="B")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def workload_name(cfg, world):
+    return (f"{cfg.name}: {cfg.n}^3 SYN map (s_Vox={cfg.voxel_size} m, R_o={cfg.r_o:g} vox), "
+            f"{cfg.n_persp} perspectives/rank ({'ball' if cfg.persp_mode == 0 else 'surface'} r_S={cfg.persp_radius} m) "
+            f"x {cfg.width}x{cfg.height} rays, range {cfg.range_} m; + map deltas, + {N_QUERIES} IDW queries "
+            f"over N_B={N_B}")
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons every 100 ms; keeps samples with timestamps."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.samples = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", gpu_id, f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append((time.time(), parts))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        inside = [p for t, p in self.samples if t0 <= t <= t1 + 0.15]
+        note = "sampled during the timed region"
+        if not inside and self.samples:
+            best = min(self.samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))
+            inside = [best[1]]
+            note = "timed region shorter than the 100 ms sampling period: nearest sample"
+        if not inside:
+            return None
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(p[1]) for p in inside if num(p[1]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in inside for i in range(4) if p[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(inside[0][2]),
+                "reasons": reasons, "samples": len(inside), "note": note}
+
+
+# ------------------------------------------------------------ CPU oracle leg
+
+def cpu_oracle_sample(cfg, codes, budget_s, steps=1):
+    """Time the oracle (all host cores) on a bounded, strided sample of the workload's
+    perspectives; returns rays/s, voxel-steps/s and a description."""
+    import oracle
+    oracle.build()
+    nthreads = os.cpu_count() or 1
+    om = oracle.OracleMap(codes, voxel_size=cfg.voxel_size)
+    cam = oracle.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    ne = oracle.num_rays(cam)
+    persp = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)
+    k = max(1, min(nthreads, cfg.n_persp))
+    t = time.perf_counter()
+    oracle.id_compute(om, cfg.poi, persp[:: max(1, cfg.n_persp // k)][:k], cam, cfg.range_, nthreads=nthreads)
+    t_probe = time.perf_counter() - t
+    per_persp = t_probe / k
+    n = int(max(1, min(cfg.n_persp, budget_s / max(per_persp, 1e-9) / steps)))
+    sel = persp[:: max(1, cfg.n_persp // n)][:n]
+    return om, cam, ne, sel, nthreads
+
+
+def run_cpu_baseline(cfg, codes, budget_s):
+    import oracle
+    om, cam, ne, sel, nthreads = cpu_oracle_sample(cfg, codes, budget_s)
+    t = time.perf_counter()
+    _, _, c = oracle.id_compute(om, cfg.poi, sel, cam, cfg.range_, nthreads=nthreads)
+    dt = time.perf_counter() - t
+    rays = len(sel) * ne
+    return {"value": rays / dt, "unit": "rays/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"{len(sel)} of {cfg.n_persp} perspectives (strided) of config {cfg.name}, all {ne} rays "
+                      f"each, OpenMP over perspectives on {nthreads} host threads, {dt:.2f} s",
+            "voxel_steps_per_s": float(c[:, :3].sum()) / dt, "lookups_per_s": float(c[:, 3].sum()) / dt}
+
+
+def reference_arm(args, cfg):
+    """--impl reference: the CPU oracle as it stands, on the same metric/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    codes = cfg.map_codes()
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    om, cam, ne, sel, nthreads = cpu_oracle_sample(cfg, codes, budget * (args.steps + args.warmup),
+                                                   steps=args.steps + args.warmup)
+    deltas = [cycle_deltas(cfg.n, (cfg.n // 2,) * 3, c, codes, seed=1) for c in range(N_DELTA_SETS)]
+    q = query_points(N_QUERIES, cfg.poi, cfg.persp_radius, 0.5, 1.2, seed=5)
+    entries = []
+    times, rays = [], 0
+    for step in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        ijk, vals = deltas[step % N_DELTA_SETS]
+        oracle.map_update(om, ijk, vals)
+        xyz, g, _ = oracle.id_compute(om, cfg.poi, sel, cam, cfg.range_, nthreads=nthreads)
+        entries = (entries + [(xyz, g)])[-N_B:]
+        oracle.idw_query(entries, q, power_p=POWER_P)
+        dt = time.perf_counter() - t
+        if step >= args.warmup:
+            times.append(dt)
+            rays += len(sel) * ne
+    total = sum(times)
+    value = rays / total
+    line = {"metric": "rays/s", "value": value, "unit": "rays/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": {"workload": workload_name(cfg, 1),
+                                            "sample_per_step": f"{len(sel)} of {cfg.n_persp} perspectives"},
+            "cpu_baseline": {"value": value, "unit": "rays/s", "cores": nthreads, "kind": "oracle",
+                             "sample": f"{len(sel)} strided perspectives of config {cfg.name} per step, all {ne} "
+                                       f"rays each; deltas + ID + {N_QUERIES} IDW queries; {nthreads} threads"},
+            "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------- our arm
+
+def main_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_22588_b200 as nbt
+    from paper_2503_22588_b200 import dist as ndist
+
+    rank, world, local = ndist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    # one dedicated stream shared by libnbt, torch's events and NCCL (the legacy default
+    # stream handle 0 would make libnbt create its own stream)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx = nbt.Ctx(local, stream.cuda_stream)
+    pk, pk_kind = peaks()
+
+    # ---- map: built and uploaded on rank 0, replicated by NCCL broadcast (excluded from timing)
+    desc = nbt.map_desc(cfg.n, cfg.n, cfg.n, cfg.voxel_size)
+    m = nbt.Map(ctx, desc)
+    codes = cfg.map_codes() if rank == 0 else None
+    if rank == 0:
+        m.upload(codes)
+    if world > 1:
+        ndist.replicate_map(m, src=0)
+    ctx.sync()
+
+    # ---- per-cycle inputs, resident in HBM before timing
+    host_deltas = []
+    base = codes if codes is not None else np.zeros((cfg.n,) * 3, np.uint8)
+    for c in range(N_DELTA_SETS):
+        host_deltas.append(cycle_deltas(cfg.n, (cfg.n // 2,) * 3, c, base, seed=1))
+    nd = max(len(v) for _, v in host_deltas)
+    pad = []
+    for ijk, vals in host_deltas:      # equal length per cycle (re-applying the last delta is a no-op)
+        k = nd - len(vals)
+        pad.append((np.concatenate([ijk, np.repeat(ijk[-1:], k, 0)]), np.concatenate([vals, np.repeat(vals[-1:], k)])))
+    host_deltas = pad
+    d_ijk = [torch.from_numpy(a).to(dev) for a, _ in host_deltas]
+    d_val = [torch.from_numpy(v).to(dev) for _, v in host_deltas]
+    q_host = query_points(N_QUERIES, cfg.poi, cfg.persp_radius, 0.5, 1.2, seed=5)
+    q_dev = torch.from_numpy(q_host).to(dev)
+    q_out = torch.empty(N_QUERIES, dtype=torch.float64, device=dev)
+    n_p = cfg.n_persp
+    n_tot = n_p * world
+    persp = torch.empty((n_p, 3), dtype=torch.float64, device=dev)
+    cloud = nbt.empty_cloud(n_p, device=dev)
+    buf = nbt.IdBuffer(ctx, N_B, n_tot)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    ne = cam.num_rays
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    acc = torch.zeros(4, dtype=torch.int64, device=dev)
+
+    def step(t):
+        ijk, val = d_ijk[t % N_DELTA_SETS], d_val[t % N_DELTA_SETS]
+        if world > 1:
+            ndist.broadcast_deltas(ijk, val, src=0)
+        m.update(ijk, val)                                                       # a2
+        nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_p, 1000003 * t + rank, cfg.persp_mode,
+                                out=persp)                                       # a3
+        nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=cloud)       # a4-a8
+        if world > 1:
+            xyz = ndist.all_gather_rows(cloud.xyz, n_tot, world, strided=False)
+            gain = ndist.all_gather_rows(cloud.gain, n_tot, world, strided=False)
+            full = nbt.IgCloud(xyz, gain, None)
+        else:
+            full = cloud
+        buf.push(full, n_tot)                                                    # a9
+        buf.query(q_dev, power_p=POWER_P, out=q_out)
+
+    for t in range(args.warmup):
+        step(t)
+    ctx.sync()
+
+    # ---- timed region: K steps, device time per step with CUDA events on the ctx stream
+    gpu_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid).replace("GPU-", "")
+    clocks = ClockSampler(gpu_id)
+    time.sleep(0.25)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ctx.set_profiling(True)
+    for k in range(nbt.KERNEL_MAP_UPDATE + 1):
+        ctx.profile_read(k, reset=True)
+    launches0 = ctx.launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.time()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)                      # evict the map and inputs from L2 (outside the events)
+        ev0[i].record(stream)
+        step(args.warmup + i)
+        ev1[i].record(stream)
+        acc += cloud.counts.sum(0)                 # work accounting, outside the events
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_wall1 = time.time()
+    launches = ctx.launches - launches0
+    dev_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+    prof = {k: ctx.profile_read(k, reset=True) for k in range(nbt.KERNEL_MAP_UPDATE + 1)}
+    ctx.set_profiling(False)
+    clocks.stop()
+    clk = clocks.summary(t_wall0, t_wall1)
+    counts = acc.cpu().numpy()
+    visits, lookups = float(counts[:3].sum()), float(counts[3])
+
+    # ---- end to end through the public API with HOST buffers (H2D inputs, D2H results)
+    e2e = None
+    if not args.no_e2e:
+        e2e_persp = [nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_p, 77 + 1000003 * s + rank,
+                                             cfg.persp_mode) for s in range(min(args.steps, 16))]
+        q_res = np.empty(N_QUERIES)
+        loc = nbt.empty_cloud(n_p, device=dev, counts=False)
+
+        def e2e_step(s):
+            ijk, vals = host_deltas[s % N_DELTA_SETS]
+            if world > 1:
+                ti, tv = torch.from_numpy(ijk).to(dev), torch.from_numpy(vals).to(dev)
+                ndist.broadcast_deltas(ti, tv, src=0)
+                m.update(ti, tv)
+            else:
+                m.update(ijk, vals)                                              # H2D deltas
+            nbt.id_compute(ctx, m, cfg.poi, e2e_persp[s % len(e2e_persp)], cam, cfg.range_, out=loc)  # H2D persp
+            if world > 1:
+                full = nbt.IgCloud(ndist.all_gather_rows(loc.xyz, n_tot, world, strided=False),
+                                   ndist.all_gather_rows(loc.gain, n_tot, world, strided=False), None)
+            else:
+                full = loc
+            buf.push(full, n_tot)
+            buf.query(q_host, power_p=POWER_P, out=q_res)                        # H2D queries, D2H values
+            return full.gain.cpu().numpy(), full.xyz.cpu().numpy()               # D2H the IG cloud
+
+        for s in range(2):
+            e2e_step(s)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for s in range(args.steps):
+            e2e_step(s)
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        h2d = nd * 13 + n_p * 24 + N_QUERIES * 24
+        d2h = N_QUERIES * 8 + n_tot * 32
+        e2e = {"value": args.steps * n_tot * ne / t_e2e, "unit": "rays/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e / args.steps}
+
+    # ---- max over ranks
+    t_dev = dev_ms
+    if world > 1:
+        tt = torch.tensor([dev_ms, visits, lookups], dtype=torch.float64, device=dev)
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        t_dev = float(mx[0].item())
+        visits, lookups = float(tt[1].item()), float(tt[2].item())
+        clk_all = [None] * world
+        dist.all_gather_object(clk_all, clk)
+    else:
+        clk_all = [clk]
+
+    if rank == 0:
+        rays_total = args.steps * n_tot * ne
+        sec = t_dev / 1e3
+        tr_ms, tr_n = prof[nbt.KERNEL_TRACE]
+        tr_avg = tr_ms / max(tr_n, 1)
+        f_max = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_tops = sms * INT_LANES_PER_SM_CLK * f_max / 1e12
+        lookups_rank0 = float(counts[3])
+        achieved = lookups_rank0 * OPS_PER_LOOKUP / (tr_ms / 1e3) / 1e12 if tr_ms > 0 else None
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
+        if os.path.exists(tfile):
+            with open(tfile) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        reasons = sorted({r for c in clk_all if c for r in c["reasons"]})
+        clocks_out = dict(clk_all[0]) if clk_all[0] else None
+        if clocks_out:
+            clocks_out["reasons"] = reasons
+        shares = {name: round(prof[k][0] / max(dev_ms, 1e-9), 4) for k, name in
+                  [(nbt.KERNEL_TRACE, "k_id_trace"), (nbt.KERNEL_FRAMES, "k_persp_frames"),
+                   (nbt.KERNEL_FINALIZE, "k_id_finalize"), (nbt.KERNEL_IDW, "k_idw_query"),
+                   (nbt.KERNEL_SAMPLE, "k_sample_perspectives"), (nbt.KERNEL_MAP_UPDATE, "map_update")]}
+        line = {
+            "metric": "rays/s", "value": rays_total / sec, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_dev / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg, world), "map": f"{cfg.n}^3 SYN(R_o={cfg.r_o:g}, seed "
+                       f"{cfg.map_seed}) 2-bit packed", "perspectives_per_step": n_tot, "rays_per_perspective": ne,
+                       "l2": "flushed before every timed step (256 MiB write, outside the step events)",
+                       "parallelism": f"perspectives sharded over {world} GPU(s), weak scaling"},
+            "voxel_steps_per_s": visits / sec, "lookups_per_s": lookups / sec,
+            "id_latency_ms": t_dev / args.steps,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32)",
+                         "frac": (achieved / peak_tops) if achieved else None, "traffic": traffic,
+                         "kernel": "k_id_trace", "kernel_avg_ms": tr_avg, "kernel_launches": tr_n,
+                         "work": f"{OPS_PER_LOOKUP} int32 ops x in-grid voxel steps (DESIGN.md section 6)",
+                         "peak_basis": f"{sms} SMs x {INT_LANES_PER_SM_CLK} int32 lanes/clk x "
+                                       f"{f_max / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)"},
+            "kernel_share_of_step": shares,
+            "gpu_launches": launches,
+            "clocks": clocks_out,
+            "e2e": e2e,
+            "cpu_baseline": None,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = run_cpu_baseline(cfg, codes, args.cpu_budget_s)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return reference_arm(args, cfg)
+    return main_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

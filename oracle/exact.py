@@ -14,7 +14,7 @@ from __future__ import annotations
 from fractions import Fraction as Fr
 from math import floor
 
-Q = 65536
+Q = 4096   # the walk's fixed point: Q12 (reading Q19)
 
 
 def _axis_interval(o, d, lo, hi, closed_cube):
@@ -44,9 +44,9 @@ def _meets(o, d, v, closed_cube):
     return a < b or (a == b and a_c and b_c)
 
 
-def segment(o_q16, e_q16):
-    o = [Fr(int(x), Q) for x in o_q16]
-    e = [Fr(int(x), Q) for x in e_q16]
+def segment(o_q, e_q):
+    o = [Fr(int(x), Q) for x in o_q]
+    e = [Fr(int(x), Q) for x in e_q]
     return o, [e[k] - o[k] for k in range(3)]
 
 
@@ -59,15 +59,15 @@ def candidate_voxels(o, d):
                 yield (x, y, z)
 
 
-def floor_set(o_q16, e_q16):
+def floor_set(o_q, e_q):
     """{floor(P(t)) : t in [0,1]} -- voxels containing a point of the closed segment."""
-    o, d = segment(o_q16, e_q16)
+    o, d = segment(o_q, e_q)
     return {v for v in candidate_voxels(o, d) if _meets(o, d, v, closed_cube=False)}
 
 
-def touch_set(o_q16, e_q16):
+def touch_set(o_q, e_q):
     """Voxels whose CLOSED cube meets the closed segment."""
-    o, d = segment(o_q16, e_q16)
+    o, d = segment(o_q, e_q)
     return {v for v in candidate_voxels(o, d) if _meets(o, d, v, closed_cube=True)}
 
 
@@ -94,9 +94,9 @@ def _crossings(o, d):
     return out
 
 
-def same_sign_ties(o_q16, e_q16):
+def same_sign_ties(o_q, e_q):
     """Exact parameters where two axes moving the same way cross at the same t."""
-    o, d = segment(o_q16, e_q16)
+    o, d = segment(o_q, e_q)
     cr = _crossings(o, d)
     ties = []
     for a in range(3):
@@ -107,9 +107,9 @@ def same_sign_ties(o_q16, e_q16):
     return ties
 
 
-def enter_param(o_q16, e_q16, v):
+def enter_param(o_q, e_q, v):
     """Smallest t at which P(t) lies in the half-open voxel v (None if never)."""
-    o, d = segment(o_q16, e_q16)
+    o, d = segment(o_q, e_q)
     a, a_c, b, b_c = Fr(0), True, Fr(1), True
     for k in range(3):
         iv = _axis_interval(o[k], d[k], Fr(v[k]), Fr(v[k] + 1), False)

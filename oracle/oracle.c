@@ -40,8 +40,9 @@
 #define ORC_ERR_EMPTY 3
 #define ORC_ERR_SELFCHECK 9
 
-#define Q 65536            /* Q16: one voxel = 65536 units (Q19) */
-#define QLIM 1073741824LL  /* |coordinate| must stay below 2^30 (Q19) */
+#define QF 65536           /* frames and lattice: Q16, one voxel = 65536 units (Q19) */
+#define QD 4096            /* ray endpoints for the walk: Q12, one voxel = 4096 units (Q19) */
+#define QLIM 1073741824LL  /* |coordinate| must stay below 2^30 in its unit (Q19) */
 
 /* ------------------------------------------------------------------ map (O-1) */
 
@@ -216,10 +217,13 @@ typedef struct {
     int32_t stop;            /* 0 = reached the endpoint voxel, 1 = stopped on Occupied */
 } orc_ray;
 
-static int64_t floor_div_q(int64_t a) { return (a >= 0) ? a / Q : -((-a + Q - 1) / Q); }
+static int64_t floor_div(int64_t a, int64_t b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+
+/* Q16 -> Q12: round to the nearest 1/4096 voxel, halves upward (Q19). */
+static int32_t q16_to_q12(int32_t v) { return (int32_t)floor_div((int64_t)v + 8, 16); }
 
 /*
- * Walk the voxels of the segment O -> E (Q16 voxel coordinates).
+ * Walk the voxels of the segment O -> E (Q12 voxel coordinates: 4096 units per voxel).
  *
  * Definition followed: the point P(t) = O + t (E - O), t in [0,1], lies in voxel
  * floor(P(t)) (half-open voxels, O-1).  Moving in +a the index changes AT the
@@ -244,12 +248,12 @@ int orc_trace_ray(const orc_map *m, const int32_t o[3], const int32_t e[3], int3
     int64_t nsteps = 0;
     for (int a = 0; a < 3; ++a) {
         if (o[a] <= -QLIM || o[a] >= QLIM || e[a] <= -QLIM || e[a] >= QLIM) return ORC_ERR_INVALID_ARG;
-        v[a] = floor_div_q(o[a]);
-        ve[a] = floor_div_q(e[a]);
+        v[a] = floor_div(o[a], QD);
+        ve[a] = floor_div(e[a], QD);
         D[a] = (int64_t)e[a] - o[a];
         neg[a] = D[a] < 0;
         /* distance (in Q16 units) from O to the next boundary crossed along a */
-        N[a] = neg[a] ? (int64_t)o[a] - v[a] * Q : (v[a] + 1) * Q - o[a];
+        N[a] = neg[a] ? (int64_t)o[a] - v[a] * QD : (v[a] + 1) * QD - o[a];
         nsteps += llabs(ve[a] - v[a]);
     }
     memset(r, 0, sizeof *r);
@@ -286,9 +290,23 @@ int orc_trace_ray(const orc_map *m, const int32_t o[3], const int32_t e[3], int3
             if (lhs < rhs || (lhs == rhs && neg[a] < neg[best])) best = a;
         }
         v[best] += neg[best] ? -1 : 1;
-        N[best] += Q;
+        N[best] += QD;
     }
     if (len_out) *len_out = len;
+    return ORC_OK;
+}
+
+/* The segment the walk follows for ray k: both ends rounded from the Q16 lattice to
+ * Q12 (Q19). */
+static int ray_segment_q12(const orc_frame *f, const orc_camera *cam, int32_t k, int32_t o12[3], int32_t e12[3])
+{
+    int32_t e16[3];
+    int st = ray_endpoint(f, cam, k, e16);
+    if (st) return st;
+    for (int c = 0; c < 3; ++c) {
+        o12[c] = q16_to_q12(f->o[c]);
+        e12[c] = q16_to_q12(e16[c]);
+    }
     return ORC_OK;
 }
 
@@ -315,10 +333,10 @@ static int one_perspective(const orc_map *m, const double poi[3], const double p
     int64_t tu = 0, tf = 0, to = 0, tl = 0;
     double direct = 0.0;
     for (int32_t k = 0; k < ne; ++k) {
-        int32_t e[3];
-        if ((st = ray_endpoint(&f, cam, k, e))) return st;
+        int32_t o[3], e[3];
+        if ((st = ray_segment_q12(&f, cam, k, o, e))) return st;
         orc_ray r;
-        if ((st = orc_trace_ray(m, f.o, e, 0, NULL, NULL, NULL, &r))) return st;
+        if ((st = orc_trace_ray(m, o, e, 0, NULL, NULL, NULL, &r))) return st;
         direct += r.g;
         tu += r.n_u; tf += r.n_f; to += r.n_o; tl += r.lookups;
     }
@@ -373,7 +391,8 @@ int orc_id_compute(const orc_map *m, const double poi[3], const double *persp, i
     return status;
 }
 
-/* Rays of one perspective, for per-ray parity: endpoints (Q16) and counts. */
+/* Rays of one perspective, for per-ray parity: the Q12 segment ends (the origin is
+ * common to all rays) and per-ray counts. */
 int orc_perspective_rays(const orc_map *m, const double poi[3], const double p[3],
                          const orc_camera *cam, double range, int32_t *o_out, int32_t *e_out,
                          int64_t *ray_counts_out /* ne x 5: U,F,O,lookups,stop */)
@@ -382,14 +401,14 @@ int orc_perspective_rays(const orc_map *m, const double poi[3], const double p[3
     int st = orc_frame_q16(m, poi, p, cam, range, &f, NULL, NULL, NULL);
     if (st) return st;
     int32_t ne = orc_camera_num_rays(cam);
-    if (o_out) memcpy(o_out, f.o, sizeof f.o);
     for (int32_t k = 0; k < ne; ++k) {
-        int32_t e[3];
-        if ((st = ray_endpoint(&f, cam, k, e))) return st;
+        int32_t o[3], e[3];
+        if ((st = ray_segment_q12(&f, cam, k, o, e))) return st;
+        if (o_out && k == 0) memcpy(o_out, o, sizeof o);
         if (e_out) memcpy(e_out + 3 * (int64_t)k, e, sizeof e);
         if (ray_counts_out) {
             orc_ray r;
-            if ((st = orc_trace_ray(m, f.o, e, 0, NULL, NULL, NULL, &r))) return st;
+            if ((st = orc_trace_ray(m, o, e, 0, NULL, NULL, NULL, &r))) return st;
             int64_t *rc = ray_counts_out + 5 * (int64_t)k;
             rc[0] = r.n_u; rc[1] = r.n_f; rc[2] = r.n_o; rc[3] = r.lookups; rc[4] = r.stop;
         }

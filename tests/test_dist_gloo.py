@@ -1,0 +1,94 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the multi-GPU orchestration logic in
+paper_2503_22588_b200/dist.py: strided perspective sharding, padding, the all-gather +
+un-stride that assembles the IG cloud in input order, weak-scaling concatenation, and
+the map / delta broadcasts.  The per-shard compute here is the CPU oracle (test-only);
+on the B200 box the same functions move libnbt's device results over NCCL."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2503_22588_b200 import dist as ndist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle
+        from nbt_inputs import CONFIGS, FOV_H, FOV_V
+        cfg = CONFIGS["A"]
+        codes = cfg.map_codes()
+        om = oracle.OracleMap(codes, voxel_size=cfg.voxel_size)
+        cam = oracle.camera_from_fov(FOV_H, FOV_V, 16, 12)
+        n = 13                                          # not a multiple of world: padding path
+        P = oracle.sample_perspectives(cfg.poi, 20.0, n, seed=4)
+        # strided shard j -> rank j mod world
+        k = ndist.shard_count(n, rank, world)
+        mine = P[rank::world]
+        assert len(mine) == k
+        _, g, c = oracle.id_compute(om, cfg.poi, mine, cam, cfg.range_)
+        xyz = ndist.all_gather_rows(torch.from_numpy(mine), n, world)
+        gain = ndist.all_gather_rows(torch.from_numpy(g), n, world)
+        cnt = ndist.all_gather_rows(torch.from_numpy(c), n, world)
+        _, g_full, c_full = oracle.id_compute(om, cfg.poi, P, cam, cfg.range_)
+        ok = (np.array_equal(xyz.numpy(), P) and np.array_equal(gain.numpy(), g_full)
+              and np.array_equal(cnt.numpy(), c_full))
+        # weak scaling: every rank its own block, concatenated in rank order
+        blk = torch.full((3, 2), float(rank))
+        cat = ndist.all_gather_rows(blk, 3 * world, world, strided=False)
+        ok &= bool((cat[:3] == 0).all() and (cat[3:] == 1).all())
+        # map + delta broadcasts from rank 0
+        packed = torch.arange(1000, dtype=torch.uint8) if rank == 0 else torch.zeros(1000, dtype=torch.uint8)
+        dist.broadcast(packed, src=0)
+        ok &= bool((packed == torch.arange(1000, dtype=torch.uint8)).all())
+        ijk = torch.tensor([[1, 2, 3]], dtype=torch.int32) if rank == 0 else torch.zeros((1, 3), dtype=torch.int32)
+        val = torch.tensor([2], dtype=torch.uint8) if rank == 0 else torch.zeros(1, dtype=torch.uint8)
+        ndist.broadcast_deltas(ijk, val, src=0)
+        ok &= bool(ijk.tolist() == [[1, 2, 3]] and val.tolist() == [2])
+        q.put((rank, bool(ok), ""))
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+
+
+def test_sharded_id_world2_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, tb in res:
+        assert ok, f"rank {rank}: {tb}"
+
+
+@pytest.mark.parametrize("n,world", [(13, 2), (16, 4), (3, 8), (4096, 8), (1, 1)])
+def test_unstride_roundtrip(n, world):
+    full = np.arange(n * 2).reshape(n, 2)
+    R = ndist.rows_per_rank(n, world)
+    g = np.full((world, R, 2), -1)
+    for r in range(world):
+        rows = full[r::world]
+        assert len(rows) == ndist.shard_count(n, r, world)
+        g[r, :len(rows)] = rows
+    assert np.array_equal(ndist.unstride(g, n, world), full)
+    assert np.array_equal(ndist.unstride(torch.from_numpy(g), n, world).numpy(), full)

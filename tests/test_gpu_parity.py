@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
-from nbt_inputs import CONFIGS, FOV_H, FOV_V, rand_map, random_segments_q16, tie_segments_q16, syn_map
+from nbt_inputs import CONFIGS, FOV_H, FOV_V, rand_map, random_segments_q12, tie_segments_q12, syn_map
 
 pytestmark = pytest.mark.gpu
 
@@ -152,7 +152,7 @@ def test_walks_random_segments(nbt, ctx, policy):
     """Every visited voxel of 3000 random rays, inside, leaving and outside the grid."""
     codes = rand_map(12, 0.3, 0.68, 0.02, seed=7)
     m, om = make_map(nbt, ctx, codes, policy=policy)
-    o, e = random_segments_q16(3000, -5.0, 17.0, seed=policy + 1)
+    o, e = random_segments_q12(3000, -5.0, 17.0, seed=policy + 1)
     _compare_walks(nbt, ctx, m, om, o, e)
 
 
@@ -160,8 +160,8 @@ def test_walks_ties(nbt, ctx):
     """Endpoints on faces, edges and corners (exact ties of the DDA)."""
     codes = rand_map(8, 0.4, 0.6, 0.0, seed=2)
     m, om = make_map(nbt, ctx, codes)
-    o, e = tie_segments_q16(4000, 9, seed=4)
-    o -= 65536
+    o, e = tie_segments_q12(4000, 9, seed=4)
+    o -= 4096
     _compare_walks(nbt, ctx, m, om, o, e)
 
 
@@ -170,8 +170,8 @@ def test_walks_hand_traced(nbt, ctx):
     m, om = make_map(nbt, ctx, np.ones((4, 4, 4), np.uint8))
     for row in read_golden("dda_hand_traced.txt"):
         _, o, e, seq = [s.strip() for s in row.split("|")]
-        o = [int(round(float(v) * 65536)) for v in o.split()]
-        e = [int(round(float(v) * 65536)) for v in e.split()]
+        o = [int(round(float(v) * 4096)) for v in o.split()]
+        e = [int(round(float(v) * 4096)) for v in e.split()]
         want = [tuple(int(t) for t in v.split()) for v in seq.split(";")]
         ijk, _, ln, _ = nbt.debug_trace(ctx, m, [o], [e], 16)
         assert [tuple(v) for v in ijk[0, :ln[0]]] == want
@@ -181,7 +181,7 @@ def test_walks_long_rays(nbt, ctx):
     """Long walks (1000+ voxels) through a sparse map: no drift of the decision terms."""
     codes = rand_map(64, 0.5, 0.5, 0.0, seed=9)
     m, om = make_map(nbt, ctx, codes)
-    o, e = random_segments_q16(200, -30.0, 94.0, seed=12)
+    o, e = random_segments_q12(200, -30.0, 94.0, seed=12)
     _compare_walks(nbt, ctx, m, om, o, e, max_visits=400)
 
 
