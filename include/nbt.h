@@ -103,7 +103,7 @@ enum { NBT_OUTSIDE_UNKNOWN = 0, NBT_OUTSIDE_CLIP = 1 };        /* Q14 */
 typedef struct nbt_map_s *nbt_map;
 
 typedef struct {
-    int32_t nx, ny, nz;       /* voxels per axis, each >= 1; (nx+2)(ny+2)(nz+2) < 2^32 */
+    int32_t nx, ny, nz;       /* voxels per axis, each >= 1; (nx+16)(ny+16)(nz+16) < 2^32 */
     double  voxel_size;       /* s_Vox > 0 (1 cm) */
     double  origin[3];        /* world position of voxel (0,0,0)'s min corner */
     double  gain[3];          /* g[U], g[F], g[O] of Eq. 2 as per-state constants (Q15);
@@ -213,12 +213,13 @@ void       nbt_idbuf_destroy(nbt_idbuf buf);
 
 /* ----------------------------------------------------------- test hooks */
 
-/* Per-ray walk of explicit Q16 segments (host arrays, n_rays x 3 int32 each): the first
+/* Per-ray walk of explicit segments in Q12 voxel coordinates (4096 units per voxel,
+ * reading Q19; host arrays, n_rays x 3 int32 each, inside (-2^30, 2^30)): the first
  * max_visits visited voxels of ray r go to ijk_out[r*max_visits*3 ...], their codes
  * (0/1/2; 255 = outside the grid) to code_out[r*max_visits ...]; len_out[r] = number of
  * visited voxels (may exceed max_visits); counts_out[r*4 ...] = n_U, n_F, n_O, lookups.
  * Uses the same device traversal as nbt_id_compute.  Synchronizes. */
-nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map map, const int32_t *o_q16, const int32_t *e_q16,
+nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map map, const int32_t *o_q12, const int32_t *e_q12,
                            int32_t n_rays, int32_t max_visits, int32_t *ijk_out, uint8_t *code_out,
                            int32_t *len_out, uint32_t *counts_out);
 /* The device frames of n perspectives (host in/out): 18 int32 per perspective

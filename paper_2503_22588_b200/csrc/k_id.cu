@@ -2,29 +2,42 @@
 //
 //   k_persp_frames  per perspective: view frame (Q4) and its Q16 quantisation
 //                   (Q19), bound checks; zeroes the per-perspective totals.
-//   k_id_trace      persistent warps pull chunks of one perspective's rays; each lane
-//                   builds its ray's endpoint on the far plane in registers (P:158-169,
-//                   Q27), walks the exact integer 3D-DDA (Q13) through the 2-bit map,
-//                   stops at the first Occupied voxel, and counts visits per
-//                   state (Eq. 2 as integer counts, Q26).  Lanes that finish refill
-//                   with their next ray, so the warp keeps stepping until the whole
-//                   chunk is done.  One warp reduction + 4 u64 atomics per chunk.
+//   k_id_trace      persistent warps with per-lane refill: every lane owns one ray at a
+//                   time; when it finishes, the warp hands it the next ray of the
+//                   current chunk (a run of one perspective's rays in 8x4 pixel tiles).
+//                   The lane builds its endpoint on the far plane in registers
+//                   (Q27), rounds both ends to Q12, and walks the exact
+//                   integer 3D-DDA (Q13) through the 2-bit map in batches of kBatch
+//                   voxels: the DDA does not depend on the map, so a batch computes
+//                   kBatch voxel indices, issues kBatch independent loads, packs the
+//                   2-bit codes into one word and finds the first Occupied / outside
+//                   voxel with one ffs (early stop) and the Free count with one
+//                   popc.  Per-state visit counts (Eq. 2 as integers, Q26) accumulate
+//                   in registers and are flushed with 4 u64 atomics when a lane moves
+//                   to another perspective.
 //   k_id_finalize   g_P = ((T_U g_U + T_F g_F) + T_O g_O) / N_E  (Q26)
 //
-// The traversal is integer-only: voxel coordinates are Q16 fixed point (65536 per
-// voxel).  The next boundary crossed is the axis minimising N_a/|D_a| (N_a = distance
-// to its next boundary, D = E - O), compared exactly through the pairwise terms
-// f_ab = N_a|D_b| - N_b|D_a| (int64) kept incrementally: a step along a adds
-// 65536|D_b| to f_ab.  Exact ties are broken by (positive direction first, then axis
-// order) through a -1 bias folded into f_ab at ray start, so each step is three sign
-// tests and two 64-bit adds.
+// Exact decision with 32-bit arithmetic.  With D = E - O and
+// N_a the distance from O to the next boundary along a (Q12 units, S = 4096), the next
+// boundary crossed is the axis minimising N_a/|D_a|, ties broken by (positive direction
+// first, then x<y<z).  The pairwise terms e_ab = N_a|D_b| - N_b|D_a|, minus a 0/1 tie
+// bias, decide "a before b" by their sign.  Every later change of e_ab is a multiple
+// of S (a step along a adds S|D_b|), so with e_ab - bias = S q_ab + r (0 <= r < S) the
+// sign of q_ab equals the sign of e_ab - bias and q_ab changes by |D_b| (or -|D_a|).
+// q_ab is computed once per ray in 64-bit and then kept in int32, which is exact for
+// rays up to 720 voxels per axis; longer rays use the same code with 64-bit q (the
+// host picks the variant from the camera geometry).
 #include "nbt_internal.cuh"
 
 namespace nbt {
 namespace {
 
-constexpr int kFrameInts = 20;   // O, A, Rh, Uh, Rc, Uc (3 each), status, pad
+constexpr int kFrameInts = 20;   // O, A, Rh, Uh, Rc, Uc (3 each, Q16), status, pad
 constexpr int kWarpsPerBlock = 8;
+constexpr int kQShift = 12;      // walk coordinates: Q12
+constexpr int kBatch = 8;        // voxels per speculative batch (<= kBorder)
+static_assert(kBatch <= kBorder, "look-ahead must stay inside the sentinel shell");
+constexpr int kInt32MaxVoxels = 700;   // |D_a| bound (voxels) for the int32 decision terms
 
 struct MapView {
     const uint32_t *__restrict__ words;
@@ -34,73 +47,82 @@ struct MapView {
     int policy;      // NBT_OUTSIDE_UNKNOWN / NBT_OUTSIDE_CLIP
 };
 
-__device__ __forceinline__ uint32_t code_at(const MapView &m, uint32_t idx)
+__device__ __forceinline__ uint32_t padded_index(const MapView &m, int x, int y, int z)
 {
-    uint32_t w = __ldg(m.words + (idx >> 4));
-    return __funnelshift_r(w, 0u, idx << 1) & 3u;   // shift amount is taken mod 32
+    return (uint32_t)(x + kBorder) + (uint32_t)m.px * (uint32_t)(y + kBorder) +
+           (uint32_t)m.pxy * (uint32_t)(z + kBorder);
 }
 
-// Per-ray traversal state (all integer).
-struct Ray {
-    long long fxy, fxz, fyz;   // biased pairwise decision terms (negative -> first axis first)
-    long long kx, ky, kz;      // 65536 * |D_a|
-    uint32_t idx;              // padded linear voxel index (fast path)
+__device__ __forceinline__ uint32_t code_of(uint32_t word, uint32_t idx)
+{
+    return __funnelshift_r(word, 0u, idx << 1) & 3u;   // shift amount taken mod 32
+}
+
+// Per-ray walk state.  T = int (rays <= 720 voxels per axis) or long long.
+template <typename T>
+struct Walk {
+    T qxy, qxz, qyz;           // sign decides the next axis (see header)
+    T ax, ay, az;              // |D_a| in Q12 units
+    uint32_t idx;              // padded linear index of the current voxel (in-grid walk)
     int dX, dY, dZ;            // idx increments of a step along x, y, z
-    int s, n;                  // current step (0 = origin voxel), total steps
+    int s, n;                  // current step (0 = origin voxel) and total steps
     int s0;                    // step at which the walk entered the grid
-    uint32_t nf;               // Free voxels seen in the grid
+    uint32_t nf;               // Free voxels counted so far in the grid
     uint32_t pre;              // visits outside the grid before entering it
-    int vx, vy, vz;            // voxel coordinates (slow path / debug only)
+    int vx, vy, vz;            // voxel coordinates (entry path / debug only)
     int sx, sy, sz;            // +-1 per axis
 };
 
-__device__ __forceinline__ void ray_setup(Ray &r, const int o[3], const int e[3])
+template <typename T>
+__device__ __forceinline__ void walk_setup(Walk<T> &w, const int o[3], const int e[3])
 {
-    int D[3], ad[3], neg[3], v[3], N[3];
+    long long ad[3], N[3];
+    int neg[3], v[3];
     int n = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        D[a] = e[a] - o[a];                      // |D| < 2^31: both ends inside (-2^30, 2^30)
-        neg[a] = D[a] < 0;
-        ad[a] = neg[a] ? -D[a] : D[a];
-        v[a] = o[a] >> 16;                       // floor
-        int ve = e[a] >> 16;
+        int D = e[a] - o[a];                     // |D| < 2^31: both ends inside (-2^30, 2^30)
+        neg[a] = D < 0;
+        ad[a] = neg[a] ? -(long long)D : (long long)D;
+        v[a] = o[a] >> kQShift;                  // floor
+        int ve = e[a] >> kQShift;
         n += (ve > v[a]) ? ve - v[a] : v[a] - ve;
-        N[a] = neg[a] ? o[a] - v[a] * 65536 : (v[a] + 1) * 65536 - o[a];   // in [0, 65536]
+        N[a] = neg[a] ? (long long)o[a] - ((long long)v[a] << kQShift)
+                      : (((long long)v[a] + 1) << kQShift) - o[a];          // in [0, 4096]
     }
     // tie favours the lower axis unless it moves negatively and the other positively
-    long long exy = (long long)N[0] * ad[1] - (long long)N[1] * ad[0];
-    long long exz = (long long)N[0] * ad[2] - (long long)N[2] * ad[0];
-    long long eyz = (long long)N[1] * ad[2] - (long long)N[2] * ad[1];
-    r.fxy = exy - ((neg[0] && !neg[1]) ? 0 : 1);
-    r.fxz = exz - ((neg[0] && !neg[2]) ? 0 : 1);
-    r.fyz = eyz - ((neg[1] && !neg[2]) ? 0 : 1);
-    r.kx = (long long)ad[0] << 16;
-    r.ky = (long long)ad[1] << 16;
-    r.kz = (long long)ad[2] << 16;
-    r.sx = neg[0] ? -1 : 1;
-    r.sy = neg[1] ? -1 : 1;
-    r.sz = neg[2] ? -1 : 1;
-    r.vx = v[0]; r.vy = v[1]; r.vz = v[2];
-    r.s = 0;
-    r.n = n;
-    r.nf = 0;
-    r.pre = 0;
+    long long fxy = N[0] * ad[1] - N[1] * ad[0] - ((neg[0] && !neg[1]) ? 0 : 1);
+    long long fxz = N[0] * ad[2] - N[2] * ad[0] - ((neg[0] && !neg[2]) ? 0 : 1);
+    long long fyz = N[1] * ad[2] - N[2] * ad[1] - ((neg[1] && !neg[2]) ? 0 : 1);
+    w.qxy = (T)(fxy >> kQShift);                 // arithmetic shift = floor division by S
+    w.qxz = (T)(fxz >> kQShift);
+    w.qyz = (T)(fyz >> kQShift);
+    w.ax = (T)ad[0]; w.ay = (T)ad[1]; w.az = (T)ad[2];
+    w.sx = neg[0] ? -1 : 1;
+    w.sy = neg[1] ? -1 : 1;
+    w.sz = neg[2] ? -1 : 1;
+    w.vx = v[0]; w.vy = v[1]; w.vz = v[2];
+    w.s = 0;
+    w.n = n;
+    w.nf = 0;
+    w.pre = 0;
 }
 
-// Choose the next axis (0/1/2) and update the decision terms.
-__device__ __forceinline__ int ray_advance(Ray &r)
+// One DDA step: pick the axis, update the two decision terms that involve it.
+template <typename T, bool COORDS>
+__device__ __forceinline__ void walk_step(Walk<T> &w)
 {
-    if (r.fxy < 0 && r.fxz < 0) {
-        r.fxy += r.ky; r.fxz += r.kz;
-        return 0;
+    const bool px = (w.qxy & w.qxz) < 0;         // both negative
+    const bool py = !px && w.qyz < 0;
+    const bool pz = !px && !py;
+    if (px) { w.qxy += w.ay; w.qxz += w.az; w.idx += w.dX; }
+    if (py) { w.qxy -= w.ax; w.qyz += w.az; w.idx += w.dY; }
+    if (pz) { w.qxz -= w.ax; w.qyz -= w.ay; w.idx += w.dZ; }
+    if (COORDS) {
+        if (px) w.vx += w.sx;
+        if (py) w.vy += w.sy;
+        if (pz) w.vz += w.sz;
     }
-    if (r.fyz < 0) {
-        r.fxy -= r.kx; r.fyz += r.kz;
-        return 1;
-    }
-    r.fxz -= r.kx; r.fyz -= r.ky;
-    return 2;
 }
 
 __device__ __forceinline__ bool inside(const MapView &m, int x, int y, int z)
@@ -110,80 +132,90 @@ __device__ __forceinline__ bool inside(const MapView &m, int x, int y, int z)
 
 // Origin outside the grid (rare): step with explicit bounds checks until the walk
 // enters the grid or ends.  Returns true if the ray is finished.
-template <bool RECORD>
-__device__ bool ray_enter(Ray &r, const MapView &m, int32_t *rec_ijk, uint8_t *rec_code, int max_visits)
+template <typename T, bool RECORD>
+__device__ bool walk_enter(Walk<T> &w, const MapView &m, int32_t *rec_ijk, uint8_t *rec_code, int max_visits)
 {
-    while (!inside(m, r.vx, r.vy, r.vz)) {
-        if (RECORD && r.s < max_visits) {
-            rec_ijk[3 * r.s] = r.vx; rec_ijk[3 * r.s + 1] = r.vy; rec_ijk[3 * r.s + 2] = r.vz;
-            rec_code[r.s] = 255;
+    while (!inside(m, w.vx, w.vy, w.vz)) {
+        if (RECORD && w.s < max_visits) {
+            rec_ijk[3 * w.s] = w.vx; rec_ijk[3 * w.s + 1] = w.vy; rec_ijk[3 * w.s + 2] = w.vz;
+            rec_code[w.s] = 255;
         }
-        r.pre++;
-        if (r.s == r.n) return true;
-        int a = ray_advance(r);
-        if (a == 0) r.vx += r.sx; else if (a == 1) r.vy += r.sy; else r.vz += r.sz;
-        r.s++;
+        w.pre++;
+        if (w.s == w.n) return true;
+        walk_step<T, true>(w);
+        w.s++;
     }
-    r.s0 = r.s;
-    r.idx = (uint32_t)(r.vx + 1) + (uint32_t)m.px * (uint32_t)(r.vy + 1) + (uint32_t)m.pxy * (uint32_t)(r.vz + 1);
-    r.dX = r.sx;
-    r.dY = r.sy * m.px;
-    r.dZ = r.sz * m.pxy;
+    w.s0 = w.s;
+    w.idx = padded_index(m, w.vx, w.vy, w.vz);
+    w.dX = w.sx;
+    w.dY = w.sy * m.px;
+    w.dZ = w.sz * m.pxy;
     return false;
 }
 
 struct Counts { uint32_t u, f, o, l; };
 
-// Fast in-grid walk.  Ends on the first Occupied voxel, on leaving the grid (sentinel
-// code 3, Q14 tail rule: the remaining n - s + 1 visits are all outside) or at the
-// endpoint voxel.
-template <bool RECORD>
-__device__ void ray_walk(Ray &r, const MapView &m, Counts &c, int32_t *rec_ijk, uint8_t *rec_code, int max_visits)
+// Close a ray that stopped at step s_stop on `code` (2 = Occupied, 3 = left the grid;
+// Q14 tail rule: the remaining n - s + 1 visits are all outside, hence Unknown).
+template <typename T>
+__device__ __forceinline__ void walk_close_stop(const Walk<T> &w, int policy, uint32_t code, int s_stop, uint32_t nf,
+                                                Counts &c)
 {
-    for (;;) {
-        uint32_t code = code_at(m, r.idx);
-        if (RECORD && r.s < max_visits) {
-            rec_ijk[3 * r.s] = r.vx; rec_ijk[3 * r.s + 1] = r.vy; rec_ijk[3 * r.s + 2] = r.vz;
-            rec_code[r.s] = code == 3 ? 255 : (uint8_t)code;
-        }
-        if (code >= 2u) {
-            uint32_t tail = 0;
-            uint32_t l;
-            if (code == 2u) {
-                l = r.s - r.s0 + 1;
-                c.o += 1;
-                c.u += l - r.nf - 1;
-            } else {
-                l = r.s - r.s0;
-                tail = r.n - r.s + 1;
-                c.u += l - r.nf;
-                if (RECORD) {
-                    for (int s = r.s + 1; s <= r.n && s < max_visits; ++s) {
-                        int a = ray_advance(r);
-                        if (a == 0) r.vx += r.sx; else if (a == 1) r.vy += r.sy; else r.vz += r.sz;
-                        rec_ijk[3 * s] = r.vx; rec_ijk[3 * s + 1] = r.vy; rec_ijk[3 * s + 2] = r.vz;
-                        rec_code[s] = 255;
-                    }
-                }
-            }
-            if (m.policy == NBT_OUTSIDE_UNKNOWN) c.u += r.pre + tail;
-            c.f += r.nf;
-            c.l += l;
-            return;
-        }
-        r.nf += code;
-        if (r.s == r.n) {
-            uint32_t l = r.s - r.s0 + 1;
-            c.u += l - r.nf + (m.policy == NBT_OUTSIDE_UNKNOWN ? r.pre : 0);
-            c.f += r.nf;
-            c.l += l;
-            return;
-        }
-        int a = ray_advance(r);
-        r.idx += (a == 0) ? r.dX : ((a == 1) ? r.dY : r.dZ);
-        if (RECORD) { if (a == 0) r.vx += r.sx; else if (a == 1) r.vy += r.sy; else r.vz += r.sz; }
-        r.s++;
+    uint32_t l;
+    uint32_t u_out = (policy == NBT_OUTSIDE_UNKNOWN) ? w.pre : 0u;
+    if (code == 2u) {
+        l = (uint32_t)(s_stop - w.s0 + 1);
+        c.o += 1;
+        c.u += l - nf - 1 + u_out;
+    } else {
+        l = (uint32_t)(s_stop - w.s0);
+        if (policy == NBT_OUTSIDE_UNKNOWN) u_out += (uint32_t)(w.n - s_stop + 1);
+        c.u += l - nf + u_out;
     }
+    c.f += nf;
+    c.l += l;
+}
+
+template <typename T>
+__device__ __forceinline__ void walk_close_end(const Walk<T> &w, int policy, uint32_t nf, Counts &c)
+{
+    uint32_t l = (uint32_t)(w.n - w.s0 + 1);
+    c.u += l - nf + ((policy == NBT_OUTSIDE_UNKNOWN) ? w.pre : 0u);
+    c.f += nf;
+    c.l += l;
+}
+
+// One batch of kBatch visits starting at the current voxel.  Returns true when the ray
+// is finished (counts added to c).
+template <typename T>
+__device__ __forceinline__ bool walk_batch(Walk<T> &w, const MapView &m, Counts &c)
+{
+    uint32_t ids[kBatch], wd[kBatch];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+        ids[k] = w.idx;
+        wd[k] = __ldg(m.words + (w.idx >> 4));
+        walk_step<T, false>(w);
+    }
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) bits |= code_of(wd[k], ids[k]) << (2 * k);
+    const int left = w.n - w.s + 1;             // visits remaining, including the current one
+    const uint32_t valid = left >= kBatch ? 0xFFFFu : ((1u << (2 * left)) - 1u);
+    const uint32_t stop = bits & valid & 0xAAAAu;   // codes 2 (Occupied) and 3 (outside)
+    if (stop) {
+        const int k = (__ffs(stop) - 1) >> 1;
+        const uint32_t nf = w.nf + __popc(bits & ((1u << (2 * k)) - 1u) & 0x5555u);
+        walk_close_stop(w, m.policy, (bits >> (2 * k)) & 3u, w.s + k, nf, c);
+        return true;
+    }
+    w.nf += __popc(bits & valid & 0x5555u);
+    if (left <= kBatch) {
+        walk_close_end(w, m.policy, w.nf, c);
+        return true;
+    }
+    w.s += kBatch;
+    return false;
 }
 
 // ------------------------------------------------------------------ frames (a4)
@@ -325,105 +357,100 @@ __device__ __forceinline__ bool slot_ray(const TraceArgs &T, int slot, int &mi, 
     return true;
 }
 
-__device__ __forceinline__ void ray_endpoint(const int f[18], int mi, int mk, int corner, int e[3])
+// Walk segment of a ray: both ends from the Q16 lattice (modular arithmetic: the true
+// values lie inside (-2^30, 2^30), checked per perspective), rounded to Q12 (Q19).
+__device__ __forceinline__ void ray_segment(const int f[18], int mi, int mk, int corner, int o[3], int e[3])
 {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        uint32_t v;   // modular arithmetic: the true result is inside (-2^30, 2^30)
+        uint32_t v;
         if (corner < 0) {
-            v = (uint32_t)f[k] + (uint32_t)f[3 + k] + (uint32_t)mi * (uint32_t)f[6 + k] + (uint32_t)mk * (uint32_t)f[9 + k];
+            v = (uint32_t)f[k] + (uint32_t)f[3 + k] + (uint32_t)mi * (uint32_t)f[6 + k] +
+                (uint32_t)mk * (uint32_t)f[9 + k];
         } else {
             uint32_t rc = (uint32_t)f[12 + k], uc = (uint32_t)f[15 + k];
             v = (uint32_t)f[k] + (uint32_t)f[3 + k] + ((corner & 1) ? rc : 0u - rc) + ((corner & 2) ? uc : 0u - uc);
         }
-        e[k] = (int)v;
+        o[k] = (f[k] + 8) >> 4;          // round half up to Q12 (arithmetic shift = floor)
+        e[k] = ((int)v + 8) >> 4;
     }
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_id_trace(TraceArgs T)
+__device__ __forceinline__ void flush_counts(unsigned long long *totals, int j, Counts &c)
 {
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        int chunk = 0;
-        if (lane == 0) chunk = atomicAdd(T.work_counter, 1);
-        chunk = __shfl_sync(0xffffffffu, chunk, 0);
-        if (chunk >= T.total_chunks) return;
-        const int j = chunk / T.chunks_per_persp;
-        const int s_begin = (chunk - j * T.chunks_per_persp) * T.chunk;
-        const int s_end = min(s_begin + T.chunk, T.slots);
-        const int4 *fp = reinterpret_cast<const int4 *>(T.frames + (size_t)j * kFrameInts);
-        int4 q0 = __ldg(fp), q1 = __ldg(fp + 1), q2 = __ldg(fp + 2), q3 = __ldg(fp + 3), q4 = __ldg(fp + 4);
-        if (q4.z != 0) continue;   // invalid perspective (flagged by k_persp_frames); warp-uniform
-        const int f[18] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x,
-                           q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w, q4.x, q4.y};
-        Counts c{0, 0, 0, 0};
-        Ray r;
-        bool have = false;
-        int slot = s_begin + lane;
-        for (;;) {
-            if (!have) {
-                int mi = 0, mk = 0, corner = -1;
-                bool found = false;
-                while (slot < s_end) {
-                    bool ok = slot_ray(T, slot, mi, mk, corner);
-                    slot += 32;
-                    if (ok) { found = true; break; }
-                }
-                if (!found) break;
-                int e[3];
-                ray_endpoint(f, mi, mk, corner, e);
-                ray_setup(r, f, e);
-                if (ray_enter<false>(r, T.m, nullptr, nullptr, 0)) {
-                    if (T.m.policy == NBT_OUTSIDE_UNKNOWN) c.u += r.pre;
-                    continue;
-                }
-                have = true;
-            }
-            // one voxel visit + one DDA step of the fast walk
-            uint32_t code = code_at(T.m, r.idx);
-            if (code >= 2u) {
-                uint32_t tail = 0, l;
-                if (code == 2u) {
-                    l = r.s - r.s0 + 1;
-                    c.o += 1;
-                    c.u += l - r.nf - 1;
-                } else {
-                    l = r.s - r.s0;
-                    tail = r.n - r.s + 1;
-                    c.u += l - r.nf;
-                }
-                if (T.m.policy == NBT_OUTSIDE_UNKNOWN) c.u += r.pre + tail;
-                c.f += r.nf;
-                c.l += l;
-                have = false;
-                continue;
-            }
-            r.nf += code;
-            if (r.s == r.n) {
-                uint32_t l = r.s - r.s0 + 1;
-                c.u += l - r.nf + (T.m.policy == NBT_OUTSIDE_UNKNOWN ? r.pre : 0);
-                c.f += r.nf;
-                c.l += l;
-                have = false;
-                continue;
-            }
-            int a = ray_advance(r);
-            r.idx += (a == 0) ? r.dX : ((a == 1) ? r.dY : r.dZ);
-            r.s++;
-        }
-        // chunk totals: integer, so the summation order cannot change the result
-        uint32_t su = __reduce_add_sync(0xffffffffu, c.u);
-        uint32_t sf = __reduce_add_sync(0xffffffffu, c.f);
-        uint32_t so = __reduce_add_sync(0xffffffffu, c.o);
-        uint32_t sl = __reduce_add_sync(0xffffffffu, c.l);
-        if (lane == 0) {
-            unsigned long long *t = T.totals + 4 * (size_t)j;
-            atomicAdd(t + 0, (unsigned long long)su);
-            atomicAdd(t + 1, (unsigned long long)sf);
-            atomicAdd(t + 2, (unsigned long long)so);
-            atomicAdd(t + 3, (unsigned long long)sl);
-        }
+    if (j < 0) return;
+    unsigned long long *t = totals + 4 * (size_t)j;
+    if (c.u) atomicAdd(t + 0, (unsigned long long)c.u);
+    if (c.f) atomicAdd(t + 1, (unsigned long long)c.f);
+    if (c.o) atomicAdd(t + 2, (unsigned long long)c.o);
+    if (c.l) atomicAdd(t + 3, (unsigned long long)c.l);
+    c = Counts{0, 0, 0, 0};
+}
+
+// Start the ray in `slot` of perspective j.  Returns false if the slot is a tile hole
+// or the ray finished without entering the grid (its counts are then already added).
+template <typename T>
+__device__ __forceinline__ bool start_ray(const TraceArgs &A, int j, int slot, Walk<T> &w, Counts &c)
+{
+    int mi = 0, mk = 0, corner = -1;
+    if (!slot_ray(A, slot, mi, mk, corner)) return false;
+    const int4 *fp = reinterpret_cast<const int4 *>(A.frames + (size_t)j * kFrameInts);
+    int4 q0 = __ldg(fp), q1 = __ldg(fp + 1), q2 = __ldg(fp + 2), q3 = __ldg(fp + 3), q4 = __ldg(fp + 4);
+    const int f[18] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x,
+                       q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w, q4.x, q4.y};
+    int o[3], e[3];
+    ray_segment(f, mi, mk, corner, o, e);
+    walk_setup(w, o, e);
+    if (walk_enter<T, false>(w, A.m, nullptr, nullptr, 0)) {
+        if (A.m.policy == NBT_OUTSIDE_UNKNOWN) c.u += w.pre;
+        return false;
     }
+    return true;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_id_trace(TraceArgs A)
+{
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lanes_below = (1u << lane) - 1u;
+    int q_j = 0, q_next = 0, q_end = 0;      // warp-uniform chunk queue
+    bool q_done = false;
+    Walk<T> w;
+    bool have = false;
+    int jl = -1;                             // perspective of this lane's accumulators
+    Counts c{0, 0, 0, 0};
+    for (;;) {
+        // ---- refill idle lanes from the warp's chunk (fetch chunks as needed)
+        unsigned need = __ballot_sync(full, !have);
+        while (need && !q_done) {
+            if (q_next >= q_end) {
+                int ch = 0;
+                if (lane == 0) ch = atomicAdd(A.work_counter, 1);
+                ch = __shfl_sync(full, ch, 0);
+                if (ch >= A.total_chunks) { q_done = true; break; }
+                q_j = ch / A.chunks_per_persp;
+                q_next = (ch - q_j * A.chunks_per_persp) * A.chunk;
+                q_end = min(q_next + A.chunk, A.slots);
+                if (__ldg(A.frames + (size_t)q_j * kFrameInts + 18) != 0) q_next = q_end;   // invalid perspective
+                continue;
+            }
+            const int avail = q_end - q_next;
+            const int rank = __popc(need & lanes_below);
+            const bool mine = ((need >> lane) & 1u) && rank < avail;
+            const int slot = q_next + rank;
+            q_next += min(avail, __popc(need));
+            if (mine) {
+                if (jl != q_j) { flush_counts(A.totals, jl, c); jl = q_j; }
+                have = start_ray<T>(A, q_j, slot, w, c);
+            }
+            need = __ballot_sync(full, !have);
+        }
+        if (q_done && !__any_sync(full, have)) break;
+        // ---- kBatch voxels of the walk
+        if (have && walk_batch<T>(w, A.m, c)) have = false;
+    }
+    flush_counts(A.totals, jl, c);
 }
 
 // ------------------------------------------------------------ finalize (a8)
@@ -456,6 +483,9 @@ __global__ void k_id_finalize(FrameArgs A, const int32_t *__restrict__ frames,
 
 // ------------------------------------------------------------ debug hooks
 
+// Per-ray walk of an explicit Q12 segment, recording every visited voxel; the same
+// Walk / walk_step / walk_enter code as k_id_trace, one voxel at a time.
+template <typename T>
 __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const int32_t *__restrict__ e, int n_rays,
                               int max_visits, int32_t *ijk, uint8_t *code, int32_t *len, uint32_t *counts)
 {
@@ -463,18 +493,49 @@ __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const in
     if (r >= n_rays) return;
     int oo[3] = {o[3 * r], o[3 * r + 1], o[3 * r + 2]};
     int ee[3] = {e[3 * r], e[3 * r + 1], e[3 * r + 2]};
-    Ray ray;
-    ray_setup(ray, oo, ee);
+    Walk<T> w;
+    walk_setup(w, oo, ee);
     int32_t *ri = ijk + (size_t)r * max_visits * 3;
     uint8_t *rc = code + (size_t)r * max_visits;
     Counts c{0, 0, 0, 0};
-    if (ray_enter<true>(ray, m, ri, rc, max_visits)) {
-        if (m.policy == NBT_OUTSIDE_UNKNOWN) c.u += ray.pre;
+    int visits;
+    if (walk_enter<T, true>(w, m, ri, rc, max_visits)) {
+        if (m.policy == NBT_OUTSIDE_UNKNOWN) c.u += w.pre;
+        visits = w.n + 1;
     } else {
-        ray_walk<true>(ray, m, c, ri, rc, max_visits);
+        for (;;) {
+            uint32_t cd = code_of(__ldg(m.words + (w.idx >> 4)), w.idx);
+            if (w.s < max_visits) {
+                ri[3 * w.s] = w.vx; ri[3 * w.s + 1] = w.vy; ri[3 * w.s + 2] = w.vz;
+                rc[w.s] = cd == 3u ? 255 : (uint8_t)cd;
+            }
+            if (cd >= 2u) {
+                walk_close_stop(w, m.policy, cd, w.s, w.nf, c);
+                if (cd == 2u) {
+                    visits = w.s + 1;
+                } else {   // record the outside tail too
+                    for (int s = w.s + 1; s <= w.n; ++s) {
+                        walk_step<T, true>(w);
+                        if (s < max_visits) {
+                            ri[3 * s] = w.vx; ri[3 * s + 1] = w.vy; ri[3 * s + 2] = w.vz;
+                            rc[s] = 255;
+                        }
+                    }
+                    visits = w.n + 1;
+                }
+                break;
+            }
+            w.nf += cd;
+            if (w.s == w.n) {
+                walk_close_end(w, m.policy, w.nf, c);
+                visits = w.n + 1;
+                break;
+            }
+            walk_step<T, true>(w);
+            w.s++;
+        }
     }
-    // visits recorded: everything up to the stop (or the whole walk)
-    len[r] = (c.o ? ray.s + 1 : ray.n + 1);
+    len[r] = visits;
     counts[4 * r + 0] = c.u; counts[4 * r + 1] = c.f; counts[4 * r + 2] = c.o; counts[4 * r + 3] = c.l;
 }
 
@@ -513,6 +574,19 @@ FrameArgs frame_args(nbt_map m, const double *d_persp, int32_t first, int32_t st
     return A;
 }
 
+// Conservative bound (voxels) on |D_a| of every ray of a camera: the longest ray of the
+// frustum (its far-plane corner) plus rounding.
+double max_ray_voxels(const nbt_camera &cam, double range, double voxel_size)
+{
+    double rs = range / voxel_size;
+    double ex = (cam.width - 1) / (2.0 * cam.fx), ey = (cam.height - 1) / (2.0 * cam.fy);
+    if (cam.add_corners) {
+        ex = fmax(ex, cam.tan_half_fov_h);
+        ey = fmax(ey, cam.tan_half_fov_v);
+    }
+    return rs * sqrt(1.0 + ex * ex + ey * ey) * 1.001 + 2.0;
+}
+
 }  // namespace
 
 nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
@@ -525,11 +599,11 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     FrameArgs A = frame_args(m, L.d_persp, L.first, L.stride, L.n, L.poi, L.cam, L.range);
     int *counter = ctx->counter.as<int>();
     {
-    ProfScope ps(ctx, NBT_KERNEL_FRAMES);
-    k_persp_frames<<<(L.n + 127) / 128, 128, 0, ctx->stream>>>(A, ctx->frames.as<int32_t>(),
-                                                                ctx->totals.as<unsigned long long>(), counter,
-                                                                ctx->d_err);
-    NBT_LAUNCHED(ctx);
+        ProfScope ps(ctx, NBT_KERNEL_FRAMES);
+        k_persp_frames<<<(L.n + 127) / 128, 128, 0, ctx->stream>>>(A, ctx->frames.as<int32_t>(),
+                                                                    ctx->totals.as<unsigned long long>(), counter,
+                                                                    ctx->d_err);
+        NBT_LAUNCHED(ctx);
     }
 
     TraceArgs T;
@@ -543,16 +617,17 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     int Ht = (T.H + 3) / 4;
     T.n_tile_slots = T.tiled ? T.Wt * Ht * 32 : T.W * T.H;
     T.slots = T.n_tile_slots + (T.add_corners ? 4 : 0);
+    const bool wide = max_ray_voxels(L.cam, L.range, m->desc.voxel_size) > kInt32MaxVoxels;
     if (ctx->trace_blocks_per_sm == 0) {
         int b = 0;
-        NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_id_trace, kWarpsPerBlock * 32, 0));
+        NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_id_trace<int>, kWarpsPerBlock * 32, 0));
         ctx->trace_blocks_per_sm = b > 0 ? b : 1;
     }
     long long resident_warps = (long long)ctx->num_sms * ctx->trace_blocks_per_sm * kWarpsPerBlock;
     long long total_slots = (long long)L.n * T.slots;
-    long long per = total_slots / (8 * resident_warps);          // aim for >= 8 chunks per warp
+    long long per = total_slots / (4 * resident_warps);           // aim for >= 4 chunks per warp
     int chunk = (int)((per / 32) * 32);
-    chunk = chunk < 32 ? 32 : (chunk > 512 ? 512 : chunk);
+    chunk = chunk < 32 ? 32 : (chunk > 1024 ? 1024 : chunk);
     T.chunk = chunk;
     T.chunks_per_persp = (T.slots + chunk - 1) / chunk;
     long long tc = (long long)T.chunks_per_persp * L.n;
@@ -563,7 +638,10 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     int blocks = (int)(want_blocks < max_blocks ? want_blocks : max_blocks);
     {
         ProfScope ps(ctx, NBT_KERNEL_TRACE);
-        k_id_trace<<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T);
+        if (wide)
+            k_id_trace<long long><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T);
+        else
+            k_id_trace<int><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T);
         NBT_LAUNCHED(ctx);
     }
 
@@ -579,13 +657,28 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
 
 nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const int32_t *d_e, int32_t n_rays,
                               int32_t max_visits, int32_t *d_ijk, uint8_t *d_code, int32_t *d_len,
-                              uint32_t *d_counts)
+                              uint32_t *d_counts, bool wide)
 {
     if (n_rays == 0) return NBT_OK;
-    k_debug_trace<<<(n_rays + 127) / 128, 128, 0, ctx->stream>>>(view_of(m), d_o, d_e, n_rays, max_visits, d_ijk,
-                                                                 d_code, d_len, d_counts);
+    if (wide)
+        k_debug_trace<long long><<<(n_rays + 127) / 128, 128, 0, ctx->stream>>>(view_of(m), d_o, d_e, n_rays,
+                                                                                 max_visits, d_ijk, d_code, d_len,
+                                                                                 d_counts);
+    else
+        k_debug_trace<int><<<(n_rays + 127) / 128, 128, 0, ctx->stream>>>(view_of(m), d_o, d_e, n_rays, max_visits,
+                                                                           d_ijk, d_code, d_len, d_counts);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
+}
+
+bool debug_needs_wide(const int32_t *o_q12, const int32_t *e_q12, int32_t n_rays)
+{
+    for (int32_t i = 0; i < 3 * n_rays; ++i) {
+        long long d = (long long)e_q12[i] - o_q12[i];
+        if (d < 0) d = -d;
+        if ((d >> kQShift) + 2 > kInt32MaxVoxels) return true;
+    }
+    return false;
 }
 
 nbt_status launch_debug_frames(nbt_ctx ctx, nbt_map m, const double poi[3], const double *d_persp, int32_t n,

@@ -1,12 +1,13 @@
 // Voxel-map store kernels.
 //
-// Layout in HBM: the nx*ny*nz grid is surrounded by a ring of
-// sentinel voxels (code 3 = "outside") and stored x-fastest, 2 bits per voxel, 16
-// voxels per 32-bit word: padded voxel (x+1, y+1, z+1) has linear index
-// i = (x+1) + px*((y+1) + py*(z+1)) and lives in bits 2*(i&15).. of word i>>4.
-// 256^3 -> 4.1 MiB, 512^3 -> 32.4 MiB: both stay resident in the 126 MB L2.
-// The sentinel ring lets the traversal detect leaving the grid with the same
-// "code >= 2" test that detects an Occupied voxel (no bounds check in the hot loop).
+// Layout in HBM: the nx*ny*nz grid is surrounded by a shell of
+// kBorder sentinel voxels (code 3 = "outside") and stored x-fastest, 2 bits per voxel,
+// 16 voxels per 32-bit word: voxel (x, y, z) is padded voxel (x+B, y+B, z+B) with
+// linear index i = (x+B) + px*((y+B) + py*(z+B)), px = nx + 2B, stored in bits
+// 2*(i&15).. of word i>>4.  256^3 -> 5.0 MiB, 512^3 -> 36 MiB: L2-resident (126 MB).
+// The sentinel shell lets the walk detect leaving the grid with the same "code >= 2"
+// test that detects an Occupied voxel (no bounds check in the hot loop), and its
+// thickness B >= the walk's speculative batch keeps look-ahead loads inside the store.
 #include <cub/cub.cuh>
 
 #include "nbt_internal.cuh"
@@ -32,7 +33,7 @@ __global__ void k_map_pack(const uint8_t *__restrict__ codes, int nx, int ny, in
     for (int k = 0; k < 16; ++k) {
         uint32_t c = kOutside;
         if (i0 + k < nvox_pad) {
-            int gx = (int)x - 1, gy = (int)y - 1, gz = (int)z - 1;
+            int gx = (int)x - kBorder, gy = (int)y - kBorder, gz = (int)z - kBorder;
             if (gx >= 0 && gy >= 0 && gz >= 0 && gx < nx && gy < ny && gz < nz) {
                 c = codes[(size_t)gx + (size_t)nx * ((size_t)gy + (size_t)ny * gz)];
                 if (c > 2u) { bad = true; c = 0u; }
@@ -88,7 +89,8 @@ __global__ void k_delta_apply(const unsigned long long *__restrict__ keys, uint3
     if (k == ~0ull) return;
     if (i + 1 < n && (keys[i + 1] >> 32) == (k >> 32)) return;
     uint32_t pos = (uint32_t)(k & 0xffffffffu);
-    uint32_t x = (uint32_t)ijk[3 * pos] + 1, y = (uint32_t)ijk[3 * pos + 1] + 1, z = (uint32_t)ijk[3 * pos + 2] + 1;
+    uint32_t x = (uint32_t)ijk[3 * pos] + kBorder, y = (uint32_t)ijk[3 * pos + 1] + kBorder,
+             z = (uint32_t)ijk[3 * pos + 2] + kBorder;
     uint64_t pi = (uint64_t)x + (uint64_t)px * ((uint64_t)y + (uint64_t)py * z);
     uint32_t *w = words + (pi >> 4);
     uint32_t sh = (uint32_t)(pi & 15) * 2;
@@ -106,7 +108,7 @@ __global__ void k_map_unpack(const uint32_t *__restrict__ words, int nx, int ny,
     uint32_t x = (uint32_t)(i % nx);
     size_t r = i / nx;
     uint32_t y = (uint32_t)(r % ny), z = (uint32_t)(r / ny);
-    uint64_t pi = (uint64_t)(x + 1) + (uint64_t)px * ((uint64_t)(y + 1) + (uint64_t)py * (z + 1));
+    uint64_t pi = (uint64_t)(x + kBorder) + (uint64_t)px * ((uint64_t)(y + kBorder) + (uint64_t)py * (z + kBorder));
     codes[i] = (uint8_t)((words[pi >> 4] >> ((pi & 15) * 2)) & 3u);
 }
 

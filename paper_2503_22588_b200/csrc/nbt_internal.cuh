@@ -32,8 +32,9 @@ nbt_status cuda_fail(cudaError_t e, const char *what);
         if (e_ != cudaSuccess) return ::nbt::cuda_fail(e_, "kernel launch"); \
     } while (0)
 
-// Device error word bits (first error wins; read and cleared by nbt_ctx_sync).
-enum : int { DERR_NONE = 0 };
+// Thickness of the sentinel shell around the stored grid (k_map.cu); bounds the
+// walk's speculative look-ahead (k_id.cu kBatch <= kBorder).
+constexpr int kBorder = 8;
 
 // ----------------------------------------------------------- buffers
 
@@ -107,7 +108,7 @@ struct nbt_ctx_s {
 struct nbt_map_s {
     nbt_ctx ctx = nullptr;
     nbt_map_desc desc{};
-    uint32_t px = 0, py = 0, pz = 0;  // padded extents (one sentinel voxel each side)
+    uint32_t px = 0, py = 0, pz = 0;  // padded extents (kBorder sentinel voxels each side)
     uint64_t nvox_pad = 0;
     size_t nwords = 0;
     uint32_t *d_words = nullptr;      // 2-bit codes, 16 voxels per 32-bit word
@@ -153,7 +154,8 @@ struct IdLaunch {
 nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L);
 nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const int32_t *d_e, int32_t n_rays,
                               int32_t max_visits, int32_t *d_ijk, uint8_t *d_code, int32_t *d_len,
-                              uint32_t *d_counts);
+                              uint32_t *d_counts, bool wide);
+bool debug_needs_wide(const int32_t *o_q12, const int32_t *e_q12, int32_t n_rays);
 nbt_status launch_debug_frames(nbt_ctx ctx, nbt_map m, const double poi[3], const double *d_persp, int32_t n,
                                const nbt_camera &cam, double range, int32_t *d_frames);
 

@@ -319,8 +319,8 @@ static nbt_status check_desc(const nbt_map_desc *d)
     if (!d) return fail(NBT_ERR_INVALID_ARG, "null map desc");
     if (d->nx < 1 || d->ny < 1 || d->nz < 1 || d->nx > 16384 || d->ny > 16384 || d->nz > 16384)
         return fail(NBT_ERR_INVALID_ARG, "map extents must be in [1, 16384]");
-    uint64_t pad = (uint64_t)(d->nx + 2) * (d->ny + 2) * (d->nz + 2);
-    if (pad >= (1ull << 32)) return fail(NBT_ERR_INVALID_ARG, "(nx+2)(ny+2)(nz+2) must be < 2^32");
+    uint64_t pad = (uint64_t)(d->nx + 2 * kBorder) * (d->ny + 2 * kBorder) * (d->nz + 2 * kBorder);
+    if (pad >= (1ull << 32)) return fail(NBT_ERR_INVALID_ARG, "(nx+16)(ny+16)(nz+16) must be < 2^32");
     if (!(d->voxel_size > 0) || !isfinite(d->voxel_size)) return fail(NBT_ERR_INVALID_ARG, "voxel_size must be > 0");
     if (!finite3(d->origin)) return fail(NBT_ERR_INVALID_ARG, "origin must be finite");
     for (int k = 0; k < 3; ++k)
@@ -340,7 +340,7 @@ nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
     if (!m) return fail(NBT_ERR_OUT_OF_MEMORY, "nbt_map_create");
     m->ctx = ctx;
     m->desc = *desc;
-    m->px = desc->nx + 2; m->py = desc->ny + 2; m->pz = desc->nz + 2;
+    m->px = desc->nx + 2 * kBorder; m->py = desc->ny + 2 * kBorder; m->pz = desc->nz + 2 * kBorder;
     m->nvox_pad = (uint64_t)m->px * m->py * m->pz;
     m->nwords = (size_t)((m->nvox_pad + 15) / 16);
     cudaError_t e = cudaMalloc(&m->d_words, m->nwords * 4);
@@ -777,19 +777,19 @@ void nbt_idbuf_destroy(nbt_idbuf b)
 
 // -------------------------------------------------------------- test hooks
 
-nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *o_q16, const int32_t *e_q16, int32_t n_rays,
+nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *o_q12, const int32_t *e_q12, int32_t n_rays,
                            int32_t max_visits, int32_t *ijk_out, uint8_t *code_out, int32_t *len_out,
                            uint32_t *counts_out)
 {
     nbt_status s;
     if ((s = bind(ctx))) return s;
     if (!m || m->ctx != ctx) return fail(NBT_ERR_STATE, "nbt_debug_trace: map of another ctx");
-    if (n_rays < 0 || max_visits < 1 || (n_rays > 0 && (!o_q16 || !e_q16 || !ijk_out || !code_out || !len_out ||
+    if (n_rays < 0 || max_visits < 1 || (n_rays > 0 && (!o_q12 || !e_q12 || !ijk_out || !code_out || !len_out ||
                                                         !counts_out)))
         return fail(NBT_ERR_INVALID_ARG, "nbt_debug_trace: bad argument");
     if (n_rays == 0) return NBT_OK;
     for (int32_t i = 0; i < 3 * n_rays; ++i)
-        if (o_q16[i] <= -(1 << 30) || o_q16[i] >= (1 << 30) || e_q16[i] <= -(1 << 30) || e_q16[i] >= (1 << 30))
+        if (o_q12[i] <= -(1 << 30) || o_q12[i] >= (1 << 30) || e_q12[i] <= -(1 << 30) || e_q12[i] >= (1 << 30))
             return fail(NBT_ERR_INVALID_ARG, "nbt_debug_trace: coordinate outside (-2^30, 2^30)");
     size_t nr = n_rays, mv = max_visits;
     size_t b_in = nr * 12, b_ijk = nr * mv * 12, b_code = nr * mv, b_len = nr * 4, b_cnt = nr * 16;
@@ -801,9 +801,10 @@ nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *o_q16, const i
     int32_t *d_len = (int32_t *)(base + 2 * b_in + b_ijk);
     uint32_t *d_cnt = (uint32_t *)(base + 2 * b_in + b_ijk + b_len);
     uint8_t *d_code = (uint8_t *)(base + 2 * b_in + b_ijk + b_len + b_cnt);
-    NBT_CUDA(cudaMemcpyAsync(d_o, o_q16, b_in, cudaMemcpyHostToDevice, ctx->stream));
-    NBT_CUDA(cudaMemcpyAsync(d_e, e_q16, b_in, cudaMemcpyHostToDevice, ctx->stream));
-    if ((s = launch_debug_trace(ctx, m, d_o, d_e, n_rays, max_visits, d_ijk, d_code, d_len, d_cnt))) return s;
+    NBT_CUDA(cudaMemcpyAsync(d_o, o_q12, b_in, cudaMemcpyHostToDevice, ctx->stream));
+    NBT_CUDA(cudaMemcpyAsync(d_e, e_q12, b_in, cudaMemcpyHostToDevice, ctx->stream));
+    const bool wide = debug_needs_wide(o_q12, e_q12, n_rays);
+    if ((s = launch_debug_trace(ctx, m, d_o, d_e, n_rays, max_visits, d_ijk, d_code, d_len, d_cnt, wide))) return s;
     NBT_CUDA(cudaMemcpyAsync(ijk_out, d_ijk, b_ijk, cudaMemcpyDeviceToHost, ctx->stream));
     NBT_CUDA(cudaMemcpyAsync(code_out, d_code, b_code, cudaMemcpyDeviceToHost, ctx->stream));
     NBT_CUDA(cudaMemcpyAsync(len_out, d_len, b_len, cudaMemcpyDeviceToHost, ctx->stream));

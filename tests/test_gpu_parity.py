@@ -448,3 +448,26 @@ def test_full_size_config_b_sampled(nbt, ctx):
     _, g, c = oracle.id_compute(om, cfg.poi, P[idx], ocam, cfg.range_, nthreads=NTHREADS)
     assert np.array_equal(counts[idx].astype(np.int64), c)
     assert np.array_equal(gain[idx], g)
+
+
+# ------------------------------------------------ 64-bit decision-term variant
+
+def test_walks_very_long_rays_wide_path(nbt, ctx):
+    """Segments longer than 720 voxels per axis run the int64 variant of the same walk."""
+    codes = rand_map(40, 0.5, 0.5, 0.0, seed=13)
+    m, om = make_map(nbt, ctx, codes)
+    rng = np.random.default_rng(5)
+    o = np.round(rng.uniform(5, 35, (60, 3)) * 4096).astype(np.int32)
+    d = rng.normal(size=(60, 3)); d /= np.linalg.norm(d, axis=1, keepdims=True)
+    e = np.round((o / 4096 + d * rng.uniform(800, 2500, (60, 1))) * 4096).astype(np.int32)
+    _compare_walks(nbt, ctx, m, om, o, e, max_visits=64)
+
+
+def test_id_wide_path(nbt, ctx):
+    """A range long enough (> 700 voxels) to select the int64 trace kernel."""
+    codes = rand_map(48, 0.3, 0.69, 0.01, seed=17)
+    m, om = make_map(nbt, ctx, codes, 1.0)
+    poi = np.array([24.5, 24.5, 24.5])
+    P = oracle.sample_perspectives(poi, 15.0, 12, seed=6)
+    cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 12, 9, 900.0, corners=True)
+    assert_cloud_equal(cloud, P, g, c)
