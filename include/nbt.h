@@ -103,7 +103,7 @@ enum { NBT_OUTSIDE_UNKNOWN = 0, NBT_OUTSIDE_CLIP = 1 };        /* Q14 */
 typedef struct nbt_map_s *nbt_map;
 
 typedef struct {
-    int32_t nx, ny, nz;       /* voxels per axis, each >= 1; (nx+16)(ny+16)(nz+16) < 2^32 */
+    int32_t nx, ny, nz;       /* voxels per axis, each >= 1; (nx+32)(ny+32)(nz+32) < 2^32 */
     double  voxel_size;       /* s_Vox > 0 (1 cm) */
     double  origin[3];        /* world position of voxel (0,0,0)'s min corner */
     double  gain[3];          /* g[U], g[F], g[O] of Eq. 2 as per-state constants (Q15);

@@ -7,14 +7,16 @@
 //                   current chunk (a run of one perspective's rays in 8x4 pixel tiles).
 //                   The lane builds its endpoint on the far plane in registers
 //                   (Q27), rounds both ends to Q12, and walks the exact
-//                   integer 3D-DDA (Q13) through the 2-bit map in batches of kBatch
+//                   integer 3D-DDA (Q13) through the 2-bit map in batches of K = 16
 //                   voxels: the DDA does not depend on the map, so a batch computes
-//                   kBatch voxel indices, issues kBatch independent loads, packs the
+//                   K voxel indices, issues K independent loads, packs the
 //                   2-bit codes into one word and finds the first Occupied / outside
 //                   voxel with one ffs (early stop) and the Free count with one
-//                   popc.  Per-state visit counts (Eq. 2 as integers, Q26) accumulate
-//                   in registers and are flushed with 4 u64 atomics when a lane moves
-//                   to another perspective.
+//                   popc.  Ray set-up (frame, endpoint, 64-bit DDA init, grid entry)
+//                   runs converged for 32 rays at a time into a per-warp shared-memory
+//                   queue; lanes refill from it when their ray ends.  Per-state visit
+//                   counts (Eq. 2 as integers, Q26) accumulate in registers and are
+//                   flushed with 4 u64 atomics when a lane moves to another perspective.
 //   k_id_finalize   g_P = ((T_U g_U + T_F g_F) + T_O g_O) / N_E  (Q26)
 //
 // Exact decision with 32-bit arithmetic.  With D = E - O and
@@ -27,6 +29,8 @@
 // q_ab is computed once per ray in 64-bit and then kept in int32, which is exact for
 // rays up to 720 voxels per axis; longer rays use the same code with 64-bit q (the
 // host picks the variant from the camera geometry).
+#include <stdlib.h>
+
 #include "nbt_internal.cuh"
 
 namespace nbt {
@@ -35,8 +39,9 @@ namespace {
 constexpr int kFrameInts = 20;   // O, A, Rh, Uh, Rc, Uc (3 each, Q16), status, pad
 constexpr int kWarpsPerBlock = 8;
 constexpr int kQShift = 12;      // walk coordinates: Q12
-constexpr int kBatch = 8;        // voxels per speculative batch (<= kBorder)
-static_assert(kBatch <= kBorder, "look-ahead must stay inside the sentinel shell");
+// Trace variants: K voxels per speculative batch; PIPE = the next batch's loads are in
+// flight while the current batch is consumed (look-ahead 2K, which must stay inside
+// the kBorder-voxel sentinel shell).
 constexpr int kInt32MaxVoxels = 700;   // |D_a| bound (voxels) for the int32 decision terms
 
 struct MapView {
@@ -63,8 +68,9 @@ template <typename T>
 struct Walk {
     T qxy, qxz, qyz;           // sign decides the next axis (see header)
     T ax, ay, az;              // |D_a| in Q12 units
+    T nax;                     // -|D_x| (hot path)
     uint32_t idx;              // padded linear index of the current voxel (in-grid walk)
-    int dX, dY, dZ;            // idx increments of a step along x, y, z
+    int dX, dY, ndZ;           // idx increments of a step along x, y and (negated) z
     int s, n;                  // current step (0 = origin voxel) and total steps
     int s0;                    // step at which the walk entered the grid
     uint32_t nf;               // Free voxels counted so far in the grid
@@ -98,6 +104,7 @@ __device__ __forceinline__ void walk_setup(Walk<T> &w, const int o[3], const int
     w.qxz = (T)(fxz >> kQShift);
     w.qyz = (T)(fyz >> kQShift);
     w.ax = (T)ad[0]; w.ay = (T)ad[1]; w.az = (T)ad[2];
+    w.nax = -w.ax;
     w.sx = neg[0] ? -1 : 1;
     w.sy = neg[1] ? -1 : 1;
     w.sz = neg[2] ? -1 : 1;
@@ -108,20 +115,42 @@ __device__ __forceinline__ void walk_setup(Walk<T> &w, const int o[3], const int
     w.pre = 0;
 }
 
+__device__ __forceinline__ int mad_i32(int a, int b, int c)
+{
+    int d;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 // One DDA step: pick the axis, update the two decision terms that involve it.
 template <typename T, bool COORDS>
 __device__ __forceinline__ void walk_step(Walk<T> &w)
 {
-    const bool px = (w.qxy & w.qxz) < 0;         // both negative
-    const bool py = !px && w.qyz < 0;
-    const bool pz = !px && !py;
-    if (px) { w.qxy += w.ay; w.qxz += w.az; w.idx += w.dX; }
-    if (py) { w.qxy -= w.ax; w.qyz += w.az; w.idx += w.dY; }
-    if (pz) { w.qxz -= w.ax; w.qyz -= w.ay; w.idx += w.dZ; }
-    if (COORDS) {
-        if (px) w.vx += w.sx;
-        if (py) w.vy += w.sy;
-        if (pz) w.vz += w.sz;
+    if constexpr (sizeof(T) == 4 && !COORDS) {
+        // Hot path: the axis choice as 0/1 and 0/-1 integers from the sign bits (6 ALU
+        // ops), the updates as 9 multiply-adds on the FMA pipe, so the two integer
+        // pipes share the step instead of queueing on the ALU pipe (selects).
+        const int t1 = w.qxy & w.qxz;            // sign: x first
+        const int t2 = w.qyz & ~t1;              // sign: y first
+        const int px = (int)((unsigned)t1 >> 31);
+        const int py = (int)((unsigned)t2 >> 31);
+        const int npz = px + py - 1;             // -1 if z first, else 0
+        w.qxy = mad_i32(px, w.ay, mad_i32(py, w.nax, w.qxy));
+        w.qxz = mad_i32(px, w.az, mad_i32(npz, w.ax, w.qxz));
+        w.qyz = mad_i32(py, w.az, mad_i32(npz, w.ay, w.qyz));
+        w.idx = (uint32_t)mad_i32(px, w.dX, mad_i32(py, w.dY, mad_i32(npz, w.ndZ, (int)w.idx)));
+    } else {
+        const bool px = (w.qxy & w.qxz) < 0;     // both negative
+        const bool py = !px && w.qyz < 0;
+        const bool pz = !px && !py;
+        if (px) { w.qxy += w.ay; w.qxz += w.az; w.idx += w.dX; }
+        if (py) { w.qxy -= w.ax; w.qyz += w.az; w.idx += w.dY; }
+        if (pz) { w.qxz -= w.ax; w.qyz -= w.ay; w.idx -= w.ndZ; }
+        if (COORDS) {
+            if (px) w.vx += w.sx;
+            if (py) w.vy += w.sy;
+            if (pz) w.vz += w.sz;
+        }
     }
 }
 
@@ -149,7 +178,7 @@ __device__ bool walk_enter(Walk<T> &w, const MapView &m, int32_t *rec_ijk, uint8
     w.idx = padded_index(m, w.vx, w.vy, w.vz);
     w.dX = w.sx;
     w.dY = w.sy * m.px;
-    w.dZ = w.sz * m.pxy;
+    w.ndZ = -w.sz * m.pxy;
     return false;
 }
 
@@ -185,36 +214,57 @@ __device__ __forceinline__ void walk_close_end(const Walk<T> &w, int policy, uin
     c.l += l;
 }
 
-// One batch of kBatch visits starting at the current voxel.  Returns true when the ray
-// is finished (counts added to c).
-template <typename T>
-__device__ __forceinline__ bool walk_batch(Walk<T> &w, const MapView &m, Counts &c)
+// A batch of K visits: the loaded map words and, per visit, the rotate amount that
+// brings its 2-bit code to bits 2k..2k+1 of the packed word.
+template <int K>
+struct Batch {
+    uint32_t wd[K];
+    uint32_t rot[K];
+};
+
+template <int K>
+__device__ __forceinline__ constexpr uint32_t lanes_mask(uint32_t pattern)
 {
-    uint32_t ids[kBatch], wd[kBatch];
+    return K >= 16 ? pattern : (pattern & ((1u << (2 * K)) - 1u));
+}
+
+// Issue the K loads of the next K visits (the DDA does not depend on the map, so
+// this runs ahead of the codes) and advance the DDA by K steps.
+template <typename T, int K>
+__device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<K> &b)
+{
 #pragma unroll
-    for (int k = 0; k < kBatch; ++k) {
-        ids[k] = w.idx;
-        wd[k] = __ldg(m.words + (w.idx >> 4));
+    for (int k = 0; k < K; ++k) {
+        b.rot[k] = (w.idx << 1) - 2 * k;        // rotate amounts are taken mod 32
+        b.wd[k] = __ldg(m.words + (w.idx >> 4));
         walk_step<T, false>(w);
     }
+}
+
+// Consume the batch holding visits s..s+K-1.  Returns true when the ray is finished
+// (counts added to c): first code >= 2 by one ffs (Occupied: early stop, P:213;
+// 3: left the grid), Free voxels by one popc.
+template <typename T, int K>
+__device__ __forceinline__ bool batch_consume(Walk<T> &w, const Batch<K> &b, int policy, Counts &c)
+{
     uint32_t bits = 0;
 #pragma unroll
-    for (int k = 0; k < kBatch; ++k) bits |= code_of(wd[k], ids[k]) << (2 * k);
+    for (int k = 0; k < K; ++k) bits |= __funnelshift_r(b.wd[k], b.wd[k], b.rot[k]) & (3u << (2 * k));
     const int left = w.n - w.s + 1;             // visits remaining, including the current one
-    const uint32_t valid = left >= kBatch ? 0xFFFFu : ((1u << (2 * left)) - 1u);
-    const uint32_t stop = bits & valid & 0xAAAAu;   // codes 2 (Occupied) and 3 (outside)
+    const uint32_t valid = left >= K ? lanes_mask<K>(0xFFFFFFFFu) : ((1u << (2 * left)) - 1u);
+    const uint32_t stop = bits & valid & 0xAAAAAAAAu;   // codes 2 (Occupied) and 3 (outside)
     if (stop) {
         const int k = (__ffs(stop) - 1) >> 1;
-        const uint32_t nf = w.nf + __popc(bits & ((1u << (2 * k)) - 1u) & 0x5555u);
-        walk_close_stop(w, m.policy, (bits >> (2 * k)) & 3u, w.s + k, nf, c);
+        const uint32_t nf = w.nf + __popc(bits & ((1u << (2 * k)) - 1u) & 0x55555555u);
+        walk_close_stop(w, policy, (bits >> (2 * k)) & 3u, w.s + k, nf, c);
         return true;
     }
-    w.nf += __popc(bits & valid & 0x5555u);
-    if (left <= kBatch) {
-        walk_close_end(w, m.policy, w.nf, c);
+    w.nf += __popc(bits & valid & 0x55555555u);
+    if (left <= K) {
+        walk_close_end(w, policy, w.nf, c);
         return true;
     }
-    w.s += kBatch;
+    w.s += K;
     return false;
 }
 
@@ -387,10 +437,11 @@ __device__ __forceinline__ void flush_counts(unsigned long long *totals, int j, 
     c = Counts{0, 0, 0, 0};
 }
 
-// Start the ray in `slot` of perspective j.  Returns false if the slot is a tile hole
-// or the ray finished without entering the grid (its counts are then already added).
+// Prepare the ray in `slot` of perspective j (frame, segment, DDA set-up, grid
+// entry).  Returns false if the slot is a tile hole or the ray ends without entering
+// the grid (its Unknown visits are then added to the totals directly).
 template <typename T>
-__device__ __forceinline__ bool start_ray(const TraceArgs &A, int j, int slot, Walk<T> &w, Counts &c)
+__device__ __forceinline__ bool prep_ray(const TraceArgs &A, int j, int slot, Walk<T> &w)
 {
     int mi = 0, mk = 0, corner = -1;
     if (!slot_ray(A, slot, mi, mk, corner)) return false;
@@ -402,53 +453,119 @@ __device__ __forceinline__ bool start_ray(const TraceArgs &A, int j, int slot, W
     ray_segment(f, mi, mk, corner, o, e);
     walk_setup(w, o, e);
     if (walk_enter<T, false>(w, A.m, nullptr, nullptr, 0)) {
-        if (A.m.policy == NBT_OUTSIDE_UNKNOWN) c.u += w.pre;
+        if (A.m.policy == NBT_OUTSIDE_UNKNOWN) atomicAdd(A.totals + 4 * (size_t)j, (unsigned long long)w.pre);
         return false;
     }
     return true;
 }
 
+// Per-warp queue of prepared walks in shared memory (structure of arrays, one column
+// per entry, so 32 lanes touching 32 entries hit 32 banks).
 template <typename T>
+struct WalkQueue {
+    T q[3][32];
+    T a[3][32];
+    uint32_t idx[32];
+    int d[3][32];
+    int n[32], s0[32];
+    uint32_t pre[32];
+    int j[32];
+};
+
+template <typename T>
+__device__ __forceinline__ void queue_put(WalkQueue<T> &Q, int i, const Walk<T> &w, int j)
+{
+    Q.q[0][i] = w.qxy; Q.q[1][i] = w.qxz; Q.q[2][i] = w.qyz;
+    Q.a[0][i] = w.ax; Q.a[1][i] = w.ay; Q.a[2][i] = w.az;
+    Q.idx[i] = w.idx;
+    Q.d[0][i] = w.dX; Q.d[1][i] = w.dY; Q.d[2][i] = w.ndZ;
+    Q.n[i] = w.n; Q.s0[i] = w.s0; Q.pre[i] = w.pre; Q.j[i] = j;
+}
+
+template <typename T>
+__device__ __forceinline__ int queue_get(const WalkQueue<T> &Q, int i, Walk<T> &w)
+{
+    w.qxy = Q.q[0][i]; w.qxz = Q.q[1][i]; w.qyz = Q.q[2][i];
+    w.ax = Q.a[0][i]; w.ay = Q.a[1][i]; w.az = Q.a[2][i];
+    w.nax = -w.ax;
+    w.idx = Q.idx[i];
+    w.dX = Q.d[0][i]; w.dY = Q.d[1][i]; w.ndZ = Q.d[2][i];
+    w.n = Q.n[i]; w.s0 = Q.s0[i]; w.s = w.s0; w.pre = Q.pre[i]; w.nf = 0;
+    return Q.j[i];
+}
+
+template <typename T, int K, bool PIPE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_id_trace(TraceArgs A)
 {
+    static_assert((PIPE ? 2 * K : K) <= kBorder, "look-ahead must stay inside the sentinel shell");
+    __shared__ WalkQueue<T> queues[kWarpsPerBlock];
+    WalkQueue<T> &Q = queues[threadIdx.x >> 5];
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lanes_below = (1u << lane) - 1u;
-    int q_j = 0, q_next = 0, q_end = 0;      // warp-uniform chunk queue
+    int q_j = 0, q_next = 0, q_end = 0;      // warp-uniform chunk cursor
     bool q_done = false;
+    int qhead = 0, qcount = 0;               // warp-uniform prepared-walk queue
     Walk<T> w;
+    Batch<K> b0, b1;
     bool have = false;
     int jl = -1;                             // perspective of this lane's accumulators
     Counts c{0, 0, 0, 0};
     for (;;) {
-        // ---- refill idle lanes from the warp's chunk (fetch chunks as needed)
-        unsigned need = __ballot_sync(full, !have);
-        while (need && !q_done) {
-            if (q_next >= q_end) {
-                int ch = 0;
-                if (lane == 0) ch = atomicAdd(A.work_counter, 1);
-                ch = __shfl_sync(full, ch, 0);
-                if (ch >= A.total_chunks) { q_done = true; break; }
-                q_j = ch / A.chunks_per_persp;
-                q_next = (ch - q_j * A.chunks_per_persp) * A.chunk;
-                q_end = min(q_next + A.chunk, A.slots);
-                if (__ldg(A.frames + (size_t)q_j * kFrameInts + 18) != 0) q_next = q_end;   // invalid perspective
-                continue;
+        const unsigned need = __ballot_sync(full, !have);
+        if (need) {
+            // all 32 lanes prepare up to 32 rays at once, so the set-up runs converged
+            while (qcount == 0 && !q_done) {
+                if (q_next >= q_end) {
+                    int ch = 0;
+                    if (lane == 0) ch = atomicAdd(A.work_counter, 1);
+                    ch = __shfl_sync(full, ch, 0);
+                    if (ch >= A.total_chunks) { q_done = true; break; }
+                    q_j = ch / A.chunks_per_persp;
+                    q_next = (ch - q_j * A.chunks_per_persp) * A.chunk;
+                    q_end = min(q_next + A.chunk, A.slots);
+                    if (__ldg(A.frames + (size_t)q_j * kFrameInts + 18) != 0) q_next = q_end;   // invalid
+                    continue;
+                }
+                const int avail = min(32, q_end - q_next);
+                Walk<T> t;
+                const bool ok = lane < avail && prep_ray<T>(A, q_j, q_next + lane, t);
+                q_next += avail;
+                const unsigned vm = __ballot_sync(full, ok);
+                if (ok) queue_put(Q, __popc(vm & lanes_below), t, q_j);
+                __syncwarp();
+                qhead = 0;
+                qcount = __popc(vm);
             }
-            const int avail = q_end - q_next;
-            const int rank = __popc(need & lanes_below);
-            const bool mine = ((need >> lane) & 1u) && rank < avail;
-            const int slot = q_next + rank;
-            q_next += min(avail, __popc(need));
-            if (mine) {
-                if (jl != q_j) { flush_counts(A.totals, jl, c); jl = q_j; }
-                have = start_ray<T>(A, q_j, slot, w, c);
+            if (qcount) {
+                const int rank = __popc(need & lanes_below);
+                const int take = min(__popc(need), qcount);
+                if (!have && rank < take) {
+                    const int j = queue_get(Q, qhead + rank, w);
+                    if (j != jl) { flush_counts(A.totals, jl, c); jl = j; }
+                    have = true;
+                    if (PIPE) batch_issue<T, K>(w, A.m, b0);
+                }
+                qhead += take;
+                qcount -= take;
+                __syncwarp();
             }
-            need = __ballot_sync(full, !have);
         }
-        if (q_done && !__any_sync(full, have)) break;
-        // ---- kBatch voxels of the walk
-        if (have && walk_batch<T>(w, A.m, c)) have = false;
+        if (q_done && qcount == 0 && !__any_sync(full, have)) break;
+        if (!have) continue;
+        if (!PIPE) {
+            batch_issue<T, K>(w, A.m, b0);
+            if (batch_consume<T, K>(w, b0, A.m.policy, c)) have = false;
+        } else {
+            // b0 holds visits s..s+K-1; keep the next batch in flight while consuming
+            if (w.n - w.s + 1 > K) batch_issue<T, K>(w, A.m, b1);
+            if (batch_consume<T, K>(w, b0, A.m.policy, c)) {
+                have = false;
+            } else {
+                if (w.n - w.s + 1 > K) batch_issue<T, K>(w, A.m, b0);
+                if (batch_consume<T, K>(w, b1, A.m.policy, c)) have = false;
+            }
+        }
     }
     flush_counts(A.totals, jl, c);
 }
@@ -574,6 +691,17 @@ FrameArgs frame_args(nbt_map m, const double *d_persp, int32_t first, int32_t st
     return A;
 }
 
+// Trace kernel variant (experiments, profiles/r01_trace_variants.md): NBT_TRACE_VARIANT =
+// 0 (K=16, default), 1 (K=8), 2 (K=4 pipelined), 3 (K=8 pipelined).
+int trace_variant()
+{
+    static int v = [] {
+        const char *e = getenv("NBT_TRACE_VARIANT");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 // Conservative bound (voxels) on |D_a| of every ray of a camera: the longest ray of the
 // frustum (its far-plane corner) plus rounding.
 double max_ray_voxels(const nbt_camera &cam, double range, double voxel_size)
@@ -618,10 +746,16 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     T.n_tile_slots = T.tiled ? T.Wt * Ht * 32 : T.W * T.H;
     T.slots = T.n_tile_slots + (T.add_corners ? 4 : 0);
     const bool wide = max_ray_voxels(L.cam, L.range, m->desc.voxel_size) > kInt32MaxVoxels;
-    if (ctx->trace_blocks_per_sm == 0) {
+    const int variant = trace_variant();
+    if (ctx->trace_blocks_per_sm == 0 || ctx->trace_variant_cached != variant) {
         int b = 0;
-        NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_id_trace<int>, kWarpsPerBlock * 32, 0));
+        const void *fn = (const void *)k_id_trace<int, 16, false>;
+        if (variant == 1) fn = (const void *)k_id_trace<int, 8, false>;
+        if (variant == 2) fn = (const void *)k_id_trace<int, 4, true>;
+        if (variant == 3) fn = (const void *)k_id_trace<int, 8, true>;
+        NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kWarpsPerBlock * 32, 0));
         ctx->trace_blocks_per_sm = b > 0 ? b : 1;
+        ctx->trace_variant_cached = variant;
     }
     long long resident_warps = (long long)ctx->num_sms * ctx->trace_blocks_per_sm * kWarpsPerBlock;
     long long total_slots = (long long)L.n * T.slots;
@@ -638,10 +772,16 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     int blocks = (int)(want_blocks < max_blocks ? want_blocks : max_blocks);
     {
         ProfScope ps(ctx, NBT_KERNEL_TRACE);
-        if (wide)
-            k_id_trace<long long><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T);
-        else
-            k_id_trace<int><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T);
+        if (wide) {
+            k_id_trace<long long, 16, false><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T);
+        } else {
+            switch (variant) {
+            case 1: k_id_trace<int, 8, false><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T); break;
+            case 2: k_id_trace<int, 4, true><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T); break;
+            case 3: k_id_trace<int, 8, true><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T); break;
+            default: k_id_trace<int, 16, false><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T); break;
+            }
+        }
         NBT_LAUNCHED(ctx);
     }
 

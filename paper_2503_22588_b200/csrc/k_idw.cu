@@ -1,62 +1,99 @@
 // IDW query over the ID ring buffer (Eq. 4).
 //
-//   G(x) = sum_u w_u * [ sum_j g_P,j d_j(x)^-p / sum_j d_j(x)^-p ]
+//   G(x) = sum_u w_u * v_u(x),   v_u(x) = sum_j g_P,j d_j(x)^-p / sum_j d_j(x)^-p
 //
 // over the buffered clouds u = oldest..newest with w_u = 1/(m-u) (newest weighs 1,
 // reading Q21), each cloud's own perspectives (Q20) and all of them (Q22); if the
-// nearest perspective is closer than zero_eps the bracket is its gain (Q23).
-// One warp per query: lanes stride over an entry's perspectives, FP64 throughout
-// (p = 2 needs no pow: d^-2 = 1/d^2), warp shuffles combine the partial sums and the
-// (distance, index) argmin -- the nearest-perspective decision is made on
-// correctly-rounded d = sqrt(d^2) so it is exactly reproducible.
+// nearest perspective is closer than zero_eps, v_u is its gain (Q23).
+//
+//   k_idw_entry    grid (query blocks) x (entries): a block stages one entry's
+//                  perspectives through shared memory in tiles and each thread walks
+//                  them for its query in ascending j -- the same summation order as the
+//                  definition, every product and sum rounded once, so for p = 2
+//                  (d^-2 = 1/d^2, no pow) v_u is reproduced bit for bit.  The nearest
+//                  perspective is tracked on d^2 (monotone in d); only when it is within
+//                  zero_eps is d = sqrt(d^2) evaluated, with a second pass to pick the
+//                  lowest j among exactly equal d.
+//   k_idw_combine  per query: G = sum_u w_u v_u in entry order (optionally / sum_u w_u).
 #include "nbt_internal.cuh"
 
 namespace nbt {
 namespace {
 
-constexpr int kWarps = 8;
+constexpr int kThreads = 128;
+constexpr int kTile = 256;
 
-__global__ void __launch_bounds__(kWarps * 32)
-    k_idw_query(const double *__restrict__ xyz, const double *__restrict__ gain, int32_t max_persp, IdwEntries E,
-                const double *__restrict__ q, int32_t n_q, double power_p, double zero_eps, int32_t normalize,
-                double *__restrict__ out)
+__device__ __forceinline__ double dist2(double x0, double x1, double x2, double p0, double p1, double p2)
 {
-    const int lane = threadIdx.x & 31;
-    const int qi = blockIdx.x * kWarps + (threadIdx.x >> 5);
-    if (qi >= n_q) return;
-    const double x0 = q[3 * (size_t)qi], x1 = q[3 * (size_t)qi + 1], x2 = q[3 * (size_t)qi + 2];
+    double dx = __dsub_rn(x0, p0), dy = __dsub_rn(x1, p1), dz = __dsub_rn(x2, p2);
+    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_idw_entry(const double *__restrict__ xyz, const double *__restrict__ gain, int32_t max_persp, IdwEntries E,
+                const double *__restrict__ q, int32_t n_q, double power_p, double zero_eps,
+                double *__restrict__ v_out)
+{
+    __shared__ double sp[kTile][4];
+    const int e = blockIdx.y;
+    const int qi = blockIdx.x * kThreads + threadIdx.x;
+    const bool active = qi < n_q;
+    const double *P = xyz + (size_t)E.slot[e] * max_persp * 3;
+    const double *G = gain + (size_t)E.slot[e] * max_persp;
+    const int np = E.size[e];
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+    if (active) { x0 = q[3 * (size_t)qi]; x1 = q[3 * (size_t)qi + 1]; x2 = q[3 * (size_t)qi + 2]; }
     const bool p2 = power_p == 2.0;
     const double hp = -0.5 * power_p;
-    double G = 0.0, wsum = 0.0;
-    for (int e = 0; e < E.m; ++e) {
-        const double *P = xyz + (size_t)E.slot[e] * max_persp * 3;
-        const double *Gn = gain + (size_t)E.slot[e] * max_persp;
-        const int np = E.size[e];
-        double num = 0.0, den = 0.0, dmin = __longlong_as_double(0x7ff0000000000000LL);
-        int jmin = 0x7fffffff;
-        for (int j = lane; j < np; j += 32) {
-            double dx = __dsub_rn(x0, P[3 * j]), dy = __dsub_rn(x1, P[3 * j + 1]), dz = __dsub_rn(x2, P[3 * j + 2]);
-            double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-            double d = __dsqrt_rn(d2);
-            if (d < dmin) { dmin = d; jmin = j; }
-            double w = p2 ? __drcp_rn(d2) : pow(d2, hp);
-            num = fma(Gn[j], w, num);
-            den += w;
+    double num = 0.0, den = 0.0, d2min = __longlong_as_double(0x7ff0000000000000LL);
+    int jmin = 0;
+    for (int base = 0; base < np; base += kTile) {
+        const int nt = min(kTile, np - base);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nt; t += kThreads) {
+            sp[t][0] = P[3 * (size_t)(base + t)];
+            sp[t][1] = P[3 * (size_t)(base + t) + 1];
+            sp[t][2] = P[3 * (size_t)(base + t) + 2];
+            sp[t][3] = G[base + t];
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            num += __shfl_xor_sync(0xffffffffu, num, off);
-            den += __shfl_xor_sync(0xffffffffu, den, off);
-            double od = __shfl_xor_sync(0xffffffffu, dmin, off);
-            int oj = __shfl_xor_sync(0xffffffffu, jmin, off);
-            if (od < dmin || (od == dmin && oj < jmin)) { dmin = od; jmin = oj; }
+        __syncthreads();
+        if (active) {
+            for (int t = 0; t < nt; ++t) {
+                const double d2 = dist2(x0, x1, x2, sp[t][0], sp[t][1], sp[t][2]);
+                if (d2 < d2min) { d2min = d2; jmin = base + t; }
+                const double w = p2 ? __drcp_rn(d2) : pow(d2, hp);
+                num = __dadd_rn(num, __dmul_rn(sp[t][3], w));
+                den = __dadd_rn(den, w);
+            }
         }
-        double v = (dmin < zero_eps) ? Gn[jmin] : num / den;
-        double wu = 1.0 / (double)(E.m - e);
-        G += wu * v;
-        wsum += wu;
     }
-    if (lane == 0) out[qi] = normalize ? G / wsum : G;
+    if (!active) return;
+    double v = __ddiv_rn(num, den);
+    const double dmin = __dsqrt_rn(d2min);
+    if (dmin < zero_eps) {
+        // nearest by d (not d^2): lowest j among perspectives whose rounded d equals dmin
+        int jbest = jmin;
+        for (int j = 0; j < jmin; ++j) {
+            const double d2 = dist2(x0, x1, x2, P[3 * (size_t)j], P[3 * (size_t)j + 1], P[3 * (size_t)j + 2]);
+            if (__dsqrt_rn(d2) == dmin) { jbest = j; break; }
+        }
+        v = G[jbest];
+    }
+    v_out[(size_t)e * n_q + qi] = v;
+}
+
+__global__ void k_idw_combine(const double *__restrict__ v, int32_t m, int32_t n_q, int32_t normalize,
+                              double *__restrict__ out)
+{
+    const int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= n_q) return;
+    double g = 0.0, wsum = 0.0;
+    for (int e = 0; e < m; ++e) {
+        const double wu = __ddiv_rn(1.0, (double)(m - e));
+        g = __dadd_rn(g, __dmul_rn(wu, v[(size_t)e * n_q + qi]));
+        wsum = __dadd_rn(wsum, wu);
+    }
+    out[qi] = normalize ? __ddiv_rn(g, wsum) : g;
 }
 
 }  // namespace
@@ -65,9 +102,15 @@ nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, co
                       double power_p, double zero_eps, int32_t normalize, double *d_out)
 {
     if (n_q == 0) return NBT_OK;
+    nbt_status st;
+    if ((st = ctx->idw_tmp.ensure((size_t)E.m * n_q * 8))) return st;
     ProfScope ps(ctx, NBT_KERNEL_IDW);
-    k_idw_query<<<(n_q + kWarps - 1) / kWarps, kWarps * 32, 0, ctx->stream>>>(
-        b->d_xyz, b->d_gain, b->max_persp, E, d_q, n_q, power_p, zero_eps, normalize, d_out);
+    dim3 grid((n_q + kThreads - 1) / kThreads, E.m);
+    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, E, d_q, n_q, power_p,
+                                                     zero_eps, ctx->idw_tmp.as<double>());
+    NBT_LAUNCHED(ctx);
+    k_idw_combine<<<(n_q + 127) / 128, 128, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), E.m, n_q, normalize,
+                                                               d_out);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }

@@ -33,8 +33,8 @@ nbt_status cuda_fail(cudaError_t e, const char *what);
     } while (0)
 
 // Thickness of the sentinel shell around the stored grid (k_map.cu); bounds the
-// walk's speculative look-ahead (k_id.cu kBatch <= kBorder).
-constexpr int kBorder = 8;
+// walk's speculative look-ahead (k_id.cu: batch size, twice that when pipelined).
+constexpr int kBorder = 16;
 
 // ----------------------------------------------------------- buffers
 
@@ -90,6 +90,7 @@ struct nbt_ctx_s {
     int *d_err = nullptr;             // device-side validation status (nbt_status value)
     int *h_err = nullptr;             // pinned mirror
     int trace_blocks_per_sm = 0;      // cached occupancy of the trace kernel
+    int trace_variant_cached = -1;
     // scratch
     nbt::DevBuf persp;                // staged perspective origins (n x 3 f64)
     nbt::DevBuf frames;               // per-perspective Q16 frames
@@ -98,7 +99,7 @@ struct nbt_ctx_s {
     nbt::DevBuf out_tmp;              // device staging for host outputs
     nbt::DevBuf deltas;               // staged map deltas
     nbt::DevBuf keys, keys_alt, cub_tmp;
-    nbt::DevBuf queries, qout;
+    nbt::DevBuf queries, qout, idw_tmp;
     nbt::DevBuf dbg;                  // debug entry points
     nbt::HostStage stage_in[3];
     nbt::HostStage stage_out;

@@ -287,7 +287,7 @@ void nbt_ctx_destroy(nbt_ctx ctx)
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf *bufs[] = {&ctx->persp, &ctx->frames, &ctx->totals, &ctx->counter, &ctx->out_tmp, &ctx->deltas,
-                      &ctx->keys, &ctx->keys_alt, &ctx->cub_tmp, &ctx->queries, &ctx->qout, &ctx->dbg};
+                      &ctx->keys, &ctx->keys_alt, &ctx->cub_tmp, &ctx->queries, &ctx->qout, &ctx->idw_tmp, &ctx->dbg};
     for (DevBuf *b : bufs) b->release();
     for (auto &st : ctx->stage_in) st.release();
     for (auto &v : ctx->prof.pending)
@@ -320,7 +320,7 @@ static nbt_status check_desc(const nbt_map_desc *d)
     if (d->nx < 1 || d->ny < 1 || d->nz < 1 || d->nx > 16384 || d->ny > 16384 || d->nz > 16384)
         return fail(NBT_ERR_INVALID_ARG, "map extents must be in [1, 16384]");
     uint64_t pad = (uint64_t)(d->nx + 2 * kBorder) * (d->ny + 2 * kBorder) * (d->nz + 2 * kBorder);
-    if (pad >= (1ull << 32)) return fail(NBT_ERR_INVALID_ARG, "(nx+16)(ny+16)(nz+16) must be < 2^32");
+    if (pad >= (1ull << 32)) return fail(NBT_ERR_INVALID_ARG, "(nx+32)(ny+32)(nz+32) must be < 2^32");
     if (!(d->voxel_size > 0) || !isfinite(d->voxel_size)) return fail(NBT_ERR_INVALID_ARG, "voxel_size must be > 0");
     if (!finite3(d->origin)) return fail(NBT_ERR_INVALID_ARG, "origin must be finite");
     for (int k = 0; k < 3; ++k)

@@ -403,7 +403,10 @@ def test_idw_matches_oracle(nbt, ctx, power_p, normalize):
     q[:5] = entries[-1][0][:5]                        # zero distance to the newest entry
     got = buf.query(q, power_p=power_p, normalize=normalize)
     want = oracle.idw_query(entries[-10:], q, power_p=power_p, normalize=normalize)
-    assert np.allclose(got, want, rtol=1e-12, atol=0)
+    if power_p == 2.0:
+        assert np.array_equal(got, want)          # same summation order, no pow: bit-exact
+    else:
+        assert np.allclose(got, want, rtol=1e-12, atol=0)
 
 
 def test_idw_empty_and_device(nbt, ctx):

@@ -1,0 +1,49 @@
+"""Time the trace kernel on config workloads (device-resident inputs, CUDA events around
+each k_id_trace launch).  Variant via NBT_TRACE_VARIANT (read by libnbt at first use).
+
+    NBT_TRACE_VARIANT=1 python tools/trace_variants.py B "C'"
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
+import paper_2503_22588_b200 as nbt
+from nbt_inputs import CONFIGS, FOV_H, FOV_V
+
+
+def run(cfg_name, reps=5):
+    cfg = CONFIGS[cfg_name]
+    dev = torch.device("cuda", 0)
+    s = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(s)
+    ctx = nbt.Ctx(0, s.cuda_stream)
+    m = nbt.Map(ctx, nbt.map_desc(cfg.n, cfg.n, cfg.n, cfg.voxel_size))
+    m.upload(cfg.map_codes())
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    persp = torch.empty((cfg.n_persp, 3), dtype=torch.float64, device=dev)
+    nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode, out=persp)
+    out = nbt.empty_cloud(cfg.n_persp, device=dev)
+    nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=out)
+    ctx.sync()
+    ctx.set_profiling(True)
+    ctx.profile_read(nbt.KERNEL_TRACE, reset=True)
+    for _ in range(reps):
+        nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=out)
+    ms, n = ctx.profile_read(nbt.KERNEL_TRACE, reset=True)
+    counts = out.counts.cpu().numpy()
+    lookups = float(counts[:, 3].sum())
+    ms /= n
+    return {"config": cfg_name, "variant": os.environ.get("NBT_TRACE_VARIANT", "0"), "trace_ms": ms,
+            "rays_per_s": cfg.rays_per_id / (ms / 1e3), "lookups_per_s": lookups / (ms / 1e3),
+            "lookups": lookups, "checksum": int(counts.sum())}
+
+
+if __name__ == "__main__":
+    for name in sys.argv[1:] or ["B"]:
+        print(json.dumps(run(name)), flush=True)
