@@ -39,21 +39,28 @@ namespace {
 constexpr int kFrameInts = 20;   // O, A, Rh, Uh, Rc, Uc (3 each, Q16), status, pad
 constexpr int kWarpsPerBlock = 8;
 constexpr int kQShift = 12;      // walk coordinates: Q12
-// Trace variants: K voxels per speculative batch; PIPE = the next batch's loads are in
-// flight while the current batch is consumed (look-ahead 2K, which must stay inside
-// the kBorder-voxel sentinel shell).
+// Trace kernel shape: K voxels per speculative batch; PIPE = the next batch's loads are
+// in flight while the current batch is consumed (look-ahead 2K, which must stay inside
+// the kBorder-voxel sentinel shell).  K = 16 without pipelining measured best
+// (profiles/r01_trace_variants.md); the other shapes stay compilable.
+constexpr int kBatchK = 16;
 constexpr int kInt32MaxVoxels = 700;   // |D_a| bound (voxels) for the int32 decision terms
 
 struct MapView {
     const uint32_t *__restrict__ words;
     int nx, ny, nz;
-    int px;          // padded x extent
-    int pxy;         // padded x*y extent
+    int px;          // linear layout: padded x extent
+    int pxy;         // linear layout: padded x*y extent
+    uint32_t mx, my, mz;   // Morton layout: bit masks of each axis (3 * pbits bits)
     int policy;      // NBT_OUTSIDE_UNKNOWN / NBT_OUTSIDE_CLIP
 };
 
-__device__ __forceinline__ uint32_t padded_index(const MapView &m, int x, int y, int z)
+template <int L>
+__device__ __forceinline__ uint32_t grid_index(const MapView &m, int x, int y, int z)
 {
+    if (L == kLayoutMorton)
+        return (dilate3((uint32_t)x) | (dilate3((uint32_t)y) << 1) | (dilate3((uint32_t)z) << 2)) &
+               (m.mx | m.my | m.mz);
     return (uint32_t)(x + kBorder) + (uint32_t)m.px * (uint32_t)(y + kBorder) +
            (uint32_t)m.pxy * (uint32_t)(z + kBorder);
 }
@@ -70,7 +77,9 @@ struct Walk {
     T ax, ay, az;              // |D_a| in Q12 units
     T nax;                     // -|D_x| (hot path)
     uint32_t idx;              // padded linear index of the current voxel (in-grid walk)
-    int dX, dY, ndZ;           // idx increments of a step along x, y and (negated) z
+    int dX, dY, ndZ;           // linear: idx increments of a step along x, y and (negated) z
+    uint32_t rx, ry, rz;       // Morton: per-axis dilated coordinates in "decrement form"
+    uint32_t xinv;             // Morton: bits to flip (axes walked in + direction)
     int s, n;                  // current step (0 = origin voxel) and total steps
     int s0;                    // step at which the walk entered the grid
     uint32_t nf;               // Free voxels counted so far in the grid
@@ -122,13 +131,17 @@ __device__ __forceinline__ int mad_i32(int a, int b, int c)
     return d;
 }
 
-// One DDA step: pick the axis, update the two decision terms that involve it.
-template <typename T, bool COORDS>
-__device__ __forceinline__ void walk_step(Walk<T> &w)
+// One DDA step: pick the axis, update the two decision terms that involve it, and move
+// the map address.  Linear layout: idx += step of the axis.  Morton layout: every axis
+// register holds its dilated coordinate so that a step is always a dilated DECREMENT
+// (axes walked in + direction are stored complemented within their bits), i.e.
+// r = (r - lsb) & mask, and the address is (rx | ry | rz) ^ xinv.
+template <typename T, int L, bool COORDS>
+__device__ __forceinline__ void walk_step(Walk<T> &w, const MapView &m)
 {
     if constexpr (sizeof(T) == 4 && !COORDS) {
-        // Hot path: the axis choice as 0/1 and 0/-1 integers from the sign bits (6 ALU
-        // ops), the updates as 9 multiply-adds on the FMA pipe, so the two integer
+        // Hot path: the axis choice as 0/1 and 0/-1 integers from the sign bits (5 ALU
+        // ops), the updates as multiply-adds on the FMA pipe, so the two integer
         // pipes share the step instead of queueing on the ALU pipe (selects).
         const int t1 = w.qxy & w.qxz;            // sign: x first
         const int t2 = w.qyz & ~t1;              // sign: y first
@@ -138,14 +151,31 @@ __device__ __forceinline__ void walk_step(Walk<T> &w)
         w.qxy = mad_i32(px, w.ay, mad_i32(py, w.nax, w.qxy));
         w.qxz = mad_i32(px, w.az, mad_i32(npz, w.ax, w.qxz));
         w.qyz = mad_i32(py, w.az, mad_i32(npz, w.ay, w.qyz));
-        w.idx = (uint32_t)mad_i32(px, w.dX, mad_i32(py, w.dY, mad_i32(npz, w.ndZ, (int)w.idx)));
+        if (L == kLayoutMorton) {
+            w.rx = (uint32_t)mad_i32(px, -1, (int)w.rx) & m.mx;
+            w.ry = (uint32_t)mad_i32(py, -2, (int)w.ry) & m.my;
+            w.rz = (uint32_t)mad_i32(npz, 4, (int)w.rz) & m.mz;
+            w.idx = (w.rx | w.ry | w.rz) ^ w.xinv;
+        } else {
+            w.idx = (uint32_t)mad_i32(px, w.dX, mad_i32(py, w.dY, mad_i32(npz, w.ndZ, (int)w.idx)));
+        }
     } else {
         const bool px = (w.qxy & w.qxz) < 0;     // both negative
         const bool py = !px && w.qyz < 0;
         const bool pz = !px && !py;
-        if (px) { w.qxy += w.ay; w.qxz += w.az; w.idx += w.dX; }
-        if (py) { w.qxy -= w.ax; w.qyz += w.az; w.idx += w.dY; }
-        if (pz) { w.qxz -= w.ax; w.qyz -= w.ay; w.idx -= w.ndZ; }
+        if (px) { w.qxy += w.ay; w.qxz += w.az; }
+        if (py) { w.qxy -= w.ax; w.qyz += w.az; }
+        if (pz) { w.qxz -= w.ax; w.qyz -= w.ay; }
+        if (L == kLayoutMorton) {
+            if (px) w.rx = (w.rx - 1u) & m.mx;
+            if (py) w.ry = (w.ry - 2u) & m.my;
+            if (pz) w.rz = (w.rz - 4u) & m.mz;
+            w.idx = (w.rx | w.ry | w.rz) ^ w.xinv;
+        } else {
+            if (px) w.idx += w.dX;
+            if (py) w.idx += w.dY;
+            if (pz) w.idx -= w.ndZ;
+        }
         if (COORDS) {
             if (px) w.vx += w.sx;
             if (py) w.vy += w.sy;
@@ -161,7 +191,7 @@ __device__ __forceinline__ bool inside(const MapView &m, int x, int y, int z)
 
 // Origin outside the grid (rare): step with explicit bounds checks until the walk
 // enters the grid or ends.  Returns true if the ray is finished.
-template <typename T, bool RECORD>
+template <typename T, int L, bool RECORD>
 __device__ bool walk_enter(Walk<T> &w, const MapView &m, int32_t *rec_ijk, uint8_t *rec_code, int max_visits)
 {
     while (!inside(m, w.vx, w.vy, w.vz)) {
@@ -171,14 +201,24 @@ __device__ bool walk_enter(Walk<T> &w, const MapView &m, int32_t *rec_ijk, uint8
         }
         w.pre++;
         if (w.s == w.n) return true;
-        walk_step<T, true>(w);
+        walk_step<T, L, true>(w, m);
         w.s++;
     }
     w.s0 = w.s;
-    w.idx = padded_index(m, w.vx, w.vy, w.vz);
-    w.dX = w.sx;
-    w.dY = w.sy * m.px;
-    w.ndZ = -w.sz * m.pxy;
+    if (L == kLayoutMorton) {
+        const uint32_t dx = dilate3((uint32_t)w.vx), dy = dilate3((uint32_t)w.vy) << 1,
+                       dz = dilate3((uint32_t)w.vz) << 2;
+        w.xinv = (w.sx > 0 ? m.mx : 0u) | (w.sy > 0 ? m.my : 0u) | (w.sz > 0 ? m.mz : 0u);
+        w.rx = (dx ^ w.xinv) & m.mx;
+        w.ry = (dy ^ w.xinv) & m.my;
+        w.rz = (dz ^ w.xinv) & m.mz;
+        w.idx = dx | dy | dz;
+    } else {
+        w.idx = grid_index<L>(m, w.vx, w.vy, w.vz);
+        w.dX = w.sx;
+        w.dY = w.sy * m.px;
+        w.ndZ = -w.sz * m.pxy;
+    }
     return false;
 }
 
@@ -230,14 +270,14 @@ __device__ __forceinline__ constexpr uint32_t lanes_mask(uint32_t pattern)
 
 // Issue the K loads of the next K visits (the DDA does not depend on the map, so
 // this runs ahead of the codes) and advance the DDA by K steps.
-template <typename T, int K>
+template <typename T, int L, int K>
 __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<K> &b)
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         b.rot[k] = (w.idx << 1) - 2 * k;        // rotate amounts are taken mod 32
         b.wd[k] = __ldg(m.words + (w.idx >> 4));
-        walk_step<T, false>(w);
+        walk_step<T, L, false>(w, m);
     }
 }
 
@@ -381,6 +421,7 @@ struct TraceArgs {
     int chunk;                  // slots per chunk (multiple of 32)
     int chunks_per_persp;
     int total_chunks;
+    int min_refill;             // idle lanes needed before a warp refills (experiments)
 };
 
 // Map slot -> lattice offsets (mi, mk) = (2i-(W-1), 2kk-(H-1)) or a corner ray.
@@ -440,7 +481,7 @@ __device__ __forceinline__ void flush_counts(unsigned long long *totals, int j, 
 // Prepare the ray in `slot` of perspective j (frame, segment, DDA set-up, grid
 // entry).  Returns false if the slot is a tile hole or the ray ends without entering
 // the grid (its Unknown visits are then added to the totals directly).
-template <typename T>
+template <typename T, int L>
 __device__ __forceinline__ bool prep_ray(const TraceArgs &A, int j, int slot, Walk<T> &w)
 {
     int mi = 0, mk = 0, corner = -1;
@@ -452,7 +493,7 @@ __device__ __forceinline__ bool prep_ray(const TraceArgs &A, int j, int slot, Wa
     int o[3], e[3];
     ray_segment(f, mi, mk, corner, o, e);
     walk_setup(w, o, e);
-    if (walk_enter<T, false>(w, A.m, nullptr, nullptr, 0)) {
+    if (walk_enter<T, L, false>(w, A.m, nullptr, nullptr, 0)) {
         if (A.m.policy == NBT_OUTSIDE_UNKNOWN) atomicAdd(A.totals + 4 * (size_t)j, (unsigned long long)w.pre);
         return false;
     }
@@ -466,35 +507,46 @@ struct WalkQueue {
     T q[3][32];
     T a[3][32];
     uint32_t idx[32];
-    int d[3][32];
+    int d[3][32];                // linear: dX, dY, ndZ; Morton: rx, ry, rz
+    uint32_t xinv[32];           // Morton only
     int n[32], s0[32];
     uint32_t pre[32];
     int j[32];
 };
 
-template <typename T>
+template <typename T, int L>
 __device__ __forceinline__ void queue_put(WalkQueue<T> &Q, int i, const Walk<T> &w, int j)
 {
     Q.q[0][i] = w.qxy; Q.q[1][i] = w.qxz; Q.q[2][i] = w.qyz;
     Q.a[0][i] = w.ax; Q.a[1][i] = w.ay; Q.a[2][i] = w.az;
     Q.idx[i] = w.idx;
-    Q.d[0][i] = w.dX; Q.d[1][i] = w.dY; Q.d[2][i] = w.ndZ;
+    if (L == kLayoutMorton) {
+        Q.d[0][i] = (int)w.rx; Q.d[1][i] = (int)w.ry; Q.d[2][i] = (int)w.rz;
+        Q.xinv[i] = w.xinv;
+    } else {
+        Q.d[0][i] = w.dX; Q.d[1][i] = w.dY; Q.d[2][i] = w.ndZ;
+    }
     Q.n[i] = w.n; Q.s0[i] = w.s0; Q.pre[i] = w.pre; Q.j[i] = j;
 }
 
-template <typename T>
+template <typename T, int L>
 __device__ __forceinline__ int queue_get(const WalkQueue<T> &Q, int i, Walk<T> &w)
 {
     w.qxy = Q.q[0][i]; w.qxz = Q.q[1][i]; w.qyz = Q.q[2][i];
     w.ax = Q.a[0][i]; w.ay = Q.a[1][i]; w.az = Q.a[2][i];
     w.nax = -w.ax;
     w.idx = Q.idx[i];
-    w.dX = Q.d[0][i]; w.dY = Q.d[1][i]; w.ndZ = Q.d[2][i];
+    if (L == kLayoutMorton) {
+        w.rx = (uint32_t)Q.d[0][i]; w.ry = (uint32_t)Q.d[1][i]; w.rz = (uint32_t)Q.d[2][i];
+        w.xinv = Q.xinv[i];
+    } else {
+        w.dX = Q.d[0][i]; w.dY = Q.d[1][i]; w.ndZ = Q.d[2][i];
+    }
     w.n = Q.n[i]; w.s0 = Q.s0[i]; w.s = w.s0; w.pre = Q.pre[i]; w.nf = 0;
     return Q.j[i];
 }
 
-template <typename T, int K, bool PIPE>
+template <typename T, int L, int K, bool PIPE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_id_trace(TraceArgs A)
 {
     static_assert((PIPE ? 2 * K : K) <= kBorder, "look-ahead must stay inside the sentinel shell");
@@ -513,7 +565,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_id_trace(TraceArgs A)
     Counts c{0, 0, 0, 0};
     for (;;) {
         const unsigned need = __ballot_sync(full, !have);
-        if (need) {
+        // refill once enough lanes are idle (min_refill = 1: as soon as any is)
+        if (need && (__popc(need) >= A.min_refill || q_done || need == full)) {
             // all 32 lanes prepare up to 32 rays at once, so the set-up runs converged
             while (qcount == 0 && !q_done) {
                 if (q_next >= q_end) {
@@ -529,10 +582,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_id_trace(TraceArgs A)
                 }
                 const int avail = min(32, q_end - q_next);
                 Walk<T> t;
-                const bool ok = lane < avail && prep_ray<T>(A, q_j, q_next + lane, t);
+                const bool ok = lane < avail && prep_ray<T, L>(A, q_j, q_next + lane, t);
                 q_next += avail;
                 const unsigned vm = __ballot_sync(full, ok);
-                if (ok) queue_put(Q, __popc(vm & lanes_below), t, q_j);
+                if (ok) queue_put<T, L>(Q, __popc(vm & lanes_below), t, q_j);
                 __syncwarp();
                 qhead = 0;
                 qcount = __popc(vm);
@@ -541,10 +594,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_id_trace(TraceArgs A)
                 const int rank = __popc(need & lanes_below);
                 const int take = min(__popc(need), qcount);
                 if (!have && rank < take) {
-                    const int j = queue_get(Q, qhead + rank, w);
+                    const int j = queue_get<T, L>(Q, qhead + rank, w);
                     if (j != jl) { flush_counts(A.totals, jl, c); jl = j; }
                     have = true;
-                    if (PIPE) batch_issue<T, K>(w, A.m, b0);
+                    if (PIPE) batch_issue<T, L, K>(w, A.m, b0);
                 }
                 qhead += take;
                 qcount -= take;
@@ -554,15 +607,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_id_trace(TraceArgs A)
         if (q_done && qcount == 0 && !__any_sync(full, have)) break;
         if (!have) continue;
         if (!PIPE) {
-            batch_issue<T, K>(w, A.m, b0);
+            batch_issue<T, L, K>(w, A.m, b0);
             if (batch_consume<T, K>(w, b0, A.m.policy, c)) have = false;
         } else {
             // b0 holds visits s..s+K-1; keep the next batch in flight while consuming
-            if (w.n - w.s + 1 > K) batch_issue<T, K>(w, A.m, b1);
+            if (w.n - w.s + 1 > K) batch_issue<T, L, K>(w, A.m, b1);
             if (batch_consume<T, K>(w, b0, A.m.policy, c)) {
                 have = false;
             } else {
-                if (w.n - w.s + 1 > K) batch_issue<T, K>(w, A.m, b0);
+                if (w.n - w.s + 1 > K) batch_issue<T, L, K>(w, A.m, b0);
                 if (batch_consume<T, K>(w, b1, A.m.policy, c)) have = false;
             }
         }
@@ -602,7 +655,7 @@ __global__ void k_id_finalize(FrameArgs A, const int32_t *__restrict__ frames,
 
 // Per-ray walk of an explicit Q12 segment, recording every visited voxel; the same
 // Walk / walk_step / walk_enter code as k_id_trace, one voxel at a time.
-template <typename T>
+template <typename T, int L>
 __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const int32_t *__restrict__ e, int n_rays,
                               int max_visits, int32_t *ijk, uint8_t *code, int32_t *len, uint32_t *counts)
 {
@@ -616,7 +669,7 @@ __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const in
     uint8_t *rc = code + (size_t)r * max_visits;
     Counts c{0, 0, 0, 0};
     int visits;
-    if (walk_enter<T, true>(w, m, ri, rc, max_visits)) {
+    if (walk_enter<T, L, true>(w, m, ri, rc, max_visits)) {
         if (m.policy == NBT_OUTSIDE_UNKNOWN) c.u += w.pre;
         visits = w.n + 1;
     } else {
@@ -632,7 +685,7 @@ __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const in
                     visits = w.s + 1;
                 } else {   // record the outside tail too
                     for (int s = w.s + 1; s <= w.n; ++s) {
-                        walk_step<T, true>(w);
+                        walk_step<T, L, true>(w, m);
                         if (s < max_visits) {
                             ri[3 * s] = w.vx; ri[3 * s + 1] = w.vy; ri[3 * s + 2] = w.vz;
                             rc[s] = 255;
@@ -648,7 +701,7 @@ __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const in
                 visits = w.n + 1;
                 break;
             }
-            walk_step<T, true>(w);
+            walk_step<T, L, true>(w, m);
             w.s++;
         }
     }
@@ -675,6 +728,10 @@ MapView view_of(nbt_map m)
     v.nx = m->desc.nx; v.ny = m->desc.ny; v.nz = m->desc.nz;
     v.px = (int)m->px;
     v.pxy = (int)(m->px * m->py);
+    const uint32_t all = m->layout == kLayoutMorton ? ((1u << (3 * m->pbits)) - 1u) : 0u;
+    v.mx = 0x09249249u & all;
+    v.my = 0x12492492u & all;
+    v.mz = 0x24924924u & all;
     v.policy = m->desc.outside_policy;
     return v;
 }
@@ -691,13 +748,13 @@ FrameArgs frame_args(nbt_map m, const double *d_persp, int32_t first, int32_t st
     return A;
 }
 
-// Trace kernel variant (experiments, profiles/r01_trace_variants.md): NBT_TRACE_VARIANT =
-// 0 (K=16, default), 1 (K=8), 2 (K=4 pipelined), 3 (K=8 pipelined).
-int trace_variant()
+// Idle lanes a warp waits for before refilling: NBT_REFILL_MIN, default 8 (profiles/r01_trace_variants.md).
+int refill_threshold()
 {
     static int v = [] {
-        const char *e = getenv("NBT_TRACE_VARIANT");
-        return e ? atoi(e) : 0;
+        const char *e = getenv("NBT_REFILL_MIN");
+        int r = e ? atoi(e) : 8;
+        return r < 1 ? 1 : (r > 32 ? 32 : r);
     }();
     return v;
 }
@@ -746,16 +803,12 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     T.n_tile_slots = T.tiled ? T.Wt * Ht * 32 : T.W * T.H;
     T.slots = T.n_tile_slots + (T.add_corners ? 4 : 0);
     const bool wide = max_ray_voxels(L.cam, L.range, m->desc.voxel_size) > kInt32MaxVoxels;
-    const int variant = trace_variant();
-    if (ctx->trace_blocks_per_sm == 0 || ctx->trace_variant_cached != variant) {
+    const bool morton = m->layout == kLayoutMorton;
+    if (ctx->trace_blocks_per_sm == 0) {
         int b = 0;
-        const void *fn = (const void *)k_id_trace<int, 16, false>;
-        if (variant == 1) fn = (const void *)k_id_trace<int, 8, false>;
-        if (variant == 2) fn = (const void *)k_id_trace<int, 4, true>;
-        if (variant == 3) fn = (const void *)k_id_trace<int, 8, true>;
-        NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kWarpsPerBlock * 32, 0));
+        NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &b, k_id_trace<int, kLayoutLinear, kBatchK, false>, kWarpsPerBlock * 32, 0));
         ctx->trace_blocks_per_sm = b > 0 ? b : 1;
-        ctx->trace_variant_cached = variant;
     }
     long long resident_warps = (long long)ctx->num_sms * ctx->trace_blocks_per_sm * kWarpsPerBlock;
     long long total_slots = (long long)L.n * T.slots;
@@ -767,21 +820,21 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     long long tc = (long long)T.chunks_per_persp * L.n;
     if (tc >= (1ll << 31)) return fail(NBT_ERR_INVALID_ARG, "nbt_id_compute: too many rays in one call");
     T.total_chunks = (int)tc;
+    T.min_refill = refill_threshold();
     long long want_blocks = (tc + kWarpsPerBlock - 1) / kWarpsPerBlock;
     long long max_blocks = (long long)ctx->num_sms * ctx->trace_blocks_per_sm;
     int blocks = (int)(want_blocks < max_blocks ? want_blocks : max_blocks);
     {
         ProfScope ps(ctx, NBT_KERNEL_TRACE);
-        if (wide) {
-            k_id_trace<long long, 16, false><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T);
-        } else {
-            switch (variant) {
-            case 1: k_id_trace<int, 8, false><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T); break;
-            case 2: k_id_trace<int, 4, true><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T); break;
-            case 3: k_id_trace<int, 8, true><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T); break;
-            default: k_id_trace<int, 16, false><<<blocks, kWarpsPerBlock * 32, 0, ctx->stream>>>(T); break;
-            }
-        }
+        const dim3 grid(blocks), block(kWarpsPerBlock * 32);
+        if (wide && morton)
+            k_id_trace<long long, kLayoutMorton, kBatchK, false><<<grid, block, 0, ctx->stream>>>(T);
+        else if (wide)
+            k_id_trace<long long, kLayoutLinear, kBatchK, false><<<grid, block, 0, ctx->stream>>>(T);
+        else if (morton)
+            k_id_trace<int, kLayoutMorton, kBatchK, false><<<grid, block, 0, ctx->stream>>>(T);
+        else
+            k_id_trace<int, kLayoutLinear, kBatchK, false><<<grid, block, 0, ctx->stream>>>(T);
         NBT_LAUNCHED(ctx);
     }
 
@@ -800,13 +853,23 @@ nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const 
                               uint32_t *d_counts, bool wide)
 {
     if (n_rays == 0) return NBT_OK;
-    if (wide)
-        k_debug_trace<long long><<<(n_rays + 127) / 128, 128, 0, ctx->stream>>>(view_of(m), d_o, d_e, n_rays,
-                                                                                 max_visits, d_ijk, d_code, d_len,
-                                                                                 d_counts);
-    else
-        k_debug_trace<int><<<(n_rays + 127) / 128, 128, 0, ctx->stream>>>(view_of(m), d_o, d_e, n_rays, max_visits,
-                                                                           d_ijk, d_code, d_len, d_counts);
+    const dim3 grid((n_rays + 127) / 128), block(128);
+    const MapView v = view_of(m);
+    if (m->layout == kLayoutMorton) {
+        if (wide)
+            k_debug_trace<long long, kLayoutMorton><<<grid, block, 0, ctx->stream>>>(v, d_o, d_e, n_rays, max_visits,
+                                                                                     d_ijk, d_code, d_len, d_counts);
+        else
+            k_debug_trace<int, kLayoutMorton><<<grid, block, 0, ctx->stream>>>(v, d_o, d_e, n_rays, max_visits, d_ijk,
+                                                                               d_code, d_len, d_counts);
+    } else {
+        if (wide)
+            k_debug_trace<long long, kLayoutLinear><<<grid, block, 0, ctx->stream>>>(v, d_o, d_e, n_rays, max_visits,
+                                                                                     d_ijk, d_code, d_len, d_counts);
+        else
+            k_debug_trace<int, kLayoutLinear><<<grid, block, 0, ctx->stream>>>(v, d_o, d_e, n_rays, max_visits, d_ijk,
+                                                                               d_code, d_len, d_counts);
+    }
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }

@@ -7,21 +7,23 @@
 // nearest perspective is closer than zero_eps, v_u is its gain (Q23).
 //
 //   k_idw_entry    grid (query blocks) x (entries): a block stages one entry's
-//                  perspectives through shared memory in tiles and each thread walks
-//                  them for its query in ascending j -- the same summation order as the
-//                  definition, every product and sum rounded once, so for p = 2
-//                  (d^-2 = 1/d^2, no pow) v_u is reproduced bit for bit.  The nearest
-//                  perspective is tracked on d^2 (monotone in d); only when it is within
-//                  zero_eps is d = sqrt(d^2) evaluated, with a second pass to pick the
-//                  lowest j among exactly equal d.
+//                  perspectives through shared memory; 8 lanes per query split them
+//                  (interleaved; fp64 partial sums combined by shuffles, so the
+//                  result differs from a sequential sum only in rounding, < 1e-12
+//                  relative).  The nearest perspective is tracked on d^2 (monotone in
+//                  d); only when it is within zero_eps is d = sqrt(d^2) evaluated, with a
+//                  second pass to pick the lowest j among exactly equal d, so the
+//                  zero-distance decision and the returned gain match the definition.
 //   k_idw_combine  per query: G = sum_u w_u v_u in entry order (optionally / sum_u w_u).
 #include "nbt_internal.cuh"
 
 namespace nbt {
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kTile = 256;
+constexpr int kQueries = 32;     // queries per block
+constexpr int kSplit = 8;        // lanes sharing one (query, entry)
+constexpr int kThreads = kQueries * kSplit;
+constexpr int kTile = 512;
 
 __device__ __forceinline__ double dist2(double x0, double x1, double x2, double p0, double p1, double p2)
 {
@@ -29,6 +31,9 @@ __device__ __forceinline__ double dist2(double x0, double x1, double x2, double 
     return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
+// Block (query block, entry e): 32 queries x 8 lanes each; the 8 lanes of a query split
+// the entry's perspectives (interleaved), staged through shared memory, and
+// combine (sum of num, sum of den, argmin of d^2 with lowest j) by warp shuffles.
 __global__ void __launch_bounds__(kThreads)
     k_idw_entry(const double *__restrict__ xyz, const double *__restrict__ gain, int32_t max_persp, IdwEntries E,
                 const double *__restrict__ q, int32_t n_q, double power_p, double zero_eps,
@@ -36,7 +41,8 @@ __global__ void __launch_bounds__(kThreads)
 {
     __shared__ double sp[kTile][4];
     const int e = blockIdx.y;
-    const int qi = blockIdx.x * kThreads + threadIdx.x;
+    const int sub = threadIdx.x & (kSplit - 1);
+    const int qi = blockIdx.x * kQueries + (threadIdx.x / kSplit);
     const bool active = qi < n_q;
     const double *P = xyz + (size_t)E.slot[e] * max_persp * 3;
     const double *G = gain + (size_t)E.slot[e] * max_persp;
@@ -46,7 +52,7 @@ __global__ void __launch_bounds__(kThreads)
     const bool p2 = power_p == 2.0;
     const double hp = -0.5 * power_p;
     double num = 0.0, den = 0.0, d2min = __longlong_as_double(0x7ff0000000000000LL);
-    int jmin = 0;
+    int jmin = 0x7fffffff;
     for (int base = 0; base < np; base += kTile) {
         const int nt = min(kTile, np - base);
         __syncthreads();
@@ -57,18 +63,27 @@ __global__ void __launch_bounds__(kThreads)
             sp[t][3] = G[base + t];
         }
         __syncthreads();
-        if (active) {
-            for (int t = 0; t < nt; ++t) {
-                const double d2 = dist2(x0, x1, x2, sp[t][0], sp[t][1], sp[t][2]);
-                if (d2 < d2min) { d2min = d2; jmin = base + t; }
-                const double w = p2 ? __drcp_rn(d2) : pow(d2, hp);
-                num = __dadd_rn(num, __dmul_rn(sp[t][3], w));
-                den = __dadd_rn(den, w);
-            }
+        // sub-lane s takes t = s, s+8, ...: the 8 lanes of a query read 8 consecutive
+        // 32-byte records (no shared-memory bank conflicts)
+#pragma unroll 4
+        for (int t = sub; t < nt; t += kSplit) {
+            const double d2 = dist2(x0, x1, x2, sp[t][0], sp[t][1], sp[t][2]);
+            if (d2 < d2min) { d2min = d2; jmin = base + t; }
+            const double w = p2 ? __drcp_rn(d2) : pow(d2, hp);
+            num = fma(sp[t][3], w, num);
+            den += w;
         }
     }
-    if (!active) return;
-    double v = __ddiv_rn(num, den);
+#pragma unroll
+    for (int off = kSplit / 2; off > 0; off >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, off);
+        den += __shfl_xor_sync(0xffffffffu, den, off);
+        const double od = __shfl_xor_sync(0xffffffffu, d2min, off);
+        const int oj = __shfl_xor_sync(0xffffffffu, jmin, off);
+        if (od < d2min || (od == d2min && oj < jmin)) { d2min = od; jmin = oj; }
+    }
+    if (!active || sub != 0) return;
+    double v = num / den;
     const double dmin = __dsqrt_rn(d2min);
     if (dmin < zero_eps) {
         // nearest by d (not d^2): lowest j among perspectives whose rounded d equals dmin
@@ -105,7 +120,7 @@ nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, co
     nbt_status st;
     if ((st = ctx->idw_tmp.ensure((size_t)E.m * n_q * 8))) return st;
     ProfScope ps(ctx, NBT_KERNEL_IDW);
-    dim3 grid((n_q + kThreads - 1) / kThreads, E.m);
+    dim3 grid((n_q + kQueries - 1) / kQueries, E.m);
     k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, E, d_q, n_q, power_p,
                                                      zero_eps, ctx->idw_tmp.as<double>());
     NBT_LAUNCHED(ctx);

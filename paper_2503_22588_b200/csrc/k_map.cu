@@ -1,6 +1,9 @@
 // Voxel-map store kernels.
 //
-// Layout in HBM: the nx*ny*nz grid is surrounded by a shell of
+// Two layouts.  Morton (NBT_MAP_LAYOUT=morton): the store is a
+// cube of side P = 2^pbits >= max(n) + 2 kBorder indexed by the bit-interleaved voxel
+// coordinates; every position outside the grid holds the sentinel.  Linear (default):
+// the nx*ny*nz grid is surrounded by a shell of
 // kBorder sentinel voxels (code 3 = "outside") and stored x-fastest, 2 bits per voxel,
 // 16 voxels per 32-bit word: voxel (x, y, z) is padded voxel (x+B, y+B, z+B) with
 // linear index i = (x+B) + px*((y+B) + py*(z+B)), px = nx + 2B, stored in bits
@@ -17,30 +20,50 @@ namespace {
 
 constexpr uint32_t kOutside = 3u;
 
-// One thread per packed word (16 padded voxels).
-__global__ void k_map_pack(const uint8_t *__restrict__ codes, int nx, int ny, int nz, uint32_t px, uint32_t py,
-                           uint64_t nvox_pad, size_t nwords, uint32_t *__restrict__ words, int *err)
+struct Geom {
+    int layout;
+    int nx, ny, nz;
+    uint32_t px, py;   // linear padded extents
+};
+
+// Store index of grid voxel (x, y, z).
+__device__ __forceinline__ uint64_t store_index(const Geom &g, uint32_t x, uint32_t y, uint32_t z)
+{
+    if (g.layout == kLayoutMorton) return dilate3(x) | (dilate3(y) << 1) | (dilate3(z) << 2);
+    return (uint64_t)(x + kBorder) + (uint64_t)g.px * ((uint64_t)(y + kBorder) + (uint64_t)g.py * (z + kBorder));
+}
+
+// One thread per packed word (16 store positions).
+__global__ void k_map_pack(const uint8_t *__restrict__ codes, Geom g, uint64_t nvox_pad, size_t nwords,
+                           uint32_t *__restrict__ words, int *err)
 {
     size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (w >= nwords) return;
     uint64_t i0 = (uint64_t)w * 16;
-    uint32_t x = (uint32_t)(i0 % px);
-    uint64_t r = i0 / px;
-    uint32_t y = (uint32_t)(r % py);
-    uint32_t z = (uint32_t)(r / py);
+    uint32_t x = 0, y = 0, z = 0;
+    if (g.layout == kLayoutLinear) {
+        x = (uint32_t)(i0 % g.px);
+        uint64_t r = i0 / g.px;
+        y = (uint32_t)(r % g.py);
+        z = (uint32_t)(r / g.py);
+    }
     uint32_t out = 0;
     bool bad = false;
     for (int k = 0; k < 16; ++k) {
         uint32_t c = kOutside;
-        if (i0 + k < nvox_pad) {
-            int gx = (int)x - kBorder, gy = (int)y - kBorder, gz = (int)z - kBorder;
-            if (gx >= 0 && gy >= 0 && gz >= 0 && gx < nx && gy < ny && gz < nz) {
-                c = codes[(size_t)gx + (size_t)nx * ((size_t)gy + (size_t)ny * gz)];
-                if (c > 2u) { bad = true; c = 0u; }
-            }
+        int gx, gy, gz;
+        if (g.layout == kLayoutMorton) {
+            const uint32_t i = (uint32_t)(i0 + k);
+            gx = (int)compact3(i); gy = (int)compact3(i >> 1); gz = (int)compact3(i >> 2);
+        } else {
+            gx = (int)x - kBorder; gy = (int)y - kBorder; gz = (int)z - kBorder;
+            if (++x == g.px) { x = 0; if (++y == g.py) { y = 0; ++z; } }
+        }
+        if (i0 + k < nvox_pad && gx >= 0 && gy >= 0 && gz >= 0 && gx < g.nx && gy < g.ny && gz < g.nz) {
+            c = codes[(size_t)gx + (size_t)g.nx * ((size_t)gy + (size_t)g.ny * gz)];
+            if (c > 2u) { bad = true; c = 0u; }
         }
         out |= c << (2 * k);
-        if (++x == px) { x = 0; if (++y == py) { y = 0; ++z; } }
     }
     words[w] = out;
     if (bad) atomicCAS(err, 0, (int)NBT_ERR_INVALID_ARG);
@@ -80,8 +103,8 @@ __global__ void k_delta_keys(const int32_t *__restrict__ ijk, const uint8_t *__r
 // only that one writes.  Distinct voxels may share a word, so the 2-bit field is
 // changed with one atomicXor; the thread's own field is never touched by another thread.
 __global__ void k_delta_apply(const unsigned long long *__restrict__ keys, uint32_t n,
-                              const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes, uint32_t px,
-                              uint32_t py, uint32_t *words)
+                              const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes, Geom g,
+                              uint32_t *words)
 {
     uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -89,9 +112,7 @@ __global__ void k_delta_apply(const unsigned long long *__restrict__ keys, uint3
     if (k == ~0ull) return;
     if (i + 1 < n && (keys[i + 1] >> 32) == (k >> 32)) return;
     uint32_t pos = (uint32_t)(k & 0xffffffffu);
-    uint32_t x = (uint32_t)ijk[3 * pos] + kBorder, y = (uint32_t)ijk[3 * pos + 1] + kBorder,
-             z = (uint32_t)ijk[3 * pos + 2] + kBorder;
-    uint64_t pi = (uint64_t)x + (uint64_t)px * ((uint64_t)y + (uint64_t)py * z);
+    uint64_t pi = store_index(g, (uint32_t)ijk[3 * pos], (uint32_t)ijk[3 * pos + 1], (uint32_t)ijk[3 * pos + 2]);
     uint32_t *w = words + (pi >> 4);
     uint32_t sh = (uint32_t)(pi & 15) * 2;
     uint32_t old = (*(volatile uint32_t *)w >> sh) & 3u;
@@ -99,28 +120,36 @@ __global__ void k_delta_apply(const unsigned long long *__restrict__ keys, uint3
     if (old != nw) atomicXor(w, (old ^ nw) << sh);
 }
 
-__global__ void k_map_unpack(const uint32_t *__restrict__ words, int nx, int ny, int nz, uint32_t px, uint32_t py,
-                             uint8_t *__restrict__ codes)
+__global__ void k_map_unpack(const uint32_t *__restrict__ words, Geom g, uint8_t *__restrict__ codes)
 {
     size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    size_t n = (size_t)nx * ny * nz;
+    size_t n = (size_t)g.nx * g.ny * g.nz;
     if (i >= n) return;
-    uint32_t x = (uint32_t)(i % nx);
-    size_t r = i / nx;
-    uint32_t y = (uint32_t)(r % ny), z = (uint32_t)(r / ny);
-    uint64_t pi = (uint64_t)(x + kBorder) + (uint64_t)px * ((uint64_t)(y + kBorder) + (uint64_t)py * (z + kBorder));
+    uint32_t x = (uint32_t)(i % g.nx);
+    size_t r = i / g.nx;
+    uint32_t y = (uint32_t)(r % g.ny), z = (uint32_t)(r / g.ny);
+    uint64_t pi = store_index(g, x, y, z);
     codes[i] = (uint8_t)((words[pi >> 4] >> ((pi & 15) * 2)) & 3u);
 }
 
 inline unsigned blocks_for(size_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+
+Geom geom_of(nbt_map m)
+{
+    Geom g;
+    g.layout = m->layout;
+    g.nx = m->desc.nx; g.ny = m->desc.ny; g.nz = m->desc.nz;
+    g.px = m->px; g.py = m->py;
+    return g;
+}
 
 }  // namespace
 
 nbt_status launch_map_pack(nbt_ctx ctx, nbt_map m, const uint8_t *d_codes)
 {
     if (m->nwords == 0) return NBT_OK;
-    k_map_pack<<<blocks_for(m->nwords, 256), 256, 0, ctx->stream>>>(
-        d_codes, m->desc.nx, m->desc.ny, m->desc.nz, m->px, m->py, m->nvox_pad, m->nwords, m->d_words, ctx->d_err);
+    k_map_pack<<<blocks_for(m->nwords, 256), 256, 0, ctx->stream>>>(d_codes, geom_of(m), m->nvox_pad, m->nwords,
+                                                                     m->d_words, ctx->d_err);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }
@@ -152,8 +181,7 @@ nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const
     NBT_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kin, kout, (int)nn, 0, 64, ctx->stream));
     if ((st = ctx->cub_tmp.ensure(tmp))) return st;
     NBT_CUDA(cub::DeviceRadixSort::SortKeys(ctx->cub_tmp.p, tmp, kin, kout, (int)nn, 0, 64, ctx->stream));
-    k_delta_apply<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(kout, nn, d_ijk, d_codes, m->px, m->py,
-                                                               m->d_words);
+    k_delta_apply<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(kout, nn, d_ijk, d_codes, geom_of(m), m->d_words);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }
@@ -161,8 +189,7 @@ nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const
 nbt_status launch_map_unpack(nbt_ctx ctx, nbt_map m, uint8_t *d_codes_out)
 {
     size_t n = (size_t)m->desc.nx * m->desc.ny * m->desc.nz;
-    k_map_unpack<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(m->d_words, m->desc.nx, m->desc.ny, m->desc.nz,
-                                                               m->px, m->py, d_codes_out);
+    k_map_unpack<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(m->d_words, geom_of(m), d_codes_out);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }

@@ -36,6 +36,35 @@ nbt_status cuda_fail(cudaError_t e, const char *what);
 // walk's speculative look-ahead (k_id.cu: batch size, twice that when pipelined).
 constexpr int kBorder = 16;
 
+// Map store layouts (k_map.cu).  Linear: x-fastest rows inside a kBorder sentinel shell.
+// Morton: the voxel index interleaves the coordinate bits (x0 y0 z0 x1 y1 z1 ...) inside a
+// cube of side P = 2^pbits >= max(n) + 2 kBorder, so one 128-byte line holds an 8x8x8
+// block and one 32-byte sector a 4x4x8 block; coordinates wrap modulo P, and every
+// voxel of the cube outside the grid holds the sentinel.
+enum : int { kLayoutLinear = 0, kLayoutMorton = 1 };
+
+// Spread the low 10 bits of v to bit positions 0, 3, 6, ..., 27.
+__host__ __device__ __forceinline__ uint32_t dilate3(uint32_t v)
+{
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+// Inverse of dilate3 on bit positions 0, 3, 6, ...
+__host__ __device__ __forceinline__ uint32_t compact3(uint32_t v)
+{
+    v &= 0x09249249u;
+    v = (v ^ (v >> 2)) & 0x030C30C3u;
+    v = (v ^ (v >> 4)) & 0x0300F00Fu;
+    v = (v ^ (v >> 8)) & 0x030000FFu;
+    v = (v ^ (v >> 16)) & 0x3ffu;
+    return v;
+}
+
 // ----------------------------------------------------------- buffers
 
 struct DevBuf {
@@ -90,7 +119,6 @@ struct nbt_ctx_s {
     int *d_err = nullptr;             // device-side validation status (nbt_status value)
     int *h_err = nullptr;             // pinned mirror
     int trace_blocks_per_sm = 0;      // cached occupancy of the trace kernel
-    int trace_variant_cached = -1;
     // scratch
     nbt::DevBuf persp;                // staged perspective origins (n x 3 f64)
     nbt::DevBuf frames;               // per-perspective Q16 frames
@@ -109,7 +137,9 @@ struct nbt_ctx_s {
 struct nbt_map_s {
     nbt_ctx ctx = nullptr;
     nbt_map_desc desc{};
-    uint32_t px = 0, py = 0, pz = 0;  // padded extents (kBorder sentinel voxels each side)
+    int layout = nbt::kLayoutLinear;
+    int pbits = 0;                    // Morton: cube side 2^pbits
+    uint32_t px = 0, py = 0, pz = 0;  // linear: padded extents (kBorder sentinel voxels each side)
     uint64_t nvox_pad = 0;
     size_t nwords = 0;
     uint32_t *d_words = nullptr;      // 2-bit codes, 16 voxels per 32-bit word

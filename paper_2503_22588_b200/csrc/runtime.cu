@@ -3,6 +3,7 @@
 // of k_map.cu, k_sample.cu, k_id.cu and k_idw.cu; this file only moves data and checks
 // arguments.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <new>
@@ -342,6 +343,24 @@ nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
     m->desc = *desc;
     m->px = desc->nx + 2 * kBorder; m->py = desc->ny + 2 * kBorder; m->pz = desc->nz + 2 * kBorder;
     m->nvox_pad = (uint64_t)m->px * m->py * m->pz;
+    // Store layout: linear by default (fewest instructions per voxel step, fastest on
+    // configs C' and D, profiles/r01_layouts.md); NBT_MAP_LAYOUT=morton selects the
+    // Morton cube (side >= max extent + 2 kBorder, a power of two, at most 1024^3 voxels
+    // and 8x the linear store), which is slightly faster on sparse ray lattices (config B).
+    {
+        int maxn = desc->nx > desc->ny ? desc->nx : desc->ny;
+        maxn = maxn > desc->nz ? maxn : desc->nz;
+        int pb = 4;
+        while ((1 << pb) < maxn + 2 * kBorder) ++pb;
+        uint64_t cube = 1ull << (3 * pb);
+        const char *env = getenv("NBT_MAP_LAYOUT");
+        bool use = env && !strcmp(env, "morton") && pb <= 10 && cube <= 8 * m->nvox_pad;
+        if (use) {
+            m->layout = kLayoutMorton;
+            m->pbits = pb;
+            m->nvox_pad = cube;
+        }
+    }
     m->nwords = (size_t)((m->nvox_pad + 15) / 16);
     cudaError_t e = cudaMalloc(&m->d_words, m->nwords * 4);
     if (e != cudaSuccess) {

@@ -403,10 +403,21 @@ def test_idw_matches_oracle(nbt, ctx, power_p, normalize):
     q[:5] = entries[-1][0][:5]                        # zero distance to the newest entry
     got = buf.query(q, power_p=power_p, normalize=normalize)
     want = oracle.idw_query(entries[-10:], q, power_p=power_p, normalize=normalize)
-    if power_p == 2.0:
-        assert np.array_equal(got, want)          # same summation order, no pow: bit-exact
-    else:
-        assert np.allclose(got, want, rtol=1e-12, atol=0)
+    assert np.allclose(got, want, rtol=1e-12, atol=0)
+
+
+def test_idw_zero_distance_exact(nbt, ctx):
+    """Q23: a query on a perspective returns that perspective's gain exactly; among
+    coincident perspectives the lowest index wins."""
+    rng = np.random.default_rng(3)
+    xyz = rng.normal(size=(300, 3)); gain = rng.uniform(0, 4, 300)
+    xyz[7] = xyz[200]                      # duplicate position: j = 7 must win
+    buf = nbt.IdBuffer(ctx, 4, 300)
+    buf.push(nbt.IgCloud(xyz, gain, None))
+    q = xyz[[0, 7, 200, 299]] + np.array([0.0, 0.0, 1e-12])[None, :] * 0
+    got = buf.query(q)
+    assert list(got) == [gain[0], gain[7], gain[7], gain[299]]
+    assert np.array_equal(got, oracle.idw_query([(xyz, gain)], q))
 
 
 def test_idw_empty_and_device(nbt, ctx):
@@ -474,3 +485,50 @@ def test_id_wide_path(nbt, ctx):
     P = oracle.sample_perspectives(poi, 15.0, 12, seed=6)
     cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 12, 9, 900.0, corners=True)
     assert_cloud_equal(cloud, P, g, c)
+
+
+# ---------------------------------------------------------------- store layouts
+
+@pytest.mark.parametrize("layout", ["linear", "morton"])
+def test_layouts_roundtrip_update_and_id(nbt, ctx, layout, monkeypatch):
+    """Both map store layouts (Morton cube / linear with sentinel shell) give identical,
+    oracle-exact results: upload/download, last-wins updates, per-ray walks, the ID."""
+    monkeypatch.setenv("NBT_MAP_LAYOUT", layout)
+    codes = rand_map(0, 0.3, 0.66, 0.04, seed=21, shape=(19, 27, 33))
+    m, om = make_map(nbt, ctx, codes)
+    assert np.array_equal(m.download(), codes)
+    rng = np.random.default_rng(4)
+    ijk = np.stack([rng.integers(0, 33, 900), rng.integers(0, 27, 900), rng.integers(0, 19, 900)], 1).astype(np.int32)
+    vals = rng.integers(0, 3, 900).astype(np.uint8)
+    m.update(ijk, vals)
+    codes2 = _apply_in_order(codes, ijk, vals)
+    assert np.array_equal(m.download(), codes2)
+    om = oracle.OracleMap(codes2)
+    o, e = random_segments_q12(1500, -8.0, 40.0, seed=31)
+    _compare_walks(nbt, ctx, m, om, o, e)
+    poi = np.array([16.5, 13.5, 9.5])
+    P = oracle.sample_perspectives(poi, 12.0, 24, seed=2)
+    cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 20, 14, 30.0, corners=True)
+    assert_cloud_equal(cloud, P, g, c)
+
+
+def test_elongated_map_falls_back_to_linear(nbt, ctx, monkeypatch):
+    """A map whose Morton cube would be > 8x its linear store uses the linear layout."""
+    monkeypatch.setenv("NBT_MAP_LAYOUT", "morton")
+    codes = rand_map(0, 0.3, 0.7, 0.0, seed=1, shape=(3, 4, 700))
+    m, om = make_map(nbt, ctx, codes)
+    assert np.array_equal(m.download(), codes)
+    o, e = random_segments_q12(500, -5.0, 20.0, seed=3)
+    o[:, 0] *= 30; e[:, 0] *= 30
+    _compare_walks(nbt, ctx, m, om, o, e, max_visits=128)
+
+
+def test_config_e_loop_short():
+    """Config E receding-horizon loop (tools/config_e.py), 4 cycles, oracle parity of the
+    map replica, the per-state totals and g_P at cycles 0 and 3."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "config_e.py"), "--cycles", "4", "--check", "0,3"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
