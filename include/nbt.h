@@ -211,6 +211,22 @@ nbt_status nbt_ig_query(nbt_idbuf buf, const double *query_xyz, int32_t n_q, int
                         double *g_out, int out_on_device);
 void       nbt_idbuf_destroy(nbt_idbuf buf);
 
+/* The MHP's information cost over candidate trajectories:
+ * for n_traj trajectories of poses_per_traj camera poses each (K + 1 = 31 in P:309),
+ * pose i = (pose_xyz[3i..], pose_axis[3i..] = optical axis, any length > 0):
+ *   O_i = cos(theta_i) if theta_i <= theta_cut else 0, theta_i = angle(axis_i, PoI - pos_i)
+ *         (the FoV cut as cos(theta_i) >= cos_theta_cut, reading Q31),
+ *   G_i = the IDW value of nbt_ig_query at pos_i,
+ *   c_out[t] = sum over the trajectory's poses, in order, of w_i / (O_i * G_i + eps)
+ *         (eps = 1e-7 in P:259).
+ * o_out / g_out (n_traj * poses_per_traj doubles) may be NULL.  NBT_ERR_DEGENERATE if a
+ * host pose lies within 1e-9 of the PoI (device poses: flagged, reported by the next
+ * nbt_ctx_sync and their outputs are NaN).  NBT_ERR_EMPTY on an empty buffer. */
+nbt_status nbt_info_cost(nbt_idbuf buf, const double *pose_xyz, const double *pose_axis, int32_t n_traj,
+                         int32_t poses_per_traj, int poses_on_device, const double poi[3], double cos_theta_cut,
+                         double w_i, double eps, double power_p, double zero_eps, int32_t normalize_weights,
+                         double *o_out, double *g_out, double *c_out, int out_on_device);
+
 /* ----------------------------------------------------------- test hooks */
 
 /* Per-ray walk of explicit segments in Q12 voxel coordinates (4096 units per voxel,

@@ -82,6 +82,9 @@ def lib():
         L.orc_classify.argtypes = [C.POINTER(C.c_float), u8p, C.c_int64, C.c_double, C.c_double, u8p]
         L.orc_classify.restype = None
         L.orc_map_update.argtypes = [u8p, C.c_int32, C.c_int32, C.c_int32, ip, u8p, C.c_int64]
+        L.orc_orientation_factor.argtypes = [dp, dp, dp, C.c_double, dp]
+        L.orc_info_cost.argtypes = [C.c_int32, ip, C.POINTER(dp), C.POINTER(dp), dp, dp, C.c_int32, C.c_int32, dp,
+                                    C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32, dp, dp, dp]
     return _lib
 
 
@@ -240,3 +243,33 @@ def map_update(m: OracleMap, ijk, vals):
     st = lib().orc_map_update(_p(m.codes, C.c_uint8), nx, ny, nz, _p(ijk, C.c_int32), _p(vals, C.c_uint8), len(vals))
     if st:
         raise OracleError(st, "map_update")
+
+
+def orientation_factor(pos, axis, poi, cos_cut):
+    pos, axis, poi = (np.ascontiguousarray(v, dtype=np.float64) for v in (pos, axis, poi))
+    o = C.c_double()
+    st = lib().orc_orientation_factor(_d(pos), _d(axis), _d(poi), float(cos_cut), C.byref(o))
+    if st:
+        raise OracleError(st, "orientation_factor")
+    return o.value
+
+
+def info_cost(entries, pos, axis, per, poi, cos_cut, w_i, eps=1e-7, power_p=2.0, zero_eps=1e-9, normalize=False):
+    """(O [n], G [n], c_I [n_traj]) for n = n_traj * per poses (trajectories of `per` poses)."""
+    ents = [(np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 3), np.ascontiguousarray(g, dtype=np.float64))
+            for x, g in entries]
+    sizes = np.array([len(g) for _, g in ents], np.int32)
+    xs = (C.POINTER(C.c_double) * max(1, len(ents)))(*[_d(x) for x, _ in ents])
+    gs = (C.POINTER(C.c_double) * max(1, len(ents)))(*[_d(g) for _, g in ents])
+    pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+    axis = np.ascontiguousarray(axis, dtype=np.float64).reshape(-1, 3)
+    poi = np.ascontiguousarray(poi, dtype=np.float64)
+    n = pos.shape[0]
+    n_traj = n // per
+    o = np.zeros(n); g = np.zeros(n); c = np.zeros(n_traj)
+    st = lib().orc_info_cost(len(ents), _p(sizes, C.c_int32), xs, gs, _d(pos), _d(axis), n_traj, per, _d(poi),
+                             float(cos_cut), float(w_i), float(eps), float(power_p), float(zero_eps),
+                             int(bool(normalize)), _d(o), _d(g), _d(c))
+    if st:
+        raise OracleError(st, "info_cost")
+    return o, g, c

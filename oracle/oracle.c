@@ -472,6 +472,52 @@ int orc_idw_query(int32_t n_entries, const int32_t *entry_sizes, const double *c
     return ORC_OK;
 }
 
+/* ------------------------- orientation factor and information cost (f2) */
+
+/* O(x): the cosine of the angle between the camera's actual optical axis and
+ * the ideal orientation towards the PoI; 0 when the PoI is outside the field of view,
+ * read as theta > theta_cut with theta_cut = min(FoV_h, FoV_v)/2.  The
+ * test theta <= theta_cut is written as cos(theta) >= cos(theta_cut) (reading Q31).
+ * Returns ORC_ERR_DEGENERATE if the position is within 1e-9 of the PoI. */
+int orc_orientation_factor(const double pos[3], const double axis[3], const double poi[3], double cos_cut,
+                           double *o_out)
+{
+    double d[3] = {poi[0] - pos[0], poi[1] - pos[1], poi[2] - pos[2]};
+    double nd = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+    if (nd < 1e-9) return ORC_ERR_DEGENERATE;
+    double na = sqrt((axis[0] * axis[0] + axis[1] * axis[1]) + axis[2] * axis[2]);
+    if (!(na > 0)) return ORC_ERR_INVALID_ARG;
+    double c = ((axis[0] * d[0] + axis[1] * d[1]) + axis[2] * d[2]) / (na * nd);
+    *o_out = (c >= cos_cut) ? c : 0.0;
+    return ORC_OK;
+}
+
+/* c_I(x_{0:K}) = sum_k w_I / (O(x_k) G(x_k) + eps)  (eps = 1e-7 P:259) for each of
+ * n_traj trajectories of `per` poses (K + 1 = per), poses in order; G by orc_idw_query. */
+int orc_info_cost(int32_t n_entries, const int32_t *entry_sizes, const double *const *entry_xyz,
+                  const double *const *entry_gain, const double *pos, const double *axis, int32_t n_traj,
+                  int32_t per, const double poi[3], double cos_cut, double w_i, double eps, double power_p,
+                  double zero_eps, int32_t normalize, double *o_out, double *g_out, double *c_out)
+{
+    int32_t n = n_traj * per;
+    int st = orc_idw_query(n_entries, entry_sizes, entry_xyz, entry_gain, pos, n, power_p, zero_eps, normalize,
+                           g_out);
+    if (st) return st;
+    for (int32_t t = 0; t < n_traj; ++t) {
+        double c = 0.0;
+        for (int32_t k = 0; k < per; ++k) {
+            int32_t i = t * per + k;
+            double o;
+            if ((st = orc_orientation_factor(pos + 3 * (int64_t)i, axis + 3 * (int64_t)i, poi, cos_cut, &o)))
+                return st;
+            if (o_out) o_out[i] = o;
+            c += w_i / (o * g_out[i] + eps);
+        }
+        c_out[t] = c;
+    }
+    return ORC_OK;
+}
+
 /* ------------------------------------------------ sampler (a3, Eq. 1, O-9, Q1-Q3) */
 
 /* Philox4x32-10 (Salmon et al., Random123): counter-based, so the same draws

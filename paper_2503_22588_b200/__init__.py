@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnbt.so")
+LIB_PATH = os.environ.get("NBT_LIB") or os.path.join(_HERE, "libnbt.so")   # NBT_LIB: experiment builds
 
 OK, ERR_INVALID_ARG, ERR_DEGENERATE, ERR_EMPTY, ERR_OUT_OF_MEMORY, ERR_CUDA, ERR_NCCL, ERR_STATE = range(8)
 UNKNOWN, FREE, OCCUPIED = 0, 1, 2
@@ -38,6 +38,7 @@ EXPORTS = [
     "nbt_camera_from_fov", "nbt_camera_from_grid_scaling", "nbt_camera_num_rays",
     "nbt_sample_perspectives", "nbt_id_compute", "nbt_id_compute_slice",
     "nbt_idbuf_create", "nbt_idbuf_push", "nbt_idbuf_clear", "nbt_idbuf_size", "nbt_ig_query", "nbt_idbuf_destroy",
+    "nbt_info_cost",
     "nbt_debug_trace", "nbt_debug_frames",
 ]
 
@@ -113,6 +114,8 @@ def lib():
         "nbt_idbuf_size": ([vp], i32),
         "nbt_ig_query": ([vp, vp, i32, C.c_int, dbl, dbl, i32, vp, C.c_int], C.c_int),
         "nbt_idbuf_destroy": ([vp], None),
+        "nbt_info_cost": ([vp, vp, vp, i32, i32, C.c_int, vp, dbl, dbl, dbl, dbl, dbl, i32, vp, vp, vp, C.c_int],
+                          C.c_int),
         "nbt_debug_trace": ([vp, vp, vp, vp, i32, i32, vp, vp, vp, vp], C.c_int),
         "nbt_debug_frames": ([vp, vp, vp, vp, i32, C.POINTER(Camera), dbl, vp, vp], C.c_int),
     }
@@ -370,6 +373,26 @@ class IdBuffer:
         po, odev, _ = _ptr(out, np.float64)
         check(lib().nbt_ig_query(self.h, pq, int(nq), qdev, float(power_p), float(zero_eps), int(bool(normalize)),
                                  po, odev))
+        return out
+
+    def info_cost(self, pos, axis, poses_per_traj, poi, cos_theta_cut, w_i, eps=1e-7, power_p=2.0, zero_eps=1e-9,
+                  normalize=False, out=None):
+        """f2: (O per pose, G per pose, c_I per trajectory) -- host numpy unless out=(o, g, c) tensors."""
+        pp, pdev, kp = _ptr(pos, np.float64)
+        pa, adev, ka = _ptr(axis, np.float64)
+        if pdev != adev:
+            raise ValueError("pos and axis must both be host or both device")
+        n = kp.shape[0] if kp is not None else 0
+        n_traj = n // int(poses_per_traj)
+        if out is None:
+            out = (np.empty(n), np.empty(n), np.empty(n_traj))
+        po, odev, _ = _ptr(out[0], np.float64)
+        pg, _, _ = _ptr(out[1], np.float64)
+        pc, _, _ = _ptr(out[2], np.float64)
+        ppoi, keep = _poi(poi)
+        check(lib().nbt_info_cost(self.h, pp, pa, int(n_traj), int(poses_per_traj), pdev, ppoi, float(cos_theta_cut),
+                                  float(w_i), float(eps), float(power_p), float(zero_eps), int(bool(normalize)),
+                                  po, pg, pc, odev))
         return out
 
     def close(self):

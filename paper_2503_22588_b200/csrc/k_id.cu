@@ -546,8 +546,11 @@ __device__ __forceinline__ int queue_get(const WalkQueue<T> &Q, int i, Walk<T> &
     return Q.j[i];
 }
 
+#ifndef NBT_TRACE_MIN_BLOCKS
+#define NBT_TRACE_MIN_BLOCKS 1
+#endif
 template <typename T, int L, int K, bool PIPE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_id_trace(TraceArgs A)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, NBT_TRACE_MIN_BLOCKS) k_id_trace(TraceArgs A)
 {
     static_assert((PIPE ? 2 * K : K) <= kBorder, "look-ahead must stay inside the sentinel shell");
     __shared__ WalkQueue<T> queues[kWarpsPerBlock];

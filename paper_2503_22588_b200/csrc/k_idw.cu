@@ -111,7 +111,64 @@ __global__ void k_idw_combine(const double *__restrict__ v, int32_t m, int32_t n
     out[qi] = normalize ? __ddiv_rn(g, wsum) : g;
 }
 
+// Information cost (f2): one thread per trajectory, poses in order.  O by the rounded-
+// once dot product / norms (the same expression as the definition, so the FoV decision
+// is reproducible), G from the per-entry IDW values, c = sum_k w_i / (O G + eps).
+__global__ void k_info_cost(const double *__restrict__ v, int32_t m, InfoCostArgs a, int32_t normalize, int *err)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.n_traj) return;
+    const int n_q = a.n_traj * a.per;
+    double c = 0.0;
+    for (int k = 0; k < a.per; ++k) {
+        const int i = t * a.per + k;
+        double g = 0.0, wsum = 0.0;
+        for (int e = 0; e < m; ++e) {
+            const double wu = __ddiv_rn(1.0, (double)(m - e));
+            g = __dadd_rn(g, __dmul_rn(wu, v[(size_t)e * n_q + i]));
+            wsum = __dadd_rn(wsum, wu);
+        }
+        if (normalize) g = __ddiv_rn(g, wsum);
+        const double *p = a.pos + 3 * (size_t)i, *ax = a.axis + 3 * (size_t)i;
+        const double d0 = __dsub_rn(a.poi[0], p[0]), d1 = __dsub_rn(a.poi[1], p[1]), d2 = __dsub_rn(a.poi[2], p[2]);
+        const double nd = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)));
+        const double na =
+            __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(ax[0], ax[0]), __dmul_rn(ax[1], ax[1])), __dmul_rn(ax[2], ax[2])));
+        double o;
+        if (nd < 1e-9 || !(na > 0.0)) {
+            atomicCAS(err, 0, nd < 1e-9 ? (int)NBT_ERR_DEGENERATE : (int)NBT_ERR_INVALID_ARG);
+            o = __longlong_as_double(0x7ff8000000000000LL);
+        } else {
+            const double dot = __dadd_rn(__dadd_rn(__dmul_rn(ax[0], d0), __dmul_rn(ax[1], d1)), __dmul_rn(ax[2], d2));
+            const double cs = __ddiv_rn(dot, __dmul_rn(na, nd));
+            o = cs >= a.cos_cut ? cs : 0.0;
+        }
+        if (a.o_out) a.o_out[i] = o;
+        if (a.g_out) a.g_out[i] = g;
+        c = __dadd_rn(c, __ddiv_rn(a.w_i, __dadd_rn(__dmul_rn(o, g), a.eps)));
+    }
+    a.c_out[t] = c;
+}
+
 }  // namespace
+
+nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, const InfoCostArgs &a,
+                            double power_p, double zero_eps, int32_t normalize)
+{
+    const int32_t n_q = a.n_traj * a.per;
+    if (n_q == 0) return NBT_OK;
+    nbt_status st;
+    if ((st = ctx->idw_tmp.ensure((size_t)E.m * n_q * 8))) return st;
+    ProfScope ps(ctx, NBT_KERNEL_IDW);
+    dim3 grid((n_q + kQueries - 1) / kQueries, E.m);
+    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, E, a.pos, n_q, power_p,
+                                                     zero_eps, ctx->idw_tmp.as<double>());
+    NBT_LAUNCHED(ctx);
+    k_info_cost<<<(a.n_traj + 63) / 64, 64, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), E.m, a, normalize,
+                                                              ctx->d_err);
+    NBT_LAUNCHED(ctx);
+    return NBT_OK;
+}
 
 nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, const double *d_q, int32_t n_q,
                       double power_p, double zero_eps, int32_t normalize, double *d_out)

@@ -127,7 +127,7 @@ struct nbt_ctx_s {
     nbt::DevBuf out_tmp;              // device staging for host outputs
     nbt::DevBuf deltas;               // staged map deltas
     nbt::DevBuf keys, keys_alt, cub_tmp;
-    nbt::DevBuf queries, qout, idw_tmp;
+    nbt::DevBuf queries, qout, idw_tmp, poses;
     nbt::DevBuf dbg;                  // debug entry points
     nbt::HostStage stage_in[3];
     nbt::HostStage stage_out;
@@ -198,5 +198,14 @@ struct IdwEntries {
 };
 nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, const double *d_q, int32_t n_q,
                       double power_p, double zero_eps, int32_t normalize, double *d_out);
+struct InfoCostArgs {
+    const double *pos, *axis;
+    int32_t n_traj, per;
+    double poi[3];
+    double cos_cut, w_i, eps;
+    double *o_out, *g_out, *c_out;   // device; o/g may be null
+};
+nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, const InfoCostArgs &a,
+                            double power_p, double zero_eps, int32_t normalize);
 
 }  // namespace nbt

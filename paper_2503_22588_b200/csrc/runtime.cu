@@ -288,7 +288,7 @@ void nbt_ctx_destroy(nbt_ctx ctx)
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf *bufs[] = {&ctx->persp, &ctx->frames, &ctx->totals, &ctx->counter, &ctx->out_tmp, &ctx->deltas,
-                      &ctx->keys, &ctx->keys_alt, &ctx->cub_tmp, &ctx->queries, &ctx->qout, &ctx->idw_tmp, &ctx->dbg};
+                      &ctx->keys, &ctx->keys_alt, &ctx->cub_tmp, &ctx->queries, &ctx->qout, &ctx->idw_tmp, &ctx->poses, &ctx->dbg};
     for (DevBuf *b : bufs) b->release();
     for (auto &st : ctx->stage_in) st.release();
     for (auto &v : ctx->prof.pending)
@@ -782,6 +782,75 @@ nbt_status nbt_ig_query(nbt_idbuf b, const double *query_xyz, int32_t n_q, int q
     if ((s = launch_idw(ctx, b, E, dq, n_q, power_p, zero_eps, normalize_weights, dout))) return s;
     if (!out_on_device) return d2h_sync(ctx, g_out, dout, (size_t)n_q * 8);
     return NBT_OK;
+}
+
+nbt_status nbt_info_cost(nbt_idbuf b, const double *pose_xyz, const double *pose_axis, int32_t n_traj,
+                         int32_t per, int poses_on_device, const double poi[3], double cos_theta_cut, double w_i,
+                         double eps, double power_p, double zero_eps, int32_t normalize, double *o_out, double *g_out,
+                         double *c_out, int out_on_device)
+{
+    if (!b) return fail(NBT_ERR_INVALID_ARG, "nbt_info_cost: null buffer");
+    nbt_ctx ctx = b->ctx;
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (b->count == 0) return fail(NBT_ERR_EMPTY, "nbt_info_cost: no distribution available");
+    if (n_traj < 0 || per < 1 || (n_traj > 0 && (!pose_xyz || !pose_axis || !c_out)) || !poi || !finite3(poi) ||
+        !isfinite(cos_theta_cut) || !isfinite(w_i) || !isfinite(eps) || !(power_p >= 0) || !isfinite(power_p) ||
+        !(zero_eps >= 0) || (int64_t)n_traj * per > (1ll << 30))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_info_cost: bad argument");
+    if (n_traj == 0) return NBT_OK;
+    const size_t n = (size_t)n_traj * per;
+    IdwEntries E;
+    E.m = b->count;
+    for (int e = 0; e < b->count; ++e) {
+        E.slot[e] = (b->head + e) % b->capacity;
+        E.size[e] = b->sizes[E.slot[e]];
+    }
+    InfoCostArgs a;
+    a.n_traj = n_traj;
+    a.per = per;
+    for (int k = 0; k < 3; ++k) a.poi[k] = poi[k];
+    a.cos_cut = cos_theta_cut;
+    a.w_i = w_i;
+    a.eps = eps;
+    if (poses_on_device) {
+        a.pos = pose_xyz;
+        a.axis = pose_axis;
+    } else {
+        for (size_t i = 0; i < n; ++i) {
+            const double *p = pose_xyz + 3 * i, *ax = pose_axis + 3 * i;
+            if (!finite3(p) || !finite3(ax)) return fail(NBT_ERR_INVALID_ARG, "nbt_info_cost: non-finite pose");
+            double d0 = poi[0] - p[0], d1 = poi[1] - p[1], d2 = poi[2] - p[2];
+            if (sqrt((d0 * d0 + d1 * d1) + d2 * d2) < 1e-9)
+                return fail(NBT_ERR_DEGENERATE, "nbt_info_cost: pose " + std::to_string(i) + " at the PoI");
+        }
+        if ((s = ctx->poses.ensure(n * 48)) || (s = ctx->stage_in[2].acquire(n * 48))) return s;
+        memcpy(ctx->stage_in[2].p, pose_xyz, n * 24);
+        memcpy((char *)ctx->stage_in[2].p + n * 24, pose_axis, n * 24);
+        NBT_CUDA(cudaMemcpyAsync(ctx->poses.p, ctx->stage_in[2].p, n * 48, cudaMemcpyHostToDevice, ctx->stream));
+        if ((s = ctx->stage_in[2].mark(ctx->stream))) return s;
+        a.pos = ctx->poses.as<double>();
+        a.axis = ctx->poses.as<double>() + 3 * n;
+    }
+    double *tmp = nullptr;
+    if (out_on_device) {
+        a.o_out = o_out; a.g_out = g_out; a.c_out = c_out;
+    } else {
+        if ((s = ctx->qout.ensure(n * 16 + (size_t)n_traj * 8))) return s;
+        tmp = ctx->qout.as<double>();
+        a.o_out = tmp; a.g_out = tmp + n; a.c_out = tmp + 2 * n;
+    }
+    if ((s = launch_info_cost(ctx, b, E, a, power_p, zero_eps, normalize))) return s;
+    if (out_on_device) return NBT_OK;
+    const size_t total = n * 16 + (size_t)n_traj * 8;
+    if ((s = ctx->stage_out.acquire(total))) return s;
+    NBT_CUDA(cudaMemcpyAsync(ctx->stage_out.p, tmp, total, cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double *h = static_cast<const double *>(ctx->stage_out.p);
+    if (o_out) memcpy(o_out, h, n * 8);
+    if (g_out) memcpy(g_out, h + n, n * 8);
+    memcpy(c_out, h + 2 * n, (size_t)n_traj * 8);
+    return take_device_error(ctx, "nbt_info_cost");
 }
 
 void nbt_idbuf_destroy(nbt_idbuf b)

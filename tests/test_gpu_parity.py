@@ -532,3 +532,43 @@ def test_config_e_loop_short():
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "config_e.py"), "--cycles", "4", "--check", "0,3"],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+# ------------------------------------------- f2: orientation factor + information cost
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_info_cost_matches_oracle(nbt, ctx, on_device):
+    """O(x) bit-exact (same rounded-once expression), G within 1e-12, c_I within 1e-12, for
+    64 trajectories of K+1 = 31 poses."""
+    import torch
+    rng = np.random.default_rng(11)
+    poi = np.array([0.3, -0.1, 0.5])
+    buf = nbt.IdBuffer(ctx, 10, 512)
+    entries = []
+    for _ in range(4):
+        xyz = poi + rng.normal(size=(512, 3)) * 0.6
+        gain = rng.uniform(0, 80, 512)
+        buf.push(nbt.IgCloud(xyz, gain, None))
+        entries.append((xyz, gain))
+    n = 64 * 31
+    pos = poi + rng.normal(size=(n, 3)) * 0.8
+    axis = (poi - pos) + rng.normal(size=(n, 3)) * 0.4          # mostly towards the PoI
+    axis[::7] *= -1.0                                           # some looking away
+    cut = math.cos(math.radians(32.5))
+    o_ref, g_ref, c_ref = oracle.info_cost(entries, pos, axis, 31, poi, cut, w_i=25.0)
+    if on_device:
+        tp, ta = torch.from_numpy(pos).cuda(), torch.from_numpy(axis).cuda()
+        out = tuple(torch.empty(k, dtype=torch.float64, device="cuda") for k in (n, n, 64))
+        buf.info_cost(tp, ta, 31, poi, cut, 25.0, out=out)
+        ctx.sync()
+        o, g, c = (t.cpu().numpy() for t in out)
+    else:
+        o, g, c = buf.info_cost(pos, axis, 31, poi, cut, 25.0)
+    assert np.array_equal(o, o_ref)
+    assert (o == 0).any() and (o > 0).any()
+    assert np.allclose(g, g_ref, rtol=1e-12)
+    assert np.allclose(c, c_ref, rtol=1e-12)
+    with pytest.raises(nbt.NbtError) as ei:
+        bad = pos.copy(); bad[5] = poi
+        buf.info_cost(bad, axis, 31, poi, cut, 25.0)
+    assert ei.value.status == nbt.ERR_DEGENERATE
