@@ -471,7 +471,88 @@ def main_ours(args, cfg):
     return 0
 
 
+# ------------------------------------------------------ paper benchmark sweep (f4)
+# the paper's ID runtime benchmark in shape (Fig.
+# "Mean runtimes of GPU and CPU over 100 iterations").  Sweep N_P in
+# {100..1000} x s_G in {5, 50, 100, 200} with the paper's s_G endpoint lattice (spacing
+# s_G * s_Vox on the far plane plus the 4 corner rays; FoV 75 x 65 deg, d_Cam = 3.86 m,
+# S:476) on the synthetic 256^3 / 1 cm scene.  GPU leg: libnbt through the C ABI with host
+# perspectives in and the host IG cloud out (the paper's GPU time includes its transfers,
+# P:335; here the map stays resident), mean/std over --iters (100 in P:318).  CPU baseline
+# leg: the oracle on ONE thread (the paper's sequential implementation), iterations
+# bounded by --cpu-budget-s per point.  Writes the CSV of S:193 (n_p,s_g,mode,mean_s,std_s).
+#     python bench.py --paper-sweep [--out profiles/r01_paper_sweep.csv]
+
+D_CAM = 3.86
+
+
+def paper_sweep(argv):
+    ap = argparse.ArgumentParser(prog="bench.py --paper-sweep")
+    ap.add_argument("--iters", type=int, default=100)
+    ap.add_argument("--cpu-budget-s", type=float, default=6.0)
+    ap.add_argument("--n-p", default="100,200,300,400,500,600,700,800,900,1000")
+    ap.add_argument("--s-g", default="5,50,100,200")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args(argv)
+    import torch
+    import paper_2503_22588_b200 as nbt
+    cfg = CONFIGS["B"]
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(st)
+    ctx = nbt.Ctx(0, st.cuda_stream)
+    codes = cfg.map_codes()
+    m = nbt.Map(ctx, nbt.map_desc(cfg.n, cfg.n, cfg.n, cfg.voxel_size))
+    m.upload(codes)
+    n_ps = [int(x) for x in args.n_p.split(",")]
+    s_gs = [float(x) for x in args.s_g.split(",")]
+    rows = []
+    om = None
+    if not args.no_cpu:
+        import oracle
+        om = oracle.OracleMap(codes, voxel_size=cfg.voxel_size)
+    for s_g in s_gs:
+        cam = nbt.camera_from_grid_scaling(FOV_H, FOV_V, D_CAM, cfg.voxel_size, s_g)
+        for n_p in n_ps:
+            persp = nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_p, 7 + n_p, 0)
+            out = nbt.empty_cloud(n_p)
+            nbt.id_compute(ctx, m, cfg.poi, persp, cam, D_CAM, out=out)          # warm-up
+            ts = []
+            for _ in range(args.iters):
+                t0 = time.perf_counter()
+                nbt.id_compute(ctx, m, cfg.poi, persp, cam, D_CAM, out=out)      # host in, host out (syncs)
+                ts.append(time.perf_counter() - t0)
+            rows.append((n_p, s_g, "gpu", float(np.mean(ts)), float(np.std(ts)), cam.num_rays))
+            print(f"n_p={n_p} s_g={s_g:g} N_E={cam.num_rays} gpu mean {np.mean(ts)*1e3:.3f} ms", flush=True)
+            if om is not None:
+                ocam = oracle.camera_from_grid_scaling(FOV_H, FOV_V, D_CAM, cfg.voxel_size, s_g)
+                ts = []
+                spent = 0.0
+                while len(ts) < args.iters and (spent < args.cpu_budget_s or not ts):
+                    t0 = time.perf_counter()
+                    _, g, _ = oracle.id_compute(om, cfg.poi, persp, ocam, D_CAM, nthreads=1)
+                    ts.append(time.perf_counter() - t0)
+                    spent += ts[-1]
+                rows.append((n_p, s_g, "cpu_oracle_1thread", float(np.mean(ts)), float(np.std(ts)), len(ts)))
+                assert np.allclose(g, out.gain, rtol=0, atol=0) or np.array_equal(g, out.gain)
+                print(f"n_p={n_p} s_g={s_g:g} cpu mean {np.mean(ts):.3f} s over {len(ts)} iters", flush=True)
+    lines = ["n_p,s_g,mode,mean_s,std_s,note"]
+    for n_p, s_g, mode, mu, sd, note in rows:
+        extra = f"N_E={note}" if mode == "gpu" else f"iters={note}"
+        lines.append(f"{n_p},{s_g:g},{mode},{mu:.6g},{sd:.3g},{extra}")
+    text = "\n".join(lines) + "\n"
+    print(text)
+    print("paper (P:330, i5-12600KF, sequential CPU): s_G=5, N_P=1000 -> 144.93 s; GPU (RTX 3060) ~75% lower (P:333)")
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(text)
+
+
+
 def main():
+    if "--paper-sweep" in sys.argv:
+        return paper_sweep([a for a in sys.argv[1:] if a != "--paper-sweep"]) or 0
     args = parse()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
