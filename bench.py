@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-north-star", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     return ap.parse_args()
 
@@ -275,26 +276,61 @@ def main_ours(args, cfg):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     acc = torch.zeros(4, dtype=torch.int64, device=dev)
 
-    def step(t):
-        ijk, val = d_ijk[t % N_DELTA_SETS], d_val[t % N_DELTA_SETS]
-        if world > 1:
-            ndist.broadcast_deltas(ijk, val, src=0)
-        m.update(ijk, val)                                                       # a2
-        nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_p, 1000003 * t + rank, cfg.persp_mode,
+    gathered = (nbt.IgCloud(torch.empty((n_tot, 3), dtype=torch.float64, device=dev),
+                            torch.empty(n_tot, dtype=torch.float64, device=dev), None) if world > 1 else cloud)
+
+    def part_a(c):                      # rows a2-a8 on this rank
+        m.update(d_ijk[c], d_val[c])                                             # a2
+        nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_p, 1000003 * c + rank, cfg.persp_mode,
                                 out=persp)                                       # a3
         nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=cloud)       # a4-a8
-        if world > 1:
-            xyz = ndist.all_gather_rows(cloud.xyz, n_tot, world, strided=False)
-            gain = ndist.all_gather_rows(cloud.gain, n_tot, world, strided=False)
-            full = nbt.IgCloud(xyz, gain, None)
-        else:
-            full = cloud
-        buf.push(full, n_tot)                                                    # a9
+
+    def part_b():                       # row a9 on the assembled cloud
+        buf.push(gathered, n_tot)
         buf.query(q_dev, power_p=POWER_P, out=q_out)
 
+    def exchange_deltas(c):
+        if world > 1:
+            ndist.broadcast_deltas(d_ijk[c], d_val[c], src=0)
+
+    def exchange_cloud():
+        if world > 1:
+            gathered.xyz.copy_(ndist.all_gather_rows(cloud.xyz, n_tot, world, strided=False))
+            gathered.gain.copy_(ndist.all_gather_rows(cloud.gain, n_tot, world, strided=False))
+
+    def step_eager(t):
+        c = t % N_DELTA_SETS
+        exchange_deltas(c)
+        part_a(c)
+        exchange_cloud()
+        part_b()
+
     for t in range(args.warmup):
-        step(t)
+        step_eager(t)
     ctx.sync()
+
+    # ---- CUDA graphs: one per delta set for rows a2-a8 and one for a9 (the NCCL exchanges
+    #      stay eager between them).  Profiling is switched on before capture so every
+    #      graph carries event nodes around its kernels.
+    ctx.set_profiling(True)
+    graphs_a, graph_b = [], None
+    if not args.no_graph:
+        for c in range(N_DELTA_SETS):
+            ctx.capture_begin()
+            part_a(c)
+            graphs_a.append(ctx.capture_end())
+        ctx.capture_begin()
+        part_b()
+        graph_b = ctx.capture_end()
+
+    def step(t):
+        c = t % N_DELTA_SETS
+        if args.no_graph:
+            return step_eager(t)
+        exchange_deltas(c)
+        graphs_a[c].launch()
+        exchange_cloud()
+        graph_b.launch()
 
     # ---- timed region: K steps, device time per step with CUDA events on the ctx stream
     gpu_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid).replace("GPU-", "")
@@ -302,9 +338,9 @@ def main_ours(args, cfg):
     time.sleep(0.25)
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ctx.set_profiling(True)
     for k in range(nbt.KERNEL_MAP_UPDATE + 1):
         ctx.profile_read(k, reset=True)
+    graph_prof = {k: [0.0, 0] for k in range(nbt.KERNEL_MAP_UPDATE + 1)}
     launches0 = ctx.launches
     if world > 1:
         dist.barrier()
@@ -315,6 +351,12 @@ def main_ours(args, cfg):
         ev0[i].record(stream)
         step(args.warmup + i)
         ev1[i].record(stream)
+        if not args.no_graph:                      # kernel times of this replay (event nodes)
+            for k in graph_prof:
+                for g in (graphs_a[(args.warmup + i) % N_DELTA_SETS], graph_b):
+                    ms_k, n_k = g.profile_read(k)
+                    graph_prof[k][0] += ms_k
+                    graph_prof[k][1] += n_k
         acc += cloud.counts.sum(0)                 # work accounting, outside the events
     torch.cuda.synchronize()
     if world > 1:
@@ -323,6 +365,8 @@ def main_ours(args, cfg):
     launches = ctx.launches - launches0
     dev_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
     prof = {k: ctx.profile_read(k, reset=True) for k in range(nbt.KERNEL_MAP_UPDATE + 1)}
+    if not args.no_graph:
+        prof = {k: (v[0], v[1]) for k, v in graph_prof.items()}
     ctx.set_profiling(False)
     clocks.stop()
     clk = clocks.summary(t_wall0, t_wall1)

@@ -95,6 +95,22 @@ nbt_status nbt_ctx_set_profiling(nbt_ctx ctx, int enable);
  * reset; synchronizes the stream.  reset != 0 clears the record. */
 nbt_status nbt_ctx_profile_read(nbt_ctx ctx, int32_t kernel, double *total_ms, uint64_t *launches, int reset);
 
+/* CUDA-graph capture of a sequence of calls on the ctx (an MHP cycle with device-resident
+ * inputs and outputs), replayed with one launch.  Between begin and end, calls are
+ * RECORDED, not executed: only device pointers are allowed (host inputs or outputs give
+ * NBT_ERR_STATE), and scratch buffers must already have their size (run the sequence
+ * once before capturing).  The ID ring buffer keeps its state on the device, so replays
+ * push and query correctly.  Kernel parameters (PoI, seeds, pointers) are fixed at
+ * capture time.  With profiling on, the captured kernels are bracketed by event nodes
+ * whose times nbt_graph_profile_read returns for the last replay. */
+typedef struct nbt_graph_s *nbt_graph;
+nbt_status nbt_ctx_capture_begin(nbt_ctx ctx);
+nbt_status nbt_ctx_capture_end(nbt_ctx ctx, nbt_graph *out);
+nbt_status nbt_graph_launch(nbt_graph graph);
+/* Sum of the last replay's durations (ms) of the captured launches of `kernel`; syncs. */
+nbt_status nbt_graph_profile_read(nbt_graph graph, int32_t kernel, double *total_ms, uint64_t *launches);
+void       nbt_graph_destroy(nbt_graph graph);
+
 /* ------------------------------------------------------- voxel map (row a1, a2) */
 
 enum { NBT_UNKNOWN = 0, NBT_FREE = 1, NBT_OCCUPIED = 2 };      /* three states (Eq. 2) */

@@ -33,6 +33,7 @@ EXPORTS = [
     "nbt_abi_version", "nbt_status_string", "nbt_last_error_message",
     "nbt_ctx_create", "nbt_ctx_set_stream", "nbt_ctx_sync", "nbt_ctx_destroy", "nbt_ctx_launch_count",
     "nbt_ctx_set_profiling", "nbt_ctx_profile_read",
+    "nbt_ctx_capture_begin", "nbt_ctx_capture_end", "nbt_graph_launch", "nbt_graph_profile_read", "nbt_graph_destroy",
     "nbt_map_desc_default", "nbt_map_create", "nbt_map_upload", "nbt_map_upload_prob", "nbt_map_update",
     "nbt_map_device_buffer", "nbt_map_download", "nbt_map_get_desc", "nbt_map_destroy",
     "nbt_camera_from_fov", "nbt_camera_from_grid_scaling", "nbt_camera_num_rays",
@@ -92,6 +93,11 @@ def lib():
         "nbt_ctx_launch_count": ([vp], u64),
         "nbt_ctx_set_profiling": ([vp, C.c_int], C.c_int),
         "nbt_ctx_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(u64), C.c_int], C.c_int),
+        "nbt_ctx_capture_begin": ([vp], C.c_int),
+        "nbt_ctx_capture_end": ([vp, C.POINTER(vp)], C.c_int),
+        "nbt_graph_launch": ([vp], C.c_int),
+        "nbt_graph_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(u64)], C.c_int),
+        "nbt_graph_destroy": ([vp], None),
         "nbt_map_desc_default": ([C.POINTER(MapDesc), i32, i32, i32, dbl], None),
         "nbt_map_create": ([vp, C.POINTER(MapDesc), C.POINTER(vp)], C.c_int),
         "nbt_map_upload": ([vp, vp, sz, C.c_int], C.c_int),
@@ -200,9 +206,44 @@ class Ctx:
         check(lib().nbt_ctx_profile_read(self.h, int(kernel), C.byref(ms), C.byref(n), int(bool(reset))))
         return ms.value, int(n.value)
 
+    def capture_begin(self):
+        """Start recording the following calls on this ctx into a CUDA graph (device buffers only)."""
+        check(lib().nbt_ctx_capture_begin(self.h))
+
+    def capture_end(self):
+        g = C.c_void_p()
+        check(lib().nbt_ctx_capture_end(self.h, C.byref(g)))
+        return Graph(g, self)
+
     def close(self):
         if getattr(self, "h", None):
             lib().nbt_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class Graph:
+    """nbt_graph: a captured sequence of libnbt calls, replayed with one launch."""
+
+    def __init__(self, h, ctx):
+        self.h, self.ctx = h, ctx
+
+    def launch(self):
+        check(lib().nbt_graph_launch(self.h))
+
+    def profile_read(self, kernel):
+        ms, n = C.c_double(), C.c_uint64()
+        check(lib().nbt_graph_profile_read(self.h, int(kernel), C.byref(ms), C.byref(n)))
+        return ms.value, int(n.value)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().nbt_graph_destroy(self.h)
             self.h = None
 
     def __del__(self):

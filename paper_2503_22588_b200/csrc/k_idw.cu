@@ -35,18 +35,22 @@ __device__ __forceinline__ double dist2(double x0, double x1, double x2, double 
 // the entry's perspectives (interleaved), staged through shared memory, and
 // combine (sum of num, sum of den, argmin of d^2 with lowest j) by warp shuffles.
 __global__ void __launch_bounds__(kThreads)
-    k_idw_entry(const double *__restrict__ xyz, const double *__restrict__ gain, int32_t max_persp, IdwEntries E,
-                const double *__restrict__ q, int32_t n_q, double power_p, double zero_eps,
-                double *__restrict__ v_out)
+    k_idw_entry(const double *__restrict__ xyz, const double *__restrict__ gain, int32_t max_persp,
+                const int32_t *__restrict__ meta, int32_t cap, const double *__restrict__ q, int32_t n_q,
+                double power_p, double zero_eps, double *__restrict__ v_out)
 {
     __shared__ double sp[kTile][4];
     const int e = blockIdx.y;
+    const int pushes = meta[0];
+    const int m = min(pushes, cap);
+    if (e >= m) return;
+    const int slot = (pushes - m + e) % cap;                  // entry e, oldest first
     const int sub = threadIdx.x & (kSplit - 1);
     const int qi = blockIdx.x * kQueries + (threadIdx.x / kSplit);
     const bool active = qi < n_q;
-    const double *P = xyz + (size_t)E.slot[e] * max_persp * 3;
-    const double *G = gain + (size_t)E.slot[e] * max_persp;
-    const int np = E.size[e];
+    const double *P = xyz + (size_t)slot * max_persp * 3;
+    const double *G = gain + (size_t)slot * max_persp;
+    const int np = meta[1 + slot];
     double x0 = 0.0, x1 = 0.0, x2 = 0.0;
     if (active) { x0 = q[3 * (size_t)qi]; x1 = q[3 * (size_t)qi + 1]; x2 = q[3 * (size_t)qi + 2]; }
     const bool p2 = power_p == 2.0;
@@ -97,11 +101,12 @@ __global__ void __launch_bounds__(kThreads)
     v_out[(size_t)e * n_q + qi] = v;
 }
 
-__global__ void k_idw_combine(const double *__restrict__ v, int32_t m, int32_t n_q, int32_t normalize,
-                              double *__restrict__ out)
+__global__ void k_idw_combine(const double *__restrict__ v, const int32_t *__restrict__ meta, int32_t cap, int32_t n_q,
+                              int32_t normalize, double *__restrict__ out)
 {
     const int qi = blockIdx.x * blockDim.x + threadIdx.x;
     if (qi >= n_q) return;
+    const int m = min(meta[0], cap);
     double g = 0.0, wsum = 0.0;
     for (int e = 0; e < m; ++e) {
         const double wu = __ddiv_rn(1.0, (double)(m - e));
@@ -114,10 +119,12 @@ __global__ void k_idw_combine(const double *__restrict__ v, int32_t m, int32_t n
 // Information cost (f2): one thread per trajectory, poses in order.  O by the rounded-
 // once dot product / norms (the same expression as the definition, so the FoV decision
 // is reproducible), G from the per-entry IDW values, c = sum_k w_i / (O G + eps).
-__global__ void k_info_cost(const double *__restrict__ v, int32_t m, InfoCostArgs a, int32_t normalize, int *err)
+__global__ void k_info_cost(const double *__restrict__ v, const int32_t *__restrict__ meta, int32_t cap, InfoCostArgs a,
+                            int32_t normalize, int *err)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.n_traj) return;
+    const int m = min(meta[0], cap);
     const int n_q = a.n_traj * a.per;
     double c = 0.0;
     for (int k = 0; k < a.per; ++k) {
@@ -150,39 +157,69 @@ __global__ void k_info_cost(const double *__restrict__ v, int32_t m, InfoCostArg
     a.c_out[t] = c;
 }
 
+// Ring push, device side (so a captured CUDA graph can replay it): copy the cloud into
+// slot pushes % cap, then advance the counter in a second, single-thread kernel.
+__global__ void k_idbuf_copy(const int32_t *__restrict__ meta, int32_t cap, int32_t max_persp,
+                             const double *__restrict__ src_xyz, const double *__restrict__ src_gain, int32_t n,
+                             double *__restrict__ xyz, double *__restrict__ gain)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 4 * n) return;
+    const int slot = meta[0] % cap;
+    if (i < 3 * n) xyz[(size_t)slot * max_persp * 3 + i] = src_xyz[i];
+    else gain[(size_t)slot * max_persp + (i - 3 * n)] = src_gain[i - 3 * n];
+}
+
+__global__ void k_idbuf_advance(int32_t *meta, int32_t cap, int32_t n)
+{
+    const int slot = meta[0] % cap;
+    meta[1 + slot] = n;
+    meta[0] = meta[0] + 1;
+}
+
 }  // namespace
 
-nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, const InfoCostArgs &a,
-                            double power_p, double zero_eps, int32_t normalize)
+nbt_status launch_idbuf_push(nbt_ctx ctx, nbt_idbuf_s *b, const double *d_xyz, const double *d_gain, int32_t n)
 {
-    const int32_t n_q = a.n_traj * a.per;
-    if (n_q == 0) return NBT_OK;
-    nbt_status st;
-    if ((st = ctx->idw_tmp.ensure((size_t)E.m * n_q * 8))) return st;
-    ProfScope ps(ctx, NBT_KERNEL_IDW);
-    dim3 grid((n_q + kQueries - 1) / kQueries, E.m);
-    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, E, a.pos, n_q, power_p,
-                                                     zero_eps, ctx->idw_tmp.as<double>());
+    k_idbuf_copy<<<(4 * n + 255) / 256, 256, 0, ctx->stream>>>(b->d_meta, b->capacity, b->max_persp, d_xyz, d_gain,
+                                                                  n, b->d_xyz, b->d_gain);
     NBT_LAUNCHED(ctx);
-    k_info_cost<<<(a.n_traj + 63) / 64, 64, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), E.m, a, normalize,
-                                                              ctx->d_err);
+    k_idbuf_advance<<<1, 1, 0, ctx->stream>>>(b->d_meta, b->capacity, n);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }
 
-nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, const double *d_q, int32_t n_q,
-                      double power_p, double zero_eps, int32_t normalize, double *d_out)
+nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const InfoCostArgs &a, double power_p,
+                            double zero_eps, int32_t normalize)
+{
+    const int32_t n_q = a.n_traj * a.per;
+    if (n_q == 0) return NBT_OK;
+    nbt_status st;
+    if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_q * 8))) return st;
+    ProfScope ps(ctx, NBT_KERNEL_IDW);
+    dim3 grid((n_q + kQueries - 1) / kQueries, b->capacity);
+    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, a.pos,
+                                                     n_q, power_p, zero_eps, ctx->idw_tmp.as<double>());
+    NBT_LAUNCHED(ctx);
+    k_info_cost<<<(a.n_traj + 63) / 64, 64, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), b->d_meta, b->capacity, a,
+                                                              normalize, ctx->d_err);
+    NBT_LAUNCHED(ctx);
+    return NBT_OK;
+}
+
+nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const double *d_q, int32_t n_q, double power_p,
+                      double zero_eps, int32_t normalize, double *d_out)
 {
     if (n_q == 0) return NBT_OK;
     nbt_status st;
-    if ((st = ctx->idw_tmp.ensure((size_t)E.m * n_q * 8))) return st;
+    if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_q * 8))) return st;
     ProfScope ps(ctx, NBT_KERNEL_IDW);
-    dim3 grid((n_q + kQueries - 1) / kQueries, E.m);
-    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, E, d_q, n_q, power_p,
-                                                     zero_eps, ctx->idw_tmp.as<double>());
+    dim3 grid((n_q + kQueries - 1) / kQueries, b->capacity);
+    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, d_q,
+                                                     n_q, power_p, zero_eps, ctx->idw_tmp.as<double>());
     NBT_LAUNCHED(ctx);
-    k_idw_combine<<<(n_q + 127) / 128, 128, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), E.m, n_q, normalize,
-                                                               d_out);
+    k_idw_combine<<<(n_q + 127) / 128, 128, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), b->d_meta, b->capacity,
+                                                               n_q, normalize, d_out);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }

@@ -86,6 +86,15 @@ struct HostStage {
     void release();
 };
 
+// True while the calling thread's ctx stream is being captured into a CUDA graph:
+// buffers must not grow (warm up first) and nothing may synchronize.
+extern thread_local bool g_capturing;
+
+struct CapPair {
+    int kernel;
+    cudaEvent_t start, end;
+};
+
 // Per-kernel-family event timing (nbt_ctx_set_profiling).
 struct Profiler {
     bool on = false;
@@ -132,6 +141,17 @@ struct nbt_ctx_s {
     nbt::HostStage stage_in[3];
     nbt::HostStage stage_out;
     nbt::Profiler prof;
+    bool capturing = false;
+    uint64_t cap_launches0 = 0;
+    std::vector<nbt::CapPair> cap_pairs;  // profiling events recorded inside the capture
+};
+
+struct nbt_graph_s {
+    nbt_ctx ctx = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t kernels = 0;                 // kernel nodes per launch
+    std::vector<nbt::CapPair> pairs;
 };
 
 struct nbt_map_s {
@@ -148,8 +168,8 @@ struct nbt_map_s {
 struct nbt_idbuf_s {
     nbt_ctx ctx = nullptr;
     int32_t capacity = 0, max_persp = 0;
-    int32_t head = 0, count = 0;      // ring: slot of the oldest entry, number of entries
-    int32_t sizes[64] = {0};
+    int32_t count = 0;                // host mirror of min(pushes, capacity) (validation only)
+    int32_t *d_meta = nullptr;        // device: [0] = pushes so far, [1 + slot] = entry sizes
     double *d_xyz = nullptr;          // capacity x max_persp x 3
     double *d_gain = nullptr;         // capacity x max_persp
 };
@@ -190,14 +210,11 @@ bool debug_needs_wide(const int32_t *o_q12, const int32_t *e_q12, int32_t n_rays
 nbt_status launch_debug_frames(nbt_ctx ctx, nbt_map m, const double poi[3], const double *d_persp, int32_t n,
                                const nbt_camera &cam, double range, int32_t *d_frames);
 
-// IDW (k_idw.cu)
-struct IdwEntries {
-    int32_t m;               // entries, oldest first
-    int32_t slot[64];
-    int32_t size[64];
-};
-nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, const double *d_q, int32_t n_q,
-                      double power_p, double zero_eps, int32_t normalize, double *d_out);
+// IDW (k_idw.cu).  The ring state lives on the device (nbt_idbuf_s::d_meta) so that a
+// captured graph replays pushes and queries correctly.
+nbt_status launch_idbuf_push(nbt_ctx ctx, nbt_idbuf_s *b, const double *d_xyz, const double *d_gain, int32_t n);
+nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const double *d_q, int32_t n_q, double power_p,
+                      double zero_eps, int32_t normalize, double *d_out);
 struct InfoCostArgs {
     const double *pos, *axis;
     int32_t n_traj, per;
@@ -205,7 +222,7 @@ struct InfoCostArgs {
     double cos_cut, w_i, eps;
     double *o_out, *g_out, *c_out;   // device; o/g may be null
 };
-nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const IdwEntries &E, const InfoCostArgs &a,
-                            double power_p, double zero_eps, int32_t normalize);
+nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const InfoCostArgs &a, double power_p,
+                            double zero_eps, int32_t normalize);
 
 }  // namespace nbt

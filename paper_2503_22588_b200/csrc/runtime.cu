@@ -14,6 +14,7 @@
 namespace nbt {
 
 static thread_local std::string g_last_error;
+thread_local bool g_capturing = false;
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
@@ -32,6 +33,8 @@ nbt_status cuda_fail(cudaError_t e, const char *what)
 nbt_status DevBuf::ensure(size_t bytes)
 {
     if (bytes <= cap && p) return NBT_OK;
+    if (g_capturing) return fail(NBT_ERR_STATE, "a scratch buffer would grow during graph capture: run the "
+                                                "sequence once before capturing");
     size_t want = bytes < 256 ? 256 : bytes;
     want = want + want / 4;
     if (p) {
@@ -145,15 +148,30 @@ cudaEvent_t Profiler::take()
 
 ProfScope::ProfScope(nbt_ctx c, int k) : ctx(c), kernel(k)
 {
-    if (ctx->prof.on) {
-        start = ctx->prof.take();
-        if (start) cudaEventRecord(start, ctx->stream);
+    if (!ctx->prof.on) return;
+    if (ctx->capturing) {
+        // a fresh event owned by the graph; recorded as an event node at every replay
+        if (cudaEventCreate(&start) != cudaSuccess) start = nullptr;
+        if (start) cudaEventRecordWithFlags(start, ctx->stream, cudaEventRecordExternal);
+        return;
     }
+    start = ctx->prof.take();
+    if (start) cudaEventRecord(start, ctx->stream);
 }
 
 ProfScope::~ProfScope()
 {
     if (!start) return;
+    if (ctx->capturing) {
+        cudaEvent_t end = nullptr;
+        if (cudaEventCreate(&end) == cudaSuccess) {
+            cudaEventRecordWithFlags(end, ctx->stream, cudaEventRecordExternal);
+            ctx->cap_pairs.push_back(CapPair{kernel, start, end});
+        } else {
+            cudaEventDestroy(start);
+        }
+        return;
+    }
     cudaEvent_t end = ctx->prof.take();
     if (!end) {
         ctx->prof.pool.push_back(start);
@@ -243,10 +261,97 @@ nbt_status nbt_ctx_sync(nbt_ctx ctx)
 {
     nbt_status s;
     if ((s = bind(ctx))) return s;
+    if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_ctx_sync during graph capture");
     return take_device_error(ctx, "nbt_ctx_sync");
 }
 
 uint64_t nbt_ctx_launch_count(nbt_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+nbt_status nbt_ctx_capture_begin(nbt_ctx ctx)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_ctx_capture_begin: already capturing");
+    NBT_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    ctx->capturing = true;
+    g_capturing = true;
+    ctx->cap_pairs.clear();
+    ctx->cap_launches0 = ctx->launches;
+    return NBT_OK;
+}
+
+nbt_status nbt_ctx_capture_end(nbt_ctx ctx, nbt_graph *out)
+{
+    nbt_status s;
+    if (!out) return fail(NBT_ERR_INVALID_ARG, "nbt_ctx_capture_end: null out");
+    *out = nullptr;
+    if ((s = bind(ctx))) return s;
+    if (!ctx->capturing) return fail(NBT_ERR_STATE, "nbt_ctx_capture_end: not capturing");
+    ctx->capturing = false;
+    g_capturing = false;
+    nbt_graph g = new (std::nothrow) nbt_graph_s();
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    if (e != cudaSuccess || !g) {
+        delete g;
+        for (auto &p : ctx->cap_pairs) { cudaEventDestroy(p.start); cudaEventDestroy(p.end); }
+        ctx->cap_pairs.clear();
+        return e != cudaSuccess ? cuda_fail(e, "nbt_ctx_capture_end") : fail(NBT_ERR_OUT_OF_MEMORY, "graph");
+    }
+    g->ctx = ctx;
+    g->graph = graph;
+    g->pairs.swap(ctx->cap_pairs);
+    g->kernels = ctx->launches - ctx->cap_launches0;
+    ctx->launches = ctx->cap_launches0;            // recorded, not launched
+    e = cudaGraphInstantiate(&g->exec, graph, 0);
+    if (e != cudaSuccess) {
+        nbt_graph_destroy(g);
+        return cuda_fail(e, "cudaGraphInstantiate");
+    }
+    *out = g;
+    return NBT_OK;
+}
+
+nbt_status nbt_graph_launch(nbt_graph g)
+{
+    nbt_status s;
+    if (!g) return fail(NBT_ERR_INVALID_ARG, "nbt_graph_launch: null graph");
+    if ((s = bind(g->ctx))) return s;
+    NBT_CUDA(cudaGraphLaunch(g->exec, g->ctx->stream));
+    g->ctx->launches += g->kernels;
+    return NBT_OK;
+}
+
+nbt_status nbt_graph_profile_read(nbt_graph g, int32_t kernel, double *total_ms, uint64_t *launches)
+{
+    nbt_status s;
+    if (!g || !total_ms || !launches) return fail(NBT_ERR_INVALID_ARG, "nbt_graph_profile_read: bad argument");
+    if ((s = bind(g->ctx))) return s;
+    NBT_CUDA(cudaStreamSynchronize(g->ctx->stream));
+    double ms = 0.0;
+    uint64_t n = 0;
+    for (auto &p : g->pairs) {
+        if (p.kernel != kernel) continue;
+        float t = 0.f;
+        NBT_CUDA(cudaEventElapsedTime(&t, p.start, p.end));
+        ms += t;
+        ++n;
+    }
+    *total_ms = ms;
+    *launches = n;
+    return NBT_OK;
+}
+
+void nbt_graph_destroy(nbt_graph g)
+{
+    if (!g) return;
+    cudaSetDevice(g->ctx->device);
+    cudaStreamSynchronize(g->ctx->stream);
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    for (auto &p : g->pairs) { cudaEventDestroy(p.start); cudaEventDestroy(p.end); }
+    delete g;
+}
 
 nbt_status nbt_ctx_set_profiling(nbt_ctx ctx, int enable)
 {
@@ -458,6 +563,7 @@ nbt_status nbt_map_update(nbt_map m, const int32_t *ijk, const uint8_t *codes, s
     if (!ijk || !codes) return fail(NBT_ERR_INVALID_ARG, "nbt_map_update: null input");
     const int32_t *dijk = ijk;
     const uint8_t *dcodes = codes;
+    if (ctx->capturing && !on_device) return fail(NBT_ERR_STATE, "nbt_map_update: host deltas during graph capture");
     if (!on_device) {
         for (size_t i = 0; i < n; ++i) {
             const int32_t *v = ijk + 3 * i;
@@ -594,6 +700,8 @@ nbt_status nbt_sample_perspectives(nbt_ctx ctx, const double poi[3], double r_s,
         (mode != NBT_SAMPLE_BALL && mode != NBT_SAMPLE_SURFACE))
         return fail(NBT_ERR_INVALID_ARG, "nbt_sample_perspectives: bad argument");
     if (n == 0) return NBT_OK;
+    if (ctx->capturing && !out_on_device)
+        return fail(NBT_ERR_STATE, "nbt_sample_perspectives: host output during graph capture");
     double *dst = xyz_out;
     if (!out_on_device) {
         if ((s = ctx->out_tmp.ensure((size_t)n * 24))) return s;
@@ -617,6 +725,8 @@ static nbt_status id_common(nbt_ctx ctx, nbt_map m, const double poi[3], const d
         return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": bad argument");
     if ((s = check_camera(cam))) return s;
     if (first < 0 || stride < 1) return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": bad first/stride");
+    if (ctx->capturing && (!persp_on_device || !out->on_device))
+        return fail(NBT_ERR_STATE, std::string(who) + ": host buffers during graph capture");
     int32_t n = (first < n_persp) ? (n_persp - first + stride - 1) / stride : 0;
     if (n == 0) return NBT_OK;
     if (!persp || !out->xyz || !out->gain) return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": null buffer");
@@ -697,6 +807,8 @@ nbt_status nbt_idbuf_create(nbt_ctx ctx, int32_t capacity_nb, int32_t max_persp,
     b->max_persp = max_persp;
     cudaError_t e = cudaMalloc(&b->d_xyz, (size_t)capacity_nb * max_persp * 24);
     if (e == cudaSuccess) e = cudaMalloc(&b->d_gain, (size_t)capacity_nb * max_persp * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&b->d_meta, 65 * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMemsetAsync(b->d_meta, 0, 65 * sizeof(int32_t), ctx->stream);
     if (e != cudaSuccess) {
         nbt_idbuf_destroy(b);
         return cuda_fail(e, "nbt_idbuf_create");
@@ -713,37 +825,29 @@ nbt_status nbt_idbuf_push(nbt_idbuf b, const nbt_ig_cloud *cloud, int32_t n)
     if ((s = bind(ctx))) return s;
     if (n < 1 || n > b->max_persp) return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_push: need 1 <= n <= max_persp");
     if (!cloud->xyz || !cloud->gain) return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_push: null cloud buffers");
-    int32_t slot;
-    if (b->count < b->capacity) {
-        slot = (b->head + b->count) % b->capacity;
-        b->count++;
-    } else {
-        slot = b->head;                              // evict the oldest
-        b->head = (b->head + 1) % b->capacity;
+    if (b->count < b->capacity) b->count++;
+    const double *sx = cloud->xyz, *sg = cloud->gain;
+    if (!cloud->on_device) {
+        if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_idbuf_push: host cloud during graph capture");
+        if ((s = ctx->out_tmp.ensure((size_t)n * 32)) || (s = ctx->stage_in[2].acquire((size_t)n * 32))) return s;
+        memcpy(ctx->stage_in[2].p, cloud->xyz, (size_t)n * 24);
+        memcpy((char *)ctx->stage_in[2].p + (size_t)n * 24, cloud->gain, (size_t)n * 8);
+        NBT_CUDA(cudaMemcpyAsync(ctx->out_tmp.p, ctx->stage_in[2].p, (size_t)n * 32, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        if ((s = ctx->stage_in[2].mark(ctx->stream))) return s;
+        sx = ctx->out_tmp.as<double>();
+        sg = sx + 3 * (size_t)n;
     }
-    b->sizes[slot] = n;
-    double *dx = b->d_xyz + (size_t)slot * b->max_persp * 3;
-    double *dg = b->d_gain + (size_t)slot * b->max_persp;
-    cudaMemcpyKind kind = cloud->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (cloud->on_device) {
-        NBT_CUDA(cudaMemcpyAsync(dx, cloud->xyz, (size_t)n * 24, kind, ctx->stream));
-        NBT_CUDA(cudaMemcpyAsync(dg, cloud->gain, (size_t)n * 8, kind, ctx->stream));
-        return NBT_OK;
-    }
-    HostStage &st = ctx->stage_in[2];
-    if ((s = st.acquire((size_t)n * 32))) return s;
-    memcpy(st.p, cloud->xyz, (size_t)n * 24);
-    memcpy((char *)st.p + (size_t)n * 24, cloud->gain, (size_t)n * 8);
-    NBT_CUDA(cudaMemcpyAsync(dx, st.p, (size_t)n * 24, kind, ctx->stream));
-    NBT_CUDA(cudaMemcpyAsync(dg, (char *)st.p + (size_t)n * 24, (size_t)n * 8, kind, ctx->stream));
-    return st.mark(ctx->stream);
+    return launch_idbuf_push(ctx, b, sx, sg, n);
 }
 
 nbt_status nbt_idbuf_clear(nbt_idbuf b)
 {
     if (!b) return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_clear: null buffer");
-    b->head = 0;
+    nbt_status s;
+    if ((s = bind(b->ctx))) return s;
     b->count = 0;
+    NBT_CUDA(cudaMemsetAsync(b->d_meta, 0, 65 * sizeof(int32_t), b->ctx->stream));
     return NBT_OK;
 }
 
@@ -761,12 +865,8 @@ nbt_status nbt_ig_query(nbt_idbuf b, const double *query_xyz, int32_t n_q, int q
         !(zero_eps >= 0) || !isfinite(zero_eps))
         return fail(NBT_ERR_INVALID_ARG, "nbt_ig_query: bad argument");
     if (n_q == 0) return NBT_OK;
-    IdwEntries E;
-    E.m = b->count;
-    for (int e = 0; e < b->count; ++e) {
-        E.slot[e] = (b->head + e) % b->capacity;
-        E.size[e] = b->sizes[E.slot[e]];
-    }
+    if (ctx->capturing && (!q_on_device || !out_on_device))
+        return fail(NBT_ERR_STATE, "nbt_ig_query: host buffers during graph capture");
     const double *dq = query_xyz;
     if (!q_on_device) {
         for (int32_t i = 0; i < n_q; ++i)
@@ -779,7 +879,7 @@ nbt_status nbt_ig_query(nbt_idbuf b, const double *query_xyz, int32_t n_q, int q
         if ((s = ctx->qout.ensure((size_t)n_q * 8))) return s;
         dout = ctx->qout.as<double>();
     }
-    if ((s = launch_idw(ctx, b, E, dq, n_q, power_p, zero_eps, normalize_weights, dout))) return s;
+    if ((s = launch_idw(ctx, b, dq, n_q, power_p, zero_eps, normalize_weights, dout))) return s;
     if (!out_on_device) return d2h_sync(ctx, g_out, dout, (size_t)n_q * 8);
     return NBT_OK;
 }
@@ -800,12 +900,8 @@ nbt_status nbt_info_cost(nbt_idbuf b, const double *pose_xyz, const double *pose
         return fail(NBT_ERR_INVALID_ARG, "nbt_info_cost: bad argument");
     if (n_traj == 0) return NBT_OK;
     const size_t n = (size_t)n_traj * per;
-    IdwEntries E;
-    E.m = b->count;
-    for (int e = 0; e < b->count; ++e) {
-        E.slot[e] = (b->head + e) % b->capacity;
-        E.size[e] = b->sizes[E.slot[e]];
-    }
+    if (ctx->capturing && (!poses_on_device || !out_on_device))
+        return fail(NBT_ERR_STATE, "nbt_info_cost: host buffers during graph capture");
     InfoCostArgs a;
     a.n_traj = n_traj;
     a.per = per;
@@ -840,7 +936,7 @@ nbt_status nbt_info_cost(nbt_idbuf b, const double *pose_xyz, const double *pose
         tmp = ctx->qout.as<double>();
         a.o_out = tmp; a.g_out = tmp + n; a.c_out = tmp + 2 * n;
     }
-    if ((s = launch_info_cost(ctx, b, E, a, power_p, zero_eps, normalize))) return s;
+    if ((s = launch_info_cost(ctx, b, a, power_p, zero_eps, normalize))) return s;
     if (out_on_device) return NBT_OK;
     const size_t total = n * 16 + (size_t)n_traj * 8;
     if ((s = ctx->stage_out.acquire(total))) return s;
@@ -860,6 +956,7 @@ void nbt_idbuf_destroy(nbt_idbuf b)
     cudaStreamSynchronize(b->ctx->stream);
     if (b->d_xyz) cudaFree(b->d_xyz);
     if (b->d_gain) cudaFree(b->d_gain);
+    if (b->d_meta) cudaFree(b->d_meta);
     delete b;
 }
 

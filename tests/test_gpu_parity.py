@@ -592,3 +592,62 @@ def test_info_cost_matches_oracle(nbt, ctx, on_device):
         bad = pos.copy(); bad[5] = poi
         buf.info_cost(bad, axis, 31, poi, cut, 25.0)
     assert ei.value.status == nbt.ERR_DEGENERATE
+
+
+# ------------------------------------------------------------------ CUDA graphs
+
+def test_graph_capture_replays_the_cycle(nbt):
+    """An MHP cycle (deltas -> sampling -> ID -> push -> IDW) captured into CUDA graphs and
+    replayed gives exactly the eager results, including the device-side ring buffer."""
+    import torch
+    cfg = CONFIGS["A"]
+    codes = cfg.map_codes()
+    rng = np.random.default_rng(0)
+    deltas = []
+    for _ in range(2):
+        ijk = rng.integers(0, cfg.n, (300, 3)).astype(np.int32)
+        deltas.append((torch.from_numpy(ijk).cuda(), torch.from_numpy(rng.integers(0, 3, 300).astype(np.uint8)).cuda()))
+    q = torch.from_numpy(oracle.sample_perspectives(cfg.poi, 30.0, 200, seed=9)).cuda()
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 24, 18)
+
+    def setup():
+        ctx = nbt.Ctx(0)
+        m = nbt.Map(ctx, nbt.map_desc(cfg.n, cfg.n, cfg.n, cfg.voxel_size))
+        m.upload(codes)
+        st = dict(ctx=ctx, m=m, persp=torch.empty((40, 3), dtype=torch.float64, device="cuda"),
+                  cloud=nbt.empty_cloud(40, device="cuda"), buf=nbt.IdBuffer(ctx, 3, 40),
+                  out=torch.empty(200, dtype=torch.float64, device="cuda"))
+        return st
+
+    def cycle(st, c):
+        ijk, val = deltas[c % 2]
+        st["m"].update(ijk, val)
+        nbt.sample_perspectives(st["ctx"], cfg.poi, 20.0, 40, 100 + c % 2, 0, out=st["persp"])
+        nbt.id_compute(st["ctx"], st["m"], cfg.poi, st["persp"], cam, cfg.range_, out=st["cloud"])
+        st["buf"].push(st["cloud"], 40)
+        st["buf"].query(q, out=st["out"])
+
+    def snapshot(st):
+        st["ctx"].sync()
+        return (st["m"].download(), st["cloud"].counts.cpu().numpy(), st["cloud"].gain.cpu().numpy(),
+                st["out"].cpu().numpy())
+
+    A, B = setup(), setup()
+    cycle(A, 0); cycle(B, 0)                       # warm-up: sizes every scratch buffer
+    graphs = []
+    for c in (0, 1):
+        B["ctx"].capture_begin()
+        cycle(B, c)
+        graphs.append(B["ctx"].capture_end())
+    for c in range(1, 7):
+        cycle(A, c)
+        graphs[c % 2].launch()
+        for a, b in zip(snapshot(A), snapshot(B)):
+            assert np.array_equal(a, b), c
+    with pytest.raises(nbt.NbtError) as ei:        # host buffers are refused while capturing
+        B["ctx"].capture_begin()
+        try:
+            nbt.id_compute(B["ctx"], B["m"], cfg.poi, np.zeros((2, 3)), cam, cfg.range_)
+        finally:
+            B["ctx"].capture_end().close()
+    assert ei.value.status == nbt.ERR_STATE
