@@ -751,6 +751,17 @@ FrameArgs frame_args(nbt_map m, const double *d_persp, int32_t first, int32_t st
     return A;
 }
 
+// Preferred shared-memory carveout (percent of the unified L1/shared capacity) for the
+// trace kernel: NBT_TRACE_CARVEOUT, default 25 (-1 leaves the driver's choice).
+int trace_carveout()
+{
+    static int v = [] {
+        const char *e = getenv("NBT_TRACE_CARVEOUT");
+        return e ? atoi(e) : 25;
+    }();
+    return v;
+}
+
 // Idle lanes a warp waits for before refilling: NBT_REFILL_MIN, default 8 (profiles/r01_trace_variants.md).
 int refill_threshold()
 {
@@ -808,6 +819,19 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     const bool wide = max_ray_voxels(L.cam, L.range, m->desc.voxel_size) > kInt32MaxVoxels;
     const bool morton = m->layout == kLayoutMorton;
     if (ctx->trace_blocks_per_sm == 0) {
+        // smallest shared-memory carveout that holds the walk queues of the resident blocks,
+        // so the rest of the SM's 256 KB stays L1 for the map lines
+        const int carve = trace_carveout();
+        if (carve >= 0) {
+            NBT_CUDA(cudaFuncSetAttribute(k_id_trace<int, kLayoutLinear, kBatchK, false>,
+                                          cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            NBT_CUDA(cudaFuncSetAttribute(k_id_trace<int, kLayoutMorton, kBatchK, false>,
+                                          cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            NBT_CUDA(cudaFuncSetAttribute(k_id_trace<long long, kLayoutLinear, kBatchK, false>,
+                                          cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            NBT_CUDA(cudaFuncSetAttribute(k_id_trace<long long, kLayoutMorton, kBatchK, false>,
+                                          cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+        }
         int b = 0;
         NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &b, k_id_trace<int, kLayoutLinear, kBatchK, false>, kWarpsPerBlock * 32, 0));

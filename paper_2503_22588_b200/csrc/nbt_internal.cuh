@@ -120,6 +120,8 @@ struct ProfScope {
 // ----------------------------------------------------------------- handles
 
 struct nbt_ctx_s {
+    int refs = 1;                     // 1 for the ctx itself + 1 per live map / ID buffer / graph
+    bool closed = false;              // nbt_ctx_destroy called
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;

@@ -183,6 +183,34 @@ ProfScope::~ProfScope()
 
 static bool finite3(const double *p) { return isfinite(p[0]) && isfinite(p[1]) && isfinite(p[2]); }
 
+// The ctx is released when nbt_ctx_destroy has been called AND every map, ID buffer and
+// graph created on it has been destroyed (handles may be destroyed in any order).
+static void ctx_free(nbt_ctx ctx)
+{
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    DevBuf *bufs[] = {&ctx->persp, &ctx->frames, &ctx->totals, &ctx->counter, &ctx->out_tmp, &ctx->deltas,
+                      &ctx->keys, &ctx->keys_alt, &ctx->cub_tmp, &ctx->queries, &ctx->qout, &ctx->idw_tmp, &ctx->poses, &ctx->dbg};
+    for (DevBuf *b : bufs) b->release();
+    for (auto &st : ctx->stage_in) st.release();
+    for (auto &v : ctx->prof.pending)
+        for (auto &pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
+    ctx->stage_out.release();
+    if (ctx->d_err) cudaFree(ctx->d_err);
+    if (ctx->h_err) cudaFreeHost(ctx->h_err);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+static void ctx_retain(nbt_ctx ctx) { ctx->refs++; }
+
+static void ctx_release(nbt_ctx ctx)
+{
+    if (--ctx->refs == 0) ctx_free(ctx);
+}
+
+
 }  // namespace nbt
 
 using namespace nbt;
@@ -299,6 +327,7 @@ nbt_status nbt_ctx_capture_end(nbt_ctx ctx, nbt_graph *out)
         return e != cudaSuccess ? cuda_fail(e, "nbt_ctx_capture_end") : fail(NBT_ERR_OUT_OF_MEMORY, "graph");
     }
     g->ctx = ctx;
+    ctx_retain(ctx);
     g->graph = graph;
     g->pairs.swap(ctx->cap_pairs);
     g->kernels = ctx->launches - ctx->cap_launches0;
@@ -350,7 +379,9 @@ void nbt_graph_destroy(nbt_graph g)
     if (g->exec) cudaGraphExecDestroy(g->exec);
     if (g->graph) cudaGraphDestroy(g->graph);
     for (auto &p : g->pairs) { cudaEventDestroy(p.start); cudaEventDestroy(p.end); }
+    nbt_ctx ctx = g->ctx;
     delete g;
+    ctx_release(ctx);
 }
 
 nbt_status nbt_ctx_set_profiling(nbt_ctx ctx, int enable)
@@ -389,21 +420,9 @@ nbt_status nbt_ctx_profile_read(nbt_ctx ctx, int32_t kernel, double *total_ms, u
 
 void nbt_ctx_destroy(nbt_ctx ctx)
 {
-    if (!ctx) return;
-    cudaSetDevice(ctx->device);
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    DevBuf *bufs[] = {&ctx->persp, &ctx->frames, &ctx->totals, &ctx->counter, &ctx->out_tmp, &ctx->deltas,
-                      &ctx->keys, &ctx->keys_alt, &ctx->cub_tmp, &ctx->queries, &ctx->qout, &ctx->idw_tmp, &ctx->poses, &ctx->dbg};
-    for (DevBuf *b : bufs) b->release();
-    for (auto &st : ctx->stage_in) st.release();
-    for (auto &v : ctx->prof.pending)
-        for (auto &pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
-    for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
-    ctx->stage_out.release();
-    if (ctx->d_err) cudaFree(ctx->d_err);
-    if (ctx->h_err) cudaFreeHost(ctx->h_err);
-    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
-    delete ctx;
+    if (!ctx || ctx->closed) return;
+    ctx->closed = true;
+    ctx_release(ctx);
 }
 
 // --------------------------------------------------------------------- map
@@ -445,6 +464,7 @@ nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
     nbt_map m = new (std::nothrow) nbt_map_s();
     if (!m) return fail(NBT_ERR_OUT_OF_MEMORY, "nbt_map_create");
     m->ctx = ctx;
+    ctx_retain(ctx);
     m->desc = *desc;
     m->px = desc->nx + 2 * kBorder; m->py = desc->ny + 2 * kBorder; m->pz = desc->nz + 2 * kBorder;
     m->nvox_pad = (uint64_t)m->px * m->py * m->pz;
@@ -469,7 +489,7 @@ nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
     m->nwords = (size_t)((m->nvox_pad + 15) / 16);
     cudaError_t e = cudaMalloc(&m->d_words, m->nwords * 4);
     if (e != cudaSuccess) {
-        delete m;
+        nbt_map_destroy(m);
         return cuda_fail(e, "nbt_map_create: cudaMalloc");
     }
     // all Unknown inside, sentinel ring outside: pack from a null code array
@@ -624,7 +644,9 @@ void nbt_map_destroy(nbt_map m)
     cudaSetDevice(m->ctx->device);
     cudaStreamSynchronize(m->ctx->stream);
     if (m->d_words) cudaFree(m->d_words);
+    nbt_ctx ctx = m->ctx;
     delete m;
+    ctx_release(ctx);
 }
 
 // ------------------------------------------------------------------ camera
@@ -803,6 +825,7 @@ nbt_status nbt_idbuf_create(nbt_ctx ctx, int32_t capacity_nb, int32_t max_persp,
     nbt_idbuf b = new (std::nothrow) nbt_idbuf_s();
     if (!b) return fail(NBT_ERR_OUT_OF_MEMORY, "nbt_idbuf_create");
     b->ctx = ctx;
+    ctx_retain(ctx);
     b->capacity = capacity_nb;
     b->max_persp = max_persp;
     cudaError_t e = cudaMalloc(&b->d_xyz, (size_t)capacity_nb * max_persp * 24);
@@ -957,7 +980,9 @@ void nbt_idbuf_destroy(nbt_idbuf b)
     if (b->d_xyz) cudaFree(b->d_xyz);
     if (b->d_gain) cudaFree(b->d_gain);
     if (b->d_meta) cudaFree(b->d_meta);
+    nbt_ctx ctx = b->ctx;
     delete b;
+    ctx_release(ctx);
 }
 
 // -------------------------------------------------------------- test hooks

@@ -651,3 +651,23 @@ def test_graph_capture_replays_the_cycle(nbt):
         finally:
             B["ctx"].capture_end().close()
     assert ei.value.status == nbt.ERR_STATE
+
+
+def test_handles_destroyed_in_any_order(nbt):
+    """Destroying the ctx before its maps, buffers and graphs defers the release (no crash)."""
+    import torch
+    ctx = nbt.Ctx(0)
+    m = nbt.Map(ctx, nbt.map_desc(8, 8, 8, 1.0))
+    buf = nbt.IdBuffer(ctx, 2, 4)
+    buf.push(nbt.IgCloud(torch.zeros((4, 3), dtype=torch.float64, device="cuda"),
+                         torch.ones(4, dtype=torch.float64, device="cuda"), None), 4)
+    ctx.capture_begin()
+    buf.push(nbt.IgCloud(torch.zeros((4, 3), dtype=torch.float64, device="cuda"),
+                         torch.ones(4, dtype=torch.float64, device="cuda"), None), 4)
+    g = ctx.capture_end()
+    ctx.close()
+    g.launch()
+    g.close()
+    assert (m.download() == 0).all()
+    buf.close()
+    m.close()
