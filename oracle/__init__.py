@@ -40,7 +40,7 @@ def build(force: bool = False) -> str:
 class Map(C.Structure):
     _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
                 ("voxel_size", C.c_double), ("origin", C.c_double * 3), ("gain", C.c_double * 3),
-                ("outside_policy", C.c_int32), ("codes", C.POINTER(C.c_uint8))]
+                ("outside_policy", C.c_int32), ("codes", C.POINTER(C.c_uint8)), ("levels", C.POINTER(C.c_uint8))]
 
 
 class Camera(C.Structure):
@@ -51,7 +51,7 @@ class Camera(C.Structure):
 
 class Ray(C.Structure):
     _fields_ = [("n_u", C.c_int64), ("n_f", C.c_int64), ("n_o", C.c_int64), ("lookups", C.c_int64),
-                ("visits", C.c_int64), ("g", C.c_double), ("stop", C.c_int32)]
+                ("visits", C.c_int64), ("g63", C.c_int64), ("g", C.c_double), ("stop", C.c_int32)]
 
 
 _lib = None
@@ -69,7 +69,7 @@ def lib():
         L.orc_camera_num_rays.restype = C.c_int32
         L.orc_trace_ray.argtypes = [C.POINTER(Map), ip, ip, C.c_int32, ip, u8p, ip, C.POINTER(Ray)]
         L.orc_id_compute.argtypes = [C.POINTER(Map), dp, dp, C.c_int32, C.POINTER(Camera), C.c_double,
-                                     C.c_int32, dp, dp, i64p, ip]
+                                     C.c_int32, dp, dp, i64p, i64p, ip]
         L.orc_perspective_rays.argtypes = [C.POINTER(Map), dp, dp, C.POINTER(Camera), C.c_double, ip, ip, i64p]
         L.orc_frame_export.argtypes = [C.POINTER(Map), dp, dp, C.POINTER(Camera), C.c_double, ip, dp]
         L.orc_idw_query.argtypes = [C.c_int32, ip, C.POINTER(dp), C.POINTER(dp), dp, C.c_int32, C.c_double,
@@ -81,6 +81,8 @@ def lib():
         L.orc_eq1.restype = None
         L.orc_classify.argtypes = [C.POINTER(C.c_float), u8p, C.c_int64, C.c_double, C.c_double, u8p]
         L.orc_classify.restype = None
+        L.orc_quantize_prob.argtypes = [C.POINTER(C.c_float), u8p, C.c_int64, C.c_double, C.c_double, u8p, u8p]
+        L.orc_quantize_prob.restype = None
         L.orc_map_update.argtypes = [u8p, C.c_int32, C.c_int32, C.c_int32, ip, u8p, C.c_int64]
         L.orc_orientation_factor.argtypes = [dp, dp, dp, C.c_double, dp]
         L.orc_info_cost.argtypes = [C.c_int32, ip, C.POINTER(dp), C.POINTER(dp), dp, dp, C.c_int32, C.c_int32, dp,
@@ -100,11 +102,14 @@ class OracleMap:
     """Keeps the code array alive while the C struct points into it."""
 
     def __init__(self, codes_zyx, voxel_size=1.0, origin=(0.0, 0.0, 0.0), gain=(1.0, 0.12, 0.03),
-                 outside_policy=0):
+                 outside_policy=0, levels=None):
+        """levels (uint8, 0..63, same shape) switches on the per-voxel probability P = level/63."""
         self.codes = np.ascontiguousarray(codes_zyx, dtype=np.uint8)
+        self.levels = None if levels is None else np.ascontiguousarray(levels, dtype=np.uint8)
         nz, ny, nx = self.codes.shape
         self.s = Map(nx, ny, nz, float(voxel_size), (C.c_double * 3)(*origin), (C.c_double * 3)(*gain),
-                     int(outside_policy), _p(self.codes, C.c_uint8))
+                     int(outside_policy), _p(self.codes, C.c_uint8),
+                     _p(self.levels, C.c_uint8) if self.levels is not None else None)
 
 
 def camera_from_fov(fov_h, fov_v, w, h) -> Camera:
@@ -143,18 +148,19 @@ def trace_ray(m: OracleMap, o_q16, e_q16, max_visits=4096):
     return ijk[:k].copy(), codes[:k].copy(), r
 
 
-def id_compute(m: OracleMap, poi, persp_xyz, cam: Camera, range_, nthreads=1):
-    """The whole ID: returns (xyz [n,3], gain [n], counts [n,4] = T_U,T_F,T_O,lookups)."""
+def id_compute(m: OracleMap, poi, persp_xyz, cam: Camera, range_, nthreads=1, with_tg=False):
+    """The whole ID: returns (xyz [n,3], gain [n], counts [n,4] = T_U,T_F,T_O,lookups)
+    (+ tg [n] = 63 * sum of g_R in the per-voxel-probability mode if with_tg)."""
     poi = np.ascontiguousarray(poi, dtype=np.float64)
     P = np.ascontiguousarray(persp_xyz, dtype=np.float64).reshape(-1, 3)
     n = P.shape[0]
-    xyz = np.zeros((n, 3)); gain = np.zeros(n); counts = np.zeros((n, 4), np.int64)
+    xyz = np.zeros((n, 3)); gain = np.zeros(n); counts = np.zeros((n, 4), np.int64); tg = np.zeros(n, np.int64)
     bad = C.c_int32(-1)
     st = lib().orc_id_compute(C.byref(m.s), _d(poi), _d(P), n, C.byref(cam), float(range_), int(nthreads),
-                              _d(xyz), _d(gain), _p(counts, C.c_int64), C.byref(bad))
+                              _d(xyz), _d(gain), _p(counts, C.c_int64), _p(tg, C.c_int64), C.byref(bad))
     if st:
         raise OracleError(st, f"id_compute (perspective {bad.value})")
-    return xyz, gain, counts
+    return (xyz, gain, counts, tg) if with_tg else (xyz, gain, counts)
 
 
 def perspective_rays(m: OracleMap, poi, p, cam: Camera, range_, with_counts=True):
@@ -273,3 +279,13 @@ def info_cost(entries, pos, axis, per, poi, cos_cut, w_i, eps=1e-7, power_p=2.0,
     if st:
         raise OracleError(st, "info_cost")
     return o, g, c
+
+
+def quantize_prob(p, observed, t_occ=0.5, t_free=0.5):
+    """(codes, levels) of the per-voxel-probability map (S:69 states, P -> level = rne(63 P))."""
+    p = np.ascontiguousarray(p, dtype=np.float32)
+    obs = np.ascontiguousarray(observed, dtype=np.uint8)
+    codes = np.zeros(p.shape, np.uint8); levels = np.zeros(p.shape, np.uint8)
+    lib().orc_quantize_prob(_p(p, C.c_float), _p(obs, C.c_uint8), p.size, float(t_occ), float(t_free),
+                            _p(codes, C.c_uint8), _p(levels, C.c_uint8))
+    return codes, levels

@@ -53,7 +53,25 @@ typedef struct {
     double gain[3];          /* g[U], g[F], g[O]  (Eq. 2, Q15) */
     int32_t outside_policy;  /* 0 = outside counts as Unknown, 1 = clip */
     const uint8_t *codes;    /* x fastest, nx*ny*nz */
+    const uint8_t *levels;   /* NULL: per-state gains (Q15).  Else per-voxel probability
+                                P = level / 63 (level 0..63) and Eq. 2 exactly (f1, Q32) */
 } orc_map;
+
+#define PLEVELS 63           /* P quantised to k / 63 (reading Q32) */
+
+/* Eq. 2 for a quantised probability, in units of 1/63:
+ * Unknown -> 1, Free -> P, Occupied -> 1 - P. */
+static int64_t gain_q63(int code, int level)
+{
+    if (code == 0) return PLEVELS;
+    if (code == 1) return level;
+    return PLEVELS - level;
+}
+
+static int level_at(const orc_map *m, int64_t x, int64_t y, int64_t z)
+{
+    return m->levels[x + (int64_t)m->nx * (y + (int64_t)m->ny * z)];
+}
 
 /* code of voxel (x,y,z); -1 if outside the grid */
 static int code_at(const orc_map *m, int64_t x, int64_t y, int64_t z)
@@ -213,6 +231,7 @@ typedef struct {
     int64_t n_u, n_f, n_o;   /* per-state counts of the N_O counted voxels (Eq. 2) */
     int64_t lookups;         /* in-grid visits (memory-touching subset) */
     int64_t visits;          /* voxels visited including uncounted (clipped) ones */
+    int64_t g63;             /* per-voxel-probability mode: 63 * g_R as an integer */
     double g;                /* g_R = sum of g(v_i) over the counted voxels, in visit order */
     int32_t stop;            /* 0 = reached the endpoint voxel, 1 = stopped on Occupied */
 } orc_ray;
@@ -274,7 +293,14 @@ int orc_trace_ray(const orc_map *m, const int32_t o[3], const int32_t e[3], int3
             /* clipped: not counted */
         } else {
             int c = code < 0 ? 0 : code;
-            r->g += m->gain[c];
+            if (m->levels) {
+                int lv = code < 0 ? 0 : level_at(m, v[0], v[1], v[2]);
+                int64_t gq = gain_q63(c, lv);
+                r->g63 += gq;
+                r->g += (c == 0) ? 1.0 : (c == 1 ? (double)lv / PLEVELS : 1.0 - (double)lv / PLEVELS);
+            } else {
+                r->g += m->gain[c];
+            }
             if (c == 0) r->n_u++;
             else if (c == 1) r->n_f++;
             else { r->n_o++; r->stop = 1; break; }
@@ -316,6 +342,7 @@ typedef struct {
     double xyz[3];
     double gain;                  /* g_P,j */
     int64_t t_u, t_f, t_o, lookups;
+    int64_t t_g;                  /* per-voxel-probability mode: 63 * sum of g_R */
 } orc_persp_out;
 
 /* g_P,j for perspective j = (1/N_E) sum_k g_R,k,j with
@@ -330,7 +357,7 @@ static int one_perspective(const orc_map *m, const double poi[3], const double p
     int st = orc_frame_q16(m, poi, p, cam, range, &f, NULL, NULL, NULL);
     if (st) return st;
     int32_t ne = orc_camera_num_rays(cam);
-    int64_t tu = 0, tf = 0, to = 0, tl = 0;
+    int64_t tu = 0, tf = 0, to = 0, tl = 0, tg = 0;
     double direct = 0.0;
     for (int32_t k = 0; k < ne; ++k) {
         int32_t o[3], e[3];
@@ -338,15 +365,17 @@ static int one_perspective(const orc_map *m, const double poi[3], const double p
         orc_ray r;
         if ((st = orc_trace_ray(m, o, e, 0, NULL, NULL, NULL, &r))) return st;
         direct += r.g;
-        tu += r.n_u; tf += r.n_f; to += r.n_o; tl += r.lookups;
+        tu += r.n_u; tf += r.n_f; to += r.n_o; tl += r.lookups; tg += r.g63;
     }
-    double canon = (((double)tu * m->gain[0] + (double)tf * m->gain[1]) + (double)to * m->gain[2]) / (double)ne;
+    double canon = m->levels ? (double)tg / ((double)PLEVELS * (double)ne)
+                             : (((double)tu * m->gain[0] + (double)tf * m->gain[1]) + (double)to * m->gain[2]) /
+                                   (double)ne;
     direct = direct / (double)ne;
     double scale = fabs(canon) > 1.0 ? fabs(canon) : 1.0;
     if (fabs(direct - canon) > 1e-12 * scale) return ORC_ERR_SELFCHECK;
     memcpy(out->xyz, p, 3 * sizeof(double));
     out->gain = canon;
-    out->t_u = tu; out->t_f = tf; out->t_o = to; out->lookups = tl;
+    out->t_u = tu; out->t_f = tf; out->t_o = to; out->lookups = tl; out->t_g = tg;
     return ORC_OK;
 }
 
@@ -356,7 +385,7 @@ static int one_perspective(const orc_map *m, const double poi[3], const double p
  * Returns the first failing perspective's index in *bad_index. */
 int orc_id_compute(const orc_map *m, const double poi[3], const double *persp, int32_t n_persp,
                    const orc_camera *cam, double range, int32_t nthreads,
-                   double *xyz_out, double *gain_out, int64_t *counts_out, int32_t *bad_index)
+                   double *xyz_out, double *gain_out, int64_t *counts_out, int64_t *tg_out, int32_t *bad_index)
 {
     if (!m || !poi || !persp || !cam || n_persp < 0 || !(range > 0)) return ORC_ERR_INVALID_ARG;
     if (cam->width < 1 || cam->height < 1) return ORC_ERR_INVALID_ARG;
@@ -386,6 +415,7 @@ int orc_id_compute(const orc_map *m, const double poi[3], const double *persp, i
             counts_out[4 * (int64_t)j + 2] = o.t_o;
             counts_out[4 * (int64_t)j + 3] = o.lookups;
         }
+        if (tg_out) tg_out[j] = o.t_g;
     }
     if (bad_index) *bad_index = bad;
     return status;
@@ -584,6 +614,21 @@ void orc_eq1(const double poi[3], double r_s, const double X[3], double x_r, dou
 }
 
 /* ------------------------------------------------- classification (Q16) */
+
+/* Per-voxel probability for the exact Eq. 2 (f1): state by the rule below, and
+ * level = round-half-even(clamp(P, 0, 1) * 63) (reading Q32); unobserved -> level 0. */
+void orc_quantize_prob(const float *p, const uint8_t *observed, int64_t n, double t_occ, double t_free,
+                       uint8_t *codes_out, uint8_t *levels_out)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        double v = (double)p[i];
+        int c = 0;
+        if (observed[i]) c = (v >= t_occ) ? 2 : (v <= t_free ? 1 : 0);
+        codes_out[i] = (uint8_t)c;
+        double cl = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+        levels_out[i] = observed[i] ? (uint8_t)nearbyint(cl * PLEVELS) : 0;
+    }
+}
 
 /* unobserved -> Unknown; P >= t_occ -> Occupied; P <= t_free -> Free; else Unknown. */
 void orc_classify(const float *p, const uint8_t *observed, int64_t n, double t_occ, double t_free,
