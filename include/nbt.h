@@ -131,6 +131,11 @@ typedef struct {
 void nbt_map_desc_default(nbt_map_desc *desc, int32_t nx, int32_t ny, int32_t nz, double voxel_size);
 /* Create a map whose every voxel is Unknown (UFOMap's default). */
 nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out);
+/* Create a map that also stores each voxel's occupancy probability, so the ID scores every
+ * voxel by Eq. 2 exactly: Unknown 1, Free P, Occupied 1 - P,
+ * with P quantised to k/63 (reading Q32) and desc->gain unused by the ID.  8 bits per voxel.
+ * State-only writes (nbt_map_upload, nbt_map_update) store P_F = gain[1], P_O = 1 - gain[2]. */
+nbt_status nbt_map_create_prob(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out);
 /* Replace all voxels: codes[x + nx*(y + ny*z)] in {0,1,2}; n must equal nx*ny*nz.
  * Synchronizes the ctx stream; a code >= 3 gives NBT_ERR_INVALID_ARG (map unchanged
  * for host input; for device input the offending voxels become Unknown). */
@@ -138,6 +143,12 @@ nbt_status nbt_map_upload(nbt_map map, const uint8_t *codes, size_t n, int on_de
 /* Replace all voxels from occupancy probabilities (Q16): observed[i] == 0 ->
  * Unknown; p[i] >= t_occ -> Occupied; p[i] <= t_free -> Free; else Unknown. */
 nbt_status nbt_map_upload_prob(nbt_map map, const float *p, const uint8_t *observed, size_t n,
+                               int on_device, double t_occ, double t_free);
+/* Per-voxel-probability deltas (maps of nbt_map_create_prob; on a state-only map the
+ * probabilities are ignored): voxel i := classify(p[i], observed[i]) by S:69 with the
+ * probability level round-half-even(63 clamp(p, 0, 1)).  Same ordering and validation as
+ * nbt_map_update. */
+nbt_status nbt_map_update_prob(nbt_map map, const int32_t *ijk, const float *p, const uint8_t *observed, size_t n,
                                int on_device, double t_occ, double t_free);
 /* Apply n sparse deltas: voxel (ijk[3i], ijk[3i+1], ijk[3i+2]) := codes[i].  Indices must
  * lie inside the grid and codes in {0,1,2}.  Duplicated voxels resolve to the LAST delta
@@ -148,6 +159,8 @@ nbt_status nbt_map_update(nbt_map map, const int32_t *ijk, const uint8_t *codes,
 nbt_status nbt_map_device_buffer(nbt_map map, void **dev_ptr, size_t *bytes);
 /* Unpack to dense x-fastest uint8 codes (host buffer of n = nx*ny*nz bytes); syncs. */
 nbt_status nbt_map_download(nbt_map map, uint8_t *codes_out, size_t n);
+/* Probability levels (P = level / 63; 0 for Unknown) of a nbt_map_create_prob map; syncs. */
+nbt_status nbt_map_download_levels(nbt_map map, uint8_t *levels_out, size_t n);
 /* Copy of the descriptor. */
 nbt_status nbt_map_get_desc(nbt_map map, nbt_map_desc *out);
 void       nbt_map_destroy(nbt_map map);

@@ -34,8 +34,9 @@ EXPORTS = [
     "nbt_ctx_create", "nbt_ctx_set_stream", "nbt_ctx_sync", "nbt_ctx_destroy", "nbt_ctx_launch_count",
     "nbt_ctx_set_profiling", "nbt_ctx_profile_read",
     "nbt_ctx_capture_begin", "nbt_ctx_capture_end", "nbt_graph_launch", "nbt_graph_profile_read", "nbt_graph_destroy",
-    "nbt_map_desc_default", "nbt_map_create", "nbt_map_upload", "nbt_map_upload_prob", "nbt_map_update",
-    "nbt_map_device_buffer", "nbt_map_download", "nbt_map_get_desc", "nbt_map_destroy",
+    "nbt_map_desc_default", "nbt_map_create", "nbt_map_create_prob", "nbt_map_upload", "nbt_map_upload_prob",
+    "nbt_map_update", "nbt_map_update_prob", "nbt_map_device_buffer", "nbt_map_download", "nbt_map_download_levels",
+    "nbt_map_get_desc", "nbt_map_destroy",
     "nbt_camera_from_fov", "nbt_camera_from_grid_scaling", "nbt_camera_num_rays",
     "nbt_sample_perspectives", "nbt_id_compute", "nbt_id_compute_slice",
     "nbt_idbuf_create", "nbt_idbuf_push", "nbt_idbuf_clear", "nbt_idbuf_size", "nbt_ig_query", "nbt_idbuf_destroy",
@@ -100,6 +101,9 @@ def lib():
         "nbt_graph_destroy": ([vp], None),
         "nbt_map_desc_default": ([C.POINTER(MapDesc), i32, i32, i32, dbl], None),
         "nbt_map_create": ([vp, C.POINTER(MapDesc), C.POINTER(vp)], C.c_int),
+        "nbt_map_create_prob": ([vp, C.POINTER(MapDesc), C.POINTER(vp)], C.c_int),
+        "nbt_map_update_prob": ([vp, vp, vp, vp, sz, C.c_int, dbl, dbl], C.c_int),
+        "nbt_map_download_levels": ([vp, vp, sz], C.c_int),
         "nbt_map_upload": ([vp, vp, sz, C.c_int], C.c_int),
         "nbt_map_upload_prob": ([vp, vp, vp, sz, C.c_int, dbl, dbl], C.c_int),
         "nbt_map_update": ([vp, vp, vp, sz, C.c_int], C.c_int),
@@ -266,10 +270,12 @@ def map_desc(nx, ny, nz, voxel_size, origin=(0.0, 0.0, 0.0), gain=None, outside_
 class Map:
     """nbt_map: the device-resident 2-bit voxel store (row a1)."""
 
-    def __init__(self, ctx: Ctx, desc: MapDesc):
+    def __init__(self, ctx: Ctx, desc: MapDesc, prob: bool = False):
+        """prob=True: also store per-voxel probabilities for the exact Eq. 2 (f1)."""
         h = C.c_void_p()
-        check(lib().nbt_map_create(ctx.h, C.byref(desc), C.byref(h)))
-        self.h, self.ctx, self.desc = h, ctx, desc
+        create = lib().nbt_map_create_prob if prob else lib().nbt_map_create
+        check(create(ctx.h, C.byref(desc), C.byref(h)))
+        self.h, self.ctx, self.desc, self.prob = h, ctx, desc, prob
 
     @property
     def shape(self):
@@ -297,6 +303,20 @@ class Map:
             raise ValueError("ijk and codes must both be host or both device")
         n = (k2.numel() if _is_torch(k2) else k2.size) if k2 is not None else 0
         check(lib().nbt_map_update(self.h, pi, pc, n, dev))
+
+    def update_prob(self, ijk, p, observed, t_occ=0.5, t_free=0.5):
+        pi, dev, k1 = _ptr(ijk, np.int32)
+        pp, dev2, k2 = _ptr(p, np.float32)
+        po, dev3, k3 = _ptr(observed, np.uint8)
+        if not dev == dev2 == dev3:
+            raise ValueError("ijk, p and observed must all be host or all device")
+        n = (k2.numel() if _is_torch(k2) else k2.size) if k2 is not None else 0
+        check(lib().nbt_map_update_prob(self.h, pi, pp, po, n, dev, float(t_occ), float(t_free)))
+
+    def download_levels(self):
+        out = np.empty(self.shape, np.uint8)
+        check(lib().nbt_map_download_levels(self.h, C.c_void_p(out.ctypes.data), self.nvox))
+        return out
 
     def device_buffer(self):
         p, n = C.c_void_p(), C.c_size_t()

@@ -37,6 +37,7 @@ namespace nbt {
 namespace {
 
 constexpr int kFrameInts = 20;   // O, A, Rh, Uh, Rc, Uc (3 each, Q16), status, pad
+constexpr int kTotals = 5;       // per perspective: T_U, T_F, T_O, L, T_G (Eq. 2 gain, 1/63 units)
 constexpr int kWarpsPerBlock = 8;
 constexpr int kQShift = 12;      // walk coordinates: Q12
 // Trace kernel shape: K voxels per speculative batch; PIPE = the next batch's loads are
@@ -83,6 +84,7 @@ struct Walk {
     int s, n;                  // current step (0 = origin voxel) and total steps
     int s0;                    // step at which the walk entered the grid
     uint32_t nf;               // Free voxels counted so far in the grid
+    uint32_t ng;               // 8-bit store: Eq. 2 gain counted so far (1/63 units)
     uint32_t pre;              // visits outside the grid before entering it
     int vx, vy, vz;            // voxel coordinates (entry path / debug only)
     int sx, sy, sz;            // +-1 per axis
@@ -121,6 +123,7 @@ __device__ __forceinline__ void walk_setup(Walk<T> &w, const int o[3], const int
     w.s = 0;
     w.n = n;
     w.nf = 0;
+    w.ng = 0;
     w.pre = 0;
 }
 
@@ -222,13 +225,16 @@ __device__ bool walk_enter(Walk<T> &w, const MapView &m, int32_t *rec_ijk, uint8
     return false;
 }
 
-struct Counts { uint32_t u, f, o, l; };
+// Per-lane integer accumulators of one perspective: visits per state, in-grid lookups,
+// and (8-bit store) the Eq. 2 gain in units of 1/63.
+struct Counts { uint32_t u, f, o, l, g; };
 
 // Close a ray that stopped at step s_stop on `code` (2 = Occupied, 3 = left the grid;
-// Q14 tail rule: the remaining n - s + 1 visits are all outside, hence Unknown).
+// Q14 tail rule: the remaining n - s + 1 visits are all outside, hence Unknown).  ng = the
+// in-grid gain (1/63 units) up to and including the stop.
 template <typename T>
 __device__ __forceinline__ void walk_close_stop(const Walk<T> &w, int policy, uint32_t code, int s_stop, uint32_t nf,
-                                                Counts &c)
+                                                uint32_t ng, Counts &c)
 {
     uint32_t l;
     uint32_t u_out = (policy == NBT_OUTSIDE_UNKNOWN) ? w.pre : 0u;
@@ -243,19 +249,22 @@ __device__ __forceinline__ void walk_close_stop(const Walk<T> &w, int policy, ui
     }
     c.f += nf;
     c.l += l;
+    c.g += ng + 63u * u_out;
 }
 
 template <typename T>
-__device__ __forceinline__ void walk_close_end(const Walk<T> &w, int policy, uint32_t nf, Counts &c)
+__device__ __forceinline__ void walk_close_end(const Walk<T> &w, int policy, uint32_t nf, uint32_t ng, Counts &c)
 {
-    uint32_t l = (uint32_t)(w.n - w.s0 + 1);
-    c.u += l - nf + ((policy == NBT_OUTSIDE_UNKNOWN) ? w.pre : 0u);
+    const uint32_t l = (uint32_t)(w.n - w.s0 + 1);
+    const uint32_t u_out = (policy == NBT_OUTSIDE_UNKNOWN) ? w.pre : 0u;
+    c.u += l - nf + u_out;
     c.f += nf;
     c.l += l;
+    c.g += ng + 63u * u_out;
 }
 
 // A batch of K visits: the loaded map words and, per visit, the rotate amount that
-// brings its 2-bit code to bits 2k..2k+1 of the packed word.
+// brings its value's state bits to bits 2k..2k+1 of the packed word.
 template <int K>
 struct Batch {
     uint32_t wd[K];
@@ -269,41 +278,59 @@ __device__ __forceinline__ constexpr uint32_t lanes_mask(uint32_t pattern)
 }
 
 // Issue the K loads of the next K visits (the DDA does not depend on the map, so
-// this runs ahead of the codes) and advance the DDA by K steps.
-template <typename T, int L, int K>
+// this runs ahead of the codes) and advance the DDA by K steps.  VB = bits per voxel.
+template <typename T, int L, int VB, int K>
 __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<K> &b)
 {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        b.rot[k] = (w.idx << 1) - 2 * k;        // rotate amounts are taken mod 32
-        b.wd[k] = __ldg(m.words + (w.idx >> 4));
+        if (VB == 2) {
+            b.rot[k] = (w.idx << 1) - 2 * k;    // rotate amounts are taken mod 32
+            b.wd[k] = __ldg(m.words + (w.idx >> 4));
+        } else {
+            b.rot[k] = ((w.idx & 3u) << 3) - 2 * k;
+            b.wd[k] = __ldg(m.words + (w.idx >> 2));
+        }
         walk_step<T, L, false>(w, m);
     }
 }
 
 // Consume the batch holding visits s..s+K-1.  Returns true when the ray is finished
 // (counts added to c): first code >= 2 by one ffs (Occupied: early stop, P:213;
-// 3: left the grid), Free voxels by one popc.
-template <typename T, int K>
+// 3: left the grid), Free voxels by one popc; with the 8-bit store also the Eq. 2 gains.
+template <typename T, int VB, int K>
 __device__ __forceinline__ bool batch_consume(Walk<T> &w, const Batch<K> &b, int policy, Counts &c)
 {
-    uint32_t bits = 0;
+    uint32_t bits = 0, gsum = 0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) bits |= __funnelshift_r(b.wd[k], b.wd[k], b.rot[k]) & (3u << (2 * k));
+    for (int k = 0; k < K; ++k) {
+        const uint32_t r = __funnelshift_r(b.wd[k], b.wd[k], b.rot[k]);
+        bits |= r & (3u << (2 * k));
+        if (VB == 8) gsum += (b.wd[k] >> (b.rot[k] + 2 * k + 2)) & 63u;   // byte offset + 2
+    }
     const int left = w.n - w.s + 1;             // visits remaining, including the current one
     const uint32_t valid = left >= K ? lanes_mask<K>(0xFFFFFFFFu) : ((1u << (2 * left)) - 1u);
     const uint32_t stop = bits & valid & 0xAAAAAAAAu;   // codes 2 (Occupied) and 3 (outside)
-    if (stop) {
-        const int k = (__ffs(stop) - 1) >> 1;
-        const uint32_t nf = w.nf + __popc(bits & ((1u << (2 * k)) - 1u) & 0x55555555u);
-        walk_close_stop(w, policy, (bits >> (2 * k)) & 3u, w.s + k, nf, c);
+    if (stop || left <= K) {
+        // last batch of the ray: only visits up to the stop (or the end) count
+        const int last = stop ? ((__ffs(stop) - 1) >> 1) : left - 1;
+        const uint32_t upto = last >= 15 ? 0xFFFFFFFFu : ((1u << (2 * last + 2)) - 1u);
+        uint32_t ng = w.ng;
+        if (VB == 8) {
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (k <= last) ng += (b.wd[k] >> (b.rot[k] + 2 * k + 2)) & 63u;
+        }
+        if (stop) {
+            const uint32_t nf = w.nf + __popc(bits & (upto >> 2) & 0x55555555u);
+            walk_close_stop(w, policy, (bits >> (2 * last)) & 3u, w.s + last, nf, ng, c);
+        } else {
+            walk_close_end(w, policy, w.nf + __popc(bits & upto & 0x55555555u), ng, c);
+        }
         return true;
     }
-    w.nf += __popc(bits & valid & 0x55555555u);
-    if (left <= K) {
-        walk_close_end(w, policy, w.nf, c);
-        return true;
-    }
+    w.nf += __popc(bits & 0x55555555u);
+    if (VB == 8) w.ng += gsum;
     w.s += K;
     return false;
 }
@@ -402,7 +429,7 @@ __global__ void k_persp_frames(FrameArgs A, int32_t *__restrict__ frames, unsign
     dst[18] = st;
     dst[19] = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) totals[4 * (size_t)i + k] = 0ull;
+    for (int k = 0; k < kTotals; ++k) totals[kTotals * (size_t)i + k] = 0ull;
     if (st) atomicCAS(err, 0, st);
 }
 
@@ -470,12 +497,13 @@ __device__ __forceinline__ void ray_segment(const int f[18], int mi, int mk, int
 __device__ __forceinline__ void flush_counts(unsigned long long *totals, int j, Counts &c)
 {
     if (j < 0) return;
-    unsigned long long *t = totals + 4 * (size_t)j;
+    unsigned long long *t = totals + kTotals * (size_t)j;
     if (c.u) atomicAdd(t + 0, (unsigned long long)c.u);
     if (c.f) atomicAdd(t + 1, (unsigned long long)c.f);
     if (c.o) atomicAdd(t + 2, (unsigned long long)c.o);
     if (c.l) atomicAdd(t + 3, (unsigned long long)c.l);
-    c = Counts{0, 0, 0, 0};
+    if (c.g) atomicAdd(t + 4, (unsigned long long)c.g);
+    c = Counts{0, 0, 0, 0, 0};
 }
 
 // Prepare the ray in `slot` of perspective j (frame, segment, DDA set-up, grid
@@ -494,7 +522,10 @@ __device__ __forceinline__ bool prep_ray(const TraceArgs &A, int j, int slot, Wa
     ray_segment(f, mi, mk, corner, o, e);
     walk_setup(w, o, e);
     if (walk_enter<T, L, false>(w, A.m, nullptr, nullptr, 0)) {
-        if (A.m.policy == NBT_OUTSIDE_UNKNOWN) atomicAdd(A.totals + 4 * (size_t)j, (unsigned long long)w.pre);
+        if (A.m.policy == NBT_OUTSIDE_UNKNOWN) {
+            atomicAdd(A.totals + kTotals * (size_t)j, (unsigned long long)w.pre);
+            atomicAdd(A.totals + kTotals * (size_t)j + 4, 63ull * w.pre);
+        }
         return false;
     }
     return true;
@@ -542,14 +573,14 @@ __device__ __forceinline__ int queue_get(const WalkQueue<T> &Q, int i, Walk<T> &
     } else {
         w.dX = Q.d[0][i]; w.dY = Q.d[1][i]; w.ndZ = Q.d[2][i];
     }
-    w.n = Q.n[i]; w.s0 = Q.s0[i]; w.s = w.s0; w.pre = Q.pre[i]; w.nf = 0;
+    w.n = Q.n[i]; w.s0 = Q.s0[i]; w.s = w.s0; w.pre = Q.pre[i]; w.nf = 0; w.ng = 0;
     return Q.j[i];
 }
 
 #ifndef NBT_TRACE_MIN_BLOCKS
 #define NBT_TRACE_MIN_BLOCKS 1
 #endif
-template <typename T, int L, int K, bool PIPE>
+template <typename T, int L, int VB, int K, bool PIPE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, NBT_TRACE_MIN_BLOCKS) k_id_trace(TraceArgs A)
 {
     static_assert((PIPE ? 2 * K : K) <= kBorder, "look-ahead must stay inside the sentinel shell");
@@ -565,7 +596,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, NBT_TRACE_MIN_BLOCKS) k_i
     Batch<K> b0, b1;
     bool have = false;
     int jl = -1;                             // perspective of this lane's accumulators
-    Counts c{0, 0, 0, 0};
+    Counts c{0, 0, 0, 0, 0};
     for (;;) {
         const unsigned need = __ballot_sync(full, !have);
         // refill once enough lanes are idle (min_refill = 1: as soon as any is)
@@ -600,7 +631,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, NBT_TRACE_MIN_BLOCKS) k_i
                     const int j = queue_get<T, L>(Q, qhead + rank, w);
                     if (j != jl) { flush_counts(A.totals, jl, c); jl = j; }
                     have = true;
-                    if (PIPE) batch_issue<T, L, K>(w, A.m, b0);
+                    if (PIPE) batch_issue<T, L, VB, K>(w, A.m, b0);
                 }
                 qhead += take;
                 qcount -= take;
@@ -610,16 +641,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, NBT_TRACE_MIN_BLOCKS) k_i
         if (q_done && qcount == 0 && !__any_sync(full, have)) break;
         if (!have) continue;
         if (!PIPE) {
-            batch_issue<T, L, K>(w, A.m, b0);
-            if (batch_consume<T, K>(w, b0, A.m.policy, c)) have = false;
+            batch_issue<T, L, VB, K>(w, A.m, b0);
+            if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) have = false;
         } else {
             // b0 holds visits s..s+K-1; keep the next batch in flight while consuming
-            if (w.n - w.s + 1 > K) batch_issue<T, L, K>(w, A.m, b1);
-            if (batch_consume<T, K>(w, b0, A.m.policy, c)) {
+            if (w.n - w.s + 1 > K) batch_issue<T, L, VB, K>(w, A.m, b1);
+            if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) {
                 have = false;
             } else {
-                if (w.n - w.s + 1 > K) batch_issue<T, L, K>(w, A.m, b0);
-                if (batch_consume<T, K>(w, b1, A.m.policy, c)) have = false;
+                if (w.n - w.s + 1 > K) batch_issue<T, L, VB, K>(w, A.m, b0);
+                if (batch_consume<T, VB, K>(w, b1, A.m.policy, c)) have = false;
             }
         }
     }
@@ -630,7 +661,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, NBT_TRACE_MIN_BLOCKS) k_i
 
 __global__ void k_id_finalize(FrameArgs A, const int32_t *__restrict__ frames,
                               const unsigned long long *__restrict__ totals, double g_u, double g_f, double g_o,
-                              double n_e, double *__restrict__ xyz_out, double *__restrict__ gain_out,
+                              int prob, double n_e, double *__restrict__ xyz_out, double *__restrict__ gain_out,
                               unsigned long long *__restrict__ counts_out)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -639,11 +670,13 @@ __global__ void k_id_finalize(FrameArgs A, const int32_t *__restrict__ frames,
     xyz_out[3 * (size_t)i + 0] = pp[0];
     xyz_out[3 * (size_t)i + 1] = pp[1];
     xyz_out[3 * (size_t)i + 2] = pp[2];
-    unsigned long long tu = totals[4 * (size_t)i], tf = totals[4 * (size_t)i + 1];
-    unsigned long long to = totals[4 * (size_t)i + 2], tl = totals[4 * (size_t)i + 3];
-    double g = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn((double)tu, g_u), __dmul_rn((double)tf, g_f)),
-                                   __dmul_rn((double)to, g_o)),
-                         n_e);
+    const unsigned long long *t = totals + kTotals * (size_t)i;
+    unsigned long long tu = t[0], tf = t[1], to = t[2], tl = t[3], tg = t[4];
+    // per-state gains (Q26) or, with per-voxel probabilities, the exact Eq. 2 sum (Q32)
+    double g = prob ? __ddiv_rn((double)tg, __dmul_rn(63.0, n_e))
+                    : __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn((double)tu, g_u), __dmul_rn((double)tf, g_f)),
+                                          __dmul_rn((double)to, g_o)),
+                                n_e);
     if (frames[(size_t)i * kFrameInts + 18] != 0) g = __longlong_as_double(0x7ff8000000000000LL);   // NaN
     gain_out[i] = g;
     if (counts_out) {
@@ -658,7 +691,7 @@ __global__ void k_id_finalize(FrameArgs A, const int32_t *__restrict__ frames,
 
 // Per-ray walk of an explicit Q12 segment, recording every visited voxel; the same
 // Walk / walk_step / walk_enter code as k_id_trace, one voxel at a time.
-template <typename T, int L>
+template <typename T, int L, int VB>
 __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const int32_t *__restrict__ e, int n_rays,
                               int max_visits, int32_t *ijk, uint8_t *code, int32_t *len, uint32_t *counts)
 {
@@ -670,20 +703,21 @@ __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const in
     walk_setup(w, oo, ee);
     int32_t *ri = ijk + (size_t)r * max_visits * 3;
     uint8_t *rc = code + (size_t)r * max_visits;
-    Counts c{0, 0, 0, 0};
+    Counts c{0, 0, 0, 0, 0};
     int visits;
     if (walk_enter<T, L, true>(w, m, ri, rc, max_visits)) {
         if (m.policy == NBT_OUTSIDE_UNKNOWN) c.u += w.pre;
         visits = w.n + 1;
     } else {
         for (;;) {
-            uint32_t cd = code_of(__ldg(m.words + (w.idx >> 4)), w.idx);
+            const uint32_t cd = VB == 2 ? code_of(__ldg(m.words + (w.idx >> 4)), w.idx)
+                                        : (__ldg(m.words + (w.idx >> 2)) >> ((w.idx & 3u) << 3)) & 3u;
             if (w.s < max_visits) {
                 ri[3 * w.s] = w.vx; ri[3 * w.s + 1] = w.vy; ri[3 * w.s + 2] = w.vz;
                 rc[w.s] = cd == 3u ? 255 : (uint8_t)cd;
             }
             if (cd >= 2u) {
-                walk_close_stop(w, m.policy, cd, w.s, w.nf, c);
+                walk_close_stop(w, m.policy, cd, w.s, w.nf, 0u, c);
                 if (cd == 2u) {
                     visits = w.s + 1;
                 } else {   // record the outside tail too
@@ -700,7 +734,7 @@ __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const in
             }
             w.nf += cd;
             if (w.s == w.n) {
-                walk_close_end(w, m.policy, w.nf, c);
+                walk_close_end(w, m.policy, w.nf, 0u, c);
                 visits = w.n + 1;
                 break;
             }
@@ -786,6 +820,22 @@ double max_ray_voxels(const nbt_camera &cam, double range, double voxel_size)
     return rs * sqrt(1.0 + ex * ex + ey * ey) * 1.001 + 2.0;
 }
 
+// The trace kernel instances: [wide][layout][8-bit store].
+using TraceFn = void (*)(TraceArgs);
+const TraceFn kTraceFns[2][2][2] = {
+    {{k_id_trace<int, kLayoutLinear, 2, kBatchK, false>, k_id_trace<int, kLayoutLinear, 8, kBatchK, false>},
+     {k_id_trace<int, kLayoutMorton, 2, kBatchK, false>, k_id_trace<int, kLayoutMorton, 8, kBatchK, false>}},
+    {{k_id_trace<long long, kLayoutLinear, 2, kBatchK, false>, k_id_trace<long long, kLayoutLinear, 8, kBatchK, false>},
+     {k_id_trace<long long, kLayoutMorton, 2, kBatchK, false>, k_id_trace<long long, kLayoutMorton, 8, kBatchK, false>}}};
+
+using DebugFn = void (*)(MapView, const int32_t *, const int32_t *, int, int, int32_t *, uint8_t *, int32_t *,
+                         uint32_t *);
+const DebugFn kDebugFns[2][2][2] = {
+    {{k_debug_trace<int, kLayoutLinear, 2>, k_debug_trace<int, kLayoutLinear, 8>},
+     {k_debug_trace<int, kLayoutMorton, 2>, k_debug_trace<int, kLayoutMorton, 8>}},
+    {{k_debug_trace<long long, kLayoutLinear, 2>, k_debug_trace<long long, kLayoutLinear, 8>},
+     {k_debug_trace<long long, kLayoutMorton, 2>, k_debug_trace<long long, kLayoutMorton, 8>}}};
+
 }  // namespace
 
 nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
@@ -793,7 +843,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     if (L.n == 0) return NBT_OK;
     nbt_status st;
     if ((st = ctx->frames.ensure((size_t)L.n * kFrameInts * 4))) return st;
-    if ((st = ctx->totals.ensure((size_t)L.n * 32))) return st;
+    if ((st = ctx->totals.ensure((size_t)L.n * kTotals * 8))) return st;
     if ((st = ctx->counter.ensure(64))) return st;
     FrameArgs A = frame_args(m, L.d_persp, L.first, L.stride, L.n, L.poi, L.cam, L.range);
     int *counter = ctx->counter.as<int>();
@@ -817,24 +867,18 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     T.n_tile_slots = T.tiled ? T.Wt * Ht * 32 : T.W * T.H;
     T.slots = T.n_tile_slots + (T.add_corners ? 4 : 0);
     const bool wide = max_ray_voxels(L.cam, L.range, m->desc.voxel_size) > kInt32MaxVoxels;
-    const bool morton = m->layout == kLayoutMorton;
+    const TraceFn fn = kTraceFns[wide][m->layout == kLayoutMorton][m->vbits == 8];
     if (ctx->trace_blocks_per_sm == 0) {
         // smallest shared-memory carveout that holds the walk queues of the resident blocks,
         // so the rest of the SM's 256 KB stays L1 for the map lines
         const int carve = trace_carveout();
-        if (carve >= 0) {
-            NBT_CUDA(cudaFuncSetAttribute(k_id_trace<int, kLayoutLinear, kBatchK, false>,
-                                          cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-            NBT_CUDA(cudaFuncSetAttribute(k_id_trace<int, kLayoutMorton, kBatchK, false>,
-                                          cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-            NBT_CUDA(cudaFuncSetAttribute(k_id_trace<long long, kLayoutLinear, kBatchK, false>,
-                                          cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-            NBT_CUDA(cudaFuncSetAttribute(k_id_trace<long long, kLayoutMorton, kBatchK, false>,
-                                          cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-        }
+        if (carve >= 0)
+            for (auto &a : kTraceFns)
+                for (auto &b : a)
+                    for (TraceFn f : b)
+                        NBT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
         int b = 0;
-        NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &b, k_id_trace<int, kLayoutLinear, kBatchK, false>, kWarpsPerBlock * 32, 0));
+        NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kTraceFns[0][0][0], kWarpsPerBlock * 32, 0));
         ctx->trace_blocks_per_sm = b > 0 ? b : 1;
     }
     long long resident_warps = (long long)ctx->num_sms * ctx->trace_blocks_per_sm * kWarpsPerBlock;
@@ -853,15 +897,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     int blocks = (int)(want_blocks < max_blocks ? want_blocks : max_blocks);
     {
         ProfScope ps(ctx, NBT_KERNEL_TRACE);
-        const dim3 grid(blocks), block(kWarpsPerBlock * 32);
-        if (wide && morton)
-            k_id_trace<long long, kLayoutMorton, kBatchK, false><<<grid, block, 0, ctx->stream>>>(T);
-        else if (wide)
-            k_id_trace<long long, kLayoutLinear, kBatchK, false><<<grid, block, 0, ctx->stream>>>(T);
-        else if (morton)
-            k_id_trace<int, kLayoutMorton, kBatchK, false><<<grid, block, 0, ctx->stream>>>(T);
-        else
-            k_id_trace<int, kLayoutLinear, kBatchK, false><<<grid, block, 0, ctx->stream>>>(T);
+        fn<<<dim3(blocks), dim3(kWarpsPerBlock * 32), 0, ctx->stream>>>(T);
         NBT_LAUNCHED(ctx);
     }
 
@@ -869,7 +905,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     ProfScope ps(ctx, NBT_KERNEL_FINALIZE);
     k_id_finalize<<<(L.n + 127) / 128, 128, 0, ctx->stream>>>(
         A, ctx->frames.as<int32_t>(), ctx->totals.as<unsigned long long>(), m->desc.gain[0], m->desc.gain[1],
-        m->desc.gain[2], (double)ne, L.d_xyz_out, L.d_gain_out,
+        m->desc.gain[2], m->vbits == 8 ? 1 : 0, (double)ne, L.d_xyz_out, L.d_gain_out,
         reinterpret_cast<unsigned long long *>(L.d_counts_out));
     NBT_LAUNCHED(ctx);
     return NBT_OK;
@@ -880,23 +916,9 @@ nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const 
                               uint32_t *d_counts, bool wide)
 {
     if (n_rays == 0) return NBT_OK;
-    const dim3 grid((n_rays + 127) / 128), block(128);
-    const MapView v = view_of(m);
-    if (m->layout == kLayoutMorton) {
-        if (wide)
-            k_debug_trace<long long, kLayoutMorton><<<grid, block, 0, ctx->stream>>>(v, d_o, d_e, n_rays, max_visits,
-                                                                                     d_ijk, d_code, d_len, d_counts);
-        else
-            k_debug_trace<int, kLayoutMorton><<<grid, block, 0, ctx->stream>>>(v, d_o, d_e, n_rays, max_visits, d_ijk,
-                                                                               d_code, d_len, d_counts);
-    } else {
-        if (wide)
-            k_debug_trace<long long, kLayoutLinear><<<grid, block, 0, ctx->stream>>>(v, d_o, d_e, n_rays, max_visits,
-                                                                                     d_ijk, d_code, d_len, d_counts);
-        else
-            k_debug_trace<int, kLayoutLinear><<<grid, block, 0, ctx->stream>>>(v, d_o, d_e, n_rays, max_visits, d_ijk,
-                                                                               d_code, d_len, d_counts);
-    }
+    const DebugFn fn = kDebugFns[wide][m->layout == kLayoutMorton][m->vbits == 8];
+    fn<<<dim3((n_rays + 127) / 128), dim3(128), 0, ctx->stream>>>(view_of(m), d_o, d_e, n_rays, max_visits, d_ijk,
+                                                                   d_code, d_len, d_counts);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }

@@ -1,16 +1,18 @@
-// Voxel-map store kernels.
+// Voxel-map store kernels (8(f) row f1).
 //
-// Two layouts.  Morton (NBT_MAP_LAYOUT=morton): the store is a
-// cube of side P = 2^pbits >= max(n) + 2 kBorder indexed by the bit-interleaved voxel
-// coordinates; every position outside the grid holds the sentinel.  Linear (default):
-// the nx*ny*nz grid is surrounded by a shell of
-// kBorder sentinel voxels (code 3 = "outside") and stored x-fastest, 2 bits per voxel,
-// 16 voxels per 32-bit word: voxel (x, y, z) is padded voxel (x+B, y+B, z+B) with
-// linear index i = (x+B) + px*((y+B) + py*(z+B)), px = nx + 2B, stored in bits
-// 2*(i&15).. of word i>>4.  256^3 -> 5.0 MiB, 512^3 -> 36 MiB: L2-resident (126 MB).
-// The sentinel shell lets the walk detect leaving the grid with the same "code >= 2"
-// test that detects an Occupied voxel (no bounds check in the hot loop), and its
-// thickness B >= the walk's speculative batch keeps look-ahead loads inside the store.
+// Two layouts.  Linear (default): the nx*ny*nz grid is surrounded
+// by a shell of kBorder sentinel voxels and stored x-fastest: voxel (x, y, z) is padded
+// voxel (x+B, y+B, z+B) with index i = (x+B) + px*((y+B) + py*(z+B)), px = nx + 2B.
+// Morton (NBT_MAP_LAYOUT=morton): a cube of side P = 2^pbits >= max(n) + 2 kBorder indexed
+// by the bit-interleaved coordinates; every position outside the grid is sentinel.  The
+// sentinel lets the walk detect leaving the grid with the same "code >= 2" test that
+// detects an Occupied voxel, and its thickness keeps look-ahead loads inside the store.
+//
+// Two value widths.  2 bits per voxel (the three states, 0 U / 1 F / 2 O, 3 = sentinel),
+// 16 voxels per word: per-state gains (reading Q15).  8 bits per voxel (f1, exact Eq. 2,
+// reading Q32), 4 voxels per word: bits 0-1 the state, bits 2-7 the voxel's Eq. 2 gain in
+// units of 1/63 -- 63 for Unknown, level for Free (P = level/63), 63 - level for
+// Occupied -- so the walk reads the gain with one shift.
 #include <cub/cub.cuh>
 
 #include "nbt_internal.cuh"
@@ -22,8 +24,10 @@ constexpr uint32_t kOutside = 3u;
 
 struct Geom {
     int layout;
+    int vbits;                 // 2 or 8
     int nx, ny, nz;
-    uint32_t px, py;   // linear padded extents
+    uint32_t px, py;           // linear padded extents
+    uint32_t def_level[3];     // 8-bit store: level used for U / F / O when none is given
 };
 
 // Store index of grid voxel (x, y, z).
@@ -33,13 +37,28 @@ __device__ __forceinline__ uint64_t store_index(const Geom &g, uint32_t x, uint3
     return (uint64_t)(x + kBorder) + (uint64_t)g.px * ((uint64_t)(y + kBorder) + (uint64_t)g.py * (z + kBorder));
 }
 
-// One thread per packed word (16 store positions).
-__global__ void k_map_pack(const uint8_t *__restrict__ codes, Geom g, uint64_t nvox_pad, size_t nwords,
-                           uint32_t *__restrict__ words, int *err)
+__device__ __forceinline__ uint32_t word_of(const Geom &g, uint64_t i) { return (uint32_t)(i >> (g.vbits == 2 ? 4 : 2)); }
+__device__ __forceinline__ uint32_t shift_of(const Geom &g, uint64_t i)
+{
+    return g.vbits == 2 ? (uint32_t)(i & 15) * 2 : (uint32_t)(i & 3) * 8;
+}
+
+// The stored value of a grid voxel: the state, or state | Eq. 2 gain (1/63 units) << 2.
+__device__ __forceinline__ uint32_t stored_value(const Geom &g, uint32_t code, uint32_t level)
+{
+    if (g.vbits == 2) return code;
+    const uint32_t gq = code == 0 ? 63u : (code == 1 ? level : 63u - level);
+    return code | (gq << 2);
+}
+
+// One thread per packed word.
+__global__ void k_map_pack(const uint8_t *__restrict__ codes, const uint8_t *__restrict__ levels, Geom g,
+                           uint64_t nvox_pad, size_t nwords, uint32_t *__restrict__ words, int *err)
 {
     size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (w >= nwords) return;
-    uint64_t i0 = (uint64_t)w * 16;
+    const int per = g.vbits == 2 ? 16 : 4;
+    uint64_t i0 = (uint64_t)w * per;
     uint32_t x = 0, y = 0, z = 0;
     if (g.layout == kLayoutLinear) {
         x = (uint32_t)(i0 % g.px);
@@ -49,8 +68,8 @@ __global__ void k_map_pack(const uint8_t *__restrict__ codes, Geom g, uint64_t n
     }
     uint32_t out = 0;
     bool bad = false;
-    for (int k = 0; k < 16; ++k) {
-        uint32_t c = kOutside;
+    for (int k = 0; k < per; ++k) {
+        uint32_t v = kOutside;
         int gx, gy, gz;
         if (g.layout == kLayoutMorton) {
             const uint32_t i = (uint32_t)(i0 + k);
@@ -60,18 +79,24 @@ __global__ void k_map_pack(const uint8_t *__restrict__ codes, Geom g, uint64_t n
             if (++x == g.px) { x = 0; if (++y == g.py) { y = 0; ++z; } }
         }
         if (i0 + k < nvox_pad && gx >= 0 && gy >= 0 && gz >= 0 && gx < g.nx && gy < g.ny && gz < g.nz) {
-            c = codes[(size_t)gx + (size_t)g.nx * ((size_t)gy + (size_t)g.ny * gz)];
+            const size_t src = (size_t)gx + (size_t)g.nx * ((size_t)gy + (size_t)g.ny * gz);
+            uint32_t c = codes[src];
             if (c > 2u) { bad = true; c = 0u; }
+            uint32_t lv = levels ? levels[src] : g.def_level[c];
+            if (lv > 63u) { bad = true; lv = 63u; }
+            v = stored_value(g, c, lv);
         }
-        out |= c << (2 * k);
+        out |= v << (g.vbits * k);
     }
     words[w] = out;
     if (bad) atomicCAS(err, 0, (int)NBT_ERR_INVALID_ARG);
 }
 
-// S:66-74 classification: unobserved -> U; P >= t_occ -> O; P <= t_free -> F; else U.
+// S:66-74 classification: unobserved -> U; P >= t_occ -> O; P <= t_free -> F; else U.  With
+// levels_out (8-bit store): level = round-half-even(63 clamp(P, 0, 1)), 0 if unobserved (Q32).
 __global__ void k_map_classify(const float *__restrict__ p, const uint8_t *__restrict__ obs, size_t n,
-                               double t_occ, double t_free, uint8_t *__restrict__ codes)
+                               double t_occ, double t_free, uint8_t *__restrict__ codes,
+                               uint8_t *__restrict__ levels_out)
 {
     size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -79,16 +104,22 @@ __global__ void k_map_classify(const float *__restrict__ p, const uint8_t *__res
     uint8_t c = NBT_UNKNOWN;
     if (obs[i]) c = (v >= t_occ) ? NBT_OCCUPIED : (v <= t_free ? NBT_FREE : NBT_UNKNOWN);
     codes[i] = c;
+    if (levels_out) {
+        const double cl = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+        levels_out[i] = obs[i] ? (uint8_t)__double2int_rn(__dmul_rn(cl, 63.0)) : 0;
+    }
 }
 
 // Delta keys: (linear voxel index << 32) | array position; invalid deltas sort last.
-__global__ void k_delta_keys(const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes, uint32_t n,
-                             int nx, int ny, int nz, unsigned long long *__restrict__ keys, int *err)
+__global__ void k_delta_keys(const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes,
+                             const uint8_t *__restrict__ levels, uint32_t n, int nx, int ny, int nz,
+                             unsigned long long *__restrict__ keys, int *err)
 {
     uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int x = ijk[3 * i], y = ijk[3 * i + 1], z = ijk[3 * i + 2];
-    bool ok = x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz && codes[i] <= 2;
+    bool ok = x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz && codes[i] <= 2 &&
+              (!levels || levels[i] <= 63);
     if (!ok) {
         keys[i] = ~0ull;
         atomicCAS(err, 0, (int)NBT_ERR_INVALID_ARG);
@@ -100,11 +131,11 @@ __global__ void k_delta_keys(const int32_t *__restrict__ ijk, const uint8_t *__r
 }
 
 // After sorting, the last key of each voxel run is the last delta in array order (Q30):
-// only that one writes.  Distinct voxels may share a word, so the 2-bit field is
-// changed with one atomicXor; the thread's own field is never touched by another thread.
+// only that one writes.  Distinct voxels may share a word, so the field is changed with
+// one atomicXor; the thread's own field is never touched by another thread.
 __global__ void k_delta_apply(const unsigned long long *__restrict__ keys, uint32_t n,
-                              const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes, Geom g,
-                              uint32_t *words)
+                              const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes,
+                              const uint8_t *__restrict__ levels, Geom g, uint32_t *words)
 {
     uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -113,14 +144,18 @@ __global__ void k_delta_apply(const unsigned long long *__restrict__ keys, uint3
     if (i + 1 < n && (keys[i + 1] >> 32) == (k >> 32)) return;
     uint32_t pos = (uint32_t)(k & 0xffffffffu);
     uint64_t pi = store_index(g, (uint32_t)ijk[3 * pos], (uint32_t)ijk[3 * pos + 1], (uint32_t)ijk[3 * pos + 2]);
-    uint32_t *w = words + (pi >> 4);
-    uint32_t sh = (uint32_t)(pi & 15) * 2;
-    uint32_t old = (*(volatile uint32_t *)w >> sh) & 3u;
-    uint32_t nw = codes[pos];
+    uint32_t *w = words + word_of(g, pi);
+    const uint32_t sh = shift_of(g, pi);
+    const uint32_t mask = g.vbits == 2 ? 3u : 0xffu;
+    const uint32_t c = codes[pos];
+    const uint32_t nw = stored_value(g, c, levels ? levels[pos] : g.def_level[c]);
+    const uint32_t old = (*(volatile uint32_t *)w >> sh) & mask;
     if (old != nw) atomicXor(w, (old ^ nw) << sh);
 }
 
-__global__ void k_map_unpack(const uint32_t *__restrict__ words, Geom g, uint8_t *__restrict__ codes)
+// Dense codes (and, for the 8-bit store, the probability levels) of the grid.
+__global__ void k_map_unpack(const uint32_t *__restrict__ words, Geom g, uint8_t *__restrict__ codes,
+                             uint8_t *__restrict__ levels)
 {
     size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     size_t n = (size_t)g.nx * g.ny * g.nz;
@@ -129,7 +164,13 @@ __global__ void k_map_unpack(const uint32_t *__restrict__ words, Geom g, uint8_t
     size_t r = i / g.nx;
     uint32_t y = (uint32_t)(r % g.ny), z = (uint32_t)(r / g.ny);
     uint64_t pi = store_index(g, x, y, z);
-    codes[i] = (uint8_t)((words[pi >> 4] >> ((pi & 15) * 2)) & 3u);
+    const uint32_t v = (words[word_of(g, pi)] >> shift_of(g, pi)) & (g.vbits == 2 ? 3u : 0xffu);
+    const uint32_t c = v & 3u;
+    if (codes) codes[i] = (uint8_t)c;
+    if (levels) {
+        const uint32_t gq = v >> 2;
+        levels[i] = (uint8_t)(c == 1 ? gq : (c == 2 ? 63u - gq : 0u));
+    }
 }
 
 inline unsigned blocks_for(size_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
@@ -138,32 +179,40 @@ Geom geom_of(nbt_map m)
 {
     Geom g;
     g.layout = m->layout;
+    g.vbits = m->vbits;
     g.nx = m->desc.nx; g.ny = m->desc.ny; g.nz = m->desc.nz;
     g.px = m->px; g.py = m->py;
+    // a state-only write to the 8-bit store uses the per-state constants of the desc:
+    // P_F = g_F and 1 - P_O = g_O (reading Q15), rounded to k/63
+    g.def_level[0] = 0;
+    g.def_level[1] = (uint32_t)nearbyint(fmin(fmax(m->desc.gain[1], 0.0), 1.0) * 63.0);
+    g.def_level[2] = (uint32_t)nearbyint(fmin(fmax(1.0 - m->desc.gain[2], 0.0), 1.0) * 63.0);
     return g;
 }
 
 }  // namespace
 
-nbt_status launch_map_pack(nbt_ctx ctx, nbt_map m, const uint8_t *d_codes)
+nbt_status launch_map_pack(nbt_ctx ctx, nbt_map m, const uint8_t *d_codes, const uint8_t *d_levels)
 {
     if (m->nwords == 0) return NBT_OK;
-    k_map_pack<<<blocks_for(m->nwords, 256), 256, 0, ctx->stream>>>(d_codes, geom_of(m), m->nvox_pad, m->nwords,
-                                                                     m->d_words, ctx->d_err);
+    k_map_pack<<<blocks_for(m->nwords, 256), 256, 0, ctx->stream>>>(d_codes, d_levels, geom_of(m), m->nvox_pad,
+                                                                     m->nwords, m->d_words, ctx->d_err);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }
 
 nbt_status launch_map_classify(nbt_ctx ctx, const float *d_p, const uint8_t *d_obs, size_t n, double t_occ,
-                               double t_free, uint8_t *d_codes_out)
+                               double t_free, uint8_t *d_codes_out, uint8_t *d_levels_out)
 {
     if (n == 0) return NBT_OK;
-    k_map_classify<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(d_p, d_obs, n, t_occ, t_free, d_codes_out);
+    k_map_classify<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(d_p, d_obs, n, t_occ, t_free, d_codes_out,
+                                                                d_levels_out);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }
 
-nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const uint8_t *d_codes, size_t n)
+nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const uint8_t *d_codes,
+                             const uint8_t *d_levels, size_t n)
 {
     if (n == 0) return NBT_OK;
     if (n >= (1ull << 31)) return fail(NBT_ERR_INVALID_ARG, "nbt_map_update: too many deltas");
@@ -174,22 +223,23 @@ nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const
     if ((st = ctx->keys_alt.ensure(n * 8))) return st;
     auto *kin = ctx->keys.as<unsigned long long>();
     auto *kout = ctx->keys_alt.as<unsigned long long>();
-    k_delta_keys<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(d_ijk, d_codes, nn, m->desc.nx, m->desc.ny,
+    k_delta_keys<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(d_ijk, d_codes, d_levels, nn, m->desc.nx, m->desc.ny,
                                                               m->desc.nz, kin, ctx->d_err);
     NBT_LAUNCHED(ctx);
     size_t tmp = 0;
     NBT_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kin, kout, (int)nn, 0, 64, ctx->stream));
     if ((st = ctx->cub_tmp.ensure(tmp))) return st;
     NBT_CUDA(cub::DeviceRadixSort::SortKeys(ctx->cub_tmp.p, tmp, kin, kout, (int)nn, 0, 64, ctx->stream));
-    k_delta_apply<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(kout, nn, d_ijk, d_codes, geom_of(m), m->d_words);
+    k_delta_apply<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(kout, nn, d_ijk, d_codes, d_levels, geom_of(m),
+                                                               m->d_words);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }
 
-nbt_status launch_map_unpack(nbt_ctx ctx, nbt_map m, uint8_t *d_codes_out)
+nbt_status launch_map_unpack(nbt_ctx ctx, nbt_map m, uint8_t *d_codes_out, uint8_t *d_levels_out)
 {
     size_t n = (size_t)m->desc.nx * m->desc.ny * m->desc.nz;
-    k_map_unpack<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(m->d_words, geom_of(m), d_codes_out);
+    k_map_unpack<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(m->d_words, geom_of(m), d_codes_out, d_levels_out);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }

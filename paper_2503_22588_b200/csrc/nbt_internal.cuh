@@ -160,6 +160,7 @@ struct nbt_map_s {
     nbt_ctx ctx = nullptr;
     nbt_map_desc desc{};
     int layout = nbt::kLayoutLinear;
+    int vbits = 2;                    // 2: states only; 8: state + Eq. 2 gain (f1)
     int pbits = 0;                    // Morton: cube side 2^pbits
     uint32_t px = 0, py = 0, pz = 0;  // linear: padded extents (kBorder sentinel voxels each side)
     uint64_t nvox_pad = 0;
@@ -181,11 +182,12 @@ struct nbt_idbuf_s {
 namespace nbt {
 
 // Map store (k_map.cu)
-nbt_status launch_map_pack(nbt_ctx ctx, nbt_map m, const uint8_t *d_codes);
+nbt_status launch_map_pack(nbt_ctx ctx, nbt_map m, const uint8_t *d_codes, const uint8_t *d_levels);
 nbt_status launch_map_classify(nbt_ctx ctx, const float *d_p, const uint8_t *d_obs, size_t n, double t_occ,
-                               double t_free, uint8_t *d_codes_out);
-nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const uint8_t *d_codes, size_t n);
-nbt_status launch_map_unpack(nbt_ctx ctx, nbt_map m, uint8_t *d_codes_out);
+                               double t_free, uint8_t *d_codes_out, uint8_t *d_levels_out);
+nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const uint8_t *d_codes,
+                             const uint8_t *d_levels, size_t n);
+nbt_status launch_map_unpack(nbt_ctx ctx, nbt_map m, uint8_t *d_codes_out, uint8_t *d_levels_out);
 
 // Perspectives (k_sample.cu)
 nbt_status launch_sample(nbt_ctx ctx, const double poi[3], double r_s, int32_t n, uint64_t seed, int32_t mode,

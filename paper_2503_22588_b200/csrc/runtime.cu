@@ -455,7 +455,7 @@ static nbt_status check_desc(const nbt_map_desc *d)
     return NBT_OK;
 }
 
-nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
+static nbt_status map_create(nbt_ctx ctx, const nbt_map_desc *desc, int vbits, nbt_map *out)
 {
     nbt_status s;
     if (!out) return fail(NBT_ERR_INVALID_ARG, "nbt_map_create: null out");
@@ -466,6 +466,7 @@ nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
     m->ctx = ctx;
     ctx_retain(ctx);
     m->desc = *desc;
+    m->vbits = vbits;
     m->px = desc->nx + 2 * kBorder; m->py = desc->ny + 2 * kBorder; m->pz = desc->nz + 2 * kBorder;
     m->nvox_pad = (uint64_t)m->px * m->py * m->pz;
     // Store layout: linear by default (fewest instructions per voxel step, fastest on
@@ -486,7 +487,8 @@ nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
             m->nvox_pad = cube;
         }
     }
-    m->nwords = (size_t)((m->nvox_pad + 15) / 16);
+    const size_t per_word = vbits == 2 ? 16 : 4;
+    m->nwords = (size_t)((m->nvox_pad + per_word - 1) / per_word);
     cudaError_t e = cudaMalloc(&m->d_words, m->nwords * 4);
     if (e != cudaSuccess) {
         nbt_map_destroy(m);
@@ -497,7 +499,7 @@ nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
     size_t n = (size_t)desc->nx * desc->ny * desc->nz;
     if ((s = zeros.ensure(n))) { nbt_map_destroy(m); return s; }
     e = cudaMemsetAsync(zeros.p, 0, n, ctx->stream);
-    if (e == cudaSuccess) s = launch_map_pack(ctx, m, zeros.as<uint8_t>());
+    if (e == cudaSuccess) s = launch_map_pack(ctx, m, zeros.as<uint8_t>(), nullptr);
     else s = cuda_fail(e, "nbt_map_create: memset");
     if (s == NBT_OK) {
         e = cudaStreamSynchronize(ctx->stream);
@@ -507,6 +509,16 @@ nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
     if (s) { nbt_map_destroy(m); return s; }
     *out = m;
     return NBT_OK;
+}
+
+nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
+{
+    return map_create(ctx, desc, 2, out);
+}
+
+nbt_status nbt_map_create_prob(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
+{
+    return map_create(ctx, desc, 8, out);
 }
 
 static nbt_status map_nvox(nbt_map m, size_t n, const char *who)
@@ -535,7 +547,7 @@ nbt_status nbt_map_upload(nbt_map m, const uint8_t *codes, size_t n, int on_devi
         if (e != cudaSuccess) { tmp.release(); return cuda_fail(e, "nbt_map_upload: H2D"); }
         src = tmp.as<uint8_t>();
     }
-    s = launch_map_pack(ctx, m, src);
+    s = launch_map_pack(ctx, m, src, nullptr);
     if (s == NBT_OK) s = take_device_error(ctx, "nbt_map_upload");
     tmp.release();
     return s;
@@ -550,7 +562,7 @@ nbt_status nbt_map_upload_prob(nbt_map m, const float *p, const uint8_t *observe
     if ((s = bind(ctx))) return s;
     if (!p || !observed) return fail(NBT_ERR_INVALID_ARG, "nbt_map_upload_prob: null input");
     if (!isfinite(t_occ) || !isfinite(t_free)) return fail(NBT_ERR_INVALID_ARG, "thresholds must be finite");
-    DevBuf dp, dobs, codes;
+    DevBuf dp, dobs, codes, levels;
     const float *sp = p;
     const uint8_t *so = observed;
     cudaError_t e = cudaSuccess;
@@ -561,15 +573,17 @@ nbt_status nbt_map_upload_prob(nbt_map m, const float *p, const uint8_t *observe
         sp = dp.as<float>();
         so = dobs.as<uint8_t>();
     }
-    if (e == cudaSuccess && (s = codes.ensure(n)) == NBT_OK) {
-        s = launch_map_classify(ctx, sp, so, n, t_occ, t_free, codes.as<uint8_t>());
-        if (s == NBT_OK) s = launch_map_pack(ctx, m, codes.as<uint8_t>());
+    const bool prob = m->vbits == 8;
+    if (e == cudaSuccess && (s = codes.ensure(n)) == NBT_OK && (!prob || (s = levels.ensure(n)) == NBT_OK)) {
+        s = launch_map_classify(ctx, sp, so, n, t_occ, t_free, codes.as<uint8_t>(),
+                                prob ? levels.as<uint8_t>() : nullptr);
+        if (s == NBT_OK) s = launch_map_pack(ctx, m, codes.as<uint8_t>(), prob ? levels.as<uint8_t>() : nullptr);
         if (s == NBT_OK) s = take_device_error(ctx, "nbt_map_upload_prob");
     } else if (e != cudaSuccess) {
         s = cuda_fail(e, "nbt_map_upload_prob: H2D");
     }
     cudaStreamSynchronize(ctx->stream);
-    dp.release(); dobs.release(); codes.release();
+    dp.release(); dobs.release(); codes.release(); levels.release();
     return s;
 }
 
@@ -601,7 +615,50 @@ nbt_status nbt_map_update(nbt_map m, const int32_t *ijk, const uint8_t *codes, s
         dijk = ctx->deltas.as<int32_t>();
         dcodes = ctx->deltas.as<uint8_t>() + n * 12;
     }
-    return launch_map_update(ctx, m, dijk, dcodes, n);
+    return launch_map_update(ctx, m, dijk, dcodes, nullptr, n);
+}
+
+nbt_status nbt_map_update_prob(nbt_map m, const int32_t *ijk, const float *p, const uint8_t *observed, size_t n,
+                               int on_device, double t_occ, double t_free)
+{
+    if (!m) return fail(NBT_ERR_INVALID_ARG, "nbt_map_update_prob: null map");
+    nbt_ctx ctx = m->ctx;
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (n == 0) return NBT_OK;
+    if (!ijk || !p || !observed || !isfinite(t_occ) || !isfinite(t_free))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_map_update_prob: bad argument");
+    if (n >= (1ull << 31)) return fail(NBT_ERR_INVALID_ARG, "nbt_map_update_prob: too many deltas");
+    if (ctx->capturing && !on_device)
+        return fail(NBT_ERR_STATE, "nbt_map_update_prob: host deltas during graph capture");
+    // device scratch: [ijk 12n | p 4n | observed n | codes n | levels n]
+    const size_t bytes = n * 19;
+    if ((s = ctx->deltas.ensure(bytes))) return s;
+    char *base = ctx->deltas.as<char>();
+    const int32_t *dijk = ijk;
+    const float *dp = p;
+    const uint8_t *dobs = observed;
+    if (!on_device) {
+        for (size_t i = 0; i < n; ++i) {
+            const int32_t *v = ijk + 3 * i;
+            if (v[0] < 0 || v[1] < 0 || v[2] < 0 || v[0] >= m->desc.nx || v[1] >= m->desc.ny || v[2] >= m->desc.nz)
+                return fail(NBT_ERR_INVALID_ARG, "nbt_map_update_prob: voxel outside the grid at " + std::to_string(i));
+            if (!isfinite(p[i])) return fail(NBT_ERR_INVALID_ARG, "nbt_map_update_prob: non-finite p");
+        }
+        if ((s = ctx->stage_in[1].acquire(n * 17))) return s;
+        memcpy(ctx->stage_in[1].p, ijk, n * 12);
+        memcpy((char *)ctx->stage_in[1].p + n * 12, p, n * 4);
+        memcpy((char *)ctx->stage_in[1].p + n * 16, observed, n);
+        NBT_CUDA(cudaMemcpyAsync(base, ctx->stage_in[1].p, n * 17, cudaMemcpyHostToDevice, ctx->stream));
+        if ((s = ctx->stage_in[1].mark(ctx->stream))) return s;
+        dijk = reinterpret_cast<const int32_t *>(base);
+        dp = reinterpret_cast<const float *>(base + n * 12);
+        dobs = reinterpret_cast<const uint8_t *>(base + n * 16);
+    }
+    uint8_t *dcodes = reinterpret_cast<uint8_t *>(base + n * 17);
+    uint8_t *dlevels = reinterpret_cast<uint8_t *>(base + n * 18);
+    if ((s = launch_map_classify(ctx, dp, dobs, n, t_occ, t_free, dcodes, dlevels))) return s;
+    return launch_map_update(ctx, m, dijk, dcodes, m->vbits == 8 ? dlevels : nullptr, n);
 }
 
 nbt_status nbt_map_device_buffer(nbt_map m, void **dev_ptr, size_t *bytes)
@@ -621,11 +678,31 @@ nbt_status nbt_map_download(nbt_map m, uint8_t *codes_out, size_t n)
     if ((s = bind(ctx))) return s;
     DevBuf tmp;
     if ((s = tmp.ensure(n))) return s;
-    s = launch_map_unpack(ctx, m, tmp.as<uint8_t>());
+    s = launch_map_unpack(ctx, m, tmp.as<uint8_t>(), nullptr);
     if (s == NBT_OK) {
         cudaError_t e = cudaMemcpyAsync(codes_out, tmp.p, n, cudaMemcpyDeviceToHost, ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) s = cuda_fail(e, "nbt_map_download");
+    }
+    tmp.release();
+    return s;
+}
+
+nbt_status nbt_map_download_levels(nbt_map m, uint8_t *levels_out, size_t n)
+{
+    nbt_status s;
+    if ((s = map_nvox(m, n, "nbt_map_download_levels"))) return s;
+    if (!levels_out) return fail(NBT_ERR_INVALID_ARG, "nbt_map_download_levels: null out");
+    if (m->vbits != 8) return fail(NBT_ERR_STATE, "nbt_map_download_levels: map stores no probabilities");
+    nbt_ctx ctx = m->ctx;
+    if ((s = bind(ctx))) return s;
+    DevBuf tmp;
+    if ((s = tmp.ensure(n))) return s;
+    s = launch_map_unpack(ctx, m, nullptr, tmp.as<uint8_t>());
+    if (s == NBT_OK) {
+        cudaError_t e = cudaMemcpyAsync(levels_out, tmp.p, n, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) s = cuda_fail(e, "nbt_map_download_levels");
     }
     tmp.release();
     return s;

@@ -671,3 +671,75 @@ def test_handles_destroyed_in_any_order(nbt):
     assert (m.download() == 0).all()
     buf.close()
     m.close()
+
+
+# ------------------------------------------- f1: per-voxel probability (exact Eq. 2)
+
+def _prob_scene(shape, seed):
+    rng = np.random.default_rng(seed)
+    codes = rand_map(0, 0.3, 0.65, 0.05, seed=seed, shape=shape)
+    p = np.where(codes == 1, rng.uniform(0.12, 0.5, shape), rng.uniform(0.5, 0.97, shape)).astype(np.float32)
+    observed = (codes != 0).astype(np.uint8)
+    return p, observed
+
+
+@pytest.mark.parametrize("layout", ["linear", "morton"])
+def test_prob_map_id_matches_oracle(nbt, ctx, layout, monkeypatch):
+    """8-bit store: upload_prob reproduces the oracle's states and levels, and the ID (exact
+    Eq. 2 per voxel) matches the oracle bit for bit: per-state totals and g_P."""
+    monkeypatch.setenv("NBT_MAP_LAYOUT", layout)
+    p, obs = _prob_scene((22, 26, 30), seed=5)
+    codes, levels = oracle.quantize_prob(p, obs)
+    m = nbt.Map(ctx, nbt.map_desc(30, 26, 22, 1.0), prob=True)
+    m.upload_prob(p, obs)
+    assert np.array_equal(m.download(), codes)
+    assert np.array_equal(m.download_levels(), levels)
+    om = oracle.OracleMap(codes, levels=levels)
+    poi = np.array([15.5, 13.5, 11.5])
+    P = oracle.sample_perspectives(poi, 10.0, 30, seed=3)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 24, 17)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, 24, 17)
+    cam.add_corners = ocam.add_corners = 1
+    cloud = nbt.id_compute(ctx, m, poi, P, cam, 30.0)
+    _, g, c, tg = oracle.id_compute(om, poi, P, ocam, 30.0, nthreads=NTHREADS, with_tg=True)
+    assert np.array_equal(cloud.counts.astype(np.int64), c)
+    assert np.array_equal(cloud.gain, g)
+    assert (tg > 0).all()
+
+
+def test_prob_map_updates_and_defaults(nbt, ctx):
+    """update_prob applies (state, level) deltas in order (last wins); state-only writes store
+    P_F = g_F and P_O = 1 - g_O rounded to k/63 (8 and 61 with the default gains)."""
+    p, obs = _prob_scene((9, 10, 11), seed=8)
+    codes, levels = oracle.quantize_prob(p, obs)
+    m = nbt.Map(ctx, nbt.map_desc(11, 10, 9, 1.0), prob=True)
+    m.upload_prob(p, obs)
+    rng = np.random.default_rng(1)
+    n = 700
+    ijk = np.stack([rng.integers(0, 11, n), rng.integers(0, 10, n), rng.integers(0, 9, n)], 1).astype(np.int32)
+    ijk[n // 2:] = ijk[:n - n // 2]
+    dp = rng.uniform(0, 1, n).astype(np.float32)
+    dobs = (rng.uniform(size=n) < 0.9).astype(np.uint8)
+    m.update_prob(ijk, dp, dobs)
+    dc, dl = oracle.quantize_prob(dp, dobs)
+    want_c, want_l = codes.copy(), levels.copy()
+    for (x, y, z), cc, ll in zip(ijk, dc, dl):
+        want_c[z, y, x] = cc
+        want_l[z, y, x] = ll
+    assert np.array_equal(m.download(), want_c)
+    assert np.array_equal(m.download_levels(), want_l)
+    m.update(np.array([[1, 2, 3], [4, 5, 6], [7, 8, 0]], np.int32), np.array([1, 2, 0], np.uint8))
+    lv = m.download_levels()
+    assert (lv[3, 2, 1], lv[6, 5, 4], lv[0, 8, 7]) == (8, 61, 0)
+    ctx.sync()
+
+
+def test_prob_map_walks(nbt, ctx):
+    """The 8-bit store walks the same voxels with the same states as the 2-bit store."""
+    p, obs = _prob_scene((12, 12, 12), seed=2)
+    codes, levels = oracle.quantize_prob(p, obs)
+    m = nbt.Map(ctx, nbt.map_desc(12, 12, 12, 1.0), prob=True)
+    m.upload_prob(p, obs)
+    om = oracle.OracleMap(codes)
+    o, e = random_segments_q12(1500, -5.0, 17.0, seed=6)
+    _compare_walks(nbt, ctx, m, om, o, e)

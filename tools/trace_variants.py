@@ -1,7 +1,8 @@
 """Time the trace kernel on config workloads (device-resident inputs, CUDA events around
-each k_id_trace launch).  Variant via NBT_TRACE_VARIANT (read by libnbt at first use).
+each k_id_trace launch).  Experiment knobs are environment variables read by libnbt (NBT_MAP_LAYOUT, NBT_REFILL_MIN,
+NBT_TRACE_CARVEOUT); --prob uses the 8-bit per-voxel-probability store (f1).
 
-    NBT_TRACE_VARIANT=1 python tools/trace_variants.py B "C'"
+    python tools/trace_variants.py B "C'" [--prob]
 """
 import json
 import os
@@ -17,14 +18,21 @@ import paper_2503_22588_b200 as nbt
 from nbt_inputs import CONFIGS, FOV_H, FOV_V
 
 
-def run(cfg_name, reps=5):
+def run(cfg_name, reps=5, prob=False):
     cfg = CONFIGS[cfg_name]
     dev = torch.device("cuda", 0)
     s = torch.cuda.Stream(dev)
     torch.cuda.set_stream(s)
     ctx = nbt.Ctx(0, s.cuda_stream)
-    m = nbt.Map(ctx, nbt.map_desc(cfg.n, cfg.n, cfg.n, cfg.voxel_size))
-    m.upload(cfg.map_codes())
+    m = nbt.Map(ctx, nbt.map_desc(cfg.n, cfg.n, cfg.n, cfg.voxel_size), prob=prob)
+    codes = cfg.map_codes()
+    if prob:      # per-voxel probabilities: Free P in [0.12, 0.5), Occupied in [0.5, 0.97]
+        rng = np.random.default_rng(0)
+        u = rng.random(codes.shape, dtype=np.float32)
+        p = np.where(codes == 1, 0.12 + 0.38 * u, 0.5 + 0.47 * u).astype(np.float32)
+        m.upload_prob(p, (codes != 0).astype(np.uint8))
+    else:
+        m.upload(codes)
     cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
     persp = torch.empty((cfg.n_persp, 3), dtype=torch.float64, device=dev)
     nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode, out=persp)
@@ -39,11 +47,12 @@ def run(cfg_name, reps=5):
     counts = out.counts.cpu().numpy()
     lookups = float(counts[:, 3].sum())
     ms /= n
-    return {"config": cfg_name, "variant": os.environ.get("NBT_TRACE_VARIANT", "0"), "trace_ms": ms,
+    return {"config": cfg_name, "store": "8-bit prob" if prob else "2-bit", "trace_ms": ms,
             "rays_per_s": cfg.rays_per_id / (ms / 1e3), "lookups_per_s": lookups / (ms / 1e3),
             "lookups": lookups, "checksum": int(counts.sum())}
 
 
 if __name__ == "__main__":
-    for name in sys.argv[1:] or ["B"]:
-        print(json.dumps(run(name)), flush=True)
+    prob = "--prob" in sys.argv
+    for name in [a for a in sys.argv[1:] if not a.startswith("--")] or ["B"]:
+        print(json.dumps(run(name, prob=prob)), flush=True)
