@@ -209,3 +209,99 @@ CONFIGS = {
     "E": Config("E", 256, 0.01, 15.0, 1, 512, 1.0, 0, 1000, 64, 48, 1.5,
                 extra={"cycles": 200, "n_b": 10, "queries": 1984, "power_p": 2.0}),
 }
+
+
+# ----------------------------------------------------------- sensor clouds
+
+@dataclass(frozen=True)
+class CloudConfig:
+    """A map-integration workload (DESIGN.md input recipe, row f3): depth frames of the
+    SYN scene taken from sensors circling the PoI, integrated into an empty map."""
+    name: str
+    n: int                   # map edge in voxels
+    voxel_size: float        # s_Vox
+    r_o: float               # object radius (voxels), as SYN
+    width: int               # depth image W (Azure Kinect NFOV unbinned: 640 x 576)
+    height: int
+    sensor_dist: float       # sensor distance to the PoI (world units)
+    n_clouds: int            # frames per workload (one per sensor pose)
+    leaf: float              # voxel-filter leaf (world units)
+    max_range: float         # integration range (world units)
+    seed: int
+
+    @property
+    def poi(self) -> np.ndarray:
+        return poi_voxel_centre(self.n, self.voxel_size)
+
+    def sensor(self, k: int) -> np.ndarray:
+        """Pose k: on a circle around the PoI, 25 degrees above its horizontal plane."""
+        phi = 2.0 * math.pi * (k + 0.125) / max(1, self.n_clouds)
+        el = math.radians(25.0)
+        d = np.array([math.cos(phi) * math.cos(el), math.sin(phi) * math.cos(el), math.sin(el)])
+        return self.poi + self.sensor_dist * d
+
+    def cloud(self, k: int) -> np.ndarray:
+        return sensor_cloud(self.n, self.voxel_size, self.r_o, self.sensor(k), self.poi, self.width, self.height,
+                            seed=self.seed + 104729 * k)
+
+
+def sensor_cloud(n: int, voxel_size: float, r_o: float, sensor, target, width: int, height: int,
+                 noise: float = 1e-3, drop: float = 0.01, seed: int = 0) -> np.ndarray:
+    """Synthetic depth frame of the SYN scene (world units, float64 [m, 3]).
+
+    The scene is SYN's geometry as surfaces: the object sphere (radius r_o voxels at
+    the PoI), the table top (the slab's upper face, a square of half-side 0.35 N about
+    the map centre) and the boundary of observed space as a spherical wall of radius
+    0.45 N about the map centre.  A pinhole sensor at `sensor` looks at `target`
+    (up hint +z) over a width x height pixel lattice spanning the 75 x 65 degree FoV;
+    each pixel returns the nearest surface along its ray, with N(0, noise) depth noise,
+    and is dropped w.p. `drop` (invalid depth).  Scene generation only: none of the
+    mapping method's arithmetic.
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    s = voxel_size
+    o = np.asarray(sensor, dtype=np.float64)
+    tgt = np.asarray(target, dtype=np.float64)
+    fwd = tgt - o
+    fwd /= np.linalg.norm(fwd)
+    right = np.cross(fwd, [0.0, 0.0, 1.0])
+    right /= np.linalg.norm(right)
+    up = np.cross(right, fwd)
+    u = np.linspace(-1.0, 1.0, width) * math.tan(FOV_H / 2)
+    v = np.linspace(-1.0, 1.0, height) * math.tan(FOV_V / 2)
+    U, V = np.meshgrid(u, v, indexing="xy")
+    d = fwd[None, :] + U.reshape(-1, 1) * right[None, :] + V.reshape(-1, 1) * up[None, :]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    inf = np.full(d.shape[0], np.inf)
+    # object sphere (outside surface)
+    c = (n // 2 + 0.5) * s
+    oc = o - np.array([c, c, c])
+    b = d @ oc
+    disc = b * b - (oc @ oc - (r_o * s) ** 2)
+    t_obj = np.where(disc >= 0, -b - np.sqrt(np.maximum(disc, 0.0)), np.inf)
+    t_obj = np.where(t_obj > 0, t_obj, np.inf)
+    # table top plane
+    mc = n / 2.0 * s
+    z_top = (n // 2 + 0.5 - r_o - 2.0) * s
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t_tab = (z_top - o[2]) / d[:, 2]
+    hit = o[None, :] + t_tab[:, None] * d
+    ok = (t_tab > 0) & (np.abs(hit[:, 0] - mc) <= 0.35 * n * s) & (np.abs(hit[:, 1] - mc) <= 0.35 * n * s)
+    t_tab = np.where(ok, t_tab, inf)
+    # boundary wall (inside surface of a sphere about the map centre)
+    om = o - np.array([mc, mc, mc])
+    b2 = d @ om
+    disc2 = b2 * b2 - (om @ om - (0.45 * n * s) ** 2)
+    t_wall = np.where(disc2 >= 0, -b2 + np.sqrt(np.maximum(disc2, 0.0)), np.inf)
+    t = np.minimum(np.minimum(t_obj, t_tab), t_wall)
+    t = t + rng.normal(0.0, noise, t.shape)
+    keep = np.isfinite(t) & (t > 0) & (rng.random(t.shape) >= drop)
+    return o[None, :] + t[keep, None] * d[keep]
+
+
+CLOUD_CONFIGS = {
+    # small: 64^3 map, 160 x 144 frames (oracle in well under a second)
+    "F0": CloudConfig("F0", 64, 0.04, 4.0, 160, 144, 0.6, 4, 0.04, 1.2, 11),
+    # full: config B's 256^3 / 1 cm map, Azure Kinect NFOV unbinned 640 x 576 frames
+    "F": CloudConfig("F", 256, 0.01, 15.0, 640, 576, 0.6, 8, 0.01, 1.2, 12),
+}

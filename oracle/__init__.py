@@ -87,6 +87,13 @@ def lib():
         L.orc_orientation_factor.argtypes = [dp, dp, dp, C.c_double, dp]
         L.orc_info_cost.argtypes = [C.c_int32, ip, C.POINTER(dp), C.POINTER(dp), dp, dp, C.c_int32, C.c_int32, dp,
                                     C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32, dp, dp, dp]
+        fp = C.POINTER(C.c_float)
+        L.orc_voxel_filter.argtypes = [dp, C.c_int64, C.c_double, dp, ip, i64p]
+        L.orc_integrate.argtypes = [fp, C.c_int32, C.c_int32, C.c_int32, C.c_double, dp, dp, dp, C.c_int64,
+                                    C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                    u8p, i64p]
+        L.orc_occ_classify.argtypes = [fp, C.c_int64, C.c_double, C.c_double, u8p, u8p]
+        L.orc_occ_classify.restype = None
     return _lib
 
 
@@ -288,4 +295,55 @@ def quantize_prob(p, observed, t_occ=0.5, t_free=0.5):
     codes = np.zeros(p.shape, np.uint8); levels = np.zeros(p.shape, np.uint8)
     lib().orc_quantize_prob(_p(p, C.c_float), _p(obs, C.c_uint8), p.size, float(t_occ), float(t_free),
                             _p(codes, C.c_uint8), _p(levels, C.c_uint8))
+    return codes, levels
+
+
+# ------------------------------------------------------------ map integration (f3)
+
+INTEGRATE_DEFAULTS = dict(p_hit=0.7, p_miss=0.4, p_min=0.12, p_max=0.97, max_range=5.0)
+
+
+def voxel_filter(points, leaf):
+    """(centroids [m, 3], counts [m]) of the voxel filter (reading Q33)."""
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    n = pts.shape[0]
+    out = np.zeros((max(n, 1), 3)); cnt = np.zeros(max(n, 1), np.int32)
+    m = C.c_int64()
+    st = lib().orc_voxel_filter(_d(pts), n, float(leaf), _d(out), _p(cnt, C.c_int32), C.byref(m))
+    if st:
+        raise OracleError(st, "voxel_filter")
+    return out[:m.value].copy(), cnt[:m.value].copy()
+
+
+def new_logodds(shape_zyx):
+    """A log-odds store with every voxel unobserved (NaN), indexed [z, y, x]."""
+    return np.full(shape_zyx, np.nan, dtype=np.float32)
+
+
+def integrate(L, voxel_size, map_origin, origin, points, leaf=0.0, p_hit=0.7, p_miss=0.4, p_min=0.12, p_max=0.97,
+              max_range=5.0):
+    """Integrate one cloud into the float32 log-odds store L ([z, y, x], in place, Q33-Q37).
+
+    Returns (touched [z, y, x] uint8: 0 / 1 miss / 3 hit, number of rays)."""
+    assert L.dtype == np.float32 and L.flags.c_contiguous
+    nz, ny, nx = L.shape
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    mo = np.ascontiguousarray(map_origin, dtype=np.float64)
+    o = np.ascontiguousarray(origin, dtype=np.float64)
+    touched = np.zeros(L.shape, np.uint8)
+    nr = C.c_int64()
+    st = lib().orc_integrate(_p(L, C.c_float), nx, ny, nz, float(voxel_size), _d(mo), _d(o), _d(pts), pts.shape[0],
+                             float(p_hit), float(p_miss), float(p_min), float(p_max), float(max_range), float(leaf),
+                             _p(touched, C.c_uint8), C.byref(nr))
+    if st:
+        raise OracleError(st, "integrate")
+    return touched, nr.value
+
+
+def occ_classify(L, t_occ=0.5, t_free=0.5):
+    """(codes, levels) of a log-odds store (reading Q37)."""
+    L = np.ascontiguousarray(L, dtype=np.float32)
+    codes = np.zeros(L.shape, np.uint8); levels = np.zeros(L.shape, np.uint8)
+    lib().orc_occ_classify(_p(L, C.c_float), L.size, float(t_occ), float(t_free), _p(codes, C.c_uint8),
+                           _p(levels, C.c_uint8))
     return codes, levels

@@ -25,6 +25,9 @@
  *   orc_sample_perspectives pinned (forced-sample example, radius bounds, radial CDF)
  *   orc_classify           pinned  (S:69-74 threshold rule examples)
  *   orc_philox4x32         pinned  (published Random123 known-answer vectors)
+ *   orc_voxel_filter       pinned  (S:53-56 examples, brute-force bucketing)
+ *   orc_integrate          pinned  (S:61-64 examples, range truncation, hit-wins, exact touch sets)
+ *   orc_occ_classify       pinned  (S:72-74 examples, round(63 sigmoid(L)) away from boundaries)
  */
 #include <math.h>
 #include <stdint.h>
@@ -652,6 +655,196 @@ int orc_map_update(uint8_t *codes, int32_t nx, int32_t ny, int32_t nz, const int
         codes[x + (int64_t)nx * (y + (int64_t)ny * z)] = vals[i];
     }
     return ORC_OK;
+}
+
+/* ------------------------------------------- map integration */
+
+/* Voxel filter (reading Q33): every point goes to the leaf cell
+ * (floor(x/leaf), floor(y/leaf), floor(z/leaf)); each occupied cell yields ONE point,
+ * the centroid of its inputs, summed in input order and divided by the count.  Cells
+ * are output in ascending (iz, iy, ix) order.  |cell index| must stay below 2^20 and
+ * every coordinate must be finite (INVALID_ARG otherwise).  out_xyz / out_count hold
+ * room for n cells; *m_out = number of cells. */
+typedef struct { int64_t c[3]; int64_t idx; } orc_cellkey;
+
+static int cellkey_cmp(const void *a, const void *b)
+{
+    const orc_cellkey *x = (const orc_cellkey *)a, *y = (const orc_cellkey *)b;
+    for (int k = 2; k >= 0; --k)
+        if (x->c[k] != y->c[k]) return x->c[k] < y->c[k] ? -1 : 1;
+    return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+
+int orc_voxel_filter(const double *pts, int64_t n, double leaf, double *out_xyz, int32_t *out_count, int64_t *m_out)
+{
+    if (n < 0 || !(leaf > 0) || !m_out || (n > 0 && (!pts || !out_xyz))) return ORC_ERR_INVALID_ARG;
+    *m_out = 0;
+    if (n == 0) return ORC_OK;
+    orc_cellkey *k = (orc_cellkey *)malloc((size_t)n * sizeof *k);
+    if (!k) return ORC_ERR_INVALID_ARG;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int a = 0; a < 3; ++a) {
+            double v = pts[3 * i + a];
+            if (!isfinite(v)) { free(k); return ORC_ERR_INVALID_ARG; }
+            double c = floor(v / leaf);
+            if (!(fabs(c) < 1048576.0)) { free(k); return ORC_ERR_INVALID_ARG; }
+            k[i].c[a] = (int64_t)c;
+        }
+        k[i].idx = i;
+    }
+    qsort(k, (size_t)n, sizeof *k, cellkey_cmp);
+    int64_t m = 0;
+    for (int64_t i = 0; i < n;) {
+        int64_t j = i;
+        double sum[3] = {0.0, 0.0, 0.0};
+        while (j < n && k[j].c[0] == k[i].c[0] && k[j].c[1] == k[i].c[1] && k[j].c[2] == k[i].c[2]) {
+            for (int a = 0; a < 3; ++a) sum[a] += pts[3 * k[j].idx + a];   /* ascending input index */
+            ++j;
+        }
+        for (int a = 0; a < 3; ++a) out_xyz[3 * m + a] = sum[a] / (double)(j - i);
+        if (out_count) out_count[m] = (int32_t)(j - i);
+        ++m;
+        i = j;
+    }
+    free(k);
+    *m_out = m;
+    return ORC_OK;
+}
+
+/* World position -> Q12 walk coordinate (reading Q34): round-half-even of
+ * ((x - origin) / s) * 4096. */
+static int world_to_q12(double x, double origin, double s, int32_t *out)
+{
+    double q = ((x - origin) / s) * 4096.0;
+    if (!(fabs(q) < (double)QLIM)) return ORC_ERR_INVALID_ARG;
+    *out = (int32_t)nearbyint(q);
+    return ORC_OK;
+}
+
+/* Log-odds of a probability, rounded to float (reading Q36). */
+static float logodds_f(double p) { return (float)log(p / (1.0 - p)); }
+
+/*
+ * Integrate one point cloud into a log-odds store (readings Q33-Q37).
+ *
+ *   L[x + nx (y + ny z)]  float log-odds per voxel, NaN = never observed (prior P = 0.5)
+ *   origin                the sensor position (world)
+ *   pts, n                the cloud (world); filtered by orc_voxel_filter when leaf > 0
+ *
+ * Every (filtered) point p gives the segment origin -> p; if |p - origin| > max_range
+ * (> 0) the segment is cut at max_range and carves only (no hit).  Both ends go to Q12
+ * (world_to_q12) and the exact DDA of orc_trace_ray lists the voxels the segment
+ * visits.  Per cloud every in-grid voxel is updated at most once (Q35): by L_hit if some
+ * segment ENDS in it with a hit, else by L_miss if some segment visits it (the end
+ * voxel of a cut segment, and the sensor's own voxel, included).  The update is
+ * L := clamp((observed ? L : 0) + delta, L_min, L_max) in float.  touched (optional,
+ * nx*ny*nz bytes) receives 0 / 1 (miss) / 3 (hit; bit 0 = visited, bit 1 = hit).
+ */
+int orc_integrate(float *L, int32_t nx, int32_t ny, int32_t nz, double voxel_size, const double map_origin[3],
+                  const double origin[3], const double *pts, int64_t n, double p_hit, double p_miss, double p_min,
+                  double p_max, double max_range, double leaf, uint8_t *touched, int64_t *n_rays_out)
+{
+    if (!L || nx < 1 || ny < 1 || nz < 1 || !(voxel_size > 0) || n < 0 || (n > 0 && !pts)) return ORC_ERR_INVALID_ARG;
+    if (!(leaf >= 0) || !(p_hit > 0 && p_hit < 1) || !(p_miss > 0 && p_miss < 1) || !(p_min > 0 && p_min < 1) ||
+        !(p_max > 0 && p_max < 1) || !(p_min <= p_max))
+        return ORC_ERR_INVALID_ARG;
+    for (int a = 0; a < 3; ++a)
+        if (!isfinite(origin[a])) return ORC_ERR_INVALID_ARG;
+    int64_t nvox = (int64_t)nx * ny * nz;
+    const double *ray_end = pts;
+    double *filt = NULL;
+    int64_t m = n;
+    if (leaf > 0 && n > 0) {
+        filt = (double *)malloc((size_t)n * 3 * sizeof(double));
+        int st = orc_voxel_filter(pts, n, leaf, filt, NULL, &m);
+        if (st) { free(filt); return st; }
+        ray_end = filt;
+    } else {
+        for (int64_t i = 0; i < 3 * n; ++i)
+            if (!isfinite(pts[i])) return ORC_ERR_INVALID_ARG;
+    }
+    uint8_t *flag = (uint8_t *)calloc((size_t)nvox, 1);
+    uint8_t *all_free = (uint8_t *)malloc((size_t)nvox);
+    memset(all_free, 1, (size_t)nvox);
+    orc_map walk = {nx, ny, nz, voxel_size, {map_origin[0], map_origin[1], map_origin[2]}, {1.0, 1.0, 1.0}, 0,
+                    all_free, NULL};
+    int status = ORC_OK;
+    int32_t o12[3];
+    for (int a = 0; a < 3; ++a) status |= world_to_q12(origin[a], map_origin[a], voxel_size, &o12[a]);
+    for (int64_t i = 0; i < m && status == ORC_OK; ++i) {
+        const double *p = ray_end + 3 * i;
+        double d[3] = {p[0] - origin[0], p[1] - origin[1], p[2] - origin[2]};
+        double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+        double q[3] = {p[0], p[1], p[2]};
+        int hit = 1;
+        if (max_range > 0 && dist > max_range) {
+            double f = max_range / dist;
+            for (int a = 0; a < 3; ++a) q[a] = origin[a] + d[a] * f;
+            hit = 0;
+        }
+        int32_t e12[3];
+        for (int a = 0; a < 3; ++a) status |= world_to_q12(q[a], map_origin[a], voxel_size, &e12[a]);
+        if (status) break;
+        int64_t len = 1;
+        for (int a = 0; a < 3; ++a) len += llabs(floor_div(e12[a], QD) - floor_div(o12[a], QD));
+        int32_t *ijk = (int32_t *)malloc((size_t)len * 3 * sizeof(int32_t));
+        uint8_t *code = (uint8_t *)malloc((size_t)len);
+        int32_t got = 0;
+        orc_ray r;
+        status = orc_trace_ray(&walk, o12, e12, (int32_t)len, ijk, code, &got, &r);
+        if (!status && got != len) status = ORC_ERR_SELFCHECK;   /* all-Free map: no early stop */
+        for (int64_t s = 0; s < got && !status; ++s) {
+            if (code[s] == 255) continue;                           /* outside the grid */
+            int64_t v = ijk[3 * s] + (int64_t)nx * (ijk[3 * s + 1] + (int64_t)ny * ijk[3 * s + 2]);
+            flag[v] |= (s == got - 1 && hit) ? 3 : 1;
+        }
+        free(ijk);
+        free(code);
+    }
+    if (status == ORC_OK) {
+        float lh = logodds_f(p_hit), lm = logodds_f(p_miss), lo = logodds_f(p_min), hi = logodds_f(p_max);
+        for (int64_t v = 0; v < nvox; ++v) {
+            if (!flag[v]) continue;
+            float l0 = isnan(L[v]) ? 0.0f : L[v];
+            float l1 = l0 + ((flag[v] & 2) ? lh : lm);
+            if (l1 < lo) l1 = lo;
+            if (l1 > hi) l1 = hi;
+            L[v] = l1;
+        }
+        if (touched) memcpy(touched, flag, (size_t)nvox);
+    }
+    if (n_rays_out) *n_rays_out = m;
+    free(flag);
+    free(all_free);
+    free(filt);
+    return status;
+}
+
+/* State and probability level of each voxel of a log-odds store (Q37):
+ * never observed -> Unknown, level 0; L >= logit(t_occ) -> Occupied; L <= logit(t_free)
+ * -> Free; else Unknown; level = number of k in 1..63 with L >= logit((k - 1/2)/63),
+ * i.e. round(63 P) with the rounding boundaries taken in log-odds (thresholds rounded
+ * to float once). */
+void orc_occ_classify(const float *L, int64_t n, double t_occ, double t_free, uint8_t *codes_out,
+                      uint8_t *levels_out)
+{
+    float th_occ = logodds_f(t_occ), th_free = logodds_f(t_free);
+    float phi[PLEVELS];
+    for (int k = 1; k <= PLEVELS; ++k) phi[k - 1] = logodds_f((k - 0.5) / PLEVELS);
+    for (int64_t i = 0; i < n; ++i) {
+        float l = L[i];
+        if (isnan(l)) {
+            codes_out[i] = 0;
+            if (levels_out) levels_out[i] = 0;
+            continue;
+        }
+        codes_out[i] = (l >= th_occ) ? 2 : (l <= th_free ? 1 : 0);
+        if (levels_out) {
+            int lv = 0;
+            for (int k = 0; k < PLEVELS; ++k) lv += (l >= phi[k]);
+            levels_out[i] = (uint8_t)lv;
+        }
+    }
 }
 
 int orc_version(void) { return 1; }
