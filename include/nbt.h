@@ -88,7 +88,8 @@ enum {
     NBT_KERNEL_IDW = 3,         /* k_idw_query: row a9 */
     NBT_KERNEL_SAMPLE = 4,      /* k_sample_perspectives: row a3 */
     NBT_KERNEL_MAP_UPDATE = 5,  /* k_delta_keys + radix sort + k_delta_apply: row a2 */
-    NBT_KERNEL_COUNT = 6
+    NBT_KERNEL_INTEGRATE = 6,   /* voxel filter + k_integrate_rays + k_integrate_apply: row f3 */
+    NBT_KERNEL_COUNT = 7
 };
 nbt_status nbt_ctx_set_profiling(nbt_ctx ctx, int enable);
 /* Sum of the recorded durations (ms) and number of launches of `kernel` since the last
@@ -164,6 +165,65 @@ nbt_status nbt_map_download_levels(nbt_map map, uint8_t *levels_out, size_t n);
 /* Copy of the descriptor. */
 nbt_status nbt_map_get_desc(nbt_map map, nbt_map_desc *out);
 void       nbt_map_destroy(nbt_map map);
+
+/* ------------------------------------------- map integration */
+
+/* The step before the ID: a depth frame is thinned by a voxel filter
+ * and integrated into a probabilistic occupancy store by log-odds hit / miss updates with
+ * free-space carving along the sensor rays (the paper defers the occupancy
+ * model to its mapping framework).  The store keeps float32 log-odds per voxel
+ * (NaN = never observed, reading Q36); every integration also writes the resulting
+ * state (and, for a nbt_map_create_prob map, the probability level) of each changed
+ * voxel into an ID map on the device and records those changes as a2 deltas. */
+typedef struct nbt_occ_s *nbt_occ;
+
+typedef struct {
+    double p_hit, p_miss;     /* hit / miss probabilities: 0.7, 0.4 */
+    double p_min, p_max;      /* clamp: 0.12, 0.97 */
+    double t_occ, t_free;     /* state thresholds: 0.5, 0.5 */
+    double max_range;         /* r_max, world units; a farther point is cut there and only
+                                 carves; <= 0 = unlimited; default 5.0 */
+    double leaf;              /* voxel-filter leaf, world units; 0 = no filter (Q33);
+                                 default = the map's voxel size */
+} nbt_integrate_params;
+
+/* Fill *p with the defaults above for a map of the given voxel size. */
+void nbt_integrate_params_default(nbt_integrate_params *p, double voxel_size);
+
+/* Occupancy store over desc's grid (nx*ny*nz < 2^32), every voxel never observed.
+ * Owns ~18 bytes of device memory per voxel (log-odds, flags, touched list, deltas). */
+nbt_status nbt_occ_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_occ *out);
+/* Replace / read all log-odds (dense x-fastest float32, NaN = never observed); n must be
+ * nx*ny*nz.  Upload is stream-ordered (host input is staged); download syncs. */
+nbt_status nbt_occ_upload(nbt_occ occ, const float *logodds, size_t n, int on_device);
+nbt_status nbt_occ_download(nbt_occ occ, float *logodds_out, size_t n);
+/* Integrate one cloud of n points (xyz float64, world units; host or device memory)
+ * seen from sensor[3] (host).  prm NULL = defaults.  Each (filtered) point gives the ray
+ * sensor -> point walked by the exact DDA of the ID (Q34); per call each in-grid voxel
+ * is updated once: by the hit if some ray ends in it, else by the miss if some ray
+ * visits it (Q35); L := clamp(L + delta) in float (Q36).  map (NULL allowed; same nx,
+ * ny, nz) receives the new state -- L >= logit(t_occ) Occupied, <= logit(t_free) Free,
+ * else Unknown -- and level round(63 P) (Q37) of every voxel whose (state, level)
+ * changed.  A non-finite point, a leaf cell index >= 2^20 or a Q12 overflow makes the
+ * whole call a no-op, reported as NBT_ERR_INVALID_ARG by the next nbt_ctx_sync or
+ * nbt_occ_stats (points are validated on the device).  n < 2^31.  Stream-ordered; host
+ * points are staged through pinned memory, no sync. */
+nbt_status nbt_occ_integrate(nbt_occ occ, nbt_map map, const double sensor[3], const double *points, int64_t n,
+                             int on_device, const nbt_integrate_params *prm);
+/* Counters of the last integrate (syncs): out[0] input points, out[1] rays after the
+ * filter, out[2] voxels updated, out[3] a2 deltas emitted. */
+nbt_status nbt_occ_stats(nbt_occ occ, int64_t out[4]);
+/* The a2 deltas of the last integrate, in unspecified order (syncs): voxel (ijk[3i],
+ * ijk[3i+1], ijk[3i+2]) now has state codes[i] and level levels[i] (0 if never
+ * observed).  Copies min(cap, count) entries; *n_out = count. */
+nbt_status nbt_occ_deltas(nbt_occ occ, int32_t *ijk, uint8_t *codes, uint8_t *levels, size_t cap, size_t *n_out);
+void       nbt_occ_destroy(nbt_occ occ);
+
+/* The voxel filter alone (Q33): one centroid per occupied leaf cell, cells in
+ * ascending (iz, iy, ix) order; out_xyz (3 n doubles) and out_count (n, may be NULL) are
+ * host buffers; *m_out = number of cells.  Syncs. */
+nbt_status nbt_voxel_filter(nbt_ctx ctx, const double *points, int64_t n, int on_device, double leaf,
+                            double *out_xyz, int32_t *out_count, int64_t *m_out);
 
 /* ------------------------------------------------------------ camera (row a5) */
 

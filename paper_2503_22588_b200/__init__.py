@@ -26,7 +26,8 @@ OK, ERR_INVALID_ARG, ERR_DEGENERATE, ERR_EMPTY, ERR_OUT_OF_MEMORY, ERR_CUDA, ERR
 UNKNOWN, FREE, OCCUPIED = 0, 1, 2
 OUTSIDE_UNKNOWN, OUTSIDE_CLIP = 0, 1
 SAMPLE_BALL, SAMPLE_SURFACE = 0, 1
-KERNEL_TRACE, KERNEL_FRAMES, KERNEL_FINALIZE, KERNEL_IDW, KERNEL_SAMPLE, KERNEL_MAP_UPDATE = range(6)
+(KERNEL_TRACE, KERNEL_FRAMES, KERNEL_FINALIZE, KERNEL_IDW, KERNEL_SAMPLE, KERNEL_MAP_UPDATE,
+ KERNEL_INTEGRATE) = range(7)
 
 # Every symbol include/nbt.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -41,6 +42,8 @@ EXPORTS = [
     "nbt_sample_perspectives", "nbt_id_compute", "nbt_id_compute_slice",
     "nbt_idbuf_create", "nbt_idbuf_push", "nbt_idbuf_clear", "nbt_idbuf_size", "nbt_ig_query", "nbt_idbuf_destroy",
     "nbt_info_cost",
+    "nbt_integrate_params_default", "nbt_occ_create", "nbt_occ_upload", "nbt_occ_download", "nbt_occ_integrate",
+    "nbt_occ_stats", "nbt_occ_deltas", "nbt_occ_destroy", "nbt_voxel_filter",
     "nbt_debug_trace", "nbt_debug_frames",
 ]
 
@@ -64,6 +67,11 @@ class Camera(C.Structure):
     @property
     def num_rays(self):
         return self.width * self.height + (4 if self.add_corners else 0)
+
+
+class IntegrateParams(C.Structure):
+    _fields_ = [("p_hit", C.c_double), ("p_miss", C.c_double), ("p_min", C.c_double), ("p_max", C.c_double),
+                ("t_occ", C.c_double), ("t_free", C.c_double), ("max_range", C.c_double), ("leaf", C.c_double)]
 
 
 class IgCloudC(C.Structure):
@@ -126,6 +134,15 @@ def lib():
         "nbt_idbuf_destroy": ([vp], None),
         "nbt_info_cost": ([vp, vp, vp, i32, i32, C.c_int, vp, dbl, dbl, dbl, dbl, dbl, i32, vp, vp, vp, C.c_int],
                           C.c_int),
+        "nbt_integrate_params_default": ([C.POINTER(IntegrateParams), dbl], None),
+        "nbt_occ_create": ([vp, C.POINTER(MapDesc), C.POINTER(vp)], C.c_int),
+        "nbt_occ_upload": ([vp, vp, sz, C.c_int], C.c_int),
+        "nbt_occ_download": ([vp, vp, sz], C.c_int),
+        "nbt_occ_integrate": ([vp, vp, vp, vp, i64, C.c_int, C.POINTER(IntegrateParams)], C.c_int),
+        "nbt_occ_stats": ([vp, C.POINTER(i64)], C.c_int),
+        "nbt_occ_deltas": ([vp, vp, vp, vp, sz, C.POINTER(sz)], C.c_int),
+        "nbt_occ_destroy": ([vp], None),
+        "nbt_voxel_filter": ([vp, vp, i64, C.c_int, dbl, vp, vp, C.POINTER(i64)], C.c_int),
         "nbt_debug_trace": ([vp, vp, vp, vp, i32, i32, vp, vp, vp, vp], C.c_int),
         "nbt_debug_frames": ([vp, vp, vp, vp, i32, C.POINTER(Camera), dbl, vp, vp], C.c_int),
     }
@@ -338,6 +355,90 @@ class Map:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+
+# ------------------------------------------------------- map integration (row f3)
+
+def integrate_params(voxel_size, **kw) -> IntegrateParams:
+    """nbt_integrate_params with the defaults of nbt_integrate_params_default, overridden by kw."""
+    prm = IntegrateParams()
+    lib().nbt_integrate_params_default(C.byref(prm), float(voxel_size))
+    for k, v in kw.items():
+        setattr(prm, k, float(v))
+    return prm
+
+
+class OccMap:
+    """nbt_occ: the float32 log-odds occupancy store that depth frames are integrated into."""
+
+    def __init__(self, ctx: Ctx, desc: MapDesc):
+        h = C.c_void_p()
+        check(lib().nbt_occ_create(ctx.h, C.byref(desc), C.byref(h)))
+        self.h, self.ctx, self.desc = h, ctx, desc
+
+    @property
+    def shape(self):
+        return (self.desc.nz, self.desc.ny, self.desc.nx)
+
+    @property
+    def nvox(self):
+        return self.desc.nx * self.desc.ny * self.desc.nz
+
+    def upload(self, logodds):
+        p, dev, keep = _ptr(logodds, np.float32)
+        check(lib().nbt_occ_upload(self.h, p, self.nvox, dev))
+
+    def download(self):
+        out = np.empty(self.shape, np.float32)
+        check(lib().nbt_occ_download(self.h, C.c_void_p(out.ctypes.data), self.nvox))
+        return out
+
+    def integrate(self, sensor, points, map: Map | None = None, params: IntegrateParams | None = None):
+        """Integrate one cloud ([n, 3] float64, host array or CUDA tensor); stream-ordered."""
+        ps, keep_s = _poi(sensor)
+        pp, dev, keep = _ptr(points, np.float64)
+        n = (keep.numel() // 3 if _is_torch(keep) else keep.size // 3) if keep is not None else 0
+        prm = params if params is not None else integrate_params(self.desc.voxel_size)
+        check(lib().nbt_occ_integrate(self.h, map.h if map is not None else None, ps, pp, n, dev, C.byref(prm)))
+
+    def stats(self):
+        """(points, rays after the filter, voxels updated, deltas) of the last integrate; syncs."""
+        out = (C.c_int64 * 4)()
+        check(lib().nbt_occ_stats(self.h, out))
+        return tuple(int(v) for v in out)
+
+    def deltas(self):
+        """(ijk [k, 3] int32, codes [k], levels [k]) of the last integrate, unspecified order."""
+        n = C.c_size_t()
+        check(lib().nbt_occ_deltas(self.h, None, None, None, 0, C.byref(n)))
+        k = n.value
+        ijk = np.zeros((max(k, 1), 3), np.int32); codes = np.zeros(max(k, 1), np.uint8)
+        levels = np.zeros(max(k, 1), np.uint8)
+        check(lib().nbt_occ_deltas(self.h, C.c_void_p(ijk.ctypes.data), C.c_void_p(codes.ctypes.data),
+                                   C.c_void_p(levels.ctypes.data), k, C.byref(n)))
+        return ijk[:k], codes[:k], levels[:k]
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().nbt_occ_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def voxel_filter(ctx: Ctx, points, leaf):
+    """(centroids [m, 3], counts [m]) of the device voxel filter (cells in (iz, iy, ix) order)."""
+    pp, dev, keep = _ptr(points, np.float64)
+    n = (keep.numel() // 3 if _is_torch(keep) else keep.size // 3) if keep is not None else 0
+    out = np.zeros((max(n, 1), 3)); cnt = np.zeros(max(n, 1), np.int32)
+    m = C.c_int64()
+    check(lib().nbt_voxel_filter(ctx.h, pp, n, dev, float(leaf), C.c_void_p(out.ctypes.data),
+                                 C.c_void_p(cnt.ctypes.data), C.byref(m)))
+    return out[:m.value].copy(), cnt[:m.value].copy()
 
 
 def camera_from_fov(fov_h, fov_v, w, h) -> Camera:

@@ -32,165 +32,21 @@
 #include <stdlib.h>
 
 #include "nbt_internal.cuh"
+#include "dda.cuh"
 
 namespace nbt {
 namespace {
+using namespace dda;
 
 constexpr int kFrameInts = 20;   // O, A, Rh, Uh, Rc, Uc (3 each, Q16), status, pad
 constexpr int kTotals = 5;       // per perspective: T_U, T_F, T_O, L, T_G (Eq. 2 gain, 1/63 units)
 constexpr int kWarpsPerBlock = 8;
-constexpr int kQShift = 12;      // walk coordinates: Q12
 // Trace kernel shape: K voxels per speculative batch; PIPE = the next batch's loads are
 // in flight while the current batch is consumed (look-ahead 2K, which must stay inside
 // the kBorder-voxel sentinel shell).  K = 16 without pipelining measured best
 // (profiles/r01_trace_variants.md); the other shapes stay compilable.
 constexpr int kBatchK = 16;
 constexpr int kInt32MaxVoxels = 700;   // |D_a| bound (voxels) for the int32 decision terms
-
-struct MapView {
-    const uint32_t *__restrict__ words;
-    int nx, ny, nz;
-    int px;          // linear layout: padded x extent
-    int pxy;         // linear layout: padded x*y extent
-    uint32_t mx, my, mz;   // Morton layout: bit masks of each axis (3 * pbits bits)
-    int policy;      // NBT_OUTSIDE_UNKNOWN / NBT_OUTSIDE_CLIP
-};
-
-template <int L>
-__device__ __forceinline__ uint32_t grid_index(const MapView &m, int x, int y, int z)
-{
-    if (L == kLayoutMorton)
-        return (dilate3((uint32_t)x) | (dilate3((uint32_t)y) << 1) | (dilate3((uint32_t)z) << 2)) &
-               (m.mx | m.my | m.mz);
-    return (uint32_t)(x + kBorder) + (uint32_t)m.px * (uint32_t)(y + kBorder) +
-           (uint32_t)m.pxy * (uint32_t)(z + kBorder);
-}
-
-__device__ __forceinline__ uint32_t code_of(uint32_t word, uint32_t idx)
-{
-    return __funnelshift_r(word, 0u, idx << 1) & 3u;   // shift amount taken mod 32
-}
-
-// Per-ray walk state.  T = int (rays <= 720 voxels per axis) or long long.
-template <typename T>
-struct Walk {
-    T qxy, qxz, qyz;           // sign decides the next axis (see header)
-    T ax, ay, az;              // |D_a| in Q12 units
-    T nax;                     // -|D_x| (hot path)
-    uint32_t idx;              // padded linear index of the current voxel (in-grid walk)
-    int dX, dY, ndZ;           // linear: idx increments of a step along x, y and (negated) z
-    uint32_t rx, ry, rz;       // Morton: per-axis dilated coordinates in "decrement form"
-    uint32_t xinv;             // Morton: bits to flip (axes walked in + direction)
-    int s, n;                  // current step (0 = origin voxel) and total steps
-    int s0;                    // step at which the walk entered the grid
-    uint32_t nf;               // Free voxels counted so far in the grid
-    uint32_t ng;               // 8-bit store: Eq. 2 gain counted so far (1/63 units)
-    uint32_t pre;              // visits outside the grid before entering it
-    int vx, vy, vz;            // voxel coordinates (entry path / debug only)
-    int sx, sy, sz;            // +-1 per axis
-};
-
-template <typename T>
-__device__ __forceinline__ void walk_setup(Walk<T> &w, const int o[3], const int e[3])
-{
-    long long ad[3], N[3];
-    int neg[3], v[3];
-    int n = 0;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        int D = e[a] - o[a];                     // |D| < 2^31: both ends inside (-2^30, 2^30)
-        neg[a] = D < 0;
-        ad[a] = neg[a] ? -(long long)D : (long long)D;
-        v[a] = o[a] >> kQShift;                  // floor
-        int ve = e[a] >> kQShift;
-        n += (ve > v[a]) ? ve - v[a] : v[a] - ve;
-        N[a] = neg[a] ? (long long)o[a] - ((long long)v[a] << kQShift)
-                      : (((long long)v[a] + 1) << kQShift) - o[a];          // in [0, 4096]
-    }
-    // tie favours the lower axis unless it moves negatively and the other positively
-    long long fxy = N[0] * ad[1] - N[1] * ad[0] - ((neg[0] && !neg[1]) ? 0 : 1);
-    long long fxz = N[0] * ad[2] - N[2] * ad[0] - ((neg[0] && !neg[2]) ? 0 : 1);
-    long long fyz = N[1] * ad[2] - N[2] * ad[1] - ((neg[1] && !neg[2]) ? 0 : 1);
-    w.qxy = (T)(fxy >> kQShift);                 // arithmetic shift = floor division by S
-    w.qxz = (T)(fxz >> kQShift);
-    w.qyz = (T)(fyz >> kQShift);
-    w.ax = (T)ad[0]; w.ay = (T)ad[1]; w.az = (T)ad[2];
-    w.nax = -w.ax;
-    w.sx = neg[0] ? -1 : 1;
-    w.sy = neg[1] ? -1 : 1;
-    w.sz = neg[2] ? -1 : 1;
-    w.vx = v[0]; w.vy = v[1]; w.vz = v[2];
-    w.s = 0;
-    w.n = n;
-    w.nf = 0;
-    w.ng = 0;
-    w.pre = 0;
-}
-
-__device__ __forceinline__ int mad_i32(int a, int b, int c)
-{
-    int d;
-    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-    return d;
-}
-
-// One DDA step: pick the axis, update the two decision terms that involve it, and move
-// the map address.  Linear layout: idx += step of the axis.  Morton layout: every axis
-// register holds its dilated coordinate so that a step is always a dilated DECREMENT
-// (axes walked in + direction are stored complemented within their bits), i.e.
-// r = (r - lsb) & mask, and the address is (rx | ry | rz) ^ xinv.
-template <typename T, int L, bool COORDS>
-__device__ __forceinline__ void walk_step(Walk<T> &w, const MapView &m)
-{
-    if constexpr (sizeof(T) == 4 && !COORDS) {
-        // Hot path: the axis choice as 0/1 and 0/-1 integers from the sign bits (5 ALU
-        // ops), the updates as multiply-adds on the FMA pipe, so the two integer
-        // pipes share the step instead of queueing on the ALU pipe (selects).
-        const int t1 = w.qxy & w.qxz;            // sign: x first
-        const int t2 = w.qyz & ~t1;              // sign: y first
-        const int px = (int)((unsigned)t1 >> 31);
-        const int py = (int)((unsigned)t2 >> 31);
-        const int npz = px + py - 1;             // -1 if z first, else 0
-        w.qxy = mad_i32(px, w.ay, mad_i32(py, w.nax, w.qxy));
-        w.qxz = mad_i32(px, w.az, mad_i32(npz, w.ax, w.qxz));
-        w.qyz = mad_i32(py, w.az, mad_i32(npz, w.ay, w.qyz));
-        if (L == kLayoutMorton) {
-            w.rx = (uint32_t)mad_i32(px, -1, (int)w.rx) & m.mx;
-            w.ry = (uint32_t)mad_i32(py, -2, (int)w.ry) & m.my;
-            w.rz = (uint32_t)mad_i32(npz, 4, (int)w.rz) & m.mz;
-            w.idx = (w.rx | w.ry | w.rz) ^ w.xinv;
-        } else {
-            w.idx = (uint32_t)mad_i32(px, w.dX, mad_i32(py, w.dY, mad_i32(npz, w.ndZ, (int)w.idx)));
-        }
-    } else {
-        const bool px = (w.qxy & w.qxz) < 0;     // both negative
-        const bool py = !px && w.qyz < 0;
-        const bool pz = !px && !py;
-        if (px) { w.qxy += w.ay; w.qxz += w.az; }
-        if (py) { w.qxy -= w.ax; w.qyz += w.az; }
-        if (pz) { w.qxz -= w.ax; w.qyz -= w.ay; }
-        if (L == kLayoutMorton) {
-            if (px) w.rx = (w.rx - 1u) & m.mx;
-            if (py) w.ry = (w.ry - 2u) & m.my;
-            if (pz) w.rz = (w.rz - 4u) & m.mz;
-            w.idx = (w.rx | w.ry | w.rz) ^ w.xinv;
-        } else {
-            if (px) w.idx += w.dX;
-            if (py) w.idx += w.dY;
-            if (pz) w.idx -= w.ndZ;
-        }
-        if (COORDS) {
-            if (px) w.vx += w.sx;
-            if (py) w.vy += w.sy;
-            if (pz) w.vz += w.sz;
-        }
-    }
-}
-
-__device__ __forceinline__ bool inside(const MapView &m, int x, int y, int z)
-{
-    return (unsigned)x < (unsigned)m.nx && (unsigned)y < (unsigned)m.ny && (unsigned)z < (unsigned)m.nz;
-}
 
 // Origin outside the grid (rare): step with explicit bounds checks until the walk
 // enters the grid or ends.  Returns true if the ray is finished.

@@ -726,6 +726,234 @@ void nbt_map_destroy(nbt_map m)
     ctx_release(ctx);
 }
 
+// ------------------------------------------------------- map integration (f3)
+
+void nbt_integrate_params_default(nbt_integrate_params *p, double voxel_size)
+{
+    if (!p) return;
+    p->p_hit = 0.7; p->p_miss = 0.4;
+    p->p_min = 0.12; p->p_max = 0.97;
+    p->t_occ = 0.5; p->t_free = 0.5;
+    p->max_range = 5.0;
+    p->leaf = voxel_size;
+}
+
+static void occ_free(nbt_occ_s *o)
+{
+    for (void *q : {(void *)o->d_L, (void *)o->d_flags, (void *)o->d_touched, (void *)o->d_didx, (void *)o->d_dval,
+                    (void *)o->d_ctl})
+        if (q) cudaFree(q);
+    for (DevBuf *b : {&o->pts, &o->keys, &o->keys_alt, &o->idx, &o->idx_alt, &o->runs, &o->filtered, &o->cub_tmp})
+        b->release();
+}
+
+nbt_status nbt_occ_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_occ *out)
+{
+    nbt_status s;
+    if (!out) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_create: null out");
+    *out = nullptr;
+    if ((s = bind(ctx))) return s;
+    if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_occ_create during graph capture");
+    if (!desc || desc->nx < 1 || desc->ny < 1 || desc->nz < 1 || !(desc->voxel_size > 0) ||
+        !isfinite(desc->voxel_size) || !isfinite(desc->origin[0]) || !isfinite(desc->origin[1]) ||
+        !isfinite(desc->origin[2]))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_occ_create: bad descriptor");
+    const uint64_t nvox = (uint64_t)desc->nx * desc->ny * desc->nz;
+    if (nvox >= (1ull << 32) - 4) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_create: grid too large (>= 2^32 voxels)");
+    auto *o = new nbt_occ_s;
+    o->ctx = ctx;
+    o->desc = *desc;
+    o->nvox = nvox;
+    const size_t nwords = (nvox + 3) / 4;
+    cudaError_t e = cudaMalloc(&o->d_L, nvox * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&o->d_flags, nwords * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&o->d_touched, nvox * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&o->d_didx, nvox * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&o->d_dval, nvox * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&o->d_ctl, kOccCtlInts * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(o->d_L, 0xff, nvox * 4, ctx->stream);   // 0xffffffff: a NaN
+    if (e == cudaSuccess) e = cudaMemsetAsync(o->d_flags, 0, nwords * 4, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(o->d_ctl, 0, kOccCtlInts * sizeof(int), ctx->stream);
+    if (e != cudaSuccess) {
+        occ_free(o);
+        delete o;
+        return e == cudaErrorMemoryAllocation ? fail(NBT_ERR_OUT_OF_MEMORY, "nbt_occ_create: out of device memory")
+                                              : cuda_fail(e, "nbt_occ_create");
+    }
+    ctx_retain(ctx);
+    *out = o;
+    return NBT_OK;
+}
+
+void nbt_occ_destroy(nbt_occ o)
+{
+    if (!o) return;
+    cudaSetDevice(o->ctx->device);
+    cudaStreamSynchronize(o->ctx->stream);
+    occ_free(o);
+    nbt_ctx ctx = o->ctx;
+    delete o;
+    ctx_release(ctx);
+}
+
+nbt_status nbt_occ_upload(nbt_occ o, const float *logodds, size_t n, int on_device)
+{
+    if (!o || !logodds) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_upload: null argument");
+    if (n != o->nvox) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_upload: n must be nx*ny*nz");
+    nbt_ctx ctx = o->ctx;
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (ctx->capturing && !on_device) return fail(NBT_ERR_STATE, "nbt_occ_upload: host input during graph capture");
+    if (on_device) {
+        NBT_CUDA(cudaMemcpyAsync(o->d_L, logodds, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        return NBT_OK;
+    }
+    NBT_CUDA(cudaMemcpyAsync(o->d_L, logodds, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    NBT_CUDA(cudaStreamSynchronize(ctx->stream));   // pageable source: keep it alive until copied
+    return NBT_OK;
+}
+
+nbt_status nbt_occ_download(nbt_occ o, float *out, size_t n)
+{
+    if (!o || !out) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_download: null argument");
+    if (n != o->nvox) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_download: n must be nx*ny*nz");
+    nbt_ctx ctx = o->ctx;
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_occ_download during graph capture");
+    NBT_CUDA(cudaMemcpyAsync(out, o->d_L, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return NBT_OK;
+}
+
+static nbt_status check_integrate_params(const nbt_integrate_params &p)
+{
+    auto prob = [](double v) { return v > 0.0 && v < 1.0; };
+    if (!prob(p.p_hit) || !prob(p.p_miss) || !prob(p.p_min) || !prob(p.p_max) || !(p.p_min <= p.p_max) ||
+        !prob(p.t_occ) || !prob(p.t_free) || isnan(p.max_range) || !(p.leaf >= 0.0) || !isfinite(p.leaf))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_integrate_params: probabilities must lie in (0,1), p_min <= p_max, "
+                                         "leaf >= 0 finite");
+    return NBT_OK;
+}
+
+nbt_status nbt_occ_integrate(nbt_occ o, nbt_map map, const double sensor[3], const double *points, int64_t n,
+                             int on_device, const nbt_integrate_params *prm)
+{
+    if (!o || !sensor) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_integrate: null argument");
+    nbt_ctx ctx = o->ctx;
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (n < 0 || n >= (1ll << 31)) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_integrate: n out of range");
+    if (n > 0 && !points) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_integrate: null points");
+    if (!isfinite(sensor[0]) || !isfinite(sensor[1]) || !isfinite(sensor[2]))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_occ_integrate: non-finite sensor origin");
+    if (map && (map->ctx != ctx || map->desc.nx != o->desc.nx || map->desc.ny != o->desc.ny ||
+                map->desc.nz != o->desc.nz))
+        return fail(NBT_ERR_STATE, "nbt_occ_integrate: map of another ctx or grid");
+    nbt_integrate_params p;
+    if (prm) p = *prm;
+    else nbt_integrate_params_default(&p, o->desc.voxel_size);
+    if ((s = check_integrate_params(p))) return s;
+    if (ctx->capturing && !on_device && n > 0)
+        return fail(NBT_ERR_STATE, "nbt_occ_integrate: host points during graph capture");
+    const double *dpts = points;
+    if (!on_device && n > 0) {
+        if ((s = stage_h2d(ctx, ctx->stage_in[0], o->pts, points, (size_t)n * 24))) return s;
+        dpts = o->pts.as<double>();
+    }
+    return launch_integrate(ctx, o, map, sensor, dpts, (uint32_t)n, p);
+}
+
+nbt_status nbt_occ_stats(nbt_occ o, int64_t out[4])
+{
+    if (!o || !out) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_stats: null argument");
+    nbt_ctx ctx = o->ctx;
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_occ_stats during graph capture");
+    int ctl[kOccCtlInts];
+    if ((s = d2h_sync(ctx, ctl, o->d_ctl, sizeof ctl))) return s;
+    if ((s = take_device_error(ctx, "nbt_occ_integrate"))) return s;
+    out[0] = o->last_points;
+    out[1] = o->last_filtered ? (int64_t)(uint32_t)ctl[kOccRays] : (int64_t)o->last_points;
+    out[2] = (uint32_t)ctl[kOccTouched];
+    out[3] = (uint32_t)ctl[kOccDeltas];
+    return NBT_OK;
+}
+
+nbt_status nbt_occ_deltas(nbt_occ o, int32_t *ijk, uint8_t *codes, uint8_t *levels, size_t cap, size_t *n_out)
+{
+    if (!o || !n_out || (cap > 0 && (!ijk || !codes || !levels)))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_occ_deltas: null argument");
+    nbt_ctx ctx = o->ctx;
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_occ_deltas during graph capture");
+    int ctl[kOccCtlInts];
+    if ((s = d2h_sync(ctx, ctl, o->d_ctl, sizeof ctl))) return s;
+    const size_t cnt = (uint32_t)ctl[kOccDeltas];
+    *n_out = cnt;
+    const size_t k = cnt < cap ? cnt : cap;
+    if (k == 0) return NBT_OK;
+    std::vector<uint32_t> idx(k);
+    std::vector<uint16_t> val(k);
+    NBT_CUDA(cudaMemcpyAsync(idx.data(), o->d_didx, k * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaMemcpyAsync(val.data(), o->d_dval, k * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    NBT_CUDA(cudaStreamSynchronize(ctx->stream));
+    const uint32_t nx = (uint32_t)o->desc.nx, ny = (uint32_t)o->desc.ny;
+    for (size_t i = 0; i < k; ++i) {
+        const uint32_t v = idx[i];
+        ijk[3 * i] = (int32_t)(v % nx);
+        ijk[3 * i + 1] = (int32_t)((v / nx) % ny);
+        ijk[3 * i + 2] = (int32_t)(v / nx / ny);
+        codes[i] = (uint8_t)(val[i] & 0xff);
+        levels[i] = (uint8_t)(val[i] >> 8);
+    }
+    return NBT_OK;
+}
+
+nbt_status nbt_voxel_filter(nbt_ctx ctx, const double *points, int64_t n, int on_device, double leaf,
+                            double *out_xyz, int32_t *out_count, int64_t *m_out)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (!m_out || n < 0 || n >= (1ll << 31) || (n > 0 && (!points || !out_xyz)) || !(leaf > 0) ||
+        !isfinite(leaf))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_voxel_filter: bad argument");
+    if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_voxel_filter during graph capture");
+    *m_out = 0;
+    if (n == 0) return NBT_OK;
+    nbt_occ_s tmp;
+    tmp.ctx = ctx;
+    DevBuf ctl, cnt;
+    if ((s = ctl.ensure(kOccCtlInts * sizeof(int))) || (s = cnt.ensure((size_t)n * 4))) return s;
+    tmp.d_ctl = ctl.as<int>();
+    NBT_CUDA(cudaMemsetAsync(tmp.d_ctl, 0, kOccCtlInts * sizeof(int), ctx->stream));
+    const double *dpts = points;
+    if (!on_device) {
+        if ((s = stage_h2d(ctx, ctx->stage_in[0], tmp.pts, points, (size_t)n * 24))) return s;
+        dpts = tmp.pts.as<double>();
+    }
+    s = launch_voxel_filter(ctx, &tmp, dpts, (uint32_t)n, leaf, cnt.as<int32_t>());
+    int c[kOccCtlInts] = {0};
+    if (s == NBT_OK) s = d2h_sync(ctx, c, tmp.d_ctl, sizeof c);
+    if (s == NBT_OK) s = take_device_error(ctx, "nbt_voxel_filter");
+    if (s == NBT_OK) {
+        const size_t m = (uint32_t)c[kOccRays];
+        cudaError_t e = cudaMemcpyAsync(out_xyz, tmp.filtered.p, m * 24, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess && out_count)
+            e = cudaMemcpyAsync(out_count, cnt.p, m * 4, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) s = cuda_fail(e, "nbt_voxel_filter");
+        *m_out = (int64_t)m;
+    }
+    cudaStreamSynchronize(ctx->stream);
+    for (DevBuf *b : {&ctl, &cnt, &tmp.pts, &tmp.keys, &tmp.keys_alt, &tmp.idx, &tmp.idx_alt, &tmp.runs,
+                      &tmp.filtered, &tmp.cub_tmp})
+        b->release();
+    return s;
+}
+
 // ------------------------------------------------------------------ camera
 
 nbt_status nbt_camera_from_fov(double fov_h, double fov_v, int32_t w, int32_t h, nbt_camera *out)

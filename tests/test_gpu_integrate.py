@@ -1,0 +1,221 @@
+"""Map integration on the device vs the CPU oracle, on the same seeded
+depth frames: the voxel filter's centroids and counts, the float32 log-odds store, the ID map
+states and probability levels, and the emitted a2 deltas must all be bit-exact (every step
+is integer, or IEEE operations in the same order on both sides: readings Q33-Q37)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import nbt_inputs as I
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nbt():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    from paper_2503_22588_b200 import _build
+    _build.build()
+    import paper_2503_22588_b200 as mod
+    return mod
+
+
+@pytest.fixture(scope="module")
+def ctx(nbt):
+    return nbt.Ctx(0)
+
+
+def same_logodds(a, b):
+    """Bit-exact, except that every NaN (never observed) matches every NaN."""
+    na, nb = np.isnan(a), np.isnan(b)
+    return np.array_equal(na, nb) and np.array_equal(a[~na].view(np.uint32), b[~nb].view(np.uint32))
+
+
+def oracle_deltas(L0, L1, touched):
+    """The (voxel -> (state, level)) changes the oracle's before/after stores imply."""
+    c0, l0 = oracle.occ_classify(L0)
+    c1, l1 = oracle.occ_classify(L1)
+    ch = (touched > 0) & ((c0 != c1) | (l0 != l1))
+    zyx = np.argwhere(ch)
+    return {(int(x), int(y), int(z)): (int(c1[z, y, x]), int(l1[z, y, x])) for z, y, x in zyx}
+
+
+def device_deltas(occ):
+    ijk, codes, levels = occ.deltas()
+    d = {}
+    for (x, y, z), c, lv in zip(ijk.tolist(), codes.tolist(), levels.tolist()):
+        assert (x, y, z) not in d, "a voxel appears twice in one cloud's deltas"
+        d[(x, y, z)] = (c, lv)
+    return d
+
+
+def map_levels_expected(codes, levels):
+    """download_levels reports 0 for Unknown voxels."""
+    return np.where(codes == 0, 0, levels).astype(np.uint8)
+
+
+@pytest.mark.parametrize("name", ["F0", "F"])
+def test_voxel_filter_matches_oracle(nbt, ctx, name):
+    cf = I.CLOUD_CONFIGS[name]
+    pts = cf.cloud(1)
+    want, wcnt = oracle.voxel_filter(pts, cf.leaf)
+    got, gcnt = nbt.voxel_filter(ctx, pts, cf.leaf)
+    assert got.shape == want.shape
+    assert np.array_equal(gcnt, wcnt)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 1000, 65537])
+def test_voxel_filter_ragged_and_negative(nbt, ctx, n):
+    rng = np.random.default_rng(n)
+    pts = rng.normal(0.0, 0.3, (n, 3))
+    pts[: n // 3] = np.round(pts[: n // 3] * 40) / 40          # points on cell faces
+    want, wcnt = oracle.voxel_filter(pts, 0.025)
+    got, gcnt = nbt.voxel_filter(ctx, pts, 0.025)
+    assert np.array_equal(gcnt, wcnt) and np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_voxel_filter_device_input_and_errors(nbt, ctx):
+    import torch
+    pts = I.CLOUD_CONFIGS["F0"].cloud(0)
+    want, wcnt = oracle.voxel_filter(pts, 0.04)
+    got, gcnt = nbt.voxel_filter(ctx, torch.from_numpy(pts).cuda(), 0.04)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64)) and np.array_equal(gcnt, wcnt)
+    e, c = nbt.voxel_filter(ctx, np.zeros((0, 3)), 0.1)
+    assert e.shape == (0, 3)
+    bad = pts.copy()
+    bad[5, 1] = np.nan
+    with pytest.raises(nbt.NbtError):
+        nbt.voxel_filter(ctx, bad, 0.04)
+    with pytest.raises(nbt.NbtError):
+        nbt.voxel_filter(ctx, np.array([[1e9, 0.0, 0.0]]), 1e-3)   # cell index >= 2^20
+
+
+def _run_sequence(nbt, ctx, cf, n_clouds, prob, layout, monkeypatch, params=None, L_start=None):
+    monkeypatch.setenv("NBT_MAP_LAYOUT", layout)
+    n = cf.n
+    desc = nbt.map_desc(n, n, n, cf.voxel_size)
+    occ = nbt.OccMap(ctx, desc)
+    m = nbt.Map(ctx, desc, prob=prob)
+    L = oracle.new_logodds((n, n, n))
+    kw = dict(leaf=cf.leaf, max_range=cf.max_range)
+    if params:
+        kw.update(params)
+    if L_start is not None:
+        assert not prob
+        L[...] = L_start
+        occ.upload(L_start)
+        c0, _ = oracle.occ_classify(L)
+        m.upload(c0)                     # the ID map starts consistent with the store
+    prm = nbt.integrate_params(cf.voxel_size, **kw)
+    for k in range(n_clouds):
+        pts = cf.cloud(k)
+        L_before = L.copy()
+        touched, nr = oracle.integrate(L, cf.voxel_size, (0, 0, 0), cf.sensor(k), pts, **kw)
+        occ.integrate(cf.sensor(k), pts, map=m, params=prm)
+        st = occ.stats()
+        assert st[0] == len(pts) and st[1] == nr
+        assert st[2] == int((touched > 0).sum())
+        assert same_logodds(occ.download(), L), f"cloud {k}: log-odds differ"
+        want = oracle_deltas(L_before, L, touched)
+        got = device_deltas(occ)
+        assert st[3] == len(got)
+        assert got == want, f"cloud {k}: deltas differ"
+    codes, levels = oracle.occ_classify(L)
+    assert np.array_equal(m.download(), codes)
+    if prob:
+        assert np.array_equal(m.download_levels(), map_levels_expected(codes, levels))
+    return occ, m, L
+
+
+@pytest.mark.parametrize("prob", [False, True])
+@pytest.mark.parametrize("layout", ["linear", "morton"])
+def test_integrate_sequence_small(nbt, ctx, prob, layout, monkeypatch):
+    cf = I.CLOUD_CONFIGS["F0"]
+    _run_sequence(nbt, ctx, cf, cf.n_clouds, prob, layout, monkeypatch)
+
+
+@pytest.mark.parametrize("prob", [False, True])
+def test_integrate_sequence_full_size(nbt, ctx, prob, monkeypatch):
+    """Config F: 256^3 at 1 cm, 640x576 Azure-Kinect-size frames, 3 poses."""
+    cf = I.CLOUD_CONFIGS["F"]
+    _run_sequence(nbt, ctx, cf, 3, prob, "linear", monkeypatch)
+
+
+def test_integrate_without_filter_and_unlimited_range(nbt, ctx, monkeypatch):
+    """leaf = 0 (every point is a ray) and max_range <= 0 (the 64-bit DDA variant)."""
+    cf = I.CLOUD_CONFIGS["F0"]
+    _run_sequence(nbt, ctx, cf, 2, True, "linear", monkeypatch, params=dict(leaf=0.0, max_range=0.0))
+
+
+def test_integrate_from_observed_start_hits_clamps(nbt, ctx, monkeypatch):
+    """Start from a store with random observed log-odds near the clamps and thresholds."""
+    cf = I.CLOUD_CONFIGS["F0"]
+    rng = np.random.default_rng(8)
+    L0 = rng.choice(np.array([np.nan, 0.0, -0.4054651, 3.4, -1.9, 0.5, -1e-7, 1e-7], np.float32),
+                    size=(cf.n,) * 3).astype(np.float32)
+    _run_sequence(nbt, ctx, cf, 2, False, "linear", monkeypatch, L_start=L0)
+
+
+def test_integrate_sensor_and_points_outside_grid(nbt, ctx, monkeypatch):
+    """A sensor outside the grid, points on both sides: only in-grid voxels change."""
+    cf = I.CloudConfig("Fo", 40, 0.05, 3.0, 96, 80, 1.6, 2, 0.05, 3.0, 5)
+    _run_sequence(nbt, ctx, cf, 2, True, "linear", monkeypatch)
+
+
+def test_integrate_zero_points_and_bad_cloud(nbt, ctx):
+    cf = I.CLOUD_CONFIGS["F0"]
+    desc = nbt.map_desc(cf.n, cf.n, cf.n, cf.voxel_size)
+    occ = nbt.OccMap(ctx, desc)
+    m = nbt.Map(ctx, desc)
+    occ.integrate(cf.sensor(0), np.zeros((0, 3)), map=m)
+    assert occ.stats() == (0, 0, 0, 0)
+    assert np.isnan(occ.download()).all()
+    pts = cf.cloud(0)
+    occ.integrate(cf.sensor(0), pts, map=m, params=nbt.integrate_params(cf.voxel_size, leaf=cf.leaf))
+    before = occ.download()
+    codes_before = m.download()
+    bad = pts.copy()
+    bad[100] = [np.inf, 0.0, 0.0]
+    occ.integrate(cf.sensor(1), bad, map=m)
+    with pytest.raises(nbt.NbtError):
+        occ.stats()
+    assert same_logodds(occ.download(), before) and np.array_equal(m.download(), codes_before)
+    # the flags were cleared: the next good cloud matches the oracle
+    L = before.copy()
+    oracle.integrate(L, cf.voxel_size, (0, 0, 0), cf.sensor(1), pts, leaf=cf.voxel_size, max_range=5.0)
+    occ.integrate(cf.sensor(1), pts, map=m)
+    occ.stats()
+    assert same_logodds(occ.download(), L)
+
+
+def test_integrate_device_points_and_id_after(nbt, ctx):
+    """Device-resident frames; the integrated map then feeds the ID (the f3 -> a7 chain),
+    whose result equals the oracle's ID on the oracle-integrated map."""
+    import torch
+    cf = I.CLOUD_CONFIGS["F0"]
+    desc = nbt.map_desc(cf.n, cf.n, cf.n, cf.voxel_size)
+    occ = nbt.OccMap(ctx, desc)
+    m = nbt.Map(ctx, desc)
+    L = oracle.new_logodds((cf.n,) * 3)
+    for k in range(cf.n_clouds):
+        pts = cf.cloud(k)
+        oracle.integrate(L, cf.voxel_size, (0, 0, 0), cf.sensor(k), pts, leaf=cf.leaf, max_range=cf.max_range)
+        occ.integrate(cf.sensor(k), torch.from_numpy(pts).cuda(), map=m,
+                      params=nbt.integrate_params(cf.voxel_size, leaf=cf.leaf, max_range=cf.max_range))
+    ctx.sync()
+    codes, _ = oracle.occ_classify(L)
+    assert np.array_equal(m.download(), codes)
+    om = oracle.OracleMap(codes, voxel_size=cf.voxel_size)
+    poi = cf.poi
+    persp = oracle.sample_perspectives(poi, 0.5, 24, 3, 1)
+    cam = nbt.camera_from_fov(I.FOV_H, I.FOV_V, 16, 12)
+    cloud = nbt.id_compute(ctx, m, poi, persp, cam, 1.0)
+    ocam = oracle.camera_from_fov(I.FOV_H, I.FOV_V, 16, 12)
+    xyz, g, c = oracle.id_compute(om, poi, persp, ocam, 1.0)
+    assert np.array_equal(cloud.counts.astype(np.int64), c)
+    assert np.array_equal(cloud.gain, g)
