@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-north-star", action="store_true")
+    ap.add_argument("--no-integrate", action="store_true", help="skip the row-f3 map-integration block")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     return ap.parse_args()
@@ -212,6 +213,69 @@ def reference_arm(args, cfg):
 
 
 # -------------------------------------------------------------- our arm
+
+def run_integration(nbt, ctx, stream, dev, flush, reps=2):
+    """Row f3 on config F: Azure-Kinect-size depth frames (640 x 576, ~365 k
+    points) from 8 poses integrated into an empty 256^3 / 1 cm store and a 2-bit ID map:
+    voxel filter + log-odds rays + apply, device time per frame with the points resident
+    (L2 flushed before every frame), then end to end from host numpy points (staging +
+    H2D + kernels + the D2H of the frame's counters)."""
+    import torch
+    from nbt_inputs import CLOUD_CONFIGS
+    cf = CLOUD_CONFIGS["F"]
+    clouds = [cf.cloud(k) for k in range(cf.n_clouds)]
+    d_clouds = [torch.from_numpy(c).to(dev) for c in clouds]
+    desc = nbt.map_desc(cf.n, cf.n, cf.n, cf.voxel_size)
+    occ = nbt.OccMap(ctx, desc)
+    mi = nbt.Map(ctx, desc)
+    prm = nbt.integrate_params(cf.voxel_size, leaf=cf.leaf, max_range=cf.max_range)
+    empty_L = torch.full((cf.n,) * 3, float("nan"), dtype=torch.float32, device=dev)
+    empty_codes = torch.zeros((cf.n,) * 3, dtype=torch.uint8, device=dev)
+
+    def reset():
+        occ.upload(empty_L)
+        mi.upload(empty_codes)
+
+    for k in range(cf.n_clouds):                    # warm-up: scratch buffers grow once
+        occ.integrate(cf.sensor(k), d_clouds[k], map=mi, params=prm)
+    ctx.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times, st = [], []
+    for _ in range(reps):
+        reset()
+        for k in range(cf.n_clouds):
+            flush.fill_(k & 0xFF)
+            e0.record(stream)
+            occ.integrate(cf.sensor(k), d_clouds[k], map=mi, params=prm)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            st.append(occ.stats())
+    e2e = []
+    for _ in range(reps):
+        reset()
+        ctx.sync()
+        for k in range(cf.n_clouds):
+            t0 = time.perf_counter()
+            occ.integrate(cf.sensor(k), clouds[k], map=mi, params=prm)
+            occ.stats()                                 # D2H of the counters (syncs)
+            e2e.append(1e3 * (time.perf_counter() - t0))
+    pts = sum(s[0] for s in st)
+    rays = sum(s[1] for s in st)
+    upd = sum(s[2] for s in st)
+    tot = sum(times) / 1e3
+    out = {"config": f"F: {cf.n}^3 / {cf.voxel_size * 100:g} cm store, {cf.width}x{cf.height} frames from "
+                     f"{cf.n_clouds} poses, leaf {cf.leaf * 100:g} cm, r_max {cf.max_range:g} m",
+           "frames": len(times), "ms_per_frame": statistics.mean(times), "ms_per_frame_p50": statistics.median(times),
+           "points_per_s": pts / tot, "rays_per_s": rays / tot, "voxel_updates_per_s": upd / tot,
+           "mean_points": pts / len(st), "mean_rays": rays / len(st), "mean_voxels_updated": upd / len(st),
+           "mean_deltas": sum(s[3] for s in st) / len(st),
+           "e2e_ms_per_frame": statistics.mean(e2e), "e2e_h2d_bytes_per_frame": int(24 * pts / len(st)),
+           "l2": "flushed before every frame"}
+    occ.close()
+    mi.close()
+    return out
+
 
 def main_ours(args, cfg):
     import torch
@@ -401,6 +465,11 @@ def main_ours(args, cfg):
                  "id_latency_ms": ms, "rays_per_s": cn.rays_per_id / (ms / 1e3), "target_ms": 100.0,
                  "steps": len(times)}
 
+    # ---- row f3: map integration of depth frames (the step before the path)
+    integ = None
+    if cfg.name == "B" and not args.no_integrate and rank == 0:
+        integ = run_integration(nbt, ctx, stream, dev, flush)
+
     # ---- end to end through the public API with HOST buffers (H2D inputs, D2H results)
     e2e = None
     if not args.no_e2e:
@@ -501,6 +570,7 @@ def main_ours(args, cfg):
                                        f"{f_max / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)"},
             "kernel_share_of_step": shares,
             "north_star": north,
+            "map_integration": integ,
             "gpu_launches": launches,
             "clocks": clocks_out,
             "e2e": e2e,

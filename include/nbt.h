@@ -190,8 +190,8 @@ typedef struct {
 /* Fill *p with the defaults above for a map of the given voxel size. */
 void nbt_integrate_params_default(nbt_integrate_params *p, double voxel_size);
 
-/* Occupancy store over desc's grid (nx*ny*nz < 2^32), every voxel never observed.
- * Owns ~18 bytes of device memory per voxel (log-odds, flags, touched list, deltas). */
+/* Occupancy store over desc's grid (nx*ny*nz < 2^31), every voxel never observed.
+ * Owns ~15 bytes of device memory per voxel (log-odds, flag byte, voxel and delta lists). */
 nbt_status nbt_occ_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_occ *out);
 /* Replace / read all log-odds (dense x-fastest float32, NaN = never observed); n must be
  * nx*ny*nz.  Upload is stream-ordered (host input is staged); download syncs. */

@@ -182,15 +182,15 @@ struct nbt_occ_s {
     nbt_map_desc desc{};
     size_t nvox = 0;
     float *d_L = nullptr;             // log-odds, dense x-fastest, NaN = never observed (Q36)
-    uint32_t *d_flags = nullptr;      // one flag byte per voxel (4 per word), zero between calls
-    uint32_t *d_touched = nullptr;    // voxels flagged by the current cloud (capacity nvox)
+    uint32_t *d_flags = nullptr;      // one flag byte per voxel (16-byte padded), zero between calls
+    uint32_t *d_list = nullptr;       // flagged voxels of the current cloud (bit 31: hit)
     uint32_t *d_didx = nullptr;       // a2 deltas of the last cloud: dense voxel index ...
     uint16_t *d_dval = nullptr;       // ... and state | level << 8
     int *d_ctl = nullptr;             // per-call control words (kOcc*)
     uint32_t last_points = 0;         // host mirror of the last call's input size
     bool last_filtered = false;
     nbt::DevBuf pts;                  // staged host points
-    nbt::DevBuf keys, keys_alt, idx, idx_alt, runs, filtered, cub_tmp;
+    nbt::DevBuf keys, keys_alt, idx, idx_alt, runs, sorted, filtered, cub_tmp;
 };
 
 // ------------------------------------------------------------- kernel API
@@ -246,7 +246,7 @@ nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const InfoCostArg
                             double zero_eps, int32_t normalize);
 
 // Map integration (k_integrate.cu).  d_ctl words of an occupancy store:
-enum : int { kOccBad = 0, kOccRays = 1, kOccTouched = 2, kOccDeltas = 3, kOccCtlInts = 4 };
+enum : int { kOccBad = 0, kOccRays = 1, kOccTouched = 2, kOccDeltas = 3, kOccValid = 4, kOccCtlInts = 8 };
 nbt_status launch_voxel_filter(nbt_ctx ctx, nbt_occ_s *o, const double *d_pts, uint32_t n, double leaf,
                                int32_t *d_count_out);
 nbt_status launch_integrate(nbt_ctx ctx, nbt_occ_s *o, nbt_map m, const double sensor[3], const double *d_pts,

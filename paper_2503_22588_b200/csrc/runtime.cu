@@ -740,10 +740,11 @@ void nbt_integrate_params_default(nbt_integrate_params *p, double voxel_size)
 
 static void occ_free(nbt_occ_s *o)
 {
-    for (void *q : {(void *)o->d_L, (void *)o->d_flags, (void *)o->d_touched, (void *)o->d_didx, (void *)o->d_dval,
+    for (void *q : {(void *)o->d_L, (void *)o->d_flags, (void *)o->d_list, (void *)o->d_didx, (void *)o->d_dval,
                     (void *)o->d_ctl})
         if (q) cudaFree(q);
-    for (DevBuf *b : {&o->pts, &o->keys, &o->keys_alt, &o->idx, &o->idx_alt, &o->runs, &o->filtered, &o->cub_tmp})
+    for (DevBuf *b : {&o->pts, &o->keys, &o->keys_alt, &o->idx, &o->idx_alt, &o->runs, &o->sorted, &o->filtered,
+                      &o->cub_tmp})
         b->release();
 }
 
@@ -759,15 +760,15 @@ nbt_status nbt_occ_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_occ *out)
         !isfinite(desc->origin[2]))
         return fail(NBT_ERR_INVALID_ARG, "nbt_occ_create: bad descriptor");
     const uint64_t nvox = (uint64_t)desc->nx * desc->ny * desc->nz;
-    if (nvox >= (1ull << 32) - 4) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_create: grid too large (>= 2^32 voxels)");
+    if (nvox >= (1ull << 31)) return fail(NBT_ERR_INVALID_ARG, "nbt_occ_create: grid too large (>= 2^31 voxels)");
     auto *o = new nbt_occ_s;
     o->ctx = ctx;
     o->desc = *desc;
     o->nvox = nvox;
-    const size_t nwords = (nvox + 3) / 4;
+    const size_t nwords = (nvox + 15) / 16 * 4;       // flag bytes, padded to 16-byte groups
     cudaError_t e = cudaMalloc(&o->d_L, nvox * 4);
     if (e == cudaSuccess) e = cudaMalloc(&o->d_flags, nwords * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&o->d_touched, nvox * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&o->d_list, nvox * 4);
     if (e == cudaSuccess) e = cudaMalloc(&o->d_didx, nvox * 4);
     if (e == cudaSuccess) e = cudaMalloc(&o->d_dval, nvox * 2);
     if (e == cudaSuccess) e = cudaMalloc(&o->d_ctl, kOccCtlInts * sizeof(int));
@@ -949,7 +950,7 @@ nbt_status nbt_voxel_filter(nbt_ctx ctx, const double *points, int64_t n, int on
     }
     cudaStreamSynchronize(ctx->stream);
     for (DevBuf *b : {&ctl, &cnt, &tmp.pts, &tmp.keys, &tmp.keys_alt, &tmp.idx, &tmp.idx_alt, &tmp.runs,
-                      &tmp.filtered, &tmp.cub_tmp})
+                      &tmp.sorted, &tmp.filtered, &tmp.cub_tmp})
         b->release();
     return s;
 }

@@ -219,3 +219,25 @@ def test_integrate_device_points_and_id_after(nbt, ctx):
     xyz, g, c = oracle.id_compute(om, poi, persp, ocam, 1.0)
     assert np.array_equal(cloud.counts.astype(np.int64), c)
     assert np.array_equal(cloud.gain, g)
+
+
+def test_integrate_exact_ties_and_long_rays(nbt, ctx, monkeypatch):
+    """Rays whose ends sit on voxel faces, edges and corners (exact ties in the DDA) and long
+    rays cut into many pieces: sensor on a voxel corner, points on the Q12 lattice, no
+    filter, unlimited range (64-bit walk) and a 3-voxel range (int32 walk)."""
+    n = 48
+    rng = np.random.default_rng(12)
+    sensor = np.array([20.0, 17.0, 23.0])
+    pts = np.concatenate([
+        rng.integers(-30, n + 30, (3000, 3)).astype(np.float64),                    # corners
+        rng.integers(-30, n + 30, (3000, 3)) + rng.integers(0, 2, (3000, 3)) * 0.5,  # faces / edges
+        sensor + rng.normal(0, 1, (500, 3)) * np.array([1.0, 0.0, 0.0]),          # axis-parallel
+        rng.uniform(-40, n + 40, (3000, 3))])
+    for mr in (0.0, 3.0, 30.0):
+        L = oracle.new_logodds((n, n, n))
+        touched, _ = oracle.integrate(L, 1.0, (0, 0, 0), sensor, pts, leaf=0.0, max_range=mr)
+        desc = nbt.map_desc(n, n, n, 1.0)
+        occ = nbt.OccMap(ctx, desc)
+        occ.integrate(sensor, pts, params=nbt.integrate_params(1.0, leaf=0.0, max_range=mr))
+        assert occ.stats()[2] == int((touched > 0).sum())
+        assert same_logodds(occ.download(), L), f"max_range {mr}"
