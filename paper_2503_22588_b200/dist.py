@@ -8,6 +8,8 @@ exchange, both real data movement of the method:
   broadcast once from the rank that built it, and each cycle's map deltas (KB-scale)
   are broadcast so every replica applies the same update (the single-writer rule,
   S:97-98, holds per replica by stream order);
+* depth frames (row f3) -- the sensor rank broadcasts each frame's points and every
+  replica integrates it (deterministic, so the maps stay identical);
 * the IG point cloud -- each rank computes a strided slice of the perspective set
   (perspective j -> rank j mod G, so cheap in-object and expensive open-space
   perspectives spread evenly), and one all-gather assembles the cloud in input order on
@@ -111,6 +113,36 @@ def broadcast_deltas(ijk, codes, src: int = 0, group=None):
     import torch.distributed as dist
     dist.broadcast(ijk, src=src, group=group)
     dist.broadcast(codes, src=src, group=group)
+
+
+def broadcast_frame(points, sensor, src: int = 0, device=None, group=None):
+    """Broadcast one depth frame (row f3) from the sensor rank: (sensor float64[3], points
+    float64 [n, 3] tensor on `device`) on every rank.  Other ranks pass points=None.  Every
+    replica then integrates the same frame; the integration is deterministic (per-cloud set
+    update, Q35), so the replicated maps stay bit-identical without a delta exchange."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    head = torch.zeros(4, dtype=torch.float64, device=device)
+    if rank == src:
+        pts = torch.as_tensor(points, dtype=torch.float64).reshape(-1, 3).to(device)
+        head[0] = float(pts.shape[0])
+        head[1:] = torch.as_tensor(np.asarray(sensor, dtype=np.float64), device=device)
+    dist.broadcast(head, src=src, group=group)
+    n = int(head[0].item())
+    if rank != src:
+        pts = torch.empty((n, 3), dtype=torch.float64, device=device)
+    if n:
+        dist.broadcast(pts, src=src, group=group)
+    return head[1:].cpu().numpy(), pts.contiguous()
+
+
+def integrate_replicated(occ, m, points, sensor, params=None, src: int = 0, group=None):
+    """Row f3 on every replica: broadcast the frame from `src`, integrate it locally."""
+    import torch
+    dev = torch.device("cuda", occ.ctx.device)
+    sensor, pts = broadcast_frame(points, sensor, src=src, device=dev, group=group)
+    occ.integrate(sensor, pts, map=m, params=params)
 
 
 def all_gather_rows(local, n_total: int, world: int, strided: bool = True, group=None):

@@ -59,6 +59,18 @@ def _worker(rank, world, port, q):
         val = torch.tensor([2], dtype=torch.uint8) if rank == 0 else torch.zeros(1, dtype=torch.uint8)
         ndist.broadcast_deltas(ijk, val, src=0)
         ok &= bool(ijk.tolist() == [[1, 2, 3]] and val.tolist() == [2])
+        # depth-frame broadcast (row f3): identical frames, hence identical replicated stores
+        from nbt_inputs import CLOUD_CONFIGS
+        cf = CLOUD_CONFIGS["F0"]
+        pts0 = cf.cloud(0)[:2000] if rank == 0 else None
+        sensor, pts = ndist.broadcast_frame(pts0, cf.sensor(0) if rank == 0 else None, src=0)
+        ok &= bool(np.array_equal(sensor, cf.sensor(0)) and np.array_equal(pts.numpy(), cf.cloud(0)[:2000]))
+        L = oracle.new_logodds((cf.n,) * 3)
+        oracle.integrate(L, cf.voxel_size, (0, 0, 0), sensor, pts.numpy(), leaf=cf.leaf, max_range=cf.max_range)
+        digest = torch.tensor([int(np.nan_to_num(L, nan=7.0).astype(np.float64).sum() * 1e6)], dtype=torch.int64)
+        both = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(both, digest)
+        ok &= bool(both[0].item() == both[1].item())
         q.put((rank, bool(ok), ""))
         dist.destroy_process_group()
     except Exception as e:  # noqa: BLE001
