@@ -29,6 +29,7 @@
 // q_ab is computed once per ray in 64-bit and then kept in int32, which is exact for
 // rays up to 720 voxels per axis; longer rays use the same code with 64-bit q (the
 // host picks the variant from the camera geometry).
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "nbt_internal.cuh"
@@ -45,7 +46,14 @@ constexpr int kWarpsPerBlock = 8;
 // in flight while the current batch is consumed (look-ahead 2K, which must stay inside
 // the kBorder-voxel sentinel shell).  K = 16 without pipelining measured best
 // (profiles/r01_trace_variants.md); the other shapes stay compilable.
-constexpr int kBatchK = 16;
+#ifndef NBT_BATCH_K
+#define NBT_BATCH_K 16
+#endif
+#ifndef NBT_PIPE
+#define NBT_PIPE false
+#endif
+constexpr int kBatchK = NBT_BATCH_K;
+constexpr bool kPipe = NBT_PIPE;
 constexpr int kInt32MaxVoxels = 700;   // |D_a| bound (voxels) for the int32 decision terms
 
 // Origin outside the grid (rare): step with explicit bounds checks until the walk
@@ -433,11 +441,21 @@ __device__ __forceinline__ int queue_get(const WalkQueue<T> &Q, int i, Walk<T> &
     return Q.j[i];
 }
 
+// Resident blocks per SM the register allocation must allow: 4 (64 registers, 32 warps) for
+// the 32-bit 2-bit-store instance that every config uses -- measured 5-10% faster than the
+// unconstrained 92 registers (2 blocks) -- 3 for the 8-bit store and 2 for the 64-bit-term
+// instances (long rays), which would spill at fewer registers.
 #ifndef NBT_TRACE_MIN_BLOCKS
-#define NBT_TRACE_MIN_BLOCKS 1
+#define NBT_TRACE_MIN_BLOCKS 0
 #endif
+template <typename T, int VB>
+constexpr int trace_min_blocks()
+{
+    return NBT_TRACE_MIN_BLOCKS > 0 ? NBT_TRACE_MIN_BLOCKS : (sizeof(T) == 8 ? 2 : (VB == 2 ? 4 : 3));
+}
+
 template <typename T, int L, int VB, int K, bool PIPE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, NBT_TRACE_MIN_BLOCKS) k_id_trace(TraceArgs A)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()) k_id_trace(TraceArgs A)
 {
     static_assert((PIPE ? 2 * K : K) <= kBorder, "look-ahead must stay inside the sentinel shell");
     __shared__ WalkQueue<T> queues[kWarpsPerBlock];
@@ -679,10 +697,10 @@ double max_ray_voxels(const nbt_camera &cam, double range, double voxel_size)
 // The trace kernel instances: [wide][layout][8-bit store].
 using TraceFn = void (*)(TraceArgs);
 const TraceFn kTraceFns[2][2][2] = {
-    {{k_id_trace<int, kLayoutLinear, 2, kBatchK, false>, k_id_trace<int, kLayoutLinear, 8, kBatchK, false>},
-     {k_id_trace<int, kLayoutMorton, 2, kBatchK, false>, k_id_trace<int, kLayoutMorton, 8, kBatchK, false>}},
-    {{k_id_trace<long long, kLayoutLinear, 2, kBatchK, false>, k_id_trace<long long, kLayoutLinear, 8, kBatchK, false>},
-     {k_id_trace<long long, kLayoutMorton, 2, kBatchK, false>, k_id_trace<long long, kLayoutMorton, 8, kBatchK, false>}}};
+    {{k_id_trace<int, kLayoutLinear, 2, kBatchK, kPipe>, k_id_trace<int, kLayoutLinear, 8, kBatchK, kPipe>},
+     {k_id_trace<int, kLayoutMorton, 2, kBatchK, kPipe>, k_id_trace<int, kLayoutMorton, 8, kBatchK, kPipe>}},
+    {{k_id_trace<long long, kLayoutLinear, 2, kBatchK, kPipe>, k_id_trace<long long, kLayoutLinear, 8, kBatchK, kPipe>},
+     {k_id_trace<long long, kLayoutMorton, 2, kBatchK, kPipe>, k_id_trace<long long, kLayoutMorton, 8, kBatchK, kPipe>}}};
 
 using DebugFn = void (*)(MapView, const int32_t *, const int32_t *, int, int, int32_t *, uint8_t *, int32_t *,
                          uint32_t *);
@@ -724,6 +742,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     T.slots = T.n_tile_slots + (T.add_corners ? 4 : 0);
     const bool wide = max_ray_voxels(L.cam, L.range, m->desc.voxel_size) > kInt32MaxVoxels;
     const TraceFn fn = kTraceFns[wide][m->layout == kLayoutMorton][m->vbits == 8];
+    const int fi = (wide ? 4 : 0) + (m->layout == kLayoutMorton ? 2 : 0) + (m->vbits == 8 ? 1 : 0);
     if (ctx->trace_blocks_per_sm == 0) {
         // smallest shared-memory carveout that holds the walk queues of the resident blocks,
         // so the rest of the SM's 256 KB stays L1 for the map lines
@@ -733,11 +752,20 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
                 for (auto &b : a)
                     for (TraceFn f : b)
                         NBT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-        int b = 0;
-        NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kTraceFns[0][0][0], kWarpsPerBlock * 32, 0));
-        ctx->trace_blocks_per_sm = b > 0 ? b : 1;
+        for (int k = 0; k < 8; ++k) {
+            int b = 0;
+            NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kTraceFns[k >> 2][(k >> 1) & 1][k & 1],
+                                                                   kWarpsPerBlock * 32, 0));
+            ctx->trace_bps[k] = b > 0 ? b : 1;
+        }
+        ctx->trace_blocks_per_sm = ctx->trace_bps[0];
+        if (getenv("NBT_VERBOSE"))
+            fprintf(stderr, "libnbt: k_id_trace resident blocks/SM %d %d %d %d %d %d %d %d (carveout %d)\n",
+                    ctx->trace_bps[0], ctx->trace_bps[1], ctx->trace_bps[2], ctx->trace_bps[3], ctx->trace_bps[4],
+                    ctx->trace_bps[5], ctx->trace_bps[6], ctx->trace_bps[7], carve);
     }
-    long long resident_warps = (long long)ctx->num_sms * ctx->trace_blocks_per_sm * kWarpsPerBlock;
+    const int bps = ctx->trace_bps[fi];
+    long long resident_warps = (long long)ctx->num_sms * bps * kWarpsPerBlock;
     long long total_slots = (long long)L.n * T.slots;
     long long per = total_slots / (4 * resident_warps);           // aim for >= 4 chunks per warp
     int chunk = (int)((per / 32) * 32);
@@ -749,7 +777,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     T.total_chunks = (int)tc;
     T.min_refill = refill_threshold();
     long long want_blocks = (tc + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    long long max_blocks = (long long)ctx->num_sms * ctx->trace_blocks_per_sm;
+    long long max_blocks = (long long)ctx->num_sms * bps;
     int blocks = (int)(want_blocks < max_blocks ? want_blocks : max_blocks);
     {
         ProfScope ps(ctx, NBT_KERNEL_TRACE);

@@ -129,7 +129,8 @@ struct nbt_ctx_s {
     uint64_t launches = 0;
     int *d_err = nullptr;             // device-side validation status (nbt_status value)
     int *h_err = nullptr;             // pinned mirror
-    int trace_blocks_per_sm = 0;      // cached occupancy of the trace kernel
+    int trace_blocks_per_sm = 0;      // cached occupancy of the trace kernel (set once)
+    int trace_bps[8] = {0};           // ... per instance [wide][morton][8-bit store]
     // scratch
     nbt::DevBuf persp;                // staged perspective origins (n x 3 f64)
     nbt::DevBuf frames;               // per-perspective Q16 frames
