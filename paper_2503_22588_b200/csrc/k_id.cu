@@ -42,10 +42,11 @@ using namespace dda;
 constexpr int kFrameInts = 20;   // O, A, Rh, Uh, Rc, Uc (3 each, Q16), status, pad
 constexpr int kTotals = 5;       // per perspective: T_U, T_F, T_O, L, T_G (Eq. 2 gain, 1/63 units)
 constexpr int kWarpsPerBlock = 8;
-// Trace kernel shape: K voxels per speculative batch; PIPE = the next batch's loads are
-// in flight while the current batch is consumed (look-ahead 2K, which must stay inside
-// the kBorder-voxel sentinel shell).  K = 16 without pipelining measured best
-// (profiles/r01_trace_variants.md); the other shapes stay compilable.
+// Trace kernel shape: K voxels per speculative batch; PIPE = in-place software pipeline
+// (batch_cycle: the next batch's loads replace the current one's slot by slot, look-ahead
+// 2K, so build with NBT_BORDER >= 2K).  K = 16 without pipelining measured best: the
+// pipelined shapes spill at the 64-register budget or lose to the doubled speculation
+// past a stop (profiles/r01_trace_variants.md); they stay compilable for experiments.
 #ifndef NBT_BATCH_K
 #define NBT_BATCH_K 16
 #endif
@@ -141,37 +142,46 @@ __device__ __forceinline__ constexpr uint32_t lanes_mask(uint32_t pattern)
     return K >= 16 ? pattern : (pattern & ((1u << (2 * K)) - 1u));
 }
 
+// Store kinds (the VB template parameter): kStore2 = 2-bit codes, 16 per word (rows a1, a6);
+// kStoreByte = one byte per voxel holding the code alone; kStoreProb = one byte per voxel,
+// code in bits 0-1 and the Eq. 2 gain in bits 2-7 (f1).  Byte stores load the voxel's own
+// byte, so a visit needs no rotate and the code packs with one shift-add.
+constexpr int kStore2 = 2, kStoreByte = 1, kStoreProb = 8;
+
 // Issue the K loads of the next K visits (the DDA does not depend on the map, so
-// this runs ahead of the codes) and advance the DDA by K steps.  VB = bits per voxel.
+// this runs ahead of the codes) and advance the DDA by K steps.
 template <typename T, int L, int VB, int K>
 __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<K> &b)
 {
+    const uint8_t *bytes = reinterpret_cast<const uint8_t *>(m.words);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        if (VB == 2) {
+        if (VB == kStore2) {
             b.rot[k] = (w.idx << 1) - 2 * k;    // rotate amounts are taken mod 32
             b.wd[k] = __ldg(m.words + (w.idx >> 4));
         } else {
-            b.rot[k] = ((w.idx & 3u) << 3) - 2 * k;
-            b.wd[k] = __ldg(m.words + (w.idx >> 2));
+            b.wd[k] = __ldg(bytes + w.idx);
         }
         walk_step<T, L, false>(w, m);
     }
 }
 
-// Consume the batch holding visits s..s+K-1.  Returns true when the ray is finished
-// (counts added to c): first code >= 2 by one ffs (Occupied: early stop, P:213;
-// 3: left the grid), Free voxels by one popc; with the 8-bit store also the Eq. 2 gains.
-template <typename T, int VB, int K>
-__device__ __forceinline__ bool batch_consume(Walk<T> &w, const Batch<K> &b, int policy, Counts &c)
+// The packed 2-bit code of visit k of a batch, at bits 2k..2k+1 (stores without a gain).
+template <int VB, int K>
+__device__ __forceinline__ uint32_t batch_code(const Batch<K> &b, int k)
 {
-    uint32_t bits = 0, gsum = 0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const uint32_t r = __funnelshift_r(b.wd[k], b.wd[k], b.rot[k]);
-        bits |= r & (3u << (2 * k));
-        if (VB == 8) gsum += (b.wd[k] >> (b.rot[k] + 2 * k + 2)) & 63u;   // byte offset + 2
-    }
+    if (VB == kStore2) return __funnelshift_r(b.wd[k], b.wd[k], b.rot[k]) & (3u << (2 * k));
+    return b.wd[k] << (2 * k);                   // byte store: the byte is the code
+}
+
+// Close or advance the walk after the batch holding visits s..s+K-1, whose codes are
+// packed in `bits` (and, with the 8-bit store, whose gains sum to gsum / are read from b).
+// Returns true when the ray is finished (counts added to c): first code >= 2 by one ffs
+// (Occupied: early stop; 3: left the grid), Free voxels by one popc.
+template <typename T, int VB, int K>
+__device__ __forceinline__ bool batch_finish(Walk<T> &w, uint32_t bits, uint32_t gsum, const Batch<K> &b,
+                                             int policy, Counts &c)
+{
     const int left = w.n - w.s + 1;             // visits remaining, including the current one
     const uint32_t valid = left >= K ? lanes_mask<K>(0xFFFFFFFFu) : ((1u << (2 * left)) - 1u);
     const uint32_t stop = bits & valid & 0xAAAAAAAAu;   // codes 2 (Occupied) and 3 (outside)
@@ -180,10 +190,10 @@ __device__ __forceinline__ bool batch_consume(Walk<T> &w, const Batch<K> &b, int
         const int last = stop ? ((__ffs(stop) - 1) >> 1) : left - 1;
         const uint32_t upto = last >= 15 ? 0xFFFFFFFFu : ((1u << (2 * last + 2)) - 1u);
         uint32_t ng = w.ng;
-        if (VB == 8) {
+        if (VB == kStoreProb) {
 #pragma unroll
             for (int k = 0; k < K; ++k)
-                if (k <= last) ng += (b.wd[k] >> (b.rot[k] + 2 * k + 2)) & 63u;
+                if (k <= last) ng += b.wd[k] >> 2;
         }
         if (stop) {
             const uint32_t nf = w.nf + __popc(bits & (upto >> 2) & 0x55555555u);
@@ -194,9 +204,49 @@ __device__ __forceinline__ bool batch_consume(Walk<T> &w, const Batch<K> &b, int
         return true;
     }
     w.nf += __popc(bits & 0x55555555u);
-    if (VB == 8) w.ng += gsum;
+    if (VB == kStoreProb) w.ng += gsum;
     w.s += K;
     return false;
+}
+
+// Consume the batch holding visits s..s+K-1 (see batch_finish).
+template <typename T, int VB, int K>
+__device__ __forceinline__ bool batch_consume(Walk<T> &w, const Batch<K> &b, int policy, Counts &c)
+{
+    uint32_t bits = 0, gsum = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        if (VB == kStoreProb) {
+            bits += (b.wd[k] & 3u) << (2 * k);
+            gsum += b.wd[k] >> 2;                // Eq. 2 gain in 1/63 units
+        } else {
+            bits |= batch_code<VB, K>(b, k);
+        }
+    }
+    return batch_finish<T, VB, K>(w, bits, gsum, b, policy, c);
+}
+
+// In-place software pipeline (stores without a gain): extract the codes of the batch in b
+// (visits s..s+K-1) and, slot by slot, overwrite it with the loads of the next K visits, so
+// every load has a whole batch of DDA work to arrive before it is read.  Look-ahead 2K
+// voxels past the consumed position (kBorder >= 2K).
+template <typename T, int L, int VB, int K>
+__device__ __forceinline__ uint32_t batch_cycle(Walk<T> &w, const MapView &m, Batch<K> &b)
+{
+    const uint8_t *bytes = reinterpret_cast<const uint8_t *>(m.words);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        bits |= batch_code<VB, K>(b, k);
+        if (VB == kStore2) {
+            b.rot[k] = (w.idx << 1) - 2 * k;
+            b.wd[k] = __ldg(m.words + (w.idx >> 4));
+        } else {
+            b.wd[k] = __ldg(bytes + w.idx);
+        }
+        walk_step<T, L, false>(w, m);
+    }
+    return bits;
 }
 
 // ------------------------------------------------------------------ frames (a4)
@@ -451,13 +501,14 @@ __device__ __forceinline__ int queue_get(const WalkQueue<T> &Q, int i, Walk<T> &
 template <typename T, int VB>
 constexpr int trace_min_blocks()
 {
-    return NBT_TRACE_MIN_BLOCKS > 0 ? NBT_TRACE_MIN_BLOCKS : (sizeof(T) == 8 ? 2 : (VB == 2 ? 4 : 3));
+    return NBT_TRACE_MIN_BLOCKS > 0 ? NBT_TRACE_MIN_BLOCKS : (sizeof(T) == 8 ? 2 : (VB == kStoreProb ? 3 : 4));
 }
 
 template <typename T, int L, int VB, int K, bool PIPE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()) k_id_trace(TraceArgs A)
 {
-    static_assert((PIPE ? 2 * K : K) <= kBorder, "look-ahead must stay inside the sentinel shell");
+    constexpr bool CYCLE = PIPE && VB != kStoreProb;     // in-place pipeline (batch_cycle)
+    static_assert((CYCLE ? 2 * K : K) <= kBorder, "look-ahead must stay inside the sentinel shell");
     __shared__ WalkQueue<T> queues[kWarpsPerBlock];
     WalkQueue<T> &Q = queues[threadIdx.x >> 5];
     const unsigned full = 0xffffffffu;
@@ -467,7 +518,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
     bool q_done = false;
     int qhead = 0, qcount = 0;               // warp-uniform prepared-walk queue
     Walk<T> w;
-    Batch<K> b0, b1;
+    Batch<K> b0;
     bool have = false;
     int jl = -1;                             // perspective of this lane's accumulators
     Counts c{0, 0, 0, 0, 0};
@@ -505,7 +556,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     const int j = queue_get<T, L>(Q, qhead + rank, w);
                     if (j != jl) { flush_counts(A.totals, jl, c); jl = j; }
                     have = true;
-                    if (PIPE) batch_issue<T, L, VB, K>(w, A.m, b0);
+                    if (CYCLE) batch_issue<T, L, VB, K>(w, A.m, b0);
                 }
                 qhead += take;
                 qcount -= take;
@@ -514,18 +565,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
         }
         if (q_done && qcount == 0 && !__any_sync(full, have)) break;
         if (!have) continue;
-        if (!PIPE) {
+        if (CYCLE) {
+            // b0 holds visits s..s+K-1 (issued at the ray's start or by the last cycle)
+            uint32_t bits;
+            if (w.n - w.s + 1 > K) {
+                bits = batch_cycle<T, L, VB, K>(w, A.m, b0);
+            } else {
+                bits = 0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) bits |= batch_code<VB, K>(b0, k);
+            }
+            if (batch_finish<T, VB, K>(w, bits, 0u, b0, A.m.policy, c)) have = false;
+        } else {
             batch_issue<T, L, VB, K>(w, A.m, b0);
             if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) have = false;
-        } else {
-            // b0 holds visits s..s+K-1; keep the next batch in flight while consuming
-            if (w.n - w.s + 1 > K) batch_issue<T, L, VB, K>(w, A.m, b1);
-            if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) {
-                have = false;
-            } else {
-                if (w.n - w.s + 1 > K) batch_issue<T, L, VB, K>(w, A.m, b0);
-                if (batch_consume<T, VB, K>(w, b1, A.m.policy, c)) have = false;
-            }
         }
     }
     flush_counts(A.totals, jl, c);
@@ -584,8 +637,8 @@ __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const in
         visits = w.n + 1;
     } else {
         for (;;) {
-            const uint32_t cd = VB == 2 ? code_of(__ldg(m.words + (w.idx >> 4)), w.idx)
-                                        : (__ldg(m.words + (w.idx >> 2)) >> ((w.idx & 3u) << 3)) & 3u;
+            const uint32_t cd = VB == kStore2 ? code_of(__ldg(m.words + (w.idx >> 4)), w.idx)
+                                              : __ldg(reinterpret_cast<const uint8_t *>(m.words) + w.idx) & 3u;
             if (w.s < max_visits) {
                 ri[3 * w.s] = w.vx; ri[3 * w.s + 1] = w.vy; ri[3 * w.s + 2] = w.vz;
                 rc[w.s] = cd == 3u ? 255 : (uint8_t)cd;
@@ -694,21 +747,25 @@ double max_ray_voxels(const nbt_camera &cam, double range, double voxel_size)
     return rs * sqrt(1.0 + ex * ex + ey * ey) * 1.001 + 2.0;
 }
 
-// The trace kernel instances: [wide][layout][8-bit store].
+// The kernel instances: [wide][layout][store: 2-bit, byte, byte + gain].
+#define NBT_TRACE_ROW(T, L)                                                                     \
+    {k_id_trace<T, L, kStore2, kBatchK, kPipe>, k_id_trace<T, L, kStoreByte, kBatchK, kPipe>, \
+     k_id_trace<T, L, kStoreProb, kBatchK, kPipe>}
 using TraceFn = void (*)(TraceArgs);
-const TraceFn kTraceFns[2][2][2] = {
-    {{k_id_trace<int, kLayoutLinear, 2, kBatchK, kPipe>, k_id_trace<int, kLayoutLinear, 8, kBatchK, kPipe>},
-     {k_id_trace<int, kLayoutMorton, 2, kBatchK, kPipe>, k_id_trace<int, kLayoutMorton, 8, kBatchK, kPipe>}},
-    {{k_id_trace<long long, kLayoutLinear, 2, kBatchK, kPipe>, k_id_trace<long long, kLayoutLinear, 8, kBatchK, kPipe>},
-     {k_id_trace<long long, kLayoutMorton, 2, kBatchK, kPipe>, k_id_trace<long long, kLayoutMorton, 8, kBatchK, kPipe>}}};
+const TraceFn kTraceFns[2][2][3] = {{NBT_TRACE_ROW(int, kLayoutLinear), NBT_TRACE_ROW(int, kLayoutMorton)},
+                                    {NBT_TRACE_ROW(long long, kLayoutLinear), NBT_TRACE_ROW(long long, kLayoutMorton)}};
+#undef NBT_TRACE_ROW
 
 using DebugFn = void (*)(MapView, const int32_t *, const int32_t *, int, int, int32_t *, uint8_t *, int32_t *,
                          uint32_t *);
-const DebugFn kDebugFns[2][2][2] = {
-    {{k_debug_trace<int, kLayoutLinear, 2>, k_debug_trace<int, kLayoutLinear, 8>},
-     {k_debug_trace<int, kLayoutMorton, 2>, k_debug_trace<int, kLayoutMorton, 8>}},
-    {{k_debug_trace<long long, kLayoutLinear, 2>, k_debug_trace<long long, kLayoutLinear, 8>},
-     {k_debug_trace<long long, kLayoutMorton, 2>, k_debug_trace<long long, kLayoutMorton, 8>}}};
+#define NBT_DEBUG_ROW(T, L) \
+    {k_debug_trace<T, L, kStore2>, k_debug_trace<T, L, kStoreByte>, k_debug_trace<T, L, kStoreProb>}
+const DebugFn kDebugFns[2][2][3] = {{NBT_DEBUG_ROW(int, kLayoutLinear), NBT_DEBUG_ROW(int, kLayoutMorton)},
+                                    {NBT_DEBUG_ROW(long long, kLayoutLinear), NBT_DEBUG_ROW(long long, kLayoutMorton)}};
+#undef NBT_DEBUG_ROW
+
+// Store kind of a map handle (index of the tables above).
+int store_kind(nbt_map m) { return m->vbits == 2 ? 0 : (m->prob ? 2 : 1); }
 
 }  // namespace
 
@@ -741,8 +798,9 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     T.n_tile_slots = T.tiled ? T.Wt * Ht * 32 : T.W * T.H;
     T.slots = T.n_tile_slots + (T.add_corners ? 4 : 0);
     const bool wide = max_ray_voxels(L.cam, L.range, m->desc.voxel_size) > kInt32MaxVoxels;
-    const TraceFn fn = kTraceFns[wide][m->layout == kLayoutMorton][m->vbits == 8];
-    const int fi = (wide ? 4 : 0) + (m->layout == kLayoutMorton ? 2 : 0) + (m->vbits == 8 ? 1 : 0);
+    const int sk = store_kind(m);
+    const TraceFn fn = kTraceFns[wide][m->layout == kLayoutMorton][sk];
+    const int fi = (wide ? 6 : 0) + (m->layout == kLayoutMorton ? 3 : 0) + sk;
     if (ctx->trace_blocks_per_sm == 0) {
         // smallest shared-memory carveout that holds the walk queues of the resident blocks,
         // so the rest of the SM's 256 KB stays L1 for the map lines
@@ -752,17 +810,18 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
                 for (auto &b : a)
                     for (TraceFn f : b)
                         NBT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 12; ++k) {
             int b = 0;
-            NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kTraceFns[k >> 2][(k >> 1) & 1][k & 1],
+            NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kTraceFns[k / 6][(k / 3) & 1][k % 3],
                                                                    kWarpsPerBlock * 32, 0));
             ctx->trace_bps[k] = b > 0 ? b : 1;
         }
         ctx->trace_blocks_per_sm = ctx->trace_bps[0];
-        if (getenv("NBT_VERBOSE"))
-            fprintf(stderr, "libnbt: k_id_trace resident blocks/SM %d %d %d %d %d %d %d %d (carveout %d)\n",
-                    ctx->trace_bps[0], ctx->trace_bps[1], ctx->trace_bps[2], ctx->trace_bps[3], ctx->trace_bps[4],
-                    ctx->trace_bps[5], ctx->trace_bps[6], ctx->trace_bps[7], carve);
+        if (getenv("NBT_VERBOSE")) {
+            fprintf(stderr, "libnbt: k_id_trace resident blocks/SM");
+            for (int k = 0; k < 12; ++k) fprintf(stderr, " %d", ctx->trace_bps[k]);
+            fprintf(stderr, " (carveout %d)\n", carve);
+        }
     }
     const int bps = ctx->trace_bps[fi];
     long long resident_warps = (long long)ctx->num_sms * bps * kWarpsPerBlock;
@@ -789,7 +848,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     ProfScope ps(ctx, NBT_KERNEL_FINALIZE);
     k_id_finalize<<<(L.n + 127) / 128, 128, 0, ctx->stream>>>(
         A, ctx->frames.as<int32_t>(), ctx->totals.as<unsigned long long>(), m->desc.gain[0], m->desc.gain[1],
-        m->desc.gain[2], m->vbits == 8 ? 1 : 0, (double)ne, L.d_xyz_out, L.d_gain_out,
+        m->desc.gain[2], m->prob ? 1 : 0, (double)ne, L.d_xyz_out, L.d_gain_out,
         reinterpret_cast<unsigned long long *>(L.d_counts_out));
     NBT_LAUNCHED(ctx);
     return NBT_OK;
@@ -800,7 +859,7 @@ nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const 
                               uint32_t *d_counts, bool wide)
 {
     if (n_rays == 0) return NBT_OK;
-    const DebugFn fn = kDebugFns[wide][m->layout == kLayoutMorton][m->vbits == 8];
+    const DebugFn fn = kDebugFns[wide][m->layout == kLayoutMorton][store_kind(m)];
     fn<<<dim3((n_rays + 127) / 128), dim3(128), 0, ctx->stream>>>(view_of(m), d_o, d_e, n_rays, max_visits, d_ijk,
                                                                    d_code, d_len, d_counts);
     NBT_LAUNCHED(ctx);

@@ -153,6 +153,7 @@ Geom geom_of(nbt_map m)
     Geom g;
     g.layout = m->layout;
     g.vbits = m->vbits;
+    g.prob = m->prob ? 1 : 0;
     g.nx = m->desc.nx; g.ny = m->desc.ny; g.nz = m->desc.nz;
     g.px = m->px; g.py = m->py;
     // a state-only write to the 8-bit store uses the per-state constants of the desc:

@@ -9,6 +9,7 @@ namespace nbt {
 struct Geom {
     int layout;
     int vbits;                 // 2 or 8
+    int prob;                  // 8-bit store holds the Eq. 2 gain in bits 2-7 (f1)
     int nx, ny, nz;
     uint32_t px, py;           // linear padded extents
     uint32_t def_level[3];     // 8-bit store: level used for U / F / O when none is given
@@ -30,7 +31,7 @@ __device__ __forceinline__ uint32_t shift_of(const Geom &g, uint64_t i)
 // The stored value of a grid voxel: the state, or state | Eq. 2 gain (1/63 units) << 2.
 __device__ __forceinline__ uint32_t stored_value(const Geom &g, uint32_t code, uint32_t level)
 {
-    if (g.vbits == 2) return code;
+    if (g.vbits == 2 || !g.prob) return code;
     const uint32_t gq = code == 0 ? 63u : (code == 1 ? level : 63u - level);
     return code | (gq << 2);
 }

@@ -34,7 +34,10 @@ nbt_status cuda_fail(cudaError_t e, const char *what);
 
 // Thickness of the sentinel shell around the stored grid (k_map.cu); bounds the
 // walk's speculative look-ahead (k_id.cu: batch size, twice that when pipelined).
-constexpr int kBorder = 16;
+#ifndef NBT_BORDER
+#define NBT_BORDER 16
+#endif
+constexpr int kBorder = NBT_BORDER;
 
 // Map store layouts (k_map.cu).  Linear: x-fastest rows inside a kBorder sentinel shell.
 // Morton: the voxel index interleaves the coordinate bits (x0 y0 z0 x1 y1 z1 ...) inside a
@@ -130,7 +133,7 @@ struct nbt_ctx_s {
     int *d_err = nullptr;             // device-side validation status (nbt_status value)
     int *h_err = nullptr;             // pinned mirror
     int trace_blocks_per_sm = 0;      // cached occupancy of the trace kernel (set once)
-    int trace_bps[8] = {0};           // ... per instance [wide][morton][8-bit store]
+    int trace_bps[12] = {0};          // ... per instance [wide][morton][store kind]
     // scratch
     nbt::DevBuf persp;                // staged perspective origins (n x 3 f64)
     nbt::DevBuf frames;               // per-perspective Q16 frames
@@ -161,7 +164,8 @@ struct nbt_map_s {
     nbt_ctx ctx = nullptr;
     nbt_map_desc desc{};
     int layout = nbt::kLayoutLinear;
-    int vbits = 2;                    // 2: states only; 8: state + Eq. 2 gain (f1)
+    int vbits = 2;                    // 2: 2-bit codes; 8: one byte per voxel
+    bool prob = false;                // byte store also holds the Eq. 2 gain (f1)
     int pbits = 0;                    // Morton: cube side 2^pbits
     uint32_t px = 0, py = 0, pz = 0;  // linear: padded extents (kBorder sentinel voxels each side)
     uint64_t nvox_pad = 0;

@@ -455,7 +455,7 @@ static nbt_status check_desc(const nbt_map_desc *d)
     return NBT_OK;
 }
 
-static nbt_status map_create(nbt_ctx ctx, const nbt_map_desc *desc, int vbits, nbt_map *out)
+static nbt_status map_create(nbt_ctx ctx, const nbt_map_desc *desc, int vbits, bool prob, nbt_map *out)
 {
     nbt_status s;
     if (!out) return fail(NBT_ERR_INVALID_ARG, "nbt_map_create: null out");
@@ -467,6 +467,7 @@ static nbt_status map_create(nbt_ctx ctx, const nbt_map_desc *desc, int vbits, n
     ctx_retain(ctx);
     m->desc = *desc;
     m->vbits = vbits;
+    m->prob = prob;
     m->px = desc->nx + 2 * kBorder; m->py = desc->ny + 2 * kBorder; m->pz = desc->nz + 2 * kBorder;
     m->nvox_pad = (uint64_t)m->px * m->py * m->pz;
     // Store layout: linear by default (fewest instructions per voxel step, fastest on
@@ -511,14 +512,22 @@ static nbt_status map_create(nbt_ctx ctx, const nbt_map_desc *desc, int vbits, n
     return NBT_OK;
 }
 
+// Bits per voxel of a state-only map: NBT_MAP_BITS=2 (packed codes) or 8 (one byte per
+// voxel: no rotate per visit, 4x the bytes); default 2.
+static int state_store_bits()
+{
+    const char *e = getenv("NBT_MAP_BITS");
+    return (e && atoi(e) == 8) ? 8 : 2;
+}
+
 nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
 {
-    return map_create(ctx, desc, 2, out);
+    return map_create(ctx, desc, state_store_bits(), false, out);
 }
 
 nbt_status nbt_map_create_prob(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
 {
-    return map_create(ctx, desc, 8, out);
+    return map_create(ctx, desc, 8, true, out);
 }
 
 static nbt_status map_nvox(nbt_map m, size_t n, const char *who)
@@ -573,7 +582,7 @@ nbt_status nbt_map_upload_prob(nbt_map m, const float *p, const uint8_t *observe
         sp = dp.as<float>();
         so = dobs.as<uint8_t>();
     }
-    const bool prob = m->vbits == 8;
+    const bool prob = m->prob;
     if (e == cudaSuccess && (s = codes.ensure(n)) == NBT_OK && (!prob || (s = levels.ensure(n)) == NBT_OK)) {
         s = launch_map_classify(ctx, sp, so, n, t_occ, t_free, codes.as<uint8_t>(),
                                 prob ? levels.as<uint8_t>() : nullptr);
@@ -658,7 +667,7 @@ nbt_status nbt_map_update_prob(nbt_map m, const int32_t *ijk, const float *p, co
     uint8_t *dcodes = reinterpret_cast<uint8_t *>(base + n * 17);
     uint8_t *dlevels = reinterpret_cast<uint8_t *>(base + n * 18);
     if ((s = launch_map_classify(ctx, dp, dobs, n, t_occ, t_free, dcodes, dlevels))) return s;
-    return launch_map_update(ctx, m, dijk, dcodes, m->vbits == 8 ? dlevels : nullptr, n);
+    return launch_map_update(ctx, m, dijk, dcodes, m->prob ? dlevels : nullptr, n);
 }
 
 nbt_status nbt_map_device_buffer(nbt_map m, void **dev_ptr, size_t *bytes)
@@ -693,7 +702,7 @@ nbt_status nbt_map_download_levels(nbt_map m, uint8_t *levels_out, size_t n)
     nbt_status s;
     if ((s = map_nvox(m, n, "nbt_map_download_levels"))) return s;
     if (!levels_out) return fail(NBT_ERR_INVALID_ARG, "nbt_map_download_levels: null out");
-    if (m->vbits != 8) return fail(NBT_ERR_STATE, "nbt_map_download_levels: map stores no probabilities");
+    if (!m->prob) return fail(NBT_ERR_STATE, "nbt_map_download_levels: map stores no probabilities");
     nbt_ctx ctx = m->ctx;
     if ((s = bind(ctx))) return s;
     DevBuf tmp;

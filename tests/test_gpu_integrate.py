@@ -132,11 +132,12 @@ def _run_sequence(nbt, ctx, cf, n_clouds, prob, layout, monkeypatch, params=None
     return occ, m, L
 
 
-@pytest.mark.parametrize("prob", [False, True])
+@pytest.mark.parametrize("store", ["2bit", "byte", "prob"])
 @pytest.mark.parametrize("layout", ["linear", "morton"])
-def test_integrate_sequence_small(nbt, ctx, prob, layout, monkeypatch):
+def test_integrate_sequence_small(nbt, ctx, store, layout, monkeypatch):
     cf = I.CLOUD_CONFIGS["F0"]
-    _run_sequence(nbt, ctx, cf, cf.n_clouds, prob, layout, monkeypatch)
+    monkeypatch.setenv("NBT_MAP_BITS", "8" if store == "byte" else "2")
+    _run_sequence(nbt, ctx, cf, cf.n_clouds, store == "prob", layout, monkeypatch)
 
 
 @pytest.mark.parametrize("prob", [False, True])

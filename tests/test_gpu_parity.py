@@ -489,11 +489,14 @@ def test_id_wide_path(nbt, ctx):
 
 # ---------------------------------------------------------------- store layouts
 
+@pytest.mark.parametrize("bits", [2, 8])
 @pytest.mark.parametrize("layout", ["linear", "morton"])
-def test_layouts_roundtrip_update_and_id(nbt, ctx, layout, monkeypatch):
-    """Both map store layouts (Morton cube / linear with sentinel shell) give identical,
-    oracle-exact results: upload/download, last-wins updates, per-ray walks, the ID."""
+def test_layouts_roundtrip_update_and_id(nbt, ctx, layout, bits, monkeypatch):
+    """Both map store layouts (Morton cube / linear with sentinel shell) and both state
+    widths (2-bit codes / one byte per voxel) give identical, oracle-exact results:
+    upload/download, last-wins updates, per-ray walks, the ID."""
     monkeypatch.setenv("NBT_MAP_LAYOUT", layout)
+    monkeypatch.setenv("NBT_MAP_BITS", str(bits))
     codes = rand_map(0, 0.3, 0.66, 0.04, seed=21, shape=(19, 27, 33))
     m, om = make_map(nbt, ctx, codes)
     assert np.array_equal(m.download(), codes)
@@ -743,3 +746,14 @@ def test_prob_map_walks(nbt, ctx):
     om = oracle.OracleMap(codes)
     o, e = random_segments_q12(1500, -5.0, 17.0, seed=6)
     _compare_walks(nbt, ctx, m, om, o, e)
+
+
+def test_byte_store_config_b_subset(nbt, ctx, monkeypatch):
+    """The byte-per-voxel state store on config B's map and camera: bit-exact vs the oracle."""
+    monkeypatch.setenv("NBT_MAP_BITS", "8")
+    cfg = CONFIGS["B"]
+    codes = cfg.map_codes()
+    m, om = make_map(nbt, ctx, codes, voxel_size=cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, 24, seed=cfg.persp_seed, mode=cfg.persp_mode)
+    cloud, g, c = run_both(nbt, ctx, m, om, cfg.poi, P, cfg.width, cfg.height, cfg.range_)
+    assert_cloud_equal(cloud, P, g, c)
