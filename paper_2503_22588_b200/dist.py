@@ -35,8 +35,19 @@ def env_rank_world():
 
 
 def init_process_group(backend="nccl"):
+    """Join the torchrun job.  NBT_DIST_BACKEND=gloo overrides the backend and maps every
+    rank onto the visible GPUs round-robin: a functional check of the multi-rank path on a
+    one-GPU box (collectives through the host, so no rank's kernel waits on another's);
+    returns local = the CUDA device to use."""
     import torch.distributed as dist
     rank, world, local = env_rank_world()
+    override = os.environ.get("NBT_DIST_BACKEND")
+    if override:
+        backend = override
+        if backend != "nccl":
+            import torch
+            if torch.cuda.is_available():
+                local = local % torch.cuda.device_count()
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29531")
