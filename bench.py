@@ -46,7 +46,7 @@ INT_LANES_PER_SM_CLK = 128
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="B")
@@ -77,31 +77,66 @@ def workload_name(cfg, world):
 # ----------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons every 100 ms; keeps samples with timestamps."""
+    """SM clocks + throttle reasons sampled every 5 ms through NVML in a thread (fallback:
+    nvidia-smi every 100 ms); keeps samples with timestamps."""
 
-    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, gpu_id):
-        self.samples = []
+    def __init__(self, gpu_id, period_s=0.005):
+        self.samples = []                    # (t, sm_mhz, max_mhz, [reason names])
         self.proc = None
+        self.running = True
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", gpu_id, f"--query-gpu={self.FIELDS}",
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByUUID(gpu_id)
+            self._nv = (pynvml, h)
+            self.thread = threading.Thread(target=self._poll_nvml, args=(period_s,), daemon=True)
+            self.thread.start()
+            return
+        except Exception:  # noqa: BLE001 -- no NVML: fall back to nvidia-smi
+            self._nv = None
+        try:
+            fields = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                      "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                      "clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", gpu_id, f"--query-gpu={fields}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread = threading.Thread(target=self._read_smi, daemon=True)
         self.thread.start()
 
-    def _read(self):
+    def _poll_nvml(self, period_s):
+        nv, h = self._nv
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while self.running:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((time.time(), float(sm), float(mx),
+                                     [n for n, b in zip(self.REASONS, bits) if r & b]))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(period_s)
+
+    def _read_smi(self):
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
         for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.samples.append((time.time(), parts))
+            p = [q.strip() for q in line.split(",")]
+            if len(p) >= 7:
+                self.samples.append((time.time(), num(p[1]), num(p[2]),
+                                     [n for n, v in zip(self.REASONS, p[3:7]) if v.lower() == "active"]))
 
     def stop(self):
+        self.running = False
         if self.proc:
             self.proc.terminate()
             try:
@@ -110,25 +145,18 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self, t0, t1):
-        inside = [p for t, p in self.samples if t0 <= t <= t1 + 0.15]
-        note = "sampled during the timed region"
+        inside = [x for x in self.samples if t0 <= x[0] <= t1]
+        note = "sampled during the timed region (NVML, 5 ms)" if self._nv else \
+            "sampled during the timed region (nvidia-smi, 100 ms)"
         if not inside and self.samples:
-            best = min(self.samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))
-            inside = [best[1]]
-            note = "timed region shorter than the 100 ms sampling period: nearest sample"
+            inside = [min(self.samples, key=lambda x: min(abs(x[0] - t0), abs(x[0] - t1)))]
+            note = "timed region shorter than the sampling period: nearest sample"
         if not inside:
             return None
-
-        def num(x):
-            try:
-                return float(x)
-            except ValueError:
-                return None
-        sm = [num(p[1]) for p in inside if num(p[1]) is not None]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for p in inside for i in range(4) if p[4 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(inside[0][2]),
-                "reasons": reasons, "samples": len(inside), "note": note}
+        sm = [x[1] for x in inside if x[1] is not None]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
+                "sm_max_mhz": inside[0][2], "reasons": sorted({n for x in inside for n in x[3]}),
+                "samples": len(inside), "note": note}
 
 
 # ------------------------------------------------------------ CPU oracle leg
