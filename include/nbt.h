@@ -204,7 +204,7 @@ nbt_status nbt_occ_download(nbt_occ occ, float *logodds_out, size_t n);
  * visits it (Q35); L := clamp(L + delta) in float (Q36).  map (NULL allowed; same nx,
  * ny, nz) receives the new state -- L >= logit(t_occ) Occupied, <= logit(t_free) Free,
  * else Unknown -- and level round(63 P) (Q37) of every voxel whose (state, level)
- * changed.  A non-finite point, a leaf cell index >= 2^20 or a Q12 overflow makes the
+ * changed.  A non-finite point, a leaf cell index |c| >= 2^15 - 1 or a Q12 overflow makes the
  * whole call a no-op, reported as NBT_ERR_INVALID_ARG by the next nbt_ctx_sync or
  * nbt_occ_stats (points are validated on the device).  n < 2^31.  Stream-ordered; host
  * points are staged through pinned memory, no sync. */

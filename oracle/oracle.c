@@ -662,7 +662,7 @@ int orc_map_update(uint8_t *codes, int32_t nx, int32_t ny, int32_t nz, const int
 /* Voxel filter (reading Q33): every point goes to the leaf cell
  * (floor(x/leaf), floor(y/leaf), floor(z/leaf)); each occupied cell yields ONE point,
  * the centroid of its inputs, summed in input order and divided by the count.  Cells
- * are output in ascending (iz, iy, ix) order.  |cell index| must stay below 2^20 and
+ * are output in ascending (iz, iy, ix) order.  |cell index| must stay below 2^15 - 1 and
  * every coordinate must be finite (INVALID_ARG otherwise).  out_xyz / out_count hold
  * room for n cells; *m_out = number of cells. */
 typedef struct { int64_t c[3]; int64_t idx; } orc_cellkey;
@@ -687,7 +687,7 @@ int orc_voxel_filter(const double *pts, int64_t n, double leaf, double *out_xyz,
             double v = pts[3 * i + a];
             if (!isfinite(v)) { free(k); return ORC_ERR_INVALID_ARG; }
             double c = floor(v / leaf);
-            if (!(fabs(c) < 1048576.0)) { free(k); return ORC_ERR_INVALID_ARG; }
+            if (!(fabs(c) < 32767.0)) { free(k); return ORC_ERR_INVALID_ARG; }
             k[i].c[a] = (int64_t)c;
         }
         k[i].idx = i;

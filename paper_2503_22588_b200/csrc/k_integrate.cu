@@ -3,7 +3,7 @@
 // host round trip (the paper blames host <-> device map traffic for its GPU
 // losses at small N_P).
 //
-//   k_filter_keys     voxel filter, part 1 (Q33): one 63-bit cell key per point,
+//   k_filter_keys     voxel filter, part 1 (Q33): one 48-bit cell key per point,
 //                     (iz, iy, ix) from high to low bits so that key order is the output
 //                     order; non-finite or out-of-range points poison the cloud.
 //   (cub)             stable radix sort of (key, input index).
@@ -39,8 +39,9 @@ namespace {
 
 using dda::Walk;
 
-constexpr double kKeyLimit = 1048576.0;          // |cell index| < 2^20 (Q33)
-constexpr uint64_t kBadKey = ~0ull;
+constexpr double kKeyLimit = 32767.0;            // |cell index| < 2^15 - 1 (Q33)
+constexpr int kKeyBits = 48;                     // 16 bits per axis: 6 radix passes instead of 8
+constexpr uint64_t kBadKey = (1ull << kKeyBits) - 1;   // above every valid key (fields <= 0xFFFE)
 constexpr double kQ12Limit = 1073741824.0;       // |Q12 coordinate| < 2^30 (Q19)
 constexpr int kWideRayVoxels = 700;              // int32 DDA terms up to this many voxels per axis
 
@@ -60,7 +61,7 @@ __global__ void k_filter_keys(const double *__restrict__ pts, uint32_t n, double
             const double v = pts[3 * (size_t)i + a];
             const double c = floor(__ddiv_rn(v, leaf));
             ok = ok && isfinite(v) && fabs(c) < kKeyLimit;
-            if (ok) key |= (unsigned long long)((long long)c + (1ll << 20)) << (21 * a);
+            if (ok) key |= (unsigned long long)((long long)c + (1ll << 15)) << (16 * a);
         }
         if (!ok) {
             key = kBadKey;
@@ -447,12 +448,12 @@ nbt_status launch_voxel_filter(nbt_ctx ctx, nbt_occ_s *o, const double *d_pts, u
     NBT_LAUNCHED(ctx);
     thrust::counting_iterator<uint32_t> iota(0);
     size_t t1 = 0, t2 = 0;
-    NBT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys_s, idx, idx_s, (int)n, 0, 64, ctx->stream));
+    NBT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys_s, idx, idx_s, (int)n, 0, kKeyBits, ctx->stream));
     NBT_CUDA(cub::DeviceSelect::Flagged(nullptr, t2, iota, head, run_off, n_runs, (int)n, ctx->stream));
     const size_t tmp = t1 > t2 ? t1 : t2;
     if ((st = o->cub_tmp.ensure(tmp))) return st;
     size_t tt = tmp;
-    NBT_CUDA(cub::DeviceRadixSort::SortPairs(o->cub_tmp.p, tt, keys, keys_s, idx, idx_s, (int)n, 0, 64,
+    NBT_CUDA(cub::DeviceRadixSort::SortPairs(o->cub_tmp.p, tt, keys, keys_s, idx, idx_s, (int)n, 0, kKeyBits,
                                              ctx->stream));
     k_filter_gather<<<gr, 256, 0, ctx->stream>>>(d_pts, idx_s, keys_s, n, o->sorted.as<double>(), head,
                                                  ctl + kOccValid);

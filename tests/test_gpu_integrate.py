@@ -92,7 +92,13 @@ def test_voxel_filter_device_input_and_errors(nbt, ctx):
     with pytest.raises(nbt.NbtError):
         nbt.voxel_filter(ctx, bad, 0.04)
     with pytest.raises(nbt.NbtError):
-        nbt.voxel_filter(ctx, np.array([[1e9, 0.0, 0.0]]), 1e-3)   # cell index >= 2^20
+        nbt.voxel_filter(ctx, np.array([[1e9, 0.0, 0.0]]), 1e-3)   # cell index out of range
+    edge = np.array([[32766.5, -32765.5, 0.0], [-32765.25, 32766.75, 5.0]])
+    got, gcnt = nbt.voxel_filter(ctx, edge, 1.0)                    # the extreme valid cells
+    want, wcnt = oracle.voxel_filter(edge, 1.0)
+    assert np.array_equal(got, want) and np.array_equal(gcnt, wcnt)
+    with pytest.raises(nbt.NbtError):
+        nbt.voxel_filter(ctx, np.array([[0.0, 32767.5, 0.0]]), 1.0)
 
 
 def _run_sequence(nbt, ctx, cf, n_clouds, prob, layout, monkeypatch, params=None, L_start=None):

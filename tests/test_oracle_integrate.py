@@ -66,6 +66,12 @@ def test_filter_edge_cases():
         oracle.voxel_filter(np.array([[0.0, np.nan, 0.0]]), 0.5)
     with pytest.raises(oracle.OracleError):
         oracle.voxel_filter(np.array([[0.0, 0.0, 0.0]]), 0.0)
+    # cell-index range (Q33): |cell| <= 32766 accepted, 32767 rejected
+    out, cnt = oracle.voxel_filter(np.array([[32766.5, -32765.5, 0.0]]), 1.0)
+    assert cnt.tolist() == [1]
+    for bad in ([32767.5, 0.0, 0.0], [0.0, -32766.5, 0.0]):
+        with pytest.raises(oracle.OracleError):
+            oracle.voxel_filter(np.array([bad]), 1.0)
     # negative coordinates floor downwards
     out, cnt = oracle.voxel_filter(np.array([[-0.05, 0.0, 0.0], [-0.01, 0.0, 0.0], [0.01, 0.0, 0.0]]), 0.1)
     assert cnt.tolist() == [2, 1]
