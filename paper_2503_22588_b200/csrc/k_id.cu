@@ -41,7 +41,10 @@ using namespace dda;
 
 constexpr int kFrameInts = 20;   // O, A, Rh, Uh, Rc, Uc (3 each, Q16), status, pad
 constexpr int kTotals = 5;       // per perspective: T_U, T_F, T_O, L, T_G (Eq. 2 gain, 1/63 units)
-constexpr int kWarpsPerBlock = 8;
+#ifndef NBT_WARPS_PER_BLOCK
+#define NBT_WARPS_PER_BLOCK 8
+#endif
+constexpr int kWarpsPerBlock = NBT_WARPS_PER_BLOCK;
 // Trace kernel shape: K voxels per speculative batch; PIPE = in-place software pipeline
 // (batch_cycle: the next batch's loads replace the current one's slot by slot, look-ahead
 // 2K, so build with NBT_BORDER >= 2K).  K = 16 without pipelining measured best: the
@@ -501,7 +504,9 @@ __device__ __forceinline__ int queue_get(const WalkQueue<T> &Q, int i, Walk<T> &
 template <typename T, int VB>
 constexpr int trace_min_blocks()
 {
-    return NBT_TRACE_MIN_BLOCKS > 0 ? NBT_TRACE_MIN_BLOCKS : (sizeof(T) == 8 ? 2 : (VB == kStoreProb ? 3 : 4));
+    // resident warps per SM the register budget must allow: 32 (64 registers), 24 or 16
+    return NBT_TRACE_MIN_BLOCKS > 0 ? NBT_TRACE_MIN_BLOCKS
+                                    : (sizeof(T) == 8 ? 16 : (VB == kStoreProb ? 24 : 32)) / kWarpsPerBlock;
 }
 
 template <typename T, int L, int VB, int K, bool PIPE>
