@@ -248,3 +248,55 @@ def test_integrate_exact_ties_and_long_rays(nbt, ctx, monkeypatch):
         occ.integrate(sensor, pts, params=nbt.integrate_params(1.0, leaf=0.0, max_range=mr))
         assert occ.stats()[2] == int((touched > 0).sum())
         assert same_logodds(occ.download(), L), f"max_range {mr}"
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_integrate_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
+    """Random non-cubic grids (voxel size, origin), sensors inside or outside, random point
+    clouds (Gaussian blobs, uniform, on the Q12 lattice), random leaf / range / probabilities /
+    thresholds, random start store, layout and store kind: log-odds, deltas and the ID map
+    bit-exact vs the oracle over 3 clouds."""
+    rng = np.random.default_rng(2000 + seed)
+    monkeypatch.setenv("NBT_MAP_LAYOUT", "morton" if rng.random() < 0.3 else "linear")
+    store = rng.choice(["2bit", "byte", "prob"])
+    monkeypatch.setenv("NBT_MAP_BITS", "8" if store == "byte" else "2")
+    nx, ny, nz = (int(v) for v in rng.integers(4, 40, 3))
+    s = float(rng.choice([0.02, 0.1, 0.5, 1.0]))
+    origin = tuple(float(v) for v in rng.uniform(-10, 10, 3) * s)
+    ext = np.array([nx, ny, nz], float) * s
+    desc = nbt.map_desc(nx, ny, nz, s, origin)
+    occ = nbt.OccMap(ctx, desc)
+    m = nbt.Map(ctx, desc, prob=store == "prob")
+    kw = dict(leaf=float(rng.choice([0.0, s, 0.5 * s, 2.7 * s])),
+              max_range=float(rng.choice([0.0, 0.3, 1.0]) * ext.max()),
+              p_hit=float(rng.uniform(0.55, 0.95)), p_miss=float(rng.uniform(0.05, 0.45)),
+              p_min=float(rng.uniform(0.05, 0.3)), p_max=float(rng.uniform(0.7, 0.99)))
+    t_occ = float(rng.uniform(0.4, 0.7))
+    t_free = float(min(t_occ, rng.uniform(0.3, 0.5)))
+    L = oracle.new_logodds((nz, ny, nx))
+    prm = nbt.integrate_params(s, **kw, t_occ=t_occ, t_free=t_free)
+    for k in range(3):
+        sensor = np.array(origin) + rng.uniform(-0.2, 1.2, 3) * ext
+        n = int(rng.integers(0, 4000))
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            pts = sensor + rng.normal(0, 0.4, (n, 3)) * ext
+        elif kind == 1:
+            pts = np.array(origin) + rng.uniform(-0.3, 1.3, (n, 3)) * ext
+        else:
+            pts = np.array(origin) + np.round(rng.uniform(-0.3, 1.3, (n, 3)) * ext / s * 2) * s / 2
+        L_before = L.copy()
+        touched, nr = oracle.integrate(L, s, origin, sensor, pts, **kw)
+        occ.integrate(sensor, pts, map=m, params=prm)
+        st = occ.stats()
+        assert st[1] == nr and st[2] == int((touched > 0).sum())
+        assert same_logodds(occ.download(), L), f"cloud {k}"
+        c0, l0 = oracle.occ_classify(L_before, t_occ, t_free)
+        c1, l1 = oracle.occ_classify(L, t_occ, t_free)
+        ch = (touched > 0) & ((c0 != c1) | (l0 != l1))
+        want = {(int(x), int(y), int(z)): (int(c1[z, y, x]), int(l1[z, y, x])) for z, y, x in np.argwhere(ch)}
+        assert device_deltas(occ) == want
+    codes, levels = oracle.occ_classify(L, t_occ, t_free)
+    assert np.array_equal(m.download(), codes)
+    if store == "prob":
+        assert np.array_equal(m.download_levels(), map_levels_expected(codes, levels))

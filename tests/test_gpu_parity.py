@@ -757,3 +757,36 @@ def test_byte_store_config_b_subset(nbt, ctx, monkeypatch):
     P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, 24, seed=cfg.persp_seed, mode=cfg.persp_mode)
     cloud, g, c = run_both(nbt, ctx, m, om, cfg.poi, P, cfg.width, cfg.height, cfg.range_)
     assert_cloud_equal(cloud, P, g, c)
+
+
+# ---------------------------------------------------------------- randomized configurations
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
+    """Random non-cubic maps (random voxel size and origin, random codes or SYN), random
+    PoI and perspectives (some outside the grid), random lattice shape, corners, range,
+    outside policy, gains, layout and state width: the whole ID bit-exact vs the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    monkeypatch.setenv("NBT_MAP_LAYOUT", "morton" if rng.random() < 0.3 else "linear")
+    monkeypatch.setenv("NBT_MAP_BITS", "8" if rng.random() < 0.3 else "2")
+    nx, ny, nz = (int(v) for v in rng.integers(3, 48, 3))
+    s = float(rng.choice([0.01, 0.05, 0.37, 1.0, 2.5]))
+    origin = tuple(float(v) for v in rng.uniform(-20, 20, 3) * s)
+    if rng.random() < 0.5:
+        codes = rand_map(0, *rng.dirichlet([2, 5, 0.5]), seed=seed, shape=(nz, ny, nx))
+    else:
+        n = int(min(nx, ny, nz))
+        codes = syn_map(max(n, 8), max(2.0, n / 6), seed)[:nz, :ny, :nx].copy()
+        codes = np.pad(codes, ((0, nz - codes.shape[0]), (0, ny - codes.shape[1]), (0, nx - codes.shape[2])),
+                       constant_values=1)
+    policy = int(rng.random() < 0.3)
+    gain = tuple(float(v) for v in rng.uniform(0, 1, 3))
+    m, om = make_map(nbt, ctx, codes, voxel_size=s, origin=origin, gain=gain, policy=policy)
+    ext = np.array([nx, ny, nz], float) * s
+    poi = np.array(origin) + rng.uniform(-0.1, 1.1, 3) * ext
+    r_s = float(rng.uniform(0.2, 1.5) * ext.max())
+    P = oracle.sample_perspectives(poi, r_s, int(rng.integers(1, 40)), seed=seed, mode=int(rng.integers(0, 2)))
+    w, h = int(rng.integers(1, 24)), int(rng.integers(1, 18))
+    range_ = float(rng.uniform(0.1, 2.0) * ext.max())
+    cloud, g, c = run_both(nbt, ctx, m, om, poi, P, w, h, range_, corners=bool(rng.random() < 0.4))
+    assert_cloud_equal(cloud, P, g, c)
