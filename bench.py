@@ -654,12 +654,20 @@ def paper_sweep(argv):
     if not args.no_cpu:
         import oracle
         om = oracle.OracleMap(codes, voxel_size=cfg.voxel_size)
+    # bring the GPU to its boost clock before the first point (~0.5 s of work)
+    cam0 = nbt.camera_from_grid_scaling(FOV_H, FOV_V, D_CAM, cfg.voxel_size, s_gs[0])
+    p0 = nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, max(n_ps), 3, 0)
+    o0 = nbt.empty_cloud(max(n_ps))
+    t_end = time.perf_counter() + 0.5
+    while time.perf_counter() < t_end:
+        nbt.id_compute(ctx, m, cfg.poi, p0, cam0, D_CAM, out=o0)
     for s_g in s_gs:
         cam = nbt.camera_from_grid_scaling(FOV_H, FOV_V, D_CAM, cfg.voxel_size, s_g)
         for n_p in n_ps:
             persp = nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_p, 7 + n_p, 0)
             out = nbt.empty_cloud(n_p)
-            nbt.id_compute(ctx, m, cfg.poi, persp, cam, D_CAM, out=out)          # warm-up
+            for _ in range(3):                                                  # warm-up
+                nbt.id_compute(ctx, m, cfg.poi, persp, cam, D_CAM, out=out)
             ts = []
             for _ in range(args.iters):
                 t0 = time.perf_counter()

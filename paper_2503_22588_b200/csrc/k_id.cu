@@ -423,6 +423,43 @@ __device__ __forceinline__ void flush_counts(unsigned long long *totals, int j, 
     c = Counts{0, 0, 0, 0, 0};
 }
 
+// Warp-cooperative flush (all 32 lanes call it): every lane with `fl` set adds its counts
+// to perspective jl's totals and zeroes them; lanes with the same jl are summed first, so
+// each (perspective, counter) takes one atomic per warp.  u, f, o, l are summed in 32 bits
+// (bounded by the perspective's total), the Eq. 2 gain (63x larger) in 64.
+template <bool GAIN>
+__device__ __forceinline__ void flush_counts_warp(unsigned long long *totals, int jl, Counts &c, bool fl, int lane)
+{
+    const unsigned full = 0xffffffffu;
+    unsigned fm = __ballot_sync(full, fl && jl >= 0);
+    while (fm) {
+        const int leader = __ffs(fm) - 1;
+        const int pj = __shfl_sync(full, jl, leader);
+        const bool mine = fl && jl == pj;
+        const unsigned grp = __ballot_sync(full, mine);
+        const uint32_t su = __reduce_add_sync(full, mine ? c.u : 0u);
+        const uint32_t sf = __reduce_add_sync(full, mine ? c.f : 0u);
+        const uint32_t so = __reduce_add_sync(full, mine ? c.o : 0u);
+        const uint32_t sl = __reduce_add_sync(full, mine ? c.l : 0u);
+        unsigned long long sg = 0;
+        if (GAIN) {
+            sg = mine ? (unsigned long long)c.g : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sg += __shfl_xor_sync(full, sg, o);
+        }
+        if (lane == leader) {
+            unsigned long long *t = totals + kTotals * (size_t)pj;
+            if (su) atomicAdd(t + 0, (unsigned long long)su);
+            if (sf) atomicAdd(t + 1, (unsigned long long)sf);
+            if (so) atomicAdd(t + 2, (unsigned long long)so);
+            if (sl) atomicAdd(t + 3, (unsigned long long)sl);
+            if (GAIN && sg) atomicAdd(t + 4, sg);
+        }
+        if (mine) c = Counts{0, 0, 0, 0, 0};
+        fm &= ~grp;
+    }
+}
+
 // Prepare the ray in `slot` of perspective j (frame, segment, DDA set-up, grid
 // entry).  Returns false if the slot is a tile hole or the ray ends without entering
 // the grid (its Unknown visits are then added to the totals directly).
@@ -557,9 +594,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
             if (qcount) {
                 const int rank = __popc(need & lanes_below);
                 const int take = min(__popc(need), qcount);
-                if (!have && rank < take) {
-                    const int j = queue_get<T, L>(Q, qhead + rank, w);
-                    if (j != jl) { flush_counts(A.totals, jl, c); jl = j; }
+                int j = -1;
+                if (!have && rank < take) j = queue_get<T, L>(Q, qhead + rank, w);
+                // lanes moving to another perspective flush their counts, one atomic per
+                // counter per (warp, perspective): many lanes of a warp hold the same one
+                const bool fl = j >= 0 && j != jl;
+                flush_counts_warp<VB == kStoreProb>(A.totals, jl, c, fl, lane);
+                if (j >= 0) {
+                    jl = j;
                     have = true;
                     if (CYCLE) batch_issue<T, L, VB, K>(w, A.m, b0);
                 }
@@ -728,6 +770,19 @@ int trace_carveout()
     return v;
 }
 
+// Smallest chunk (ray slots a warp takes per grab of the global work counter):
+// NBT_CHUNK_MIN, default 64 (a multiple of 32; profiles/r01_chunk_flush.log).
+int chunk_min()
+{
+    static int v = [] {
+        const char *e = getenv("NBT_CHUNK_MIN");
+        int r = e ? atoi(e) : 64;
+        r = (r + 31) / 32 * 32;
+        return r < 32 ? 32 : (r > 1024 ? 1024 : r);
+    }();
+    return v;
+}
+
 // Idle lanes a warp waits for before refilling: NBT_REFILL_MIN, default 8 (profiles/r01_trace_variants.md).
 int refill_threshold()
 {
@@ -833,7 +888,8 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     long long total_slots = (long long)L.n * T.slots;
     long long per = total_slots / (4 * resident_warps);           // aim for >= 4 chunks per warp
     int chunk = (int)((per / 32) * 32);
-    chunk = chunk < 32 ? 32 : (chunk > 1024 ? 1024 : chunk);
+    const int cmin = chunk_min();
+    chunk = chunk < cmin ? cmin : (chunk > 1024 ? 1024 : chunk);
     T.chunk = chunk;
     T.chunks_per_persp = (T.slots + chunk - 1) / chunk;
     long long tc = (long long)T.chunks_per_persp * L.n;
