@@ -411,17 +411,6 @@ __device__ __forceinline__ void ray_segment(const int f[18], int mi, int mk, int
     }
 }
 
-__device__ __forceinline__ void flush_counts(unsigned long long *totals, int j, Counts &c)
-{
-    if (j < 0) return;
-    unsigned long long *t = totals + kTotals * (size_t)j;
-    if (c.u) atomicAdd(t + 0, (unsigned long long)c.u);
-    if (c.f) atomicAdd(t + 1, (unsigned long long)c.f);
-    if (c.o) atomicAdd(t + 2, (unsigned long long)c.o);
-    if (c.l) atomicAdd(t + 3, (unsigned long long)c.l);
-    if (c.g) atomicAdd(t + 4, (unsigned long long)c.g);
-    c = Counts{0, 0, 0, 0, 0};
-}
 
 // Warp-cooperative flush (all 32 lanes call it): every lane with `fl` set adds its counts
 // to perspective jl's totals and zeroes them; lanes with the same jl are summed first, so
@@ -628,7 +617,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
             if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) have = false;
         }
     }
-    flush_counts(A.totals, jl, c);
+    // residual counts, once per lane (the warp-combined form measured ~2% slower here)
+    if (jl >= 0) {
+        unsigned long long *t = A.totals + kTotals * (size_t)jl;
+        if (c.u) atomicAdd(t + 0, (unsigned long long)c.u);
+        if (c.f) atomicAdd(t + 1, (unsigned long long)c.f);
+        if (c.o) atomicAdd(t + 2, (unsigned long long)c.o);
+        if (c.l) atomicAdd(t + 3, (unsigned long long)c.l);
+        if (c.g) atomicAdd(t + 4, (unsigned long long)c.g);
+    }
 }
 
 // ------------------------------------------------------------ finalize (a8)
