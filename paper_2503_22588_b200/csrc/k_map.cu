@@ -81,10 +81,12 @@ __global__ void k_map_classify(const float *__restrict__ p, const uint8_t *__res
     }
 }
 
-// Delta keys: (linear voxel index << 32) | array position; invalid deltas sort last.
+// Delta keys: (linear voxel index << pbits) | array position, in vbits + pbits bits (just
+// enough for nx*ny*nz and n, so the radix sort runs only the passes it needs); invalid
+// deltas get the all-ones key, which sorts last and no valid key reaches.
 __global__ void k_delta_keys(const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes,
-                             const uint8_t *__restrict__ levels, uint32_t n, int nx, int ny, int nz,
-                             unsigned long long *__restrict__ keys, int *err)
+                             const uint8_t *__restrict__ levels, uint32_t n, int nx, int ny, int nz, int pbits,
+                             unsigned long long bad, unsigned long long *__restrict__ keys, int *err)
 {
     uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -92,28 +94,29 @@ __global__ void k_delta_keys(const int32_t *__restrict__ ijk, const uint8_t *__r
     bool ok = x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz && codes[i] <= 2 &&
               (!levels || levels[i] <= 63);
     if (!ok) {
-        keys[i] = ~0ull;
+        keys[i] = bad;
         atomicCAS(err, 0, (int)NBT_ERR_INVALID_ARG);
         return;
     }
     unsigned long long lin = (unsigned long long)x + (unsigned long long)nx * ((unsigned long long)y +
                                                                              (unsigned long long)ny * z);
-    keys[i] = (lin << 32) | i;
+    keys[i] = (lin << pbits) | i;
 }
 
 // After sorting, the last key of each voxel run is the last delta in array order (Q30):
 // only that one writes.  Distinct voxels may share a word, so the field is changed with
 // one atomicXor; the thread's own field is never touched by another thread.
-__global__ void k_delta_apply(const unsigned long long *__restrict__ keys, uint32_t n,
-                              const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes,
-                              const uint8_t *__restrict__ levels, Geom g, uint32_t *words)
+__global__ void k_delta_apply(const unsigned long long *__restrict__ keys, uint32_t n, int pbits,
+                              unsigned long long bad, const int32_t *__restrict__ ijk,
+                              const uint8_t *__restrict__ codes, const uint8_t *__restrict__ levels, Geom g,
+                              uint32_t *words)
 {
     uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     unsigned long long k = keys[i];
-    if (k == ~0ull) return;
-    if (i + 1 < n && (keys[i + 1] >> 32) == (k >> 32)) return;
-    uint32_t pos = (uint32_t)(k & 0xffffffffu);
+    if (k == bad) return;
+    if (i + 1 < n && (keys[i + 1] >> pbits) == (k >> pbits)) return;
+    uint32_t pos = (uint32_t)(k & ((1ull << pbits) - 1));
     uint64_t pi = store_index(g, (uint32_t)ijk[3 * pos], (uint32_t)ijk[3 * pos + 1], (uint32_t)ijk[3 * pos + 2]);
     uint32_t *w = words + word_of(g, pi);
     const uint32_t sh = shift_of(g, pi);
@@ -195,14 +198,19 @@ nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const
     if ((st = ctx->keys_alt.ensure(n * 8))) return st;
     auto *kin = ctx->keys.as<unsigned long long>();
     auto *kout = ctx->keys_alt.as<unsigned long long>();
+    auto bits_for = [](unsigned long long v) { int b = 1; while (b < 64 && (v >> b)) ++b; return b; };
+    const uint64_t nvox = (uint64_t)m->desc.nx * m->desc.ny * m->desc.nz;
+    const int pbits = bits_for(n - 1 > 0 ? n - 1 : 1);
+    const int tbits = bits_for(nvox) + pbits;            // <= 33 + 31: always fits 64
+    const unsigned long long bad = tbits >= 64 ? ~0ull : ((1ull << tbits) - 1);
     k_delta_keys<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(d_ijk, d_codes, d_levels, nn, m->desc.nx, m->desc.ny,
-                                                              m->desc.nz, kin, ctx->d_err);
+                                                              m->desc.nz, pbits, bad, kin, ctx->d_err);
     NBT_LAUNCHED(ctx);
     size_t tmp = 0;
-    NBT_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kin, kout, (int)nn, 0, 64, ctx->stream));
+    NBT_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kin, kout, (int)nn, 0, tbits, ctx->stream));
     if ((st = ctx->cub_tmp.ensure(tmp))) return st;
-    NBT_CUDA(cub::DeviceRadixSort::SortKeys(ctx->cub_tmp.p, tmp, kin, kout, (int)nn, 0, 64, ctx->stream));
-    k_delta_apply<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(kout, nn, d_ijk, d_codes, d_levels, geom_of(m),
+    NBT_CUDA(cub::DeviceRadixSort::SortKeys(ctx->cub_tmp.p, tmp, kin, kout, (int)nn, 0, tbits, ctx->stream));
+    k_delta_apply<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(kout, nn, pbits, bad, d_ijk, d_codes, d_levels, geom_of(m),
                                                                m->d_words);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
