@@ -7,22 +7,25 @@
 // nearest perspective is closer than zero_eps, v_u is its gain (Q23).
 //
 //   k_idw_entry    grid (query blocks) x (entries): a block stages one entry's
-//                  perspectives through shared memory; 8 lanes per query split them
-//                  (interleaved; fp64 partial sums combined by shuffles, so the
-//                  result differs from a sequential sum only in rounding, < 1e-12
-//                  relative).  The nearest perspective is tracked on d^2 (monotone in
-//                  d); only when it is within zero_eps is d = sqrt(d^2) evaluated, with a
-//                  second pass to pick the lowest j among exactly equal d, so the
-//                  zero-distance decision and the returned gain match the definition.
+//                  perspectives through shared memory; each thread holds 4 queries in
+//                  registers and 16 lanes split the perspectives (interleaved; fp64
+//                  partial sums combined by shuffles, so the result differs from a
+//                  sequential sum only in rounding, < 1e-12 relative).  The nearest
+//                  perspective is tracked on d^2 (monotone in d); only when it is within
+//                  zero_eps is d = sqrt(d^2) evaluated and the lowest j among exactly
+//                  equal d found by a rescan, so the zero-distance decision and the
+//                  returned gain match the definition.
 //   k_idw_combine  per query: G = sum_u w_u v_u in entry order (optionally / sum_u w_u).
 #include "nbt_internal.cuh"
 
 namespace nbt {
 namespace {
 
-constexpr int kQueries = 32;     // queries per block
-constexpr int kSplit = 8;        // lanes sharing one (query, entry)
-constexpr int kThreads = kQueries * kSplit;
+constexpr int kQPT = 4;                      // queries per thread (register-blocked)
+constexpr int kSplit = 16;                   // lanes sharing one (query group, entry)
+constexpr int kGroups = 16;                  // query groups per block
+constexpr int kThreads = kGroups * kSplit;   // 256
+constexpr int kQueries = kGroups * kQPT;     // 64 queries per block
 constexpr int kTile = 512;
 
 __device__ __forceinline__ double dist2(double x0, double x1, double x2, double p0, double p1, double p2)
@@ -31,72 +34,84 @@ __device__ __forceinline__ double dist2(double x0, double x1, double x2, double 
     return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
-// Block (query block, entry e): 32 queries x 8 lanes each; the 8 lanes of a query split
-// the entry's perspectives (interleaved), staged through shared memory, and
-// combine (sum of num, sum of den, argmin of d^2 with lowest j) by warp shuffles.
+// Block (query block, entry e): 16 groups of 4 queries x 16 lanes.  The 16 lanes of a
+// group split the entry's perspectives (interleaved), staged through shared memory; every
+// perspective record a lane reads is used for its 4 queries (register blocking: one
+// shared-memory read per 4 pairs), and the groups' partial sums combine by shuffles.
+// Only min d^2 is tracked per query; the rare zero-distance case rescans for the lowest j.
 __global__ void __launch_bounds__(kThreads)
     k_idw_entry(const double *__restrict__ xyz, const double *__restrict__ gain, int32_t max_persp,
                 const int32_t *__restrict__ meta, int32_t cap, const double *__restrict__ q, int32_t n_q,
                 double power_p, double zero_eps, double *__restrict__ v_out)
 {
-    __shared__ double sp[kTile][4];
+    __shared__ double4 sp[kTile];
     const int e = blockIdx.y;
     const int pushes = meta[0];
     const int m = min(pushes, cap);
     if (e >= m) return;
     const int slot = (pushes - m + e) % cap;                  // entry e, oldest first
     const int sub = threadIdx.x & (kSplit - 1);
-    const int qi = blockIdx.x * kQueries + (threadIdx.x / kSplit);
-    const bool active = qi < n_q;
+    const int q0 = blockIdx.x * kQueries + (threadIdx.x / kSplit) * kQPT;
     const double *P = xyz + (size_t)slot * max_persp * 3;
     const double *G = gain + (size_t)slot * max_persp;
     const int np = meta[1 + slot];
-    double x0 = 0.0, x1 = 0.0, x2 = 0.0;
-    if (active) { x0 = q[3 * (size_t)qi]; x1 = q[3 * (size_t)qi + 1]; x2 = q[3 * (size_t)qi + 2]; }
+    double x[kQPT][3];
+#pragma unroll
+    for (int k = 0; k < kQPT; ++k) {
+        const int qi = min(q0 + k, n_q - 1);                  // clamped: inactive queries compute garbage
+        x[k][0] = q[3 * (size_t)qi]; x[k][1] = q[3 * (size_t)qi + 1]; x[k][2] = q[3 * (size_t)qi + 2];
+    }
     const bool p2 = power_p == 2.0;
     const double hp = -0.5 * power_p;
-    double num = 0.0, den = 0.0, d2min = __longlong_as_double(0x7ff0000000000000LL);
-    int jmin = 0x7fffffff;
+    double num[kQPT], den[kQPT], d2min[kQPT];
+#pragma unroll
+    for (int k = 0; k < kQPT; ++k) { num[k] = 0.0; den[k] = 0.0; d2min[k] = __longlong_as_double(0x7ff0000000000000LL); }
     for (int base = 0; base < np; base += kTile) {
         const int nt = min(kTile, np - base);
         __syncthreads();
-        for (int t = threadIdx.x; t < nt; t += kThreads) {
-            sp[t][0] = P[3 * (size_t)(base + t)];
-            sp[t][1] = P[3 * (size_t)(base + t) + 1];
-            sp[t][2] = P[3 * (size_t)(base + t) + 2];
-            sp[t][3] = G[base + t];
-        }
+        for (int t = threadIdx.x; t < nt; t += kThreads)
+            sp[t] = make_double4(P[3 * (size_t)(base + t)], P[3 * (size_t)(base + t) + 1], P[3 * (size_t)(base + t) + 2],
+                                 G[base + t]);
         __syncthreads();
-        // sub-lane s takes t = s, s+8, ...: the 8 lanes of a query read 8 consecutive
-        // 32-byte records (no shared-memory bank conflicts)
-#pragma unroll 4
+#pragma unroll 2
         for (int t = sub; t < nt; t += kSplit) {
-            const double d2 = dist2(x0, x1, x2, sp[t][0], sp[t][1], sp[t][2]);
-            if (d2 < d2min) { d2min = d2; jmin = base + t; }
-            const double w = p2 ? __drcp_rn(d2) : pow(d2, hp);
-            num = fma(sp[t][3], w, num);
-            den += w;
+            const double4 r = sp[t];
+#pragma unroll
+            for (int k = 0; k < kQPT; ++k) {
+                const double d2 = dist2(x[k][0], x[k][1], x[k][2], r.x, r.y, r.z);
+                d2min[k] = fmin(d2min[k], d2);
+                const double w = p2 ? __drcp_rn(d2) : pow(d2, hp);
+                num[k] = fma(r.w, w, num[k]);
+                den[k] += w;
+            }
         }
     }
 #pragma unroll
     for (int off = kSplit / 2; off > 0; off >>= 1) {
-        num += __shfl_xor_sync(0xffffffffu, num, off);
-        den += __shfl_xor_sync(0xffffffffu, den, off);
-        const double od = __shfl_xor_sync(0xffffffffu, d2min, off);
-        const int oj = __shfl_xor_sync(0xffffffffu, jmin, off);
-        if (od < d2min || (od == d2min && oj < jmin)) { d2min = od; jmin = oj; }
-    }
-    if (!active || sub != 0) return;
-    double v = num / den;
-    const double dmin = __dsqrt_rn(d2min);
-    if (dmin < zero_eps) {
-        // nearest by d (not d^2): lowest j among perspectives whose rounded d equals dmin
-        int jbest = jmin;
-        for (int j = 0; j < jmin; ++j) {
-            const double d2 = dist2(x0, x1, x2, P[3 * (size_t)j], P[3 * (size_t)j + 1], P[3 * (size_t)j + 2]);
-            if (__dsqrt_rn(d2) == dmin) { jbest = j; break; }
+#pragma unroll
+        for (int k = 0; k < kQPT; ++k) {
+            num[k] += __shfl_xor_sync(0xffffffffu, num[k], off);
+            den[k] += __shfl_xor_sync(0xffffffffu, den[k], off);
+            d2min[k] = fmin(d2min[k], __shfl_xor_sync(0xffffffffu, d2min[k], off));
         }
-        v = G[jbest];
+    }
+    if (sub >= kQPT) return;
+    // lane k of the group writes query k
+    double nk = num[0], dk = den[0], mk = d2min[0];
+#pragma unroll
+    for (int k = 1; k < kQPT; ++k)
+        if (sub == k) { nk = num[k]; dk = den[k]; mk = d2min[k]; }
+    const int qi = q0 + sub;
+    if (qi >= n_q) return;
+    double v = nk / dk;
+    const double dmin = __dsqrt_rn(mk);
+    if (dmin < zero_eps) {
+        // nearest by d (not d^2): the lowest j whose rounded d equals dmin
+        const double y0 = q[3 * (size_t)qi], y1 = q[3 * (size_t)qi + 1], y2 = q[3 * (size_t)qi + 2];
+        for (int j = 0; j < np; ++j) {
+            const double d2 = dist2(y0, y1, y2, P[3 * (size_t)j], P[3 * (size_t)j + 1], P[3 * (size_t)j + 2]);
+            if (__dsqrt_rn(d2) == dmin) { v = G[j]; break; }
+        }
     }
     v_out[(size_t)e * n_q + qi] = v;
 }
