@@ -11,6 +11,7 @@ on one batch of synthetic input (config B of BASELINE.json: 256^3 SYN map, 1 cm 
   a4-a8  nbt_id_compute -> IG point cloud (frames, rays, exact DDA, scores, means)
        (N > 1: all-gather of the cloud rows over NCCL)
   a9  push the cloud into the N_B = 10 ring buffer and run 1984 IDW queries (Eq. 4)
+       (N > 1: each rank answers a contiguous slice of the queries; all-gather of the values)
 Map construction/upload is excluded.  Weak scaling: every rank computes its own
 512-perspective ID per step; `value` = rays of all ranks / max-over-ranks device time.
 Rank 0 prints one JSON line.  The L2 (126 MB) is flushed with a 256 MiB write before
@@ -358,6 +359,13 @@ def main_ours(args, cfg):
     q_host = query_points(N_QUERIES, cfg.poi, cfg.persp_radius, 0.5, 1.2, seed=5)
     q_dev = torch.from_numpy(q_host).to(dev)
     q_out = torch.empty(N_QUERIES, dtype=torch.float64, device=dev)
+    # the IDW queries are sharded too (contiguous slices, gathered after the query), so the
+    # per-rank IDW work stays constant while the assembled cloud grows with the world size
+    q_rows = (N_QUERIES + world - 1) // world
+    q_lo = min(N_QUERIES, rank * q_rows)
+    q_hi = min(N_QUERIES, q_lo + q_rows)
+    q_mine = q_dev[q_lo:q_hi]
+    q_out_mine = torch.zeros(q_rows, dtype=torch.float64, device=dev)
     n_p = cfg.n_persp
     n_tot = n_p * world
     persp = torch.empty((n_p, 3), dtype=torch.float64, device=dev)
@@ -379,7 +387,14 @@ def main_ours(args, cfg):
 
     def part_b():                       # row a9 on the assembled cloud
         buf.push(gathered, n_tot)
-        buf.query(q_dev, power_p=POWER_P, out=q_out)
+        if world == 1:
+            buf.query(q_dev, power_p=POWER_P, out=q_out)
+        elif q_hi > q_lo:
+            buf.query(q_mine, power_p=POWER_P, out=q_out_mine[:q_hi - q_lo])
+
+    def exchange_queries():
+        if world > 1:
+            q_out.copy_(ndist.all_gather_rows(q_out_mine, N_QUERIES, world, strided=False))
 
     def exchange_deltas(c):
         if world > 1:
@@ -396,6 +411,7 @@ def main_ours(args, cfg):
         part_a(c)
         exchange_cloud()
         part_b()
+        exchange_queries()
 
     for t in range(args.warmup):
         step_eager(t)
@@ -423,6 +439,7 @@ def main_ours(args, cfg):
         graphs_a[c].launch()
         exchange_cloud()
         graph_b.launch()
+        exchange_queries()
 
     # ---- timed region: K steps, device time per step with CUDA events on the ctx stream
     gpu_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid).replace("GPU-", "")
@@ -521,7 +538,13 @@ def main_ours(args, cfg):
             else:
                 full = loc
             buf.push(full, n_tot)
-            buf.query(q_host, power_p=POWER_P, out=q_res)                        # H2D queries, D2H values
+            if world == 1:
+                buf.query(q_host, power_p=POWER_P, out=q_res)                    # H2D queries, D2H values
+            else:
+                mine = np.ascontiguousarray(q_host[q_lo:q_hi])
+                if q_hi > q_lo:
+                    buf.query(mine, power_p=POWER_P, out=q_out_mine[:q_hi - q_lo])
+                q_res[:] = ndist.all_gather_rows(q_out_mine, N_QUERIES, world, strided=False).cpu().numpy()
             return full.gain.cpu().numpy(), full.xyz.cpu().numpy()               # D2H the IG cloud
 
         for s in range(2):
@@ -538,7 +561,7 @@ def main_ours(args, cfg):
             tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
-        h2d = nd * 13 + n_p * 24 + N_QUERIES * 24
+        h2d = nd * 13 + n_p * 24 + (q_hi - q_lo) * 24          # this rank's copies
         d2h = N_QUERIES * 8 + n_tot * 32
         e2e = {"value": args.steps * n_tot * ne / t_e2e, "unit": "rays/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e / args.steps}

@@ -80,6 +80,22 @@ def main():
     assert np.array_equal(gain.cpu().numpy(), np.asarray(full.gain)), "sharded g_P differ"
     assert np.array_equal(counts.cpu().numpy().astype(np.uint64), np.asarray(full.counts).astype(np.uint64))
 
+    # sharded IDW queries over the gathered cloud == all queries on one rank
+    buf = nbt.IdBuffer(ctx, 4, n_p)
+    for _ in range(3):
+        buf.push(nbt.IgCloud(xyz.contiguous(), gain.contiguous(), None), n_p)
+    qs = torch.from_numpy(cfg.poi + np.random.default_rng(5).normal(0, 3.0, (101, 3))).to(dev)
+    rows = (101 + world - 1) // world
+    lo, hi = min(101, rank * rows), min(101, rank * rows + rows)
+    mine = torch.zeros(rows, dtype=torch.float64, device=dev)
+    if hi > lo:
+        buf.query(qs[lo:hi], out=mine[:hi - lo])
+    gathered = ndist.all_gather_rows(mine, 101, world, strided=False)
+    full_q = torch.empty(101, dtype=torch.float64, device=dev)
+    buf.query(qs, out=full_q)
+    ctx.sync()
+    assert torch.equal(gathered, full_q), "sharded IDW queries differ"
+
     # f3: the sensor rank's frame, integrated by every replica
     cf = CLOUD_CONFIGS["F0"]
     fdesc = nbt.map_desc(cf.n, cf.n, cf.n, cf.voxel_size)
