@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-north-star", action="store_true")
     ap.add_argument("--no-integrate", action="store_true", help="skip the row-f3 map-integration block")
+    ap.add_argument("--no-config-d", action="store_true", help="skip the config-D strong-scaling block")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     return ap.parse_args()
@@ -306,6 +307,47 @@ def run_integration(nbt, ctx, stream, dev, flush, reps=2):
     return out
 
 
+def run_config_d(nbt, ndist, ctx, stream, dev, rank, world, reps=3):
+    """Config D (512^3 SYN map, 4096 perspectives x 160x120 rays, range 3.86 m): the whole ID
+    sharded j -> rank j mod G and all-gathered in input order on every rank; device time per
+    ID (CUDA events on the shared stream), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    cd = CONFIGS["D"]
+    m = nbt.Map(ctx, nbt.map_desc(cd.n, cd.n, cd.n, cd.voxel_size))
+    if rank == 0:
+        m.upload(cd.map_codes())
+    if world > 1:
+        ndist.replicate_map(m, src=0)
+    ctx.sync()
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cd.width, cd.height)
+    persp = torch.empty((cd.n_persp, 3), dtype=torch.float64, device=dev)
+    nbt.sample_perspectives(ctx, cd.poi, cd.persp_radius, cd.n_persp, cd.persp_seed, cd.persp_mode, out=persp)
+    ndist.id_compute_sharded(nbt, ctx, m, cd.poi, persp, cam, cd.range_, rank, world)       # warm-up
+    times = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(reps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        xyz, gain, counts = ndist.id_compute_sharded(nbt, ctx, m, cd.poi, persp, cam, cd.range_, rank, world)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times)
+    lookups = float(counts[:, 3].sum().item())
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    m.close()
+    return {"config": f"D: {cd.n}^3 SYN map (2-bit), {cd.n_persp} perspectives x {cd.width}x{cd.height} rays, "
+                      f"range {cd.range_} m, sharded j -> rank j mod {world}, all-gathered",
+            "n_gpus": world, "id_ms": ms, "rays_per_s": cd.rays_per_id / (ms / 1e3),
+            "lookups_per_s": lookups / (ms / 1e3), "reps": reps, "scaling": "strong"}
+
+
 def main_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -510,6 +552,12 @@ def main_ours(args, cfg):
                  "id_latency_ms": ms, "rays_per_s": cn.rays_per_id / (ms / 1e3), "target_ms": 100.0,
                  "steps": len(times)}
 
+    # ---- BASELINE configs[3] / SURVEY 8(d) config D: one 4096-perspective ID on the 512^3 map,
+    #      sharded across the ranks (strong scaling: strided slices + NCCL all-gather of the cloud)
+    strong = None
+    if cfg.name == "B" and not args.no_config_d:
+        strong = run_config_d(nbt, ndist, ctx, stream, dev, rank, world)
+
     # ---- row f3: map integration of depth frames (the step before the path)
     integ = None
     if cfg.name == "B" and not args.no_integrate and rank == 0:
@@ -621,6 +669,7 @@ def main_ours(args, cfg):
                                        f"{f_max / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)"},
             "kernel_share_of_step": shares,
             "north_star": north,
+            "config_d_strong": strong,
             "map_integration": integ,
             "gpu_launches": launches,
             "clocks": clocks_out,
