@@ -26,6 +26,7 @@
 // The apply pass leaves the flags zeroed, so no per-cloud clear is needed.  A poisoned
 // cloud (invalid point, Q12 overflow) updates nothing: the apply pass only clears flags.
 #include <math.h>
+#include <stdlib.h>
 
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -147,6 +148,151 @@ __global__ void __launch_bounds__(256) k_filter_centroid(const double *__restric
             out[3 * (size_t)c + 1] = __ddiv_rn(sy, dn);
             out[3 * (size_t)c + 2] = __ddiv_rn(sz, dn);
             if (out_count) out_count[c] = (int32_t)len;
+        }
+    }
+}
+
+// ------------------------------------------------------- voxel filter by hashing (integration)
+// The integration only needs each cell's centroid, not the cells in key order (the rays are
+// applied as a set, Q35), so it groups points with a hash table instead of a full sort:
+// insert each point's cell key (linear probing, atomicCAS), count per slot, scan the counts,
+// scatter point indices into their slot's segment (arbitrary order), then place each point
+// at its rank among the segment's indices -- the segment holds its points in input order, so
+// the centroid is the same in-order sum as the sort path's, bit for bit.
+
+constexpr unsigned long long kEmptyKey = ~0ull;
+
+// Multiplicative (Fibonacci) hash: the live cells spread over the whole table, so the
+// insertion atomics spread over the L2 slices.
+__device__ __forceinline__ uint32_t hash_slot(unsigned long long key, int log2cap)
+{
+    return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - log2cap));
+}
+
+__global__ void k_hash_insert(const double *__restrict__ pts, uint32_t n, double leaf, int log2cap,
+                              unsigned long long *table, uint32_t *count, uint32_t *__restrict__ slot_of, int *bad,
+                              int *err)
+{
+    const uint32_t mask = (1u << log2cap) - 1u;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        unsigned long long key = 0;
+        bool ok = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double v = pts[3 * (size_t)i + a];
+            const double c = floor(__ddiv_rn(v, leaf));
+            ok = ok && isfinite(v) && fabs(c) < kKeyLimit;
+            if (ok) key |= (unsigned long long)((long long)c + (1ll << 15)) << (16 * a);
+        }
+        if (!ok) {
+            slot_of[i] = 0xffffffffu;
+            atomicExch(bad, 1);
+            atomicCAS(err, 0, (int)NBT_ERR_INVALID_ARG);
+            continue;
+        }
+        // neighbouring pixels share cells: one insertion and one count update per distinct
+        // key among the converged lanes
+        const unsigned am = __activemask();
+        const unsigned peers = __match_any_sync(am, key);
+        const int leader = __ffs(peers) - 1;
+        uint32_t h = 0;
+        if ((int)lane_id() == leader) {
+            h = hash_slot(key, log2cap);
+            for (;;) {
+                const unsigned long long prev = atomicCAS(table + h, kEmptyKey, key);
+                if (prev == kEmptyKey || prev == key) break;
+                h = (h + 1u) & mask;
+            }
+            atomicAdd(count + h, (uint32_t)__popc(peers));
+        }
+        h = __shfl_sync(peers, h, leader);
+        slot_of[i] = h;
+    }
+}
+
+__global__ void k_hash_scatter(const uint32_t *__restrict__ slot_of, uint32_t n, const uint32_t *__restrict__ off,
+                               uint32_t *fill, uint32_t *__restrict__ seg)
+{
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t h = slot_of[i];
+        if (h == 0xffffffffu) continue;
+        seg[off[h] + atomicAdd(fill + h, 1u)] = i;
+    }
+}
+
+// Also flags the first (lowest-index) point of every cell: selecting the slots of those
+// points in index order lists the cells in the order of the depth image's pixels, so the
+// rays reach the ray kernel spatially coherent (its flag atomics depend on that) and in a
+// deterministic order.
+__global__ void k_hash_place(const double *__restrict__ pts, const uint32_t *__restrict__ slot_of, uint32_t n,
+                             const uint32_t *__restrict__ off, const uint32_t *__restrict__ count,
+                             const uint32_t *__restrict__ seg, double *__restrict__ sorted, uint8_t *__restrict__ head)
+{
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t h = slot_of[i];
+        head[i] = 0;
+        if (h == 0xffffffffu) continue;
+        const uint32_t b = off[h], len = count[h];
+        uint32_t rank = 0;
+        for (uint32_t k = 0; k < len; ++k) rank += seg[b + k] < i ? 1u : 0u;
+        head[i] = rank == 0;
+        const size_t d = 3 * (size_t)(b + rank);
+        sorted[d] = pts[3 * (size_t)i];
+        sorted[d + 1] = pts[3 * (size_t)i + 1];
+        sorted[d + 2] = pts[3 * (size_t)i + 2];
+    }
+}
+
+// Cell c = occupied slot cells[c]: run [off, off + count) of the placed points; the same
+// 8-lane in-order sum as k_filter_centroid.
+__global__ void __launch_bounds__(256) k_hash_centroid(const double *__restrict__ sorted,
+                                                       const uint32_t *__restrict__ cells,
+                                                       const uint32_t *__restrict__ n_cells,
+                                                       const uint32_t *__restrict__ off,
+                                                       const uint32_t *__restrict__ count,
+                                                       double *__restrict__ out, uint32_t *__restrict__ n_out)
+{
+    const uint32_t m = *n_cells;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = m;
+    const uint32_t sub = threadIdx.x & (kCentroidLanes - 1);
+    const uint32_t groups = gridDim.x * (blockDim.x / kCentroidLanes);
+    const uint32_t g0 = (blockIdx.x * blockDim.x + threadIdx.x) / kCentroidLanes;
+    const uint32_t warp_g0 = g0 - (lane_id() / kCentroidLanes);
+    for (uint32_t cw = warp_g0; cw < m; cw += groups) {
+        const uint32_t c = cw + lane_id() / kCentroidLanes;
+        const bool live = c < m;
+        const uint32_t h = live ? cells[c] : 0u;
+        const uint32_t b = live ? off[h] : 0u;
+        const uint32_t len = live ? count[h] : 0u;
+        const uint32_t e = b + len;
+        uint32_t rounds = (len + kCentroidLanes - 1) / kCentroidLanes;
+        rounds = __reduce_max_sync(0xffffffffu, rounds);
+        double sx = 0.0, sy = 0.0, sz = 0.0;
+        for (uint32_t r = 0; r < rounds; ++r) {
+            const uint32_t k = b + r * kCentroidLanes + sub;
+            double x = 0.0, y = 0.0, z = 0.0;
+            if (k < e) {
+                x = sorted[3 * (size_t)k];
+                y = sorted[3 * (size_t)k + 1];
+                z = sorted[3 * (size_t)k + 2];
+            }
+#pragma unroll
+            for (int j = 0; j < kCentroidLanes; ++j) {
+                const double xj = __shfl_sync(0xffffffffu, x, j, kCentroidLanes);
+                const double yj = __shfl_sync(0xffffffffu, y, j, kCentroidLanes);
+                const double zj = __shfl_sync(0xffffffffu, z, j, kCentroidLanes);
+                if (r * kCentroidLanes + j < len) {
+                    sx = __dadd_rn(sx, xj);
+                    sy = __dadd_rn(sy, yj);
+                    sz = __dadd_rn(sz, zj);
+                }
+            }
+        }
+        if (live && sub == 0) {
+            const double dn = (double)len;
+            out[3 * (size_t)c] = __ddiv_rn(sx, dn);
+            out[3 * (size_t)c + 1] = __ddiv_rn(sy, dn);
+            out[3 * (size_t)c + 2] = __ddiv_rn(sz, dn);
         }
     }
 }
@@ -467,6 +613,50 @@ nbt_status launch_voxel_filter(nbt_ctx ctx, nbt_occ_s *o, const double *d_pts, u
     return NBT_OK;
 }
 
+// The hashed voxel filter of the integration path: o->filtered = the centroids (cells in
+// hash-slot order), ctl[kOccRays] = their number.
+static nbt_status launch_voxel_filter_hashed(nbt_ctx ctx, nbt_occ_s *o, const double *d_pts, uint32_t n, double leaf)
+{
+    nbt_status st;
+    int log2cap = 10;
+    while ((1ull << log2cap) < 2ull * n) ++log2cap;
+    const size_t cap = 1ull << log2cap;
+    if ((st = o->hkeys.ensure(cap * 8)) || (st = o->hcount.ensure(cap * 12)) ||
+        (st = o->cells.ensure((size_t)n * 5 + 16)) ||
+        (st = o->idx.ensure((size_t)n * 4)) || (st = o->idx_alt.ensure((size_t)n * 4)) ||
+        (st = o->sorted.ensure((size_t)n * 24)) || (st = o->filtered.ensure((size_t)n * 24)))
+        return st;
+    auto *table = o->hkeys.as<unsigned long long>();
+    uint32_t *count = o->hcount.as<uint32_t>(), *fill = count + cap, *off = fill + cap;
+    uint32_t *cells = o->cells.as<uint32_t>(), *n_cells = cells + n;
+    uint8_t *head = reinterpret_cast<uint8_t *>(n_cells + 4);
+    uint32_t *slot_of = o->idx.as<uint32_t>(), *seg = o->idx_alt.as<uint32_t>();
+    uint32_t *ctl = reinterpret_cast<uint32_t *>(o->d_ctl);
+    NBT_CUDA(cudaMemsetAsync(table, 0xff, cap * 8, ctx->stream));
+    NBT_CUDA(cudaMemsetAsync(count, 0, cap * 8, ctx->stream));          // count and fill
+    const unsigned gr = grid_for(ctx, n, 256, 8);
+    k_hash_insert<<<gr, 256, 0, ctx->stream>>>(d_pts, n, leaf, log2cap, table, count, slot_of, o->d_ctl + kOccBad,
+                                               ctx->d_err);
+    NBT_LAUNCHED(ctx);
+    size_t t1 = 0, t2 = 0;
+    NBT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t1, count, off, (int)cap, ctx->stream));
+    NBT_CUDA(cub::DeviceSelect::Flagged(nullptr, t2, slot_of, head, cells, n_cells, (int)n, ctx->stream));
+    const size_t tmp = t1 > t2 ? t1 : t2;
+    if ((st = o->cub_tmp.ensure(tmp))) return st;
+    size_t tt = tmp;
+    NBT_CUDA(cub::DeviceScan::ExclusiveSum(o->cub_tmp.p, tt, count, off, (int)cap, ctx->stream));
+    k_hash_scatter<<<gr, 256, 0, ctx->stream>>>(slot_of, n, off, fill, seg);
+    NBT_LAUNCHED(ctx);
+    k_hash_place<<<gr, 256, 0, ctx->stream>>>(d_pts, slot_of, n, off, count, seg, o->sorted.as<double>(), head);
+    NBT_LAUNCHED(ctx);
+    tt = tmp;
+    NBT_CUDA(cub::DeviceSelect::Flagged(o->cub_tmp.p, tt, slot_of, head, cells, n_cells, (int)n, ctx->stream));
+    k_hash_centroid<<<grid_for(ctx, (size_t)n * kCentroidLanes, 256, 8), 256, 0, ctx->stream>>>(
+        o->sorted.as<double>(), cells, n_cells, off, count, o->filtered.as<double>(), ctl + kOccRays);
+    NBT_LAUNCHED(ctx);
+    return NBT_OK;
+}
+
 nbt_status launch_integrate(nbt_ctx ctx, nbt_occ_s *o, nbt_map m, const double sensor[3], const double *d_pts,
                             uint32_t n, const nbt_integrate_params &p)
 {
@@ -479,7 +669,9 @@ nbt_status launch_integrate(nbt_ctx ctx, nbt_occ_s *o, nbt_map m, const double s
     o->last_points = n;
     o->last_filtered = p.leaf > 0.0;
     if (p.leaf > 0.0 && n > 0) {
-        if ((st = launch_voxel_filter(ctx, o, d_pts, n, p.leaf, nullptr))) return st;
+        st = getenv("NBT_FILTER_SORT") ? launch_voxel_filter(ctx, o, d_pts, n, p.leaf, nullptr)
+                                       : launch_voxel_filter_hashed(ctx, o, d_pts, n, p.leaf);
+        if (st) return st;
         rays = o->filtered.as<double>();
         n_rays_dev = reinterpret_cast<const uint32_t *>(o->d_ctl + kOccRays);
     }

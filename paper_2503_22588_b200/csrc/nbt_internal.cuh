@@ -196,6 +196,7 @@ struct nbt_occ_s {
     bool last_filtered = false;
     nbt::DevBuf pts;                  // staged host points
     nbt::DevBuf keys, keys_alt, idx, idx_alt, runs, sorted, filtered, cub_tmp;
+    nbt::DevBuf hkeys, hcount, cells;  // hashed voxel filter (integration path)
 };
 
 // ------------------------------------------------------------- kernel API

@@ -753,7 +753,7 @@ static void occ_free(nbt_occ_s *o)
                     (void *)o->d_ctl})
         if (q) cudaFree(q);
     for (DevBuf *b : {&o->pts, &o->keys, &o->keys_alt, &o->idx, &o->idx_alt, &o->runs, &o->sorted, &o->filtered,
-                      &o->cub_tmp})
+                      &o->cub_tmp, &o->hkeys, &o->hcount, &o->cells})
         b->release();
 }
 
