@@ -300,3 +300,11 @@ def test_integrate_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
     assert np.array_equal(m.download(), codes)
     if store == "prob":
         assert np.array_equal(m.download_levels(), map_levels_expected(codes, levels))
+
+
+def test_integrate_sorted_filter_path_matches(nbt, ctx, monkeypatch):
+    """The sort-based voxel filter (NBT_FILTER_SORT=1, the experiment knob) integrates to the
+    same store as the default hashed grouping (both bit-exact vs the oracle)."""
+    monkeypatch.setenv("NBT_FILTER_SORT", "1")
+    cf = I.CLOUD_CONFIGS["F0"]
+    _run_sequence(nbt, ctx, cf, 2, True, "linear", monkeypatch)
