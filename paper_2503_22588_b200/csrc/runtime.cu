@@ -94,6 +94,14 @@ static nbt_status stage_h2d(nbt_ctx ctx, HostStage &st, DevBuf &dst, const void 
     nbt_status s;
     if ((s = dst.ensure(bytes))) return s;
     if (bytes == 0) return NBT_OK;
+    static const int mode = [] {
+        const char *e = getenv("NBT_H2D_MODE");
+        return e ? atoi(e) : 0;
+    }();
+    if (mode == 1) {   // experiment: let the driver stage the pageable source
+        NBT_CUDA(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        return NBT_OK;
+    }
     if ((s = st.acquire(bytes))) return s;
     memcpy(st.p, src, bytes);
     NBT_CUDA(cudaMemcpyAsync(dst.p, st.p, bytes, cudaMemcpyHostToDevice, ctx->stream));
