@@ -13,6 +13,8 @@
 // reading Q32), 4 voxels per word: bits 0-1 the state, bits 2-7 the voxel's Eq. 2 gain in
 // units of 1/63 -- 63 for Unknown, level for Free (P = level/63), 63 - level for
 // Occupied -- so the walk reads the gain with one shift.
+#include <stdlib.h>
+
 #include <cub/cub.cuh>
 
 #include "nbt_internal.cuh"
@@ -127,6 +129,48 @@ __global__ void k_delta_apply(const unsigned long long *__restrict__ keys, uint3
     if (old != nw) atomicXor(w, (old ^ nw) << sh);
 }
 
+// Winner-array form of the delta update (no sort): every valid delta i raises its voxel's
+// winner slot to i + 1 (atomicMax), so the slot ends at the LAST delta in array order (Q30);
+// the winner then writes the field and clears the slot (a loser that reads the slot after
+// the clear sees 0, never its own i + 1), leaving the array zeroed for the next update.
+__global__ void k_delta_win(const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes,
+                            const uint8_t *__restrict__ levels, uint32_t n, int nx, int ny, int nz, uint32_t *win,
+                            int *err)
+{
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int x = ijk[3 * i], y = ijk[3 * i + 1], z = ijk[3 * i + 2];
+    const bool ok = x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz && codes[i] <= 2 &&
+                    (!levels || levels[i] <= 63);
+    if (!ok) {
+        atomicCAS(err, 0, (int)NBT_ERR_INVALID_ARG);
+        return;
+    }
+    const uint32_t lin = (uint32_t)x + (uint32_t)nx * ((uint32_t)y + (uint32_t)ny * (uint32_t)z);
+    atomicMax(win + lin, i + 1u);
+}
+
+__global__ void k_delta_apply_win(const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes,
+                                  const uint8_t *__restrict__ levels, uint32_t n, Geom g, uint32_t *win,
+                                  uint32_t *words)
+{
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int x = ijk[3 * i], y = ijk[3 * i + 1], z = ijk[3 * i + 2];
+    if (x < 0 || y < 0 || z < 0 || x >= g.nx || y >= g.ny || z >= g.nz) return;
+    const uint32_t lin = (uint32_t)x + (uint32_t)g.nx * ((uint32_t)y + (uint32_t)g.ny * (uint32_t)z);
+    if (win[lin] != i + 1u) return;                     // a later delta of this voxel wins
+    win[lin] = 0u;
+    const uint64_t pi = store_index(g, (uint32_t)x, (uint32_t)y, (uint32_t)z);
+    uint32_t *w = words + word_of(g, pi);
+    const uint32_t sh = shift_of(g, pi);
+    const uint32_t mask = g.vbits == 2 ? 3u : 0xffu;
+    const uint32_t c = codes[i];
+    const uint32_t nw = stored_value(g, c, levels ? levels[i] : g.def_level[c]);
+    const uint32_t old = (*(volatile uint32_t *)w >> sh) & mask;
+    if (old != nw) atomicXor(w, (old ^ nw) << sh);
+}
+
 // Dense codes (and, for the 8-bit store, the probability levels) of the grid.
 __global__ void k_map_unpack(const uint32_t *__restrict__ words, Geom g, uint8_t *__restrict__ codes,
                              uint8_t *__restrict__ levels)
@@ -194,12 +238,34 @@ nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const
     uint32_t nn = (uint32_t)n;
     ProfScope ps(ctx, NBT_KERNEL_MAP_UPDATE);
     nbt_status st;
+    const uint64_t nvox = (uint64_t)m->desc.nx * m->desc.ny * m->desc.nz;
+    // the winner array (4 B per voxel, zero between updates) is allocated on the first update
+    // outside a graph capture; without it the sort form below is used
+    if (!m->d_win && !g_capturing && !getenv("NBT_DELTA_SORT")) {
+        if (cudaMalloc(&m->d_win, nvox * 4) == cudaSuccess) {
+            if (cudaMemsetAsync(m->d_win, 0, nvox * 4, ctx->stream) != cudaSuccess) {
+                cudaFree(m->d_win);
+                m->d_win = nullptr;
+            }
+        } else {
+            m->d_win = nullptr;
+            cudaGetLastError();
+        }
+    }
+    if (m->d_win) {
+        k_delta_win<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(d_ijk, d_codes, d_levels, nn, m->desc.nx,
+                                                                 m->desc.ny, m->desc.nz, m->d_win, ctx->d_err);
+        NBT_LAUNCHED(ctx);
+        k_delta_apply_win<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(d_ijk, d_codes, d_levels, nn, geom_of(m),
+                                                                       m->d_win, m->d_words);
+        NBT_LAUNCHED(ctx);
+        return NBT_OK;
+    }
     if ((st = ctx->keys.ensure(n * 8))) return st;
     if ((st = ctx->keys_alt.ensure(n * 8))) return st;
     auto *kin = ctx->keys.as<unsigned long long>();
     auto *kout = ctx->keys_alt.as<unsigned long long>();
     auto bits_for = [](unsigned long long v) { int b = 1; while (b < 64 && (v >> b)) ++b; return b; };
-    const uint64_t nvox = (uint64_t)m->desc.nx * m->desc.ny * m->desc.nz;
     const int pbits = bits_for(n - 1 > 0 ? n - 1 : 1);
     const int tbits = bits_for(nvox) + pbits;            // <= 33 + 31: always fits 64
     const unsigned long long bad = tbits >= 64 ? ~0ull : ((1ull << tbits) - 1);

@@ -171,6 +171,7 @@ struct nbt_map_s {
     uint64_t nvox_pad = 0;
     size_t nwords = 0;
     uint32_t *d_words = nullptr;      // 2-bit codes, 16 voxels per 32-bit word
+    uint32_t *d_win = nullptr;        // delta winner per voxel (k_map.cu), lazily allocated
 };
 
 struct nbt_idbuf_s {

@@ -738,6 +738,7 @@ void nbt_map_destroy(nbt_map m)
     cudaSetDevice(m->ctx->device);
     cudaStreamSynchronize(m->ctx->stream);
     if (m->d_words) cudaFree(m->d_words);
+    if (m->d_win) cudaFree(m->d_win);
     nbt_ctx ctx = m->ctx;
     delete m;
     ctx_release(ctx);

@@ -98,22 +98,29 @@ def _apply_in_order(codes, ijk, vals):
     return out
 
 
+@pytest.mark.parametrize("form", ["winner", "sort"])
 @pytest.mark.parametrize("on_device", [False, True])
-def test_map_update_last_wins(nbt, ctx, on_device):
+def test_map_update_last_wins(nbt, ctx, on_device, form, monkeypatch):
+    """Duplicated voxels resolve to the last delta (Q30), in both update forms (the
+    winner array, and the radix sort used when the array is absent), over repeated updates."""
     import torch
+    if form == "sort":
+        monkeypatch.setenv("NBT_DELTA_SORT", "1")
     codes = rand_map(0, seed=5, shape=(13, 17, 19))
     m, _ = make_map(nbt, ctx, codes)
     rng = np.random.default_rng(2)
-    n = 5000
-    ijk = np.stack([rng.integers(0, 19, n), rng.integers(0, 17, n), rng.integers(0, 13, n)], 1).astype(np.int32)
-    ijk[n // 2:] = ijk[: n - n // 2]                  # many duplicates
-    vals = rng.integers(0, 3, n).astype(np.uint8)
-    if on_device:
-        m.update(torch.from_numpy(ijk).cuda(), torch.from_numpy(vals).cuda())
-    else:
-        m.update(ijk, vals)
-    ctx.sync()
-    assert np.array_equal(m.download(), _apply_in_order(codes, ijk, vals))
+    for rep in range(3):
+        n = 5000
+        ijk = np.stack([rng.integers(0, 19, n), rng.integers(0, 17, n), rng.integers(0, 13, n)], 1).astype(np.int32)
+        ijk[n // 2:] = ijk[: n - n // 2]                  # many duplicates
+        vals = rng.integers(0, 3, n).astype(np.uint8)
+        if on_device:
+            m.update(torch.from_numpy(ijk).cuda(), torch.from_numpy(vals).cuda())
+        else:
+            m.update(ijk, vals)
+        ctx.sync()
+        codes = _apply_in_order(codes, ijk, vals)
+        assert np.array_equal(m.download(), codes)
 
 
 def test_map_update_validation(nbt, ctx):
