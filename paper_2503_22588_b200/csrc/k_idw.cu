@@ -18,6 +18,10 @@
 //   k_idw_combine  per query: G = sum_u w_u v_u in entry order (optionally / sum_u w_u).
 #include "nbt_internal.cuh"
 
+#ifndef NBT_IDW_EXACT_RCP
+#define NBT_IDW_EXACT_RCP 0
+#endif
+
 namespace nbt {
 namespace {
 
@@ -27,6 +31,23 @@ constexpr int kGroups = 16;                  // query groups per block
 constexpr int kThreads = kGroups * kSplit;   // 256
 constexpr int kQueries = kGroups * kQPT;     // 64 queries per block
 constexpr int kTile = 512;
+
+// 1/x to within an ulp: the hardware approximation refined by two Newton steps (the IEEE
+// correctly-rounded __drcp_rn costs a longer sequence; IDW sums are compared with 1e-12
+// relative tolerance, the zero-distance rule does not use it).  x = 0 gives +inf.
+__device__ __forceinline__ double rcp_nr(double x)
+{
+#if NBT_IDW_EXACT_RCP
+    return __drcp_rn(x);
+#else
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+#endif
+}
 
 __device__ __forceinline__ double dist2(double x0, double x1, double x2, double p0, double p1, double p2)
 {
@@ -80,7 +101,7 @@ __global__ void __launch_bounds__(kThreads)
             for (int k = 0; k < kQPT; ++k) {
                 const double d2 = dist2(x[k][0], x[k][1], x[k][2], r.x, r.y, r.z);
                 d2min[k] = fmin(d2min[k], d2);
-                const double w = p2 ? __drcp_rn(d2) : pow(d2, hp);
+                const double w = p2 ? rcp_nr(d2) : pow(d2, hp);
                 num[k] = fma(r.w, w, num[k]);
                 den[k] += w;
             }
