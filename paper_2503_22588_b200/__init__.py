@@ -187,6 +187,13 @@ def _ptr(x, dtype):
     return C.c_void_p(a.ctypes.data), 0, a
 
 
+def _count(keep) -> int:
+    """Number of elements of the array / tensor _ptr returned (0 for None)."""
+    if keep is None:
+        return 0
+    return int(keep.numel()) if _is_torch(keep) else int(keep.size)
+
+
 def _poi(poi):
     a = np.ascontiguousarray(poi, dtype=np.float64).reshape(3)
     return C.c_void_p(a.ctypes.data), a
@@ -304,21 +311,25 @@ class Map:
 
     def upload(self, codes):
         p, dev, keep = _ptr(codes, np.uint8)
-        check(lib().nbt_map_upload(self.h, p, self.nvox, dev))
+        check(lib().nbt_map_upload(self.h, p, _count(keep), dev))      # the C side checks n == nx*ny*nz
 
     def upload_prob(self, p, observed, t_occ=0.5, t_free=0.5):
         pp, dev, k1 = _ptr(p, np.float32)
         po, dev2, k2 = _ptr(observed, np.uint8)
         if dev != dev2:
             raise ValueError("p and observed must both be host or both device")
-        check(lib().nbt_map_upload_prob(self.h, pp, po, self.nvox, dev, float(t_occ), float(t_free)))
+        if _count(k1) != _count(k2):
+            raise ValueError("p and observed differ in size")
+        check(lib().nbt_map_upload_prob(self.h, pp, po, _count(k1), dev, float(t_occ), float(t_free)))
 
     def update(self, ijk, codes):
         pi, dev, k1 = _ptr(ijk, np.int32)
         pc, dev2, k2 = _ptr(codes, np.uint8)
         if dev != dev2:
             raise ValueError("ijk and codes must both be host or both device")
-        n = (k2.numel() if _is_torch(k2) else k2.size) if k2 is not None else 0
+        n = _count(k2)
+        if _count(k1) != 3 * n:
+            raise ValueError("ijk must hold 3 ints per delta")
         check(lib().nbt_map_update(self.h, pi, pc, n, dev))
 
     def update_prob(self, ijk, p, observed, t_occ=0.5, t_free=0.5):
@@ -327,7 +338,9 @@ class Map:
         po, dev3, k3 = _ptr(observed, np.uint8)
         if not dev == dev2 == dev3:
             raise ValueError("ijk, p and observed must all be host or all device")
-        n = (k2.numel() if _is_torch(k2) else k2.size) if k2 is not None else 0
+        n = _count(k2)
+        if _count(k1) != 3 * n or _count(k3) != n:
+            raise ValueError("ijk (3 per delta), p and observed differ in size")
         check(lib().nbt_map_update_prob(self.h, pi, pp, po, n, dev, float(t_occ), float(t_free)))
 
     def download_levels(self):
@@ -386,7 +399,7 @@ class OccMap:
 
     def upload(self, logodds):
         p, dev, keep = _ptr(logodds, np.float32)
-        check(lib().nbt_occ_upload(self.h, p, self.nvox, dev))
+        check(lib().nbt_occ_upload(self.h, p, _count(keep), dev))
 
     def download(self):
         out = np.empty(self.shape, np.float32)
@@ -460,6 +473,8 @@ def sample_perspectives(ctx: Ctx, poi, r_s, n, seed, mode=SAMPLE_BALL, out=None)
     if out is None:
         out = np.empty((n, 3), np.float64)
     po, dev, k = _ptr(out, np.float64)
+    if _count(k) < 3 * int(n):
+        raise ValueError("out holds fewer than 3 n values")
     check(lib().nbt_sample_perspectives(ctx.h, pp, float(r_s), int(n), int(seed) & (2 ** 64 - 1), int(mode), po, dev))
     return out
 
@@ -472,8 +487,12 @@ class IgCloud:
 
     def as_c(self):
         px, dev, _ = _ptr(self.xyz, np.float64)
-        pg, _, _ = _ptr(self.gain, np.float64)
-        pc = _ptr(self.counts, np.uint64)[0] if self.counts is not None else None
+        pg, dev2, _ = _ptr(self.gain, np.float64)
+        pc, dev3 = None, dev
+        if self.counts is not None:
+            pc, dev3, _ = _ptr(self.counts, np.uint64)
+        if not dev == dev2 == dev3:
+            raise ValueError("the cloud's buffers must all be host arrays or all CUDA tensors")
         return IgCloudC(px.value, pg.value, pc.value if pc is not None else None, dev)
 
 
@@ -486,16 +505,32 @@ def empty_cloud(n, device=None, counts=True):
                    torch.empty((n, 4), dtype=torch.int64, device=device) if counts else None)
 
 
+def _check_cloud(cloud, n):
+    """The caller-owned output buffers of a cloud hold at least n rows."""
+    need = (("xyz", 3 * n), ("gain", n), ("counts", 4 * n))
+    for name, k in need:
+        buf = getattr(cloud, name)
+        if buf is None:
+            if name == "counts":
+                continue
+            raise ValueError(f"cloud.{name} is missing")
+        if _count(buf) < k:
+            raise ValueError(f"cloud.{name} holds {_count(buf)} values, {k} needed")
+
+
 def nbt_id_compute(ctx: Ctx, m: Map, poi, persp, cam: Camera, range_, out: IgCloud | None = None,
                    first=0, stride=1):
     """The ID (rows a4-a8).  persp: (n,3) float64 numpy (host) or CUDA tensor.  With first/stride
     only rows first + i*stride are computed and written compactly (multi-GPU shards)."""
     pp, keep = _poi(poi)
     pper, dev, kp = _ptr(persp, np.float64)
-    n_src = (kp.shape[0] if kp is not None else 0)
+    if _count(kp) % 3:
+        raise ValueError("perspectives must be (n, 3) float64")
+    n_src = _count(kp) // 3
     n = max(0, (n_src - first + stride - 1) // stride) if first < n_src else 0
     if out is None:
         out = empty_cloud(n)
+    _check_cloud(out, n)
     oc = out.as_c()
     if (first, stride) == (0, 1):
         check(lib().nbt_id_compute(ctx.h, m.h, pp, pper, int(n_src), dev, C.byref(cam), float(range_), C.byref(oc)))
@@ -517,8 +552,9 @@ class IdBuffer:
         self.h, self.ctx = h, ctx
 
     def push(self, cloud: IgCloud, n=None):
+        n = n if n is not None else _count(cloud.gain)
+        _check_cloud(IgCloud(cloud.xyz, cloud.gain, None), int(n))
         oc = cloud.as_c()
-        n = n if n is not None else (cloud.gain.shape[0])
         check(lib().nbt_idbuf_push(self.h, C.byref(oc), int(n)))
 
     def clear(self):
@@ -529,10 +565,14 @@ class IdBuffer:
 
     def query(self, xyz, power_p=2.0, zero_eps=1e-9, normalize=False, out=None):
         pq, qdev, kq = _ptr(xyz, np.float64)
-        nq = kq.shape[0] if kq is not None else 0
+        if _count(kq) % 3:
+            raise ValueError("queries must be (n, 3) float64")
+        nq = _count(kq) // 3
         if out is None:
             out = np.empty(nq, np.float64)
-        po, odev, _ = _ptr(out, np.float64)
+        po, odev, ko = _ptr(out, np.float64)
+        if _count(ko) < nq:
+            raise ValueError("out holds fewer values than queries")
         check(lib().nbt_ig_query(self.h, pq, int(nq), qdev, float(power_p), float(zero_eps), int(bool(normalize)),
                                  po, odev))
         return out
@@ -544,13 +584,17 @@ class IdBuffer:
         pa, adev, ka = _ptr(axis, np.float64)
         if pdev != adev:
             raise ValueError("pos and axis must both be host or both device")
-        n = kp.shape[0] if kp is not None else 0
+        if _count(kp) % 3 or _count(ka) != _count(kp):
+            raise ValueError("pos and axis must both be (n, 3) float64")
+        n = _count(kp) // 3
         n_traj = n // int(poses_per_traj)
         if out is None:
             out = (np.empty(n), np.empty(n), np.empty(n_traj))
-        po, odev, _ = _ptr(out[0], np.float64)
-        pg, _, _ = _ptr(out[1], np.float64)
-        pc, _, _ = _ptr(out[2], np.float64)
+        po, odev, k0 = _ptr(out[0], np.float64)
+        pg, _, k1 = _ptr(out[1], np.float64)
+        pc, _, k2 = _ptr(out[2], np.float64)
+        if _count(k0) < n or _count(k1) < n or _count(k2) < n_traj:
+            raise ValueError("out buffers too small")
         ppoi, keep = _poi(poi)
         check(lib().nbt_info_cost(self.h, pp, pa, int(n_traj), int(poses_per_traj), pdev, ppoi, float(cos_theta_cut),
                                   float(w_i), float(eps), float(power_p), float(zero_eps), int(bool(normalize)),
@@ -577,6 +621,8 @@ def debug_trace(ctx: Ctx, m: Map, o_q16, e_q16, max_visits=1024):
     """Per-ray device walks of explicit Q16 segments: (ijk [n,max,3], codes [n,max], len [n], counts [n,4])."""
     o = np.ascontiguousarray(o_q16, dtype=np.int32).reshape(-1, 3)
     e = np.ascontiguousarray(e_q16, dtype=np.int32).reshape(-1, 3)
+    if o.shape != e.shape:
+        raise ValueError("o and e must hold the same number of segments")
     n = o.shape[0]
     ijk = np.zeros((n, max_visits, 3), np.int32)
     codes = np.zeros((n, max_visits), np.uint8)

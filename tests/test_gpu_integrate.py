@@ -308,3 +308,70 @@ def test_integrate_sorted_filter_path_matches(nbt, ctx, monkeypatch):
     monkeypatch.setenv("NBT_FILTER_SORT", "1")
     cf = I.CLOUD_CONFIGS["F0"]
     _run_sequence(nbt, ctx, cf, 2, True, "linear", monkeypatch)
+
+
+def test_integrate_captured_in_a_graph(nbt, ctx):
+    """Map integration of device-resident frames captured once into a CUDA graph and replayed
+    with new frame contents (same size, same sensor pose): bit-exact vs the oracle."""
+    import torch
+    cf = I.CLOUD_CONFIGS["F0"]
+    desc = nbt.map_desc(cf.n, cf.n, cf.n, cf.voxel_size)
+    gctx = nbt.Ctx(0)
+    occ = nbt.OccMap(gctx, desc)
+    m = nbt.Map(gctx, desc)
+    prm = nbt.integrate_params(cf.voxel_size, leaf=cf.leaf, max_range=cf.max_range)
+    sensor = cf.sensor(0)
+    clouds = [cf.cloud(k) for k in range(3)]
+    n = min(len(c) for c in clouds)
+    dev_pts = torch.from_numpy(np.ascontiguousarray(clouds[0][:n])).cuda()
+    L = oracle.new_logodds((cf.n,) * 3)
+    oracle.integrate(L, cf.voxel_size, (0, 0, 0), sensor, clouds[0][:n], leaf=cf.leaf, max_range=cf.max_range)
+    occ.integrate(sensor, dev_pts, map=m, params=prm)          # warm-up: scratch buffers grow
+    gctx.sync()
+    gctx.capture_begin()
+    occ.integrate(sensor, dev_pts, map=m, params=prm)
+    g = gctx.capture_end()
+    for k in (1, 2):
+        dev_pts.copy_(torch.from_numpy(np.ascontiguousarray(clouds[k][:n])))
+        torch.cuda.synchronize()
+        g.launch()
+        gctx.sync()
+        oracle.integrate(L, cf.voxel_size, (0, 0, 0), sensor, clouds[k][:n], leaf=cf.leaf, max_range=cf.max_range)
+        assert same_logodds(occ.download(), L), f"replay {k}"
+    codes, _ = oracle.occ_classify(L)
+    assert np.array_equal(m.download(), codes)
+    g.close(); occ.close(); m.close(); gctx.close()
+
+
+def test_integrate_api_misuse(nbt, ctx):
+    """Errors are reported, not crashed on: a map of another grid, wrong sizes, bad
+    parameters, host input during capture, counters during capture."""
+    cf = I.CLOUD_CONFIGS["F0"]
+    occ = nbt.OccMap(ctx, nbt.map_desc(cf.n, cf.n, cf.n, cf.voxel_size))
+    other = nbt.Map(ctx, nbt.map_desc(cf.n + 1, cf.n, cf.n, cf.voxel_size))
+    pts = cf.cloud(0)[:1000]
+    with pytest.raises(nbt.NbtError) as ei:
+        occ.integrate(cf.sensor(0), pts, map=other)
+    assert ei.value.status == nbt.ERR_STATE
+    with pytest.raises(nbt.NbtError):
+        occ.upload(np.zeros(10, np.float32))
+    with pytest.raises(nbt.NbtError):
+        occ.integrate(cf.sensor(0), pts, params=nbt.integrate_params(cf.voxel_size, p_hit=1.0))
+    with pytest.raises(nbt.NbtError):
+        occ.integrate(cf.sensor(0), pts, params=nbt.integrate_params(cf.voxel_size, leaf=-1.0))
+    with pytest.raises(nbt.NbtError):
+        occ.integrate((np.nan, 0.0, 0.0), pts)
+    with pytest.raises(nbt.NbtError):
+        nbt.voxel_filter(ctx, pts, 0.0)
+    gctx = nbt.Ctx(0)
+    occ2 = nbt.OccMap(gctx, nbt.map_desc(cf.n, cf.n, cf.n, cf.voxel_size))
+    gctx.capture_begin()
+    with pytest.raises(nbt.NbtError) as ei:
+        occ2.integrate(cf.sensor(0), pts)                       # host points while capturing
+    assert ei.value.status == nbt.ERR_STATE
+    with pytest.raises(nbt.NbtError):
+        occ2.stats()
+    gctx.capture_end().close()
+    occ.integrate(cf.sensor(0), pts)                            # the original store still works
+    assert occ.stats()[0] == 1000
+    occ2.close(); gctx.close()

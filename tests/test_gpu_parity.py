@@ -797,3 +797,32 @@ def test_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
     range_ = float(rng.uniform(0.1, 2.0) * ext.max())
     cloud, g, c = run_both(nbt, ctx, m, om, poi, P, w, h, range_, corners=bool(rng.random() < 0.4))
     assert_cloud_equal(cloud, P, g, c)
+
+
+def test_binding_rejects_mismatched_buffers(nbt, ctx):
+    """The binding checks buffer sizes before the C call (no host or device overrun)."""
+    import torch
+    m, _ = make_map(nbt, ctx, rand_map(0, seed=1, shape=(5, 6, 7)))
+    with pytest.raises((nbt.NbtError, ValueError)):
+        m.upload(np.zeros(10, np.uint8))
+    with pytest.raises(ValueError):
+        m.update(np.zeros((3, 3), np.int32), np.zeros(4, np.uint8))
+    poi = np.array([3.5, 3.0, 2.5])
+    P = np.array([[1.0, 1.0, 1.0], [6.0, 5.0, 4.0]])
+    cam = nbt.camera_from_fov(1.0, 1.0, 4, 4)
+    with pytest.raises(ValueError):
+        nbt.id_compute(ctx, m, poi, P, cam, 5.0, out=nbt.empty_cloud(1))
+    with pytest.raises(ValueError):
+        nbt.id_compute(ctx, m, poi, P.ravel()[:5], cam, 5.0)
+    buf = nbt.IdBuffer(ctx, 2, 4)
+    cloud = nbt.id_compute(ctx, m, poi, P, cam, 5.0)
+    with pytest.raises(ValueError):
+        buf.push(cloud, 3)
+    with pytest.raises(ValueError):
+        mixed = nbt.IgCloud(torch.from_numpy(cloud.xyz).cuda(), cloud.gain, None)
+        buf.push(mixed)
+    buf.push(cloud)
+    with pytest.raises(ValueError):
+        buf.query(np.zeros((4, 3)), out=np.zeros(2))
+    with pytest.raises(ValueError):
+        nbt.sample_perspectives(ctx, poi, 1.0, 10, 3, out=np.zeros((5, 3)))
