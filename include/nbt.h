@@ -92,6 +92,10 @@ enum {
     NBT_KERNEL_COUNT = 7
 };
 nbt_status nbt_ctx_set_profiling(nbt_ctx ctx, int enable);
+/* Record only the kernel families whose bit (1 << NBT_KERNEL_*) is set (0 = off).  Inside a
+ * graph every recorded family adds two event nodes (~2 us each on B200), so a timed graph
+ * should record no more than the families it reports. */
+nbt_status nbt_ctx_set_profiling_mask(nbt_ctx ctx, uint32_t kernel_mask);
 /* Sum of the recorded durations (ms) and number of launches of `kernel` since the last
  * reset; synchronizes the stream.  reset != 0 clears the record. */
 nbt_status nbt_ctx_profile_read(nbt_ctx ctx, int32_t kernel, double *total_ms, uint64_t *launches, int reset);

@@ -33,7 +33,7 @@ SAMPLE_BALL, SAMPLE_SURFACE = 0, 1
 EXPORTS = [
     "nbt_abi_version", "nbt_status_string", "nbt_last_error_message",
     "nbt_ctx_create", "nbt_ctx_set_stream", "nbt_ctx_sync", "nbt_ctx_destroy", "nbt_ctx_launch_count",
-    "nbt_ctx_set_profiling", "nbt_ctx_profile_read",
+    "nbt_ctx_set_profiling", "nbt_ctx_set_profiling_mask", "nbt_ctx_profile_read",
     "nbt_ctx_capture_begin", "nbt_ctx_capture_end", "nbt_graph_launch", "nbt_graph_profile_read", "nbt_graph_destroy",
     "nbt_map_desc_default", "nbt_map_create", "nbt_map_create_prob", "nbt_map_upload", "nbt_map_upload_prob",
     "nbt_map_update", "nbt_map_update_prob", "nbt_map_device_buffer", "nbt_map_download", "nbt_map_download_levels",
@@ -101,6 +101,7 @@ def lib():
         "nbt_ctx_destroy": ([vp], None),
         "nbt_ctx_launch_count": ([vp], u64),
         "nbt_ctx_set_profiling": ([vp, C.c_int], C.c_int),
+        "nbt_ctx_set_profiling_mask": ([vp, C.c_uint32], C.c_int),
         "nbt_ctx_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(u64), C.c_int], C.c_int),
         "nbt_ctx_capture_begin": ([vp], C.c_int),
         "nbt_ctx_capture_end": ([vp, C.POINTER(vp)], C.c_int),
@@ -224,6 +225,13 @@ class Ctx:
     @property
     def launches(self):
         return int(lib().nbt_ctx_launch_count(self.h))
+
+    def set_profiling_mask(self, kernels):
+        """Record only these kernel families (iterable of KERNEL_* ids; empty = off)."""
+        mask = 0
+        for k in kernels:
+            mask |= 1 << int(k)
+        check(lib().nbt_ctx_set_profiling_mask(self.h, mask))
 
     def set_profiling(self, on=True):
         check(lib().nbt_ctx_set_profiling(self.h, int(bool(on))))

@@ -101,6 +101,7 @@ struct CapPair {
 // Per-kernel-family event timing (nbt_ctx_set_profiling).
 struct Profiler {
     bool on = false;
+    uint32_t mask = ~0u;              // kernel families recorded (bit = NBT_KERNEL_*)
     std::vector<cudaEvent_t> pool;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[NBT_KERNEL_COUNT];
     double ms[NBT_KERNEL_COUNT] = {0};

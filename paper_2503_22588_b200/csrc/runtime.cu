@@ -156,7 +156,7 @@ cudaEvent_t Profiler::take()
 
 ProfScope::ProfScope(nbt_ctx c, int k) : ctx(c), kernel(k)
 {
-    if (!ctx->prof.on) return;
+    if (!ctx->prof.on || !((ctx->prof.mask >> k) & 1u)) return;
     if (ctx->capturing) {
         // a fresh event owned by the graph; recorded as an event node at every replay
         if (cudaEventCreate(&start) != cudaSuccess) start = nullptr;
@@ -397,6 +397,16 @@ nbt_status nbt_ctx_set_profiling(nbt_ctx ctx, int enable)
     nbt_status s;
     if ((s = bind(ctx))) return s;
     ctx->prof.on = enable != 0;
+    ctx->prof.mask = ~0u;
+    return NBT_OK;
+}
+
+nbt_status nbt_ctx_set_profiling_mask(nbt_ctx ctx, uint32_t kernel_mask)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    ctx->prof.on = kernel_mask != 0;
+    ctx->prof.mask = kernel_mask;
     return NBT_OK;
 }
 
