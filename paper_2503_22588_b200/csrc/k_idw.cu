@@ -7,7 +7,7 @@
 // nearest perspective is closer than zero_eps, v_u is its gain (Q23).
 //
 //   k_idw_entry    grid (query blocks) x (entries): a block stages one entry's
-//                  perspectives through shared memory; each thread holds 4 queries in
+//                  perspectives through shared memory; each thread holds 3 queries in
 //                  registers and 16 lanes split the perspectives (interleaved; fp64
 //                  partial sums combined by shuffles, so the result differs from a
 //                  sequential sum only in rounding, < 1e-12 relative).  The nearest
@@ -25,11 +25,17 @@
 namespace nbt {
 namespace {
 
-constexpr int kQPT = 4;                      // queries per thread (register-blocked)
-constexpr int kSplit = 16;                   // lanes sharing one (query group, entry)
-constexpr int kGroups = 16;                  // query groups per block
+#ifndef NBT_IDW_QPT
+#define NBT_IDW_QPT 3
+#endif
+#ifndef NBT_IDW_SPLIT
+#define NBT_IDW_SPLIT 16
+#endif
+constexpr int kQPT = NBT_IDW_QPT;            // queries per thread (register-blocked)
+constexpr int kSplit = NBT_IDW_SPLIT;        // lanes sharing one (query group, entry)
+constexpr int kGroups = 256 / kSplit;        // query groups per block
 constexpr int kThreads = kGroups * kSplit;   // 256
-constexpr int kQueries = kGroups * kQPT;     // 64 queries per block
+constexpr int kQueries = kGroups * kQPT;     // 48 queries per block
 constexpr int kTile = 512;
 
 // 1/x to within an ulp: the hardware approximation refined by two Newton steps (the IEEE
@@ -55,7 +61,7 @@ __device__ __forceinline__ double dist2(double x0, double x1, double x2, double 
     return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
-// Block (query block, entry e): 16 groups of 4 queries x 16 lanes.  The 16 lanes of a
+// Block (query block, entry e): 16 groups of kQPT (3) queries x 16 lanes.  The 16 lanes of a
 // group split the entry's perspectives (interleaved), staged through shared memory; every
 // perspective record a lane reads is used for its 4 queries (register blocking: one
 // shared-memory read per 4 pairs), and the groups' partial sums combine by shuffles.
