@@ -28,6 +28,12 @@
  *   orc_voxel_filter       pinned  (S:53-56 examples, brute-force bucketing)
  *   orc_integrate          pinned  (S:61-64 examples, range truncation, hit-wins, exact touch sets)
  *   orc_occ_classify       pinned  (S:72-74 examples, round(63 sigmoid(L)) away from boundaries)
+ *   orc_quantize_prob      pinned  (worked examples, hand-traced Eq. 2 ray, uniform-level identity)
+ *   orc_map_update         pinned  (hand-worked last-wins example, rejection of bad deltas)
+ *   orc_orientation_factor pinned  (SPEC worked examples, scale invariances)
+ *   orc_info_cost          pinned  (closed forms)
+ *   orc_eq1                pinned  (hand-computed forced samples)
+ *   orc_camera_*           pinned  (s_G lattice counts of the SPEC / BASELINE examples)
  */
 #include <math.h>
 #include <stdint.h>

@@ -73,3 +73,20 @@ def test_monotone_in_probability():
     down = oracle.id_compute(oracle.OracleMap(codes, levels=lv3), [9.5, 1.5, 1.5], [[0.5, 1.5, 1.5]], cam, 9.0,
                              with_tg=True)[3][0]
     assert up - base == 13 and base - down == 13
+
+
+def test_map_update_hand_example():
+    """Row a2 / Q30 on a hand-worked example: deltas apply in array order, so a voxel named
+    twice ends with the later code; untouched voxels keep theirs; out-of-grid or code >= 3
+    deltas are rejected."""
+    codes = np.zeros((2, 3, 4), np.uint8)            # [z, y, x]
+    m = oracle.OracleMap(codes)
+    oracle.map_update(m, np.array([[1, 2, 0], [3, 0, 1], [1, 2, 0]], np.int32), np.array([1, 2, 2], np.uint8))
+    want = np.zeros((2, 3, 4), np.uint8)
+    want[0, 2, 1] = 2                                 # (x=1, y=2, z=0): 1 then 2
+    want[1, 0, 3] = 2                                 # (x=3, y=0, z=1)
+    assert np.array_equal(m.codes, want)
+    with pytest.raises(oracle.OracleError):
+        oracle.map_update(m, np.array([[4, 0, 0]], np.int32), np.array([1], np.uint8))
+    with pytest.raises(oracle.OracleError):
+        oracle.map_update(m, np.array([[0, 0, 0]], np.int32), np.array([3], np.uint8))
