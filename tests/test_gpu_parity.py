@@ -826,3 +826,21 @@ def test_binding_rejects_mismatched_buffers(nbt, ctx):
         buf.query(np.zeros((4, 3)), out=np.zeros(2))
     with pytest.raises(ValueError):
         nbt.sample_perspectives(ctx, poi, 1.0, 10, 3, out=np.zeros((5, 3)))
+
+
+def test_large_grid_1024(nbt, ctx):
+    """A 1024^3 map (2-bit store 272 MB, beyond L2) with long rays crossing it: walks and the
+    ID bit-exact vs the oracle on a handful of perspectives (maximum-size case)."""
+    n = 1024
+    codes = np.ones((n, n, n), np.uint8)
+    codes[:, :, 700:702] = 2                          # an occupied wall
+    codes[100:400, 200:600, 300:310] = 0               # an unknown block
+    codes[::97, ::89, ::83] = 2                        # sparse occupied voxels
+    m, om = make_map(nbt, ctx, codes)
+    poi = np.array([512.5, 512.5, 512.5])
+    P = np.array([[20.0, 30.0, 40.0], [1000.0, 900.0, 50.0], [512.0, 10.0, 1000.0], [-50.0, 512.0, 512.0]])
+    cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 12, 9, 1500.0, corners=True)
+    assert_cloud_equal(cloud, P, g, c)
+    o, e = random_segments_q12(300, -20.0, 1040.0, seed=77)
+    _compare_walks(nbt, ctx, m, om, o, e, max_visits=3200)
+    del codes
