@@ -74,6 +74,8 @@ def lib():
         L.orc_frame_export.argtypes = [C.POINTER(Map), dp, dp, C.POINTER(Camera), C.c_double, ip, dp]
         L.orc_idw_query.argtypes = [C.c_int32, ip, C.POINTER(dp), C.POINTER(dp), dp, C.c_int32, C.c_double,
                                     C.c_double, C.c_int32, dp]
+        L.orc_idw_query_knn.argtypes = [C.c_int32, ip, C.POINTER(dp), C.POINTER(dp), dp, C.c_int32, C.c_double,
+                                        C.c_double, C.c_int32, C.c_int32, dp]
         L.orc_philox4x32.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.orc_philox4x32.restype = None
         L.orc_sample_perspectives.argtypes = [dp, C.c_double, C.c_int32, C.c_uint64, C.c_int32, dp]
@@ -213,6 +215,22 @@ def idw_query(entries, queries, power_p=2.0, zero_eps=1e-9, normalize=False):
                              float(zero_eps), int(bool(normalize)), _d(out))
     if st:
         raise OracleError(st, "idw_query")
+    return out
+
+
+def idw_query_knn(entries, queries, knn, power_p=2.0, zero_eps=1e-9, normalize=False):
+    """Eq. 4 over the knn nearest perspectives of each entry (reading Q22)."""
+    ents = [(np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 3), np.ascontiguousarray(g, dtype=np.float64))
+            for x, g in entries]
+    sizes = np.array([len(g) for _, g in ents], np.int32)
+    xs = (C.POINTER(C.c_double) * max(1, len(ents)))(*[_d(x) for x, _ in ents])
+    gs = (C.POINTER(C.c_double) * max(1, len(ents)))(*[_d(g) for _, g in ents])
+    q = np.ascontiguousarray(queries, dtype=np.float64).reshape(-1, 3)
+    out = np.zeros(q.shape[0])
+    st = lib().orc_idw_query_knn(len(ents), _p(sizes, C.c_int32), xs, gs, _d(q), q.shape[0], float(power_p),
+                                 float(zero_eps), int(bool(normalize)), int(knn), _d(out))
+    if st:
+        raise OracleError(st, "idw_query_knn")
     return out
 
 

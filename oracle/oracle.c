@@ -22,6 +22,7 @@
  *   orc_id_compute         pinned  (SPEC worked examples, closed forms, invariants)
  *                          absolute g_P values on a real scene: "parity unpinned" (paper prints none, T25)
  *   orc_idw_query          pinned  (SPEC worked examples, convexity, H_NB identity)
+ *   orc_idw_query_knn      pinned  (hand example, k >= N_P identity, k = 1 nearest, ties)
  *   orc_sample_perspectives pinned (forced-sample example, radius bounds, radial CDF)
  *   orc_classify           pinned  (S:69-74 threshold rule examples)
  *   orc_philox4x32         pinned  (published Random123 known-answer vectors)
@@ -508,6 +509,75 @@ int orc_idw_query(int32_t n_entries, const int32_t *entry_sizes, const double *c
         }
         g_out[q] = normalize ? g / wsum : g;
     }
+    return ORC_OK;
+}
+
+/* Optional k-nearest variant of Eq. 4 (reading Q22): "interpolates ...
+ * across the nearest perspectives" read as the knn nearest ones of each entry,
+ * nearest by squared distance with ties to the lower index; v_u sums them in ascending j.
+ * knn >= the entry size gives orc_idw_query exactly.  The zero-distance rule is the same
+ * as orc_idw_query's (nearest by d over the whole entry). */
+typedef struct { double d2; int32_t j; } orc_dj;
+
+static int dj_cmp(const void *a, const void *b)
+{
+    const orc_dj *x = (const orc_dj *)a, *y = (const orc_dj *)b;
+    if (x->d2 != y->d2) return x->d2 < y->d2 ? -1 : 1;
+    return (x->j > y->j) - (x->j < y->j);
+}
+
+static int j_cmp(const void *a, const void *b)
+{
+    const orc_dj *x = (const orc_dj *)a, *y = (const orc_dj *)b;
+    return (x->j > y->j) - (x->j < y->j);
+}
+
+int orc_idw_query_knn(int32_t n_entries, const int32_t *entry_sizes, const double *const *entry_xyz,
+                      const double *const *entry_gain, const double *query_xyz, int32_t n_q, double power_p,
+                      double zero_eps, int32_t normalize, int32_t knn, double *g_out)
+{
+    if (n_entries <= 0) return ORC_ERR_EMPTY;
+    if (knn < 1) return ORC_ERR_INVALID_ARG;
+    int32_t maxn = 0;
+    for (int32_t e = 0; e < n_entries; ++e) {
+        if (entry_sizes[e] <= 0) return ORC_ERR_INVALID_ARG;
+        if (entry_sizes[e] > maxn) maxn = entry_sizes[e];
+    }
+    orc_dj *dj = (orc_dj *)malloc((size_t)maxn * sizeof *dj);
+    if (!dj) return ORC_ERR_INVALID_ARG;
+    for (int32_t q = 0; q < n_q; ++q) {
+        const double *x = query_xyz + 3 * (int64_t)q;
+        double g = 0.0, wsum = 0.0;
+        for (int32_t e = 0; e < n_entries; ++e) {
+            const double *P = entry_xyz[e];
+            const double *G = entry_gain[e];
+            int32_t np = entry_sizes[e];
+            int32_t nearest = -1;
+            double dmin = 0.0;
+            for (int32_t j = 0; j < np; ++j) {
+                double dx = x[0] - P[3 * j], dy = x[1] - P[3 * j + 1], dz = x[2] - P[3 * j + 2];
+                dj[j].d2 = (dx * dx + dy * dy) + dz * dz;
+                dj[j].j = j;
+                double d = sqrt(dj[j].d2);
+                if (nearest < 0 || d < dmin) { nearest = j; dmin = d; }
+            }
+            int32_t k = knn < np ? knn : np;
+            qsort(dj, (size_t)np, sizeof *dj, dj_cmp);       /* the k nearest come first */
+            qsort(dj, (size_t)k, sizeof *dj, j_cmp);         /* ... summed in ascending j */
+            double num = 0.0, den = 0.0;
+            for (int32_t t = 0; t < k; ++t) {
+                double w = (power_p == 2.0) ? 1.0 / dj[t].d2 : pow(dj[t].d2, -power_p / 2.0);
+                num += G[dj[t].j] * w;
+                den += w;
+            }
+            double v = (dmin < zero_eps) ? G[nearest] : num / den;
+            double wu = 1.0 / (double)(n_entries - e);
+            g += wu * v;
+            wsum += wu;
+        }
+        g_out[q] = normalize ? g / wsum : g;
+    }
+    free(dj);
     return ORC_OK;
 }
 

@@ -130,3 +130,28 @@ def test_classify_rules():
     obs = np.array([1, 1, 1, 0, 0], np.uint8)
     assert list(oracle.classify(p, obs)) == [2, 1, 2, 0, 0]
     assert list(oracle.classify(p, obs, 0.7, 0.3)) == [2, 0, 0, 0, 0]
+
+
+def test_idw_knn_hand_example_and_identities():
+    """Optional k-nearest Eq. 4 (reading Q22): a hand example, k >= N_P equals the full
+    sum bit for bit, k = 1 returns the nearest gain, equal distances go to the lower j."""
+    P = np.array([[1.0, 0, 0], [0, 2.0, 0], [0, 0, 4.0]])
+    g = np.array([1.0, 2.0, 3.0])
+    x = np.zeros((1, 3))
+    # k = 2: weights 1 and 1/4 -> (1*1 + 2/4) / (1 + 1/4) = 1.2
+    v = oracle.idw_query_knn([(P, g)], x, 2)
+    assert abs(v[0] - 1.2) < 1e-15
+    rng = np.random.default_rng(3)
+    Pr = rng.normal(size=(37, 3)); gr = rng.random(37); q = rng.normal(size=(20, 3)) * 2
+    full = oracle.idw_query([(Pr, gr), (Pr[:11], gr[:11])], q)
+    for k in (37, 50):
+        assert np.array_equal(oracle.idw_query_knn([(Pr, gr), (Pr[:11], gr[:11])], q, k), full)
+    # k = 1: the nearest perspective's gain (one term: g w / w)
+    v1 = oracle.idw_query_knn([(Pr, gr)], q, 1)
+    near = np.argmin(((q[:, None, :] - Pr[None]) ** 2).sum(-1), axis=1)
+    np.testing.assert_allclose(v1, gr[near], rtol=1e-15)
+    # ties: two perspectives at the same distance, k = 1 takes the lower index
+    Pt = np.array([[0, 3.0, 0], [3.0, 0, 0], [0, 0, 9.0]]); gt = np.array([0.25, 0.75, 0.5])
+    assert oracle.idw_query_knn([(Pt, gt)], x, 1)[0] == 0.25
+    with pytest.raises(oracle.OracleError):
+        oracle.idw_query_knn([(Pt, gt)], x, 0)
