@@ -302,6 +302,12 @@ int32_t    nbt_idbuf_size(nbt_idbuf buf);
 nbt_status nbt_ig_query(nbt_idbuf buf, const double *query_xyz, int32_t n_q, int q_on_device,
                         double power_p, double zero_eps, int32_t normalize_weights,
                         double *g_out, int out_on_device);
+/* Eq. 4 over the knn nearest perspectives of each entry only (reading Q22, the optional
+ * "nearest perspectives" form of P:274): nearest by squared distance, ties to the lower
+ * index; knn in [1, 16]; knn = 0 is nbt_ig_query.  Same arguments and errors otherwise. */
+nbt_status nbt_ig_query_knn(nbt_idbuf buf, const double *query_xyz, int32_t n_q, int q_on_device,
+                            double power_p, double zero_eps, int32_t normalize_weights, int32_t knn,
+                            double *g_out, int out_on_device);
 void       nbt_idbuf_destroy(nbt_idbuf buf);
 
 /* The MHP's information cost over candidate trajectories:

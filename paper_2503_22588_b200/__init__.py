@@ -40,7 +40,7 @@ EXPORTS = [
     "nbt_map_get_desc", "nbt_map_destroy",
     "nbt_camera_from_fov", "nbt_camera_from_grid_scaling", "nbt_camera_num_rays",
     "nbt_sample_perspectives", "nbt_id_compute", "nbt_id_compute_slice",
-    "nbt_idbuf_create", "nbt_idbuf_push", "nbt_idbuf_clear", "nbt_idbuf_size", "nbt_ig_query", "nbt_idbuf_destroy",
+    "nbt_idbuf_create", "nbt_idbuf_push", "nbt_idbuf_clear", "nbt_idbuf_size", "nbt_ig_query", "nbt_ig_query_knn", "nbt_idbuf_destroy",
     "nbt_info_cost",
     "nbt_integrate_params_default", "nbt_occ_create", "nbt_occ_upload", "nbt_occ_download", "nbt_occ_integrate",
     "nbt_occ_stats", "nbt_occ_deltas", "nbt_occ_destroy", "nbt_voxel_filter",
@@ -132,6 +132,7 @@ def lib():
         "nbt_idbuf_clear": ([vp], C.c_int),
         "nbt_idbuf_size": ([vp], i32),
         "nbt_ig_query": ([vp, vp, i32, C.c_int, dbl, dbl, i32, vp, C.c_int], C.c_int),
+        "nbt_ig_query_knn": ([vp, vp, i32, C.c_int, dbl, dbl, i32, i32, vp, C.c_int], C.c_int),
         "nbt_idbuf_destroy": ([vp], None),
         "nbt_info_cost": ([vp, vp, vp, i32, i32, C.c_int, vp, dbl, dbl, dbl, dbl, dbl, i32, vp, vp, vp, C.c_int],
                           C.c_int),
@@ -571,7 +572,8 @@ class IdBuffer:
     def __len__(self):
         return int(lib().nbt_idbuf_size(self.h))
 
-    def query(self, xyz, power_p=2.0, zero_eps=1e-9, normalize=False, out=None):
+    def query(self, xyz, power_p=2.0, zero_eps=1e-9, normalize=False, out=None, knn=0):
+        """Eq. 4 at (n, 3) positions; knn > 0: only the knn nearest perspectives of each entry (Q22)."""
         pq, qdev, kq = _ptr(xyz, np.float64)
         if _count(kq) % 3:
             raise ValueError("queries must be (n, 3) float64")
@@ -581,8 +583,8 @@ class IdBuffer:
         po, odev, ko = _ptr(out, np.float64)
         if _count(ko) < nq:
             raise ValueError("out holds fewer values than queries")
-        check(lib().nbt_ig_query(self.h, pq, int(nq), qdev, float(power_p), float(zero_eps), int(bool(normalize)),
-                                 po, odev))
+        check(lib().nbt_ig_query_knn(self.h, pq, int(nq), qdev, float(power_p), float(zero_eps),
+                                     int(bool(normalize)), int(knn), po, odev))
         return out
 
     def info_cost(self, pos, axis, poses_per_traj, poi, cos_theta_cut, w_i, eps=1e-7, power_p=2.0, zero_eps=1e-9,

@@ -143,6 +143,97 @@ __global__ void __launch_bounds__(kThreads)
     v_out[(size_t)e * n_q + qi] = v;
 }
 
+// Optional k-nearest Eq. 4 (reading Q22): one warp per (query, entry).  Every lane keeps the
+// 16 nearest of its perspectives (j = lane, lane + 32, ...) sorted by (d^2, j) in registers;
+// knn rounds of a warp-wide (d^2, j) argmin then take the k nearest of the entry, each
+// summed by the lane that holds it (the order differs from the oracle's ascending j only in
+// rounding).  The zero-distance rule is the same as k_idw_entry's.
+constexpr int kKnnMax = 16;
+
+__device__ __forceinline__ bool dj_less(double a, int ja, double b, int jb)
+{
+    return a < b || (a == b && ja < jb);
+}
+
+__global__ void __launch_bounds__(256)
+    k_idw_entry_knn(const double *__restrict__ xyz, const double *__restrict__ gain, int32_t max_persp,
+                    const int32_t *__restrict__ meta, int32_t cap, const double *__restrict__ q, int32_t n_q,
+                    double power_p, double zero_eps, int32_t knn, double *__restrict__ v_out)
+{
+    const int lane = threadIdx.x & 31;
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int pushes = meta[0];
+    const int m = min(pushes, cap);
+    const int e = (int)(gw / n_q);
+    const int qi = (int)(gw % n_q);
+    if (e >= m) return;
+    const int slot = (pushes - m + e) % cap;
+    const double *P = xyz + (size_t)slot * max_persp * 3;
+    const double *G = gain + (size_t)slot * max_persp;
+    const int np = meta[1 + slot];
+    const double x0 = q[3 * (size_t)qi], x1 = q[3 * (size_t)qi + 1], x2 = q[3 * (size_t)qi + 2];
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    double d[kKnnMax];
+    int jj[kKnnMax];
+#pragma unroll
+    for (int t = 0; t < kKnnMax; ++t) { d[t] = inf; jj[t] = 0x7fffffff; }
+    double d2min = inf;
+    for (int j = lane; j < np; j += 32) {
+        const double d2 = dist2(x0, x1, x2, P[3 * (size_t)j], P[3 * (size_t)j + 1], P[3 * (size_t)j + 2]);
+        d2min = fmin(d2min, d2);
+        if (dj_less(d2, j, d[kKnnMax - 1], jj[kKnnMax - 1])) {
+            d[kKnnMax - 1] = d2;
+            jj[kKnnMax - 1] = j;
+#pragma unroll
+            for (int t = kKnnMax - 1; t > 0; --t) {
+                if (dj_less(d[t], jj[t], d[t - 1], jj[t - 1])) {
+                    const double td = d[t]; d[t] = d[t - 1]; d[t - 1] = td;
+                    const int tj = jj[t]; jj[t] = jj[t - 1]; jj[t - 1] = tj;
+                }
+            }
+        }
+    }
+    const bool p2 = power_p == 2.0;
+    const double hp = -0.5 * power_p;
+    double num = 0.0, den = 0.0;
+    for (int r = 0; r < knn; ++r) {
+        double bd = d[0];
+        int bj = jj[0];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, bd, off);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+            if (dj_less(od, oj, bd, bj)) { bd = od; bj = oj; }
+        }
+        if (bj == 0x7fffffff) break;                  // fewer than knn perspectives
+        if (jj[0] == bj) {                            // this lane holds the winner
+            const double w = p2 ? rcp_nr(bd) : pow(bd, hp);
+            num = fma(G[bj], w, num);
+            den += w;
+#pragma unroll
+            for (int t = 0; t < kKnnMax - 1; ++t) { d[t] = d[t + 1]; jj[t] = jj[t + 1]; }
+            d[kKnnMax - 1] = inf;
+            jj[kKnnMax - 1] = 0x7fffffff;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, off);
+        den += __shfl_xor_sync(0xffffffffu, den, off);
+        d2min = fmin(d2min, __shfl_xor_sync(0xffffffffu, d2min, off));
+    }
+    if (lane != 0) return;
+    double v = num / den;
+    const double dmin = __dsqrt_rn(d2min);
+    if (dmin < zero_eps) {
+        for (int j = 0; j < np; ++j) {
+            const double d2 = dist2(x0, x1, x2, P[3 * (size_t)j], P[3 * (size_t)j + 1], P[3 * (size_t)j + 2]);
+            if (__dsqrt_rn(d2) == dmin) { v = G[j]; break; }
+        }
+    }
+    v_out[(size_t)e * n_q + qi] = v;
+}
+
 __global__ void k_idw_combine(const double *__restrict__ v, const int32_t *__restrict__ meta, int32_t cap, int32_t n_q,
                               int32_t normalize, double *__restrict__ out)
 {
@@ -250,15 +341,22 @@ nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const InfoCostArg
 }
 
 nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const double *d_q, int32_t n_q, double power_p,
-                      double zero_eps, int32_t normalize, double *d_out)
+                      double zero_eps, int32_t normalize, double *d_out, int32_t knn)
 {
     if (n_q == 0) return NBT_OK;
     nbt_status st;
     if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_q * 8))) return st;
     ProfScope ps(ctx, NBT_KERNEL_IDW);
-    dim3 grid((n_q + kQueries - 1) / kQueries, b->capacity);
-    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, d_q,
-                                                     n_q, power_p, zero_eps, ctx->idw_tmp.as<double>());
+    if (knn > 0) {
+        const long long warps = (long long)n_q * b->capacity;
+        k_idw_entry_knn<<<(unsigned)((warps + 7) / 8), 256, 0, ctx->stream>>>(
+            b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, d_q, n_q, power_p, zero_eps, knn,
+            ctx->idw_tmp.as<double>());
+    } else {
+        dim3 grid((n_q + kQueries - 1) / kQueries, b->capacity);
+        k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity,
+                                                         d_q, n_q, power_p, zero_eps, ctx->idw_tmp.as<double>());
+    }
     NBT_LAUNCHED(ctx);
     k_idw_combine<<<(n_q + 127) / 128, 128, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), b->d_meta, b->capacity,
                                                                n_q, normalize, d_out);

@@ -242,7 +242,7 @@ nbt_status launch_debug_frames(nbt_ctx ctx, nbt_map m, const double poi[3], cons
 // captured graph replays pushes and queries correctly.
 nbt_status launch_idbuf_push(nbt_ctx ctx, nbt_idbuf_s *b, const double *d_xyz, const double *d_gain, int32_t n);
 nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const double *d_q, int32_t n_q, double power_p,
-                      double zero_eps, int32_t normalize, double *d_out);
+                      double zero_eps, int32_t normalize, double *d_out, int32_t knn = 0);
 struct InfoCostArgs {
     const double *pos, *axis;
     int32_t n_traj, per;

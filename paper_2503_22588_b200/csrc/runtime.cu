@@ -1213,7 +1213,15 @@ int32_t nbt_idbuf_size(nbt_idbuf b) { return b ? b->count : 0; }
 nbt_status nbt_ig_query(nbt_idbuf b, const double *query_xyz, int32_t n_q, int q_on_device, double power_p,
                         double zero_eps, int32_t normalize_weights, double *g_out, int out_on_device)
 {
+    return nbt_ig_query_knn(b, query_xyz, n_q, q_on_device, power_p, zero_eps, normalize_weights, 0, g_out,
+                            out_on_device);
+}
+
+nbt_status nbt_ig_query_knn(nbt_idbuf b, const double *query_xyz, int32_t n_q, int q_on_device, double power_p,
+                            double zero_eps, int32_t normalize_weights, int32_t knn, double *g_out, int out_on_device)
+{
     if (!b) return fail(NBT_ERR_INVALID_ARG, "nbt_ig_query: null buffer");
+    if (knn < 0 || knn > 16) return fail(NBT_ERR_INVALID_ARG, "nbt_ig_query_knn: knn must lie in [0, 16]");
     nbt_ctx ctx = b->ctx;
     nbt_status s;
     if ((s = bind(ctx))) return s;
@@ -1236,7 +1244,7 @@ nbt_status nbt_ig_query(nbt_idbuf b, const double *query_xyz, int32_t n_q, int q
         if ((s = ctx->qout.ensure((size_t)n_q * 8))) return s;
         dout = ctx->qout.as<double>();
     }
-    if ((s = launch_idw(ctx, b, dq, n_q, power_p, zero_eps, normalize_weights, dout))) return s;
+    if ((s = launch_idw(ctx, b, dq, n_q, power_p, zero_eps, normalize_weights, dout, knn))) return s;
     if (!out_on_device) return d2h_sync(ctx, g_out, dout, (size_t)n_q * 8);
     return NBT_OK;
 }

@@ -844,3 +844,31 @@ def test_large_grid_1024(nbt, ctx):
     o, e = random_segments_q12(300, -20.0, 1040.0, seed=77)
     _compare_walks(nbt, ctx, m, om, o, e, max_visits=3200)
     del codes
+
+
+@pytest.mark.parametrize("knn", [1, 3, 8, 16])
+@pytest.mark.parametrize("power_p", [2.0, 3.0])
+def test_idw_knn_matches_oracle(nbt, ctx, knn, power_p):
+    """Optional k-nearest Eq. 4 (reading Q22) vs the oracle: ragged entries (some smaller
+    than knn), an evicting ring, zero-distance queries, equal-distance ties; 1e-12 relative."""
+    rng = np.random.default_rng(int(knn * 10 + power_p))
+    buf = nbt.IdBuffer(ctx, 6, 600)
+    entries = []
+    for k in range(8):
+        n = int(rng.integers(1, 600)) if k % 3 else int(rng.integers(1, knn + 1))
+        xyz = rng.normal(size=(n, 3)); gain = rng.uniform(0, 4, n)
+        if n > 4:
+            xyz[3] = -xyz[2]                            # equal distance to the origin
+        buf.push(nbt.IgCloud(xyz, gain, None))
+        entries.append((xyz, gain))
+    q = rng.normal(size=(777, 3)) * 1.3
+    q[:4] = entries[-1][0][:4]                          # zero distance to the newest entry
+    q[4] = 0.0                                          # ties at the origin
+    got = buf.query(q, power_p=power_p, knn=knn)
+    want = oracle.idw_query_knn(entries[-6:], q, knn, power_p=power_p)
+    assert np.allclose(got, want, rtol=1e-12, atol=0)
+    # knn = 0 is the full sum
+    assert np.allclose(buf.query(q, power_p=power_p, knn=0), oracle.idw_query(entries[-6:], q, power_p=power_p),
+                       rtol=1e-12, atol=0)
+    with pytest.raises(nbt.NbtError):
+        buf.query(q, knn=17)
