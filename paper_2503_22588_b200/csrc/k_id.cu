@@ -145,6 +145,30 @@ __device__ __forceinline__ constexpr uint32_t lanes_mask(uint32_t pattern)
     return K >= 16 ? pattern : (pattern & ((1u << (2 * K)) - 1u));
 }
 
+#ifndef NBT_MAP_LOAD
+#define NBT_MAP_LOAD 0
+#endif
+// Map word load of the walk: 0 = ld.global.nc (default), 1 = L1::evict_last, 2 = L1::evict_first,
+// 3 = L1::no_allocate (experiments).
+__device__ __forceinline__ uint32_t load_map_word(const uint32_t *p)
+{
+#if NBT_MAP_LOAD == 1
+    uint32_t v;
+    asm("ld.global.nc.L1::evict_last.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#elif NBT_MAP_LOAD == 2
+    uint32_t v;
+    asm("ld.global.nc.L1::evict_first.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#elif NBT_MAP_LOAD == 3
+    uint32_t v;
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 // Store kinds (the VB template parameter): kStore2 = 2-bit codes, 16 per word (rows a1, a6);
 // kStoreByte = one byte per voxel holding the code alone; kStoreProb = one byte per voxel,
 // code in bits 0-1 and the Eq. 2 gain in bits 2-7 (f1).  Byte stores load the voxel's own
@@ -161,7 +185,7 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
     for (int k = 0; k < K; ++k) {
         if (VB == kStore2) {
             b.rot[k] = (w.idx << 1) - 2 * k;    // rotate amounts are taken mod 32
-            b.wd[k] = __ldg(m.words + (w.idx >> 4));
+            b.wd[k] = load_map_word(m.words + (w.idx >> 4));
         } else {
             b.wd[k] = __ldg(bytes + w.idx);
         }
