@@ -804,12 +804,12 @@ int chunk_min()
     return v;
 }
 
-// Idle lanes a warp waits for before refilling: NBT_REFILL_MIN, default 8 (profiles/r01_trace_variants.md).
+// Idle lanes a warp waits for before refilling: NBT_REFILL_MIN, default 6 (profiles/r01_refill_sweep.log).
 int refill_threshold()
 {
     static int v = [] {
         const char *e = getenv("NBT_REFILL_MIN");
-        int r = e ? atoi(e) : 8;
+        int r = e ? atoi(e) : 6;
         return r < 1 ? 1 : (r > 32 ? 32 : r);
     }();
     return v;
