@@ -872,3 +872,27 @@ def test_idw_knn_matches_oracle(nbt, ctx, knn, power_p):
                        rtol=1e-12, atol=0)
     with pytest.raises(nbt.NbtError):
         buf.query(q, knn=17)
+
+
+@pytest.mark.parametrize("name,sampled", [("C'", 3), ("D", 5)])
+def test_full_size_north_star_and_d_sampled(nbt, ctx, name, sampled):
+    """The north-star config C' (512 x 640x480 on 256^3) and config D (4096 x 160x120 on
+    512^3) computed whole, in bench.py's launch shape, with sampled perspectives recomputed
+    one by one by the oracle: per-state totals and g_P bit-exact."""
+    import torch
+    cfg = CONFIGS[name]
+    codes = cfg.map_codes()
+    m, om = make_map(nbt, ctx, codes, cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    out = nbt.empty_cloud(cfg.n_persp, device="cuda")
+    nbt.id_compute(ctx, m, cfg.poi, torch.from_numpy(P).cuda(), cam, cfg.range_, out=out)
+    ctx.sync()
+    counts = out.counts.cpu().numpy()
+    gain = out.gain.cpu().numpy()
+    assert np.isfinite(gain).all() and (counts[:, 2] <= cam.num_rays).all()
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    idx = np.linspace(0, cfg.n_persp - 1, sampled).astype(int)
+    _, g, c = oracle.id_compute(om, cfg.poi, P[idx], ocam, cfg.range_, nthreads=NTHREADS)
+    assert np.array_equal(counts[idx].astype(np.int64), c)
+    assert np.array_equal(gain[idx], g)
