@@ -614,7 +614,7 @@ nbt_status launch_voxel_filter(nbt_ctx ctx, nbt_occ_s *o, const double *d_pts, u
 }
 
 // The hashed voxel filter of the integration path: o->filtered = the centroids (cells in
-// hash-slot order), ctl[kOccRays] = their number.
+// the order of their first point, i.e. pixel order), ctl[kOccRays] = their number.
 static nbt_status launch_voxel_filter_hashed(nbt_ctx ctx, nbt_occ_s *o, const double *d_pts, uint32_t n, double leaf)
 {
     nbt_status st;
