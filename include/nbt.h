@@ -282,6 +282,32 @@ nbt_status nbt_id_compute_slice(nbt_ctx ctx, nbt_map map, const double poi[3], c
                                 int32_t n_persp, int persp_on_device, int32_t first, int32_t stride,
                                 const nbt_camera *cam, double range, nbt_ig_cloud *out);
 
+/* Ray-split form for multi-GPU when perspectives are fewer than GPUs (SURVEY 8e "ray-split
+ * fallback"): the rays of EVERY perspective are dealt to ray_world shards and this call
+ * walks shard ray_rank's rays only.  Units of 32 rays: with W >= 8 and H >= 4 the 8x4
+ * pixel tiles (tx, ty) = (i / 8, kk / 4), unit u = ty * ceil(W / 8) + tx; otherwise
+ * u = floor(k / 32) for the row-major ray index k = kk * W + i (Q27).  Shard r walks the
+ * units u with u mod ray_world == r; the 4 corner rays of the s_G mode belong to shard 0.
+ * totals_out: DEVICE memory of the ctx's device, n_persp x NBT_ID_TOTALS uint64 per
+ * perspective = (T_U, T_F, T_O, L, T_G) over this shard's rays (T_G: the Eq. 2 gain in 1/63
+ * units, Q32; meaningful only for a per-voxel-probability map, ignore it otherwise),
+ * overwritten.  The totals are
+ * integers, so their sum over the shards (e.g. an all-reduce) equals the whole ID's totals
+ * exactly; nbt_id_finalize turns them into the IG cloud.  Validation as nbt_id_compute;
+ * NBT_ERR_INVALID_ARG unless 0 <= ray_rank < ray_world and totals_out is device memory. */
+#define NBT_ID_TOTALS 5
+nbt_status nbt_id_compute_rays(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz,
+                               int32_t n_persp, int persp_on_device, int32_t ray_rank, int32_t ray_world,
+                               const nbt_camera *cam, double range, uint64_t *totals_out);
+/* The IG cloud of the totals summed over all ray shards (Q26/Q32), the same fp64
+ * expression nbt_id_compute ends with, so the result is bit-identical to nbt_id_compute on
+ * one GPU.  totals: DEVICE memory, n_persp x NBT_ID_TOTALS uint64 (read only); the
+ * perspectives are validated again (a degenerate one gets NBT_ERR_DEGENERATE / NaN, as in
+ * nbt_id_compute). */
+nbt_status nbt_id_finalize(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz,
+                           int32_t n_persp, int persp_on_device, const nbt_camera *cam, double range,
+                           const uint64_t *totals, nbt_ig_cloud *out);
+
 /* -------------------------------------------- ID buffer + IDW query (row a9) */
 
 typedef struct nbt_idbuf_s *nbt_idbuf;

@@ -39,7 +39,7 @@ EXPORTS = [
     "nbt_map_update", "nbt_map_update_prob", "nbt_map_device_buffer", "nbt_map_download", "nbt_map_download_levels",
     "nbt_map_get_desc", "nbt_map_destroy",
     "nbt_camera_from_fov", "nbt_camera_from_grid_scaling", "nbt_camera_num_rays",
-    "nbt_sample_perspectives", "nbt_id_compute", "nbt_id_compute_slice",
+    "nbt_sample_perspectives", "nbt_id_compute", "nbt_id_compute_slice", "nbt_id_compute_rays", "nbt_id_finalize",
     "nbt_idbuf_create", "nbt_idbuf_push", "nbt_idbuf_clear", "nbt_idbuf_size", "nbt_ig_query", "nbt_ig_query_knn", "nbt_idbuf_destroy",
     "nbt_info_cost",
     "nbt_integrate_params_default", "nbt_occ_create", "nbt_occ_upload", "nbt_occ_download", "nbt_occ_integrate",
@@ -127,6 +127,9 @@ def lib():
         "nbt_id_compute": ([vp, vp, vp, vp, i32, C.c_int, C.POINTER(Camera), dbl, C.POINTER(IgCloudC)], C.c_int),
         "nbt_id_compute_slice": ([vp, vp, vp, vp, i32, C.c_int, i32, i32, C.POINTER(Camera), dbl,
                                   C.POINTER(IgCloudC)], C.c_int),
+        "nbt_id_compute_rays": ([vp, vp, vp, vp, i32, C.c_int, i32, i32, C.POINTER(Camera), dbl, vp], C.c_int),
+        "nbt_id_finalize": ([vp, vp, vp, vp, i32, C.c_int, C.POINTER(Camera), dbl, vp, C.POINTER(IgCloudC)],
+                            C.c_int),
         "nbt_idbuf_create": ([vp, i32, i32, C.POINTER(vp)], C.c_int),
         "nbt_idbuf_push": ([vp, C.POINTER(IgCloudC), i32], C.c_int),
         "nbt_idbuf_clear": ([vp], C.c_int),
@@ -550,6 +553,55 @@ def nbt_id_compute(ctx: Ctx, m: Map, poi, persp, cam: Camera, range_, out: IgClo
 
 
 id_compute = nbt_id_compute
+
+ID_TOTALS = 5   # NBT_ID_TOTALS: T_U, T_F, T_O, L, T_G per perspective
+
+
+def _device_totals(t, n):
+    import torch
+    if not (_is_torch(t) and t.is_cuda and t.dtype == torch.int64 and t.is_contiguous()):
+        raise TypeError("totals must be a contiguous int64 CUDA tensor (the uint64 bits)")
+    if t.numel() < ID_TOTALS * n:
+        raise ValueError(f"totals holds {t.numel()} values, {ID_TOTALS * n} needed")
+    return C.c_void_p(t.data_ptr())
+
+
+def nbt_id_compute_rays(ctx: Ctx, m: Map, poi, persp, cam: Camera, range_, ray_rank, ray_world, out=None):
+    """Ray shard ray_rank of ray_world of the ID (SURVEY 8(e) ray split): the (n, 5) int64 CUDA
+    tensor of this shard's integer totals (T_U, T_F, T_O, L, T_G); sum over the shards
+    (all-reduce), then nbt_id_finalize."""
+    import torch
+    pp, keep = _poi(poi)
+    pper, dev, kp = _ptr(persp, np.float64)
+    if _count(kp) % 3:
+        raise ValueError("perspectives must be (n, 3) float64")
+    n = _count(kp) // 3
+    if out is None:
+        out = torch.empty((n, ID_TOTALS), dtype=torch.int64, device=torch.device("cuda", ctx.device))
+    pt = _device_totals(out, n)
+    check(lib().nbt_id_compute_rays(ctx.h, m.h, pp, pper, int(n), dev, int(ray_rank), int(ray_world),
+                                    C.byref(cam), float(range_), pt))
+    return out
+
+
+def nbt_id_finalize(ctx: Ctx, m: Map, poi, persp, cam: Camera, range_, totals, out: IgCloud | None = None):
+    """The IG cloud of totals summed over every ray shard (bit-identical to nbt_id_compute)."""
+    pp, keep = _poi(poi)
+    pper, dev, kp = _ptr(persp, np.float64)
+    if _count(kp) % 3:
+        raise ValueError("perspectives must be (n, 3) float64")
+    n = _count(kp) // 3
+    pt = _device_totals(totals, n)
+    if out is None:
+        out = empty_cloud(n)
+    _check_cloud(out, n)
+    oc = out.as_c()
+    check(lib().nbt_id_finalize(ctx.h, m.h, pp, pper, int(n), dev, C.byref(cam), float(range_), pt, C.byref(oc)))
+    return out
+
+
+id_compute_rays = nbt_id_compute_rays
+id_finalize = nbt_id_finalize
 
 
 class IdBuffer:

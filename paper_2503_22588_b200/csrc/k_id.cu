@@ -41,6 +41,7 @@ using namespace dda;
 
 constexpr int kFrameInts = 20;   // O, A, Rh, Uh, Rc, Uc (3 each, Q16), status, pad
 constexpr int kTotals = 5;       // per perspective: T_U, T_F, T_O, L, T_G (Eq. 2 gain, 1/63 units)
+static_assert(kTotals == NBT_ID_TOTALS, "totals layout of nbt_id_compute_rays");
 #ifndef NBT_WARPS_PER_BLOCK
 #define NBT_WARPS_PER_BLOCK 8
 #endif
@@ -385,11 +386,13 @@ struct TraceArgs {
     int tiled;                  // 1: warp-coherent 8x4 pixel tiles
     int Wt;                     // tiles per row
     int n_tile_slots;           // tiles * 32 (tiled) or W*H
-    int slots;                  // slots per perspective (incl. 4 corner slots)
+    int slots;                  // slots per perspective (incl. 4 corner slots on ray rank 0)
     int chunk;                  // slots per chunk (multiple of 32)
     int chunks_per_persp;
     int total_chunks;
     int min_refill;             // idle lanes needed before a warp refills (experiments)
+    int ray_rank, ray_world;    // ray shard: this call walks 32-slot units u = ray_rank mod ray_world
+    int local_tile_slots;       // lattice slots of this shard (its units * 32)
 };
 
 // Map slot -> lattice offsets (mi, mk) = (2i-(W-1), 2kk-(H-1)) or a corner ray.
@@ -559,7 +562,7 @@ constexpr int trace_min_blocks()
                                     : (sizeof(T) == 8 ? 16 : (VB == kStoreProb ? 24 : 32)) / kWarpsPerBlock;
 }
 
-template <typename T, int L, int VB, int K, bool PIPE>
+template <typename T, int L, int VB, int K, bool PIPE, bool SHARD>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()) k_id_trace(TraceArgs A)
 {
     constexpr bool CYCLE = PIPE && VB != kStoreProb;     // in-place pipeline (batch_cycle)
@@ -595,8 +598,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     continue;
                 }
                 const int avail = min(32, q_end - q_next);
+                int slot0 = q_next, valid = avail;
+                if (SHARD) {
+                    // ray shard: local 32-slot unit u -> lattice unit u * ray_world + ray_rank
+                    // (chunks are whole units), then shard 0's corner rays (a separate
+                    // instance, so the whole-ID kernel's code is unchanged)
+                    if (q_next < A.local_tile_slots) {
+                        slot0 = ((q_next >> 5) * A.ray_world + A.ray_rank) << 5;
+                        valid = min(avail, A.n_tile_slots - slot0);
+                    } else {
+                        slot0 = q_next - A.local_tile_slots + A.n_tile_slots;
+                    }
+                }
                 Walk<T> t;
-                const bool ok = lane < avail && prep_ray<T, L>(A, q_j, q_next + lane, t);
+                const bool ok = lane < valid && prep_ray<T, L>(A, q_j, slot0 + lane, t);
                 q_next += avail;
                 const unsigned vm = __ballot_sync(full, ok);
                 if (ok) queue_put<T, L>(Q, __popc(vm & lanes_below), t, q_j);
@@ -828,13 +843,16 @@ double max_ray_voxels(const nbt_camera &cam, double range, double voxel_size)
     return rs * sqrt(1.0 + ex * ex + ey * ey) * 1.001 + 2.0;
 }
 
-// The kernel instances: [wide][layout][store: 2-bit, byte, byte + gain].
-#define NBT_TRACE_ROW(T, L)                                                                     \
-    {k_id_trace<T, L, kStore2, kBatchK, kPipe>, k_id_trace<T, L, kStoreByte, kBatchK, kPipe>, \
-     k_id_trace<T, L, kStoreProb, kBatchK, kPipe>}
+// The kernel instances: [ray shard][wide][layout][store: 2-bit, byte, byte + gain].
+#define NBT_TRACE_ROW(T, L, S)                                                                        \
+    {k_id_trace<T, L, kStore2, kBatchK, kPipe, S>, k_id_trace<T, L, kStoreByte, kBatchK, kPipe, S>, \
+     k_id_trace<T, L, kStoreProb, kBatchK, kPipe, S>}
+#define NBT_TRACE_SET(S)                                                          \
+    {{NBT_TRACE_ROW(int, kLayoutLinear, S), NBT_TRACE_ROW(int, kLayoutMorton, S)}, \
+     {NBT_TRACE_ROW(long long, kLayoutLinear, S), NBT_TRACE_ROW(long long, kLayoutMorton, S)}}
 using TraceFn = void (*)(TraceArgs);
-const TraceFn kTraceFns[2][2][3] = {{NBT_TRACE_ROW(int, kLayoutLinear), NBT_TRACE_ROW(int, kLayoutMorton)},
-                                    {NBT_TRACE_ROW(long long, kLayoutLinear), NBT_TRACE_ROW(long long, kLayoutMorton)}};
+const TraceFn kTraceFns[2][2][2][3] = {NBT_TRACE_SET(false), NBT_TRACE_SET(true)};
+#undef NBT_TRACE_SET
 #undef NBT_TRACE_ROW
 
 using DebugFn = void (*)(MapView, const int32_t *, const int32_t *, int, int, int32_t *, uint8_t *, int32_t *,
@@ -856,13 +874,17 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     nbt_status st;
     if ((st = ctx->frames.ensure((size_t)L.n * kFrameInts * 4))) return st;
     if ((st = ctx->totals.ensure((size_t)L.n * kTotals * 8))) return st;
+    // totals the trace accumulates into (zeroed by k_persp_frames): the caller's array for a
+    // ray shard, else scratch; the finalize reads the caller's summed totals when given
+    unsigned long long *tot = L.d_totals_trace ? reinterpret_cast<unsigned long long *>(L.d_totals_trace)
+                                               : ctx->totals.as<unsigned long long>();
     if ((st = ctx->counter.ensure(64))) return st;
     FrameArgs A = frame_args(m, L.d_persp, L.first, L.stride, L.n, L.poi, L.cam, L.range);
     int *counter = ctx->counter.as<int>();
     {
         ProfScope ps(ctx, NBT_KERNEL_FRAMES);
         k_persp_frames<<<(L.n + 127) / 128, 128, 0, ctx->stream>>>(A, ctx->frames.as<int32_t>(),
-                                                                    ctx->totals.as<unsigned long long>(), counter,
+                                                                    tot, counter,
                                                                     ctx->d_err);
         NBT_LAUNCHED(ctx);
     }
@@ -870,30 +892,37 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     TraceArgs T;
     T.m = view_of(m);
     T.frames = ctx->frames.as<int32_t>();
-    T.totals = ctx->totals.as<unsigned long long>();
+    T.totals = tot;
     T.work_counter = counter;
     T.W = L.cam.width; T.H = L.cam.height; T.add_corners = L.cam.add_corners ? 1 : 0;
     T.tiled = (T.W >= 8 && T.H >= 4) ? 1 : 0;
     T.Wt = (T.W + 7) / 8;
     int Ht = (T.H + 3) / 4;
     T.n_tile_slots = T.tiled ? T.Wt * Ht * 32 : T.W * T.H;
-    T.slots = T.n_tile_slots + (T.add_corners ? 4 : 0);
+    // ray shard (SURVEY 8(e) ray split): units of 32 lattice slots dealt round-robin
+    const int units = (T.n_tile_slots + 31) / 32;
+    T.ray_rank = L.ray_rank;
+    T.ray_world = L.ray_world;
+    T.local_tile_slots = L.ray_world == 1 ? T.n_tile_slots
+                         : units > L.ray_rank ? ((units - L.ray_rank + L.ray_world - 1) / L.ray_world) * 32 : 0;
+    T.slots = T.local_tile_slots + ((T.add_corners && L.ray_rank == 0) ? 4 : 0);
     const bool wide = max_ray_voxels(L.cam, L.range, m->desc.voxel_size) > kInt32MaxVoxels;
     const int sk = store_kind(m);
-    const TraceFn fn = kTraceFns[wide][m->layout == kLayoutMorton][sk];
+    const TraceFn fn = kTraceFns[L.ray_world > 1][wide][m->layout == kLayoutMorton][sk];
     const int fi = (wide ? 6 : 0) + (m->layout == kLayoutMorton ? 3 : 0) + sk;
     if (ctx->trace_blocks_per_sm == 0) {
         // smallest shared-memory carveout that holds the walk queues of the resident blocks,
         // so the rest of the SM's 256 KB stays L1 for the map lines
         const int carve = trace_carveout();
         if (carve >= 0)
-            for (auto &a : kTraceFns)
-                for (auto &b : a)
-                    for (TraceFn f : b)
-                        NBT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            for (auto &sh : kTraceFns)
+                for (auto &a : sh)
+                    for (auto &b : a)
+                        for (TraceFn f : b)
+                            NBT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
         for (int k = 0; k < 12; ++k) {
             int b = 0;
-            NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kTraceFns[k / 6][(k / 3) & 1][k % 3],
+            NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kTraceFns[0][k / 6][(k / 3) & 1][k % 3],
                                                                    kWarpsPerBlock * 32, 0));
             ctx->trace_bps[k] = b > 0 ? b : 1;
         }
@@ -920,16 +949,19 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     long long want_blocks = (tc + kWarpsPerBlock - 1) / kWarpsPerBlock;
     long long max_blocks = (long long)ctx->num_sms * bps;
     int blocks = (int)(want_blocks < max_blocks ? want_blocks : max_blocks);
-    {
+    if (blocks > 0 && !L.d_totals_final) {
         ProfScope ps(ctx, NBT_KERNEL_TRACE);
         fn<<<dim3(blocks), dim3(kWarpsPerBlock * 32), 0, ctx->stream>>>(T);
         NBT_LAUNCHED(ctx);
     }
 
+    if (L.d_totals_trace) return NBT_OK;   // ray shard: partial totals only
     int ne = L.cam.width * L.cam.height + (L.cam.add_corners ? 4 : 0);
     ProfScope ps(ctx, NBT_KERNEL_FINALIZE);
     k_id_finalize<<<(L.n + 127) / 128, 128, 0, ctx->stream>>>(
-        A, ctx->frames.as<int32_t>(), ctx->totals.as<unsigned long long>(), m->desc.gain[0], m->desc.gain[1],
+        A, ctx->frames.as<int32_t>(),
+        L.d_totals_final ? reinterpret_cast<const unsigned long long *>(L.d_totals_final) : tot,
+        m->desc.gain[0], m->desc.gain[1],
         m->desc.gain[2], m->prob ? 1 : 0, (double)ne, L.d_xyz_out, L.d_gain_out,
         reinterpret_cast<unsigned long long *>(L.d_counts_out));
     NBT_LAUNCHED(ctx);

@@ -229,6 +229,9 @@ struct IdLaunch {
     double *d_xyz_out;       // n x 3
     double *d_gain_out;      // n
     uint64_t *d_counts_out;  // n x 4 or null
+    int32_t ray_rank = 0, ray_world = 1;      // ray shard (nbt_id_compute_rays)
+    uint64_t *d_totals_trace = nullptr;       // ray shard: trace into these n x 5 totals, no finalize
+    const uint64_t *d_totals_final = nullptr; // nbt_id_finalize: no trace, finalize these totals
 };
 nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L);
 nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const int32_t *d_e, int32_t n_rays,

@@ -1070,22 +1070,48 @@ nbt_status nbt_sample_perspectives(nbt_ctx ctx, const double poi[3], double r_s,
 
 // ----------------------------------------------------------------- the ID
 
+// Ray-shard / split-finalize options of the ID entry points (nbt_id_compute_rays,
+// nbt_id_finalize); the defaults are the whole ID.
+struct IdExtra {
+    int32_t ray_rank = 0, ray_world = 1;
+    uint64_t *totals_trace = nullptr;
+    const uint64_t *totals_final = nullptr;
+};
+
+// A caller's device array must live on the ctx's device (device or managed memory).
+static nbt_status check_device_ptr(nbt_ctx ctx, const void *p, const std::string &what)
+{
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(NBT_ERR_INVALID_ARG, what + ": not a device pointer");
+    }
+    if ((a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) || a.device != ctx->device)
+        return fail(NBT_ERR_INVALID_ARG, what + ": must be device memory on the ctx's device");
+    return NBT_OK;
+}
+
 static nbt_status id_common(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp, int32_t n_persp,
                             int persp_on_device, int32_t first, int32_t stride, const nbt_camera *cam, double range,
-                            nbt_ig_cloud *out, const char *who)
+                            nbt_ig_cloud *out, const char *who, const IdExtra &x = IdExtra())
 {
     nbt_status s;
     if ((s = bind(ctx))) return s;
     if (!m || m->ctx != ctx) return fail(NBT_ERR_STATE, std::string(who) + ": map belongs to another ctx");
-    if (!poi || !finite3(poi) || !out || n_persp < 0 || !(range > 0) || !isfinite(range))
+    const bool shard = x.totals_trace != nullptr;        // partial totals, no cloud
+    if (!poi || !finite3(poi) || (!out && !shard) || n_persp < 0 || !(range > 0) || !isfinite(range))
         return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": bad argument");
     if ((s = check_camera(cam))) return s;
     if (first < 0 || stride < 1) return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": bad first/stride");
-    if (ctx->capturing && (!persp_on_device || !out->on_device))
+    if (ctx->capturing && (!persp_on_device || (!shard && !out->on_device)))
         return fail(NBT_ERR_STATE, std::string(who) + ": host buffers during graph capture");
     int32_t n = (first < n_persp) ? (n_persp - first + stride - 1) / stride : 0;
     if (n == 0) return NBT_OK;
-    if (!persp || !out->xyz || !out->gain) return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": null buffer");
+    if (!persp || (!shard && (!out->xyz || !out->gain)))
+        return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": null buffer");
+    if (shard && (s = check_device_ptr(ctx, x.totals_trace, std::string(who) + ": totals_out"))) return s;
+    if (x.totals_final && (s = check_device_ptr(ctx, x.totals_final, std::string(who) + ": totals"))) return s;
     const double *dpersp = persp;
     if (!persp_on_device) {
         for (int32_t i = 0; i < n; ++i) {
@@ -1108,6 +1134,11 @@ static nbt_status id_common(nbt_ctx ctx, nbt_map m, const double poi[3], const d
     for (int k = 0; k < 3; ++k) L.poi[k] = poi[k];
     L.cam = *cam;
     L.range = range;
+    L.ray_rank = x.ray_rank;
+    L.ray_world = x.ray_world;
+    L.d_totals_trace = x.totals_trace;
+    L.d_totals_final = x.totals_final;
+    if (shard) return launch_id(ctx, m, L);
     size_t xyz_b = (size_t)n * 24, gain_b = (size_t)n * 8, cnt_b = (size_t)n * 32;
     if (out->on_device) {
         L.d_xyz_out = out->xyz;
@@ -1144,6 +1175,31 @@ nbt_status nbt_id_compute_slice(nbt_ctx ctx, nbt_map m, const double poi[3], con
 {
     return id_common(ctx, m, poi, persp_xyz, n_persp, persp_on_device, first, stride, cam, range, out,
                      "nbt_id_compute_slice");
+}
+
+nbt_status nbt_id_compute_rays(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp_xyz,
+                               int32_t n_persp, int persp_on_device, int32_t ray_rank, int32_t ray_world,
+                               const nbt_camera *cam, double range, uint64_t *totals_out)
+{
+    if (ray_world < 1 || ray_rank < 0 || ray_rank >= ray_world || !totals_out)
+        return fail(NBT_ERR_INVALID_ARG, "nbt_id_compute_rays: need 0 <= ray_rank < ray_world and totals_out");
+    IdExtra x;
+    x.ray_rank = ray_rank;
+    x.ray_world = ray_world;
+    x.totals_trace = totals_out;
+    return id_common(ctx, m, poi, persp_xyz, n_persp, persp_on_device, 0, 1, cam, range, nullptr,
+                     "nbt_id_compute_rays", x);
+}
+
+nbt_status nbt_id_finalize(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp_xyz, int32_t n_persp,
+                           int persp_on_device, const nbt_camera *cam, double range, const uint64_t *totals,
+                           nbt_ig_cloud *out)
+{
+    if (!totals) return fail(NBT_ERR_INVALID_ARG, "nbt_id_finalize: null totals");
+    IdExtra x;
+    x.totals_final = totals;
+    return id_common(ctx, m, poi, persp_xyz, n_persp, persp_on_device, 0, 1, cam, range, out, "nbt_id_finalize",
+                     x);
 }
 
 // ---------------------------------------------------------- ID buffer + IDW

@@ -13,8 +13,13 @@ exchange, both real data movement of the method:
 * the IG point cloud -- each rank computes a strided slice of the perspective set
   (perspective j -> rank j mod G, so cheap in-object and expensive open-space
   perspectives spread evenly), and one all-gather assembles the cloud in input order on
-  every rank, where the IDW query runs.
+  every rank, where the IDW query runs;
+* the ray split (fewer perspectives than GPUs, e.g. one perspective at full resolution):
+  every rank walks its share of each perspective's rays and one all-reduce sums the
+  integer totals before the finalize.
 
+The collectives run on torch's current stream, so the library ctx must use that stream
+(nbt.Ctx(device, torch.cuda.current_stream().cuda_stream)) for stream order to hold.
 Integer per-state totals make the result bit-identical to a single-GPU run (the g_P of a
 perspective depends only on its own totals).  The arithmetic stays in libnbt; this module
 only moves tensors.
@@ -189,3 +194,22 @@ def id_compute_sharded(nbt, ctx, m, poi, persp_dev, cam, range_, rank: int, worl
     gain = all_gather_rows(local.gain, n, world, group=group)
     counts = all_gather_rows(local.counts, n, world, group=group)
     return xyz.contiguous(), gain.contiguous(), counts.contiguous()
+
+
+def id_compute_ray_split(nbt, ctx, m, poi, persp_dev, cam, range_, rank: int, world: int, group=None):
+    """The whole ID of `persp_dev` (n x 3 CUDA tensor, identical on every rank) with the RAYS
+    of every perspective sharded over the ranks (SURVEY 8(e) ray split, for N_P < G): each
+    rank walks its 32-ray units, the integer totals are summed by one all-reduce (exact), and
+    every rank finalizes the same cloud, bit-identical to one GPU: (xyz, gain, counts)."""
+    import torch
+    import torch.distributed as dist
+    totals = nbt.id_compute_rays(ctx, m, poi, persp_dev, cam, range_, rank, world)
+    if world > 1:
+        dist.all_reduce(totals, op=dist.ReduceOp.SUM, group=group)
+    n = persp_dev.shape[0]
+    dev = persp_dev.device
+    cloud = nbt.IgCloud(torch.empty((n, 3), dtype=torch.float64, device=dev),
+                        torch.empty(n, dtype=torch.float64, device=dev),
+                        torch.empty((n, 4), dtype=torch.int64, device=dev))
+    nbt.id_finalize(ctx, m, poi, persp_dev, cam, range_, totals, out=cloud)
+    return cloud.xyz, cloud.gain, cloud.counts

@@ -93,6 +93,73 @@ def test_sharded_id_world2_gloo():
         assert ok, f"rank {rank}: {tb}"
 
 
+class _OracleRays:
+    """Stand-in for the library in the ray-split plumbing test: rank r's totals are the
+    oracle's per-ray counts summed over rays k with k mod world == r (any partition does for
+    the plumbing; the GPU tests pin libnbt's own), the finalize the canonical Q26 form."""
+
+    def __init__(self, om, ocam, gains):
+        self.om, self.ocam, self.gains = om, ocam, gains
+        from paper_2503_22588_b200 import IgCloud
+        self.IgCloud = IgCloud
+
+    def id_compute_rays(self, ctx, m, poi, persp, cam, range_, rank, world):
+        import oracle
+        rows = []
+        for p in persp.numpy():
+            rc = oracle.perspective_rays(self.om, poi, p, self.ocam, range_)[2]
+            rows.append(np.append(rc[rank::world, :4].sum(0), 0))
+        return torch.from_numpy(np.array(rows, dtype=np.int64))
+
+    def id_finalize(self, ctx, m, poi, persp, cam, range_, totals, out):
+        import oracle
+        t = totals.numpy().astype(np.float64)
+        gu, gf, go = self.gains
+        out.xyz.copy_(persp)
+        out.gain.copy_(torch.from_numpy(((t[:, 0] * gu + t[:, 1] * gf) + t[:, 2] * go) / oracle.num_rays(self.ocam)))
+        out.counts.copy_(totals[:, :4])
+
+
+def _ray_worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle
+        from nbt_inputs import CONFIGS, FOV_H, FOV_V
+        cfg = CONFIGS["A"]
+        om = oracle.OracleMap(cfg.map_codes(), voxel_size=cfg.voxel_size)
+        ocam = oracle.camera_from_fov(FOV_H, FOV_V, 20, 15)
+        P = oracle.sample_perspectives(cfg.poi, 20.0, 3, seed=9)        # fewer perspectives than ranks
+        fake = _OracleRays(om, ocam, (1.0, 0.12, 0.03))
+        xyz, gain, counts = ndist.id_compute_ray_split(fake, None, None, cfg.poi, torch.from_numpy(P), None,
+                                                       cfg.range_, rank, world)
+        _, g, c = oracle.id_compute(om, cfg.poi, P, ocam, cfg.range_)
+        ok = (np.array_equal(xyz.numpy(), P) and np.array_equal(counts.numpy(), c)
+              and np.array_equal(gain.numpy(), g))
+        q.put((rank, bool(ok), ""))
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+
+
+def test_ray_split_world4_gloo():
+    """N_P = 3 < G = 4: rays sharded, integer totals all-reduced, identical clouds everywhere."""
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ray_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, tb in res:
+        assert ok, f"rank {rank}: {tb}"
+
+
 @pytest.mark.parametrize("n,world", [(13, 2), (16, 4), (3, 8), (4096, 8), (1, 1)])
 def test_unstride_roundtrip(n, world):
     full = np.arange(n * 2).reshape(n, 2)

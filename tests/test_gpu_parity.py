@@ -343,6 +343,88 @@ def test_slices_and_device_io(nbt, ctx):
     assert np.array_equal(out.counts.cpu().numpy().astype(np.uint64), full.counts)
 
 
+def _ray_owner(w, h, corners, world):
+    """Shard of every ray (row-major k = kk*W + i, then the 4 corner rays), as include/nbt.h
+    states for nbt_id_compute_rays: 8x4-pixel tile units (or runs of 32 rays), dealt
+    round-robin; corner rays to shard 0."""
+    kk, i = np.divmod(np.arange(w * h), w)
+    if w >= 8 and h >= 4:
+        unit = (kk // 4) * ((w + 7) // 8) + i // 8
+    else:
+        unit = np.arange(w * h) // 32
+    owner = unit % world
+    return np.concatenate([owner, np.zeros(4, np.int64)]) if corners else owner
+
+
+@pytest.mark.parametrize("w,h,corners,worlds", [(24, 17, True, (1, 2, 3, 7)), (5, 3, False, (1, 2, 5)),
+                                                (64, 48, False, (2, 8)), (7, 30, True, (3,))])
+def test_ray_split_matches_oracle(nbt, ctx, w, h, corners, worlds):
+    """Ray shards (SURVEY 8(e) ray split): each shard's integer totals equal the oracle's
+    per-ray counts summed over the rays the header assigns it; the shards' sum finalizes to
+    the whole ID bit for bit; shards without rays return zeros."""
+    import torch
+    cfg = CONFIGS["A"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    n = 9
+    P = oracle.sample_perspectives(cfg.poi, 20.0, n, seed=21)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, w, h)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, w, h)
+    cam.add_corners = ocam.add_corners = int(corners)
+    full = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
+    per_ray = [oracle.perspective_rays(om, cfg.poi, p, ocam, cfg.range_)[2] for p in P]
+    dP = torch.from_numpy(P).cuda()
+    for world in worlds:
+        owner = _ray_owner(w, h, corners, world)
+        total = torch.zeros((n, nbt.ID_TOTALS), dtype=torch.int64, device="cuda")
+        for r in range(world):
+            t = nbt.id_compute_rays(ctx, m, cfg.poi, P if r % 2 else dP, cam, cfg.range_, r, world)
+            ctx.sync()
+            want = np.stack([rc[owner == r, :4].sum(0) for rc in per_ray])
+            assert np.array_equal(t.cpu().numpy()[:, :4], want), (world, r)
+            total += t
+        torch.cuda.synchronize()                      # the adds ran on torch's stream
+        fin = nbt.id_finalize(ctx, m, cfg.poi, P, cam, cfg.range_, total)
+        assert np.array_equal(fin.xyz, P)
+        assert np.array_equal(fin.counts, full.counts)
+        assert np.array_equal(fin.gain, full.gain)
+
+
+def test_ray_split_prob_map_and_misuse(nbt, ctx):
+    """8-bit store: the summed T_G finalizes to the exact Eq. 2 gains; bad shard arguments and
+    host totals are rejected."""
+    import ctypes
+    import torch
+    p, obs = _prob_scene((22, 26, 30), seed=5)
+    codes, levels = oracle.quantize_prob(p, obs)
+    m = nbt.Map(ctx, nbt.map_desc(30, 26, 22, 1.0), prob=True)
+    m.upload_prob(p, obs)
+    om = oracle.OracleMap(codes, levels=levels)
+    poi = np.array([15.5, 13.5, 11.5])
+    P = oracle.sample_perspectives(poi, 10.0, 12, seed=4)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 40, 33)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, 40, 33)
+    _, g, c, tg = oracle.id_compute(om, poi, P, ocam, 30.0, nthreads=NTHREADS, with_tg=True)
+    parts = [nbt.id_compute_rays(ctx, m, poi, P, cam, 30.0, r, 4) for r in range(4)]
+    ctx.sync()
+    total = sum(parts)
+    torch.cuda.synchronize()
+    assert np.array_equal(total.cpu().numpy()[:, :4], c)
+    assert np.array_equal(total.cpu().numpy()[:, 4], tg)
+    fin = nbt.id_finalize(ctx, m, poi, P, cam, 30.0, total)
+    assert np.array_equal(fin.gain, g)
+    for r, world in [(4, 4), (-1, 2), (0, 0)]:
+        with pytest.raises(nbt.NbtError):
+            nbt.id_compute_rays(ctx, m, poi, P, cam, 30.0, r, world)
+    with pytest.raises(TypeError):
+        nbt.id_finalize(ctx, m, poi, P, cam, 30.0, total.cpu())
+    host = np.zeros((12, 5), np.uint64)                   # a host array through the raw ABI
+    pp = np.ascontiguousarray(poi)
+    st = nbt.lib().nbt_id_compute_rays(ctx.h, m.h, ctypes.c_void_p(pp.ctypes.data),
+                                       ctypes.c_void_p(P.ctypes.data), 12, 0, 0, 1, ctypes.byref(cam),
+                                       30.0, ctypes.c_void_p(host.ctypes.data))
+    assert st == 1 and (host == 0).all()
+
+
 def test_deterministic_and_permutation(nbt, ctx):
     cfg = CONFIGS["A"]
     m, _ = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)

@@ -5,6 +5,7 @@
 
 Every rank holds a replica of the map (NCCL / gloo broadcast of the packed store), applies
 the same broadcast deltas, computes its strided shard of an ID and all-gathers the IG cloud,
+walks its ray shard of a few perspectives and all-reduces the integer totals (ray split),
 and integrates the same broadcast depth frame.  Checks, across ranks: identical map and
 occupancy replicas (digests), and a gathered cloud bit-identical to the unsharded ID that
 rank 0 computes with the same library.  Uses only libnbt (no oracle).  Prints
@@ -79,6 +80,16 @@ def main():
     assert torch.equal(xyz, persp), "gathered perspectives out of order"
     assert np.array_equal(gain.cpu().numpy(), np.asarray(full.gain)), "sharded g_P differ"
     assert np.array_equal(counts.cpu().numpy().astype(np.uint64), np.asarray(full.counts).astype(np.uint64))
+
+    # ray split (fewer perspectives than ranks): every rank walks its ray units of the same
+    # perspectives, one all-reduce of the integer totals, the same cloud as the unsharded ID
+    few = persp[:max(1, world - 1)].contiguous()
+    xyz_r, gain_r, counts_r = ndist.id_compute_ray_split(nbt, ctx, m, cfg.poi, few, cam, cfg.range_, rank, world)
+    ctx.sync()
+    k = few.shape[0]
+    assert torch.equal(xyz_r, few), "ray split: perspectives differ"
+    assert np.array_equal(gain_r.cpu().numpy(), np.asarray(full.gain)[:k]), "ray split: g_P differ"
+    assert np.array_equal(counts_r.cpu().numpy().astype(np.uint64), np.asarray(full.counts)[:k].astype(np.uint64))
 
     # sharded IDW queries over the gathered cloud == all queries on one rank
     buf = nbt.IdBuffer(ctx, 4, n_p)
