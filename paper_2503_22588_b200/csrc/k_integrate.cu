@@ -155,10 +155,15 @@ __global__ void __launch_bounds__(256) k_filter_centroid(const double *__restric
 // ------------------------------------------------------- voxel filter by hashing (integration)
 // The integration only needs each cell's centroid, not the cells in key order (the rays are
 // applied as a set, Q35), so it groups points with a hash table instead of a full sort:
-// insert each point's cell key (linear probing, atomicCAS), count per slot, scan the counts,
-// scatter point indices into their slot's segment (arbitrary order), then place each point
-// at its rank among the segment's indices -- the segment holds its points in input order, so
-// the centroid is the same in-order sum as the sort path's, bit for bit.
+// insert each point's cell key (linear probing, atomicCAS), count per slot and keep its
+// lowest point index, scan the counts, scatter point indices into their slot's segment
+// (arbitrary order), then place each point at its rank among the segment's indices -- the
+// segment holds its points in input order, so the centroid is the same in-order sum as the
+// sort path's, bit for bit.  Ranking by scanning the segment costs O(len) per point, so cells
+// of more than kBigCell points skip it and their centroid group sums them by walking the input
+// in order from the cell's first point: a frame whose points share few cells stays far from
+// quadratic (a stable radix sort by slot instead of the ranking was robust too but made every
+// camera frame 30% slower).
 
 constexpr unsigned long long kEmptyKey = ~0ull;
 
@@ -169,9 +174,11 @@ __device__ __forceinline__ uint32_t hash_slot(unsigned long long key, int log2ca
     return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - log2cap));
 }
 
+constexpr uint32_t kBigCell = 512;    // cells with more points: ordered warp walk, no ranking
+
 __global__ void k_hash_insert(const double *__restrict__ pts, uint32_t n, double leaf, int log2cap,
-                              unsigned long long *table, uint32_t *count, uint32_t *__restrict__ slot_of, int *bad,
-                              int *err)
+                              unsigned long long *table, uint32_t *count, uint32_t *first_inv,
+                              uint32_t *__restrict__ slot_of, int *bad, int *err)
 {
     const uint32_t mask = (1u << log2cap) - 1u;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -204,6 +211,7 @@ __global__ void k_hash_insert(const double *__restrict__ pts, uint32_t n, double
                 h = (h + 1u) & mask;
             }
             atomicAdd(count + h, (uint32_t)__popc(peers));
+            atomicMax(first_inv + h, ~i);            // ~(lowest index); the leader holds the peers' lowest
         }
         h = __shfl_sync(peers, h, leader);
         slot_of[i] = h;
@@ -211,11 +219,11 @@ __global__ void k_hash_insert(const double *__restrict__ pts, uint32_t n, double
 }
 
 __global__ void k_hash_scatter(const uint32_t *__restrict__ slot_of, uint32_t n, const uint32_t *__restrict__ off,
-                               uint32_t *fill, uint32_t *__restrict__ seg)
+                               const uint32_t *__restrict__ count, uint32_t *fill, uint32_t *__restrict__ seg)
 {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t h = slot_of[i];
-        if (h == 0xffffffffu) continue;
+        if (h == 0xffffffffu || count[h] > kBigCell) continue;
         seg[off[h] + atomicAdd(fill + h, 1u)] = i;
     }
 }
@@ -226,16 +234,18 @@ __global__ void k_hash_scatter(const uint32_t *__restrict__ slot_of, uint32_t n,
 // deterministic order.
 __global__ void k_hash_place(const double *__restrict__ pts, const uint32_t *__restrict__ slot_of, uint32_t n,
                              const uint32_t *__restrict__ off, const uint32_t *__restrict__ count,
-                             const uint32_t *__restrict__ seg, double *__restrict__ sorted, uint8_t *__restrict__ head)
+                             const uint32_t *__restrict__ first_inv, const uint32_t *__restrict__ seg,
+                             double *__restrict__ sorted, uint8_t *__restrict__ head)
 {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t h = slot_of[i];
         head[i] = 0;
         if (h == 0xffffffffu) continue;
+        head[i] = first_inv[h] == ~i;
         const uint32_t b = off[h], len = count[h];
+        if (len > kBigCell) continue;                 // summed by an ordered walk (k_hash_centroid)
         uint32_t rank = 0;
         for (uint32_t k = 0; k < len; ++k) rank += seg[b + k] < i ? 1u : 0u;
-        head[i] = rank == 0;
         const size_t d = 3 * (size_t)(b + rank);
         sorted[d] = pts[3 * (size_t)i];
         sorted[d + 1] = pts[3 * (size_t)i + 1];
@@ -244,17 +254,25 @@ __global__ void k_hash_place(const double *__restrict__ pts, const uint32_t *__r
 }
 
 // Cell c = occupied slot cells[c]: run [off, off + count) of the placed points; the same
-// 8-lane in-order sum as k_filter_centroid.
+// 8-lane in-order sum as k_filter_centroid.  A cell of more than kBigCell points (not placed)
+// is summed by its 8-lane group walking the INPUT in order from the cell's first point, 8
+// points per step: the group's points of a step (ballot) are added in lane order through
+// shuffles -- the same sequential in-order sum -- until all the cell's points are in.
 __global__ void __launch_bounds__(256) k_hash_centroid(const double *__restrict__ sorted,
+                                                       const double *__restrict__ pts,
+                                                       const uint32_t *__restrict__ slot_of, uint32_t n,
                                                        const uint32_t *__restrict__ cells,
                                                        const uint32_t *__restrict__ n_cells,
                                                        const uint32_t *__restrict__ off,
                                                        const uint32_t *__restrict__ count,
+                                                       const uint32_t *__restrict__ first_inv,
                                                        double *__restrict__ out, uint32_t *__restrict__ n_out)
 {
+    const unsigned full = 0xffffffffu;
     const uint32_t m = *n_cells;
     if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = m;
     const uint32_t sub = threadIdx.x & (kCentroidLanes - 1);
+    const uint32_t group_shift = lane_id() & ~(kCentroidLanes - 1);
     const uint32_t groups = gridDim.x * (blockDim.x / kCentroidLanes);
     const uint32_t g0 = (blockIdx.x * blockDim.x + threadIdx.x) / kCentroidLanes;
     const uint32_t warp_g0 = g0 - (lane_id() / kCentroidLanes);
@@ -262,11 +280,13 @@ __global__ void __launch_bounds__(256) k_hash_centroid(const double *__restrict_
         const uint32_t c = cw + lane_id() / kCentroidLanes;
         const bool live = c < m;
         const uint32_t h = live ? cells[c] : 0u;
-        const uint32_t b = live ? off[h] : 0u;
-        const uint32_t len = live ? count[h] : 0u;
+        const uint32_t len_all = live ? count[h] : 0u;
+        const bool bigc = len_all > kBigCell;
+        const uint32_t b = live && !bigc ? off[h] : 0u;
+        const uint32_t len = bigc ? 0u : len_all;
         const uint32_t e = b + len;
         uint32_t rounds = (len + kCentroidLanes - 1) / kCentroidLanes;
-        rounds = __reduce_max_sync(0xffffffffu, rounds);
+        rounds = __reduce_max_sync(full, rounds);
         double sx = 0.0, sy = 0.0, sz = 0.0;
         for (uint32_t r = 0; r < rounds; ++r) {
             const uint32_t k = b + r * kCentroidLanes + sub;
@@ -278,9 +298,9 @@ __global__ void __launch_bounds__(256) k_hash_centroid(const double *__restrict_
             }
 #pragma unroll
             for (int j = 0; j < kCentroidLanes; ++j) {
-                const double xj = __shfl_sync(0xffffffffu, x, j, kCentroidLanes);
-                const double yj = __shfl_sync(0xffffffffu, y, j, kCentroidLanes);
-                const double zj = __shfl_sync(0xffffffffu, z, j, kCentroidLanes);
+                const double xj = __shfl_sync(full, x, j, kCentroidLanes);
+                const double yj = __shfl_sync(full, y, j, kCentroidLanes);
+                const double zj = __shfl_sync(full, z, j, kCentroidLanes);
                 if (r * kCentroidLanes + j < len) {
                     sx = __dadd_rn(sx, xj);
                     sy = __dadd_rn(sy, yj);
@@ -288,8 +308,36 @@ __global__ void __launch_bounds__(256) k_hash_centroid(const double *__restrict_
                 }
             }
         }
+        if (__any_sync(full, bigc)) {                  // rare: ordered walk over the input
+            uint32_t base = bigc ? ~first_inv[h] : n, done = 0;
+            while (__any_sync(full, bigc && done < len_all && base < n)) {
+                const bool act = bigc && done < len_all && base < n;
+                const uint32_t i = base + sub;
+                const bool mine = act && i < n && slot_of[i] == h;
+                double x = 0.0, y = 0.0, z = 0.0;
+                if (mine) {
+                    x = pts[3 * (size_t)i];
+                    y = pts[3 * (size_t)i + 1];
+                    z = pts[3 * (size_t)i + 2];
+                }
+                const uint32_t bits = (__ballot_sync(full, mine) >> group_shift) & 0xffu;
+                done += __popc(bits);
+#pragma unroll
+                for (int j = 0; j < kCentroidLanes; ++j) {
+                    const double xj = __shfl_sync(full, x, j, kCentroidLanes);
+                    const double yj = __shfl_sync(full, y, j, kCentroidLanes);
+                    const double zj = __shfl_sync(full, z, j, kCentroidLanes);
+                    if ((bits >> j) & 1u) {
+                        sx = __dadd_rn(sx, xj);
+                        sy = __dadd_rn(sy, yj);
+                        sz = __dadd_rn(sz, zj);
+                    }
+                }
+                base += kCentroidLanes;
+            }
+        }
         if (live && sub == 0) {
-            const double dn = (double)len;
+            const double dn = (double)len_all;
             out[3 * (size_t)c] = __ddiv_rn(sx, dn);
             out[3 * (size_t)c + 1] = __ddiv_rn(sy, dn);
             out[3 * (size_t)c + 2] = __ddiv_rn(sz, dn);
@@ -621,22 +669,22 @@ static nbt_status launch_voxel_filter_hashed(nbt_ctx ctx, nbt_occ_s *o, const do
     int log2cap = 10;
     while ((1ull << log2cap) < 2ull * n) ++log2cap;
     const size_t cap = 1ull << log2cap;
-    if ((st = o->hkeys.ensure(cap * 8)) || (st = o->hcount.ensure(cap * 12)) ||
+    if ((st = o->hkeys.ensure(cap * 8)) || (st = o->hcount.ensure(cap * 16)) ||
         (st = o->cells.ensure((size_t)n * 5 + 16)) ||
         (st = o->idx.ensure((size_t)n * 4)) || (st = o->idx_alt.ensure((size_t)n * 4)) ||
         (st = o->sorted.ensure((size_t)n * 24)) || (st = o->filtered.ensure((size_t)n * 24)))
         return st;
     auto *table = o->hkeys.as<unsigned long long>();
-    uint32_t *count = o->hcount.as<uint32_t>(), *fill = count + cap, *off = fill + cap;
+    uint32_t *count = o->hcount.as<uint32_t>(), *fill = count + cap, *first_inv = fill + cap, *off = first_inv + cap;
     uint32_t *cells = o->cells.as<uint32_t>(), *n_cells = cells + n;
     uint8_t *head = reinterpret_cast<uint8_t *>(n_cells + 4);
     uint32_t *slot_of = o->idx.as<uint32_t>(), *seg = o->idx_alt.as<uint32_t>();
     uint32_t *ctl = reinterpret_cast<uint32_t *>(o->d_ctl);
     NBT_CUDA(cudaMemsetAsync(table, 0xff, cap * 8, ctx->stream));
-    NBT_CUDA(cudaMemsetAsync(count, 0, cap * 8, ctx->stream));          // count and fill
+    NBT_CUDA(cudaMemsetAsync(count, 0, cap * 12, ctx->stream));         // count, fill, first_inv
     const unsigned gr = grid_for(ctx, n, 256, 8);
-    k_hash_insert<<<gr, 256, 0, ctx->stream>>>(d_pts, n, leaf, log2cap, table, count, slot_of, o->d_ctl + kOccBad,
-                                               ctx->d_err);
+    k_hash_insert<<<gr, 256, 0, ctx->stream>>>(d_pts, n, leaf, log2cap, table, count, first_inv, slot_of,
+                                               o->d_ctl + kOccBad, ctx->d_err);
     NBT_LAUNCHED(ctx);
     size_t t1 = 0, t2 = 0;
     NBT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t1, count, off, (int)cap, ctx->stream));
@@ -645,14 +693,16 @@ static nbt_status launch_voxel_filter_hashed(nbt_ctx ctx, nbt_occ_s *o, const do
     if ((st = o->cub_tmp.ensure(tmp))) return st;
     size_t tt = tmp;
     NBT_CUDA(cub::DeviceScan::ExclusiveSum(o->cub_tmp.p, tt, count, off, (int)cap, ctx->stream));
-    k_hash_scatter<<<gr, 256, 0, ctx->stream>>>(slot_of, n, off, fill, seg);
+    k_hash_scatter<<<gr, 256, 0, ctx->stream>>>(slot_of, n, off, count, fill, seg);
     NBT_LAUNCHED(ctx);
-    k_hash_place<<<gr, 256, 0, ctx->stream>>>(d_pts, slot_of, n, off, count, seg, o->sorted.as<double>(), head);
+    k_hash_place<<<gr, 256, 0, ctx->stream>>>(d_pts, slot_of, n, off, count, first_inv, seg,
+                                              o->sorted.as<double>(), head);
     NBT_LAUNCHED(ctx);
     tt = tmp;
     NBT_CUDA(cub::DeviceSelect::Flagged(o->cub_tmp.p, tt, slot_of, head, cells, n_cells, (int)n, ctx->stream));
     k_hash_centroid<<<grid_for(ctx, (size_t)n * kCentroidLanes, 256, 8), 256, 0, ctx->stream>>>(
-        o->sorted.as<double>(), cells, n_cells, off, count, o->filtered.as<double>(), ctl + kOccRays);
+        o->sorted.as<double>(), d_pts, slot_of, n, cells, n_cells, off, count, first_inv, o->filtered.as<double>(),
+        ctl + kOccRays);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }

@@ -250,6 +250,34 @@ def test_integrate_exact_ties_and_long_rays(nbt, ctx, monkeypatch):
         assert same_logodds(occ.download(), L), f"max_range {mr}"
 
 
+def test_integrate_few_dense_cells(nbt, ctx):
+    """Degenerate grouping: 400 k points in a handful of filter cells (a coarse leaf, and a
+    cloud of identical points) -- bit-exact centroids and store, and fast (the grouping must
+    not be quadratic in the points per cell)."""
+    import time
+    n = 40
+    rng = np.random.default_rng(3)
+    sensor = np.array([2.0, 3.0, 4.0])
+    blob = np.array([30.0, 25.0, 20.0]) + rng.normal(0, 3.0, (400_000, 3))
+    same = np.tile(np.array([[31.3, 11.7, 8.2]]), (400_000, 1))
+    for pts, leaf in ((blob, 16.0), (same, 1.0)):
+        want, wcnt = oracle.voxel_filter(pts, leaf)
+        got, gcnt = nbt.voxel_filter(ctx, pts, leaf)
+        assert np.array_equal(gcnt, wcnt) and np.array_equal(got.view(np.uint64), want.view(np.uint64))
+        L = oracle.new_logodds((n, n, n))
+        oracle.integrate(L, 1.0, (0, 0, 0), sensor, pts, leaf=leaf, max_range=0.0)
+        occ = nbt.OccMap(ctx, nbt.map_desc(n, n, n, 1.0))
+        prm = nbt.integrate_params(1.0, leaf=leaf, max_range=0.0)
+        occ.integrate(sensor, pts, params=prm)                     # warm-up
+        occ = nbt.OccMap(ctx, nbt.map_desc(n, n, n, 1.0))
+        t0 = time.perf_counter()
+        occ.integrate(sensor, pts, params=prm)
+        ctx.sync()
+        dt = time.perf_counter() - t0
+        assert same_logodds(occ.download(), L)
+        assert dt < 0.25, f"{dt:.3f} s for one frame"
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_integrate_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
     """Random non-cubic grids (voxel size, origin), sensors inside or outside, random point
