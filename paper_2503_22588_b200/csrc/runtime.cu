@@ -6,8 +6,13 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+#include <condition_variable>
+#include <mutex>
 #include <new>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "nbt_internal.cuh"
 
@@ -88,6 +93,105 @@ void HostStage::release()
     pending = false;
 }
 
+// Host copies into and out of the pinned stages.  One memcpy thread moves ~10 GB/s, so a
+// large input (a 640x576 depth frame is 8.8 MB) is copied by a few persistent worker threads
+// in chunks, and the caller issues each chunk's DMA as soon as the chunk is staged: the host
+// copy, the PCIe transfer and the workers overlap.  NBT_COPY_THREADS sets the number of
+// workers (default 4 on hosts with >= 8 hardware threads; 0 = plain memcpy on the caller).
+class CopyPool {
+public:
+    static CopyPool &get()
+    {
+        static CopyPool *pool = new CopyPool();   // never destroyed: idle workers end with the process
+        return *pool;
+    }
+    static constexpr size_t kChunk = 512u << 10;
+    static constexpr size_t kMinParallel = 1u << 20;
+
+    // Copy src -> dst; on_chunk(offset, len) is called on the caller's thread for every
+    // chunk, in order, as soon as that chunk has landed.
+    template <typename F>
+    void copy(void *dst, const void *src, size_t bytes, F &&on_chunk)
+    {
+        if (workers_.empty() || bytes < kMinParallel) {
+            memcpy(dst, src, bytes);
+            on_chunk(0, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> caller(call_mu_);
+        const size_t n_chunks = (bytes + kChunk - 1) / kChunk;
+        if (done_.size() < n_chunks) {
+            std::vector<std::atomic<uint32_t>> fresh(n_chunks);
+            done_.swap(fresh);
+        }
+        for (size_t i = 0; i < n_chunks; ++i) done_[i].store(0, std::memory_order_relaxed);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = static_cast<char *>(dst);
+            src_ = static_cast<const char *>(src);
+            bytes_ = bytes;
+            n_chunks_ = n_chunks;
+            next_.store(0, std::memory_order_relaxed);
+            active_ = (int)workers_.size();
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (size_t i = 0; i < n_chunks; ++i) {
+            while (done_[i].load(std::memory_order_acquire) == 0) std::this_thread::yield();
+            const size_t off = i * kChunk;
+            on_chunk(off, bytes - off < kChunk ? bytes - off : kChunk);
+        }
+        std::unique_lock<std::mutex> lk(mu_);        // workers are done with dst/src
+        idle_cv_.wait(lk, [&] { return active_ == 0; });
+    }
+    void copy(void *dst, const void *src, size_t bytes)
+    {
+        copy(dst, src, bytes, [](size_t, size_t) {});
+    }
+
+private:
+    CopyPool()
+    {
+        int n = 0;
+        if (const char *e = getenv("NBT_COPY_THREADS")) {
+            n = atoi(e);
+        } else {
+            n = std::thread::hardware_concurrency() >= 8 ? 4 : 0;
+        }
+        for (int k = 0; k < n; ++k) workers_.emplace_back([this] { run(); });
+    }
+    void run()
+    {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+            }
+            for (;;) {
+                const size_t i = next_.fetch_add(1, std::memory_order_relaxed);
+                if (i >= n_chunks_) break;
+                const size_t off = i * kChunk;
+                memcpy(dst_ + off, src_ + off, bytes_ - off < kChunk ? bytes_ - off : kChunk);
+                done_[i].store(1, std::memory_order_release);
+            }
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--active_ == 0) idle_cv_.notify_one();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::vector<std::atomic<uint32_t>> done_;
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, idle_cv_;
+    char *dst_ = nullptr;
+    const char *src_ = nullptr;
+    size_t bytes_ = 0, n_chunks_ = 0;
+    std::atomic<size_t> next_{0};
+    int active_ = 0;
+    uint64_t gen_ = 0;
+};
+
 // Copy a host array into device scratch through a pinned stage (async, stream-ordered).
 static nbt_status stage_h2d(nbt_ctx ctx, HostStage &st, DevBuf &dst, const void *src, size_t bytes)
 {
@@ -103,8 +207,13 @@ static nbt_status stage_h2d(nbt_ctx ctx, HostStage &st, DevBuf &dst, const void 
         return NBT_OK;
     }
     if ((s = st.acquire(bytes))) return s;
-    memcpy(st.p, src, bytes);
-    NBT_CUDA(cudaMemcpyAsync(dst.p, st.p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    cudaError_t e = cudaSuccess;
+    CopyPool::get().copy(st.p, src, bytes, [&](size_t off, size_t len) {
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(static_cast<char *>(dst.p) + off, static_cast<char *>(st.p) + off, len,
+                                cudaMemcpyHostToDevice, ctx->stream);
+    });
+    if (e != cudaSuccess) return cuda_fail(e, "stage_h2d");
     return st.mark(ctx->stream);
 }
 
@@ -116,7 +225,7 @@ static nbt_status d2h_sync(nbt_ctx ctx, void *dst, const void *src, size_t bytes
     if ((s = ctx->stage_out.acquire(bytes))) return s;
     NBT_CUDA(cudaMemcpyAsync(ctx->stage_out.p, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     NBT_CUDA(cudaStreamSynchronize(ctx->stream));
-    memcpy(dst, ctx->stage_out.p, bytes);
+    CopyPool::get().copy(dst, ctx->stage_out.p, bytes);
     return NBT_OK;
 }
 
