@@ -389,6 +389,29 @@ def test_ray_split_matches_oracle(nbt, ctx, w, h, corners, worlds):
         assert np.array_equal(fin.gain, full.gain)
 
 
+@pytest.mark.parametrize("layout", ["linear", "morton"])
+@pytest.mark.parametrize("range_", [30.0, 800.0])
+def test_ray_split_layouts_and_wide_rays(nbt, ctx, layout, range_, monkeypatch):
+    """The ray-shard kernel instances of both map layouts and of the 64-bit walk (rays over
+    700 voxels per axis): shard totals sum to the whole ID's, which equals the oracle's."""
+    import torch
+    monkeypatch.setenv("NBT_MAP_LAYOUT", layout)
+    codes = rand_map(0, 0.35, 0.64, 0.01, seed=11, shape=(40, 44, 48))
+    m, om = make_map(nbt, ctx, codes)
+    poi = np.array([24.5, 22.5, 20.5])
+    P = oracle.sample_perspectives(poi, 15.0, 6, seed=5)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 21, 13)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, 21, 13)
+    _, g, c = oracle.id_compute(om, poi, P, ocam, range_, nthreads=NTHREADS)
+    parts = [nbt.id_compute_rays(ctx, m, poi, P, cam, range_, r, 3) for r in range(3)]
+    ctx.sync()
+    total = sum(parts)
+    torch.cuda.synchronize()
+    assert np.array_equal(total.cpu().numpy()[:, :4], c)
+    fin = nbt.id_finalize(ctx, m, poi, P, cam, range_, total)
+    assert np.array_equal(fin.gain, g)
+
+
 def test_ray_split_prob_map_and_misuse(nbt, ctx):
     """8-bit store: the summed T_G finalizes to the exact Eq. 2 gains; bad shard arguments and
     host totals are rejected."""
