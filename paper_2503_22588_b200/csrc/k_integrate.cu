@@ -381,8 +381,14 @@ __device__ __forceinline__ bool to_q12(double x, double org, double s, int &out)
 // start state to the next piece's start.
 constexpr int kDedupSteps = 32;
 constexpr int kRayThreads = 256;
-constexpr int kPieceEvents = 24;                          // dominant-axis events per piece
-constexpr int kPieceSlots = 8;                            // threads per ray (pieces j, j + 8, ...)
+#ifndef NBT_PIECE_EVENTS
+#define NBT_PIECE_EVENTS 24
+#endif
+#ifndef NBT_PIECE_SLOTS
+#define NBT_PIECE_SLOTS 8
+#endif
+constexpr int kPieceEvents = NBT_PIECE_EVENTS;            // dominant-axis events per piece
+constexpr int kPieceSlots = NBT_PIECE_SLOTS;              // threads per ray (pieces j, j + 8, ...)
 
 __device__ __forceinline__ long long floor_div_ll(long long a, long long b)   // b > 0
 {
