@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--unprofiled-graphs", action="store_true", help="experiment: graphs without event nodes")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--gather", choices=["nccl", "p2p"], default="nccl",
+                    help="N > 1: IG-cloud all-gather over NCCL, or fused into the finalize over peer memory")
     return ap.parse_args()
 
 
@@ -424,12 +426,26 @@ def main_ours(args, cfg):
 
     gathered = (nbt.IgCloud(torch.empty((n_tot, 3), dtype=torch.float64, device=dev),
                             torch.empty(n_tot, dtype=torch.float64, device=dev), None) if world > 1 else cloud)
+    p2p = world > 1 and args.gather == "p2p"
+    if p2p:
+        # the all-gather fused into the finalize: every rank stores its rows into all ranks'
+        # buffers over peer memory; one buffer suffices because the query all-gather of the
+        # previous step orders every rank's ID-buffer push before the next step's stores
+        pgather = ndist.PeerGather(nbt, ctx, n_tot, rank, world, n_buffers=1)
+        gc = pgather.bufs[0].cloud()
+        gathered = nbt.IgCloud(gc.xyz, gc.gain, None)
+        cloud = nbt.IgCloud(gc.xyz[rank * n_p:(rank + 1) * n_p], gc.gain[rank * n_p:(rank + 1) * n_p],
+                            gc.counts[rank * n_p:(rank + 1) * n_p])
+        token = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def part_a(c):                      # rows a2-a8 on this rank
         m.update(d_ijk[c], d_val[c])                                             # a2
         nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_p, 1000003 * c + rank, cfg.persp_mode,
                                 out=persp)                                       # a3
-        nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=cloud)       # a4-a8
+        if p2p:                                                                  # a4-a8 + the gather
+            pgather.bufs[0].compute(m, cfg.poi, persp, cam, cfg.range_, first=0, stride=1, row0=rank * n_p)
+        else:
+            nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=cloud)   # a4-a8
 
     def part_b():                       # row a9 on the assembled cloud
         buf.push(gathered, n_tot)
@@ -447,7 +463,13 @@ def main_ours(args, cfg):
             ndist.broadcast_deltas(d_ijk[c], d_val[c], src=0)
 
     def exchange_cloud():
-        if world > 1:
+        if p2p:
+            # order every rank's peer stores before any rank's push: a one-word all-reduce on
+            # the stream (NCCL); gloo runs on the host, so there the stream is drained first
+            if dist.get_backend() != "nccl":
+                ctx.sync()
+            dist.all_reduce(token)
+        elif world > 1:
             gathered.xyz.copy_(ndist.all_gather_rows(cloud.xyz, n_tot, world, strided=False))
             gathered.gain.copy_(ndist.all_gather_rows(cloud.gain, n_tot, world, strided=False))
 
@@ -744,7 +766,9 @@ def main_ours(args, cfg):
             "config": {"workload": workload_name(cfg, world), "map": f"{cfg.n}^3 SYN(R_o={cfg.r_o:g}, seed "
                        f"{cfg.map_seed}) 2-bit packed", "perspectives_per_step": n_tot, "rays_per_perspective": ne,
                        "l2": "flushed before every timed step (256 MiB write, outside the step events)",
-                       "parallelism": f"perspectives sharded over {world} GPU(s), weak scaling"},
+                       "parallelism": f"perspectives sharded over {world} GPU(s), weak scaling"
+                       + ("" if world == 1 else (", IG-cloud all-gather fused into the finalize (peer memory)"
+                                                 if args.gather == "p2p" else ", IG-cloud all-gather over NCCL"))},
             "voxel_steps_per_s": visits / sec, "lookups_per_s": lookups / sec,
             "id_latency_ms": t_dev / args.steps,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32)",

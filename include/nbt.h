@@ -87,7 +87,7 @@ enum {
     NBT_KERNEL_FINALIZE = 2,    /* k_id_finalize: row a8 */
     NBT_KERNEL_IDW = 3,         /* k_idw_query: row a9 */
     NBT_KERNEL_SAMPLE = 4,      /* k_sample_perspectives: row a3 */
-    NBT_KERNEL_MAP_UPDATE = 5,  /* k_delta_keys + radix sort + k_delta_apply: row a2 */
+    NBT_KERNEL_MAP_UPDATE = 5,  /* k_delta_win + k_delta_apply_win (or the sort form): row a2 */
     NBT_KERNEL_INTEGRATE = 6,   /* voxel filter + k_integrate_rays + k_integrate_apply: row f3 */
     NBT_KERNEL_COUNT = 7
 };
@@ -307,6 +307,37 @@ nbt_status nbt_id_compute_rays(nbt_ctx ctx, nbt_map map, const double poi[3], co
 nbt_status nbt_id_finalize(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz,
                            int32_t n_persp, int persp_on_device, const nbt_camera *cam, double range,
                            const uint64_t *totals, nbt_ig_cloud *out);
+
+/* Peer-memory gather of the IG cloud (one process per GPU): the all-gather after
+ * the sharded ID is fused into the finalize kernel, which stores every computed row straight
+ * into each rank's row buffer (other GPUs' buffers mapped with CUDA IPC, so the stores cross
+ * NVLink/NVSwitch; on one GPU shared by several processes they are plain device stores).
+ *   nbt_gather_create   this rank's buffer for the whole cloud: `rows` rows, owned by the
+ *                       handle (device memory, one cudaMalloc); world <= 16, 0 <= rank < world.
+ *   nbt_gather_export   its CUDA IPC handle (NBT_PEER_HANDLE_BYTES opaque bytes) for the peers.
+ *   nbt_gather_attach   map peer_rank's exported buffer (a handle from ANOTHER process; this
+ *                       rank's own entry needs no attach).  NBT_ERR_CUDA if IPC is unavailable.
+ *   nbt_gather_rows     device pointers of this rank's buffer as a cloud (xyz rows x 3, gain
+ *                       rows, counts rows x 4; on_device = 1), e.g. for nbt_idbuf_push.
+ *   nbt_id_compute_gather  nbt_id_compute_slice(first, stride) whose finalize writes the row
+ *                       of perspective j = first + i*stride (of persp_xyz, n_persp rows) to row
+ *                       row0 + j of EVERY rank's buffer: row0 = 0 with the whole perspective
+ *                       set on every rank (strided shards), row0 = rank * n with each rank's
+ *                       own n perspectives (weak scaling).  NBT_ERR_INVALID_ARG unless
+ *                       row0 + n_persp <= rows; every rank must be attached (NBT_ERR_STATE).
+ * Ordering is the caller's: a rank may read its buffer after every rank's call has completed
+ * (e.g. each rank synchronises its stream, then a process barrier), and a buffer must not be
+ * rewritten while a peer may still read it (alternate two gathers between cycles). */
+#define NBT_PEER_HANDLE_BYTES 64
+typedef struct nbt_gather_s *nbt_gather;
+nbt_status nbt_gather_create(nbt_ctx ctx, int32_t rows, int32_t world, int32_t rank, nbt_gather *out);
+nbt_status nbt_gather_export(nbt_gather g, uint8_t handle_out[NBT_PEER_HANDLE_BYTES]);
+nbt_status nbt_gather_attach(nbt_gather g, int32_t peer_rank, const uint8_t handle[NBT_PEER_HANDLE_BYTES]);
+nbt_status nbt_gather_rows(nbt_gather g, nbt_ig_cloud *rows_out);
+nbt_status nbt_id_compute_gather(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz,
+                                 int32_t n_persp, int persp_on_device, int32_t first, int32_t stride,
+                                 int32_t row0, const nbt_camera *cam, double range, nbt_gather g);
+void       nbt_gather_destroy(nbt_gather g);
 
 /* -------------------------------------------- ID buffer + IDW query (row a9) */
 

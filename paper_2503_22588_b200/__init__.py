@@ -40,6 +40,8 @@ EXPORTS = [
     "nbt_map_get_desc", "nbt_map_destroy",
     "nbt_camera_from_fov", "nbt_camera_from_grid_scaling", "nbt_camera_num_rays",
     "nbt_sample_perspectives", "nbt_id_compute", "nbt_id_compute_slice", "nbt_id_compute_rays", "nbt_id_finalize",
+    "nbt_gather_create", "nbt_gather_export", "nbt_gather_attach", "nbt_gather_rows", "nbt_id_compute_gather",
+    "nbt_gather_destroy",
     "nbt_idbuf_create", "nbt_idbuf_push", "nbt_idbuf_clear", "nbt_idbuf_size", "nbt_ig_query", "nbt_ig_query_knn", "nbt_idbuf_destroy",
     "nbt_info_cost",
     "nbt_integrate_params_default", "nbt_occ_create", "nbt_occ_upload", "nbt_occ_download", "nbt_occ_integrate",
@@ -130,6 +132,13 @@ def lib():
         "nbt_id_compute_rays": ([vp, vp, vp, vp, i32, C.c_int, i32, i32, C.POINTER(Camera), dbl, vp], C.c_int),
         "nbt_id_finalize": ([vp, vp, vp, vp, i32, C.c_int, C.POINTER(Camera), dbl, vp, C.POINTER(IgCloudC)],
                             C.c_int),
+        "nbt_gather_create": ([vp, i32, i32, i32, C.POINTER(vp)], C.c_int),
+        "nbt_gather_export": ([vp, vp], C.c_int),
+        "nbt_gather_attach": ([vp, i32, vp], C.c_int),
+        "nbt_gather_rows": ([vp, C.POINTER(IgCloudC)], C.c_int),
+        "nbt_id_compute_gather": ([vp, vp, vp, vp, i32, C.c_int, i32, i32, i32, C.POINTER(Camera), dbl, vp],
+                                  C.c_int),
+        "nbt_gather_destroy": ([vp], None),
         "nbt_idbuf_create": ([vp, i32, i32, C.POINTER(vp)], C.c_int),
         "nbt_idbuf_push": ([vp, C.POINTER(IgCloudC), i32], C.c_int),
         "nbt_idbuf_clear": ([vp], C.c_int),
@@ -602,6 +611,69 @@ def nbt_id_finalize(ctx: Ctx, m: Map, poi, persp, cam: Camera, range_, totals, o
 
 id_compute_rays = nbt_id_compute_rays
 id_finalize = nbt_id_finalize
+
+PEER_HANDLE_BYTES = 64
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3}
+
+
+class Gather:
+    """Peer-memory gather buffer of the IG cloud (nbt_gather_*): this rank's rows of the whole
+    cloud, filled by every rank's Gather.compute through CUDA IPC mappings."""
+
+    def __init__(self, ctx: Ctx, rows: int, world: int, rank: int):
+        h = C.c_void_p()
+        check(lib().nbt_gather_create(ctx.h, int(rows), int(world), int(rank), C.byref(h)))
+        self.h, self.ctx, self.rows, self.world, self.rank = h, ctx, int(rows), int(world), int(rank)
+
+    def export(self) -> bytes:
+        buf = (C.c_uint8 * PEER_HANDLE_BYTES)()
+        check(lib().nbt_gather_export(self.h, buf))
+        return bytes(buf)
+
+    def attach(self, peer_rank: int, handle: bytes):
+        buf = (C.c_uint8 * PEER_HANDLE_BYTES).from_buffer_copy(bytes(handle))
+        check(lib().nbt_gather_attach(self.h, int(peer_rank), buf))
+
+    def cloud(self) -> IgCloud:
+        """This rank's whole cloud as CUDA tensors viewing the library's buffer."""
+        import torch
+        oc = IgCloudC()
+        check(lib().nbt_gather_rows(self.h, C.byref(oc)))
+        n = self.rows
+        return IgCloud(torch.as_tensor(_DevArray(oc.xyz, (n, 3), "<f8"), device=f"cuda:{self.ctx.device}"),
+                       torch.as_tensor(_DevArray(oc.gain, (n,), "<f8"), device=f"cuda:{self.ctx.device}"),
+                       torch.as_tensor(_DevArray(oc.counts, (n, 4), "<i8"), device=f"cuda:{self.ctx.device}"))
+
+    def compute(self, m: Map, poi, persp, cam: Camera, range_, first=None, stride=None, row0=0):
+        """Perspectives first, first + stride, ... of `persp` (default: the strided shard
+        rank, rank + world, ... of the whole set) into rows row0 + j of every rank's buffer."""
+        pp, keep = _poi(poi)
+        pper, dev, kp = _ptr(persp, np.float64)
+        if _count(kp) % 3:
+            raise ValueError("perspectives must be (n, 3) float64")
+        n = _count(kp) // 3
+        first = self.rank if first is None else first
+        stride = self.world if stride is None else stride
+        check(lib().nbt_id_compute_gather(self.ctx.h, m.h, pp, pper, int(n), dev, int(first), int(stride),
+                                          int(row0), C.byref(cam), float(range_), self.h))
+
+    def close(self):
+        if self.h:
+            lib().nbt_gather_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 class IdBuffer:

@@ -697,6 +697,37 @@ __global__ void k_id_finalize(FrameArgs A, const int32_t *__restrict__ frames,
     }
 }
 
+// The finalize of a shard fused with the all-gather: row i of this call (perspective
+// first + i*stride of the call's array) is row row0 + first + i*stride of the whole cloud, written (same values as k_id_finalize) into every
+// destination's row buffer -- the other ranks' buffers are peer mappings, so the stores
+// travel over NVLink/NVSwitch.
+__global__ void k_id_finalize_gather(FrameArgs A, const int32_t *__restrict__ frames,
+                                     const unsigned long long *__restrict__ totals, double g_u, double g_f,
+                                     double g_o, int prob, double n_e, int32_t row0,
+                                     const __grid_constant__ GatherDst dst)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const size_t src = (size_t)A.first + (size_t)i * A.stride;
+    const size_t row = (size_t)row0 + src;
+    const double *pp = A.persp + 3 * src;
+    const double px = pp[0], py = pp[1], pz = pp[2];
+    const unsigned long long *t = totals + kTotals * (size_t)i;
+    const unsigned long long tu = t[0], tf = t[1], to = t[2], tl = t[3], tg = t[4];
+    double g = prob ? __ddiv_rn((double)tg, __dmul_rn(63.0, n_e))
+                    : __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn((double)tu, g_u), __dmul_rn((double)tf, g_f)),
+                                          __dmul_rn((double)to, g_o)),
+                                n_e);
+    if (frames[(size_t)i * kFrameInts + 18] != 0) g = __longlong_as_double(0x7ff8000000000000LL);   // NaN
+    for (int d = 0; d < dst.n; ++d) {
+        double *x = dst.xyz[d] + 3 * row;
+        x[0] = px; x[1] = py; x[2] = pz;
+        dst.gain[d][row] = g;
+        unsigned long long *c = dst.counts[d] + 4 * row;
+        c[0] = tu; c[1] = tf; c[2] = to; c[3] = tl;
+    }
+}
+
 // ------------------------------------------------------------ debug hooks
 
 // Per-ray walk of an explicit Q12 segment, recording every visited voxel; the same
@@ -958,6 +989,13 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     if (L.d_totals_trace) return NBT_OK;   // ray shard: partial totals only
     int ne = L.cam.width * L.cam.height + (L.cam.add_corners ? 4 : 0);
     ProfScope ps(ctx, NBT_KERNEL_FINALIZE);
+    if (L.gather) {
+        k_id_finalize_gather<<<(L.n + 127) / 128, 128, 0, ctx->stream>>>(
+            A, ctx->frames.as<int32_t>(), tot, m->desc.gain[0], m->desc.gain[1], m->desc.gain[2], m->prob ? 1 : 0,
+            (double)ne, L.gather_row0, *L.gather);
+        NBT_LAUNCHED(ctx);
+        return NBT_OK;
+    }
     k_id_finalize<<<(L.n + 127) / 128, 128, 0, ctx->stream>>>(
         A, ctx->frames.as<int32_t>(),
         L.d_totals_final ? reinterpret_cast<const unsigned long long *>(L.d_totals_final) : tot,

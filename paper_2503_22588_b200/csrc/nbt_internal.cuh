@@ -184,6 +184,24 @@ struct nbt_idbuf_s {
     double *d_gain = nullptr;         // capacity x max_persp
 };
 
+// Peer-memory gather of the IG cloud (multi-GPU): every rank's finalize writes
+// its rows straight into all ranks' row buffers (mapped with CUDA IPC; over NVLink/NVSwitch
+// when the owner is another GPU), so the all-gather is fused into the finalize kernel.
+constexpr int kMaxGatherRanks = 16;
+struct GatherDst {
+    int n = 0;                                      // destinations
+    double *xyz[kMaxGatherRanks] = {};
+    double *gain[kMaxGatherRanks] = {};
+    unsigned long long *counts[kMaxGatherRanks] = {};
+};
+
+struct nbt_gather_s {
+    nbt_ctx ctx = nullptr;
+    int32_t rows = 0, world = 0, rank = 0;
+    char *base = nullptr;             // local rows: xyz rows*24 | gain rows*8 | counts rows*32
+    char *peer[kMaxGatherRanks] = {}; // rank r's rows (own: base; others: opened IPC mappings)
+};
+
 struct nbt_occ_s {
     nbt_ctx ctx = nullptr;
     nbt_map_desc desc{};
@@ -232,6 +250,8 @@ struct IdLaunch {
     int32_t ray_rank = 0, ray_world = 1;      // ray shard (nbt_id_compute_rays)
     uint64_t *d_totals_trace = nullptr;       // ray shard: trace into these n x 5 totals, no finalize
     const uint64_t *d_totals_final = nullptr; // nbt_id_finalize: no trace, finalize these totals
+    const GatherDst *gather = nullptr;        // nbt_id_compute_gather: rows to every destination
+    int32_t gather_row0 = 0;                  // ... at row gather_row0 + first + i*stride
 };
 nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L);
 nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const int32_t *d_e, int32_t n_rays,

@@ -1185,6 +1185,8 @@ struct IdExtra {
     int32_t ray_rank = 0, ray_world = 1;
     uint64_t *totals_trace = nullptr;
     const uint64_t *totals_final = nullptr;
+    const GatherDst *gather = nullptr;
+    int32_t gather_row0 = 0;
 };
 
 // A caller's device array must live on the ctx's device (device or managed memory).
@@ -1208,7 +1210,7 @@ static nbt_status id_common(nbt_ctx ctx, nbt_map m, const double poi[3], const d
     nbt_status s;
     if ((s = bind(ctx))) return s;
     if (!m || m->ctx != ctx) return fail(NBT_ERR_STATE, std::string(who) + ": map belongs to another ctx");
-    const bool shard = x.totals_trace != nullptr;        // partial totals, no cloud
+    const bool shard = x.totals_trace != nullptr || x.gather != nullptr;   // no caller cloud
     if (!poi || !finite3(poi) || (!out && !shard) || n_persp < 0 || !(range > 0) || !isfinite(range))
         return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": bad argument");
     if ((s = check_camera(cam))) return s;
@@ -1219,7 +1221,8 @@ static nbt_status id_common(nbt_ctx ctx, nbt_map m, const double poi[3], const d
     if (n == 0) return NBT_OK;
     if (!persp || (!shard && (!out->xyz || !out->gain)))
         return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": null buffer");
-    if (shard && (s = check_device_ptr(ctx, x.totals_trace, std::string(who) + ": totals_out"))) return s;
+    if (x.totals_trace && (s = check_device_ptr(ctx, x.totals_trace, std::string(who) + ": totals_out")))
+        return s;
     if (x.totals_final && (s = check_device_ptr(ctx, x.totals_final, std::string(who) + ": totals"))) return s;
     const double *dpersp = persp;
     if (!persp_on_device) {
@@ -1247,6 +1250,8 @@ static nbt_status id_common(nbt_ctx ctx, nbt_map m, const double poi[3], const d
     L.ray_world = x.ray_world;
     L.d_totals_trace = x.totals_trace;
     L.d_totals_final = x.totals_final;
+    L.gather = x.gather;
+    L.gather_row0 = x.gather_row0;
     if (shard) return launch_id(ctx, m, L);
     size_t xyz_b = (size_t)n * 24, gain_b = (size_t)n * 8, cnt_b = (size_t)n * 32;
     if (out->on_device) {
@@ -1309,6 +1314,109 @@ nbt_status nbt_id_finalize(nbt_ctx ctx, nbt_map m, const double poi[3], const do
     x.totals_final = totals;
     return id_common(ctx, m, poi, persp_xyz, n_persp, persp_on_device, 0, 1, cam, range, out, "nbt_id_finalize",
                      x);
+}
+
+// ------------------------------------------------- peer-memory gather (multi-GPU)
+
+nbt_status nbt_gather_create(nbt_ctx ctx, int32_t rows, int32_t world, int32_t rank, nbt_gather *out)
+{
+    nbt_status s;
+    if (!out) return fail(NBT_ERR_INVALID_ARG, "nbt_gather_create: null out");
+    *out = nullptr;
+    if ((s = bind(ctx))) return s;
+    if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_gather_create during graph capture");
+    if (rows < 1 || world < 1 || world > kMaxGatherRanks || rank < 0 || rank >= world)
+        return fail(NBT_ERR_INVALID_ARG, "nbt_gather_create: need rows >= 1, 1 <= world <= 16, 0 <= rank < world");
+    nbt_gather g = new (std::nothrow) nbt_gather_s();
+    if (!g) return fail(NBT_ERR_OUT_OF_MEMORY, "nbt_gather_create");
+    cudaError_t e = cudaMalloc(&g->base, (size_t)rows * 64);
+    if (e != cudaSuccess) {
+        delete g;
+        return cuda_fail(e, "nbt_gather_create");
+    }
+    g->ctx = ctx;
+    ctx_retain(ctx);
+    g->rows = rows;
+    g->world = world;
+    g->rank = rank;
+    g->peer[rank] = g->base;
+    *out = g;
+    return NBT_OK;
+}
+
+nbt_status nbt_gather_export(nbt_gather g, uint8_t handle_out[NBT_PEER_HANDLE_BYTES])
+{
+    nbt_status s;
+    if (!g || !handle_out) return fail(NBT_ERR_INVALID_ARG, "nbt_gather_export: null argument");
+    if ((s = bind(g->ctx))) return s;
+    static_assert(sizeof(cudaIpcMemHandle_t) <= NBT_PEER_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    NBT_CUDA(cudaIpcGetMemHandle(&h, g->base));
+    memset(handle_out, 0, NBT_PEER_HANDLE_BYTES);
+    memcpy(handle_out, &h, sizeof h);
+    return NBT_OK;
+}
+
+nbt_status nbt_gather_attach(nbt_gather g, int32_t peer_rank, const uint8_t handle[NBT_PEER_HANDLE_BYTES])
+{
+    nbt_status s;
+    if (!g || !handle || peer_rank < 0 || peer_rank >= (g ? g->world : 0))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_gather_attach: bad argument");
+    if (peer_rank == g->rank) return NBT_OK;           // own rows: the local buffer
+    if ((s = bind(g->ctx))) return s;
+    if (g->peer[peer_rank]) return fail(NBT_ERR_STATE, "nbt_gather_attach: rank already attached");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    void *p = nullptr;
+    NBT_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    g->peer[peer_rank] = static_cast<char *>(p);
+    return NBT_OK;
+}
+
+nbt_status nbt_gather_rows(nbt_gather g, nbt_ig_cloud *rows_out)
+{
+    if (!g || !rows_out) return fail(NBT_ERR_INVALID_ARG, "nbt_gather_rows: null argument");
+    rows_out->xyz = reinterpret_cast<double *>(g->base);
+    rows_out->gain = reinterpret_cast<double *>(g->base + (size_t)g->rows * 24);
+    rows_out->counts = reinterpret_cast<uint64_t *>(g->base + (size_t)g->rows * 32);
+    rows_out->on_device = 1;
+    return NBT_OK;
+}
+
+nbt_status nbt_id_compute_gather(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp_xyz,
+                                 int32_t n_persp, int persp_on_device, int32_t first, int32_t stride, int32_t row0,
+                                 const nbt_camera *cam, double range, nbt_gather g)
+{
+    if (!g || g->ctx != ctx) return fail(NBT_ERR_STATE, "nbt_id_compute_gather: gather of another ctx");
+    if (row0 < 0 || n_persp < 0 || (int64_t)row0 + n_persp > g->rows)
+        return fail(NBT_ERR_INVALID_ARG, "nbt_id_compute_gather: need 0 <= row0 and row0 + n_persp <= rows");
+    GatherDst dst;
+    dst.n = g->world;
+    for (int r = 0; r < g->world; ++r) {
+        if (!g->peer[r]) return fail(NBT_ERR_STATE, "nbt_id_compute_gather: rank " + std::to_string(r) +
+                                                        " not attached");
+        dst.xyz[r] = reinterpret_cast<double *>(g->peer[r]);
+        dst.gain[r] = reinterpret_cast<double *>(g->peer[r] + (size_t)g->rows * 24);
+        dst.counts[r] = reinterpret_cast<unsigned long long *>(g->peer[r] + (size_t)g->rows * 32);
+    }
+    IdExtra x;
+    x.gather = &dst;
+    x.gather_row0 = row0;
+    return id_common(ctx, m, poi, persp_xyz, n_persp, persp_on_device, first, stride, cam, range, nullptr,
+                     "nbt_id_compute_gather", x);
+}
+
+void nbt_gather_destroy(nbt_gather g)
+{
+    if (!g) return;
+    cudaSetDevice(g->ctx->device);
+    cudaStreamSynchronize(g->ctx->stream);
+    for (int r = 0; r < g->world; ++r)
+        if (g->peer[r] && r != g->rank) cudaIpcCloseMemHandle(g->peer[r]);
+    if (g->base) cudaFree(g->base);
+    nbt_ctx ctx = g->ctx;
+    delete g;
+    ctx_release(ctx);
 }
 
 // ---------------------------------------------------------- ID buffer + IDW

@@ -213,3 +213,43 @@ def id_compute_ray_split(nbt, ctx, m, poi, persp_dev, cam, range_, rank: int, wo
                         torch.empty((n, 4), dtype=torch.int64, device=dev))
     nbt.id_finalize(ctx, m, poi, persp_dev, cam, range_, totals, out=cloud)
     return cloud.xyz, cloud.gain, cloud.counts
+
+
+class PeerGather:
+    """The IG-cloud all-gather fused into the finalize over peer memory (nbt_gather_*): two
+    library-owned row buffers per rank (alternated between cycles, so a rank never rewrites a
+    buffer a peer may still read), their CUDA IPC handles exchanged once through the process
+    group, every peer's buffers mapped.  Each cycle, every rank's finalize stores its rows
+    into all ranks' current buffers; a stream sync plus a process barrier then orders the
+    readers after every rank's stores (no kernel waits on another rank's kernel)."""
+
+    def __init__(self, nbt, ctx, rows: int, rank: int, world: int, group=None, n_buffers: int = 2):
+        import torch.distributed as dist
+        self.nbt, self.ctx, self.rows, self.rank, self.world, self.group = nbt, ctx, rows, rank, world, group
+        self.bufs = [nbt.Gather(ctx, rows, world, rank) for _ in range(n_buffers)]
+        mine = [g.export() for g in self.bufs]
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        for g_idx, g in enumerate(self.bufs):
+            for r in range(world):
+                if r != rank:
+                    g.attach(r, everyone[r][g_idx])
+        self.cycle = 0
+
+    def id_compute(self, m, poi, persp_dev, cam, range_):
+        """The whole ID of `persp_dev` (identical on every rank), perspective j computed by rank
+        j mod world and stored into every rank's buffer: returns this rank's (xyz, gain, counts)
+        CUDA tensors viewing the current buffer (valid until the buffer is reused two cycles on)."""
+        import torch.distributed as dist
+        g = self.bufs[self.cycle % len(self.bufs)]
+        self.cycle += 1
+        g.compute(m, poi, persp_dev, cam, range_)
+        self.ctx.sync()
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        c = g.cloud()
+        return c.xyz, c.gain, c.counts
+
+    def close(self):
+        for g in self.bufs:
+            g.close()

@@ -6,6 +6,7 @@
 Every rank holds a replica of the map (NCCL / gloo broadcast of the packed store), applies
 the same broadcast deltas, computes its strided shard of an ID and all-gathers the IG cloud,
 walks its ray shard of a few perspectives and all-reduces the integer totals (ray split),
+gathers the cloud through peer memory with the finalize-fused all-gather (nbt_gather_*),
 and integrates the same broadcast depth frame.  Checks, across ranks: identical map and
 occupancy replicas (digests), and a gathered cloud bit-identical to the unsharded ID that
 rank 0 computes with the same library.  Uses only libnbt (no oracle).  Prints
@@ -80,6 +81,35 @@ def main():
     assert torch.equal(xyz, persp), "gathered perspectives out of order"
     assert np.array_equal(gain.cpu().numpy(), np.asarray(full.gain)), "sharded g_P differ"
     assert np.array_equal(counts.cpu().numpy().astype(np.uint64), np.asarray(full.counts).astype(np.uint64))
+
+    # the all-gather fused into the finalize over peer memory (CUDA IPC; plain device stores
+    # when the ranks share one GPU): every rank's buffer holds the unsharded ID, two cycles so
+    # both alternating buffers are used
+    pg = ndist.PeerGather(nbt, ctx, n_p, rank, world)
+    for _ in range(2):
+        xyz_p, gain_p, counts_p = pg.id_compute(m, cfg.poi, persp, cam, cfg.range_)
+        assert torch.equal(xyz_p, persp), "peer gather: perspectives out of order"
+        assert np.array_equal(gain_p.cpu().numpy(), np.asarray(full.gain)), "peer gather: g_P differ"
+        assert np.array_equal(counts_p.cpu().numpy().astype(np.uint64), np.asarray(full.counts).astype(np.uint64))
+        dist.barrier()
+    pg.close()
+    # weak-scaling form: each rank's own perspectives into rows rank*k .. rank*k + k-1, equal
+    # to the collective all-gather of the ranks' own IDs
+    k_own = 9
+    own = torch.empty((k_own, 3), dtype=torch.float64, device=dev)
+    nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, k_own, 100 + rank, cfg.persp_mode, out=own)
+    mine = nbt.id_compute(ctx, m, cfg.poi, own, cam, cfg.range_, out=nbt.empty_cloud(k_own, device=dev))
+    ctx.sync()
+    want_g = ndist.all_gather_rows(mine.gain, k_own * world, world, strided=False)
+    want_c = ndist.all_gather_rows(mine.counts, k_own * world, world, strided=False)
+    pw = ndist.PeerGather(nbt, ctx, k_own * world, rank, world, n_buffers=1)
+    pw.bufs[0].compute(m, cfg.poi, own, cam, cfg.range_, first=0, stride=1, row0=rank * k_own)
+    ctx.sync()
+    dist.barrier()
+    got = pw.bufs[0].cloud()
+    assert torch.equal(got.gain, want_g) and torch.equal(got.counts, want_c), "peer gather (weak form) differs"
+    dist.barrier()
+    pw.close()
 
     # ray split (fewer perspectives than ranks): every rank walks its ray units of the same
     # perspectives, one all-reduce of the integer totals, the same cloud as the unsharded ID
