@@ -313,7 +313,7 @@ def run_integration(nbt, ctx, stream, dev, flush, reps=2):
     return out
 
 
-def run_config_d(nbt, ndist, ctx, stream, dev, rank, world, reps=3):
+def run_config_d(nbt, ndist, ctx, stream, dev, rank, world, reps=3, gather="nccl"):
     """Config D (512^3 SYN map, 4096 perspectives x 160x120 rays, range 3.86 m): the whole ID
     sharded j -> rank j mod G and all-gathered in input order on every rank; device time per
     ID (CUDA events on the shared stream), max over ranks."""
@@ -329,7 +329,15 @@ def run_config_d(nbt, ndist, ctx, stream, dev, rank, world, reps=3):
     cam = nbt.camera_from_fov(FOV_H, FOV_V, cd.width, cd.height)
     persp = torch.empty((cd.n_persp, 3), dtype=torch.float64, device=dev)
     nbt.sample_perspectives(ctx, cd.poi, cd.persp_radius, cd.n_persp, cd.persp_seed, cd.persp_mode, out=persp)
-    ndist.id_compute_sharded(nbt, ctx, m, cd.poi, persp, cam, cd.range_, rank, world)       # warm-up
+    if world > 1 and gather == "p2p":
+        pg = ndist.PeerGather(nbt, ctx, cd.n_persp, rank, world)
+
+        def whole_id():
+            return pg.id_compute(m, cd.poi, persp, cam, cd.range_)
+    else:
+        def whole_id():
+            return ndist.id_compute_sharded(nbt, ctx, m, cd.poi, persp, cam, cd.range_, rank, world)
+    whole_id()                                                                            # warm-up
     times = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(reps):
@@ -337,7 +345,7 @@ def run_config_d(nbt, ndist, ctx, stream, dev, rank, world, reps=3):
             dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        xyz, gain, counts = ndist.id_compute_sharded(nbt, ctx, m, cd.poi, persp, cam, cd.range_, rank, world)
+        xyz, gain, counts = whole_id()
         e1.record(stream)
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
@@ -347,11 +355,14 @@ def run_config_d(nbt, ndist, ctx, stream, dev, rank, world, reps=3):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    if world > 1 and gather == "p2p":
+        pg.close()
     m.close()
     return {"config": f"D: {cd.n}^3 SYN map (2-bit), {cd.n_persp} perspectives x {cd.width}x{cd.height} rays, "
                       f"range {cd.range_} m, sharded j -> rank j mod {world}, all-gathered",
             "n_gpus": world, "id_ms": ms, "rays_per_s": cd.rays_per_id / (ms / 1e3),
-            "lookups_per_s": lookups / (ms / 1e3), "reps": reps, "scaling": "strong"}
+            "lookups_per_s": lookups / (ms / 1e3), "reps": reps, "scaling": "strong",
+            "gather": "fused into the finalize (peer memory)" if world > 1 and gather == "p2p" else "NCCL"}
 
 
 def main_ours(args, cfg):
@@ -436,7 +447,6 @@ def main_ours(args, cfg):
         gathered = nbt.IgCloud(gc.xyz, gc.gain, None)
         cloud = nbt.IgCloud(gc.xyz[rank * n_p:(rank + 1) * n_p], gc.gain[rank * n_p:(rank + 1) * n_p],
                             gc.counts[rank * n_p:(rank + 1) * n_p])
-        token = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def part_a(c):                      # rows a2-a8 on this rank
         m.update(d_ijk[c], d_val[c])                                             # a2
@@ -464,11 +474,7 @@ def main_ours(args, cfg):
 
     def exchange_cloud():
         if p2p:
-            # order every rank's peer stores before any rank's push: a one-word all-reduce on
-            # the stream (NCCL); gloo runs on the host, so there the stream is drained first
-            if dist.get_backend() != "nccl":
-                ctx.sync()
-            dist.all_reduce(token)
+            pgather.order_readers()     # every rank's peer stores before any rank's push
         elif world > 1:
             gathered.xyz.copy_(ndist.all_gather_rows(cloud.xyz, n_tot, world, strided=False))
             gathered.gain.copy_(ndist.all_gather_rows(cloud.gain, n_tot, world, strided=False))
@@ -613,7 +619,7 @@ def main_ours(args, cfg):
     #      sharded across the ranks (strong scaling: strided slices + NCCL all-gather of the cloud)
     strong = None
     if cfg.name == "B" and not args.no_config_d:
-        strong = run_config_d(nbt, ndist, ctx, stream, dev, rank, world)
+        strong = run_config_d(nbt, ndist, ctx, stream, dev, rank, world, gather=args.gather)
 
     # ---- row f3: map integration of depth frames (the step before the path)
     integ = None

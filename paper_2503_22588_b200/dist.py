@@ -244,11 +244,23 @@ class PeerGather:
         g = self.bufs[self.cycle % len(self.bufs)]
         self.cycle += 1
         g.compute(m, poi, persp_dev, cam, range_)
-        self.ctx.sync()
-        if self.world > 1:
-            dist.barrier(group=self.group)
+        self.order_readers()
         c = g.cloud()
         return c.xyz, c.gain, c.counts
+
+    def order_readers(self):
+        """Order every later read of this rank (in its stream) after all ranks' stores: a
+        word-sized all-reduce on the stream under NCCL (no host synchronisation); gloo works
+        on the host, so there the stream is drained first."""
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        if dist.get_backend(self.group) != "nccl":
+            self.ctx.sync()
+        if not hasattr(self, "_token"):
+            self._token = torch.zeros(1, dtype=torch.int64, device=torch.device("cuda", self.ctx.device))
+        dist.all_reduce(self._token, group=self.group)
 
     def close(self):
         for g in self.bufs:
