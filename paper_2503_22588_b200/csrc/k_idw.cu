@@ -310,10 +310,36 @@ __global__ void k_idbuf_advance(int32_t *meta, int32_t cap, int32_t n)
     meta[0] = meta[0] + 1;
 }
 
+// Small clouds: copy and advance in one single-block launch (every thread reads the slot
+// before the barrier, thread 0 advances the ring after it).
+constexpr int kPushOneBlock = 1024;
+__global__ void __launch_bounds__(kPushOneBlock) k_idbuf_push_small(int32_t *meta, int32_t cap, int32_t max_persp,
+                                                                    const double *__restrict__ src_xyz,
+                                                                    const double *__restrict__ src_gain, int32_t n,
+                                                                    double *__restrict__ xyz, double *__restrict__ gain)
+{
+    const int slot = meta[0] % cap;
+    for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) {
+        if (i < 3 * n) xyz[(size_t)slot * max_persp * 3 + i] = src_xyz[i];
+        else gain[(size_t)slot * max_persp + (i - 3 * n)] = src_gain[i - 3 * n];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        meta[1 + slot] = n;
+        meta[0] = meta[0] + 1;
+    }
+}
+
 }  // namespace
 
 nbt_status launch_idbuf_push(nbt_ctx ctx, nbt_idbuf_s *b, const double *d_xyz, const double *d_gain, int32_t n)
 {
+    if (4 * n <= 8 * kPushOneBlock) {
+        k_idbuf_push_small<<<1, kPushOneBlock, 0, ctx->stream>>>(b->d_meta, b->capacity, b->max_persp, d_xyz, d_gain,
+                                                                 n, b->d_xyz, b->d_gain);
+        NBT_LAUNCHED(ctx);
+        return NBT_OK;
+    }
     k_idbuf_copy<<<(4 * n + 255) / 256, 256, 0, ctx->stream>>>(b->d_meta, b->capacity, b->max_persp, d_xyz, d_gain,
                                                                   n, b->d_xyz, b->d_gain);
     NBT_LAUNCHED(ctx);
