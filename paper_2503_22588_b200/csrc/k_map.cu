@@ -171,6 +171,45 @@ __global__ void k_delta_apply_win(const int32_t *__restrict__ ijk, const uint8_t
     if (old != nw) atomicXor(w, (old ^ nw) << sh);
 }
 
+// Small delta sets: both passes in one single-block launch, the block barrier between them
+// (every atomicMax of the block is performed before any winner test reads the array).
+constexpr int kDeltaOneBlock = 1024;
+#ifndef NBT_DELTA_SMALL
+#define NBT_DELTA_SMALL (8 * kDeltaOneBlock)     // largest delta set of the single-block form
+#endif
+__global__ void __launch_bounds__(kDeltaOneBlock)
+    k_delta_win_apply_small(const int32_t *__restrict__ ijk, const uint8_t *__restrict__ codes,
+                            const uint8_t *__restrict__ levels, uint32_t n, Geom g, uint32_t *win, uint32_t *words,
+                            int *err)
+{
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int x = ijk[3 * i], y = ijk[3 * i + 1], z = ijk[3 * i + 2];
+        const bool ok = x >= 0 && y >= 0 && z >= 0 && x < g.nx && y < g.ny && z < g.nz && codes[i] <= 2 &&
+                        (!levels || levels[i] <= 63);
+        if (!ok) {
+            atomicCAS(err, 0, (int)NBT_ERR_INVALID_ARG);
+            continue;
+        }
+        atomicMax(win + ((uint32_t)x + (uint32_t)g.nx * ((uint32_t)y + (uint32_t)g.ny * (uint32_t)z)), i + 1u);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int x = ijk[3 * i], y = ijk[3 * i + 1], z = ijk[3 * i + 2];
+        if (x < 0 || y < 0 || z < 0 || x >= g.nx || y >= g.ny || z >= g.nz) continue;
+        const uint32_t lin = (uint32_t)x + (uint32_t)g.nx * ((uint32_t)y + (uint32_t)g.ny * (uint32_t)z);
+        if (*(volatile uint32_t *)(win + lin) != i + 1u) continue;     // a later delta of this voxel wins
+        win[lin] = 0u;
+        const uint64_t pi = store_index(g, (uint32_t)x, (uint32_t)y, (uint32_t)z);
+        uint32_t *w = words + word_of(g, pi);
+        const uint32_t sh = shift_of(g, pi);
+        const uint32_t mask = g.vbits == 2 ? 3u : 0xffu;
+        const uint32_t c = codes[i];
+        const uint32_t nw = stored_value(g, c, levels ? levels[i] : g.def_level[c]);
+        const uint32_t old = (*(volatile uint32_t *)w >> sh) & mask;
+        if (old != nw) atomicXor(w, (old ^ nw) << sh);
+    }
+}
+
 // Dense codes (and, for the 8-bit store, the probability levels) of the grid.
 __global__ void k_map_unpack(const uint32_t *__restrict__ words, Geom g, uint8_t *__restrict__ codes,
                              uint8_t *__restrict__ levels)
@@ -253,6 +292,12 @@ nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const
         }
     }
     if (m->d_win) {
+        if (n <= NBT_DELTA_SMALL) {
+            k_delta_win_apply_small<<<1, kDeltaOneBlock, 0, ctx->stream>>>(d_ijk, d_codes, d_levels, nn, geom_of(m),
+                                                                          m->d_win, m->d_words, ctx->d_err);
+            NBT_LAUNCHED(ctx);
+            return NBT_OK;
+        }
         k_delta_win<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(d_ijk, d_codes, d_levels, nn, m->desc.nx,
                                                                  m->desc.ny, m->desc.nz, m->d_win, ctx->d_err);
         NBT_LAUNCHED(ctx);

@@ -98,11 +98,13 @@ def _apply_in_order(codes, ijk, vals):
     return out
 
 
+@pytest.mark.parametrize("n", [5000, 20000])
 @pytest.mark.parametrize("form", ["winner", "sort"])
 @pytest.mark.parametrize("on_device", [False, True])
-def test_map_update_last_wins(nbt, ctx, on_device, form, monkeypatch):
+def test_map_update_last_wins(nbt, ctx, on_device, form, n, monkeypatch):
     """Duplicated voxels resolve to the last delta (Q30), in both update forms (the
-    winner array, and the radix sort used when the array is absent), over repeated updates."""
+    winner array -- one single-block launch up to 8192 deltas, two grid-wide passes above --
+    and the radix sort used when the array is absent), over repeated updates."""
     import torch
     if form == "sort":
         monkeypatch.setenv("NBT_DELTA_SORT", "1")
@@ -110,7 +112,6 @@ def test_map_update_last_wins(nbt, ctx, on_device, form, monkeypatch):
     m, _ = make_map(nbt, ctx, codes)
     rng = np.random.default_rng(2)
     for rep in range(3):
-        n = 5000
         ijk = np.stack([rng.integers(0, 19, n), rng.integers(0, 17, n), rng.integers(0, 13, n)], 1).astype(np.int32)
         ijk[n // 2:] = ijk[: n - n // 2]                  # many duplicates
         vals = rng.integers(0, 3, n).astype(np.uint8)
