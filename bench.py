@@ -768,7 +768,7 @@ def main_ours(args, cfg):
         line = {
             "metric": "rays/s", "value": rays_total / sec, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": workload_name(cfg, world), "map": f"{cfg.n}^3 SYN(R_o={cfg.r_o:g}, seed "
                        f"{cfg.map_seed}) 2-bit packed", "perspectives_per_step": n_tot, "rays_per_perspective": ne,
                        "l2": "flushed before every timed step (256 MiB write, outside the step events)",
