@@ -78,6 +78,30 @@ def build_variant(name: str, defines: list[str]) -> str:
     return lib
 
 
+def build_tools() -> list[str]:
+    """Standalone CUDA tools under tools/ (e.g. the walk's instruction-mix microbenchmark)
+    into build/ at the repo root."""
+    out_dir = os.path.join(ROOT, "build")
+    os.makedirs(out_dir, exist_ok=True)
+    outs = []
+    tools = os.path.join(ROOT, "tools")
+    for f in sorted(os.listdir(tools)):
+        if not f.endswith(".cu"):
+            continue
+        src = os.path.join(tools, f)
+        exe = os.path.join(out_dir, f[:-3])
+        if os.path.exists(exe) and os.path.getmtime(exe) >= max(os.path.getmtime(p) for p in _deps() + [src]):
+            outs.append(exe)
+            continue
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+               src, "-o", exe]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        outs.append(exe)
+    return outs
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[1] == "--variant":
         print(build_variant(sys.argv[2], sys.argv[3:]))
