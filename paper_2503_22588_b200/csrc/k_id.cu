@@ -60,6 +60,11 @@ constexpr int kWarpsPerBlock = NBT_WARPS_PER_BLOCK;
 constexpr int kBatchK = NBT_BATCH_K;
 constexpr bool kPipe = NBT_PIPE;
 constexpr int kInt32MaxVoxels = 700;   // |D_a| bound (voxels) for the int32 decision terms
+#ifndef NBT_TILE_W
+#define NBT_TILE_W 8
+#endif
+constexpr int kTileW = NBT_TILE_W;       // a warp's 32 rays: a kTileW x kTileH pixel tile
+constexpr int kTileH = 32 / kTileW;
 
 // Origin outside the grid (rare): step with explicit bounds checks until the walk
 // enters the grid or ends.  Returns true if the ray is finished.
@@ -407,8 +412,8 @@ __device__ __forceinline__ bool slot_ray(const TraceArgs &T, int slot, int &mi, 
     if (T.tiled) {
         int tile = slot >> 5, l = slot & 31;
         int ty = tile / T.Wt, tx = tile - ty * T.Wt;
-        i = tx * 8 + (l & 7);
-        kk = ty * 4 + (l >> 3);
+        i = tx * kTileW + (l & (kTileW - 1));
+        kk = ty * kTileH + l / kTileW;
         if (i >= T.W || kk >= T.H) return false;
     } else {
         kk = slot / T.W;
@@ -926,9 +931,9 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     T.totals = tot;
     T.work_counter = counter;
     T.W = L.cam.width; T.H = L.cam.height; T.add_corners = L.cam.add_corners ? 1 : 0;
-    T.tiled = (T.W >= 8 && T.H >= 4) ? 1 : 0;
-    T.Wt = (T.W + 7) / 8;
-    int Ht = (T.H + 3) / 4;
+    T.tiled = (T.W >= kTileW && T.H >= kTileH) ? 1 : 0;
+    T.Wt = (T.W + kTileW - 1) / kTileW;
+    int Ht = (T.H + kTileH - 1) / kTileH;
     T.n_tile_slots = T.tiled ? T.Wt * Ht * 32 : T.W * T.H;
     // ray shard (SURVEY 8(e) ray split): units of 32 lattice slots dealt round-robin
     const int units = (T.n_tile_slots + 31) / 32;
