@@ -16,8 +16,12 @@
 //                   runs converged for 32 rays at a time into a per-warp shared-memory
 //                   queue; lanes refill from it when their ray ends.  Per-state visit
 //                   counts (Eq. 2 as integers, Q26) accumulate in registers and are
-//                   flushed with 4 u64 atomics when a lane moves to another perspective.
+//                   flushed warp-combined (one u64 atomic per counter per warp and
+//                   perspective) when lanes move to another perspective.  A separate
+//                   SHARD instance walks one ray shard (nbt_id_compute_rays).
 //   k_id_finalize   g_P = ((T_U g_U + T_F g_F) + T_O g_O) / N_E  (Q26)
+//   k_id_finalize_gather  the same rows stored into every rank's peer-mapped buffer
+//                   (the all-gather fused into the finalize, nbt_id_compute_gather)
 //
 // Exact decision with 32-bit arithmetic.  With D = E - O and
 // N_a the distance from O to the next boundary along a (Q12 units, S = 4096), the next
