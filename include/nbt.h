@@ -337,6 +337,18 @@ nbt_status nbt_gather_rows(nbt_gather g, nbt_ig_cloud *rows_out);
 nbt_status nbt_id_compute_gather(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz,
                                  int32_t n_persp, int persp_on_device, int32_t first, int32_t stride,
                                  int32_t row0, const nbt_camera *cam, double range, nbt_gather g);
+/* Ray split with the all-reduce fused into the walk (N_P < G): like
+ * nbt_id_compute_rays with ray_rank = the gather's rank and ray_world = its world, but the
+ * walk's count flushes add straight into EVERY rank's buffer, read as n_persp x NBT_ID_TOTALS
+ * uint64 totals at its start (remote atomics over the peer mappings; n_persp * 40 bytes must
+ * fit rows * 64).  Each rank first clears its own buffer with nbt_gather_zero; the caller
+ * orders all ranks' clears before any rank's call and all calls before the readers (e.g. a
+ * stream-ordered all-reduce of one word), then nbt_id_finalize turns a buffer's summed totals
+ * into the cloud -- bit-identical to nbt_id_compute on one GPU. */
+nbt_status nbt_gather_zero(nbt_gather g);
+nbt_status nbt_id_compute_rays_gather(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz,
+                                      int32_t n_persp, int persp_on_device, const nbt_camera *cam, double range,
+                                      nbt_gather g);
 void       nbt_gather_destroy(nbt_gather g);
 
 /* -------------------------------------------- ID buffer + IDW query (row a9) */

@@ -41,7 +41,7 @@ EXPORTS = [
     "nbt_camera_from_fov", "nbt_camera_from_grid_scaling", "nbt_camera_num_rays",
     "nbt_sample_perspectives", "nbt_id_compute", "nbt_id_compute_slice", "nbt_id_compute_rays", "nbt_id_finalize",
     "nbt_gather_create", "nbt_gather_export", "nbt_gather_attach", "nbt_gather_rows", "nbt_id_compute_gather",
-    "nbt_gather_destroy",
+    "nbt_gather_destroy", "nbt_gather_zero", "nbt_id_compute_rays_gather",
     "nbt_idbuf_create", "nbt_idbuf_push", "nbt_idbuf_clear", "nbt_idbuf_size", "nbt_ig_query", "nbt_ig_query_knn", "nbt_idbuf_destroy",
     "nbt_info_cost",
     "nbt_integrate_params_default", "nbt_occ_create", "nbt_occ_upload", "nbt_occ_download", "nbt_occ_integrate",
@@ -139,6 +139,8 @@ def lib():
         "nbt_id_compute_gather": ([vp, vp, vp, vp, i32, C.c_int, i32, i32, i32, C.POINTER(Camera), dbl, vp],
                                   C.c_int),
         "nbt_gather_destroy": ([vp], None),
+        "nbt_gather_zero": ([vp], C.c_int),
+        "nbt_id_compute_rays_gather": ([vp, vp, vp, vp, i32, C.c_int, C.POINTER(Camera), dbl, vp], C.c_int),
         "nbt_idbuf_create": ([vp, i32, i32, C.POINTER(vp)], C.c_int),
         "nbt_idbuf_push": ([vp, C.POINTER(IgCloudC), i32], C.c_int),
         "nbt_idbuf_clear": ([vp], C.c_int),
@@ -161,6 +163,8 @@ def lib():
         "nbt_debug_frames": ([vp, vp, vp, vp, i32, C.POINTER(Camera), dbl, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("NBT_LIB") and not hasattr(L, name):
+            continue                  # an older experiment build: only the calls it has
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
@@ -663,6 +667,26 @@ class Gather:
         stride = self.world if stride is None else stride
         check(lib().nbt_id_compute_gather(self.ctx.h, m.h, pp, pper, int(n), dev, int(first), int(stride),
                                           int(row0), C.byref(cam), float(range_), self.h))
+
+    def zero(self):
+        check(lib().nbt_gather_zero(self.h))
+
+    def compute_rays(self, m: Map, poi, persp, cam: Camera, range_):
+        """This rank's ray shard of every perspective, its counts added into every rank's buffer
+        (read as (n, 5) uint64 totals; nbt_id_compute_rays_gather)."""
+        pp, keep = _poi(poi)
+        pper, dev, kp = _ptr(persp, np.float64)
+        if _count(kp) % 3:
+            raise ValueError("perspectives must be (n, 3) float64")
+        check(lib().nbt_id_compute_rays_gather(self.ctx.h, m.h, pp, pper, _count(kp) // 3, dev, C.byref(cam),
+                                               float(range_), self.h))
+
+    def totals(self, n: int):
+        """The buffer's first n rows of totals as an (n, 5) int64 CUDA tensor view."""
+        import torch
+        oc = IgCloudC()
+        check(lib().nbt_gather_rows(self.h, C.byref(oc)))
+        return torch.as_tensor(_DevArray(oc.xyz, (n, ID_TOTALS), "<i8"), device=f"cuda:{self.ctx.device}")
 
     def close(self):
         if self.h:

@@ -404,6 +404,15 @@ struct TraceArgs {
     int local_tile_slots;       // lattice slots of this shard (its units * 32)
 };
 
+// SHARD instance: the peer totals of a fused ray split live in the work-counter buffer, after
+// the counter (n = 0: add into the call's totals).  Kept out of TraceArgs, whose layout the
+// whole-ID kernel's code generation is sensitive to (profiles/r01_ray_split_ab.log).
+constexpr int kPeerTotalsOffset = 16;   // ints
+__device__ __forceinline__ const PeerTotals *peer_totals_of(const TraceArgs &A)
+{
+    return reinterpret_cast<const PeerTotals *>(A.work_counter + kPeerTotalsOffset);
+}
+
 // Map slot -> lattice offsets (mi, mk) = (2i-(W-1), 2kk-(H-1)) or a corner ray.
 __device__ __forceinline__ bool slot_ray(const TraceArgs &T, int slot, int &mi, int &mk, int &corner)
 {
@@ -479,6 +488,42 @@ __device__ __forceinline__ void flush_counts_warp(unsigned long long *totals, in
             if (so) atomicAdd(t + 2, (unsigned long long)so);
             if (sl) atomicAdd(t + 3, (unsigned long long)sl);
             if (GAIN && sg) atomicAdd(t + 4, sg);
+        }
+        if (mine) c = Counts{0, 0, 0, 0, 0};
+        fm &= ~grp;
+    }
+}
+
+// The same flush into every rank's totals (the ray split's all-reduce fused into the walk).
+template <bool GAIN>
+__device__ __forceinline__ void flush_counts_warp_peer(const PeerTotals *pt, int jl, Counts &c, bool fl, int lane)
+{
+    const unsigned full = 0xffffffffu;
+    unsigned fm = __ballot_sync(full, fl && jl >= 0);
+    while (fm) {
+        const int leader = __ffs(fm) - 1;
+        const int pj = __shfl_sync(full, jl, leader);
+        const bool mine = fl && jl == pj;
+        const unsigned grp = __ballot_sync(full, mine);
+        const uint32_t su = __reduce_add_sync(full, mine ? c.u : 0u);
+        const uint32_t sf = __reduce_add_sync(full, mine ? c.f : 0u);
+        const uint32_t so = __reduce_add_sync(full, mine ? c.o : 0u);
+        const uint32_t sl = __reduce_add_sync(full, mine ? c.l : 0u);
+        unsigned long long sg = 0;
+        if (GAIN) {
+            sg = mine ? (unsigned long long)c.g : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sg += __shfl_xor_sync(full, sg, o);
+        }
+        if (lane == leader) {
+            for (int d = 0; d < pt->n; ++d) {       // every rank's totals, through the peer mappings
+                unsigned long long *t = pt->t[d] + kTotals * (size_t)pj;
+                if (su) atomicAdd(t + 0, (unsigned long long)su);
+                if (sf) atomicAdd(t + 1, (unsigned long long)sf);
+                if (so) atomicAdd(t + 2, (unsigned long long)so);
+                if (sl) atomicAdd(t + 3, (unsigned long long)sl);
+                if (GAIN && sg) atomicAdd(t + 4, sg);
+            }
         }
         if (mine) c = Counts{0, 0, 0, 0, 0};
         fm &= ~grp;
@@ -636,7 +681,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                 // lanes moving to another perspective flush their counts, one atomic per
                 // counter per (warp, perspective): many lanes of a warp hold the same one
                 const bool fl = j >= 0 && j != jl;
-                flush_counts_warp<VB == kStoreProb>(A.totals, jl, c, fl, lane);
+                if (SHARD && peer_totals_of(A)->n > 0)
+                    flush_counts_warp_peer<VB == kStoreProb>(peer_totals_of(A), jl, c, fl, lane);
+                else
+                    flush_counts_warp<VB == kStoreProb>(A.totals, jl, c, fl, lane);
                 if (j >= 0) {
                     jl = j;
                     have = true;
@@ -666,7 +714,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
         }
     }
     // residual counts, once per lane (the warp-combined form measured ~2% slower here)
-    if (jl >= 0) {
+    if (jl >= 0 && SHARD && peer_totals_of(A)->n > 0) {
+        const PeerTotals *pt = peer_totals_of(A);
+        for (int d = 0; d < pt->n; ++d) {
+            unsigned long long *t = pt->t[d] + kTotals * (size_t)jl;
+            if (c.u) atomicAdd(t + 0, (unsigned long long)c.u);
+            if (c.f) atomicAdd(t + 1, (unsigned long long)c.f);
+            if (c.o) atomicAdd(t + 2, (unsigned long long)c.o);
+            if (c.l) atomicAdd(t + 3, (unsigned long long)c.l);
+            if (c.g) atomicAdd(t + 4, (unsigned long long)c.g);
+        }
+    } else if (jl >= 0) {
         unsigned long long *t = A.totals + kTotals * (size_t)jl;
         if (c.u) atomicAdd(t + 0, (unsigned long long)c.u);
         if (c.f) atomicAdd(t + 1, (unsigned long long)c.f);
@@ -918,7 +976,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     // ray shard, else scratch; the finalize reads the caller's summed totals when given
     unsigned long long *tot = L.d_totals_trace ? reinterpret_cast<unsigned long long *>(L.d_totals_trace)
                                                : ctx->totals.as<unsigned long long>();
-    if ((st = ctx->counter.ensure(64))) return st;
+    if ((st = ctx->counter.ensure(kPeerTotalsOffset * 4 + sizeof(PeerTotals)))) return st;
     FrameArgs A = frame_args(m, L.d_persp, L.first, L.stride, L.n, L.poi, L.cam, L.range);
     int *counter = ctx->counter.as<int>();
     {
@@ -948,7 +1006,13 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     T.slots = T.local_tile_slots + ((T.add_corners && L.ray_rank == 0) ? 4 : 0);
     const bool wide = max_ray_voxels(L.cam, L.range, m->desc.voxel_size) > kInt32MaxVoxels;
     const int sk = store_kind(m);
-    const TraceFn fn = kTraceFns[L.ray_world > 1][wide][m->layout == kLayoutMorton][sk];
+    const bool peer = L.peer_totals != nullptr && L.peer_totals->n > 0;
+    if (L.ray_world > 1 || peer) {   // the SHARD instance reads its peer totals (n = 0: none)
+        PeerTotals none;
+        NBT_CUDA(cudaMemcpyAsync(counter + kPeerTotalsOffset, peer ? L.peer_totals : &none, sizeof(PeerTotals),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    }
+    const TraceFn fn = kTraceFns[L.ray_world > 1 || peer][wide][m->layout == kLayoutMorton][sk];
     const int fi = (wide ? 6 : 0) + (m->layout == kLayoutMorton ? 3 : 0) + sk;
     if (ctx->trace_blocks_per_sm == 0) {
         // smallest shared-memory carveout that holds the walk queues of the resident blocks,
@@ -995,7 +1059,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
         NBT_LAUNCHED(ctx);
     }
 
-    if (L.d_totals_trace) return NBT_OK;   // ray shard: partial totals only
+    if (L.d_totals_trace || L.peer_totals) return NBT_OK;   // ray shard: partial totals only
     int ne = L.cam.width * L.cam.height + (L.cam.add_corners ? 4 : 0);
     ProfScope ps(ctx, NBT_KERNEL_FINALIZE);
     if (L.gather) {

@@ -195,6 +195,13 @@ struct GatherDst {
     unsigned long long *counts[kMaxGatherRanks] = {};
 };
 
+// Ray-shard counts added straight into every rank's totals (the all-reduce of the ray split
+// fused into the trace's count flushes: remote atomics over NVLink/NVSwitch).
+struct PeerTotals {
+    int n = 0;
+    unsigned long long *t[kMaxGatherRanks] = {};
+};
+
 struct nbt_gather_s {
     nbt_ctx ctx = nullptr;
     int32_t rows = 0, world = 0, rank = 0;
@@ -252,6 +259,7 @@ struct IdLaunch {
     const uint64_t *d_totals_final = nullptr; // nbt_id_finalize: no trace, finalize these totals
     const GatherDst *gather = nullptr;        // nbt_id_compute_gather: rows to every destination
     int32_t gather_row0 = 0;                  // ... at row gather_row0 + first + i*stride
+    const PeerTotals *peer_totals = nullptr;  // nbt_id_compute_rays_gather: counts into every rank
 };
 nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L);
 nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const int32_t *d_e, int32_t n_rays,

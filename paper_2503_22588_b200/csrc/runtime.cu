@@ -1187,6 +1187,7 @@ struct IdExtra {
     const uint64_t *totals_final = nullptr;
     const GatherDst *gather = nullptr;
     int32_t gather_row0 = 0;
+    const PeerTotals *peer_totals = nullptr;
 };
 
 // A caller's device array must live on the ctx's device (device or managed memory).
@@ -1210,7 +1211,7 @@ static nbt_status id_common(nbt_ctx ctx, nbt_map m, const double poi[3], const d
     nbt_status s;
     if ((s = bind(ctx))) return s;
     if (!m || m->ctx != ctx) return fail(NBT_ERR_STATE, std::string(who) + ": map belongs to another ctx");
-    const bool shard = x.totals_trace != nullptr || x.gather != nullptr;   // no caller cloud
+    const bool shard = x.totals_trace != nullptr || x.gather != nullptr || x.peer_totals != nullptr;
     if (!poi || !finite3(poi) || (!out && !shard) || n_persp < 0 || !(range > 0) || !isfinite(range))
         return fail(NBT_ERR_INVALID_ARG, std::string(who) + ": bad argument");
     if ((s = check_camera(cam))) return s;
@@ -1252,6 +1253,7 @@ static nbt_status id_common(nbt_ctx ctx, nbt_map m, const double poi[3], const d
     L.d_totals_final = x.totals_final;
     L.gather = x.gather;
     L.gather_row0 = x.gather_row0;
+    L.peer_totals = x.peer_totals;
     if (shard) return launch_id(ctx, m, L);
     size_t xyz_b = (size_t)n * 24, gain_b = (size_t)n * 8, cnt_b = (size_t)n * 32;
     if (out->on_device) {
@@ -1404,6 +1406,37 @@ nbt_status nbt_id_compute_gather(nbt_ctx ctx, nbt_map m, const double poi[3], co
     x.gather_row0 = row0;
     return id_common(ctx, m, poi, persp_xyz, n_persp, persp_on_device, first, stride, cam, range, nullptr,
                      "nbt_id_compute_gather", x);
+}
+
+nbt_status nbt_gather_zero(nbt_gather g)
+{
+    nbt_status s;
+    if (!g) return fail(NBT_ERR_INVALID_ARG, "nbt_gather_zero: null gather");
+    if ((s = bind(g->ctx))) return s;
+    NBT_CUDA(cudaMemsetAsync(g->base, 0, (size_t)g->rows * 64, g->ctx->stream));
+    return NBT_OK;
+}
+
+nbt_status nbt_id_compute_rays_gather(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp_xyz,
+                                      int32_t n_persp, int persp_on_device, const nbt_camera *cam, double range,
+                                      nbt_gather g)
+{
+    if (!g || g->ctx != ctx) return fail(NBT_ERR_STATE, "nbt_id_compute_rays_gather: gather of another ctx");
+    if (n_persp < 0 || (int64_t)n_persp * NBT_ID_TOTALS * 8 > (int64_t)g->rows * 64)
+        return fail(NBT_ERR_INVALID_ARG, "nbt_id_compute_rays_gather: the totals do not fit the gather buffers");
+    PeerTotals pt;
+    pt.n = g->world;
+    for (int r = 0; r < g->world; ++r) {
+        if (!g->peer[r]) return fail(NBT_ERR_STATE, "nbt_id_compute_rays_gather: rank " + std::to_string(r) +
+                                                        " not attached");
+        pt.t[r] = reinterpret_cast<unsigned long long *>(g->peer[r]);
+    }
+    IdExtra x;
+    x.ray_rank = g->rank;
+    x.ray_world = g->world;
+    x.peer_totals = &pt;
+    return id_common(ctx, m, poi, persp_xyz, n_persp, persp_on_device, 0, 1, cam, range, nullptr,
+                     "nbt_id_compute_rays_gather", x);
 }
 
 void nbt_gather_destroy(nbt_gather g)

@@ -262,6 +262,24 @@ class PeerGather:
             self._token = torch.zeros(1, dtype=torch.int64, device=torch.device("cuda", self.ctx.device))
         dist.all_reduce(self._token, group=self.group)
 
+    def ray_split(self, m, poi, persp_dev, cam, range_):
+        """The ID with the RAYS of every perspective sharded over the ranks and the totals'
+        all-reduce fused into the walk (remote atomics into every rank's buffer): returns the
+        same (xyz, gain, counts) on every rank, bit-identical to one GPU."""
+        import torch
+        g = self.bufs[0]
+        n = persp_dev.shape[0]
+        g.zero()
+        self.order_readers()                 # every rank's clear before any rank's adds
+        g.compute_rays(m, poi, persp_dev, cam, range_)
+        self.order_readers()                 # every rank's adds before the finalize
+        dev = persp_dev.device
+        cloud = self.nbt.IgCloud(torch.empty((n, 3), dtype=torch.float64, device=dev),
+                                 torch.empty(n, dtype=torch.float64, device=dev),
+                                 torch.empty((n, 4), dtype=torch.int64, device=dev))
+        self.nbt.id_finalize(self.ctx, m, poi, persp_dev, cam, range_, g.totals(n), out=cloud)
+        return cloud.xyz, cloud.gain, cloud.counts
+
     def close(self):
         for g in self.bufs:
             g.close()

@@ -413,6 +413,29 @@ def test_ray_split_layouts_and_wide_rays(nbt, ctx, layout, range_, monkeypatch):
     assert np.array_equal(fin.gain, g)
 
 
+def test_ray_split_fused_into_peer_totals_one_rank(nbt, ctx):
+    """nbt_id_compute_rays_gather with one rank: the shard instance's count flushes go through
+    the peer-totals path (atomics into the gather buffer) and finalize to the whole ID."""
+    import torch
+    cfg = CONFIGS["A"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, 20.0, 7, seed=31)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 24, 17)
+    full = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
+    g = nbt.Gather(ctx, 16, 1, 0)
+    for _ in range(2):                                   # the buffer is cleared between calls
+        g.zero()
+        g.compute_rays(m, cfg.poi, P, cam, cfg.range_)
+        ctx.sync()
+        t = g.totals(7).clone()
+        assert np.array_equal(t.cpu().numpy()[:, :4], full.counts.astype(np.int64))
+        fin = nbt.id_finalize(ctx, m, cfg.poi, P, cam, cfg.range_, t)
+        assert np.array_equal(fin.gain, full.gain)
+    with pytest.raises(nbt.NbtError):                    # 20 x 40 B do not fit 16 x 64 B
+        g.compute_rays(m, cfg.poi, oracle.sample_perspectives(cfg.poi, 20.0, 30, seed=1), cam, cfg.range_)
+    g.close()
+
+
 def test_ray_split_prob_map_and_misuse(nbt, ctx):
     """8-bit store: the summed T_G finalizes to the exact Eq. 2 gains; bad shard arguments and
     host totals are rejected."""

@@ -111,6 +111,19 @@ def main():
     dist.barrier()
     pw.close()
 
+    # the same ray split with the all-reduce fused into the walk: count flushes add straight
+    # into every rank's buffer through the peer mappings
+    pr = ndist.PeerGather(nbt, ctx, 16, rank, world, n_buffers=1)
+    for _ in range(2):
+        few2 = persp[:max(1, world - 1)].contiguous()
+        xyz_f, gain_f, counts_f = pr.ray_split(m, cfg.poi, few2, cam, cfg.range_)
+        ctx.sync()
+        k2 = few2.shape[0]
+        assert np.array_equal(gain_f.cpu().numpy(), np.asarray(full.gain)[:k2]), "fused ray split: g_P differ"
+        assert np.array_equal(counts_f.cpu().numpy().astype(np.uint64), np.asarray(full.counts)[:k2].astype(np.uint64))
+    dist.barrier()
+    pr.close()
+
     # ray split (fewer perspectives than ranks): every rank walks its ray units of the same
     # perspectives, one all-reduce of the integer totals, the same cloud as the unsharded ID
     few = persp[:max(1, world - 1)].contiguous()
