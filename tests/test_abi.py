@@ -99,3 +99,15 @@ def test_camera_rejects_bad_args(lib):
         nbt.camera_from_fov(1.0, 1.0, 0, 4)
     with pytest.raises(nbt.NbtError):
         nbt.camera_from_grid_scaling(1.0, 1.0, 1.0, 0.01, 0.5)
+
+
+def test_header_constants_match_the_binding():
+    """Sizes the binding hard-codes equal the header's (#define / enum values)."""
+    src = open(os.path.join(ROOT, "include", "nbt.h")).read()
+    defs = dict(re.findall(r"#define\s+(NBT_[A-Z_]+)\s+(\d+)", src))
+    assert int(defs["NBT_ID_TOTALS"]) == nbt.ID_TOTALS
+    assert int(defs["NBT_PEER_HANDLE_BYTES"]) == nbt.PEER_HANDLE_BYTES
+    kernels = dict((k, int(v)) for k, v in re.findall(r"(NBT_KERNEL_[A-Z_]+)\s*=\s*(\d+)", src))
+    assert kernels["NBT_KERNEL_TRACE"] == nbt.KERNEL_TRACE
+    assert kernels["NBT_KERNEL_MAP_UPDATE"] == nbt.KERNEL_MAP_UPDATE
+    assert kernels["NBT_KERNEL_INTEGRATE"] == nbt.KERNEL_INTEGRATE
