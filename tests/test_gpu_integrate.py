@@ -3,6 +3,7 @@ depth frames: the voxel filter's centroids and counts, the float32 log-odds stor
 states and probability levels, and the emitted a2 deltas must all be bit-exact (every step
 is integer, or IEEE operations in the same order on both sides: readings Q33-Q37)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -278,7 +279,7 @@ def test_integrate_few_dense_cells(nbt, ctx):
         assert dt < 0.25, f"{dt:.3f} s for one frame"
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("NBT_FUZZ_SEEDS", "8"))))
 def test_integrate_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
     """Random non-cubic grids (voxel size, origin), sensors inside or outside, random point
     clouds (Gaussian blobs, uniform, on the Q12 lattice), random leaf / range / probabilities /

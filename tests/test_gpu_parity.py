@@ -897,7 +897,7 @@ def test_byte_store_config_b_subset(nbt, ctx, monkeypatch):
 
 # ---------------------------------------------------------------- randomized configurations
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("NBT_FUZZ_SEEDS", "12"))))
 def test_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
     """Random non-cubic maps (random voxel size and origin, random codes or SYN), random
     PoI and perspectives (some outside the grid), random lattice shape, corners, range,
