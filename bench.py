@@ -784,8 +784,10 @@ def main_ours(args, cfg):
                          "peak_basis": f"{sms} SMs x {INT_LANES_PER_SM_CLK} int32 lanes/clk x "
                                        f"{f_max / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)"},
             "kernel_share_of_step": shares,
-            "kernel_share_note": "from a separate fully profiled graph run after the timed region (each profiled kernel "
-                                 "adds two ~2 us event nodes); the timed graphs record only k_id_trace",
+            "kernel_share_note": ("eager launches, every kernel family bracketed by CUDA events inside the timed region"
+                                  if args.no_graph else
+                                  "from a separate fully profiled graph run after the timed region (each profiled "
+                                  "kernel adds two ~2 us event nodes); the timed graphs record only k_id_trace"),
             "north_star": north,
             "config_d_strong": strong,
             "map_integration": integ,
