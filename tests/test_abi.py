@@ -111,3 +111,12 @@ def test_header_constants_match_the_binding():
     assert kernels["NBT_KERNEL_TRACE"] == nbt.KERNEL_TRACE
     assert kernels["NBT_KERNEL_MAP_UPDATE"] == nbt.KERNEL_MAP_UPDATE
     assert kernels["NBT_KERNEL_INTEGRATE"] == nbt.KERNEL_INTEGRATE
+
+
+def test_missing_library_fails_loudly():
+    """No CPU fallback: without libnbt.so the binding raises on first use."""
+    code = ("import paper_2503_22588_b200 as nbt\n"
+            "try:\n    nbt.lib()\nexcept ImportError as e:\n    print('raised', e)\n")
+    env = dict(os.environ, NBT_LIB=os.path.join(ROOT, "no_such_libnbt.so"))
+    r = subprocess.run(["python", "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "raised" in r.stdout, r.stdout + r.stderr
