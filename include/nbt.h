@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define NBT_ABI_VERSION 1
+#define NBT_ABI_VERSION 2
 
 typedef enum {
     NBT_OK = 0,
@@ -78,6 +78,29 @@ nbt_status nbt_ctx_sync(nbt_ctx ctx);
 void       nbt_ctx_destroy(nbt_ctx ctx);
 /* Number of kernels libnbt has launched on this ctx since creation. */
 uint64_t   nbt_ctx_launch_count(nbt_ctx ctx);
+
+/* Tuning options of a ctx.  None of them changes any result: every setting gives the
+ * same clouds, maps and IDW values bit for bit (the parity tests run the alternatives);
+ * they select between measured implementations (knob table).  libnbt
+ * reads no environment variable.  NBT_ERR_INVALID_ARG for an unknown option or a value
+ * outside its range; get returns the current value. */
+enum {
+    NBT_OPT_TRACE_REFILL_MIN = 1,   /* idle lanes before a trace warp pops prepared rays: 1..32, default 6 */
+    NBT_OPT_TRACE_CHUNK_MIN = 2,    /* smallest ray-slot chunk per work grab: 32..1024 (rounded up to 32), default 64 */
+    NBT_OPT_TRACE_CARVEOUT = 3,     /* shared-memory carveout (%) of the trace kernel: -1 (driver) .. 100, default 25 */
+    NBT_OPT_DELTA_SORT = 4,         /* 1: map deltas by a CUB radix sort instead of the winner array; default 0 */
+    NBT_OPT_FILTER_SORT = 5,        /* 1: the integration's voxel filter by sorting instead of hashing; default 0 */
+    NBT_OPT_H2D_MODE = 6,           /* 1: host inputs copied by the driver (pageable) instead of the pinned stage; default 0 */
+    NBT_OPT_COPY_THREADS = 7,       /* 0: host staging copies on the caller's thread; 1: chunked over the library's
+                                       copy workers (4) while the DMA of landed chunks runs; default 1 on hosts with
+                                       >= 8 hardware threads, else 0 */
+    NBT_OPT_WALK_WIDTH = 8,         /* decision-term width of nbt_debug_trace: 0 = automatic (int32 unless a
+                                       segment has |E_a - O_a| >= 2^30 - 1 Q16 units), 32 or 64 = forced (tests of
+                                       the int32 bound; forcing 32 on a longer segment gives NBT_ERR_INVALID_ARG) */
+    NBT_OPT_VERBOSE = 9             /* 1: print the trace kernel's occupancy to stderr once; default 0 */
+};
+nbt_status nbt_ctx_set_option(nbt_ctx ctx, int32_t option, int64_t value);
+nbt_status nbt_ctx_get_option(nbt_ctx ctx, int32_t option, int64_t *value);
 
 /* Optional per-kernel device timing with CUDA events recorded on the ctx stream around
  * each launch of the named kernel family (used by bench.py for the roofline). */
@@ -120,6 +143,9 @@ void       nbt_graph_destroy(nbt_graph graph);
 
 enum { NBT_UNKNOWN = 0, NBT_FREE = 1, NBT_OCCUPIED = 2 };      /* three states (Eq. 2) */
 enum { NBT_OUTSIDE_UNKNOWN = 0, NBT_OUTSIDE_CLIP = 1 };        /* Q14 */
+/* Store layouts: linear x-fastest inside a sentinel shell (default), or a
+ * Morton cube (bit-interleaved coordinates; a 128-B line is an 8x8x8 block). */
+enum { NBT_LAYOUT_LINEAR = 0, NBT_LAYOUT_MORTON = 1 };
 
 typedef struct nbt_map_s *nbt_map;
 
@@ -130,6 +156,10 @@ typedef struct {
     double  gain[3];          /* g[U], g[F], g[O] of Eq. 2 as per-state constants (Q15);
                                  default {1.0, 0.12, 0.03}; each finite, >= 0 */
     int32_t outside_policy;   /* NBT_OUTSIDE_UNKNOWN (default) or NBT_OUTSIDE_CLIP */
+    int32_t layout;           /* NBT_LAYOUT_LINEAR (default) or NBT_LAYOUT_MORTON (the Morton cube must
+                                 fit 1024^3 voxels and 8x the linear store, else NBT_ERR_INVALID_ARG) */
+    int32_t state_bits;       /* bits per voxel of nbt_map_create: 2 (default: 16 voxels per 32-bit
+                                 word) or 8 (one byte per voxel); nbt_map_create_prob always uses 8 */
 } nbt_map_desc;
 
 /* Fill *desc with the defaults above for an nx*ny*nz grid of voxel_size at origin 0. */
@@ -208,7 +238,7 @@ nbt_status nbt_occ_download(nbt_occ occ, float *logodds_out, size_t n);
  * visits it (Q35); L := clamp(L + delta) in float (Q36).  map (NULL allowed; same nx,
  * ny, nz) receives the new state -- L >= logit(t_occ) Occupied, <= logit(t_free) Free,
  * else Unknown -- and level round(63 P) (Q37) of every voxel whose (state, level)
- * changed.  A non-finite point, a leaf cell index |c| >= 2^15 - 1 or a Q12 overflow makes the
+ * changed.  A non-finite point, a leaf cell index |c| >= 2^15 - 1 or a Q16 overflow makes the
  * whole call a no-op, reported as NBT_ERR_INVALID_ARG by the next nbt_ctx_sync or
  * nbt_occ_stats (points are validated on the device).  n < 2^31.  Stream-ordered; host
  * points are staged through pinned memory, no sync. */
@@ -397,15 +427,22 @@ nbt_status nbt_info_cost(nbt_idbuf buf, const double *pose_xyz, const double *po
 
 /* ----------------------------------------------------------- test hooks */
 
-/* Per-ray walk of explicit segments in Q12 voxel coordinates (4096 units per voxel,
+/* Per-ray walk of explicit segments in Q16 voxel coordinates (65536 units per voxel,
  * reading Q19; host arrays, n_rays x 3 int32 each, inside (-2^30, 2^30)): the first
  * max_visits visited voxels of ray r go to ijk_out[r*max_visits*3 ...], their codes
  * (0/1/2; 255 = outside the grid) to code_out[r*max_visits ...]; len_out[r] = number of
  * visited voxels (may exceed max_visits); counts_out[r*4 ...] = n_U, n_F, n_O, lookups.
  * Uses the same device traversal as nbt_id_compute.  Synchronizes. */
-nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map map, const int32_t *o_q12, const int32_t *e_q12,
+nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map map, const int32_t *o_q16, const int32_t *e_q16,
                            int32_t n_rays, int32_t max_visits, int32_t *ijk_out, uint8_t *code_out,
                            int32_t *len_out, uint32_t *counts_out);
+/* Per-ray counts of the PRODUCTION trace (the k_id_trace code nbt_id_compute runs, in an
+ * instance that also records every closed ray): n host perspectives, the same arguments as
+ * nbt_id_compute; ray_counts_out (host, n x N_E x 5 uint32) receives for ray k of perspective
+ * j (Q27 order: row-major lattice rows, then the 4 corner rays) its n_U, n_F, n_O, in-grid
+ * lookups and stop flag (1 = stopped on an Occupied voxel).  Synchronizes. */
+nbt_status nbt_debug_id_rays(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz, int32_t n,
+                             const nbt_camera *cam, double range, uint32_t *ray_counts_out);
 /* The device frames of n perspectives (host in/out): 18 int32 per perspective
  * (O, A, Rh, Uh, Rc, Uc, each xyz) and a status per perspective (0 ok). Synchronizes. */
 nbt_status nbt_debug_frames(nbt_ctx ctx, nbt_map map, const double poi[3], const double *persp_xyz,

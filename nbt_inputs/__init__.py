@@ -102,23 +102,23 @@ def rand_map(n, p_u=0.3, p_f=0.65, p_o=0.05, seed=0, shape=None) -> np.ndarray:
     return out
 
 
-Q12 = 4096   # ray-walk fixed point: 4096 units per voxel (reading Q19)
+Q16 = 65536   # ray-walk fixed point: 65536 units per voxel (reading Q19)
 
 
-def random_segments_q12(count: int, lo: float, hi: float, seed: int) -> tuple[np.ndarray, np.ndarray]:
-    """Random ray segments in Q12 voxel coordinates (int32), for DDA fuzzing."""
+def random_segments_q16(count: int, lo: float, hi: float, seed: int) -> tuple[np.ndarray, np.ndarray]:
+    """Random ray segments in Q16 voxel coordinates (int32), for DDA fuzzing."""
     rng = np.random.Generator(np.random.PCG64(seed))
-    o = np.round(rng.uniform(lo, hi, (count, 3)) * Q12).astype(np.int32)
-    e = np.round(rng.uniform(lo, hi, (count, 3)) * Q12).astype(np.int32)
+    o = np.round(rng.uniform(lo, hi, (count, 3)) * Q16).astype(np.int32)
+    e = np.round(rng.uniform(lo, hi, (count, 3)) * Q16).astype(np.int32)
     return o, e
 
 
-def tie_segments_q12(count: int, n: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
-    """Segments (Q12) whose endpoints sit on voxel faces / edges / corners (exact ties)."""
+def tie_segments_q16(count: int, n: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
+    """Segments (Q16) whose endpoints sit on voxel faces / edges / corners (exact ties)."""
     rng = np.random.Generator(np.random.PCG64(seed))
-    o = rng.integers(0, n, (count, 3)) * Q12
-    e = rng.integers(0, n, (count, 3)) * Q12
-    half = rng.integers(0, 2, (count, 3)) * (Q12 // 2)
+    o = rng.integers(0, n, (count, 3)) * Q16
+    e = rng.integers(0, n, (count, 3)) * Q16
+    half = rng.integers(0, 2, (count, 3)) * (Q16 // 2)
     o = o + half * rng.integers(0, 2, (count, 3))
     e = e + half * rng.integers(0, 2, (count, 3))
     return o.astype(np.int32), e.astype(np.int32)

@@ -14,7 +14,7 @@ from __future__ import annotations
 from fractions import Fraction as Fr
 from math import floor
 
-Q = 4096   # the walk's fixed point: Q12 (reading Q19)
+Q = 65536   # the walk's fixed point: Q16 (reading Q19)
 
 
 def _axis_interval(o, d, lo, hi, closed_cube):

@@ -50,8 +50,7 @@
 #define ORC_ERR_EMPTY 3
 #define ORC_ERR_SELFCHECK 9
 
-#define QF 65536           /* frames and lattice: Q16, one voxel = 65536 units (Q19) */
-#define QD 4096            /* ray endpoints for the walk: Q12, one voxel = 4096 units (Q19) */
+#define QF 65536           /* frames, lattice and the walk: Q16, one voxel = 65536 units (Q19, SURVEY O-3/O-5) */
 #define QLIM 1073741824LL  /* |coordinate| must stay below 2^30 in its unit (Q19) */
 
 /* ------------------------------------------------------------------ map (O-1) */
@@ -248,11 +247,9 @@ typedef struct {
 
 static int64_t floor_div(int64_t a, int64_t b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
 
-/* Q16 -> Q12: round to the nearest 1/4096 voxel, halves upward (Q19). */
-static int32_t q16_to_q12(int32_t v) { return (int32_t)floor_div((int64_t)v + 8, 16); }
-
 /*
- * Walk the voxels of the segment O -> E (Q12 voxel coordinates: 4096 units per voxel).
+ * Walk the voxels of the segment O -> E (Q16 voxel coordinates: 65536 units per voxel,
+ * SURVEY 8(c) O-5 with S = 65536).
  *
  * Definition followed: the point P(t) = O + t (E - O), t in [0,1], lies in voxel
  * floor(P(t)) (half-open voxels, O-1).  Moving in +a the index changes AT the
@@ -265,7 +262,7 @@ static int32_t q16_to_q12(int32_t v) { return (int32_t)floor_div((int64_t)v + 8,
  * Each visited voxel is scored by its state (Eq. 2): outside the
  * grid is Unknown (Q14) unless the clip policy is set; the walk stops
  * after the first Occupied voxel, which is counted (Q11); the origin
- * voxel is counted (Q12).  If ijk_out != NULL the visited voxels (up to
+ * voxel is counted (reading Q12).  If ijk_out != NULL the visited voxels (up to
  * max_visits) are written there and their codes (0/1/2, 255 = outside) to
  * code_out.
  */
@@ -277,12 +274,12 @@ int orc_trace_ray(const orc_map *m, const int32_t o[3], const int32_t e[3], int3
     int64_t nsteps = 0;
     for (int a = 0; a < 3; ++a) {
         if (o[a] <= -QLIM || o[a] >= QLIM || e[a] <= -QLIM || e[a] >= QLIM) return ORC_ERR_INVALID_ARG;
-        v[a] = floor_div(o[a], QD);
-        ve[a] = floor_div(e[a], QD);
+        v[a] = floor_div(o[a], QF);
+        ve[a] = floor_div(e[a], QF);
         D[a] = (int64_t)e[a] - o[a];
         neg[a] = D[a] < 0;
         /* distance (in Q16 units) from O to the next boundary crossed along a */
-        N[a] = neg[a] ? (int64_t)o[a] - v[a] * QD : (v[a] + 1) * QD - o[a];
+        N[a] = neg[a] ? (int64_t)o[a] - v[a] * QF : (v[a] + 1) * QF - o[a];
         nsteps += llabs(ve[a] - v[a]);
     }
     memset(r, 0, sizeof *r);
@@ -326,23 +323,19 @@ int orc_trace_ray(const orc_map *m, const int32_t o[3], const int32_t e[3], int3
             if (lhs < rhs || (lhs == rhs && neg[a] < neg[best])) best = a;
         }
         v[best] += neg[best] ? -1 : 1;
-        N[best] += QD;
+        N[best] += QF;
     }
     if (len_out) *len_out = len;
     return ORC_OK;
 }
 
-/* The segment the walk follows for ray k: both ends rounded from the Q16 lattice to
- * Q12 (Q19). */
-static int ray_segment_q12(const orc_frame *f, const orc_camera *cam, int32_t k, int32_t o12[3], int32_t e12[3])
+/* The segment the walk follows for ray k: the perspective origin O and the ray's
+ * far-plane endpoint E, both on the Q16 lattice (O-3, O-4; Q19). */
+static int ray_segment_q16(const orc_frame *f, const orc_camera *cam, int32_t k, int32_t o16[3], int32_t e16[3])
 {
-    int32_t e16[3];
     int st = ray_endpoint(f, cam, k, e16);
     if (st) return st;
-    for (int c = 0; c < 3; ++c) {
-        o12[c] = q16_to_q12(f->o[c]);
-        e12[c] = q16_to_q12(e16[c]);
-    }
+    for (int c = 0; c < 3; ++c) o16[c] = f->o[c];
     return ORC_OK;
 }
 
@@ -371,7 +364,7 @@ static int one_perspective(const orc_map *m, const double poi[3], const double p
     double direct = 0.0;
     for (int32_t k = 0; k < ne; ++k) {
         int32_t o[3], e[3];
-        if ((st = ray_segment_q12(&f, cam, k, o, e))) return st;
+        if ((st = ray_segment_q16(&f, cam, k, o, e))) return st;
         orc_ray r;
         if ((st = orc_trace_ray(m, o, e, 0, NULL, NULL, NULL, &r))) return st;
         direct += r.g;
@@ -431,7 +424,7 @@ int orc_id_compute(const orc_map *m, const double poi[3], const double *persp, i
     return status;
 }
 
-/* Rays of one perspective, for per-ray parity: the Q12 segment ends (the origin is
+/* Rays of one perspective, for per-ray parity: the Q16 segment ends (the origin is
  * common to all rays) and per-ray counts. */
 int orc_perspective_rays(const orc_map *m, const double poi[3], const double p[3],
                          const orc_camera *cam, double range, int32_t *o_out, int32_t *e_out,
@@ -443,7 +436,7 @@ int orc_perspective_rays(const orc_map *m, const double poi[3], const double p[3
     int32_t ne = orc_camera_num_rays(cam);
     for (int32_t k = 0; k < ne; ++k) {
         int32_t o[3], e[3];
-        if ((st = ray_segment_q12(&f, cam, k, o, e))) return st;
+        if ((st = ray_segment_q16(&f, cam, k, o, e))) return st;
         if (o_out && k == 0) memcpy(o_out, o, sizeof o);
         if (e_out) memcpy(e_out + 3 * (int64_t)k, e, sizeof e);
         if (ray_counts_out) {
@@ -787,11 +780,11 @@ int orc_voxel_filter(const double *pts, int64_t n, double leaf, double *out_xyz,
     return ORC_OK;
 }
 
-/* World position -> Q12 walk coordinate (reading Q34): round-half-even of
- * ((x - origin) / s) * 4096. */
-static int world_to_q12(double x, double origin, double s, int32_t *out)
+/* World position -> Q16 walk coordinate (reading Q34): round-half-even of
+ * ((x - origin) / s) * 65536. */
+static int world_to_q16(double x, double origin, double s, int32_t *out)
 {
-    double q = ((x - origin) / s) * 4096.0;
+    double q = ((x - origin) / s) * 65536.0;
     if (!(fabs(q) < (double)QLIM)) return ORC_ERR_INVALID_ARG;
     *out = (int32_t)nearbyint(q);
     return ORC_OK;
@@ -808,8 +801,8 @@ static float logodds_f(double p) { return (float)log(p / (1.0 - p)); }
  *   pts, n                the cloud (world); filtered by orc_voxel_filter when leaf > 0
  *
  * Every (filtered) point p gives the segment origin -> p; if |p - origin| > max_range
- * (> 0) the segment is cut at max_range and carves only (no hit).  Both ends go to Q12
- * (world_to_q12) and the exact DDA of orc_trace_ray lists the voxels the segment
+ * (> 0) the segment is cut at max_range and carves only (no hit).  Both ends go to Q16
+ * (world_to_q16) and the exact DDA of orc_trace_ray lists the voxels the segment
  * visits.  Per cloud every in-grid voxel is updated at most once (Q35): by L_hit if some
  * segment ENDS in it with a hit, else by L_miss if some segment visits it (the end
  * voxel of a cut segment, and the sensor's own voxel, included).  The update is
@@ -845,8 +838,8 @@ int orc_integrate(float *L, int32_t nx, int32_t ny, int32_t nz, double voxel_siz
     orc_map walk = {nx, ny, nz, voxel_size, {map_origin[0], map_origin[1], map_origin[2]}, {1.0, 1.0, 1.0}, 0,
                     all_free, NULL};
     int status = ORC_OK;
-    int32_t o12[3];
-    for (int a = 0; a < 3; ++a) status |= world_to_q12(origin[a], map_origin[a], voxel_size, &o12[a]);
+    int32_t o16[3];
+    for (int a = 0; a < 3; ++a) status |= world_to_q16(origin[a], map_origin[a], voxel_size, &o16[a]);
     for (int64_t i = 0; i < m && status == ORC_OK; ++i) {
         const double *p = ray_end + 3 * i;
         double d[3] = {p[0] - origin[0], p[1] - origin[1], p[2] - origin[2]};
@@ -858,16 +851,16 @@ int orc_integrate(float *L, int32_t nx, int32_t ny, int32_t nz, double voxel_siz
             for (int a = 0; a < 3; ++a) q[a] = origin[a] + d[a] * f;
             hit = 0;
         }
-        int32_t e12[3];
-        for (int a = 0; a < 3; ++a) status |= world_to_q12(q[a], map_origin[a], voxel_size, &e12[a]);
+        int32_t e16[3];
+        for (int a = 0; a < 3; ++a) status |= world_to_q16(q[a], map_origin[a], voxel_size, &e16[a]);
         if (status) break;
         int64_t len = 1;
-        for (int a = 0; a < 3; ++a) len += llabs(floor_div(e12[a], QD) - floor_div(o12[a], QD));
+        for (int a = 0; a < 3; ++a) len += llabs(floor_div(e16[a], QF) - floor_div(o16[a], QF));
         int32_t *ijk = (int32_t *)malloc((size_t)len * 3 * sizeof(int32_t));
         uint8_t *code = (uint8_t *)malloc((size_t)len);
         int32_t got = 0;
         orc_ray r;
-        status = orc_trace_ray(&walk, o12, e12, (int32_t)len, ijk, code, &got, &r);
+        status = orc_trace_ray(&walk, o16, e16, (int32_t)len, ijk, code, &got, &r);
         if (!status && got != len) status = ORC_ERR_SELFCHECK;   /* all-Free map: no early stop */
         for (int64_t s = 0; s < got && !status; ++s) {
             if (code[s] == 255) continue;                           /* outside the grid */

@@ -25,6 +25,9 @@ LIB_PATH = os.environ.get("NBT_LIB") or os.path.join(_HERE, "libnbt.so")   # NBT
 OK, ERR_INVALID_ARG, ERR_DEGENERATE, ERR_EMPTY, ERR_OUT_OF_MEMORY, ERR_CUDA, ERR_NCCL, ERR_STATE = range(8)
 UNKNOWN, FREE, OCCUPIED = 0, 1, 2
 OUTSIDE_UNKNOWN, OUTSIDE_CLIP = 0, 1
+LAYOUT_LINEAR, LAYOUT_MORTON = 0, 1
+(OPT_TRACE_REFILL_MIN, OPT_TRACE_CHUNK_MIN, OPT_TRACE_CARVEOUT, OPT_DELTA_SORT, OPT_FILTER_SORT, OPT_H2D_MODE,
+ OPT_COPY_THREADS, OPT_WALK_WIDTH, OPT_VERBOSE) = range(1, 10)
 SAMPLE_BALL, SAMPLE_SURFACE = 0, 1
 (KERNEL_TRACE, KERNEL_FRAMES, KERNEL_FINALIZE, KERNEL_IDW, KERNEL_SAMPLE, KERNEL_MAP_UPDATE,
  KERNEL_INTEGRATE) = range(7)
@@ -33,6 +36,7 @@ SAMPLE_BALL, SAMPLE_SURFACE = 0, 1
 EXPORTS = [
     "nbt_abi_version", "nbt_status_string", "nbt_last_error_message",
     "nbt_ctx_create", "nbt_ctx_set_stream", "nbt_ctx_sync", "nbt_ctx_destroy", "nbt_ctx_launch_count",
+    "nbt_ctx_set_option", "nbt_ctx_get_option",
     "nbt_ctx_set_profiling", "nbt_ctx_set_profiling_mask", "nbt_ctx_profile_read",
     "nbt_ctx_capture_begin", "nbt_ctx_capture_end", "nbt_graph_launch", "nbt_graph_profile_read", "nbt_graph_destroy",
     "nbt_map_desc_default", "nbt_map_create", "nbt_map_create_prob", "nbt_map_upload", "nbt_map_upload_prob",
@@ -46,7 +50,7 @@ EXPORTS = [
     "nbt_info_cost",
     "nbt_integrate_params_default", "nbt_occ_create", "nbt_occ_upload", "nbt_occ_download", "nbt_occ_integrate",
     "nbt_occ_stats", "nbt_occ_deltas", "nbt_occ_destroy", "nbt_voxel_filter",
-    "nbt_debug_trace", "nbt_debug_frames",
+    "nbt_debug_trace", "nbt_debug_frames", "nbt_debug_id_rays",
 ]
 
 
@@ -58,7 +62,8 @@ class NbtError(RuntimeError):
 
 class MapDesc(C.Structure):
     _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("voxel_size", C.c_double),
-                ("origin", C.c_double * 3), ("gain", C.c_double * 3), ("outside_policy", C.c_int32)]
+                ("origin", C.c_double * 3), ("gain", C.c_double * 3), ("outside_policy", C.c_int32),
+                ("layout", C.c_int32), ("state_bits", C.c_int32)]
 
 
 class Camera(C.Structure):
@@ -102,6 +107,8 @@ def lib():
         "nbt_ctx_sync": ([vp], C.c_int),
         "nbt_ctx_destroy": ([vp], None),
         "nbt_ctx_launch_count": ([vp], u64),
+        "nbt_ctx_set_option": ([vp, i32, i64], C.c_int),
+        "nbt_ctx_get_option": ([vp, i32, C.POINTER(i64)], C.c_int),
         "nbt_ctx_set_profiling": ([vp, C.c_int], C.c_int),
         "nbt_ctx_set_profiling_mask": ([vp, C.c_uint32], C.c_int),
         "nbt_ctx_profile_read": ([vp, i32, C.POINTER(C.c_double), C.POINTER(u64), C.c_int], C.c_int),
@@ -161,6 +168,7 @@ def lib():
         "nbt_voxel_filter": ([vp, vp, i64, C.c_int, dbl, vp, vp, C.POINTER(i64)], C.c_int),
         "nbt_debug_trace": ([vp, vp, vp, vp, i32, i32, vp, vp, vp, vp], C.c_int),
         "nbt_debug_frames": ([vp, vp, vp, vp, i32, C.POINTER(Camera), dbl, vp, vp], C.c_int),
+        "nbt_debug_id_rays": ([vp, vp, vp, vp, i32, C.POINTER(Camera), dbl, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("NBT_LIB") and not hasattr(L, name):
@@ -243,6 +251,15 @@ class Ctx:
     def launches(self):
         return int(lib().nbt_ctx_launch_count(self.h))
 
+    def set_option(self, option, value):
+        """nbt_ctx_set_option: a tuning option (OPT_*); no option changes any result."""
+        check(lib().nbt_ctx_set_option(self.h, int(option), int(value)))
+
+    def get_option(self, option):
+        v = C.c_int64()
+        check(lib().nbt_ctx_get_option(self.h, int(option), C.byref(v)))
+        return int(v.value)
+
     def set_profiling_mask(self, kernels):
         """Record only these kernel families (iterable of KERNEL_* ids; empty = off)."""
         mask = 0
@@ -306,13 +323,20 @@ class Graph:
             pass
 
 
-def map_desc(nx, ny, nz, voxel_size, origin=(0.0, 0.0, 0.0), gain=None, outside_policy=OUTSIDE_UNKNOWN):
+def map_desc(nx, ny, nz, voxel_size, origin=(0.0, 0.0, 0.0), gain=None, outside_policy=OUTSIDE_UNKNOWN,
+             layout=LAYOUT_LINEAR, state_bits=2):
+    """nbt_map_desc: grid, voxel size, origin, Eq. 2 gains, outside policy, store layout
+    (LAYOUT_LINEAR / LAYOUT_MORTON, or "linear" / "morton") and bits per voxel (2 or 8)."""
     d = MapDesc()
     lib().nbt_map_desc_default(C.byref(d), int(nx), int(ny), int(nz), float(voxel_size))
     d.origin[:] = [float(v) for v in origin]
     if gain is not None:
         d.gain[:] = [float(v) for v in gain]
     d.outside_policy = int(outside_policy)
+    if isinstance(layout, str):
+        layout = {"linear": LAYOUT_LINEAR, "morton": LAYOUT_MORTON}[layout]
+    d.layout = int(layout)
+    d.state_bits = int(state_bits)
     return d
 
 
@@ -790,6 +814,16 @@ def debug_trace(ctx: Ctx, m: Map, o_q16, e_q16, max_visits=1024):
                                 C.c_void_p(ijk.ctypes.data), C.c_void_p(codes.ctypes.data),
                                 C.c_void_p(ln.ctypes.data), C.c_void_p(cnt.ctypes.data)))
     return ijk, codes, ln, cnt
+
+
+def debug_id_rays(ctx: Ctx, m: Map, poi, persp, cam: Camera, range_):
+    """Per-ray (n_U, n_F, n_O, lookups, stop) of the production trace kernel: [n, N_E, 5] uint32."""
+    pp, keep = _poi(poi)
+    P = np.ascontiguousarray(persp, dtype=np.float64).reshape(-1, 3)
+    out = np.zeros((P.shape[0], cam.num_rays, 5), np.uint32)
+    check(lib().nbt_debug_id_rays(ctx.h, m.h, pp, C.c_void_p(P.ctypes.data), P.shape[0], C.byref(cam),
+                                  float(range_), C.c_void_p(out.ctypes.data)))
+    return out
 
 
 def debug_frames(ctx: Ctx, m: Map, poi, persp, cam: Camera, range_):

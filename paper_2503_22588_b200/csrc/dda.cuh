@@ -8,7 +8,7 @@
 namespace nbt {
 namespace dda {
 
-constexpr int kQShift = 12;      // walk coordinates: Q12
+constexpr int kQShift = 16;      // walk coordinates: Q16, the frames' lattice
 
 struct MapView {
     const uint32_t *__restrict__ words;
@@ -34,11 +34,11 @@ __device__ __forceinline__ uint32_t code_of(uint32_t word, uint32_t idx)
     return __funnelshift_r(word, 0u, idx << 1) & 3u;   // shift amount taken mod 32
 }
 
-// Per-ray walk state.  T = int (rays <= 720 voxels per axis) or long long.
+// Per-ray walk state.  T = int (rays < 2^14 voxels per axis, k_id.cu header) or long long.
 template <typename T>
 struct Walk {
     T qxy, qxz, qyz;           // sign decides the next axis (see header)
-    T ax, ay, az;              // |D_a| in Q12 units
+    T ax, ay, az;              // |D_a| in Q16 units
     T nax;                     // -|D_x| (hot path)
     uint32_t idx;              // padded linear index of the current voxel (in-grid walk)
     int dX, dY, ndZ;           // linear: idx increments of a step along x, y and (negated) z
@@ -68,7 +68,7 @@ __device__ __forceinline__ void walk_setup(Walk<T> &w, const int o[3], const int
         int ve = e[a] >> kQShift;
         n += (ve > v[a]) ? ve - v[a] : v[a] - ve;
         N[a] = neg[a] ? (long long)o[a] - ((long long)v[a] << kQShift)
-                      : (((long long)v[a] + 1) << kQShift) - o[a];          // in [0, 4096]
+                      : (((long long)v[a] + 1) << kQShift) - o[a];          // in [0, 65536]
     }
     // tie favours the lower axis unless it moves negatively and the other positively
     long long fxy = N[0] * ad[1] - N[1] * ad[0] - ((neg[0] && !neg[1]) ? 0 : 1);

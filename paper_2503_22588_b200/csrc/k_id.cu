@@ -6,7 +6,7 @@
 //                   time; when it finishes, the warp hands it the next ray of the
 //                   current chunk (a run of one perspective's rays in 8x4 pixel tiles).
 //                   The lane builds its endpoint on the far plane in registers
-//                   (Q27), rounds both ends to Q12, and walks the exact
+//                   (Q27) on the frame's Q16 lattice, and walks the exact
 //                   integer 3D-DDA (Q13) through the 2-bit map in batches of K = 16
 //                   voxels: the DDA does not depend on the map, so a batch computes
 //                   K voxel indices, issues K independent loads, packs the
@@ -24,17 +24,22 @@
 //                   (the all-gather fused into the finalize, nbt_id_compute_gather)
 //
 // Exact decision with 32-bit arithmetic.  With D = E - O and
-// N_a the distance from O to the next boundary along a (Q12 units, S = 4096), the next
+// N_a the distance from O to the next boundary along a (Q16 units, S = 65536), the next
 // boundary crossed is the axis minimising N_a/|D_a|, ties broken by (positive direction
 // first, then x<y<z).  The pairwise terms e_ab = N_a|D_b| - N_b|D_a|, minus a 0/1 tie
 // bias, decide "a before b" by their sign.  Every later change of e_ab is a multiple
 // of S (a step along a adds S|D_b|), so with e_ab - bias = S q_ab + r (0 <= r < S) the
 // sign of q_ab equals the sign of e_ab - bias and q_ab changes by |D_b| (or -|D_a|).
-// q_ab is computed once per ray in 64-bit and then kept in int32, which is exact for
-// rays up to 720 voxels per axis; longer rays use the same code with 64-bit q (the
-// host picks the variant from the camera geometry).
+// q_ab is computed once per ray in 64-bit and then kept in int32.  Bound (tight): N_a is
+// in [0, S], so q_ab starts in [-|D_a| - 1, |D_b|]; an a-step (taken only while q_ab < 0)
+// adds |D_b|, a b-step (only while q_ab >= 0) subtracts |D_a|, a c-step leaves it, so
+// q_ab -- and every intermediate value, speculative steps past the ray end included --
+// stays in [-|D_a| - 1, |D_b|].  int32 is therefore exact while max |D| < 2^30 - 1, i.e.
+// for rays shorter than 16383 voxels per axis; the host picks the 64-bit instance of the
+// same code above kInt32MaxVoxels (tests/test_gpu_parity.py::test_int32_bound_*).
 #include <stdio.h>
-#include <stdlib.h>
+
+#include <type_traits>
 
 #include "nbt_internal.cuh"
 #include "dda.cuh"
@@ -63,7 +68,7 @@ constexpr int kWarpsPerBlock = NBT_WARPS_PER_BLOCK;
 #endif
 constexpr int kBatchK = NBT_BATCH_K;
 constexpr bool kPipe = NBT_PIPE;
-constexpr int kInt32MaxVoxels = 700;   // |D_a| bound (voxels) for the int32 decision terms
+constexpr int kInt32MaxVoxels = 16000;   // |D_a| bound (voxels) for the int32 decision terms (< 16383)
 #ifndef NBT_TILE_W
 #define NBT_TILE_W 8
 #endif
@@ -412,6 +417,13 @@ __device__ __forceinline__ const PeerTotals *peer_totals_of(const TraceArgs &A)
 {
     return reinterpret_cast<const PeerTotals *>(A.work_counter + kPeerTotalsOffset);
 }
+// REC instance (nbt_debug_id_rays): the per-ray record array lives in the same buffer.
+constexpr int kRecordOffset = 64;       // ints (after the peer totals)
+static_assert(kPeerTotalsOffset * 4 + sizeof(PeerTotals) <= kRecordOffset * 4, "record after the peer totals");
+__device__ __forceinline__ uint32_t *record_of(const TraceArgs &A)
+{
+    return *reinterpret_cast<uint32_t *const *>(A.work_counter + kRecordOffset);
+}
 
 // Map slot -> lattice offsets (mi, mk) = (2i-(W-1), 2kk-(H-1)) or a corner ray.
 __device__ __forceinline__ bool slot_ray(const TraceArgs &T, int slot, int &mi, int &mk, int &corner)
@@ -437,8 +449,26 @@ __device__ __forceinline__ bool slot_ray(const TraceArgs &T, int slot, int &mi, 
     return true;
 }
 
-// Walk segment of a ray: both ends from the Q16 lattice (modular arithmetic: the true
-// values lie inside (-2^30, 2^30), checked per perspective), rounded to Q12 (Q19).
+// Ray index k (Q27 order: row-major lattice, then the corner rays) of a (non-shard) slot.
+__device__ __forceinline__ int ray_index_of_slot(const TraceArgs &T, int slot)
+{
+    int mi = 0, mk = 0, corner = -1;
+    slot_ray(T, slot, mi, mk, corner);
+    if (corner >= 0) return T.W * T.H + corner;
+    return ((mk + T.H - 1) >> 1) * T.W + ((mi + T.W - 1) >> 1);
+}
+
+// REC: ray k of perspective j closed with these counts (n_U, n_F, n_O, lookups, stop).
+__device__ __forceinline__ void record_ray(const TraceArgs &T, int j, int slot, uint32_t u, uint32_t f, uint32_t o,
+                                           uint32_t l)
+{
+    const int ne = T.W * T.H + (T.add_corners ? 4 : 0);
+    uint32_t *r = record_of(T) + 5 * ((size_t)j * ne + ray_index_of_slot(T, slot));
+    r[0] = u; r[1] = f; r[2] = o; r[3] = l; r[4] = o;    // n_O in {0, 1} is the stop flag
+}
+
+// Walk segment of a ray: both ends on the Q16 lattice (modular arithmetic: the true
+// values lie inside (-2^30, 2^30), checked per perspective; Q19).
 __device__ __forceinline__ void ray_segment(const int f[18], int mi, int mk, int corner, int o[3], int e[3])
 {
 #pragma unroll
@@ -451,8 +481,8 @@ __device__ __forceinline__ void ray_segment(const int f[18], int mi, int mk, int
             uint32_t rc = (uint32_t)f[12 + k], uc = (uint32_t)f[15 + k];
             v = (uint32_t)f[k] + (uint32_t)f[3 + k] + ((corner & 1) ? rc : 0u - rc) + ((corner & 2) ? uc : 0u - uc);
         }
-        o[k] = (f[k] + 8) >> 4;          // round half up to Q12 (arithmetic shift = floor)
-        e[k] = ((int)v + 8) >> 4;
+        o[k] = f[k];
+        e[k] = (int)v;
     }
 }
 
@@ -533,7 +563,21 @@ __device__ __forceinline__ void flush_counts_warp_peer(const PeerTotals *pt, int
 // Prepare the ray in `slot` of perspective j (frame, segment, DDA set-up, grid
 // entry).  Returns false if the slot is a tile hole or the ray ends without entering
 // the grid (its Unknown visits are then added to the totals directly).
-template <typename T, int L>
+// Unknown visits of a ray that never enters the grid, in a ray shard: into every rank's totals
+// for the fused ray split (like the walked rays' flushes), else into the call's totals.  Rare,
+// so kept out of line (the shard kernel's register budget).
+__device__ __noinline__ void add_unknown_shard(const TraceArgs &A, int j, uint32_t pre)
+{
+    const PeerTotals *pt = peer_totals_of(A);
+    const int nd = pt->n > 0 ? pt->n : 1;
+    for (int d = 0; d < nd; ++d) {
+        unsigned long long *t = (pt->n > 0 ? pt->t[d] : A.totals) + kTotals * (size_t)j;
+        atomicAdd(t, (unsigned long long)pre);
+        atomicAdd(t + 4, 63ull * pre);
+    }
+}
+
+template <typename T, int L, bool SHARD, bool REC = false>
 __device__ __forceinline__ bool prep_ray(const TraceArgs &A, int j, int slot, Walk<T> &w)
 {
     int mi = 0, mk = 0, corner = -1;
@@ -547,9 +591,14 @@ __device__ __forceinline__ bool prep_ray(const TraceArgs &A, int j, int slot, Wa
     walk_setup(w, o, e);
     if (walk_enter<T, L, false>(w, A.m, nullptr, nullptr, 0)) {
         if (A.m.policy == NBT_OUTSIDE_UNKNOWN) {
-            atomicAdd(A.totals + kTotals * (size_t)j, (unsigned long long)w.pre);
-            atomicAdd(A.totals + kTotals * (size_t)j + 4, 63ull * w.pre);
+            if (SHARD) {
+                add_unknown_shard(A, j, w.pre);
+            } else {
+                atomicAdd(A.totals + kTotals * (size_t)j, (unsigned long long)w.pre);
+                atomicAdd(A.totals + kTotals * (size_t)j + 4, 63ull * w.pre);
+            }
         }
+        if (REC) record_ray(A, j, slot, A.m.policy == NBT_OUTSIDE_UNKNOWN ? w.pre : 0u, 0u, 0u, 0u);
         return false;
     }
     return true;
@@ -568,9 +617,14 @@ struct WalkQueue {
     uint32_t pre[32];
     int j[32];
 };
+// REC instance: the queue also carries each prepared ray's slot.
+template <typename T>
+struct WalkQueueRec : WalkQueue<T> {
+    int slot[32];
+};
 
-template <typename T, int L>
-__device__ __forceinline__ void queue_put(WalkQueue<T> &Q, int i, const Walk<T> &w, int j)
+template <typename T, int L, typename Queue>
+__device__ __forceinline__ void queue_put(Queue &Q, int i, const Walk<T> &w, int j)
 {
     Q.q[0][i] = w.qxy; Q.q[1][i] = w.qxz; Q.q[2][i] = w.qyz;
     Q.a[0][i] = w.ax; Q.a[1][i] = w.ay; Q.a[2][i] = w.az;
@@ -584,8 +638,8 @@ __device__ __forceinline__ void queue_put(WalkQueue<T> &Q, int i, const Walk<T> 
     Q.n[i] = w.n; Q.s0[i] = w.s0; Q.pre[i] = w.pre; Q.j[i] = j;
 }
 
-template <typename T, int L>
-__device__ __forceinline__ int queue_get(const WalkQueue<T> &Q, int i, Walk<T> &w)
+template <typename T, int L, typename Queue>
+__device__ __forceinline__ int queue_get(const Queue &Q, int i, Walk<T> &w)
 {
     w.qxy = Q.q[0][i]; w.qxz = Q.q[1][i]; w.qyz = Q.q[2][i];
     w.ax = Q.a[0][i]; w.ay = Q.a[1][i]; w.az = Q.a[2][i];
@@ -616,13 +670,19 @@ constexpr int trace_min_blocks()
                                     : (sizeof(T) == 8 ? 16 : (VB == kStoreProb ? 24 : 32)) / kWarpsPerBlock;
 }
 
-template <typename T, int L, int VB, int K, bool PIPE, bool SHARD>
+// REC = per-ray record instance (nbt_debug_id_rays): the same code, which also writes every
+// closed ray's counts to the record array; a separate instance, so the production kernel's
+// code is unchanged.
+template <typename T, int L, int VB, int K, bool PIPE, bool SHARD, bool REC = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()) k_id_trace(TraceArgs A)
 {
     constexpr bool CYCLE = PIPE && VB != kStoreProb;     // in-place pipeline (batch_cycle)
     static_assert((CYCLE ? 2 * K : K) <= kBorder, "look-ahead must stay inside the sentinel shell");
-    __shared__ WalkQueue<T> queues[kWarpsPerBlock];
-    WalkQueue<T> &Q = queues[threadIdx.x >> 5];
+    static_assert(!(REC && (SHARD || CYCLE)), "the record instance is the whole-ID, unpipelined walk");
+    using Queue = std::conditional_t<REC, WalkQueueRec<T>, WalkQueue<T>>;
+    __shared__ Queue queues[kWarpsPerBlock];
+    Queue &Q = queues[threadIdx.x >> 5];
+    int my_slot = 0;                         // REC: slot of this lane's ray
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lanes_below = (1u << lane) - 1u;
@@ -665,10 +725,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     }
                 }
                 Walk<T> t;
-                const bool ok = lane < valid && prep_ray<T, L>(A, q_j, slot0 + lane, t);
+                const bool ok = lane < valid && prep_ray<T, L, SHARD, REC>(A, q_j, slot0 + lane, t);
                 q_next += avail;
                 const unsigned vm = __ballot_sync(full, ok);
                 if (ok) queue_put<T, L>(Q, __popc(vm & lanes_below), t, q_j);
+                if constexpr (REC) {
+                    if (ok) Q.slot[__popc(vm & lanes_below)] = slot0 + lane;
+                }
                 __syncwarp();
                 qhead = 0;
                 qcount = __popc(vm);
@@ -677,7 +740,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                 const int rank = __popc(need & lanes_below);
                 const int take = min(__popc(need), qcount);
                 int j = -1;
-                if (!have && rank < take) j = queue_get<T, L>(Q, qhead + rank, w);
+                if (!have && rank < take) {
+                    j = queue_get<T, L>(Q, qhead + rank, w);
+                    if constexpr (REC) my_slot = Q.slot[qhead + rank];
+                }
                 // lanes moving to another perspective flush their counts, one atomic per
                 // counter per (warp, perspective): many lanes of a warp hold the same one
                 const bool fl = j >= 0 && j != jl;
@@ -710,7 +776,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
             if (batch_finish<T, VB, K>(w, bits, 0u, b0, A.m.policy, c)) have = false;
         } else {
             batch_issue<T, L, VB, K>(w, A.m, b0);
-            if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) have = false;
+            const Counts before = c;
+            if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) {
+                have = false;
+                if (REC) record_ray(A, jl, my_slot, c.u - before.u, c.f - before.f, c.o - before.o, c.l - before.l);
+            }
         }
     }
     // residual counts, once per lane (the warp-combined form measured ~2% slower here)
@@ -797,7 +867,7 @@ __global__ void k_id_finalize_gather(FrameArgs A, const int32_t *__restrict__ fr
 
 // ------------------------------------------------------------ debug hooks
 
-// Per-ray walk of an explicit Q12 segment, recording every visited voxel; the same
+// Per-ray walk of an explicit Q16 segment, recording every visited voxel; the same
 // Walk / walk_step / walk_enter code as k_id_trace, one voxel at a time.
 template <typename T, int L, int VB>
 __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const int32_t *__restrict__ e, int n_rays,
@@ -893,41 +963,6 @@ FrameArgs frame_args(nbt_map m, const double *d_persp, int32_t first, int32_t st
     return A;
 }
 
-// Preferred shared-memory carveout (percent of the unified L1/shared capacity) for the
-// trace kernel: NBT_TRACE_CARVEOUT, default 25 (-1 leaves the driver's choice).
-int trace_carveout()
-{
-    static int v = [] {
-        const char *e = getenv("NBT_TRACE_CARVEOUT");
-        return e ? atoi(e) : 25;
-    }();
-    return v;
-}
-
-// Smallest chunk (ray slots a warp takes per grab of the global work counter):
-// NBT_CHUNK_MIN, default 64 (a multiple of 32; profiles/r01_chunk_flush.log).
-int chunk_min()
-{
-    static int v = [] {
-        const char *e = getenv("NBT_CHUNK_MIN");
-        int r = e ? atoi(e) : 64;
-        r = (r + 31) / 32 * 32;
-        return r < 32 ? 32 : (r > 1024 ? 1024 : r);
-    }();
-    return v;
-}
-
-// Idle lanes a warp waits for before refilling: NBT_REFILL_MIN, default 6 (profiles/r01_refill_sweep.log).
-int refill_threshold()
-{
-    static int v = [] {
-        const char *e = getenv("NBT_REFILL_MIN");
-        int r = e ? atoi(e) : 6;
-        return r < 1 ? 1 : (r > 32 ? 32 : r);
-    }();
-    return v;
-}
-
 // Conservative bound (voxels) on |D_a| of every ray of a camera: the longest ray of the
 // frustum (its far-plane corner) plus rounding.
 double max_ray_voxels(const nbt_camera &cam, double range, double voxel_size)
@@ -952,6 +987,14 @@ using TraceFn = void (*)(TraceArgs);
 const TraceFn kTraceFns[2][2][2][3] = {NBT_TRACE_SET(false), NBT_TRACE_SET(true)};
 #undef NBT_TRACE_SET
 #undef NBT_TRACE_ROW
+// The per-ray record instances (nbt_debug_id_rays): [wide][layout][store], unpipelined.
+#define NBT_TRACE_REC_ROW(T, L)                                                                            \
+    {k_id_trace<T, L, kStore2, kBatchK, false, false, true>, k_id_trace<T, L, kStoreByte, kBatchK, false, false, true>, \
+     k_id_trace<T, L, kStoreProb, kBatchK, false, false, true>}
+const TraceFn kTraceRecFns[2][2][3] = {{NBT_TRACE_REC_ROW(int, kLayoutLinear), NBT_TRACE_REC_ROW(int, kLayoutMorton)},
+                                       {NBT_TRACE_REC_ROW(long long, kLayoutLinear),
+                                        NBT_TRACE_REC_ROW(long long, kLayoutMorton)}};
+#undef NBT_TRACE_REC_ROW
 
 using DebugFn = void (*)(MapView, const int32_t *, const int32_t *, int, int, int32_t *, uint8_t *, int32_t *,
                          uint32_t *);
@@ -976,7 +1019,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     // ray shard, else scratch; the finalize reads the caller's summed totals when given
     unsigned long long *tot = L.d_totals_trace ? reinterpret_cast<unsigned long long *>(L.d_totals_trace)
                                                : ctx->totals.as<unsigned long long>();
-    if ((st = ctx->counter.ensure(kPeerTotalsOffset * 4 + sizeof(PeerTotals)))) return st;
+    if ((st = ctx->counter.ensure(kRecordOffset * 4 + sizeof(void *)))) return st;
     FrameArgs A = frame_args(m, L.d_persp, L.first, L.stride, L.n, L.poi, L.cam, L.range);
     int *counter = ctx->counter.as<int>();
     {
@@ -1008,22 +1051,35 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     const int sk = store_kind(m);
     const bool peer = L.peer_totals != nullptr && L.peer_totals->n > 0;
     if (L.ray_world > 1 || peer) {   // the SHARD instance reads its peer totals (n = 0: none)
-        PeerTotals none;
-        NBT_CUDA(cudaMemcpyAsync(counter + kPeerTotalsOffset, peer ? L.peer_totals : &none, sizeof(PeerTotals),
-                                 cudaMemcpyHostToDevice, ctx->stream));
+        // device-to-device copy / memset only: both are valid graph nodes (no host source)
+        if (peer)
+            NBT_CUDA(cudaMemcpyAsync(counter + kPeerTotalsOffset, L.d_peer_totals, sizeof(PeerTotals),
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+        else
+            NBT_CUDA(cudaMemsetAsync(counter + kPeerTotalsOffset, 0, sizeof(PeerTotals), ctx->stream));
     }
-    const TraceFn fn = kTraceFns[L.ray_world > 1 || peer][wide][m->layout == kLayoutMorton][sk];
+    if (L.d_record)   // REC instance: where it writes the per-ray counts (debug entry, never captured)
+        NBT_CUDA(cudaMemcpyAsync(counter + kRecordOffset, &L.d_record, sizeof(void *), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    const TraceFn fn = L.d_record ? kTraceRecFns[wide][m->layout == kLayoutMorton][sk]
+                                  : kTraceFns[L.ray_world > 1 || peer][wide][m->layout == kLayoutMorton][sk];
     const int fi = (wide ? 6 : 0) + (m->layout == kLayoutMorton ? 3 : 0) + sk;
     if (ctx->trace_blocks_per_sm == 0) {
         // smallest shared-memory carveout that holds the walk queues of the resident blocks,
         // so the rest of the SM's 256 KB stays L1 for the map lines
-        const int carve = trace_carveout();
-        if (carve >= 0)
+        // preferred shared-memory carveout (NBT_OPT_TRACE_CARVEOUT, default 25; -1 = driver)
+        const int carve = ctx->opt.carveout;
+        if (carve >= 0) {
             for (auto &sh : kTraceFns)
                 for (auto &a : sh)
                     for (auto &b : a)
                         for (TraceFn f : b)
                             NBT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            for (auto &a : kTraceRecFns)
+                for (auto &b : a)
+                    for (TraceFn f : b)
+                        NBT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+        }
         for (int k = 0; k < 12; ++k) {
             int b = 0;
             NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kTraceFns[0][k / 6][(k / 3) & 1][k % 3],
@@ -1031,7 +1087,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
             ctx->trace_bps[k] = b > 0 ? b : 1;
         }
         ctx->trace_blocks_per_sm = ctx->trace_bps[0];
-        if (getenv("NBT_VERBOSE")) {
+        if (ctx->opt.verbose) {
             fprintf(stderr, "libnbt: k_id_trace resident blocks/SM");
             for (int k = 0; k < 12; ++k) fprintf(stderr, " %d", ctx->trace_bps[k]);
             fprintf(stderr, " (carveout %d)\n", carve);
@@ -1042,14 +1098,16 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     long long total_slots = (long long)L.n * T.slots;
     long long per = total_slots / (4 * resident_warps);           // aim for >= 4 chunks per warp
     int chunk = (int)((per / 32) * 32);
-    const int cmin = chunk_min();
+    // smallest chunk per grab of the work counter (NBT_OPT_TRACE_CHUNK_MIN, default 64,
+    // profiles/r01_chunk_flush.log)
+    const int cmin = ctx->opt.chunk_min;
     chunk = chunk < cmin ? cmin : (chunk > 1024 ? 1024 : chunk);
     T.chunk = chunk;
     T.chunks_per_persp = (T.slots + chunk - 1) / chunk;
     long long tc = (long long)T.chunks_per_persp * L.n;
     if (tc >= (1ll << 31)) return fail(NBT_ERR_INVALID_ARG, "nbt_id_compute: too many rays in one call");
     T.total_chunks = (int)tc;
-    T.min_refill = refill_threshold();
+    T.min_refill = ctx->opt.refill_min;   // NBT_OPT_TRACE_REFILL_MIN (profiles/r01_refill_sweep.log)
     long long want_blocks = (tc + kWarpsPerBlock - 1) / kWarpsPerBlock;
     long long max_blocks = (long long)ctx->num_sms * bps;
     int blocks = (int)(want_blocks < max_blocks ? want_blocks : max_blocks);
@@ -1091,12 +1149,13 @@ nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const 
     return NBT_OK;
 }
 
-bool debug_needs_wide(const int32_t *o_q12, const int32_t *e_q12, int32_t n_rays)
+// The int32 decision terms are exact while every |E_a - O_a| < 2^30 - 1 (k_id.cu header).
+bool debug_needs_wide(const int32_t *o_q16, const int32_t *e_q16, int32_t n_rays)
 {
     for (int32_t i = 0; i < 3 * n_rays; ++i) {
-        long long d = (long long)e_q12[i] - o_q12[i];
+        long long d = (long long)e_q16[i] - o_q16[i];
         if (d < 0) d = -d;
-        if ((d >> kQShift) + 2 > kInt32MaxVoxels) return true;
+        if (d >= (1ll << 30) - 1) return true;
     }
     return false;
 }

@@ -12,7 +12,7 @@
 //   k_filter_centroid 8 lanes per cell: the centroid of its contiguous run, summed in input
 //                     order (the sort is stable) -- bit-identical to a sequential loop.
 //   k_integrate_rays  one thread per piece of a sensor ray (exact split, see below): range
-//                     cut, both ends to Q12
+//                     cut, both ends to Q16
 //                     (Q34), the exact DDA of the ID walk (dda.cuh, Q13) over every
 //                     visited voxel, whose flag byte gets 1 (visited) or 3 (the ray ends
 //                     here with a hit) OR-ed in with fire-and-forget atomics (Q35: each
@@ -24,7 +24,7 @@
 //                     store, the a2 delta when (state, level) changed.
 //
 // The apply pass leaves the flags zeroed, so no per-cloud clear is needed.  A poisoned
-// cloud (invalid point, Q12 overflow) updates nothing: the apply pass only clears flags.
+// cloud (invalid point, Q16 overflow) updates nothing: the apply pass only clears flags.
 #include <math.h>
 #include <stdlib.h>
 
@@ -43,8 +43,8 @@ using dda::Walk;
 constexpr double kKeyLimit = 32767.0;            // |cell index| < 2^15 - 1 (Q33)
 constexpr int kKeyBits = 48;                     // 16 bits per axis: 6 radix passes instead of 8
 constexpr uint64_t kBadKey = (1ull << kKeyBits) - 1;   // above every valid key (fields <= 0xFFFE)
-constexpr double kQ12Limit = 1073741824.0;       // |Q12 coordinate| < 2^30 (Q19)
-constexpr int kWideRayVoxels = 700;              // int32 DDA terms up to this many voxels per axis
+constexpr double kQ16Limit = 1073741824.0;       // |Q16 coordinate| < 2^30 (Q19)
+constexpr int kWideRayVoxels = 16000;            // int32 DDA terms below this many voxels per axis (k_id.cu: < 16383)
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
@@ -355,10 +355,10 @@ struct RayArgs {
     int nx, ny, nz;
 };
 
-__device__ __forceinline__ bool to_q12(double x, double org, double s, int &out)
+__device__ __forceinline__ bool to_q16(double x, double org, double s, int &out)
 {
-    const double q = __dmul_rn(__ddiv_rn(__dsub_rn(x, org), s), 4096.0);
-    if (!(fabs(q) < kQ12Limit)) return false;
+    const double q = __dmul_rn(__ddiv_rn(__dsub_rn(x, org), s), 65536.0);
+    if (!(fabs(q) < kQ16Limit)) return false;
     out = (int)rint(q);
     return true;
 }
@@ -428,10 +428,10 @@ __global__ void __launch_bounds__(kRayThreads) k_integrate_rays(const double *__
     const uint32_t n = n_rays_dev ? *n_rays_dev : n_rays_host;
     const uint64_t work = (uint64_t)n * kPieceSlots;      // thread t: slot t / n, ray t % n
     if (*bad || (uint64_t)blockIdx.x * blockDim.x >= work) return;
-    int o12[3];
+    int o16[3];
     bool ok = true;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) ok = ok && to_q12(a.sensor[k], a.org[k], a.s, o12[k]);
+    for (int k = 0; k < 3; ++k) ok = ok && to_q16(a.sensor[k], a.org[k], a.s, o16[k]);
     dda::MapView mv{};
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < work; t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t slot = (uint32_t)(t / n), i = (uint32_t)(t % n);
@@ -448,10 +448,10 @@ __global__ void __launch_bounds__(kRayThreads) k_integrate_rays(const double *__
             for (int k = 0; k < 3; ++k) q[k] = __dadd_rn(a.sensor[k], __dmul_rn(d[k], f));
             hit = 1u;
         }
-        int e12[3];
+        int e16[3];
         bool rok = ok;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) rok = rok && to_q12(q[k], a.org[k], a.s, e12[k]);
+        for (int k = 0; k < 3; ++k) rok = rok && to_q16(q[k], a.org[k], a.s, e16[k]);
         if (!rok) {
             if (slot == 0) {
                 atomicExch(bad, 1);
@@ -460,11 +460,11 @@ __global__ void __launch_bounds__(kRayThreads) k_integrate_rays(const double *__
             continue;
         }
         Walk<T> w0;
-        dda::walk_setup(w0, o12, e12);
+        dda::walk_setup(w0, o16, e16);
         long long ne[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            const long long dv = (long long)(e12[k] >> dda::kQShift) - (long long)(o12[k] >> dda::kQShift);
+            const long long dv = (long long)(e16[k] >> dda::kQShift) - (long long)(o16[k] >> dda::kQShift);
             ne[k] = dv < 0 ? -dv : dv;
         }
         const int A = (w0.ax >= w0.ay && w0.ax >= w0.az) ? 0 : (w0.ay >= w0.az ? 1 : 2);
@@ -725,8 +725,8 @@ nbt_status launch_integrate(nbt_ctx ctx, nbt_occ_s *o, nbt_map m, const double s
     o->last_points = n;
     o->last_filtered = p.leaf > 0.0;
     if (p.leaf > 0.0 && n > 0) {
-        st = getenv("NBT_FILTER_SORT") ? launch_voxel_filter(ctx, o, d_pts, n, p.leaf, nullptr)
-                                       : launch_voxel_filter_hashed(ctx, o, d_pts, n, p.leaf);
+        st = ctx->opt.filter_sort ? launch_voxel_filter(ctx, o, d_pts, n, p.leaf, nullptr)
+                                  : launch_voxel_filter_hashed(ctx, o, d_pts, n, p.leaf);
         if (st) return st;
         rays = o->filtered.as<double>();
         n_rays_dev = reinterpret_cast<const uint32_t *>(o->d_ctl + kOccRays);

@@ -279,8 +279,9 @@ nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const
     nbt_status st;
     const uint64_t nvox = (uint64_t)m->desc.nx * m->desc.ny * m->desc.nz;
     // the winner array (4 B per voxel, zero between updates) is allocated on the first update
-    // outside a graph capture; without it the sort form below is used
-    if (!m->d_win && !g_capturing && !getenv("NBT_DELTA_SORT")) {
+    // outside a graph capture; without it (or with NBT_OPT_DELTA_SORT) the sort form below is used
+    const bool sort_form = ctx->opt.delta_sort != 0;
+    if (!m->d_win && !g_capturing && !sort_form) {
         if (cudaMalloc(&m->d_win, nvox * 4) == cudaSuccess) {
             if (cudaMemsetAsync(m->d_win, 0, nvox * 4, ctx->stream) != cudaSuccess) {
                 cudaFree(m->d_win);
@@ -291,7 +292,7 @@ nbt_status launch_map_update(nbt_ctx ctx, nbt_map m, const int32_t *d_ijk, const
             cudaGetLastError();
         }
     }
-    if (m->d_win) {
+    if (m->d_win && !sort_form) {
         if (n <= NBT_DELTA_SMALL) {
             k_delta_win_apply_small<<<1, kDeltaOneBlock, 0, ctx->stream>>>(d_ijk, d_codes, d_levels, nn, geom_of(m),
                                                                           m->d_win, m->d_words, ctx->d_err);

@@ -123,6 +123,19 @@ struct ProfScope {
 
 // ----------------------------------------------------------------- handles
 
+// Tuning options of a ctx (nbt_ctx_set_option; none changes a result).
+struct NbtOptions {
+    int refill_min = 6;               // NBT_OPT_TRACE_REFILL_MIN
+    int chunk_min = 64;               // NBT_OPT_TRACE_CHUNK_MIN
+    int carveout = 25;                // NBT_OPT_TRACE_CARVEOUT
+    int delta_sort = 0;               // NBT_OPT_DELTA_SORT
+    int filter_sort = 0;              // NBT_OPT_FILTER_SORT
+    int h2d_mode = 0;                 // NBT_OPT_H2D_MODE
+    int copy_threads = 0;             // NBT_OPT_COPY_THREADS (default set at ctx creation)
+    int walk_width = 0;               // NBT_OPT_WALK_WIDTH
+    int verbose = 0;                  // NBT_OPT_VERBOSE
+};
+
 struct nbt_ctx_s {
     int refs = 1;                     // 1 for the ctx itself + 1 per live map / ID buffer / graph
     bool closed = false;              // nbt_ctx_destroy called
@@ -133,7 +146,8 @@ struct nbt_ctx_s {
     uint64_t launches = 0;
     int *d_err = nullptr;             // device-side validation status (nbt_status value)
     int *h_err = nullptr;             // pinned mirror
-    int trace_blocks_per_sm = 0;      // cached occupancy of the trace kernel (set once)
+    NbtOptions opt;
+    int trace_blocks_per_sm = 0;      // cached occupancy of the trace kernel (0: recompute at the next launch)
     int trace_bps[12] = {0};          // ... per instance [wide][morton][store kind]
     // scratch
     nbt::DevBuf persp;                // staged perspective origins (n x 3 f64)
@@ -207,6 +221,7 @@ struct nbt_gather_s {
     int32_t rows = 0, world = 0, rank = 0;
     char *base = nullptr;             // local rows: xyz rows*24 | gain rows*8 | counts rows*32
     char *peer[kMaxGatherRanks] = {}; // rank r's rows (own: base; others: opened IPC mappings)
+    PeerTotals *d_pt = nullptr;       // device copy of the peer-totals table (rewritten by every attach)
 };
 
 struct nbt_occ_s {
@@ -260,12 +275,14 @@ struct IdLaunch {
     const GatherDst *gather = nullptr;        // nbt_id_compute_gather: rows to every destination
     int32_t gather_row0 = 0;                  // ... at row gather_row0 + first + i*stride
     const PeerTotals *peer_totals = nullptr;  // nbt_id_compute_rays_gather: counts into every rank
+    const PeerTotals *d_peer_totals = nullptr; // ... the same table in device memory
+    uint32_t *d_record = nullptr;             // nbt_debug_id_rays: per-ray (U, F, O, L, stop), n x N_E x 5
 };
 nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L);
 nbt_status launch_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *d_o, const int32_t *d_e, int32_t n_rays,
                               int32_t max_visits, int32_t *d_ijk, uint8_t *d_code, int32_t *d_len,
                               uint32_t *d_counts, bool wide);
-bool debug_needs_wide(const int32_t *o_q12, const int32_t *e_q12, int32_t n_rays);
+bool debug_needs_wide(const int32_t *o_q16, const int32_t *e_q16, int32_t n_rays);
 nbt_status launch_debug_frames(nbt_ctx ctx, nbt_map m, const double poi[3], const double *d_persp, int32_t n,
                                const nbt_camera &cam, double range, int32_t *d_frames);
 

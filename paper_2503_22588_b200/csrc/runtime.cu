@@ -111,9 +111,9 @@ public:
     // Copy src -> dst; on_chunk(offset, len) is called on the caller's thread for every
     // chunk, in order, as soon as that chunk has landed.
     template <typename F>
-    void copy(void *dst, const void *src, size_t bytes, F &&on_chunk)
+    void copy(void *dst, const void *src, size_t bytes, bool parallel, F &&on_chunk)
     {
-        if (workers_.empty() || bytes < kMinParallel) {
+        if (!parallel || workers_.empty() || bytes < kMinParallel) {
             memcpy(dst, src, bytes);
             on_chunk(0, bytes);
             return;
@@ -144,22 +144,17 @@ public:
         std::unique_lock<std::mutex> lk(mu_);        // workers are done with dst/src
         idle_cv_.wait(lk, [&] { return active_ == 0; });
     }
-    void copy(void *dst, const void *src, size_t bytes)
+    void copy(void *dst, const void *src, size_t bytes, bool parallel)
     {
-        copy(dst, src, bytes, [](size_t, size_t) {});
+        copy(dst, src, bytes, parallel, [](size_t, size_t) {});
     }
 
 private:
     CopyPool()
     {
-        int n = 0;
-        if (const char *e = getenv("NBT_COPY_THREADS")) {
-            n = atoi(e);
-        } else {
-            n = std::thread::hardware_concurrency() >= 8 ? 4 : 0;
-        }
-        for (int k = 0; k < n; ++k) workers_.emplace_back([this] { run(); });
+        for (int k = 0; k < kWorkers; ++k) workers_.emplace_back([this] { run(); });
     }
+    static constexpr int kWorkers = 4;
     void run()
     {
         uint64_t seen = 0;
@@ -198,17 +193,13 @@ static nbt_status stage_h2d(nbt_ctx ctx, HostStage &st, DevBuf &dst, const void 
     nbt_status s;
     if ((s = dst.ensure(bytes))) return s;
     if (bytes == 0) return NBT_OK;
-    static const int mode = [] {
-        const char *e = getenv("NBT_H2D_MODE");
-        return e ? atoi(e) : 0;
-    }();
-    if (mode == 1) {   // experiment: let the driver stage the pageable source
+    if (ctx->opt.h2d_mode == 1) {   // experiment: let the driver stage the pageable source
         NBT_CUDA(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
         return NBT_OK;
     }
     if ((s = st.acquire(bytes))) return s;
     cudaError_t e = cudaSuccess;
-    CopyPool::get().copy(st.p, src, bytes, [&](size_t off, size_t len) {
+    CopyPool::get().copy(st.p, src, bytes, ctx->opt.copy_threads > 0, [&](size_t off, size_t len) {
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(static_cast<char *>(dst.p) + off, static_cast<char *>(st.p) + off, len,
                                 cudaMemcpyHostToDevice, ctx->stream);
@@ -225,7 +216,7 @@ static nbt_status d2h_sync(nbt_ctx ctx, void *dst, const void *src, size_t bytes
     if ((s = ctx->stage_out.acquire(bytes))) return s;
     NBT_CUDA(cudaMemcpyAsync(ctx->stage_out.p, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     NBT_CUDA(cudaStreamSynchronize(ctx->stream));
-    CopyPool::get().copy(dst, ctx->stage_out.p, bytes);
+    CopyPool::get().copy(dst, ctx->stage_out.p, bytes, ctx->opt.copy_threads > 0);
     return NBT_OK;
 }
 
@@ -366,6 +357,7 @@ nbt_status nbt_ctx_create(int device, void *cuda_stream, nbt_ctx *out)
     nbt_ctx c = new (std::nothrow) nbt_ctx_s();
     if (!c) return fail(NBT_ERR_OUT_OF_MEMORY, "nbt_ctx_create");
     c->device = device;
+    c->opt.copy_threads = std::thread::hardware_concurrency() >= 8 ? 1 : 0;
     cudaError_t e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess && cuda_stream) {
         c->stream = (cudaStream_t)cuda_stream;
@@ -382,6 +374,76 @@ nbt_status nbt_ctx_create(int device, void *cuda_stream, nbt_ctx *out)
     }
     *out = c;
     return NBT_OK;
+}
+
+// Tuning options (nbt.h): value ranges; none of them changes a result.
+nbt_status nbt_ctx_set_option(nbt_ctx ctx, int32_t option, int64_t value)
+{
+    if (!ctx) return fail(NBT_ERR_INVALID_ARG, "null ctx");
+    auto in = [&](int64_t lo, int64_t hi) { return value >= lo && value <= hi; };
+    NbtOptions &o = ctx->opt;
+    switch (option) {
+    case NBT_OPT_TRACE_REFILL_MIN:
+        if (!in(1, 32)) break;
+        o.refill_min = (int)value;
+        return NBT_OK;
+    case NBT_OPT_TRACE_CHUNK_MIN:
+        if (!in(32, 1024)) break;
+        o.chunk_min = (int)((value + 31) / 32 * 32);
+        return NBT_OK;
+    case NBT_OPT_TRACE_CARVEOUT:
+        if (!in(-1, 100)) break;
+        o.carveout = (int)value;
+        ctx->trace_blocks_per_sm = 0;     // re-apply the carveout and re-read the occupancy
+        return NBT_OK;
+    case NBT_OPT_DELTA_SORT:
+        if (!in(0, 1)) break;
+        o.delta_sort = (int)value;
+        return NBT_OK;
+    case NBT_OPT_FILTER_SORT:
+        if (!in(0, 1)) break;
+        o.filter_sort = (int)value;
+        return NBT_OK;
+    case NBT_OPT_H2D_MODE:
+        if (!in(0, 1)) break;
+        o.h2d_mode = (int)value;
+        return NBT_OK;
+    case NBT_OPT_COPY_THREADS:
+        if (!in(0, 1)) break;
+        o.copy_threads = (int)value;
+        return NBT_OK;
+    case NBT_OPT_WALK_WIDTH:
+        if (value != 0 && value != 32 && value != 64) break;
+        o.walk_width = (int)value;
+        return NBT_OK;
+    case NBT_OPT_VERBOSE:
+        if (!in(0, 1)) break;
+        o.verbose = (int)value;
+        ctx->trace_blocks_per_sm = 0;
+        return NBT_OK;
+    default:
+        return fail(NBT_ERR_INVALID_ARG, "nbt_ctx_set_option: unknown option " + std::to_string(option));
+    }
+    return fail(NBT_ERR_INVALID_ARG, "nbt_ctx_set_option: value " + std::to_string(value) + " out of range for option " +
+                                         std::to_string(option));
+}
+
+nbt_status nbt_ctx_get_option(nbt_ctx ctx, int32_t option, int64_t *value)
+{
+    if (!ctx || !value) return fail(NBT_ERR_INVALID_ARG, "nbt_ctx_get_option: null argument");
+    const NbtOptions &o = ctx->opt;
+    switch (option) {
+    case NBT_OPT_TRACE_REFILL_MIN: *value = o.refill_min; return NBT_OK;
+    case NBT_OPT_TRACE_CHUNK_MIN: *value = o.chunk_min; return NBT_OK;
+    case NBT_OPT_TRACE_CARVEOUT: *value = o.carveout; return NBT_OK;
+    case NBT_OPT_DELTA_SORT: *value = o.delta_sort; return NBT_OK;
+    case NBT_OPT_FILTER_SORT: *value = o.filter_sort; return NBT_OK;
+    case NBT_OPT_H2D_MODE: *value = o.h2d_mode; return NBT_OK;
+    case NBT_OPT_COPY_THREADS: *value = o.copy_threads; return NBT_OK;
+    case NBT_OPT_WALK_WIDTH: *value = o.walk_width; return NBT_OK;
+    case NBT_OPT_VERBOSE: *value = o.verbose; return NBT_OK;
+    default: return fail(NBT_ERR_INVALID_ARG, "nbt_ctx_get_option: unknown option " + std::to_string(option));
+    }
 }
 
 nbt_status nbt_ctx_set_stream(nbt_ctx ctx, void *cuda_stream)
@@ -564,6 +626,8 @@ void nbt_map_desc_default(nbt_map_desc *d, int32_t nx, int32_t ny, int32_t nz, d
     d->gain[1] = 0.12;    // Free: P = P_min (S:92 clamp, Q15)
     d->gain[2] = 0.03;    // Occupied: 1 - P_max (S:92 clamp, Q15)
     d->outside_policy = NBT_OUTSIDE_UNKNOWN;
+    d->layout = NBT_LAYOUT_LINEAR;
+    d->state_bits = 2;
 }
 
 static nbt_status check_desc(const nbt_map_desc *d)
@@ -579,6 +643,9 @@ static nbt_status check_desc(const nbt_map_desc *d)
         if (!(d->gain[k] >= 0) || !isfinite(d->gain[k])) return fail(NBT_ERR_INVALID_ARG, "gain must be finite, >= 0");
     if (d->outside_policy != NBT_OUTSIDE_UNKNOWN && d->outside_policy != NBT_OUTSIDE_CLIP)
         return fail(NBT_ERR_INVALID_ARG, "bad outside_policy");
+    if (d->layout != NBT_LAYOUT_LINEAR && d->layout != NBT_LAYOUT_MORTON)
+        return fail(NBT_ERR_INVALID_ARG, "bad layout");
+    if (d->state_bits != 2 && d->state_bits != 8) return fail(NBT_ERR_INVALID_ARG, "state_bits must be 2 or 8");
     return NBT_OK;
 }
 
@@ -597,23 +664,23 @@ static nbt_status map_create(nbt_ctx ctx, const nbt_map_desc *desc, int vbits, b
     m->prob = prob;
     m->px = desc->nx + 2 * kBorder; m->py = desc->ny + 2 * kBorder; m->pz = desc->nz + 2 * kBorder;
     m->nvox_pad = (uint64_t)m->px * m->py * m->pz;
-    // Store layout: linear by default (fewest instructions per voxel step, fastest on
-    // configs C' and D, profiles/r01_layouts.md); NBT_MAP_LAYOUT=morton selects the
-    // Morton cube (side >= max extent + 2 kBorder, a power of two, at most 1024^3 voxels
-    // and 8x the linear store), which is slightly faster on sparse ray lattices (config B).
-    {
+    // Store layout (desc->layout): linear by default (fewest instructions per voxel step,
+    // fastest on configs C' and D, profiles/r01_layouts.md), or the Morton cube (side >= max
+    // extent + 2 kBorder, a power of two, at most 1024^3 voxels and 8x the linear store),
+    // which is slightly faster on sparse ray lattices (config B).
+    if (desc->layout == NBT_LAYOUT_MORTON) {
         int maxn = desc->nx > desc->ny ? desc->nx : desc->ny;
         maxn = maxn > desc->nz ? maxn : desc->nz;
         int pb = 4;
         while ((1 << pb) < maxn + 2 * kBorder) ++pb;
         uint64_t cube = 1ull << (3 * pb);
-        const char *env = getenv("NBT_MAP_LAYOUT");
-        bool use = env && !strcmp(env, "morton") && pb <= 10 && cube <= 8 * m->nvox_pad;
-        if (use) {
-            m->layout = kLayoutMorton;
-            m->pbits = pb;
-            m->nvox_pad = cube;
+        if (pb > 10 || cube > 8 * m->nvox_pad) {
+            nbt_map_destroy(m);
+            return fail(NBT_ERR_INVALID_ARG, "nbt_map_create: the Morton cube must fit 1024^3 voxels and 8x the linear store");
         }
+        m->layout = kLayoutMorton;
+        m->pbits = pb;
+        m->nvox_pad = cube;
     }
     const size_t per_word = vbits == 2 ? 16 : 4;
     m->nwords = (size_t)((m->nvox_pad + per_word - 1) / per_word);
@@ -639,17 +706,11 @@ static nbt_status map_create(nbt_ctx ctx, const nbt_map_desc *desc, int vbits, b
     return NBT_OK;
 }
 
-// Bits per voxel of a state-only map: NBT_MAP_BITS=2 (packed codes) or 8 (one byte per
-// voxel: no rotate per visit, 4x the bytes); default 2.
-static int state_store_bits()
-{
-    const char *e = getenv("NBT_MAP_BITS");
-    return (e && atoi(e) == 8) ? 8 : 2;
-}
-
+// Bits per voxel of a state-only map (desc->state_bits): 2 (packed codes, default) or 8
+// (one byte per voxel: no rotate per visit, 4x the bytes).
 nbt_status nbt_map_create(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
 {
-    return map_create(ctx, desc, state_store_bits(), false, out);
+    return map_create(ctx, desc, desc ? desc->state_bits : 2, false, out);
 }
 
 nbt_status nbt_map_create_prob(nbt_ctx ctx, const nbt_map_desc *desc, nbt_map *out)
@@ -1187,7 +1248,9 @@ struct IdExtra {
     const uint64_t *totals_final = nullptr;
     const GatherDst *gather = nullptr;
     int32_t gather_row0 = 0;
-    const PeerTotals *peer_totals = nullptr;
+    const PeerTotals *peer_totals = nullptr;     // host copy (which ranks)
+    const PeerTotals *d_peer_totals = nullptr;   // the same table in device memory
+    uint32_t *record = nullptr;                  // nbt_debug_id_rays: per-ray counts (device)
 };
 
 // A caller's device array must live on the ctx's device (device or managed memory).
@@ -1254,6 +1317,8 @@ static nbt_status id_common(nbt_ctx ctx, nbt_map m, const double poi[3], const d
     L.gather = x.gather;
     L.gather_row0 = x.gather_row0;
     L.peer_totals = x.peer_totals;
+    L.d_peer_totals = x.d_peer_totals;
+    L.d_record = x.record;
     if (shard) return launch_id(ctx, m, L);
     size_t xyz_b = (size_t)n * 24, gain_b = (size_t)n * 8, cnt_b = (size_t)n * 32;
     if (out->on_device) {
@@ -1332,7 +1397,18 @@ nbt_status nbt_gather_create(nbt_ctx ctx, int32_t rows, int32_t world, int32_t r
     nbt_gather g = new (std::nothrow) nbt_gather_s();
     if (!g) return fail(NBT_ERR_OUT_OF_MEMORY, "nbt_gather_create");
     cudaError_t e = cudaMalloc(&g->base, (size_t)rows * 64);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_pt, sizeof(PeerTotals));
+    if (e == cudaSuccess) {
+        // the peer-totals table of nbt_id_compute_rays_gather, kept in device memory (rewritten
+        // by every attach) so that a captured ray-split launch copies it device to device
+        PeerTotals pt;
+        pt.n = world;
+        pt.t[rank] = reinterpret_cast<unsigned long long *>(g->base);
+        e = cudaMemcpy(g->d_pt, &pt, sizeof pt, cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) {
+        if (g->base) cudaFree(g->base);
+        if (g->d_pt) cudaFree(g->d_pt);
         delete g;
         return cuda_fail(e, "nbt_gather_create");
     }
@@ -1372,6 +1448,10 @@ nbt_status nbt_gather_attach(nbt_gather g, int32_t peer_rank, const uint8_t hand
     void *p = nullptr;
     NBT_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     g->peer[peer_rank] = static_cast<char *>(p);
+    PeerTotals pt;
+    pt.n = g->world;
+    for (int r = 0; r < g->world; ++r) pt.t[r] = reinterpret_cast<unsigned long long *>(g->peer[r]);
+    NBT_CUDA(cudaMemcpy(g->d_pt, &pt, sizeof pt, cudaMemcpyHostToDevice));
     return NBT_OK;
 }
 
@@ -1435,6 +1515,7 @@ nbt_status nbt_id_compute_rays_gather(nbt_ctx ctx, nbt_map m, const double poi[3
     x.ray_rank = g->rank;
     x.ray_world = g->world;
     x.peer_totals = &pt;
+    x.d_peer_totals = g->d_pt;
     return id_common(ctx, m, poi, persp_xyz, n_persp, persp_on_device, 0, 1, cam, range, nullptr,
                      "nbt_id_compute_rays_gather", x);
 }
@@ -1447,6 +1528,7 @@ void nbt_gather_destroy(nbt_gather g)
     for (int r = 0; r < g->world; ++r)
         if (g->peer[r] && r != g->rank) cudaIpcCloseMemHandle(g->peer[r]);
     if (g->base) cudaFree(g->base);
+    if (g->d_pt) cudaFree(g->d_pt);
     nbt_ctx ctx = g->ctx;
     delete g;
     ctx_release(ctx);
@@ -1488,7 +1570,6 @@ nbt_status nbt_idbuf_push(nbt_idbuf b, const nbt_ig_cloud *cloud, int32_t n)
     if ((s = bind(ctx))) return s;
     if (n < 1 || n > b->max_persp) return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_push: need 1 <= n <= max_persp");
     if (!cloud->xyz || !cloud->gain) return fail(NBT_ERR_INVALID_ARG, "nbt_idbuf_push: null cloud buffers");
-    if (b->count < b->capacity) b->count++;
     const double *sx = cloud->xyz, *sg = cloud->gain;
     if (!cloud->on_device) {
         if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_idbuf_push: host cloud during graph capture");
@@ -1501,7 +1582,9 @@ nbt_status nbt_idbuf_push(nbt_idbuf b, const nbt_ig_cloud *cloud, int32_t n)
         sx = ctx->out_tmp.as<double>();
         sg = sx + 3 * (size_t)n;
     }
-    return launch_idbuf_push(ctx, b, sx, sg, n);
+    if ((s = launch_idbuf_push(ctx, b, sx, sg, n))) return s;
+    if (b->count < b->capacity) b->count++;       // host mirror: only after the push is enqueued
+    return NBT_OK;
 }
 
 nbt_status nbt_idbuf_clear(nbt_idbuf b)
@@ -1635,19 +1718,19 @@ void nbt_idbuf_destroy(nbt_idbuf b)
 
 // -------------------------------------------------------------- test hooks
 
-nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *o_q12, const int32_t *e_q12, int32_t n_rays,
+nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *o_q16, const int32_t *e_q16, int32_t n_rays,
                            int32_t max_visits, int32_t *ijk_out, uint8_t *code_out, int32_t *len_out,
                            uint32_t *counts_out)
 {
     nbt_status s;
     if ((s = bind(ctx))) return s;
     if (!m || m->ctx != ctx) return fail(NBT_ERR_STATE, "nbt_debug_trace: map of another ctx");
-    if (n_rays < 0 || max_visits < 1 || (n_rays > 0 && (!o_q12 || !e_q12 || !ijk_out || !code_out || !len_out ||
+    if (n_rays < 0 || max_visits < 1 || (n_rays > 0 && (!o_q16 || !e_q16 || !ijk_out || !code_out || !len_out ||
                                                         !counts_out)))
         return fail(NBT_ERR_INVALID_ARG, "nbt_debug_trace: bad argument");
     if (n_rays == 0) return NBT_OK;
     for (int32_t i = 0; i < 3 * n_rays; ++i)
-        if (o_q12[i] <= -(1 << 30) || o_q12[i] >= (1 << 30) || e_q12[i] <= -(1 << 30) || e_q12[i] >= (1 << 30))
+        if (o_q16[i] <= -(1 << 30) || o_q16[i] >= (1 << 30) || e_q16[i] <= -(1 << 30) || e_q16[i] >= (1 << 30))
             return fail(NBT_ERR_INVALID_ARG, "nbt_debug_trace: coordinate outside (-2^30, 2^30)");
     size_t nr = n_rays, mv = max_visits;
     size_t b_in = nr * 12, b_ijk = nr * mv * 12, b_code = nr * mv, b_len = nr * 4, b_cnt = nr * 16;
@@ -1659,9 +1742,12 @@ nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *o_q12, const i
     int32_t *d_len = (int32_t *)(base + 2 * b_in + b_ijk);
     uint32_t *d_cnt = (uint32_t *)(base + 2 * b_in + b_ijk + b_len);
     uint8_t *d_code = (uint8_t *)(base + 2 * b_in + b_ijk + b_len + b_cnt);
-    NBT_CUDA(cudaMemcpyAsync(d_o, o_q12, b_in, cudaMemcpyHostToDevice, ctx->stream));
-    NBT_CUDA(cudaMemcpyAsync(d_e, e_q12, b_in, cudaMemcpyHostToDevice, ctx->stream));
-    const bool wide = debug_needs_wide(o_q12, e_q12, n_rays);
+    NBT_CUDA(cudaMemcpyAsync(d_o, o_q16, b_in, cudaMemcpyHostToDevice, ctx->stream));
+    NBT_CUDA(cudaMemcpyAsync(d_e, e_q16, b_in, cudaMemcpyHostToDevice, ctx->stream));
+    const bool need_wide = debug_needs_wide(o_q16, e_q16, n_rays);
+    if (ctx->opt.walk_width == 32 && need_wide)
+        return fail(NBT_ERR_INVALID_ARG, "nbt_debug_trace: int32 walk forced on a segment with |E - O| >= 2^30 - 1");
+    const bool wide = ctx->opt.walk_width == 64 || (ctx->opt.walk_width == 0 && need_wide);
     if ((s = launch_debug_trace(ctx, m, d_o, d_e, n_rays, max_visits, d_ijk, d_code, d_len, d_cnt, wide))) return s;
     NBT_CUDA(cudaMemcpyAsync(ijk_out, d_ijk, b_ijk, cudaMemcpyDeviceToHost, ctx->stream));
     NBT_CUDA(cudaMemcpyAsync(code_out, d_code, b_code, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1669,6 +1755,30 @@ nbt_status nbt_debug_trace(nbt_ctx ctx, nbt_map m, const int32_t *o_q12, const i
     NBT_CUDA(cudaMemcpyAsync(counts_out, d_cnt, b_cnt, cudaMemcpyDeviceToHost, ctx->stream));
     NBT_CUDA(cudaStreamSynchronize(ctx->stream));
     return NBT_OK;
+}
+
+// Per-ray counts of the production trace kernel (its REC instance: the same code, recording
+// every closed ray), for per-ray parity against the oracle's perspective_rays.
+nbt_status nbt_debug_id_rays(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp_xyz, int32_t n,
+                             const nbt_camera *cam, double range, uint32_t *ray_counts_out)
+{
+    nbt_status s;
+    if ((s = bind(ctx))) return s;
+    if (ctx->capturing) return fail(NBT_ERR_STATE, "nbt_debug_id_rays: not inside a graph capture");
+    if ((s = check_camera(cam))) return s;
+    if (n < 0 || (n > 0 && (!persp_xyz || !ray_counts_out)))
+        return fail(NBT_ERR_INVALID_ARG, "nbt_debug_id_rays: bad argument");
+    if (n == 0) return NBT_OK;
+    const size_t ne = (size_t)cam->width * cam->height + (cam->add_corners ? 4 : 0);
+    const size_t bytes = (size_t)n * ne * 5 * sizeof(uint32_t);
+    if ((s = ctx->dbg.ensure(bytes))) return s;
+    NBT_CUDA(cudaMemsetAsync(ctx->dbg.p, 0xFF, bytes, ctx->stream));     // unwritten rays read as ~0
+    std::vector<double> xyz((size_t)n * 3), gain((size_t)n);
+    nbt_ig_cloud out{xyz.data(), gain.data(), nullptr, 0};
+    IdExtra x;
+    x.record = ctx->dbg.as<uint32_t>();
+    if ((s = id_common(ctx, m, poi, persp_xyz, n, 0, 0, 1, cam, range, &out, "nbt_debug_id_rays", x))) return s;
+    return d2h_sync(ctx, ray_counts_out, ctx->dbg.p, bytes);
 }
 
 nbt_status nbt_debug_frames(nbt_ctx ctx, nbt_map m, const double poi[3], const double *persp_xyz, int32_t n,

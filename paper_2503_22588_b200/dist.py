@@ -215,6 +215,19 @@ def id_compute_ray_split(nbt, ctx, m, poi, persp_dev, cam, range_, rank: int, wo
     return cloud.xyz, cloud.gain, cloud.counts
 
 
+class PeerUnavailable(RuntimeError):
+    """Some rank could not map a peer's buffer (raised on every rank alike)."""
+
+
+def make_peer_gather(nbt, ctx, rows: int, rank: int, world: int, group=None, n_buffers: int = 2):
+    """A PeerGather, or None (on every rank) when peer mapping is unavailable: the caller then
+    uses the NCCL all-gather (id_compute_sharded / all_gather_rows) instead."""
+    try:
+        return PeerGather(nbt, ctx, rows, rank, world, group=group, n_buffers=n_buffers)
+    except PeerUnavailable:
+        return None
+
+
 class PeerGather:
     """The IG-cloud all-gather fused into the finalize over peer memory (nbt_gather_*): two
     library-owned row buffers per rank (alternated between cycles, so a rank never rewrites a
@@ -230,10 +243,21 @@ class PeerGather:
         mine = [g.export() for g in self.bufs]
         everyone = [None] * world
         dist.all_gather_object(everyone, mine, group=group)
-        for g_idx, g in enumerate(self.bufs):
-            for r in range(world):
-                if r != rank:
-                    g.attach(r, everyone[r][g_idx])
+        err = None
+        try:
+            for g_idx, g in enumerate(self.bufs):
+                for r in range(world):
+                    if r != rank:
+                        g.attach(r, everyone[r][g_idx])
+        except nbt.NbtError as e:      # e.g. CUDA IPC unavailable between these processes
+            err = str(e)
+        # every rank learns whether every rank could map every peer
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=group)
+        bad = [f"rank {r}: {x}" for r, x in enumerate(errs) if x]
+        if bad:
+            self.close()
+            raise PeerUnavailable("; ".join(bad))
         self.cycle = 0
 
     def id_compute(self, m, poi, persp_dev, cam, range_):
@@ -267,7 +291,8 @@ class PeerGather:
         all-reduce fused into the walk (remote atomics into every rank's buffer): returns the
         same (xyz, gain, counts) on every rank, bit-identical to one GPU."""
         import torch
-        g = self.bufs[0]
+        g = self.bufs[self.cycle % len(self.bufs)]     # never the buffer an earlier result views
+        self.cycle += 1
         n = persp_dev.shape[0]
         g.zero()
         self.order_readers()                 # every rank's clear before any rank's adds

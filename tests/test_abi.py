@@ -61,7 +61,7 @@ def test_no_oracle_in_product():
 
 
 def test_status_strings(lib):
-    assert nbt.nbt_abi_version() == 1
+    assert nbt.nbt_abi_version() == 2
     assert lib.nbt_status_string(2) == b"NBT_ERR_DEGENERATE"
 
 

@@ -102,10 +102,9 @@ def test_voxel_filter_device_input_and_errors(nbt, ctx):
         nbt.voxel_filter(ctx, np.array([[0.0, 32767.5, 0.0]]), 1.0)
 
 
-def _run_sequence(nbt, ctx, cf, n_clouds, prob, layout, monkeypatch, params=None, L_start=None):
-    monkeypatch.setenv("NBT_MAP_LAYOUT", layout)
+def _run_sequence(nbt, ctx, cf, n_clouds, prob, layout, params=None, L_start=None, bits=2):
     n = cf.n
-    desc = nbt.map_desc(n, n, n, cf.voxel_size)
+    desc = nbt.map_desc(n, n, n, cf.voxel_size, layout=layout, state_bits=bits)
     occ = nbt.OccMap(ctx, desc)
     m = nbt.Map(ctx, desc, prob=prob)
     L = oracle.new_logodds((n, n, n))
@@ -141,38 +140,37 @@ def _run_sequence(nbt, ctx, cf, n_clouds, prob, layout, monkeypatch, params=None
 
 @pytest.mark.parametrize("store", ["2bit", "byte", "prob"])
 @pytest.mark.parametrize("layout", ["linear", "morton"])
-def test_integrate_sequence_small(nbt, ctx, store, layout, monkeypatch):
+def test_integrate_sequence_small(nbt, ctx, store, layout):
     cf = I.CLOUD_CONFIGS["F0"]
-    monkeypatch.setenv("NBT_MAP_BITS", "8" if store == "byte" else "2")
-    _run_sequence(nbt, ctx, cf, cf.n_clouds, store == "prob", layout, monkeypatch)
+    _run_sequence(nbt, ctx, cf, cf.n_clouds, store == "prob", layout, bits=8 if store == "byte" else 2)
 
 
 @pytest.mark.parametrize("prob", [False, True])
-def test_integrate_sequence_full_size(nbt, ctx, prob, monkeypatch):
+def test_integrate_sequence_full_size(nbt, ctx, prob):
     """Config F: 256^3 at 1 cm, 640x576 Azure-Kinect-size frames, 3 poses."""
     cf = I.CLOUD_CONFIGS["F"]
-    _run_sequence(nbt, ctx, cf, 3, prob, "linear", monkeypatch)
+    _run_sequence(nbt, ctx, cf, 3, prob, "linear")
 
 
-def test_integrate_without_filter_and_unlimited_range(nbt, ctx, monkeypatch):
+def test_integrate_without_filter_and_unlimited_range(nbt, ctx):
     """leaf = 0 (every point is a ray) and max_range <= 0 (the 64-bit DDA variant)."""
     cf = I.CLOUD_CONFIGS["F0"]
-    _run_sequence(nbt, ctx, cf, 2, True, "linear", monkeypatch, params=dict(leaf=0.0, max_range=0.0))
+    _run_sequence(nbt, ctx, cf, 2, True, "linear", params=dict(leaf=0.0, max_range=0.0))
 
 
-def test_integrate_from_observed_start_hits_clamps(nbt, ctx, monkeypatch):
+def test_integrate_from_observed_start_hits_clamps(nbt, ctx):
     """Start from a store with random observed log-odds near the clamps and thresholds."""
     cf = I.CLOUD_CONFIGS["F0"]
     rng = np.random.default_rng(8)
     L0 = rng.choice(np.array([np.nan, 0.0, -0.4054651, 3.4, -1.9, 0.5, -1e-7, 1e-7], np.float32),
                     size=(cf.n,) * 3).astype(np.float32)
-    _run_sequence(nbt, ctx, cf, 2, False, "linear", monkeypatch, L_start=L0)
+    _run_sequence(nbt, ctx, cf, 2, False, "linear", L_start=L0)
 
 
-def test_integrate_sensor_and_points_outside_grid(nbt, ctx, monkeypatch):
+def test_integrate_sensor_and_points_outside_grid(nbt, ctx):
     """A sensor outside the grid, points on both sides: only in-grid voxels change."""
     cf = I.CloudConfig("Fo", 40, 0.05, 3.0, 96, 80, 1.6, 2, 0.05, 3.0, 5)
-    _run_sequence(nbt, ctx, cf, 2, True, "linear", monkeypatch)
+    _run_sequence(nbt, ctx, cf, 2, True, "linear")
 
 
 def test_integrate_zero_points_and_bad_cloud(nbt, ctx):
@@ -229,9 +227,9 @@ def test_integrate_device_points_and_id_after(nbt, ctx):
     assert np.array_equal(cloud.gain, g)
 
 
-def test_integrate_exact_ties_and_long_rays(nbt, ctx, monkeypatch):
+def test_integrate_exact_ties_and_long_rays(nbt, ctx):
     """Rays whose ends sit on voxel faces, edges and corners (exact ties in the DDA) and long
-    rays cut into many pieces: sensor on a voxel corner, points on the Q12 lattice, no
+    rays cut into many pieces: sensor on a voxel corner, points on the Q16 lattice, no
     filter, unlimited range (64-bit walk) and a 3-voxel range (int32 walk)."""
     n = 48
     rng = np.random.default_rng(12)
@@ -280,20 +278,21 @@ def test_integrate_few_dense_cells(nbt, ctx):
 
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("NBT_FUZZ_SEEDS", "8"))))
-def test_integrate_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
+def test_integrate_random_configurations_fuzz(nbt, ctx, seed):
     """Random non-cubic grids (voxel size, origin), sensors inside or outside, random point
-    clouds (Gaussian blobs, uniform, on the Q12 lattice), random leaf / range / probabilities /
+    clouds (Gaussian blobs, uniform, on the Q16 lattice), random leaf / range / probabilities /
     thresholds, random start store, layout and store kind: log-odds, deltas and the ID map
     bit-exact vs the oracle over 3 clouds."""
     rng = np.random.default_rng(2000 + seed)
-    monkeypatch.setenv("NBT_MAP_LAYOUT", "morton" if rng.random() < 0.3 else "linear")
+    layout = "morton" if rng.random() < 0.3 else "linear"
     store = rng.choice(["2bit", "byte", "prob"])
-    monkeypatch.setenv("NBT_MAP_BITS", "8" if store == "byte" else "2")
     nx, ny, nz = (int(v) for v in rng.integers(4, 40, 3))
+    if layout == "morton" and max(nx, ny, nz) ** 3 > 64 * nx * ny * nz:
+        layout = "linear"
     s = float(rng.choice([0.02, 0.1, 0.5, 1.0]))
     origin = tuple(float(v) for v in rng.uniform(-10, 10, 3) * s)
     ext = np.array([nx, ny, nz], float) * s
-    desc = nbt.map_desc(nx, ny, nz, s, origin)
+    desc = nbt.map_desc(nx, ny, nz, s, origin, layout=layout, state_bits=8 if store == "byte" else 2)
     occ = nbt.OccMap(ctx, desc)
     m = nbt.Map(ctx, desc, prob=store == "prob")
     kw = dict(leaf=float(rng.choice([0.0, s, 0.5 * s, 2.7 * s])),
@@ -331,12 +330,15 @@ def test_integrate_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
         assert np.array_equal(m.download_levels(), map_levels_expected(codes, levels))
 
 
-def test_integrate_sorted_filter_path_matches(nbt, ctx, monkeypatch):
-    """The sort-based voxel filter (NBT_FILTER_SORT=1, the experiment knob) integrates to the
-    same store as the default hashed grouping (both bit-exact vs the oracle)."""
-    monkeypatch.setenv("NBT_FILTER_SORT", "1")
-    cf = I.CLOUD_CONFIGS["F0"]
-    _run_sequence(nbt, ctx, cf, 2, True, "linear", monkeypatch)
+def test_integrate_sorted_filter_path_matches(nbt, ctx):
+    """The sort-based voxel filter (option NBT_OPT_FILTER_SORT, the experiment knob) integrates
+    to the same store as the default hashed grouping (both bit-exact vs the oracle)."""
+    ctx.set_option(nbt.OPT_FILTER_SORT, 1)
+    try:
+        cf = I.CLOUD_CONFIGS["F0"]
+        _run_sequence(nbt, ctx, cf, 2, True, "linear")
+    finally:
+        ctx.set_option(nbt.OPT_FILTER_SORT, 0)
 
 
 def test_integrate_captured_in_a_graph(nbt, ctx):

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
-from nbt_inputs import CONFIGS, FOV_H, FOV_V, rand_map, random_segments_q12, tie_segments_q12, syn_map
+from nbt_inputs import CONFIGS, FOV_H, FOV_V, Q16, rand_map, random_segments_q16, tie_segments_q16, syn_map
 
 pytestmark = pytest.mark.gpu
 
@@ -32,9 +32,11 @@ def ctx(nbt):
     return nbt.Ctx(0)
 
 
-def make_map(nbt, ctx, codes, voxel_size=1.0, origin=(0.0, 0.0, 0.0), gain=None, policy=0):
+def make_map(nbt, ctx, codes, voxel_size=1.0, origin=(0.0, 0.0, 0.0), gain=None, policy=0, layout="linear",
+             bits=2):
+    """Device map (store layout and bits per voxel chosen through the descriptor) + oracle map."""
     nz, ny, nx = codes.shape
-    m = nbt.Map(ctx, nbt.map_desc(nx, ny, nz, voxel_size, origin, gain, policy))
+    m = nbt.Map(ctx, nbt.map_desc(nx, ny, nz, voxel_size, origin, gain, policy, layout=layout, state_bits=bits))
     m.upload(codes)
     om = oracle.OracleMap(codes, voxel_size=voxel_size, origin=origin,
                           gain=gain if gain is not None else (1.0, 0.12, 0.03), outside_policy=policy)
@@ -101,13 +103,12 @@ def _apply_in_order(codes, ijk, vals):
 @pytest.mark.parametrize("n", [5000, 20000])
 @pytest.mark.parametrize("form", ["winner", "sort"])
 @pytest.mark.parametrize("on_device", [False, True])
-def test_map_update_last_wins(nbt, ctx, on_device, form, n, monkeypatch):
+def test_map_update_last_wins(nbt, ctx, on_device, form, n):
     """Duplicated voxels resolve to the last delta (Q30), in both update forms (the
     winner array -- one single-block launch up to 8192 deltas, two grid-wide passes above --
     and the radix sort used when the array is absent), over repeated updates."""
     import torch
-    if form == "sort":
-        monkeypatch.setenv("NBT_DELTA_SORT", "1")
+    ctx.set_option(nbt.OPT_DELTA_SORT, int(form == "sort"))
     codes = rand_map(0, seed=5, shape=(13, 17, 19))
     m, _ = make_map(nbt, ctx, codes)
     rng = np.random.default_rng(2)
@@ -122,6 +123,7 @@ def test_map_update_last_wins(nbt, ctx, on_device, form, n, monkeypatch):
         ctx.sync()
         codes = _apply_in_order(codes, ijk, vals)
         assert np.array_equal(m.download(), codes)
+    ctx.set_option(nbt.OPT_DELTA_SORT, 0)
 
 
 def test_map_update_validation(nbt, ctx):
@@ -160,7 +162,7 @@ def test_walks_random_segments(nbt, ctx, policy):
     """Every visited voxel of 3000 random rays, inside, leaving and outside the grid."""
     codes = rand_map(12, 0.3, 0.68, 0.02, seed=7)
     m, om = make_map(nbt, ctx, codes, policy=policy)
-    o, e = random_segments_q12(3000, -5.0, 17.0, seed=policy + 1)
+    o, e = random_segments_q16(3000, -5.0, 17.0, seed=policy + 1)
     _compare_walks(nbt, ctx, m, om, o, e)
 
 
@@ -168,8 +170,8 @@ def test_walks_ties(nbt, ctx):
     """Endpoints on faces, edges and corners (exact ties of the DDA)."""
     codes = rand_map(8, 0.4, 0.6, 0.0, seed=2)
     m, om = make_map(nbt, ctx, codes)
-    o, e = tie_segments_q12(4000, 9, seed=4)
-    o -= 4096
+    o, e = tie_segments_q16(4000, 9, seed=4)
+    o -= Q16
     _compare_walks(nbt, ctx, m, om, o, e)
 
 
@@ -178,8 +180,8 @@ def test_walks_hand_traced(nbt, ctx):
     m, om = make_map(nbt, ctx, np.ones((4, 4, 4), np.uint8))
     for row in read_golden("dda_hand_traced.txt"):
         _, o, e, seq = [s.strip() for s in row.split("|")]
-        o = [int(round(float(v) * 4096)) for v in o.split()]
-        e = [int(round(float(v) * 4096)) for v in e.split()]
+        o = [int(round(float(v) * Q16)) for v in o.split()]
+        e = [int(round(float(v) * Q16)) for v in e.split()]
         want = [tuple(int(t) for t in v.split()) for v in seq.split(";")]
         ijk, _, ln, _ = nbt.debug_trace(ctx, m, [o], [e], 16)
         assert [tuple(v) for v in ijk[0, :ln[0]]] == want
@@ -189,8 +191,58 @@ def test_walks_long_rays(nbt, ctx):
     """Long walks (1000+ voxels) through a sparse map: no drift of the decision terms."""
     codes = rand_map(64, 0.5, 0.5, 0.0, seed=9)
     m, om = make_map(nbt, ctx, codes)
-    o, e = random_segments_q12(200, -30.0, 94.0, seed=12)
+    o, e = random_segments_q16(200, -30.0, 94.0, seed=12)
     _compare_walks(nbt, ctx, m, om, o, e, max_visits=400)
+
+
+# ------------------------------------------- per-ray parity of the production trace kernel
+
+def _per_ray_check(nbt, ctx, m, om, poi, P, cam, ocam, range_):
+    rays = nbt.debug_id_rays(ctx, m, poi, P, cam, range_)
+    cloud = nbt.id_compute(ctx, m, poi, P, cam, range_)
+    for j in range(len(P)):
+        _, _, want = oracle.perspective_rays(om, poi, P[j], ocam, range_)
+        assert np.array_equal(rays[j].astype(np.int64), want), j
+    # the recorded rays sum to the production kernel's per-perspective totals
+    assert np.array_equal(rays[:, :, :4].sum(1, dtype=np.int64), cloud.counts.astype(np.int64))
+
+
+def test_production_trace_per_ray_config_a(nbt, ctx):
+    """All 12,288 rays of config A through the production k_id_trace code (batched walk,
+    ffs/popc stop masks, refill queue) in its record instance: every ray's (n_U, n_F, n_O,
+    lookups, stop) equals the oracle's (P:213 early stop, Q11-Q14), bit for bit."""
+    cfg = CONFIGS["A"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    _per_ray_check(nbt, ctx, m, om, cfg.poi, P, cam, ocam, cfg.range_)
+
+
+def test_production_trace_per_ray_config_b_subset(nbt, ctx):
+    """Config B's map and camera, 6 of its perspectives (18,432 rays): per-ray parity of the
+    production trace kernel."""
+    cfg = CONFIGS["B"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)[::85][:6]
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    _per_ray_check(nbt, ctx, m, om, cfg.poi, P, cam, ocam, cfg.range_)
+
+
+@pytest.mark.parametrize("layout,bits,policy", [("linear", 2, 1), ("morton", 2, 0), ("linear", 8, 0),
+                                                ("morton", 8, 1)])
+def test_production_trace_per_ray_stores(nbt, ctx, layout, bits, policy):
+    """Per-ray parity of the production trace on both layouts, both state widths and both
+    outside policies, with perspectives outside the map and corner rays."""
+    codes = rand_map(0, 0.3, 0.66, 0.04, seed=21, shape=(19, 27, 33))
+    m, om = make_map(nbt, ctx, codes, policy=policy, layout=layout, bits=bits)
+    poi = np.array([16.5, 13.5, 9.5])
+    P = oracle.sample_perspectives(poi, 25.0, 10, seed=2)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 21, 13)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, 21, 13)
+    cam.add_corners = ocam.add_corners = 1
+    _per_ray_check(nbt, ctx, m, om, poi, P, cam, ocam, 30.0)
 
 
 # ---------------------------------------------------------------- frames
@@ -391,18 +443,20 @@ def test_ray_split_matches_oracle(nbt, ctx, w, h, corners, worlds):
 
 
 @pytest.mark.parametrize("layout", ["linear", "morton"])
-@pytest.mark.parametrize("range_", [30.0, 800.0])
-def test_ray_split_layouts_and_wide_rays(nbt, ctx, layout, range_, monkeypatch):
-    """The ray-shard kernel instances of both map layouts and of the 64-bit walk (rays over
-    700 voxels per axis): shard totals sum to the whole ID's, which equals the oracle's."""
+@pytest.mark.parametrize("range_", [30.0, 16500.0])
+def test_ray_split_layouts_and_wide_rays(nbt, ctx, layout, range_):
+    """The ray-shard kernel instances of both map layouts and of the 64-bit walk (rays longer
+    than the int32 bound of 16383 voxels per axis: perspectives ~8200 voxels outside the map,
+    range 16500, narrow FoV): shard totals sum to the whole ID's, which equals the oracle's."""
     import torch
-    monkeypatch.setenv("NBT_MAP_LAYOUT", layout)
     codes = rand_map(0, 0.35, 0.64, 0.01, seed=11, shape=(40, 44, 48))
-    m, om = make_map(nbt, ctx, codes)
+    m, om = make_map(nbt, ctx, codes, layout=layout)
     poi = np.array([24.5, 22.5, 20.5])
-    P = oracle.sample_perspectives(poi, 15.0, 6, seed=5)
-    cam = nbt.camera_from_fov(FOV_H, FOV_V, 21, 13)
-    ocam = oracle.camera_from_fov(FOV_H, FOV_V, 21, 13)
+    wide = range_ > 16000
+    P = oracle.sample_perspectives(poi, 8200.0 if wide else 15.0, 6, seed=5, mode=int(wide))
+    fh, fv = (0.2, 0.2) if wide else (FOV_H, FOV_V)
+    cam = nbt.camera_from_fov(fh, fv, 21, 13)
+    ocam = oracle.camera_from_fov(fh, fv, 21, 13)
     _, g, c = oracle.id_compute(om, poi, P, ocam, range_, nthreads=NTHREADS)
     parts = [nbt.id_compute_rays(ctx, m, poi, P, cam, range_, r, 3) for r in range(3)]
     ctx.sync()
@@ -433,6 +487,34 @@ def test_ray_split_fused_into_peer_totals_one_rank(nbt, ctx):
         assert np.array_equal(fin.gain, full.gain)
     with pytest.raises(nbt.NbtError):                    # 20 x 40 B do not fit 16 x 64 B
         g.compute_rays(m, cfg.poi, oracle.sample_perspectives(cfg.poi, 20.0, 30, seed=1), cam, cfg.range_)
+    g.close()
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_ray_split_fused_outside_origins(nbt, ctx, policy):
+    """The fused ray split (counts into the peer totals) with perspectives outside the map and
+    rays that never enter it: their Unknown visits (outside policy) reach the peer totals, so
+    the finalized cloud equals the whole ID and the oracle."""
+    codes = rand_map(16, 0.3, 0.69, 0.01, seed=11)
+    m, om = make_map(nbt, ctx, codes, 1.0, policy=policy)
+    poi = np.array([8.0, 8.0, 8.0])
+    rng = np.random.default_rng(1)
+    d = rng.normal(size=(9, 3)); d /= np.linalg.norm(d, axis=1, keepdims=True)
+    P = poi + d * rng.uniform(9, 30, (9, 1))
+    P[0] = [-20.0, 8.0, 8.0]
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, 16, 12)
+    cam.add_corners = 1
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, 16, 12)
+    ocam.add_corners = 1
+    _, g_ref, c_ref = oracle.id_compute(om, poi, P, ocam, 40.0, nthreads=NTHREADS)
+    g = nbt.Gather(ctx, 16, 1, 0)
+    g.zero()
+    g.compute_rays(m, poi, P, cam, 40.0)
+    ctx.sync()
+    t = g.totals(len(P)).clone()
+    assert np.array_equal(t.cpu().numpy()[:, :4], c_ref)
+    fin = nbt.id_finalize(ctx, m, poi, P, cam, 40.0, t)
+    assert np.array_equal(fin.gain, g_ref)
     g.close()
 
 
@@ -603,38 +685,82 @@ def test_full_size_config_b_sampled(nbt, ctx):
 # ------------------------------------------------ 64-bit decision-term variant
 
 def test_walks_very_long_rays_wide_path(nbt, ctx):
-    """Segments longer than 720 voxels per axis run the int64 variant of the same walk."""
+    """Segments of 16000+ voxels on one axis run the int64 variant of the same walk."""
     codes = rand_map(40, 0.5, 0.5, 0.0, seed=13)
     m, om = make_map(nbt, ctx, codes)
     rng = np.random.default_rng(5)
-    o = np.round(rng.uniform(5, 35, (60, 3)) * 4096).astype(np.int32)
-    d = rng.normal(size=(60, 3)); d /= np.linalg.norm(d, axis=1, keepdims=True)
-    e = np.round((o / 4096 + d * rng.uniform(800, 2500, (60, 1))) * 4096).astype(np.int32)
-    _compare_walks(nbt, ctx, m, om, o, e, max_visits=64)
+    o = np.round(rng.uniform(5, 35, (40, 3)) * Q16).astype(np.int64)
+    d = rng.normal(size=(40, 3)) * [0.2, 0.2, 0.2]
+    d[:, 0] = -1.0                                       # x dominant, towards -x
+    e = np.round(o / Q16 + d * rng.uniform(16100, 16300, (40, 1))) * Q16
+    _compare_walks(nbt, ctx, m, om, o.astype(np.int32), e.astype(np.int32), max_visits=64)
+
+
+@pytest.mark.parametrize("width", [32, 64])
+def test_int32_bound_long_rays(nbt, ctx, width):
+    """The int32 decision terms at their tight bound (k_id.cu header: exact while every
+    |E_a - O_a| < 2^30 - 1 Q16 units, i.e. < 16383 voxels): segments with |D_x| = 2^30 - 2
+    (the longest int32 segment) and just below, axis-parallel and diagonal, walked with the
+    terms forced to int32 and to int64, equal the oracle; forcing int32 on |D_x| = 2^30 - 1
+    is refused.  Also the former 690-720-voxel boundary region, both widths."""
+    codes = rand_map(40, 0.45, 0.5, 0.0, seed=23)
+    m, om = make_map(nbt, ctx, codes)
+    rng = np.random.default_rng(8)
+    lim = (1 << 30) - 2
+    o, e = [], []
+    for k in range(24):
+        oo = np.array([int(rng.integers(0, 40 * Q16)) for _ in range(3)], np.int64)
+        dx = lim - int(rng.integers(0, 3 * Q16)) if k % 2 else lim
+        oo[0] = min(oo[0], lim - dx + 39 * Q16)          # keep E inside (-2^30, 2^30)
+        dy = int(rng.integers(-(1 << 29), 1 << 29)) if k % 3 else 0
+        dz = int(rng.integers(-(1 << 28), 1 << 28)) if k % 4 else 0
+        o.append(oo)
+        e.append(oo - np.array([dx, dy, dz], np.int64))
+    for L in (690, 699, 700, 701, 719, 720, 721):       # the former int32 switch (round 1)
+        oo = np.array([20 * Q16 + 777, 20 * Q16 + 12345, 20 * Q16 + 999], np.int64)
+        o.append(oo); e.append(oo + np.array([L * Q16 + 5, -L * Q16 + 3, 0]))
+        o.append(oo); e.append(oo + np.array([L * Q16 + 5, L * Q16 // 2 + 11, -L * Q16 // 3 - 7]))
+    o, e = np.array(o).astype(np.int32), np.array(e).astype(np.int32)
+    assert (np.abs(e.astype(np.int64) - o).max(1) <= lim).all()
+    ctx.set_option(nbt.OPT_WALK_WIDTH, width)
+    try:
+        _compare_walks(nbt, ctx, m, om, o, e, max_visits=96)
+        if width == 32:
+            too_long = np.array([[39 * Q16, 5 * Q16, 5 * Q16]], np.int32)
+            with pytest.raises(nbt.NbtError):
+                nbt.debug_trace(ctx, m, too_long, too_long - np.array([[lim + 1, 0, 0]], np.int32), 8)
+    finally:
+        ctx.set_option(nbt.OPT_WALK_WIDTH, 0)
 
 
 def test_id_wide_path(nbt, ctx):
-    """A range long enough (> 700 voxels) to select the int64 trace kernel."""
+    """Rays longer than the int32 bound (range 16500 voxels from perspectives ~8200 voxels
+    outside the map, so both ends stay inside the Q16 coordinate range) select the int64
+    trace kernel; the ID equals the oracle."""
     codes = rand_map(48, 0.3, 0.69, 0.01, seed=17)
     m, om = make_map(nbt, ctx, codes, 1.0)
     poi = np.array([24.5, 24.5, 24.5])
-    P = oracle.sample_perspectives(poi, 15.0, 12, seed=6)
-    cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 12, 9, 900.0, corners=True)
+    P = oracle.sample_perspectives(poi, 8200.0, 5, seed=6, mode=1)
+    fov = 0.2                                            # narrow: the far corners stay inside +-2^14 voxels
+    cam = nbt.camera_from_fov(fov, fov, 6, 5)
+    ocam = oracle.camera_from_fov(fov, fov, 6, 5)
+    cam.add_corners = ocam.add_corners = 1
+    cloud = nbt.id_compute(ctx, m, poi, P, cam, 16500.0)
+    _, g, c = oracle.id_compute(om, poi, P, ocam, 16500.0, nthreads=NTHREADS)
     assert_cloud_equal(cloud, P, g, c)
+    assert c[:, 3].sum() > 0                             # the rays cross the map
 
 
 # ---------------------------------------------------------------- store layouts
 
 @pytest.mark.parametrize("bits", [2, 8])
 @pytest.mark.parametrize("layout", ["linear", "morton"])
-def test_layouts_roundtrip_update_and_id(nbt, ctx, layout, bits, monkeypatch):
+def test_layouts_roundtrip_update_and_id(nbt, ctx, layout, bits):
     """Both map store layouts (Morton cube / linear with sentinel shell) and both state
     widths (2-bit codes / one byte per voxel) give identical, oracle-exact results:
     upload/download, last-wins updates, per-ray walks, the ID."""
-    monkeypatch.setenv("NBT_MAP_LAYOUT", layout)
-    monkeypatch.setenv("NBT_MAP_BITS", str(bits))
     codes = rand_map(0, 0.3, 0.66, 0.04, seed=21, shape=(19, 27, 33))
-    m, om = make_map(nbt, ctx, codes)
+    m, om = make_map(nbt, ctx, codes, layout=layout, bits=bits)
     assert np.array_equal(m.download(), codes)
     rng = np.random.default_rng(4)
     ijk = np.stack([rng.integers(0, 33, 900), rng.integers(0, 27, 900), rng.integers(0, 19, 900)], 1).astype(np.int32)
@@ -643,7 +769,7 @@ def test_layouts_roundtrip_update_and_id(nbt, ctx, layout, bits, monkeypatch):
     codes2 = _apply_in_order(codes, ijk, vals)
     assert np.array_equal(m.download(), codes2)
     om = oracle.OracleMap(codes2)
-    o, e = random_segments_q12(1500, -8.0, 40.0, seed=31)
+    o, e = random_segments_q16(1500, -8.0, 40.0, seed=31)
     _compare_walks(nbt, ctx, m, om, o, e)
     poi = np.array([16.5, 13.5, 9.5])
     P = oracle.sample_perspectives(poi, 12.0, 24, seed=2)
@@ -651,13 +777,15 @@ def test_layouts_roundtrip_update_and_id(nbt, ctx, layout, bits, monkeypatch):
     assert_cloud_equal(cloud, P, g, c)
 
 
-def test_elongated_map_falls_back_to_linear(nbt, ctx, monkeypatch):
-    """A map whose Morton cube would be > 8x its linear store uses the linear layout."""
-    monkeypatch.setenv("NBT_MAP_LAYOUT", "morton")
+def test_elongated_map_rejects_morton(nbt, ctx):
+    """A map whose Morton cube would be > 8x its linear store: the Morton layout is refused
+    (NBT_ERR_INVALID_ARG), the linear layout walks it oracle-exactly."""
     codes = rand_map(0, 0.3, 0.7, 0.0, seed=1, shape=(3, 4, 700))
+    with pytest.raises(nbt.NbtError):
+        make_map(nbt, ctx, codes, layout="morton")
     m, om = make_map(nbt, ctx, codes)
     assert np.array_equal(m.download(), codes)
-    o, e = random_segments_q12(500, -5.0, 20.0, seed=3)
+    o, e = random_segments_q16(500, -5.0, 20.0, seed=3)
     o[:, 0] *= 30; e[:, 0] *= 30
     _compare_walks(nbt, ctx, m, om, o, e, max_visits=128)
 
@@ -823,13 +951,12 @@ def _prob_scene(shape, seed):
 
 
 @pytest.mark.parametrize("layout", ["linear", "morton"])
-def test_prob_map_id_matches_oracle(nbt, ctx, layout, monkeypatch):
+def test_prob_map_id_matches_oracle(nbt, ctx, layout):
     """8-bit store: upload_prob reproduces the oracle's states and levels, and the ID (exact
     Eq. 2 per voxel) matches the oracle bit for bit: per-state totals and g_P."""
-    monkeypatch.setenv("NBT_MAP_LAYOUT", layout)
     p, obs = _prob_scene((22, 26, 30), seed=5)
     codes, levels = oracle.quantize_prob(p, obs)
-    m = nbt.Map(ctx, nbt.map_desc(30, 26, 22, 1.0), prob=True)
+    m = nbt.Map(ctx, nbt.map_desc(30, 26, 22, 1.0, layout=layout), prob=True)
     m.upload_prob(p, obs)
     assert np.array_equal(m.download(), codes)
     assert np.array_equal(m.download_levels(), levels)
@@ -880,16 +1007,15 @@ def test_prob_map_walks(nbt, ctx):
     m = nbt.Map(ctx, nbt.map_desc(12, 12, 12, 1.0), prob=True)
     m.upload_prob(p, obs)
     om = oracle.OracleMap(codes)
-    o, e = random_segments_q12(1500, -5.0, 17.0, seed=6)
+    o, e = random_segments_q16(1500, -5.0, 17.0, seed=6)
     _compare_walks(nbt, ctx, m, om, o, e)
 
 
-def test_byte_store_config_b_subset(nbt, ctx, monkeypatch):
+def test_byte_store_config_b_subset(nbt, ctx):
     """The byte-per-voxel state store on config B's map and camera: bit-exact vs the oracle."""
-    monkeypatch.setenv("NBT_MAP_BITS", "8")
     cfg = CONFIGS["B"]
     codes = cfg.map_codes()
-    m, om = make_map(nbt, ctx, codes, voxel_size=cfg.voxel_size)
+    m, om = make_map(nbt, ctx, codes, voxel_size=cfg.voxel_size, bits=8)
     P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, 24, seed=cfg.persp_seed, mode=cfg.persp_mode)
     cloud, g, c = run_both(nbt, ctx, m, om, cfg.poi, P, cfg.width, cfg.height, cfg.range_)
     assert_cloud_equal(cloud, P, g, c)
@@ -898,13 +1024,13 @@ def test_byte_store_config_b_subset(nbt, ctx, monkeypatch):
 # ---------------------------------------------------------------- randomized configurations
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("NBT_FUZZ_SEEDS", "12"))))
-def test_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
+def test_random_configurations_fuzz(nbt, ctx, seed):
     """Random non-cubic maps (random voxel size and origin, random codes or SYN), random
     PoI and perspectives (some outside the grid), random lattice shape, corners, range,
     outside policy, gains, layout and state width: the whole ID bit-exact vs the oracle."""
     rng = np.random.default_rng(1000 + seed)
-    monkeypatch.setenv("NBT_MAP_LAYOUT", "morton" if rng.random() < 0.3 else "linear")
-    monkeypatch.setenv("NBT_MAP_BITS", "8" if rng.random() < 0.3 else "2")
+    layout = "morton" if rng.random() < 0.3 else "linear"
+    bits = 8 if rng.random() < 0.3 else 2
     nx, ny, nz = (int(v) for v in rng.integers(3, 48, 3))
     s = float(rng.choice([0.01, 0.05, 0.37, 1.0, 2.5]))
     origin = tuple(float(v) for v in rng.uniform(-20, 20, 3) * s)
@@ -917,7 +1043,10 @@ def test_random_configurations_fuzz(nbt, ctx, seed, monkeypatch):
                        constant_values=1)
     policy = int(rng.random() < 0.3)
     gain = tuple(float(v) for v in rng.uniform(0, 1, 3))
-    m, om = make_map(nbt, ctx, codes, voxel_size=s, origin=origin, gain=gain, policy=policy)
+    if layout == "morton" and max(nx, ny, nz) ** 3 > 64 * nx * ny * nz:
+        layout = "linear"                  # a Morton cube > 8x the store is refused (tested above)
+    m, om = make_map(nbt, ctx, codes, voxel_size=s, origin=origin, gain=gain, policy=policy, layout=layout,
+                     bits=bits)
     ext = np.array([nx, ny, nz], float) * s
     poi = np.array(origin) + rng.uniform(-0.1, 1.1, 3) * ext
     r_s = float(rng.uniform(0.2, 1.5) * ext.max())
@@ -970,7 +1099,7 @@ def test_large_grid_1024(nbt, ctx):
     P = np.array([[20.0, 30.0, 40.0], [1000.0, 900.0, 50.0], [512.0, 10.0, 1000.0], [-50.0, 512.0, 512.0]])
     cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 12, 9, 1500.0, corners=True)
     assert_cloud_equal(cloud, P, g, c)
-    o, e = random_segments_q12(300, -20.0, 1040.0, seed=77)
+    o, e = random_segments_q16(300, -20.0, 1040.0, seed=77)
     _compare_walks(nbt, ctx, m, om, o, e, max_visits=3200)
     del codes
 

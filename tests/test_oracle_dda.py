@@ -10,13 +10,13 @@ import pytest
 
 import oracle
 from oracle import exact
-from nbt_inputs import random_segments_q12, tie_segments_q12, rand_map
+from nbt_inputs import random_segments_q16, tie_segments_q16, rand_map
 from conftest import read_golden
 
-Q = 4096   # Q12 walk coordinates (Q19)
+Q = 65536   # Q16 walk coordinates (Q19)
 
 
-def q12(xs):
+def q16(xs):
     return [int(round(float(x) * Q)) for x in xs]
 
 
@@ -25,13 +25,13 @@ def all_state(code, n=8, policy=0, gain=(1.0, 0.12, 0.03)):
 
 
 def closed_form(o, e):
-    return 1 + sum(abs((int(e[k]) >> 12) - (int(o[k]) >> 12)) for k in range(3))
+    return 1 + sum(abs((int(e[k]) >> 16) - (int(o[k]) >> 16)) for k in range(3))
 
 
 @pytest.mark.parametrize("row", read_golden("dda_hand_traced.txt"))
 def test_hand_traced(row):
     name, o, e, seq = [s.strip() for s in row.split("|")]
-    o, e = q12(o.split()), q12(e.split())
+    o, e = q16(o.split()), q16(e.split())
     want = [tuple(int(t) for t in v.split()) for v in seq.split(";")]
     m = all_state(1, n=4)  # all Free: nothing stops the walk
     ijk, codes, r = oracle.trace_ray(m, o, e)
@@ -41,13 +41,13 @@ def test_hand_traced(row):
 
 def test_closed_form_and_connectivity_random():
     """T2/T3/T7: 1 + sum|dfloor| voxels, consecutive voxels 6-adjacent, monotone per axis."""
-    o_all, e_all = random_segments_q12(2000, -3.0, 11.0, seed=11)
+    o_all, e_all = random_segments_q16(2000, -3.0, 11.0, seed=11)
     m = all_state(1)
     for o, e in zip(o_all, e_all):
         ijk, _, r = oracle.trace_ray(m, o, e, max_visits=256)
         assert r.visits == len(ijk) == closed_form(o, e)
-        assert tuple(ijk[0]) == tuple(int(x) >> 12 for x in o)
-        assert tuple(ijk[-1]) == tuple(int(x) >> 12 for x in e)
+        assert tuple(ijk[0]) == tuple(int(x) >> 16 for x in o)
+        assert tuple(ijk[-1]) == tuple(int(x) >> 16 for x in e)
         steps = np.abs(np.diff(ijk, axis=0)).sum(1)
         assert (steps == 1).all()
         for k in range(3):
@@ -71,7 +71,7 @@ def _brute_force_check(o, e, ijk):
 
 def test_brute_force_random_segments():
     """T8: F <= visited <= touched by exact slab tests; equality without same-sign ties."""
-    o_all, e_all = random_segments_q12(300, 0.0, 8.0, seed=5)
+    o_all, e_all = random_segments_q16(300, 0.0, 8.0, seed=5)
     m = all_state(1)
     for o, e in zip(o_all, e_all):
         ijk, _, _ = oracle.trace_ray(m, o, e)
@@ -80,7 +80,7 @@ def test_brute_force_random_segments():
 
 def test_brute_force_tie_segments():
     """T8 on segments whose endpoints lie on faces, edges and corners (exact ties)."""
-    o_all, e_all = tie_segments_q12(300, 6, seed=9)
+    o_all, e_all = tie_segments_q16(300, 6, seed=9)
     m = all_state(1)
     n_ties = 0
     for o, e in zip(o_all, e_all):
@@ -94,7 +94,7 @@ def test_early_stop_counts_hit_voxel():
     """T9: if the k-th visited voxel is the first Occupied one, exactly k voxels count,
     n_O = 1, and randomizing every later voxel changes nothing."""
     rng = np.random.default_rng(3)
-    o_all, e_all = random_segments_q12(200, 0.2, 7.8, seed=21)
+    o_all, e_all = random_segments_q16(200, 0.2, 7.8, seed=21)
     for o, e in zip(o_all, e_all):
         free = all_state(1)
         ijk, _, _ = oracle.trace_ray(free, o, e)
@@ -119,14 +119,14 @@ def test_early_stop_counts_hit_voxel():
 def test_occupied_origin():
     """T10: Occupied origin voxel -> one voxel counted, g_R = g_O."""
     m = all_state(2, gain=(1.0, 0.12, 0.25))
-    _, _, r = oracle.trace_ray(m, q12([3.5, 3.5, 3.5]), q12([7.5, 1.5, 2.5]))
+    _, _, r = oracle.trace_ray(m, q16([3.5, 3.5, 3.5]), q16([7.5, 1.5, 2.5]))
     assert (r.n_u, r.n_f, r.n_o, r.stop) == (0, 0, 1, 1)
     assert r.g == 0.25
 
 
 def test_monotone_free_to_unknown():
     """T12: flipping one traversed Free voxel to Unknown raises g_R by exactly 1 - g_F."""
-    o, e = q12([0.3, 0.6, 0.9]), q12([7.7, 6.1, 5.3])
+    o, e = q16([0.3, 0.6, 0.9]), q16([7.7, 6.1, 5.3])
     base = np.ones((8, 8, 8), np.uint8)
     g0 = oracle.trace_ray(oracle.OracleMap(base, gain=(1.0, 0.25, 0.0)), o, e)[2].g
     ijk, _, _ = oracle.trace_ray(oracle.OracleMap(base), o, e)
@@ -141,7 +141,7 @@ def test_outside_policy_and_tail():
     once the walk leaves the grid it never re-enters."""
     codes = rand_map(8, seed=4)
     codes[codes == 2] = 1  # no early stop
-    o_all, e_all = random_segments_q12(300, -4.0, 12.0, seed=8)
+    o_all, e_all = random_segments_q16(300, -4.0, 12.0, seed=8)
     for o, e in zip(o_all, e_all):
         mu = oracle.OracleMap(codes, outside_policy=0)
         mc = oracle.OracleMap(codes, outside_policy=1)

@@ -164,18 +164,18 @@ def test_range_truncation_carves_only():
 
 def test_touch_set_is_exact_segment_voxel_set():
     """The voxels one ray marks are exactly {floor(P(t)) : t in [0,1]} inside the grid
-    (exact rational brute force), for endpoints on the Q12 lattice (s = 1, origin 0)."""
+    (exact rational brute force), for endpoints on the Q16 lattice (s = 1, origin 0)."""
     rng = np.random.default_rng(17)
     n = 12
     for _ in range(60):
-        o12 = rng.integers(-2 * 4096, (n + 2) * 4096, 3)
-        e12 = rng.integers(-2 * 4096, (n + 2) * 4096, 3)
+        o16 = rng.integers(-2 * 65536, (n + 2) * 65536, 3)
+        e16 = rng.integers(-2 * 65536, (n + 2) * 65536, 3)
         L = oracle.new_logodds((n, n, n))
-        touched, _ = oracle.integrate(L, 1.0, (0, 0, 0), o12 / 4096.0, [e12 / 4096.0], max_range=0.0)
-        want = {v for v in exact.floor_set(o12, e12) if all(0 <= c < n for c in v)}
+        touched, _ = oracle.integrate(L, 1.0, (0, 0, 0), o16 / 65536.0, [e16 / 65536.0], max_range=0.0)
+        want = {v for v in exact.floor_set(o16, e16) if all(0 <= c < n for c in v)}
         got = {(int(x), int(y), int(z)) for z, y, x in np.argwhere(touched > 0)}
         assert got == want
-        end = tuple(int(c) // 4096 for c in e12)
+        end = tuple(int(c) // 65536 for c in e16)
         if all(0 <= c < n for c in end):
             assert touched[end[2], end[1], end[0]] == 3
             assert int((touched == 3).sum()) == 1

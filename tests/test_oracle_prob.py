@@ -8,7 +8,7 @@ import pytest
 import oracle
 from nbt_inputs import FOV_H, FOV_V, rand_map
 
-Q = 4096
+Q = 65536   # Q16 walk coordinates (Q19)
 
 
 def one_ray_cam():

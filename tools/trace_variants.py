@@ -1,8 +1,9 @@
 """Time the trace kernel on config workloads (device-resident inputs, CUDA events around
-each k_id_trace launch).  Experiment knobs are environment variables read by libnbt (NBT_MAP_LAYOUT, NBT_REFILL_MIN,
-NBT_TRACE_CARVEOUT); --prob uses the 8-bit per-voxel-probability store (f1).
+each k_id_trace launch).  Experiment knobs: --layout linear|morton and --bits 2|8 (the map
+descriptor), --opt NAME=VALUE (ctx options, e.g. --opt TRACE_REFILL_MIN=8); --prob uses the
+8-bit per-voxel-probability store (f1); NBT_LIB=<path> loads a variant library build.
 
-    python tools/trace_variants.py B "C'" [--prob]
+    python tools/trace_variants.py B "C'" D [--prob] [--layout morton] [--bits 8] [--opt TRACE_CARVEOUT=50]
 """
 import json
 import os
@@ -18,13 +19,15 @@ import paper_2503_22588_b200 as nbt
 from nbt_inputs import CONFIGS, FOV_H, FOV_V
 
 
-def run(cfg_name, reps=5, prob=False):
+def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=()):
     cfg = CONFIGS[cfg_name]
     dev = torch.device("cuda", 0)
     s = torch.cuda.Stream(dev)
     torch.cuda.set_stream(s)
     ctx = nbt.Ctx(0, s.cuda_stream)
-    m = nbt.Map(ctx, nbt.map_desc(cfg.n, cfg.n, cfg.n, cfg.voxel_size), prob=prob)
+    for name, value in opts:
+        ctx.set_option(getattr(nbt, "OPT_" + name), value)
+    m = nbt.Map(ctx, nbt.map_desc(cfg.n, cfg.n, cfg.n, cfg.voxel_size, layout=layout, state_bits=bits), prob=prob)
     codes = cfg.map_codes()
     if prob:      # per-voxel probabilities: Free P in [0.12, 0.5), Occupied in [0.5, 0.97]
         rng = np.random.default_rng(0)
@@ -47,12 +50,21 @@ def run(cfg_name, reps=5, prob=False):
     counts = out.counts.cpu().numpy()
     lookups = float(counts[:, 3].sum())
     ms /= n
-    return {"config": cfg_name, "store": "8-bit prob" if prob else "2-bit", "trace_ms": ms,
+    return {"config": cfg_name, "store": "8-bit prob" if prob else f"{bits}-bit {layout}", "trace_ms": ms,
             "rays_per_s": cfg.rays_per_id / (ms / 1e3), "lookups_per_s": lookups / (ms / 1e3),
             "lookups": lookups, "checksum": int(counts.sum())}
 
 
 if __name__ == "__main__":
-    prob = "--prob" in sys.argv
-    for name in [a for a in sys.argv[1:] if not a.startswith("--")] or ["B"]:
-        print(json.dumps(run(name, prob=prob)), flush=True)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["B"])
+    ap.add_argument("--prob", action="store_true")
+    ap.add_argument("--layout", default="linear")
+    ap.add_argument("--bits", type=int, default=2)
+    ap.add_argument("--opt", action="append", default=[])
+    ap.add_argument("--reps", type=int, default=5)
+    a = ap.parse_args()
+    opts = [(o.split("=")[0], int(o.split("=")[1])) for o in a.opt]
+    for name in a.configs:
+        print(json.dumps(run(name, reps=a.reps, prob=a.prob, layout=a.layout, bits=a.bits, opts=opts)), flush=True)
