@@ -176,6 +176,28 @@ def all_gather_rows(local, n_total: int, world: int, strided: bool = True, group
     return unstride(out.view((world, R) + tuple(loc.shape[1:])), n_total, world)
 
 
+def gather_cloud(local_xyz, local_gain, local_counts, n_total: int, world: int, strided: bool = True,
+                 out=None, group=None):
+    """One all-gather of this rank's IG-cloud rows packed as 64-byte rows (xyz 3 x f64, g_P f64,
+    counts 4 x u64 bit-cast), un-strided on every rank.  out = (xyz, gain, counts) tensors of
+    n_total rows to fill (else new ones); returns them."""
+    import torch
+    k = local_gain.shape[0]
+    rows = torch.empty((k, 8), dtype=torch.float64, device=local_gain.device)
+    rows[:, :3] = local_xyz
+    rows[:, 3] = local_gain
+    rows[:, 4:] = local_counts.view(torch.float64)
+    full = all_gather_rows(rows, n_total, world, strided=strided, group=group)
+    if out is None:
+        out = (torch.empty((n_total, 3), dtype=torch.float64, device=rows.device),
+               torch.empty(n_total, dtype=torch.float64, device=rows.device),
+               torch.empty((n_total, 4), dtype=torch.int64, device=rows.device))
+    out[0].copy_(full[:, :3])
+    out[1].copy_(full[:, 3])
+    out[2].copy_(full[:, 4:].contiguous().view(torch.int64))
+    return out
+
+
 def id_compute_sharded(nbt, ctx, m, poi, persp_dev, cam, range_, rank: int, world: int, group=None):
     """The whole ID of `persp_dev` (n x 3 CUDA tensor, identical on every rank), sharded
     j -> rank j mod world, gathered in input order on every rank: (xyz, gain, counts)."""
@@ -190,10 +212,7 @@ def id_compute_sharded(nbt, ctx, m, poi, persp_dev, cam, range_, rank: int, worl
         nbt.id_compute(ctx, m, poi, persp_dev, cam, range_, out=local, first=rank, stride=world)
     if world == 1:
         return local.xyz, local.gain, local.counts
-    xyz = all_gather_rows(local.xyz, n, world, group=group)
-    gain = all_gather_rows(local.gain, n, world, group=group)
-    counts = all_gather_rows(local.counts, n, world, group=group)
-    return xyz.contiguous(), gain.contiguous(), counts.contiguous()
+    return gather_cloud(local.xyz, local.gain, local.counts, n, world, group=group)
 
 
 def id_compute_ray_split(nbt, ctx, m, poi, persp_dev, cam, range_, rank: int, world: int, group=None):
