@@ -1,28 +1,36 @@
 #!/usr/bin/env python
 """bench.py -- throughput of the online local Information Distribution on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config B]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config D]
 
-One STEP is one pass of the whole hot path for one MHP cycle
-on one batch of synthetic input (config B of BASELINE.json: 256^3 SYN map, 1 cm voxels,
-512 perspectives x 64x48 rays, range 1.5 m):
+One STEP is one pass of the whole hot path for one MHP cycle on
+one batch of synthetic input.  The headline workload is config D of BASELINE.json
+(configs[3], the config the metric's "1/2/4/8 GPU" refers to): a 512^3 SYN map (2-bit
+packed, 1 cm voxels), 4096 perspectives x 160x120 rays, range 3.86 m:
   a2  apply this cycle's map deltas (nbt_map_update; broadcast from rank 0 when N > 1)
-  a3  sample the perspective set by Eq. 1 on the device
-  a4-a8  nbt_id_compute -> IG point cloud (frames, rays, exact DDA, scores, means)
-       (N > 1: all-gather of the cloud rows over NCCL)
-  a9  push the cloud into the N_B = 10 ring buffer and run 1984 IDW queries (Eq. 4)
-       (N > 1: each rank answers a contiguous slice of the queries; all-gather of the values)
-Map construction/upload is excluded.  Weak scaling: every rank computes its own
-512-perspective ID per step; `value` = rays of all ranks / max-over-ranks device time.
-Rank 0 prints one JSON line.  The L2 (126 MB) is flushed with a 256 MiB write before
-every timed step.  `--impl reference` times the CPU oracle (the only "reference" this
-paper-only build has) on the same workload, a bounded sample per step.
+  a3  sample the 4096 perspectives by Eq. 1 on the device (same seed on every rank)
+  a4-a8  the ID: perspective j on rank j mod N (nbt_id_compute_slice) -> IG point cloud
+       rows; N > 1: one all-gather of the 64-byte rows over NCCL (or fused into the
+       finalize over peer memory, --gather p2p)
+  a9  push the whole cloud into the N_B = 10 ring buffer and answer 1984 IDW queries
+       (Eq. 4); N > 1: each rank answers a contiguous slice, all-gather of the values
+Map construction/upload is excluded.  Strong scaling: the work per step is fixed;
+`value` = rays of the step x K / max-over-ranks device time.  Rank 0 prints one JSON line.
+The L2 (126 MB) is flushed with a 256 MiB write before every timed step.  Beside the
+headline: `north_star` (config C', 512 x 640x480 rays on the 256^3 map: the per-MHP-cycle
+latency, >= 20 repetitions with its own roofline, clocks and e2e), `config_b` (config B,
+weak scaling, the round-1 headline), `map_integration` (row f3), `cpu_baseline` (the
+oracle on the host cores, all threads and one thread).  `--impl reference` times the CPU
+oracle (the only "reference" this paper-only build has) on the same workload, a bounded
+sample per step.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -40,23 +48,23 @@ N_QUERIES = 1984          # 64 trajectories x (K + 1 = 31) poses, K = 30
 N_B = 10                  # ID buffering
 POWER_P = 2.0             # IDW power
 N_DELTA_SETS = 8
-OPS_PER_LOOKUP = 13       # algorithmic int32 ops per in-grid voxel step
-INT_LANES_PER_SM_CLK = 128
+OPS_PER_LOOKUP = 12       # algorithmic int32 ops per in-grid voxel step
+PEAKS_FILE = os.path.join(ROOT, "profiles", "r02_peaks.json")   # tools/peaks.cu on this pool's B200
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="B")
+    ap.add_argument("--config", default="D", help="headline workload (D: strong scaling; A/B/C/C': weak)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-north-star", action="store_true")
+    ap.add_argument("--north-star-reps", type=int, default=20)
+    ap.add_argument("--no-config-b", action="store_true")
     ap.add_argument("--no-integrate", action="store_true", help="skip the row-f3 map-integration block")
-    ap.add_argument("--no-config-d", action="store_true", help="skip the config-D strong-scaling block")
-    ap.add_argument("--unprofiled-graphs", action="store_true", help="experiment: graphs without event nodes")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--gather", choices=["nccl", "p2p"], default="nccl",
@@ -65,18 +73,58 @@ def parse():
 
 
 def peaks():
+    """(int32 issue peak ops/s, L2 read peak GB/s, HBM GB/s, basis): the measured numbers of
+    tools/peaks.cu (profiles/r02_peaks.json) and MEASURED_PEAKS.json; fallback: 148 SMs x
+    128 lanes x 1965 MHz and the profiling guide's HBM figure."""
+    out = {"int32_ops_per_s": 148 * 128 * 1.965e9, "l2_gbs": None, "hbm_gbs": 6650.0, "basis": "fallback"}
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        out.update(int32_ops_per_s=float(p["int32_peak_ops_per_s"]), l2_gbs=float(p["l2_read_peak_gbs"]),
+                   basis=f"measured (profiles/r02_peaks.json: best integer mix {p['int32_peak_lanes_per_clk_per_sm']}"
+                         f" lanes/clk/SM at {p['sm_mhz_measured']} MHz)")
+    except (OSError, KeyError, ValueError):
+        pass
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f), "measured"
-    except OSError:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+            out["hbm_gbs"] = float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        pass
+    return out
 
 
-def workload_name(cfg, world):
-    return (f"{cfg.name}: {cfg.n}^3 SYN map (s_Vox={cfg.voxel_size} m, R_o={cfg.r_o:g} vox), "
-            f"{cfg.n_persp} perspectives/rank ({'ball' if cfg.persp_mode == 0 else 'surface'} r_S={cfg.persp_radius} m) "
-            f"x {cfg.width}x{cfg.height} rays, range {cfg.range_} m; + map deltas, + {N_QUERIES} IDW queries "
-            f"over N_B={N_B}")
+def ncu_traffic(cfg_name):
+    """Per-launch DRAM and L2 bytes of k_id_trace from one ncu --set full capture (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg_name}.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def host_cpu():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return platform.processor() or "unknown"
+
+
+def workload_name(cfg, world, mode):
+    per = "/rank" if mode == "weak" else ""
+    shard = (f", perspective j on rank j mod {world}" if mode == "strong" else "")
+    return (f"{cfg.name}: {cfg.n}^3 SYN map (s_Vox={cfg.voxel_size} m, R_o={cfg.r_o:g} vox, 2-bit packed), "
+            f"{cfg.n_persp} perspectives{per} ({'ball' if cfg.persp_mode == 0 else 'surface'} r_S={cfg.persp_radius}"
+            f" m) x {cfg.width}x{cfg.height} rays, range {cfg.range_} m{shard}; + map deltas, + {N_QUERIES} IDW "
+            f"queries over N_B={N_B}")
+
+
+def digest64(a):
+    """64-bit BLAKE2b digest of an array's bytes (bit-exact checksum of the IG cloud across N)."""
+    return hashlib.blake2b(np.ascontiguousarray(a).tobytes(), digest_size=8).hexdigest()
 
 
 # ----------------------------------------------------------------- clocks
@@ -166,12 +214,15 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU oracle leg
 
-def cpu_oracle_sample(cfg, codes, budget_s, steps=1):
-    """Time the oracle (all host cores) on a bounded, strided sample of the workload's
-    perspectives; returns rays/s, voxel-steps/s and a description."""
+
+
+# ------------------------------------------------------------ CPU oracle leg
+
+def oracle_sample(cfg, codes, budget_s, nthreads, steps=1):
+    """A bounded, strided sample of the workload's perspectives sized so that `steps` runs of
+    the oracle on `nthreads` host threads take about budget_s seconds in total."""
     import oracle
     oracle.build()
-    nthreads = os.cpu_count() or 1
     om = oracle.OracleMap(codes, voxel_size=cfg.voxel_size)
     cam = oracle.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
     ne = oracle.num_rays(cam)
@@ -179,18 +230,16 @@ def cpu_oracle_sample(cfg, codes, budget_s, steps=1):
     k = max(1, min(nthreads, cfg.n_persp))
     t = time.perf_counter()
     oracle.id_compute(om, cfg.poi, persp[:: max(1, cfg.n_persp // k)][:k], cam, cfg.range_, nthreads=nthreads)
-    t_probe = time.perf_counter() - t
-    per_persp = t_probe / k
+    per_persp = (time.perf_counter() - t) / k
     n = int(max(1, min(cfg.n_persp, budget_s / max(per_persp, 1e-9) / steps)))
     sel = persp[:: max(1, cfg.n_persp // n)][:n]
-    return om, cam, ne, sel, nthreads
+    return om, cam, ne, sel
 
 
-def run_cpu_baseline(cfg, codes, budget_s):
+def time_oracle(cfg, om, cam, ne, sel, nthreads, min_s):
     import oracle
-    om, cam, ne, sel, nthreads = cpu_oracle_sample(cfg, codes, budget_s)
     reps, dt, visits, lookups = 0, 0.0, 0.0, 0.0
-    while dt < min(3.0, budget_s) or reps == 0:      # repeat a short sample for a stable rate
+    while dt < min_s or reps == 0:      # repeat a short sample for a stable rate
         t = time.perf_counter()
         _, _, c = oracle.id_compute(om, cfg.poi, sel, cam, cfg.range_, nthreads=nthreads)
         dt += time.perf_counter() - t
@@ -198,23 +247,41 @@ def run_cpu_baseline(cfg, codes, budget_s):
         visits += float(c[:, :3].sum())
         lookups += float(c[:, 3].sum())
     rays = reps * len(sel) * ne
-    return {"value": rays / dt, "unit": "rays/s", "cores": nthreads, "kind": "oracle",
+    return rays / dt, visits / dt, lookups / dt, reps, dt
+
+
+def run_cpu_baseline(cfg, codes, budget_s):
+    """The oracle as it stands on the box's host cores: OpenMP over perspectives on every
+    hardware thread, and on ONE thread (the paper's sequential CPU implementation)."""
+    nthreads = os.cpu_count() or 1
+    om, cam, ne, sel = oracle_sample(cfg, codes, 0.6 * budget_s, nthreads)
+    v, vs, lk, reps, dt = time_oracle(cfg, om, cam, ne, sel, nthreads, min(3.0, 0.6 * budget_s))
+    om1, cam1, ne1, sel1 = oracle_sample(cfg, codes, 0.3 * budget_s, 1)
+    v1, vs1, lk1, reps1, dt1 = time_oracle(cfg, om1, cam1, ne1, sel1, 1, 0.3 * budget_s)
+    return {"value": v, "unit": "rays/s", "cores": nthreads, "kind": "oracle",
             "sample": f"{len(sel)} of {cfg.n_persp} perspectives (strided) of config {cfg.name}, all {ne} rays "
                       f"each, x{reps} repetitions, OpenMP over perspectives on {nthreads} host threads, "
                       f"{dt:.2f} s of CPU work",
-            "voxel_steps_per_s": visits / dt, "lookups_per_s": lookups / dt}
+            "voxel_steps_per_s": vs, "lookups_per_s": lk, "host_cpu": host_cpu(),
+            "single_thread": {"value": v1, "unit": "rays/s", "cores": 1, "voxel_steps_per_s": vs1,
+                              "lookups_per_s": lk1,
+                              "sample": f"{len(sel1)} strided perspectives x {ne1} rays, x{reps1}, {dt1:.2f} s"},
+            "paper": "P:330: s_G = 5, N_P = 1000 (~11.8 M rays) in 144.93 s on an Intel i5-12600KF, one thread "
+                     "(~81 k rays/s, BASELINE.md derived); GPU ~75% lower on an RTX 3060 (P:333)"}
 
 
 def reference_arm(args, cfg):
-    """--impl reference: the CPU oracle as it stands, on the same metric/config."""
+    """--impl reference: the CPU oracle as it stands, on the same metric/config, a bounded
+    strided sample of the perspectives per step (rank 0 only; other ranks exit 0)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import oracle
     codes = cfg.map_codes()
+    nthreads = os.cpu_count() or 1
     budget = 150.0 / max(1, args.steps + args.warmup)
-    om, cam, ne, sel, nthreads = cpu_oracle_sample(cfg, codes, budget * (args.steps + args.warmup),
-                                                   steps=args.steps + args.warmup)
+    om, cam, ne, sel = oracle_sample(cfg, codes, budget * (args.steps + args.warmup), nthreads,
+                                     steps=args.steps + args.warmup)
     deltas = [cycle_deltas(cfg.n, (cfg.n // 2,) * 3, c, codes, seed=1) for c in range(N_DELTA_SETS)]
     q = query_points(N_QUERIES, cfg.poi, cfg.persp_radius, 0.5, 1.2, seed=5)
     entries = []
@@ -232,20 +299,22 @@ def reference_arm(args, cfg):
             rays += len(sel) * ne
     total = sum(times)
     value = rays / total
+    mode = "strong" if cfg.name == "D" else "weak"
     line = {"metric": "rays/s", "value": value, "unit": "rays/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic", "config": {"workload": workload_name(cfg, 1),
+            "higher_is_better": True, "scaling": mode, "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": {"workload": workload_name(cfg, 1, mode),
                                             "sample_per_step": f"{len(sel)} of {cfg.n_persp} perspectives"},
             "cpu_baseline": {"value": value, "unit": "rays/s", "cores": nthreads, "kind": "oracle",
                              "sample": f"{len(sel)} strided perspectives of config {cfg.name} per step, all {ne} "
-                                       f"rays each; deltas + ID + {N_QUERIES} IDW queries; {nthreads} threads"},
+                                       f"rays each; deltas + ID + {N_QUERIES} IDW queries; {nthreads} threads",
+                             "host_cpu": host_cpu()},
             "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-# -------------------------------------------------------------- our arm
+# ------------------------------------------------------------ map integration (f3)
 
 def run_integration(nbt, ctx, stream, dev, flush, reps=2):
     """Row f3 on config F: Azure-Kinect-size depth frames (640 x 576, ~365 k
@@ -313,78 +382,22 @@ def run_integration(nbt, ctx, stream, dev, flush, reps=2):
     return out
 
 
-def run_config_d(nbt, ndist, ctx, stream, dev, rank, world, reps=3, gather="nccl"):
-    """Config D (512^3 SYN map, 4096 perspectives x 160x120 rays, range 3.86 m): the whole ID
-    sharded j -> rank j mod G and all-gathered in input order on every rank; device time per
-    ID (CUDA events on the shared stream), max over ranks."""
+
+
+# -------------------------------------------------------------- our arm
+
+def run_cycle(args, nbt, ndist, ctx, stream, dev, rank, world, cfg, mode, steps, warmup, flush, pk,
+              want_e2e=True, want_shares=True):
+    """K timed MHP cycles of the whole hot path (rows a2-a9) on `cfg`, sharded over the ranks:
+    mode "strong" -- one perspective set per step (same seed on every rank), perspective j on
+    rank j mod N, the IG cloud all-gathered; "weak" -- every rank its own perspective set,
+    the clouds all-gathered.  Device time per step with CUDA events on the shared stream, max
+    over ranks.  Returns the numbers of the JSON line (rank 0) or None."""
     import torch
     import torch.distributed as dist
-    cd = CONFIGS["D"]
-    m = nbt.Map(ctx, nbt.map_desc(cd.n, cd.n, cd.n, cd.voxel_size))
-    if rank == 0:
-        m.upload(cd.map_codes())
-    if world > 1:
-        ndist.replicate_map(m, src=0)
-    ctx.sync()
-    cam = nbt.camera_from_fov(FOV_H, FOV_V, cd.width, cd.height)
-    persp = torch.empty((cd.n_persp, 3), dtype=torch.float64, device=dev)
-    nbt.sample_perspectives(ctx, cd.poi, cd.persp_radius, cd.n_persp, cd.persp_seed, cd.persp_mode, out=persp)
-    if world > 1 and gather == "p2p":
-        pg = ndist.PeerGather(nbt, ctx, cd.n_persp, rank, world)
-
-        def whole_id():
-            return pg.id_compute(m, cd.poi, persp, cam, cd.range_)
-    else:
-        def whole_id():
-            return ndist.id_compute_sharded(nbt, ctx, m, cd.poi, persp, cam, cd.range_, rank, world)
-    whole_id()                                                                            # warm-up
-    times = []
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(reps):
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        xyz, gain, counts = whole_id()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
-    ms = statistics.median(times)
-    lookups = float(counts[:, 3].sum().item())
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    if world > 1 and gather == "p2p":
-        pg.close()
-    m.close()
-    return {"config": f"D: {cd.n}^3 SYN map (2-bit), {cd.n_persp} perspectives x {cd.width}x{cd.height} rays, "
-                      f"range {cd.range_} m, sharded j -> rank j mod {world}, all-gathered",
-            "n_gpus": world, "id_ms": ms, "rays_per_s": cd.rays_per_id / (ms / 1e3),
-            "lookups_per_s": lookups / (ms / 1e3), "reps": reps, "scaling": "strong",
-            "gather": "fused into the finalize (peer memory)" if world > 1 and gather == "p2p" else "NCCL"}
-
-
-def main_ours(args, cfg):
-    import torch
-    import torch.distributed as dist
-
-    import paper_2503_22588_b200 as nbt
-    from paper_2503_22588_b200 import dist as ndist
-
-    rank, world, local = ndist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    # one dedicated stream shared by libnbt, torch's events and NCCL (the legacy default
-    # stream handle 0 would make libnbt create its own stream)
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
-    ctx = nbt.Ctx(local, stream.cuda_stream)
-    pk, pk_kind = peaks()
 
     # ---- map: built and uploaded on rank 0, replicated by NCCL broadcast (excluded from timing, S:188)
-    desc = nbt.map_desc(cfg.n, cfg.n, cfg.n, cfg.voxel_size)
-    m = nbt.Map(ctx, desc)
+    m = nbt.Map(ctx, nbt.map_desc(cfg.n, cfg.n, cfg.n, cfg.voxel_size))
     codes = cfg.map_codes() if rank == 0 else None
     if rank == 0:
         m.upload(codes)
@@ -392,9 +405,8 @@ def main_ours(args, cfg):
         ndist.replicate_map(m, src=0)
     ctx.sync()
 
-    # ---- per-cycle inputs, resident in HBM before timing.  The map deltas come from the
-    #      sensor rank (0); the other ranks hold same-shape buffers that every cycle's
-    #      broadcast overwrites.
+    # ---- per-cycle inputs, resident in HBM before timing.  The map deltas come from the sensor
+    #      rank (0); the other ranks hold same-shape buffers that every cycle's broadcast overwrites.
     nd = 0
     host_deltas = []
     if rank == 0:
@@ -418,44 +430,50 @@ def main_ours(args, cfg):
     q_host = query_points(N_QUERIES, cfg.poi, cfg.persp_radius, 0.5, 1.2, seed=5)
     q_dev = torch.from_numpy(q_host).to(dev)
     q_out = torch.empty(N_QUERIES, dtype=torch.float64, device=dev)
-    # the IDW queries are sharded too (contiguous slices, gathered after the query), so the
-    # per-rank IDW work stays constant while the assembled cloud grows with the world size
+    # the IDW queries are sharded too (contiguous slices, gathered after the query)
     q_rows = (N_QUERIES + world - 1) // world
     q_lo = min(N_QUERIES, rank * q_rows)
     q_hi = min(N_QUERIES, q_lo + q_rows)
     q_mine = q_dev[q_lo:q_hi]
     q_out_mine = torch.zeros(q_rows, dtype=torch.float64, device=dev)
-    n_p = cfg.n_persp
-    n_tot = n_p * world
-    persp = torch.empty((n_p, 3), dtype=torch.float64, device=dev)
-    cloud = nbt.empty_cloud(n_p, device=dev)
+
+    strong = mode == "strong"
+    n_src = cfg.n_persp                                  # perspectives sampled per rank and step
+    n_tot = n_src if strong else n_src * world           # rows of the assembled cloud
+    n_mine = ndist.shard_count(n_src, rank, world) if strong else n_src
+    first, stride = (rank, world) if strong else (0, 1)
+    persp = torch.empty((n_src, 3), dtype=torch.float64, device=dev)
     buf = nbt.IdBuffer(ctx, N_B, n_tot)
     cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
     ne = cam.num_rays
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     acc = torch.zeros(4, dtype=torch.int64, device=dev)
 
-    gathered = (nbt.IgCloud(torch.empty((n_tot, 3), dtype=torch.float64, device=dev),
-                            torch.empty(n_tot, dtype=torch.float64, device=dev), None) if world > 1 else cloud)
-    p2p = world > 1 and args.gather == "p2p"
-    if p2p:
+    gathered = nbt.empty_cloud(n_tot, device=dev)
+    local = gathered if world == 1 else nbt.empty_cloud(n_mine, device=dev)
+    p2p = None
+    if world > 1 and args.gather == "p2p":
         # the all-gather fused into the finalize: every rank stores its rows into all ranks'
         # buffers over peer memory; one buffer suffices because the query all-gather of the
         # previous step orders every rank's ID-buffer push before the next step's stores
-        pgather = ndist.PeerGather(nbt, ctx, n_tot, rank, world, n_buffers=1)
-        gc = pgather.bufs[0].cloud()
-        gathered = nbt.IgCloud(gc.xyz, gc.gain, None)
-        cloud = nbt.IgCloud(gc.xyz[rank * n_p:(rank + 1) * n_p], gc.gain[rank * n_p:(rank + 1) * n_p],
-                            gc.counts[rank * n_p:(rank + 1) * n_p])
+        p2p = ndist.make_peer_gather(nbt, ctx, n_tot, rank, world, n_buffers=1)
+        if p2p is not None:
+            gc = p2p.bufs[0].cloud()
+            gathered = nbt.IgCloud(gc.xyz, gc.gain, gc.counts)
+            local = nbt.IgCloud(None, None, gc.counts[rank::world] if strong
+                                else gc.counts[rank * n_src:(rank + 1) * n_src])
+
+    def seed_of(c):
+        return cfg.persp_seed + 1000003 * c + (0 if strong else 7919 * rank)
 
     def part_a(c):                      # rows a2-a8 on this rank
         m.update(d_ijk[c], d_val[c])                                             # a2
-        nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_p, 1000003 * c + rank, cfg.persp_mode,
+        nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_src, seed_of(c), cfg.persp_mode,
                                 out=persp)                                       # a3
-        if p2p:                                                                  # a4-a8 + the gather
-            pgather.bufs[0].compute(m, cfg.poi, persp, cam, cfg.range_, first=0, stride=1, row0=rank * n_p)
-        else:
-            nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=cloud)   # a4-a8
+        if p2p is not None:                                                      # a4-a8 + the gather
+            p2p.bufs[0].compute(m, cfg.poi, persp, cam, cfg.range_, first=first, stride=stride,
+                                row0=0 if strong else rank * n_src)
+        elif n_mine:
+            nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=local, first=first, stride=stride)
 
     def part_b():                       # row a9 on the assembled cloud
         buf.push(gathered, n_tot)
@@ -473,11 +491,11 @@ def main_ours(args, cfg):
             ndist.broadcast_deltas(d_ijk[c], d_val[c], src=0)
 
     def exchange_cloud():
-        if p2p:
-            pgather.order_readers()     # every rank's peer stores before any rank's push
+        if p2p is not None:
+            p2p.order_readers()         # every rank's peer stores before any rank's push
         elif world > 1:
-            gathered.xyz.copy_(ndist.all_gather_rows(cloud.xyz, n_tot, world, strided=False))
-            gathered.gain.copy_(ndist.all_gather_rows(cloud.gain, n_tot, world, strided=False))
+            ndist.gather_cloud(local.xyz, local.gain, local.counts, n_tot, world, strided=strong,
+                               out=(gathered.xyz, gathered.gain, gathered.counts))
 
     def step_eager(t):
         c = t % N_DELTA_SETS
@@ -487,14 +505,14 @@ def main_ours(args, cfg):
         part_b()
         exchange_queries()
 
-    for t in range(args.warmup):
+    for t in range(warmup):
         step_eager(t)
     ctx.sync()
 
-    # ---- CUDA graphs: one per delta set for rows a2-a8 and one for a9 (the NCCL exchanges
-    #      stay eager between them).  Every profiled kernel family adds two event nodes to a
-    #      graph (~2 us each), so the timed graphs record only k_id_trace (the roofline
-    #      kernel); the per-kernel shares come from a separate fully profiled run afterwards.
+    # ---- CUDA graphs: one per delta set for rows a2-a8 and one for a9 (the NCCL exchanges stay
+    #      eager between them).  Every profiled kernel family adds two event nodes to a graph
+    #      (~2 us each), so the timed graphs record only k_id_trace (the roofline kernel); the
+    #      per-kernel shares come from a separate fully profiled run afterwards.
     def capture(kernels):
         ctx.set_profiling_mask(kernels)
         ga = []
@@ -509,7 +527,7 @@ def main_ours(args, cfg):
     families = list(range(nbt.KERNEL_MAP_UPDATE + 1))
     graphs_a, graph_b = [], None
     if not args.no_graph:
-        graphs_a, graph_b = capture([] if args.unprofiled_graphs else [nbt.KERNEL_TRACE])
+        graphs_a, graph_b = capture([nbt.KERNEL_TRACE])
     else:
         ctx.set_profiling_mask(families)
 
@@ -527,277 +545,435 @@ def main_ours(args, cfg):
     gpu_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid).replace("GPU-", "")
     clocks = ClockSampler(gpu_id)
     time.sleep(0.25)
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    for k in range(nbt.KERNEL_MAP_UPDATE + 1):
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for k in families:
         ctx.profile_read(k, reset=True)
-    graph_prof = {k: [0.0, 0] for k in range(nbt.KERNEL_MAP_UPDATE + 1)}
+    graph_prof = {k: [0.0, 0] for k in families}
     launches0 = ctx.launches
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t_wall0 = time.time()
-    for i in range(args.steps):
+    for i in range(steps):
         flush.fill_(i & 0xFF)                      # evict the map and inputs from L2 (outside the events)
         ev0[i].record(stream)
-        step(args.warmup + i)
+        step(warmup + i)
         ev1[i].record(stream)
         if not args.no_graph:                      # kernel times of this replay (event nodes)
             for k in graph_prof:
-                for g in (graphs_a[(args.warmup + i) % N_DELTA_SETS], graph_b):
+                for g in (graphs_a[(warmup + i) % N_DELTA_SETS], graph_b):
                     ms_k, n_k = g.profile_read(k)
                     graph_prof[k][0] += ms_k
                     graph_prof[k][1] += n_k
-        acc += cloud.counts.sum(0)                 # work accounting, outside the events
+        acc += local.counts.sum(0)                 # work accounting, outside the events
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t_wall1 = time.time()
     launches = ctx.launches - launches0
     dev_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
-    prof = {k: ctx.profile_read(k, reset=True) for k in range(nbt.KERNEL_MAP_UPDATE + 1)}
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    prof = {k: ctx.profile_read(k, reset=True) for k in families}
     if not args.no_graph:
         prof = {k: (v[0], v[1]) for k, v in graph_prof.items()}
     clocks.stop()
     clk = clocks.summary(t_wall0, t_wall1)
+    # checksum of the last step's assembled cloud (identical on every rank and for every N)
+    last_gain = gathered.gain.cpu().numpy().copy()
+    last_counts = gathered.counts.cpu().numpy().copy() if gathered.counts is not None else None
 
     # ---- per-kernel shares of the step from a separate, fully profiled run (not timed)
     share_prof, share_ms = prof, dev_ms
-    if not args.no_graph:
+    if want_shares and not args.no_graph:
         pa, pb = capture(families)
-        n_sh = min(args.steps, 50)
+        n_sh = min(steps, 20)
         share_prof = {k: [0.0, 0] for k in families}
         share_ms = 0.0
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         for i in range(n_sh):
             flush.fill_(i & 0xFF)
             e0.record(stream)
-            step(args.warmup + args.steps + i, pa, pb)
+            step(warmup + steps + i, pa, pb)
             e1.record(stream)
             torch.cuda.synchronize()
             share_ms += e0.elapsed_time(e1)
             for k in families:
-                for g in (pa[(args.warmup + args.steps + i) % N_DELTA_SETS], pb):
+                for g in (pa[(warmup + steps + i) % N_DELTA_SETS], pb):
                     ms_k, n_k = g.profile_read(k)
                     share_prof[k][0] += ms_k
                     share_prof[k][1] += n_k
         for g in pa + [pb]:
             g.close()
     ctx.set_profiling(False)
+    for g in graphs_a + ([graph_b] if graph_b else []):
+        g.close()
     counts = acc.cpu().numpy()
-    visits, lookups = float(counts[:3].sum()), float(counts[3])
-
-    # ---- north-star workload (config C': 512 perspectives x 640x480 rays on the same 256^3
-    #      map) -- the whole hot path, device time per MHP cycle, after the timed region
-    north = None
-    if cfg.name == "B" and not args.no_north_star:
-        cn = CONFIGS["C'"]
-        cam_n = nbt.camera_from_fov(FOV_H, FOV_V, cn.width, cn.height)
-        persp_n = torch.empty((cn.n_persp, 3), dtype=torch.float64, device=dev)
-        cloud_n = nbt.empty_cloud(cn.n_persp, device=dev)
-        buf_n = nbt.IdBuffer(ctx, N_B, cn.n_persp)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        times = []
-        for t in range(4):
-            flush.fill_(t & 0xFF)
-            e0.record(stream)
-            nbt.sample_perspectives(ctx, cn.poi, cn.persp_radius, cn.n_persp, cn.persp_seed + t, cn.persp_mode,
-                                    out=persp_n)
-            nbt.id_compute(ctx, m, cn.poi, persp_n, cam_n, cn.range_, out=cloud_n)
-            buf_n.push(cloud_n, cn.n_persp)
-            buf_n.query(q_dev, power_p=POWER_P, out=q_out)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            if t > 0:
-                times.append(e0.elapsed_time(e1))
-        ms = sum(times) / len(times)
-        north = {"config": "C': 256^3 map, 512 perspectives x 640x480 rays, range 1.5 m (north_star target)",
-                 "id_latency_ms": ms, "rays_per_s": cn.rays_per_id / (ms / 1e3), "target_ms": 100.0,
-                 "steps": len(times)}
-
-    # ---- BASELINE configs[3] / SURVEY 8(d) config D: one 4096-perspective ID on the 512^3 map,
-    #      sharded across the ranks (strong scaling: strided slices + NCCL all-gather of the cloud)
-    strong = None
-    if cfg.name == "B" and not args.no_config_d:
-        strong = run_config_d(nbt, ndist, ctx, stream, dev, rank, world, gather=args.gather)
-
-    # ---- row f3: map integration of depth frames (the step before the path)
-    integ = None
-    if cfg.name == "B" and not args.no_integrate and rank == 0:
-        integ = run_integration(nbt, ctx, stream, dev, flush)
+    visits_r, lookups_r = float(counts[:3].sum()), float(counts[3])
 
     # ---- end to end through the public API with HOST buffers (H2D inputs, D2H results)
     e2e = None
-    if not args.no_e2e:
-        # inputs in pinned host memory; every step copies them in (H2D), runs the public
-        # calls on the device copies, and reads the IDW values and the IG cloud back (D2H)
-        # with one synchronisation at the end of the step
-        e2e_persp = [torch.from_numpy(nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_p,
-                                                              77 + 1000003 * s + rank, cfg.persp_mode)).pin_memory()
-                     for s in range(min(args.steps, 16))]
-        h_ijk = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a, _ in host_deltas]
-        h_val = [torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for _, v in host_deltas]
-        h_q = torch.from_numpy(np.ascontiguousarray(q_host[q_lo:q_hi] if world > 1 else q_host)).pin_memory()
-        e_ijk = torch.empty_like(h_ijk[0], device=dev)
-        e_val = torch.empty_like(h_val[0], device=dev)
-        e_persp = torch.empty((n_p, 3), dtype=torch.float64, device=dev)
-        e_q = torch.empty_like(h_q, device=dev)
-        r_q = torch.empty(N_QUERIES, dtype=torch.float64).pin_memory()
-        r_gain = torch.empty(n_tot, dtype=torch.float64).pin_memory()
-        r_xyz = torch.empty((n_tot, 3), dtype=torch.float64).pin_memory()
-        loc = nbt.empty_cloud(n_p, device=dev, counts=False)
-
-        def e2e_step(s):
-            c = s % N_DELTA_SETS
-            e_ijk.copy_(h_ijk[c], non_blocking=True)                             # H2D deltas
-            e_val.copy_(h_val[c], non_blocking=True)
-            e_persp.copy_(e2e_persp[s % len(e2e_persp)], non_blocking=True)     # H2D perspectives
-            e_q.copy_(h_q, non_blocking=True)                                    # H2D queries
-            if world > 1:
-                ndist.broadcast_deltas(e_ijk, e_val, src=0)
-            m.update(e_ijk, e_val)
-            nbt.id_compute(ctx, m, cfg.poi, e_persp, cam, cfg.range_, out=loc)
-            if world > 1:
-                full = nbt.IgCloud(ndist.all_gather_rows(loc.xyz, n_tot, world, strided=False),
-                                   ndist.all_gather_rows(loc.gain, n_tot, world, strided=False), None)
-            else:
-                full = loc
-            buf.push(full, n_tot)
-            if world == 1:
-                buf.query(e_q, power_p=POWER_P, out=q_out)
-            else:
-                if q_hi > q_lo:
-                    buf.query(e_q, power_p=POWER_P, out=q_out_mine[:q_hi - q_lo])
-                q_out.copy_(ndist.all_gather_rows(q_out_mine, N_QUERIES, world, strided=False))
-            r_q.copy_(q_out, non_blocking=True)                                  # D2H IDW values
-            r_gain.copy_(full.gain, non_blocking=True)                           # D2H the IG cloud
-            r_xyz.copy_(full.xyz, non_blocking=True)
-            stream.synchronize()
-            return r_gain, r_xyz
-
-        e2e_mode = "eager API calls, one synchronisation per step"
-        if world == 1 and not args.no_graph:
-            # the same public calls captured once (nbt_ctx_capture_begin/end) with the copies:
-            # per step the host writes the step's inputs into pinned staging, replays the
-            # graph (H2D, update, ID, push, IDW, D2H) and waits for the results
-            s_ijk, s_val = h_ijk[0].clone().pin_memory(), h_val[0].clone().pin_memory()
-            s_persp = e2e_persp[0].clone().pin_memory()
-            h_ijk_live, h_val_live, persp_live = h_ijk, h_val, e2e_persp
-            h_ijk, h_val = [s_ijk] * len(h_ijk_live), [s_val] * len(h_val_live)
-            e2e_persp = [s_persp]
-            e2e_step(0)                                # warm-up outside the capture
-            ctx.capture_begin()
-            e_ijk.copy_(s_ijk, non_blocking=True)
-            e_val.copy_(s_val, non_blocking=True)
-            e_persp.copy_(s_persp, non_blocking=True)
-            e_q.copy_(h_q, non_blocking=True)
-            m.update(e_ijk, e_val)
-            nbt.id_compute(ctx, m, cfg.poi, e_persp, cam, cfg.range_, out=loc)
-            buf.push(loc, n_tot)
-            buf.query(e_q, power_p=POWER_P, out=q_out)
-            r_q.copy_(q_out, non_blocking=True)
-            r_gain.copy_(loc.gain, non_blocking=True)
-            r_xyz.copy_(loc.xyz, non_blocking=True)
-            e2e_graph = ctx.capture_end()
-
-            def e2e_step(s):
-                s_ijk.copy_(h_ijk_live[s % N_DELTA_SETS])                      # host staging of the inputs
-                s_val.copy_(h_val_live[s % N_DELTA_SETS])
-                s_persp.copy_(persp_live[s % len(persp_live)])
-                e2e_graph.launch()
-                stream.synchronize()
-                return r_gain, r_xyz
-            e2e_mode = "one CUDA-graph replay of the public calls and the copies per step, one synchronisation"
-
-        for s in range(2):
-            e2e_step(s)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for s in range(args.steps):
-            e2e_step(s)
-        torch.cuda.synchronize()
-        t_e2e = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_e2e = float(tt.item())
-        h2d = nd * 13 + n_p * 24 + (q_hi - q_lo) * 24          # this rank's copies
-        d2h = N_QUERIES * 8 + n_tot * 32
-        e2e = {"value": args.steps * n_tot * ne / t_e2e, "unit": "rays/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e / args.steps, "mode": e2e_mode}
+    if want_e2e and not args.no_e2e:
+        e2e = run_e2e(args, nbt, ndist, ctx, stream, dev, rank, world, cfg, strong, m, buf, cam, host_deltas, nd,
+                      q_host, q_lo, q_hi, q_out, q_out_mine, n_src, n_tot, n_mine, first, stride, steps)
 
     # ---- max over ranks
     t_dev = dev_ms
+    tot_counts = counts.copy()
     if world > 1:
-        tt = torch.tensor([dev_ms, visits, lookups], dtype=torch.float64, device=dev)
-        mx = tt.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-        t_dev = float(mx[0].item())
-        visits, lookups = float(tt[1].item()), float(tt[2].item())
+        tt = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_dev = float(tt.item())
+        ct = torch.from_numpy(counts).to(dev)
+        dist.all_reduce(ct, op=dist.ReduceOp.SUM)
+        tot_counts = ct.cpu().numpy()
         clk_all = [None] * world
         dist.all_gather_object(clk_all, clk)
     else:
         clk_all = [clk]
+    buf.close()
+    m.close()
+    if p2p is not None:
+        p2p.close()
+    if rank != 0:
+        return None
+
+    rays_total = steps * n_tot * ne
+    sec = t_dev / 1e3
+    tr_ms, tr_n = prof[nbt.KERNEL_TRACE]
+    tr_avg = tr_ms / max(tr_n, 1)
+    achieved = lookups_r * OPS_PER_LOOKUP / (tr_ms / 1e3) if tr_ms > 0 else None
+    tr = ncu_traffic(cfg.name)
+    l2_bytes = tr.get("l2_bytes_per_launch")
+    reasons = sorted({r for c in clk_all if c for r in c["reasons"]})
+    clocks_out = dict(clk_all[0]) if clk_all[0] else None
+    if clocks_out:
+        clocks_out["reasons"] = reasons
+    shares = {name: round(share_prof[k][0] / max(share_ms, 1e-9), 4) for k, name in
+              [(nbt.KERNEL_TRACE, "k_id_trace"), (nbt.KERNEL_FRAMES, "k_persp_frames"),
+               (nbt.KERNEL_FINALIZE, "k_id_finalize"), (nbt.KERNEL_IDW, "k_idw_query"),
+               (nbt.KERNEL_SAMPLE, "k_sample_perspectives"), (nbt.KERNEL_MAP_UPDATE, "map_update")]}
+    roof = {"bound": "alu", "achieved": achieved / 1e12 if achieved else None,
+            "peak": pk["int32_ops_per_s"] / 1e12, "unit": "Tops/s (int32)",
+            "frac": (achieved / pk["int32_ops_per_s"]) if achieved else None,
+            "traffic": tr.get("dram_bytes_per_launch"),
+            "kernel": "k_id_trace", "kernel_avg_ms": tr_avg, "kernel_launches": tr_n,
+            "work": f"{OPS_PER_LOOKUP} int32 ops x in-grid voxel steps of rank 0's launches (SURVEY.md 8(d); "
+                    f"DESIGN.md section 6)",
+            "peak_basis": pk["basis"]}
+    if l2_bytes and tr_avg > 0:
+        roof["l2"] = {"achieved_gbs": l2_bytes / (tr_avg / 1e3) / 1e9, "peak_gbs": pk["l2_gbs"],
+                      "frac": (l2_bytes / (tr_avg / 1e3) / 1e9 / pk["l2_gbs"]) if pk["l2_gbs"] else None,
+                      "bytes_per_launch": l2_bytes,
+                      "source": tr.get("source", "ncu --set full, lts__t_sectors_srcunit_tex_op_read x 32 B")}
+    return {
+        "value": rays_total / sec, "ms_per_step": t_dev / steps,
+        "ms_per_step_p50": statistics.median(step_ms), "ms_per_step_max": max(step_ms),
+        "voxel_steps_per_s": float(tot_counts[:3].sum()) / sec, "lookups_per_s": float(tot_counts[3]) / sec,
+        "roofline": roof, "kernel_share_of_step": shares, "gpu_launches": launches, "clocks": clocks_out,
+        "e2e": e2e,
+        "checksum": {"totals_sum": [int(x) for x in tot_counts],
+                     "last_step_gain_b2b64": digest64(last_gain),
+                     "last_step_counts_b2b64": digest64(last_counts) if last_counts is not None else None},
+        "n_tot": n_tot, "ne": ne,
+    }
+
+
+def run_e2e(args, nbt, ndist, ctx, stream, dev, rank, world, cfg, strong, m, buf, cam, host_deltas, nd, q_host,
+            q_lo, q_hi, q_out, q_out_mine, n_src, n_tot, n_mine, first, stride, steps):
+    """The same step end to end through the public API: every step copies its inputs (deltas,
+    perspectives, queries) in from pinned host memory and reads the IDW values and the IG cloud
+    back.  N = 1: one CUDA-graph replay of the public calls and the copies per step (`value`),
+    and the ABI's own host-buffer path (`abi_host`: on_device = 0 pointers, the library stages
+    them); N > 1: eager calls with the NCCL exchanges between them."""
+    import torch
+    import torch.distributed as dist
+    n_sets = min(steps, 16)
+    e2e_persp = [torch.from_numpy(nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, n_src,
+                                                          77 + 1000003 * s + (0 if strong else 7919 * rank),
+                                                          cfg.persp_mode)).pin_memory()
+                 for s in range(n_sets)]
+    h_ijk = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a, _ in host_deltas]
+    h_val = [torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for _, v in host_deltas]
+    h_q = torch.from_numpy(np.ascontiguousarray(q_host[q_lo:q_hi] if world > 1 else q_host)).pin_memory()
+    e_ijk = torch.empty_like(h_ijk[0], device=dev)
+    e_val = torch.empty_like(h_val[0], device=dev)
+    e_persp = torch.empty((n_src, 3), dtype=torch.float64, device=dev)
+    e_q = torch.empty_like(h_q, device=dev)
+    r_q = torch.empty(N_QUERIES, dtype=torch.float64).pin_memory()
+    r_gain = torch.empty(n_tot, dtype=torch.float64).pin_memory()
+    r_xyz = torch.empty((n_tot, 3), dtype=torch.float64).pin_memory()
+    loc = nbt.empty_cloud(n_mine, device=dev)
+    full = nbt.empty_cloud(n_tot, device=dev) if world > 1 else loc
+
+    def e2e_step(s):
+        c = s % N_DELTA_SETS
+        e_ijk.copy_(h_ijk[c], non_blocking=True)                             # H2D deltas
+        e_val.copy_(h_val[c], non_blocking=True)
+        e_persp.copy_(e2e_persp[s % len(e2e_persp)], non_blocking=True)     # H2D perspectives
+        e_q.copy_(h_q, non_blocking=True)                                    # H2D queries
+        if world > 1:
+            ndist.broadcast_deltas(e_ijk, e_val, src=0)
+        m.update(e_ijk, e_val)
+        if n_mine:
+            nbt.id_compute(ctx, m, cfg.poi, e_persp, cam, cfg.range_, out=loc, first=first, stride=stride)
+        if world > 1:
+            ndist.gather_cloud(loc.xyz, loc.gain, loc.counts, n_tot, world, strided=strong,
+                               out=(full.xyz, full.gain, full.counts))
+        buf.push(full, n_tot)
+        if world == 1:
+            buf.query(e_q, power_p=POWER_P, out=q_out)
+        else:
+            if q_hi > q_lo:
+                buf.query(e_q, power_p=POWER_P, out=q_out_mine[:q_hi - q_lo])
+            q_out.copy_(ndist.all_gather_rows(q_out_mine, N_QUERIES, world, strided=False))
+        r_q.copy_(q_out, non_blocking=True)                                  # D2H IDW values
+        r_gain.copy_(full.gain, non_blocking=True)                           # D2H the IG cloud
+        r_xyz.copy_(full.xyz, non_blocking=True)
+        stream.synchronize()
+        return r_gain, r_xyz
+
+    mode = "eager API calls with the NCCL exchanges between them, one synchronisation per step"
+    if world == 1 and not args.no_graph:
+        # the same public calls captured once (nbt_ctx_capture_begin/end) with the copies: per
+        # step the host writes the step's inputs into pinned staging, replays the graph (H2D,
+        # update, ID, push, IDW, D2H) and waits for the results
+        s_ijk, s_val = h_ijk[0].clone().pin_memory(), h_val[0].clone().pin_memory()
+        s_persp = e2e_persp[0].clone().pin_memory()
+        h_ijk_live, h_val_live, persp_live = h_ijk, h_val, e2e_persp
+        e2e_step(0)                                # warm-up outside the capture
+        ctx.capture_begin()
+        e_ijk.copy_(s_ijk, non_blocking=True)
+        e_val.copy_(s_val, non_blocking=True)
+        e_persp.copy_(s_persp, non_blocking=True)
+        e_q.copy_(h_q, non_blocking=True)
+        m.update(e_ijk, e_val)
+        nbt.id_compute(ctx, m, cfg.poi, e_persp, cam, cfg.range_, out=loc)
+        buf.push(loc, n_tot)
+        buf.query(e_q, power_p=POWER_P, out=q_out)
+        r_q.copy_(q_out, non_blocking=True)
+        r_gain.copy_(loc.gain, non_blocking=True)
+        r_xyz.copy_(loc.xyz, non_blocking=True)
+        e2e_graph = ctx.capture_end()
+
+        def e2e_step(s):                           # noqa: F811 -- the graph form
+            s_ijk.copy_(h_ijk_live[s % N_DELTA_SETS])                      # host staging of the inputs
+            s_val.copy_(h_val_live[s % N_DELTA_SETS])
+            s_persp.copy_(persp_live[s % len(persp_live)])
+            e2e_graph.launch()
+            stream.synchronize()
+            return r_gain, r_xyz
+        mode = "one CUDA-graph replay of the public calls and the copies per step, one synchronisation"
+
+    for s in range(2):
+        e2e_step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for s in range(steps):
+        e2e_step(s)
+    torch.cuda.synchronize()
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    h2d = nd * 13 + n_src * 24 + (q_hi - q_lo) * 24          # this rank's copies
+    d2h = N_QUERIES * 8 + n_tot * 32
+    out = {"value": steps * n_tot * cam.num_rays / t_e2e, "unit": "rays/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e / steps, "mode": mode}
+
+    if world == 1:
+        # the ABI's host-buffer path: numpy inputs and outputs, on_device = 0 (the library stages
+        # them through pinned memory and synchronises where a host result is returned)
+        h_ijk_np = [a for a, _ in host_deltas]
+        h_val_np = [v for _, v in host_deltas]
+        h_persp_np = [p.numpy() for p in e2e_persp]
+        q_np = np.ascontiguousarray(q_host)
+        o_cloud = nbt.empty_cloud(n_tot)
+        o_q = np.empty(N_QUERIES)
+
+        def abi_step(s):
+            m.update(h_ijk_np[s % N_DELTA_SETS], h_val_np[s % N_DELTA_SETS])           # nbt_map_update, host
+            nbt.id_compute(ctx, m, cfg.poi, h_persp_np[s % len(h_persp_np)], cam, cfg.range_,
+                           out=o_cloud)                                                # host in, host out
+            buf.push(o_cloud, n_tot)                                                   # host cloud in
+            buf.query(q_np, power_p=POWER_P, out=o_q)                                  # host in, host out
+        for s in range(2):
+            abi_step(s)
+        t0 = time.perf_counter()
+        for s in range(steps):
+            abi_step(s)
+        t_abi = time.perf_counter() - t0
+        out["abi_host"] = {"value": steps * n_tot * cam.num_rays / t_abi, "unit": "rays/s",
+                           "ms_per_step": 1e3 * t_abi / steps,
+                           "h2d_bytes_per_step": nd * 13 + n_src * 24 + n_tot * 32 + N_QUERIES * 24,
+                           "d2h_bytes_per_step": n_tot * 64 + N_QUERIES * 8,
+                           "mode": "nbt_map_update / nbt_id_compute / nbt_idbuf_push / nbt_ig_query with host "
+                                   "pointers (on_device = 0): the library's pinned staging, eager, synchronous "
+                                   "host results"}
+    return out
+
+
+def run_cprime(args, nbt, ctx, stream, dev, flush, pk, reps):
+    """North-star block, config C' (BASELINE north_star): 512 perspectives x 640x480 rays on the
+    256^3 map, the per-MHP-cycle latency of a3-a9 (sample, ID, push, 1984 IDW queries) over
+    `reps` cycles with the L2 flushed before each, CUDA events on the stream, clocks sampled
+    across the block; its own k_id_trace roofline; e2e with host perspectives in and the host
+    IG cloud + IDW values out through the ABI (on_device = 0)."""
+    import torch
+    cn = CONFIGS["C'"]
+    m = nbt.Map(ctx, nbt.map_desc(cn.n, cn.n, cn.n, cn.voxel_size))
+    m.upload(cn.map_codes())
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cn.width, cn.height)
+    persp = torch.empty((cn.n_persp, 3), dtype=torch.float64, device=dev)
+    cloud = nbt.empty_cloud(cn.n_persp, device=dev)
+    buf = nbt.IdBuffer(ctx, N_B, cn.n_persp)
+    q_dev = torch.from_numpy(query_points(N_QUERIES, cn.poi, cn.persp_radius, 0.5, 1.2, seed=5)).to(dev)
+    q_out = torch.empty(N_QUERIES, dtype=torch.float64, device=dev)
+
+    def cycle(t):
+        nbt.sample_perspectives(ctx, cn.poi, cn.persp_radius, cn.n_persp, cn.persp_seed + t, cn.persp_mode,
+                                out=persp)
+        nbt.id_compute(ctx, m, cn.poi, persp, cam, cn.range_, out=cloud)
+        buf.push(cloud, cn.n_persp)
+        buf.query(q_dev, power_p=POWER_P, out=q_out)
+
+    cycle(0)
+    ctx.sync()
+    ctx.set_profiling_mask([nbt.KERNEL_TRACE])
+    ctx.profile_read(nbt.KERNEL_TRACE, reset=True)
+    gpu_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid).replace("GPU-", "")
+    clocks = ClockSampler(gpu_id)
+    time.sleep(0.1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times, lookups = [], 0.0
+    t_w0 = time.time()
+    for t in range(1, reps + 1):
+        flush.fill_(t & 0xFF)
+        e0.record(stream)
+        cycle(t)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        lookups += float(cloud.counts[:, 3].sum().item())
+    t_w1 = time.time()
+    clocks.stop()
+    clk = clocks.summary(t_w0, t_w1)
+    tr_ms, tr_n = ctx.profile_read(nbt.KERNEL_TRACE, reset=True)
+    ctx.set_profiling(False)
+    achieved = lookups * OPS_PER_LOOKUP / (tr_ms / 1e3) if tr_ms > 0 else None
+    tr = ncu_traffic("C'")
+    tr_avg = tr_ms / max(tr_n, 1)
+    roof = {"bound": "alu", "achieved": achieved / 1e12 if achieved else None,
+            "peak": pk["int32_ops_per_s"] / 1e12, "unit": "Tops/s (int32)",
+            "frac": achieved / pk["int32_ops_per_s"] if achieved else None,
+            "traffic": tr.get("dram_bytes_per_launch"), "kernel": "k_id_trace", "kernel_avg_ms": tr_avg,
+            "kernel_launches": tr_n, "peak_basis": pk["basis"]}
+    if tr.get("l2_bytes_per_launch") and pk["l2_gbs"]:
+        a = tr["l2_bytes_per_launch"] / (tr_avg / 1e3) / 1e9
+        roof["l2"] = {"achieved_gbs": a, "peak_gbs": pk["l2_gbs"], "frac": a / pk["l2_gbs"]}
+    # e2e: host perspectives in, host IG cloud and IDW values out, through the ABI
+    hp = [nbt.sample_perspectives(ctx, cn.poi, cn.persp_radius, cn.n_persp, 99 + t, cn.persp_mode)
+          for t in range(4)]
+    hq = q_dev.cpu().numpy()
+    ho = nbt.empty_cloud(cn.n_persp)
+    hq_out = np.empty(N_QUERIES)
+    e2e_t = []
+    for t in range(6):
+        t0 = time.perf_counter()
+        nbt.id_compute(ctx, m, cn.poi, hp[t % 4], cam, cn.range_, out=ho)
+        buf.push(ho, cn.n_persp)
+        buf.query(hq, power_p=POWER_P, out=hq_out)
+        if t >= 2:
+            e2e_t.append(1e3 * (time.perf_counter() - t0))
+    buf.close()
+    m.close()
+    ms = statistics.mean(times)
+    return {"config": "C': 256^3 SYN map, 512 perspectives x 640x480 rays, range 1.5 m (north_star target)",
+            "id_latency_ms": ms, "id_latency_ms_p50": statistics.median(times),
+            "id_latency_ms_max": max(times), "reps": len(times), "rays_per_s": cn.rays_per_id / (ms / 1e3),
+            "lookups_per_s": lookups / (sum(times) / 1e3), "target_ms": 100.0, "roofline": roof,
+            "clocks": clk, "l2": "flushed before every cycle (outside the events)",
+            "e2e": {"ms_per_cycle": statistics.mean(e2e_t), "unit": "ms",
+                    "h2d_bytes_per_cycle": cn.n_persp * 24 + cn.n_persp * 32 + N_QUERIES * 24,
+                    "d2h_bytes_per_cycle": cn.n_persp * 64 + N_QUERIES * 8,
+                    "mode": "host perspectives / cloud / queries through the ABI (on_device = 0)"}}
+
+
+def main_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_22588_b200 as nbt
+    from paper_2503_22588_b200 import dist as ndist
+
+    rank, world, local = ndist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    # one dedicated stream shared by libnbt, torch's events and NCCL (the legacy default
+    # stream handle 0 would make libnbt create its own stream)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx = nbt.Ctx(local, stream.cuda_stream)
+    pk = peaks()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    mode = "strong" if cfg.name == "D" else "weak"
+
+    head = run_cycle(args, nbt, ndist, ctx, stream, dev, rank, world, cfg, mode, args.steps, args.warmup, flush,
+                     pk)
+
+    north = None
+    if not args.no_north_star:
+        if rank == 0:
+            north = run_cprime(args, nbt, ctx, stream, dev, flush, pk, max(20, args.north_star_reps))
+        if world > 1:
+            dist.barrier()
+    cfg_b = None
+    if cfg.name != "B" and not args.no_config_b:
+        b = run_cycle(args, nbt, ndist, ctx, stream, dev, rank, world, CONFIGS["B"], "weak",
+                      max(10, min(args.steps, 40)), 3, flush, pk, want_e2e=False, want_shares=False)
+        if rank == 0:
+            cfg_b = {"config": workload_name(CONFIGS["B"], world, "weak"), "scaling": "weak",
+                     "value": b["value"], "unit": "rays/s", "ms_per_step": b["ms_per_step"],
+                     "lookups_per_s": b["lookups_per_s"], "roofline": b["roofline"], "clocks": b["clocks"]}
+    integ = None
+    if not args.no_integrate and rank == 0:
+        integ = run_integration(nbt, ctx, stream, dev, flush)
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
-        rays_total = args.steps * n_tot * ne
-        sec = t_dev / 1e3
-        tr_ms, tr_n = prof[nbt.KERNEL_TRACE]
-        tr_avg = tr_ms / max(tr_n, 1)
-        f_max = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        peak_tops = sms * INT_LANES_PER_SM_CLK * f_max / 1e12
-        lookups_rank0 = float(counts[3])
-        achieved = lookups_rank0 * OPS_PER_LOOKUP / (tr_ms / 1e3) / 1e12 if tr_ms > 0 else None
-        traffic = None
-        tfile = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
-        if os.path.exists(tfile):
-            with open(tfile) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
-        reasons = sorted({r for c in clk_all if c for r in c["reasons"]})
-        clocks_out = dict(clk_all[0]) if clk_all[0] else None
-        if clocks_out:
-            clocks_out["reasons"] = reasons
-        shares = {name: round(share_prof[k][0] / max(share_ms, 1e-9), 4) for k, name in
-                  [(nbt.KERNEL_TRACE, "k_id_trace"), (nbt.KERNEL_FRAMES, "k_persp_frames"),
-                   (nbt.KERNEL_FINALIZE, "k_id_finalize"), (nbt.KERNEL_IDW, "k_idw_query"),
-                   (nbt.KERNEL_SAMPLE, "k_sample_perspectives"), (nbt.KERNEL_MAP_UPDATE, "map_update")]}
         line = {
-            "metric": "rays/s", "value": rays_total / sec, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_dev / args.steps, "higher_is_better": True, "scaling": "weak",
+            "metric": "rays/s", "value": head["value"], "unit": "rays/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": mode,
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, world), "map": f"{cfg.n}^3 SYN(R_o={cfg.r_o:g}, seed "
-                       f"{cfg.map_seed}) 2-bit packed", "perspectives_per_step": n_tot, "rays_per_perspective": ne,
+            "config": {"workload": workload_name(cfg, world, mode),
+                       "map": f"{cfg.n}^3 SYN(R_o={cfg.r_o:g}, seed {cfg.map_seed}) 2-bit packed",
+                       "perspectives_per_step": head["n_tot"], "rays_per_perspective": head["ne"],
                        "l2": "flushed before every timed step (256 MiB write, outside the step events)",
-                       "parallelism": f"perspectives sharded over {world} GPU(s), weak scaling"
+                       "parallelism": (f"perspective j on rank j mod {world} (strong scaling)" if mode == "strong"
+                                       else f"every rank its own perspective set (weak scaling)")
                        + ("" if world == 1 else (", IG-cloud all-gather fused into the finalize (peer memory)"
                                                  if args.gather == "p2p" else ", IG-cloud all-gather over NCCL"))},
-            "voxel_steps_per_s": visits / sec, "lookups_per_s": lookups / sec,
-            "id_latency_ms": t_dev / args.steps,
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32)",
-                         "frac": (achieved / peak_tops) if achieved else None, "traffic": traffic,
-                         "kernel": "k_id_trace", "kernel_avg_ms": tr_avg, "kernel_launches": tr_n,
-                         "work": f"{OPS_PER_LOOKUP} int32 ops x in-grid voxel steps (DESIGN.md section 6)",
-                         "peak_basis": f"{sms} SMs x {INT_LANES_PER_SM_CLK} int32 lanes/clk x "
-                                       f"{f_max / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)"},
-            "kernel_share_of_step": shares,
-            "kernel_share_note": ("eager launches, every kernel family bracketed by CUDA events inside the timed region"
-                                  if args.no_graph else
-                                  "from a separate fully profiled graph run after the timed region (each profiled "
-                                  "kernel adds two ~2 us event nodes); the timed graphs record only k_id_trace"),
+            "voxel_steps_per_s": head["voxel_steps_per_s"], "lookups_per_s": head["lookups_per_s"],
+            "id_latency_ms": head["ms_per_step"], "ms_per_step_p50": head["ms_per_step_p50"],
+            "roofline": head["roofline"],
+            "kernel_share_of_step": head["kernel_share_of_step"],
+            "kernel_share_note": "from a separate fully profiled graph run after the timed region (each profiled "
+                                 "kernel adds two ~2 us event nodes); the timed graphs record only k_id_trace",
+            "checksum": head["checksum"],
             "north_star": north,
-            "config_d_strong": strong,
+            "config_b": cfg_b,
             "map_integration": integ,
-            "gpu_launches": launches,
-            "clocks": clocks_out,
-            "e2e": e2e,
+            "gpu_launches": head["gpu_launches"],
+            "clocks": head["clocks"],
+            "e2e": head["e2e"],
             "cpu_baseline": None,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = run_cpu_baseline(cfg, codes, args.cpu_budget_s)
+            line["cpu_baseline"] = run_cpu_baseline(cfg, cfg.map_codes(), args.cpu_budget_s)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -889,6 +1065,7 @@ def paper_sweep(argv):
     if args.out:
         with open(args.out, "w") as f:
             f.write(text)
+
 
 
 

@@ -352,7 +352,12 @@ typedef struct {
  * g_R,k,j = sum over the N_O counted voxels of g(v_i) (Eq. 2).
  * Canonical form (Q26): ((T_U g_U + T_F g_F) + T_O g_O) / N_E from integer
  * per-state totals.  The direct ray-order sum is also computed and must agree
- * within 1e-12 relative (self-check of the two readings of P:214). */
+ * (self-check of the two readings of P:214, Q26) within the worst-case bound of
+ * recursive summation of nonnegative terms: T terms (every counted visit plus the N_E
+ * per-ray sums) each rounded once, and each per-voxel term g(v) itself rounded once in
+ * the probability mode, give |direct - exact| <= gamma_{2T} * exact, gamma_n =
+ * n u / (1 - n u), u = 2^-53 (Higham, Accuracy and Stability, 4.2); the canonical form
+ * adds at most gamma_8. */
 static int one_perspective(const orc_map *m, const double poi[3], const double p[3],
                            const orc_camera *cam, double range, orc_persp_out *out)
 {
@@ -360,7 +365,7 @@ static int one_perspective(const orc_map *m, const double poi[3], const double p
     int st = orc_frame_q16(m, poi, p, cam, range, &f, NULL, NULL, NULL);
     if (st) return st;
     int32_t ne = orc_camera_num_rays(cam);
-    int64_t tu = 0, tf = 0, to = 0, tl = 0, tg = 0;
+    int64_t tu = 0, tf = 0, to = 0, tl = 0, tg = 0, nvis = 0;
     double direct = 0.0;
     for (int32_t k = 0; k < ne; ++k) {
         int32_t o[3], e[3];
@@ -369,13 +374,17 @@ static int one_perspective(const orc_map *m, const double poi[3], const double p
         if ((st = orc_trace_ray(m, o, e, 0, NULL, NULL, NULL, &r))) return st;
         direct += r.g;
         tu += r.n_u; tf += r.n_f; to += r.n_o; tl += r.lookups; tg += r.g63;
+        nvis += r.n_u + r.n_f + r.n_o;
     }
     double canon = m->levels ? (double)tg / ((double)PLEVELS * (double)ne)
                              : (((double)tu * m->gain[0] + (double)tf * m->gain[1]) + (double)to * m->gain[2]) /
                                    (double)ne;
     direct = direct / (double)ne;
-    double scale = fabs(canon) > 1.0 ? fabs(canon) : 1.0;
-    if (fabs(direct - canon) > 1e-12 * scale) return ORC_ERR_SELFCHECK;
+    const double u = ldexp(1.0, -53);
+    const double nt = 2.0 * (double)(nvis + ne) + 8.0;
+    const double gamma = nt * u / (1.0 - nt * u);
+    double scale = fabs(canon) > fabs(direct) ? fabs(canon) : fabs(direct);
+    if (fabs(direct - canon) > gamma * scale) return ORC_ERR_SELFCHECK;
     memcpy(out->xyz, p, 3 * sizeof(double));
     out->gain = canon;
     out->t_u = tu; out->t_f = tf; out->t_o = to; out->lookups = tl; out->t_g = tg;

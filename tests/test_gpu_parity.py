@@ -235,10 +235,10 @@ def test_production_trace_per_ray_config_b_subset(nbt, ctx):
 def test_production_trace_per_ray_stores(nbt, ctx, layout, bits, policy):
     """Per-ray parity of the production trace on both layouts, both state widths and both
     outside policies, with perspectives outside the map and corner rays."""
-    codes = rand_map(0, 0.3, 0.66, 0.04, seed=21, shape=(19, 27, 33))
+    codes = rand_map(0, 0.3, 0.66, 0.04, seed=21, shape=(33, 41, 47))
     m, om = make_map(nbt, ctx, codes, policy=policy, layout=layout, bits=bits)
-    poi = np.array([16.5, 13.5, 9.5])
-    P = oracle.sample_perspectives(poi, 25.0, 10, seed=2)
+    poi = np.array([23.5, 20.5, 16.5])
+    P = oracle.sample_perspectives(poi, 35.0, 10, seed=2)
     cam = nbt.camera_from_fov(FOV_H, FOV_V, 21, 13)
     ocam = oracle.camera_from_fov(FOV_H, FOV_V, 21, 13)
     cam.add_corners = ocam.add_corners = 1
@@ -759,20 +759,21 @@ def test_layouts_roundtrip_update_and_id(nbt, ctx, layout, bits):
     """Both map store layouts (Morton cube / linear with sentinel shell) and both state
     widths (2-bit codes / one byte per voxel) give identical, oracle-exact results:
     upload/download, last-wins updates, per-ray walks, the ID."""
-    codes = rand_map(0, 0.3, 0.66, 0.04, seed=21, shape=(19, 27, 33))
+    # ragged extents whose Morton cube (128^3 with the 16-voxel shell) is < 8x the linear store
+    codes = rand_map(0, 0.3, 0.66, 0.04, seed=21, shape=(33, 41, 47))
     m, om = make_map(nbt, ctx, codes, layout=layout, bits=bits)
     assert np.array_equal(m.download(), codes)
     rng = np.random.default_rng(4)
-    ijk = np.stack([rng.integers(0, 33, 900), rng.integers(0, 27, 900), rng.integers(0, 19, 900)], 1).astype(np.int32)
+    ijk = np.stack([rng.integers(0, 47, 900), rng.integers(0, 41, 900), rng.integers(0, 33, 900)], 1).astype(np.int32)
     vals = rng.integers(0, 3, 900).astype(np.uint8)
     m.update(ijk, vals)
     codes2 = _apply_in_order(codes, ijk, vals)
     assert np.array_equal(m.download(), codes2)
     om = oracle.OracleMap(codes2)
-    o, e = random_segments_q16(1500, -8.0, 40.0, seed=31)
+    o, e = random_segments_q16(1500, -8.0, 54.0, seed=31)
     _compare_walks(nbt, ctx, m, om, o, e)
-    poi = np.array([16.5, 13.5, 9.5])
-    P = oracle.sample_perspectives(poi, 12.0, 24, seed=2)
+    poi = np.array([23.5, 20.5, 16.5])
+    P = oracle.sample_perspectives(poi, 16.0, 24, seed=2)
     cloud, g, c = run_both(nbt, ctx, m, om, poi, P, 20, 14, 30.0, corners=True)
     assert_cloud_equal(cloud, P, g, c)
 
@@ -1155,3 +1156,31 @@ def test_full_size_north_star_and_d_sampled(nbt, ctx, name, sampled):
     _, g, c = oracle.id_compute(om, cfg.poi, P[idx], ocam, cfg.range_, nthreads=NTHREADS)
     assert np.array_equal(counts[idx].astype(np.int64), c)
     assert np.array_equal(gain[idx], g)
+
+
+def test_ctx_options_roundtrip_and_range(nbt, ctx):
+    """nbt_ctx_set_option / get_option: defaults, round trip, out-of-range and unknown options
+    rejected; a non-default trace tuning gives the same ID bit for bit."""
+    assert ctx.get_option(nbt.OPT_TRACE_REFILL_MIN) == 6
+    assert ctx.get_option(nbt.OPT_TRACE_CHUNK_MIN) == 64
+    assert ctx.get_option(nbt.OPT_WALK_WIDTH) == 0
+    for opt, bad in [(nbt.OPT_TRACE_REFILL_MIN, 0), (nbt.OPT_TRACE_REFILL_MIN, 33), (nbt.OPT_TRACE_CHUNK_MIN, 16),
+                     (nbt.OPT_TRACE_CARVEOUT, 101), (nbt.OPT_WALK_WIDTH, 48), (nbt.OPT_DELTA_SORT, 2), (99, 0)]:
+        with pytest.raises(nbt.NbtError):
+            ctx.set_option(opt, bad)
+    cfg = CONFIGS["A"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    ref = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
+    try:
+        ctx.set_option(nbt.OPT_TRACE_REFILL_MIN, 1)
+        ctx.set_option(nbt.OPT_TRACE_CHUNK_MIN, 100)
+        assert ctx.get_option(nbt.OPT_TRACE_CHUNK_MIN) == 128
+        ctx.set_option(nbt.OPT_TRACE_CARVEOUT, 50)
+        alt = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
+        assert np.array_equal(alt.counts, ref.counts) and np.array_equal(alt.gain, ref.gain)
+    finally:
+        ctx.set_option(nbt.OPT_TRACE_REFILL_MIN, 6)
+        ctx.set_option(nbt.OPT_TRACE_CHUNK_MIN, 64)
+        ctx.set_option(nbt.OPT_TRACE_CARVEOUT, 25)
