@@ -742,8 +742,8 @@ def test_id_wide_path(nbt, ctx):
     poi = np.array([24.5, 24.5, 24.5])
     P = oracle.sample_perspectives(poi, 8200.0, 5, seed=6, mode=1)
     fov = 0.2                                            # narrow: the far corners stay inside +-2^14 voxels
-    cam = nbt.camera_from_fov(fov, fov, 6, 5)
-    ocam = oracle.camera_from_fov(fov, fov, 6, 5)
+    cam = nbt.camera_from_fov(fov, fov, 7, 5)            # odd lattice: the centre ray passes the PoI
+    ocam = oracle.camera_from_fov(fov, fov, 7, 5)
     cam.add_corners = ocam.add_corners = 1
     cloud = nbt.id_compute(ctx, m, poi, P, cam, 16500.0)
     _, g, c = oracle.id_compute(om, poi, P, ocam, 16500.0, nthreads=NTHREADS)
