@@ -190,10 +190,51 @@ __device__ __forceinline__ uint32_t load_map_word(const uint32_t *p)
 // byte, so a visit needs no rotate and the code packs with one shift-add.
 constexpr int kStore2 = 2, kStoreByte = 1, kStoreProb = 8;
 
+// Step table (NBT_DDA_TABLE experiment, linear layout, int32 terms): per lane, the three
+// possible updates (dq_xy, dq_xz, dq_yz, d_idx) of a step along x, y, z in shared memory,
+// written when the lane takes a ray; a step is then the axis choice (2 LOP3 + 2 SHF), one
+// 16-byte shared load and 4 adds instead of the 9 mask multiply-adds of walk_step.
+#ifndef NBT_DDA_TABLE
+#define NBT_DDA_TABLE 0
+#endif
+constexpr bool kDdaTable = NBT_DDA_TABLE != 0;
+
+// Shared-window address of the lane's z-step entry (the x and y entries sit 1024 and 512
+// bytes below it).  The table accesses are volatile asm so that the compiler keeps the
+// lane's stores before its loads.
+__device__ __forceinline__ void table_put_row(uint32_t a, int x, int y, int z, int w)
+{
+    asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w));
+}
+
+template <typename T>
+__device__ __forceinline__ void table_put(uint32_t tz, const Walk<T> &w)
+{
+    table_put_row(tz - 1024u, (int)w.ay, (int)w.az, 0, w.dX);          // x step
+    table_put_row(tz - 512u, (int)-w.ax, 0, (int)w.az, w.dY);          // y step
+    table_put_row(tz, 0, (int)-w.ax, (int)-w.ay, -w.ndZ);              // z step
+}
+
+template <typename T>
+__device__ __forceinline__ void walk_step_table(Walk<T> &w, uint32_t tz)
+{
+    const int t1 = w.qxy & w.qxz;                // sign: x first
+    const int t2 = w.qyz & ~t1;                  // sign: y first
+    const int px = (int)((unsigned)t1 >> 31);
+    const int py = (int)((unsigned)t2 >> 31);
+    const uint32_t a = (uint32_t)mad_i32(px, -1024, mad_i32(py, -512, (int)tz));   // axis 2 - 2 px - py
+    int dx, dy, dz, di;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(dx), "=r"(dy), "=r"(dz), "=r"(di) : "r"(a));
+    w.qxy = mad_i32(1, dx, w.qxy);               // the adds as IMADs: the FMA pipe has room, the ALU not
+    w.qxz = mad_i32(1, dy, w.qxz);
+    w.qyz = mad_i32(1, dz, w.qyz);
+    w.idx = (uint32_t)mad_i32(1, di, (int)w.idx);
+}
+
 // Issue the K loads of the next K visits (the DDA does not depend on the map, so
 // this runs ahead of the codes) and advance the DDA by K steps.
-template <typename T, int L, int VB, int K>
-__device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<K> &b)
+template <typename T, int L, int VB, int K, bool TAB = false>
+__device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<K> &b, uint32_t tz = 0)
 {
     const uint8_t *bytes = reinterpret_cast<const uint8_t *>(m.words);
 #pragma unroll
@@ -204,7 +245,10 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
         } else {
             b.wd[k] = __ldg(bytes + w.idx);
         }
-        walk_step<T, L, false>(w, m);
+        if constexpr (TAB)
+            walk_step_table(w, tz);
+        else
+            walk_step<T, L, false>(w, m);
     }
 }
 
@@ -417,6 +461,34 @@ __device__ __forceinline__ const PeerTotals *peer_totals_of(const TraceArgs &A)
 {
     return reinterpret_cast<const PeerTotals *>(A.work_counter + kPeerTotalsOffset);
 }
+// SM-affine chunk order (NBT_SM_AFFINE = number of homes, experiment): perspective j belongs
+// to home j mod H; a warp first takes chunks of the home of its SM (smid mod H) -- so the
+// warps of one SM walk neighbouring tiles of the same frustum at the same time and share
+// its map lines in L1 -- and then steals from the other homes in order.
+#ifndef NBT_SM_AFFINE
+#define NBT_SM_AFFINE 0
+#endif
+constexpr int kHomes = NBT_SM_AFFINE;
+constexpr int kHomeCounterOffset = 128;  // ints: one counter per home
+__device__ __forceinline__ int next_chunk_affine(const TraceArgs &A)
+{
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int cpp = A.chunks_per_persp;
+    const int n = A.total_chunks / cpp;
+    const int homes = n < kHomes ? n : kHomes;
+    const int h0 = (int)(smid % (unsigned)homes);
+    for (int t = 0; t < homes; ++t) {
+        const int h = h0 + t < homes ? h0 + t : h0 + t - homes;
+        int *ctr = A.work_counter + kHomeCounterOffset + h;
+        const int per = ((n - h + homes - 1) / homes) * cpp;   // chunks of home h
+        if (*(volatile int *)ctr >= per) continue;
+        const int k = atomicAdd(ctr, 1);
+        if (k < per) return (h + homes * (k / cpp)) * cpp + k % cpp;
+    }
+    return A.total_chunks;
+}
+
 // REC instance (nbt_debug_id_rays): the per-ray record array lives in the same buffer.
 constexpr int kRecordOffset = 64;       // ints (after the peer totals)
 static_assert(kPeerTotalsOffset * 4 + sizeof(PeerTotals) <= kRecordOffset * 4, "record after the peer totals");
@@ -682,6 +754,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
     using Queue = std::conditional_t<REC, WalkQueueRec<T>, WalkQueue<T>>;
     __shared__ Queue queues[kWarpsPerBlock];
     Queue &Q = queues[threadIdx.x >> 5];
+    constexpr bool TAB = kDdaTable && sizeof(T) == 4 && L == kLayoutLinear && !CYCLE;
+    __shared__ int4 step_tab[TAB ? kWarpsPerBlock * 96 : 1];
+    // this lane's z-step entry: step_tab[warp][2][lane] (x, y entries 64 and 32 int4 below)
+    const uint32_t tz = (uint32_t)__cvta_generic_to_shared(step_tab) +
+                        (TAB ? (uint32_t)(((threadIdx.x >> 5) * 96 + 64 + (threadIdx.x & 31)) * 16) : 0u);
     int my_slot = 0;                         // REC: slot of this lane's ray
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -702,7 +779,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
             while (qcount == 0 && !q_done) {
                 if (q_next >= q_end) {
                     int ch = 0;
-                    if (lane == 0) ch = atomicAdd(A.work_counter, 1);
+                    if (lane == 0) ch = kHomes > 0 ? next_chunk_affine(A) : atomicAdd(A.work_counter, 1);
                     ch = __shfl_sync(full, ch, 0);
                     if (ch >= A.total_chunks) { q_done = true; break; }
                     q_j = ch / A.chunks_per_persp;
@@ -754,6 +831,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                 if (j >= 0) {
                     jl = j;
                     have = true;
+                    if (TAB) table_put(tz, w);
                     if (CYCLE) batch_issue<T, L, VB, K>(w, A.m, b0);
                 }
                 qhead += take;
@@ -775,7 +853,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
             }
             if (batch_finish<T, VB, K>(w, bits, 0u, b0, A.m.policy, c)) have = false;
         } else {
-            batch_issue<T, L, VB, K>(w, A.m, b0);
+            batch_issue<T, L, VB, K, TAB>(w, A.m, b0, tz);
             const Counts before = c;
             if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) {
                 have = false;
@@ -1019,9 +1097,12 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     // ray shard, else scratch; the finalize reads the caller's summed totals when given
     unsigned long long *tot = L.d_totals_trace ? reinterpret_cast<unsigned long long *>(L.d_totals_trace)
                                                : ctx->totals.as<unsigned long long>();
-    if ((st = ctx->counter.ensure(kRecordOffset * 4 + sizeof(void *)))) return st;
+    if ((st = ctx->counter.ensure((kHomeCounterOffset + (kHomes > 0 ? kHomes : 1)) * 4))) return st;
+    static_assert(kRecordOffset * 4 + sizeof(void *) <= kHomeCounterOffset * 4, "home counters after the record");
     FrameArgs A = frame_args(m, L.d_persp, L.first, L.stride, L.n, L.poi, L.cam, L.range);
     int *counter = ctx->counter.as<int>();
+    if (kHomes > 0)      // zeroed home counters (a memset node: valid inside a captured graph)
+        NBT_CUDA(cudaMemsetAsync(counter + kHomeCounterOffset, 0, kHomes * 4, ctx->stream));
     {
         ProfScope ps(ctx, NBT_KERNEL_FRAMES);
         k_persp_frames<<<(L.n + 127) / 128, 128, 0, ctx->stream>>>(A, ctx->frames.as<int32_t>(),

@@ -47,6 +47,17 @@ def _worker(rank, world, port, q):
         _, g_full, c_full = oracle.id_compute(om, cfg.poi, P, cam, cfg.range_)
         ok = (np.array_equal(xyz.numpy(), P) and np.array_equal(gain.numpy(), g_full)
               and np.array_equal(cnt.numpy(), c_full))
+        # the packed one-collective exchange of bench/id_compute_sharded: 64-byte rows (xyz,
+        # g_P, counts bit-cast into f64) all-gathered and un-strided; counts bit-exact
+        # (including values whose f64 bit pattern is a NaN or a denormal)
+        c64 = torch.from_numpy(c.astype(np.int64))
+        if rank == 0 and k:
+            c64[0, 3] = 0x7FF8000000000001                    # a NaN pattern as f64
+        gx, gg, gc = ndist.gather_cloud(torch.from_numpy(mine), torch.from_numpy(g), c64, n, world)
+        want_c = c_full.astype(np.int64).copy()
+        want_c[0, 3] = 0x7FF8000000000001
+        ok &= bool(np.array_equal(gx.numpy(), P) and np.array_equal(gg.numpy(), g_full)
+                   and np.array_equal(gc.numpy(), want_c))
         # weak scaling: every rank its own block, concatenated in rank order
         blk = torch.full((3, 2), float(rank))
         cat = ndist.all_gather_rows(blk, 3 * world, world, strided=False)
