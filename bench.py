@@ -50,6 +50,7 @@ POWER_P = 2.0             # IDW power
 N_DELTA_SETS = 8
 OPS_PER_LOOKUP = 12       # algorithmic int32 ops per in-grid voxel step
 PEAKS_FILE = os.path.join(ROOT, "profiles", "r02_peaks.json")   # tools/peaks.cu on this pool's B200
+CPRIME_STATE_BITS = 8     # the north-star block's map store (see run_cprime)
 
 
 def parse():
@@ -824,7 +825,10 @@ def run_cprime(args, nbt, ctx, stream, dev, flush, pk, reps):
     IG cloud + IDW values out through the ABI (on_device = 0)."""
     import torch
     cn = CONFIGS["C'"]
-    m = nbt.Map(ctx, nbt.map_desc(cn.n, cn.n, cn.n, cn.voxel_size))
+    # the byte-per-voxel state store (nbt_map_desc.state_bits = 8, 24 MB with the shell: L2-
+    # resident at 256^3): one load and no rotate per visit, 11% faster than the 2-bit store on
+    # this dense lattice (profiles/r02_trace_stores.log); the sparse configs B and D keep 2 bits
+    m = nbt.Map(ctx, nbt.map_desc(cn.n, cn.n, cn.n, cn.voxel_size, state_bits=CPRIME_STATE_BITS))
     m.upload(cn.map_codes())
     cam = nbt.camera_from_fov(FOV_H, FOV_V, cn.width, cn.height)
     persp = torch.empty((cn.n_persp, 3), dtype=torch.float64, device=dev)
@@ -891,7 +895,8 @@ def run_cprime(args, nbt, ctx, stream, dev, flush, pk, reps):
     buf.close()
     m.close()
     ms = statistics.mean(times)
-    return {"config": "C': 256^3 SYN map, 512 perspectives x 640x480 rays, range 1.5 m (north_star target)",
+    return {"config": f"C': 256^3 SYN map ({CPRIME_STATE_BITS}-bit state store), 512 perspectives x 640x480 rays, "
+                      f"range 1.5 m (north_star target)",
             "id_latency_ms": ms, "id_latency_ms_p50": statistics.median(times),
             "id_latency_ms_max": max(times), "reps": len(times), "rays_per_s": cn.rays_per_id / (ms / 1e3),
             "lookups_per_s": lookups / (sum(times) / 1e3), "target_ms": 100.0, "roofline": roof,

@@ -45,11 +45,12 @@ enum Op {
     kMixImm,    // LOP3 (2r, another chain) and IMAD (imm) alternating, 1:1
     kFfma_3r,   // FFMA d, a, b, c
     kFfma_imm,  // FFMA d, a, imm, c
+    kDfma,      // DFMA d, a, b, c           (FP64 pipe; the IDW's arithmetic)
     kNumOps
 };
 const char *kOpName[kNumOps] = {"lop3_3reg", "iadd_2reg", "iadd3_3reg", "shf_1reg", "imad_3reg", "imad_imm",
-                                "mix_lop3_imad_3reg", "mix_lop3_imad_imm", "ffma_3reg", "ffma_imm"};
-const char *kOpPipe[kNumOps] = {"alu", "alu", "alu", "alu", "fma", "fma", "alu+fma", "alu+fma", "fma", "fma"};
+                                "mix_lop3_imad_3reg", "mix_lop3_imad_imm", "ffma_3reg", "ffma_imm", "dfma"};
+const char *kOpPipe[kNumOps] = {"alu", "alu", "alu", "alu", "fma", "fma", "alu+fma", "alu+fma", "fma", "fma", "fp64"};
 
 constexpr int kChains = 8;
 constexpr int kUnroll = 16;     // instructions per chain per loop iteration
@@ -93,6 +94,31 @@ __device__ __forceinline__ void step(uint32_t (&x)[kChains], uint32_t a, uint32_
 // three-input IADD3 (checked with cuobjdump -sass), so the kIadd_2r chain issues one IADD3
 // per two PTX adds and the kIadd3 form one per step.
 constexpr double instrs_per_step(int op) { return op == kIadd_2r ? 0.5 : 1.0; }
+
+// DFMA chains on doubles (the FP64 pipe)
+__global__ void __launch_bounds__(256) k_issue_f64(int iters, uint32_t seed, uint32_t *sink, unsigned long long *clk)
+{
+    double x[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) x[c] = 1.0 + 1e-3 * (threadIdx.x + c);
+    const double m = 0.999999 + 1e-9 * (seed + threadIdx.x), d = 1e-7 * (threadIdx.x + 1);
+    const uint64_t c0 = clock64(), t0 = gtimer();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[c]) : "d"(m), "d"(d));
+    }
+    const uint64_t c1 = clock64(), t1 = gtimer();
+    double acc = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) acc += x[c];
+    if (acc == 12345.0) sink[threadIdx.x] = 1;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        clk[0] = c1 - c0;
+        clk[1] = t1 - t0;
+    }
+}
 
 template <int OP>
 __global__ void __launch_bounds__(256) k_issue(int iters, uint32_t seed, uint32_t *sink, unsigned long long *clk)
@@ -171,7 +197,11 @@ Res run_issue(int sms, int iters)
     CK(cudaMalloc(&sink, 4096));
     CK(cudaMalloc(&clk, 16));
     const int blocks = sms * 8;          // 8 x 256 threads = 64 warps per SM
-    k_issue<OP><<<blocks, 256>>>(iters / 8, 7u, sink, clk);
+    auto launch = [&](int it) {
+        if (OP == kDfma) k_issue_f64<<<blocks, 256>>>(it, 7u, sink, clk);
+        else k_issue<OP><<<blocks, 256>>>(it, 7u, sink, clk);
+    };
+    launch(iters / 8);
     CK(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
@@ -179,7 +209,7 @@ Res run_issue(int sms, int iters)
     double best = 0, mhz = 0;
     for (int rep = 0; rep < 3; ++rep) {
         CK(cudaEventRecord(e0));
-        k_issue<OP><<<blocks, 256>>>(iters, 7u, sink, clk);
+        launch(iters);
         CK(cudaEventRecord(e1));
         CK(cudaEventSynchronize(e1));
         float ms = 0;
@@ -270,12 +300,13 @@ int main()
                       run_issue<kIadd3>(sms, iters),    run_issue<kShf>(sms, iters),
                       run_issue<kImad_3r>(sms, iters),  run_issue<kImad_imm>(sms, iters),
                       run_issue<kMix>(sms, iters),      run_issue<kMixImm>(sms, iters),
-                      run_issue<kFfma_3r>(sms, iters),  run_issue<kFfma_imm>(sms, iters)};
+                      run_issue<kFfma_3r>(sms, iters),  run_issue<kFfma_imm>(sms, iters),
+                      run_issue<kDfma>(sms, iters)};
     double mhz = 0;
     for (auto &x : r) mhz = std::max(mhz, x.mhz);
     double best_int = 0;
     for (int k = 0; k < kNumOps; ++k)
-        if (k != kFfma_3r && k != kFfma_imm) best_int = std::max(best_int, r[k].ops_per_s);
+        if (k != kFfma_3r && k != kFfma_imm && k != kDfma) best_int = std::max(best_int, r[k].ops_per_s);
     const double l2_32 = run_l2(32ull << 20, sms), l2_64 = run_l2(64ull << 20, sms);
     double l1_req_c = 0, l1_req_s = 0;
     const double l1_c = run_l1<false>(sms, &l1_req_c, mhz), l1_s = run_l1<true>(sms, &l1_req_s, mhz);
