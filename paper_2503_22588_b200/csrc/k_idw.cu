@@ -80,72 +80,82 @@ __device__ __forceinline__ double dist2_fast(double x0, double x1, double x2, do
     return fma(dz, dz, fma(dy, dy, dx * dx));
 }
 
-__global__ void __launch_bounds__(kThreads)
+#ifndef NBT_IDW_LB
+#define NBT_IDW_LB 1              // resident blocks per SM the register allocation must allow
+#endif
+__global__ void __launch_bounds__(kThreads, NBT_IDW_LB)
     k_idw_entry(const double *__restrict__ xyz, const double *__restrict__ gain, int32_t max_persp,
                 const int32_t *__restrict__ meta, int32_t cap, const double *__restrict__ q, int32_t n_q,
-                double power_p, int32_t chunk, IdwPart *__restrict__ part)
+                double power_p, int32_t chunk, int32_t n_chunks, IdwPart *__restrict__ part)
 {
     __shared__ double4 sp[kTile];
-    const int e = blockIdx.y, c = blockIdx.z, n_chunks = gridDim.z;
+    // persistent: units (query block, entry, chunk), chunk-major then entry, dealt round-robin
+    const int nqb = (n_q + kQueries - 1) / kQueries;
+    const int units = nqb * cap * n_chunks;
     const int pushes = meta[0];
     const int m = min(pushes, cap);
-    if (e >= m) return;
-    const int slot = (pushes - m + e) % cap;                  // entry e, oldest first
     const int sub = threadIdx.x & (kSplit - 1);
-    const int q0 = blockIdx.x * kQueries + (threadIdx.x / kSplit) * kQPT;
-    const double *P = xyz + (size_t)slot * max_persp * 3;
-    const double *G = gain + (size_t)slot * max_persp;
-    const int np = meta[1 + slot];
-    const int j0 = c * chunk, j1 = min(np, j0 + chunk);
-    double x[kQPT][3];
-#pragma unroll
-    for (int k = 0; k < kQPT; ++k) {
-        const int qi = min(q0 + k, n_q - 1);                  // clamped: inactive queries compute garbage
-        x[k][0] = q[3 * (size_t)qi]; x[k][1] = q[3 * (size_t)qi + 1]; x[k][2] = q[3 * (size_t)qi + 2];
-    }
     const bool p2 = power_p == 2.0;
     const double hp = -0.5 * power_p;
-    double num[kQPT], den[kQPT], d2min[kQPT];
-#pragma unroll
-    for (int k = 0; k < kQPT; ++k) { num[k] = 0.0; den[k] = 0.0; d2min[k] = __longlong_as_double(0x7ff0000000000000LL); }
-    for (int base = j0; base < j1; base += kTile) {
-        const int nt = min(kTile, j1 - base);
-        __syncthreads();
-        for (int t = threadIdx.x; t < nt; t += kThreads)
-            sp[t] = make_double4(P[3 * (size_t)(base + t)], P[3 * (size_t)(base + t) + 1], P[3 * (size_t)(base + t) + 2],
-                                 G[base + t]);
-        __syncthreads();
-#pragma unroll 2
-        for (int t = sub; t < nt; t += kSplit) {
-            const double4 r = sp[t];
-#pragma unroll
-            for (int k = 0; k < kQPT; ++k) {
-                const double d2 = dist2_fast(x[k][0], x[k][1], x[k][2], r.x, r.y, r.z);
-                d2min[k] = fmin(d2min[k], d2);
-                const double w = p2 ? rcp_nr(d2) : pow(d2, hp);
-                num[k] = fma(r.w, w, num[k]);
-                den[k] += w;
-            }
-        }
-    }
-#pragma unroll
-    for (int off = kSplit / 2; off > 0; off >>= 1) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int qb = u % nqb;
+        const int e = (u / nqb) % cap;
+        const int c = u / (nqb * cap);
+        if (e >= m) continue;                                 // block-uniform
+        const int slot = (pushes - m + e) % cap;              // entry e, oldest first
+        const int q0 = qb * kQueries + (threadIdx.x / kSplit) * kQPT;
+        const double *P = xyz + (size_t)slot * max_persp * 3;
+        const double *G = gain + (size_t)slot * max_persp;
+        const int np = meta[1 + slot];
+        const int j0 = c * chunk, j1 = min(np, j0 + chunk);
+        double x[kQPT][3];
 #pragma unroll
         for (int k = 0; k < kQPT; ++k) {
-            num[k] += __shfl_xor_sync(0xffffffffu, num[k], off);
-            den[k] += __shfl_xor_sync(0xffffffffu, den[k], off);
-            d2min[k] = fmin(d2min[k], __shfl_xor_sync(0xffffffffu, d2min[k], off));
+            const int qi = min(q0 + k, n_q - 1);              // clamped: inactive queries compute garbage
+            x[k][0] = q[3 * (size_t)qi]; x[k][1] = q[3 * (size_t)qi + 1]; x[k][2] = q[3 * (size_t)qi + 2];
         }
-    }
-    if (sub >= kQPT) return;
-    // lane k of the group writes query k
-    double nk = num[0], dk = den[0], mk = d2min[0];
+        double num[kQPT], den[kQPT], d2min[kQPT];
 #pragma unroll
-    for (int k = 1; k < kQPT; ++k)
-        if (sub == k) { nk = num[k]; dk = den[k]; mk = d2min[k]; }
-    const int qi = q0 + sub;
-    if (qi >= n_q) return;
-    part[((size_t)e * n_chunks + c) * n_q + qi] = IdwPart{nk, dk, mk};
+        for (int k = 0; k < kQPT; ++k) {
+            num[k] = 0.0; den[k] = 0.0; d2min[k] = __longlong_as_double(0x7ff0000000000000LL);
+        }
+        for (int base = j0; base < j1; base += kTile) {
+            const int nt = min(kTile, j1 - base);
+            __syncthreads();
+            for (int t = threadIdx.x; t < nt; t += kThreads)
+                sp[t] = make_double4(P[3 * (size_t)(base + t)], P[3 * (size_t)(base + t) + 1],
+                                     P[3 * (size_t)(base + t) + 2], G[base + t]);
+            __syncthreads();
+#pragma unroll 2
+            for (int t = sub; t < nt; t += kSplit) {
+                const double4 r = sp[t];
+#pragma unroll
+                for (int k = 0; k < kQPT; ++k) {
+                    const double d2 = dist2_fast(x[k][0], x[k][1], x[k][2], r.x, r.y, r.z);
+                    d2min[k] = fmin(d2min[k], d2);
+                    const double w = p2 ? rcp_nr(d2) : pow(d2, hp);
+                    num[k] = fma(r.w, w, num[k]);
+                    den[k] += w;
+                }
+            }
+        }
+#pragma unroll
+        for (int off = kSplit / 2; off > 0; off >>= 1) {
+#pragma unroll
+            for (int k = 0; k < kQPT; ++k) {
+                num[k] += __shfl_xor_sync(0xffffffffu, num[k], off);
+                den[k] += __shfl_xor_sync(0xffffffffu, den[k], off);
+                d2min[k] = fmin(d2min[k], __shfl_xor_sync(0xffffffffu, d2min[k], off));
+            }
+        }
+        // lane k of the group writes query k
+        double nk = num[0], dk = den[0], mk = d2min[0];
+#pragma unroll
+        for (int k = 1; k < kQPT; ++k)
+            if (sub == k) { nk = num[k]; dk = den[k]; mk = d2min[k]; }
+        const int qi = q0 + sub;
+        if (sub < kQPT && qi < n_q) part[((size_t)e * n_chunks + c) * n_q + qi] = IdwPart{nk, dk, mk};
+    }
 }
 
 // Optional k-nearest Eq. 4 (reading Q22): one warp per (query, entry).  Every lane keeps the
@@ -239,22 +249,16 @@ __global__ void __launch_bounds__(256)
     v_out[(size_t)e * n_q + qi] = v;
 }
 
-// v_e(x) of entry e from its chunk partials (chunks in order), with the zero-distance rule
-// (Q23) decided exactly: if the nearest perspective may be closer than zero_eps (by the
-// contracted min d^2, with a 1e-6 relative margin), the entry is rescanned with the
-// correctly rounded d = sqrt(d^2) of the definition, and the lowest j attaining the
-// minimum gives v_e when that minimum is < zero_eps.
-__device__ double idw_entry_value(const IdwPart *part, int e, int n_chunks, int n_q, int qi, const double *xyz,
-                                  const double *gain, int32_t max_persp, const int32_t *meta, int32_t cap,
-                                  const double *q, double zero_eps)
+// v_e(x) of entry e from its chunk partials, with the zero-distance rule (Q23) decided
+// exactly: if the nearest perspective may be closer than zero_eps (by the contracted min d^2,
+// with a 1e-6 relative margin), the entry is rescanned with the correctly rounded d =
+// sqrt(d^2) of the definition, and the lowest j attaining the minimum gives v_e when that
+// minimum is < zero_eps.  Chunk sums are added in chunk order (one lane) so the value does
+// not depend on the launch shape beyond the chunking.
+__device__ double idw_entry_value(double num, double den, double d2m, int e, const double *xyz, const double *gain,
+                                  int32_t max_persp, const int32_t *meta, int32_t cap, const double *q, int qi,
+                                  double zero_eps)
 {
-    double num = 0.0, den = 0.0, d2m = __longlong_as_double(0x7ff0000000000000LL);
-    for (int c = 0; c < n_chunks; ++c) {
-        const IdwPart p = part[((size_t)e * n_chunks + c) * n_q + qi];
-        num += p.num;
-        den += p.den;
-        d2m = fmin(d2m, p.d2min);
-    }
     double v = num / den;
     const double lim = zero_eps * (1.0 + 1e-6);
     if (d2m < lim * lim) {
@@ -275,22 +279,48 @@ __device__ double idw_entry_value(const IdwPart *part, int e, int n_chunks, int 
     return v;
 }
 
+// Per-entry values of one query, one warp: lane e (< m) adds entry e's chunk partials in
+// order and applies the zero-distance rule; returns v_e on lane e.
+__device__ __forceinline__ double idw_chunked_entry_value(const IdwPart *part, int e, int n_chunks, int n_q, int qi,
+                                                          const double *xyz, const double *gain, int32_t max_persp,
+                                                          const int32_t *meta, int32_t cap, const double *q,
+                                                          double zero_eps)
+{
+    double num = 0.0, den = 0.0, d2m = __longlong_as_double(0x7ff0000000000000LL);
+    for (int c = 0; c < n_chunks; ++c) {
+        const IdwPart p = part[((size_t)e * n_chunks + c) * n_q + qi];
+        num += p.num;
+        den += p.den;
+        d2m = fmin(d2m, p.d2min);
+    }
+    return idw_entry_value(num, den, d2m, e, xyz, gain, max_persp, meta, cap, q, qi, zero_eps);
+}
+
+// One warp per query: the entries' values in parallel (lanes), then G = sum_u w_u v_u in entry
+// order on lane 0 (optionally / sum_u w_u).  cap <= 32 (nbt_idbuf_create allows 64: larger
+// rings loop over lanes).
 __global__ void k_idw_combine(const IdwPart *__restrict__ part, int32_t n_chunks, const double *__restrict__ xyz,
                               const double *__restrict__ gain, int32_t max_persp, const int32_t *__restrict__ meta,
                               int32_t cap, const double *__restrict__ q, int32_t n_q, double zero_eps,
                               int32_t normalize, double *__restrict__ out)
 {
-    const int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int qi = (int)(((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (qi >= n_q) return;
     const int m = min(meta[0], cap);
     double g = 0.0, wsum = 0.0;
-    for (int e = 0; e < m; ++e) {
-        const double wu = __ddiv_rn(1.0, (double)(m - e));
-        const double v = idw_entry_value(part, e, n_chunks, n_q, qi, xyz, gain, max_persp, meta, cap, q, zero_eps);
-        g = __dadd_rn(g, __dmul_rn(wu, v));
-        wsum = __dadd_rn(wsum, wu);
+    for (int e0 = 0; e0 < m; e0 += 32) {
+        const double v = e0 + lane < m ? idw_chunked_entry_value(part, e0 + lane, n_chunks, n_q, qi, xyz, gain,
+                                                                 max_persp, meta, cap, q, zero_eps)
+                                       : 0.0;
+        for (int e = e0; e < min(m, e0 + 32); ++e) {
+            const double ve = __shfl_sync(0xffffffffu, v, e - e0);
+            const double wu = __ddiv_rn(1.0, (double)(m - e));
+            g = __dadd_rn(g, __dmul_rn(wu, ve));
+            wsum = __dadd_rn(wsum, wu);
+        }
     }
-    out[qi] = normalize ? __ddiv_rn(g, wsum) : g;
+    if (lane == 0) out[qi] = normalize ? __ddiv_rn(g, wsum) : g;
 }
 
 // Combine of per-entry values (the k-nearest path writes v_e directly).
@@ -326,7 +356,8 @@ __global__ void k_info_cost(const IdwPart *__restrict__ part, int32_t n_chunks, 
         double g = 0.0, wsum = 0.0;
         for (int e = 0; e < m; ++e) {
             const double wu = __ddiv_rn(1.0, (double)(m - e));
-            const double v = idw_entry_value(part, e, n_chunks, n_q, i, xyz, gain, max_persp, meta, cap, a.pos, zero_eps);
+            const double v = idw_chunked_entry_value(part, e, n_chunks, n_q, i, xyz, gain, max_persp, meta, cap, a.pos,
+                                                     zero_eps);
             g = __dadd_rn(g, __dmul_rn(wu, v));
             wsum = __dadd_rn(wsum, wu);
         }
@@ -393,17 +424,35 @@ __global__ void __launch_bounds__(kPushOneBlock) k_idbuf_push_small(int32_t *met
 }
 
 #ifndef NBT_IDW_MIN_BLOCKS
-#define NBT_IDW_MIN_BLOCKS 4      // target resident blocks per SM the chunking aims to fill (x waves)
+#define NBT_IDW_MIN_BLOCKS 4      // units per resident block slot the chunking aims for (balance of the persistent grid)
 #endif
 #ifndef NBT_IDW_CHUNK_MIN
 #define NBT_IDW_CHUNK_MIN 64
 #endif
 // Perspective chunk per block: enough (query block, entry, chunk) blocks for ~NBT_IDW_MIN_BLOCKS
 // per SM, chunks a multiple of 32 and at least NBT_IDW_CHUNK_MIN perspectives.
+int idw_blocks_per_sm()
+{
+    static int bps = [] {
+        int v = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_idw_entry, kThreads, 0);
+        return v > 0 ? v : 1;
+    }();
+    return bps;
+}
+
+// Persistent grid of the entry kernel: every resident block slot, at most one per unit.
+int idw_grid(nbt_ctx ctx, const nbt_idbuf_s *b, int32_t n_q, int32_t n_chunks)
+{
+    const long long units = (long long)((n_q + kQueries - 1) / kQueries) * b->capacity * n_chunks;
+    const long long slots = (long long)ctx->num_sms * idw_blocks_per_sm();
+    return (int)(units < slots ? units : slots);
+}
+
 void idw_chunks(nbt_ctx ctx, const nbt_idbuf_s *b, int32_t n_q, int32_t &chunk, int32_t &n_chunks)
 {
     const long long base = (long long)((n_q + kQueries - 1) / kQueries) * b->capacity;
-    const long long want = (long long)ctx->num_sms * NBT_IDW_MIN_BLOCKS;
+    const long long want = (long long)ctx->num_sms * idw_blocks_per_sm() * NBT_IDW_MIN_BLOCKS;
     long long s = (want + base - 1) / base;
     long long c = ((long long)b->max_persp + s - 1) / s;
     c = (c + 31) / 32 * 32;
@@ -441,9 +490,8 @@ nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const InfoCostArg
     if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_chunks * n_q * sizeof(IdwPart)))) return st;
     ProfScope ps(ctx, NBT_KERNEL_IDW);
     IdwPart *part = ctx->idw_tmp.as<IdwPart>();
-    dim3 grid((n_q + kQueries - 1) / kQueries, b->capacity, n_chunks);
-    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, a.pos,
-                                                     n_q, power_p, chunk, part);
+    k_idw_entry<<<idw_grid(ctx, b, n_q, n_chunks), kThreads, 0, ctx->stream>>>(
+        b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, a.pos, n_q, power_p, chunk, n_chunks, part);
     NBT_LAUNCHED(ctx);
     k_info_cost<<<(a.n_traj + 63) / 64, 64, 0, ctx->stream>>>(part, n_chunks, b->d_xyz, b->d_gain, b->max_persp,
                                                               b->d_meta, b->capacity, zero_eps, a, normalize,
@@ -474,11 +522,10 @@ nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const double *d_q, int3
     idw_chunks(ctx, b, n_q, chunk, n_chunks);
     if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_chunks * n_q * sizeof(IdwPart)))) return st;
     IdwPart *part = ctx->idw_tmp.as<IdwPart>();
-    dim3 grid((n_q + kQueries - 1) / kQueries, b->capacity, n_chunks);
-    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, d_q,
-                                                     n_q, power_p, chunk, part);
+    k_idw_entry<<<idw_grid(ctx, b, n_q, n_chunks), kThreads, 0, ctx->stream>>>(
+        b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, d_q, n_q, power_p, chunk, n_chunks, part);
     NBT_LAUNCHED(ctx);
-    k_idw_combine<<<(n_q + 127) / 128, 128, 0, ctx->stream>>>(part, n_chunks, b->d_xyz, b->d_gain, b->max_persp,
+    k_idw_combine<<<(unsigned)(((size_t)n_q * 32 + 255) / 256), 256, 0, ctx->stream>>>(part, n_chunks, b->d_xyz, b->d_gain, b->max_persp,
                                                                b->d_meta, b->capacity, d_q, n_q, zero_eps, normalize,
                                                                d_out);
     NBT_LAUNCHED(ctx);
