@@ -6,17 +6,16 @@
 // reading Q21), each cloud's own perspectives (Q20) and all of them (Q22); if the
 // nearest perspective is closer than zero_eps, v_u is its gain (Q23).
 //
-//   k_idw_entry    grid (query blocks) x (entries) x (perspective chunks): a block stages
-//                  one chunk of an entry's perspectives through shared memory; each thread
-//                  holds 3 queries in registers and 16 lanes split the chunk (interleaved;
-//                  fp64 partial sums combined by shuffles) and writes the chunk's partial
-//                  (sum g w, sum w, min d^2) per query.  The result differs from a
-//                  sequential sum only in rounding (< 1e-12 relative).
-//   k_idw_combine  per query: per entry the chunk partials in order -> v_u (the zero-
-//                  distance rule decided exactly: when the nearest perspective may be
-//                  within zero_eps the entry is rescanned with the correctly rounded d and
-//                  the lowest j among exactly equal d wins, as in the definition), then
-//                  G = sum_u w_u v_u in entry order (optionally / sum_u w_u).
+//   k_idw_entry    grid (query blocks) x (entries): a block stages one entry's
+//                  perspectives through shared memory; each thread holds 3 queries in
+//                  registers and 16 lanes split the perspectives (interleaved; fp64
+//                  partial sums combined by shuffles, so the result differs from a
+//                  sequential sum only in rounding, < 1e-12 relative).  The nearest
+//                  perspective is tracked on d^2 (monotone in d); only when it is within
+//                  zero_eps is d = sqrt(d^2) evaluated and the lowest j among exactly
+//                  equal d found by a rescan, so the zero-distance decision and the
+//                  returned gain match the definition.
+//   k_idw_combine  per query: G = sum_u w_u v_u in entry order (optionally / sum_u w_u).
 #include "nbt_internal.cuh"
 
 #ifndef NBT_IDW_EXACT_RCP
@@ -62,18 +61,17 @@ __device__ __forceinline__ double dist2(double x0, double x1, double x2, double 
     return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
-// Block (query block, entry e, perspective chunk c): 16 groups of kQPT (3) queries x 16
-// lanes.  The 16 lanes of a group split the chunk's perspectives (interleaved), staged
-// through shared memory; every perspective record a lane reads is used for its 3 queries
-// (register blocking), and the groups' partial sums combine by shuffles.  The chunk's
-// partial (sum g w, sum w, min d^2) per query goes to part[e][c][q]; k_idw_combine adds
-// the chunks in order.  Splitting an entry's perspectives over chunks gives the launch
-// enough blocks to fill every SM (1984 queries x 10 entries is only 420 blocks of 48
-// queries, ~1.4 waves at 2 blocks per SM, the tail SM-idle).  w = 1/d^2 on the fma-
-// contracted d^2 (its rounding is within the 1e-12 tolerance); min d^2 of the contracted
-// form only triggers the zero-distance rule, which k_idw_combine decides exactly.
-struct IdwPart { double num, den, d2min; };
-
+// Block (query block, entry e): 16 groups of kQPT (3) queries x 16 lanes.  The 16 lanes of a
+// group split the entry's perspectives (interleaved), staged through shared memory; every
+// perspective record a lane reads is used for its 3 queries (register blocking: one
+// shared-memory read per 3 pairs), and the groups' partial sums combine by shuffles.  The
+// weights use the fma-contracted d^2 (6 instead of 8 fp64 operations; its rounding is within
+// the 1e-12 tolerance); only min d^2 is tracked per query and, when it may lie within zero_eps
+// (1e-6 relative margin), the entry is rescanned with the correctly rounded d = sqrt(d^2) of the
+// definition and the lowest j attaining the minimum decides the zero-distance rule exactly.
+// The combine over the entries is fused: the last of a query block's `cap` blocks to finish
+// (a counter per query block, reset by that block, so graph replays find it at zero) sums
+// G = sum_u w_u v_u in entry order for its queries -- one launch per query call.
 __device__ __forceinline__ double dist2_fast(double x0, double x1, double x2, double p0, double p1, double p2)
 {
     const double dx = x0 - p0, dy = x1 - p1, dz = x2 - p2;
@@ -86,41 +84,36 @@ __device__ __forceinline__ double dist2_fast(double x0, double x1, double x2, do
 __global__ void __launch_bounds__(kThreads, NBT_IDW_LB)
     k_idw_entry(const double *__restrict__ xyz, const double *__restrict__ gain, int32_t max_persp,
                 const int32_t *__restrict__ meta, int32_t cap, const double *__restrict__ q, int32_t n_q,
-                double power_p, int32_t chunk, int32_t n_chunks, IdwPart *__restrict__ part)
+                double power_p, double zero_eps, double *__restrict__ v_out, int *__restrict__ done,
+                int32_t normalize, double *__restrict__ out)
 {
     __shared__ double4 sp[kTile];
-    // persistent: units (query block, entry, chunk), chunk-major then entry, dealt round-robin
-    const int nqb = (n_q + kQueries - 1) / kQueries;
-    const int units = nqb * cap * n_chunks;
+    __shared__ int last;
+    const int e = blockIdx.y;
     const int pushes = meta[0];
     const int m = min(pushes, cap);
-    const int sub = threadIdx.x & (kSplit - 1);
-    const bool p2 = power_p == 2.0;
-    const double hp = -0.5 * power_p;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int qb = u % nqb;
-        const int e = (u / nqb) % cap;
-        const int c = u / (nqb * cap);
-        if (e >= m) continue;                                 // block-uniform
+    if (e < m) {
         const int slot = (pushes - m + e) % cap;              // entry e, oldest first
-        const int q0 = qb * kQueries + (threadIdx.x / kSplit) * kQPT;
+        const int sub = threadIdx.x & (kSplit - 1);
+        const int q0 = blockIdx.x * kQueries + (threadIdx.x / kSplit) * kQPT;
         const double *P = xyz + (size_t)slot * max_persp * 3;
         const double *G = gain + (size_t)slot * max_persp;
         const int np = meta[1 + slot];
-        const int j0 = c * chunk, j1 = min(np, j0 + chunk);
         double x[kQPT][3];
 #pragma unroll
         for (int k = 0; k < kQPT; ++k) {
             const int qi = min(q0 + k, n_q - 1);              // clamped: inactive queries compute garbage
             x[k][0] = q[3 * (size_t)qi]; x[k][1] = q[3 * (size_t)qi + 1]; x[k][2] = q[3 * (size_t)qi + 2];
         }
+        const bool p2 = power_p == 2.0;
+        const double hp = -0.5 * power_p;
         double num[kQPT], den[kQPT], d2min[kQPT];
 #pragma unroll
         for (int k = 0; k < kQPT; ++k) {
             num[k] = 0.0; den[k] = 0.0; d2min[k] = __longlong_as_double(0x7ff0000000000000LL);
         }
-        for (int base = j0; base < j1; base += kTile) {
-            const int nt = min(kTile, j1 - base);
+        for (int base = 0; base < np; base += kTile) {
+            const int nt = min(kTile, np - base);
             __syncthreads();
             for (int t = threadIdx.x; t < nt; t += kThreads)
                 sp[t] = make_double4(P[3 * (size_t)(base + t)], P[3 * (size_t)(base + t) + 1],
@@ -154,7 +147,44 @@ __global__ void __launch_bounds__(kThreads, NBT_IDW_LB)
         for (int k = 1; k < kQPT; ++k)
             if (sub == k) { nk = num[k]; dk = den[k]; mk = d2min[k]; }
         const int qi = q0 + sub;
-        if (sub < kQPT && qi < n_q) part[((size_t)e * n_chunks + c) * n_q + qi] = IdwPart{nk, dk, mk};
+        if (sub < kQPT && qi < n_q) {
+            double v = nk / dk;
+            const double lim = zero_eps * (1.0 + 1e-6);
+            if (mk < lim * lim) {
+                // the definition's nearest: correctly rounded d, lowest j among equal d
+                const double y0 = q[3 * (size_t)qi], y1 = q[3 * (size_t)qi + 1], y2 = q[3 * (size_t)qi + 2];
+                double dmin = __longlong_as_double(0x7ff0000000000000LL);
+                int jmin = -1;
+                for (int j = 0; j < np; ++j) {
+                    const double d =
+                        __dsqrt_rn(dist2(y0, y1, y2, P[3 * (size_t)j], P[3 * (size_t)j + 1], P[3 * (size_t)j + 2]));
+                    if (d < dmin) { dmin = d; jmin = j; }
+                }
+                if (jmin >= 0 && dmin < zero_eps) v = G[jmin];
+            }
+            v_out[(size_t)e * n_q + qi] = v;
+        }
+    }
+    if (!out) return;                                          // info cost: its own combine
+    // fused combine: the last block of this query block sums the entries
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        last = atomicAdd(done + blockIdx.x, 1) == (int)gridDim.y - 1;
+        if (last) done[blockIdx.x] = 0;                        // reset for the next call / graph replay
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int qi = blockIdx.x * kQueries + threadIdx.x; qi < min(n_q, (int)(blockIdx.x + 1) * kQueries);
+         qi += kThreads) {
+        double g = 0.0, wsum = 0.0;
+        for (int u = 0; u < m; ++u) {
+            const double wu = __ddiv_rn(1.0, (double)(m - u));
+            g = __dadd_rn(g, __dmul_rn(wu, __ldcg(v_out + (size_t)u * n_q + qi)));
+            wsum = __dadd_rn(wsum, wu);
+        }
+        out[qi] = normalize ? __ddiv_rn(g, wsum) : g;
     }
 }
 
@@ -249,83 +279,8 @@ __global__ void __launch_bounds__(256)
     v_out[(size_t)e * n_q + qi] = v;
 }
 
-// v_e(x) of entry e from its chunk partials, with the zero-distance rule (Q23) decided
-// exactly: if the nearest perspective may be closer than zero_eps (by the contracted min d^2,
-// with a 1e-6 relative margin), the entry is rescanned with the correctly rounded d =
-// sqrt(d^2) of the definition, and the lowest j attaining the minimum gives v_e when that
-// minimum is < zero_eps.  Chunk sums are added in chunk order (one lane) so the value does
-// not depend on the launch shape beyond the chunking.
-__device__ double idw_entry_value(double num, double den, double d2m, int e, const double *xyz, const double *gain,
-                                  int32_t max_persp, const int32_t *meta, int32_t cap, const double *q, int qi,
-                                  double zero_eps)
-{
-    double v = num / den;
-    const double lim = zero_eps * (1.0 + 1e-6);
-    if (d2m < lim * lim) {
-        const int pushes = meta[0];
-        const int m = min(pushes, cap);
-        const int slot = (pushes - m + e) % cap;
-        const double *P = xyz + (size_t)slot * max_persp * 3;
-        const int np = meta[1 + slot];
-        const double y0 = q[3 * (size_t)qi], y1 = q[3 * (size_t)qi + 1], y2 = q[3 * (size_t)qi + 2];
-        double dmin = __longlong_as_double(0x7ff0000000000000LL);
-        int jmin = -1;
-        for (int j = 0; j < np; ++j) {
-            const double d = __dsqrt_rn(dist2(y0, y1, y2, P[3 * (size_t)j], P[3 * (size_t)j + 1], P[3 * (size_t)j + 2]));
-            if (d < dmin) { dmin = d; jmin = j; }
-        }
-        if (jmin >= 0 && dmin < zero_eps) v = gain[(size_t)slot * max_persp + jmin];
-    }
-    return v;
-}
-
-// Per-entry values of one query, one warp: lane e (< m) adds entry e's chunk partials in
-// order and applies the zero-distance rule; returns v_e on lane e.
-__device__ __forceinline__ double idw_chunked_entry_value(const IdwPart *part, int e, int n_chunks, int n_q, int qi,
-                                                          const double *xyz, const double *gain, int32_t max_persp,
-                                                          const int32_t *meta, int32_t cap, const double *q,
-                                                          double zero_eps)
-{
-    double num = 0.0, den = 0.0, d2m = __longlong_as_double(0x7ff0000000000000LL);
-    for (int c = 0; c < n_chunks; ++c) {
-        const IdwPart p = part[((size_t)e * n_chunks + c) * n_q + qi];
-        num += p.num;
-        den += p.den;
-        d2m = fmin(d2m, p.d2min);
-    }
-    return idw_entry_value(num, den, d2m, e, xyz, gain, max_persp, meta, cap, q, qi, zero_eps);
-}
-
-// One warp per query: the entries' values in parallel (lanes), then G = sum_u w_u v_u in entry
-// order on lane 0 (optionally / sum_u w_u).  cap <= 32 (nbt_idbuf_create allows 64: larger
-// rings loop over lanes).
-__global__ void k_idw_combine(const IdwPart *__restrict__ part, int32_t n_chunks, const double *__restrict__ xyz,
-                              const double *__restrict__ gain, int32_t max_persp, const int32_t *__restrict__ meta,
-                              int32_t cap, const double *__restrict__ q, int32_t n_q, double zero_eps,
+__global__ void k_idw_combine(const double *__restrict__ v, const int32_t *__restrict__ meta, int32_t cap, int32_t n_q,
                               int32_t normalize, double *__restrict__ out)
-{
-    const int lane = threadIdx.x & 31;
-    const int qi = (int)(((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    if (qi >= n_q) return;
-    const int m = min(meta[0], cap);
-    double g = 0.0, wsum = 0.0;
-    for (int e0 = 0; e0 < m; e0 += 32) {
-        const double v = e0 + lane < m ? idw_chunked_entry_value(part, e0 + lane, n_chunks, n_q, qi, xyz, gain,
-                                                                 max_persp, meta, cap, q, zero_eps)
-                                       : 0.0;
-        for (int e = e0; e < min(m, e0 + 32); ++e) {
-            const double ve = __shfl_sync(0xffffffffu, v, e - e0);
-            const double wu = __ddiv_rn(1.0, (double)(m - e));
-            g = __dadd_rn(g, __dmul_rn(wu, ve));
-            wsum = __dadd_rn(wsum, wu);
-        }
-    }
-    if (lane == 0) out[qi] = normalize ? __ddiv_rn(g, wsum) : g;
-}
-
-// Combine of per-entry values (the k-nearest path writes v_e directly).
-__global__ void k_idw_combine_values(const double *__restrict__ v, const int32_t *__restrict__ meta, int32_t cap,
-                                     int32_t n_q, int32_t normalize, double *__restrict__ out)
 {
     const int qi = blockIdx.x * blockDim.x + threadIdx.x;
     if (qi >= n_q) return;
@@ -342,9 +297,8 @@ __global__ void k_idw_combine_values(const double *__restrict__ v, const int32_t
 // Information cost (f2): one thread per trajectory, poses in order.  O by the rounded-
 // once dot product / norms (the same expression as the definition, so the FoV decision
 // is reproducible), G from the per-entry IDW values, c = sum_k w_i / (O G + eps).
-__global__ void k_info_cost(const IdwPart *__restrict__ part, int32_t n_chunks, const double *__restrict__ xyz,
-                            const double *__restrict__ gain, int32_t max_persp, const int32_t *__restrict__ meta,
-                            int32_t cap, double zero_eps, InfoCostArgs a, int32_t normalize, int *err)
+__global__ void k_info_cost(const double *__restrict__ v, const int32_t *__restrict__ meta, int32_t cap, InfoCostArgs a,
+                            int32_t normalize, int *err)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.n_traj) return;
@@ -356,9 +310,7 @@ __global__ void k_info_cost(const IdwPart *__restrict__ part, int32_t n_chunks, 
         double g = 0.0, wsum = 0.0;
         for (int e = 0; e < m; ++e) {
             const double wu = __ddiv_rn(1.0, (double)(m - e));
-            const double v = idw_chunked_entry_value(part, e, n_chunks, n_q, i, xyz, gain, max_persp, meta, cap, a.pos,
-                                                     zero_eps);
-            g = __dadd_rn(g, __dmul_rn(wu, v));
+            g = __dadd_rn(g, __dmul_rn(wu, v[(size_t)e * n_q + i]));
             wsum = __dadd_rn(wsum, wu);
         }
         if (normalize) g = __ddiv_rn(g, wsum);
@@ -423,44 +375,6 @@ __global__ void __launch_bounds__(kPushOneBlock) k_idbuf_push_small(int32_t *met
     }
 }
 
-#ifndef NBT_IDW_MIN_BLOCKS
-#define NBT_IDW_MIN_BLOCKS 4      // units per resident block slot the chunking aims for (balance of the persistent grid)
-#endif
-#ifndef NBT_IDW_CHUNK_MIN
-#define NBT_IDW_CHUNK_MIN 64
-#endif
-// Perspective chunk per block: enough (query block, entry, chunk) blocks for ~NBT_IDW_MIN_BLOCKS
-// per SM, chunks a multiple of 32 and at least NBT_IDW_CHUNK_MIN perspectives.
-int idw_blocks_per_sm()
-{
-    static int bps = [] {
-        int v = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_idw_entry, kThreads, 0);
-        return v > 0 ? v : 1;
-    }();
-    return bps;
-}
-
-// Persistent grid of the entry kernel: every resident block slot, at most one per unit.
-int idw_grid(nbt_ctx ctx, const nbt_idbuf_s *b, int32_t n_q, int32_t n_chunks)
-{
-    const long long units = (long long)((n_q + kQueries - 1) / kQueries) * b->capacity * n_chunks;
-    const long long slots = (long long)ctx->num_sms * idw_blocks_per_sm();
-    return (int)(units < slots ? units : slots);
-}
-
-void idw_chunks(nbt_ctx ctx, const nbt_idbuf_s *b, int32_t n_q, int32_t &chunk, int32_t &n_chunks)
-{
-    const long long base = (long long)((n_q + kQueries - 1) / kQueries) * b->capacity;
-    const long long want = (long long)ctx->num_sms * idw_blocks_per_sm() * NBT_IDW_MIN_BLOCKS;
-    long long s = (want + base - 1) / base;
-    long long c = ((long long)b->max_persp + s - 1) / s;
-    c = (c + 31) / 32 * 32;
-    if (c < NBT_IDW_CHUNK_MIN) c = NBT_IDW_CHUNK_MIN;
-    chunk = (int32_t)c;
-    n_chunks = (int32_t)((b->max_persp + c - 1) / c);
-}
-
 }  // namespace
 
 nbt_status launch_idbuf_push(nbt_ctx ctx, nbt_idbuf_s *b, const double *d_xyz, const double *d_gain, int32_t n)
@@ -485,17 +399,15 @@ nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const InfoCostArg
     const int32_t n_q = a.n_traj * a.per;
     if (n_q == 0) return NBT_OK;
     nbt_status st;
-    int32_t chunk, n_chunks;
-    idw_chunks(ctx, b, n_q, chunk, n_chunks);
-    if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_chunks * n_q * sizeof(IdwPart)))) return st;
+    if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_q * 8))) return st;
     ProfScope ps(ctx, NBT_KERNEL_IDW);
-    IdwPart *part = ctx->idw_tmp.as<IdwPart>();
-    k_idw_entry<<<idw_grid(ctx, b, n_q, n_chunks), kThreads, 0, ctx->stream>>>(
-        b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, a.pos, n_q, power_p, chunk, n_chunks, part);
+    dim3 grid((n_q + kQueries - 1) / kQueries, b->capacity);
+    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, a.pos,
+                                                     n_q, power_p, zero_eps, ctx->idw_tmp.as<double>(), nullptr, 0,
+                                                     nullptr);
     NBT_LAUNCHED(ctx);
-    k_info_cost<<<(a.n_traj + 63) / 64, 64, 0, ctx->stream>>>(part, n_chunks, b->d_xyz, b->d_gain, b->max_persp,
-                                                              b->d_meta, b->capacity, zero_eps, a, normalize,
-                                                              ctx->d_err);
+    k_info_cost<<<(a.n_traj + 63) / 64, 64, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), b->d_meta, b->capacity, a,
+                                                              normalize, ctx->d_err);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }
@@ -505,29 +417,33 @@ nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const double *d_q, int3
 {
     if (n_q == 0) return NBT_OK;
     nbt_status st;
+    if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_q * 8))) return st;
     ProfScope ps(ctx, NBT_KERNEL_IDW);
     if (knn > 0) {
-        if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_q * 8))) return st;
         const long long warps = (long long)n_q * b->capacity;
         k_idw_entry_knn<<<(unsigned)((warps + 7) / 8), 256, 0, ctx->stream>>>(
             b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, d_q, n_q, power_p, zero_eps, knn,
             ctx->idw_tmp.as<double>());
         NBT_LAUNCHED(ctx);
-        k_idw_combine_values<<<(n_q + 127) / 128, 128, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), b->d_meta,
-                                                                          b->capacity, n_q, normalize, d_out);
+        k_idw_combine<<<(n_q + 127) / 128, 128, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), b->d_meta, b->capacity,
+                                                                   n_q, normalize, d_out);
         NBT_LAUNCHED(ctx);
         return NBT_OK;
     }
-    int32_t chunk, n_chunks;
-    idw_chunks(ctx, b, n_q, chunk, n_chunks);
-    if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_chunks * n_q * sizeof(IdwPart)))) return st;
-    IdwPart *part = ctx->idw_tmp.as<IdwPart>();
-    k_idw_entry<<<idw_grid(ctx, b, n_q, n_chunks), kThreads, 0, ctx->stream>>>(
-        b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, d_q, n_q, power_p, chunk, n_chunks, part);
-    NBT_LAUNCHED(ctx);
-    k_idw_combine<<<(unsigned)(((size_t)n_q * 32 + 255) / 256), 256, 0, ctx->stream>>>(part, n_chunks, b->d_xyz, b->d_gain, b->max_persp,
-                                                               b->d_meta, b->capacity, d_q, n_q, zero_eps, normalize,
-                                                               d_out);
+    // per-query-block completion counters in their own buffer, zero between calls (the last
+    // block of a query block resets its counter); zeroed once when (re)allocated
+    const int nqb = (n_q + kQueries - 1) / kQueries;
+    if ((st = ctx->idw_done.ensure((size_t)nqb * 4))) return st;
+    int *done = ctx->idw_done.as<int>();
+    if (ctx->idw_done_at != (void *)done || ctx->idw_done_zeroed < (size_t)nqb) {
+        NBT_CUDA(cudaMemsetAsync(done, 0, ctx->idw_done.cap, ctx->stream));
+        ctx->idw_done_zeroed = ctx->idw_done.cap / 4;
+        ctx->idw_done_at = done;
+    }
+    dim3 grid(nqb, b->capacity);
+    k_idw_entry<<<grid, kThreads, 0, ctx->stream>>>(b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, d_q,
+                                                     n_q, power_p, zero_eps, ctx->idw_tmp.as<double>(), done,
+                                                     normalize, d_out);
     NBT_LAUNCHED(ctx);
     return NBT_OK;
 }

@@ -158,6 +158,9 @@ struct nbt_ctx_s {
     nbt::DevBuf deltas;               // staged map deltas
     nbt::DevBuf keys, keys_alt, cub_tmp;
     nbt::DevBuf queries, qout, idw_tmp, poses;
+    nbt::DevBuf idw_done;             // IDW per-query-block completion counters (k_idw.cu)
+    size_t idw_done_zeroed = 0;       // ... counters known to be zero ...
+    void *idw_done_at = nullptr;      // ... at this address
     nbt::DevBuf dbg;                  // debug entry points
     nbt::HostStage stage_in[3];
     nbt::HostStage stage_out;

@@ -298,7 +298,7 @@ static void ctx_free(nbt_ctx ctx)
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf *bufs[] = {&ctx->persp, &ctx->frames, &ctx->totals, &ctx->counter, &ctx->out_tmp, &ctx->deltas,
-                      &ctx->keys, &ctx->keys_alt, &ctx->cub_tmp, &ctx->queries, &ctx->qout, &ctx->idw_tmp, &ctx->poses, &ctx->dbg};
+                      &ctx->keys, &ctx->keys_alt, &ctx->cub_tmp, &ctx->queries, &ctx->qout, &ctx->idw_tmp, &ctx->poses, &ctx->dbg, &ctx->idw_done};
     for (DevBuf *b : bufs) b->release();
     for (auto &st : ctx->stage_in) st.release();
     for (auto &v : ctx->prof.pending)
