@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--north-star-reps", type=int, default=20)
     ap.add_argument("--no-config-b", action="store_true")
     ap.add_argument("--no-integrate", action="store_true", help="skip the row-f3 map-integration block")
+    ap.add_argument("--no-config-e", action="store_true", help="skip the config-E receding-horizon block")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--gather", choices=["nccl", "p2p"], default="nccl",
@@ -946,6 +947,22 @@ def main_ours(args, cfg):
     integ = None
     if not args.no_integrate and rank == 0:
         integ = run_integration(nbt, ctx, stream, dev, flush)
+    cfg_e = None
+    if not args.no_config_e and rank == 0:
+        # BASELINE configs[4]: the receding-horizon loop (tools/config_e.py; its oracle parity is
+        # tests/test_gpu_parity.py::test_config_e_loop), per-cycle latency percentiles
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import config_e
+        dev_ms_e, wall_ms_e = config_e.run_loop(200)
+        torch.cuda.set_stream(stream)
+        cfg_e = {"config": "E: 256^3 SYN map, 512 perspectives x 64x48 rays per cycle, moving PoI, map deltas, "
+                           "N_B=10, 1984 IDW queries per cycle", "cycles": 200,
+                 "device_ms_p50": float(np.percentile(dev_ms_e[1:], 50)),
+                 "device_ms_p99": float(np.percentile(dev_ms_e[1:], 99)),
+                 "wall_ms_p50": float(np.percentile(wall_ms_e[1:], 50)),
+                 "wall_ms_p99": float(np.percentile(wall_ms_e[1:], 99)),
+                 "note": "per cycle: host-side delta generation outside the timing; device events and host wall "
+                         "clock around update + sample + ID + push + IDW, one sync per cycle"}
     if world > 1:
         dist.barrier()
 
@@ -972,6 +989,7 @@ def main_ours(args, cfg):
             "north_star": north,
             "config_b": cfg_b,
             "map_integration": integ,
+            "config_e": cfg_e,
             "gpu_launches": head["gpu_launches"],
             "clocks": head["clocks"],
             "e2e": head["e2e"],
