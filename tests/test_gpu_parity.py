@@ -1134,15 +1134,15 @@ def test_idw_knn_matches_oracle(nbt, ctx, knn, power_p):
         buf.query(q, knn=17)
 
 
-@pytest.mark.parametrize("name,sampled", [("C'", 3), ("D", 5)])
-def test_full_size_north_star_and_d_sampled(nbt, ctx, name, sampled):
+@pytest.mark.parametrize("name,sampled,bits", [("C'", 3, 2), ("C'", 3, 8), ("D", 5, 2)])
+def test_full_size_north_star_and_d_sampled(nbt, ctx, name, sampled, bits):
     """The north-star config C' (512 x 640x480 on 256^3) and config D (4096 x 160x120 on
     512^3) computed whole, in bench.py's launch shape, with sampled perspectives recomputed
     one by one by the oracle: per-state totals and g_P bit-exact."""
     import torch
     cfg = CONFIGS[name]
     codes = cfg.map_codes()
-    m, om = make_map(nbt, ctx, codes, cfg.voxel_size)
+    m, om = make_map(nbt, ctx, codes, cfg.voxel_size, bits=bits)
     P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)
     cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
     out = nbt.empty_cloud(cfg.n_persp, device="cuda")
@@ -1156,6 +1156,30 @@ def test_full_size_north_star_and_d_sampled(nbt, ctx, name, sampled):
     _, g, c = oracle.id_compute(om, cfg.poi, P[idx], ocam, cfg.range_, nthreads=NTHREADS)
     assert np.array_equal(counts[idx].astype(np.int64), c)
     assert np.array_equal(gain[idx], g)
+
+
+@pytest.mark.parametrize("name,bits,sampled", [("C'", 8, 2), ("D", 2, 5)])
+def test_full_size_per_ray_production_trace(nbt, ctx, name, bits, sampled):
+    """The production trace kernel at bench.py's full launch (all 512 x 640x480 rays of C' on
+    the byte store the bench's C' block uses; all 4096 x 160x120 rays of D on the 2-bit store),
+    in its record instance: every ray of sampled perspectives -- (n_U, n_F, n_O, lookups, stop)
+    -- equals the oracle's, and every perspective's recorded rays sum to the production
+    kernel's totals."""
+    import torch
+    cfg = CONFIGS[name]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size, bits=bits)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    rays = nbt.debug_id_rays(ctx, m, cfg.poi, P, cam, cfg.range_)
+    out = nbt.empty_cloud(cfg.n_persp, device="cuda")
+    nbt.id_compute(ctx, m, cfg.poi, torch.from_numpy(P).cuda(), cam, cfg.range_, out=out)
+    ctx.sync()
+    assert np.array_equal(rays[:, :, :4].sum(1, dtype=np.int64), out.counts.cpu().numpy())
+    for j in np.linspace(0, cfg.n_persp - 1, sampled).astype(int):
+        _, _, want = oracle.perspective_rays(om, cfg.poi, P[j], ocam, cfg.range_)
+        assert np.array_equal(rays[j].astype(np.int64), want), j
+    del rays
 
 
 def test_ctx_options_roundtrip_and_range(nbt, ctx):
