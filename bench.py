@@ -978,7 +978,8 @@ def main_ours(args, cfg):
                        "parallelism": (f"perspective j on rank j mod {world} (strong scaling)" if mode == "strong"
                                        else f"every rank its own perspective set (weak scaling)")
                        + ("" if world == 1 else (", IG-cloud all-gather fused into the finalize (peer memory)"
-                                                 if args.gather == "p2p" else ", IG-cloud all-gather over NCCL"))},
+                                                 if args.gather == "p2p" else
+                                                 f", IG-cloud all-gather over {dist.get_backend().upper()}"))},
             "voxel_steps_per_s": head["voxel_steps_per_s"], "lookups_per_s": head["lookups_per_s"],
             "id_latency_ms": head["ms_per_step"], "ms_per_step_p50": head["ms_per_step_p50"],
             "roofline": head["roofline"],
