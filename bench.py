@@ -893,15 +893,36 @@ def run_cprime(args, nbt, ctx, stream, dev, flush, pk, reps):
         buf.query(hq, power_p=POWER_P, out=hq_out)
         if t >= 2:
             e2e_t.append(1e3 * (time.perf_counter() - t0))
+    # BASELINE configs[2] (config C: 256 perspectives at 640x480 on the same map), same cycle
+    cc = CONFIGS["C"]
+    persp_c = persp[:cc.n_persp]
+    cloud_c = nbt.empty_cloud(cc.n_persp, device=dev)
+    times_c = []
+    for t in range(reps + 1):
+        flush.fill_(t & 0xFF)
+        e0.record(stream)
+        nbt.sample_perspectives(ctx, cc.poi, cc.persp_radius, cc.n_persp, cc.persp_seed + t, cc.persp_mode,
+                                out=persp_c)
+        nbt.id_compute(ctx, m, cc.poi, persp_c, cam, cc.range_, out=cloud_c)
+        buf.push(cloud_c, cc.n_persp)
+        buf.query(q_dev, power_p=POWER_P, out=q_out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if t > 0:
+            times_c.append(e0.elapsed_time(e1))
     buf.close()
     m.close()
     ms = statistics.mean(times)
+    config_c = {"config": "C: 256^3 SYN map (same store), 256 perspectives x 640x480 rays, range 1.5 m",
+                "id_latency_ms": statistics.mean(times_c), "id_latency_ms_p50": statistics.median(times_c),
+                "id_latency_ms_max": max(times_c), "reps": len(times_c),
+                "rays_per_s": cc.rays_per_id / (statistics.mean(times_c) / 1e3)}
     return {"config": f"C': 256^3 SYN map ({CPRIME_STATE_BITS}-bit state store), 512 perspectives x 640x480 rays, "
                       f"range 1.5 m (north_star target)",
             "id_latency_ms": ms, "id_latency_ms_p50": statistics.median(times),
             "id_latency_ms_max": max(times), "reps": len(times), "rays_per_s": cn.rays_per_id / (ms / 1e3),
             "lookups_per_s": lookups / (sum(times) / 1e3), "target_ms": 100.0, "roofline": roof,
-            "clocks": clk, "l2": "flushed before every cycle (outside the events)",
+            "clocks": clk, "l2": "flushed before every cycle (outside the events)", "config_c": config_c,
             "e2e": {"ms_per_cycle": statistics.mean(e2e_t), "unit": "ms",
                     "h2d_bytes_per_cycle": cn.n_persp * 24 + cn.n_persp * 32 + N_QUERIES * 24,
                     "d2h_bytes_per_cycle": cn.n_persp * 64 + N_QUERIES * 8,
