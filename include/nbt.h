@@ -87,7 +87,9 @@ uint64_t   nbt_ctx_launch_count(nbt_ctx ctx);
 enum {
     NBT_OPT_TRACE_REFILL_MIN = 1,   /* idle lanes before a trace warp pops prepared rays: 1..32, default 6 */
     NBT_OPT_TRACE_CHUNK_MIN = 2,    /* smallest ray-slot chunk per work grab: 32..1024 (rounded up to 32), default 64 */
-    NBT_OPT_TRACE_CARVEOUT = 3,     /* shared-memory carveout (%) of the trace kernel: -1 (driver) .. 100, default 25 */
+    NBT_OPT_TRACE_CARVEOUT = 3,     /* shared-memory carveout (%) of the trace kernel: -1 (driver) .. 100, default 25;
+                                       a function attribute, so process-wide: applied at the ctx's next
+                                       ID launch (the last ctx to apply a different value sets it) */
     NBT_OPT_DELTA_SORT = 4,         /* 1: map deltas by a CUB radix sort instead of the winner array; default 0 */
     NBT_OPT_FILTER_SORT = 5,        /* 1: the integration's voxel filter by sorting instead of hashing; default 0 */
     NBT_OPT_H2D_MODE = 6,           /* 1: host inputs copied by the driver (pageable) instead of the pinned stage; default 0 */
