@@ -152,7 +152,8 @@ enum { NBT_LAYOUT_LINEAR = 0, NBT_LAYOUT_MORTON = 1 };
 typedef struct nbt_map_s *nbt_map;
 
 typedef struct {
-    int32_t nx, ny, nz;       /* voxels per axis, each >= 1; (nx+32)(ny+32)(nz+32) < 2^32 */
+    int32_t nx, ny, nz;       /* voxels per axis, each >= 1; (nx+32)(ny+32)(nz+32) < 2^32
+                                 (< 2^31 for the 2-bit linear store) */
     double  voxel_size;       /* s_Vox > 0 (1 cm) */
     double  origin[3];        /* world position of voxel (0,0,0)'s min corner */
     double  gain[3];          /* g[U], g[F], g[O] of Eq. 2 as per-state constants (Q15);

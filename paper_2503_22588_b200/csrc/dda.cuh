@@ -29,9 +29,11 @@ __device__ __forceinline__ uint32_t grid_index(const MapView &m, int x, int y, i
            (uint32_t)m.pxy * (uint32_t)(z + kBorder);
 }
 
-__device__ __forceinline__ uint32_t code_of(uint32_t word, uint32_t idx)
+// 2-bit store: the code of the voxel whose bit offset in the store is ib (= 2 x its index;
+// the first voxel of a word sits at the top, map_store.cuh): rotate it to bits 30-31.
+__device__ __forceinline__ uint32_t code_of(uint32_t word, uint32_t ib)
 {
-    return __funnelshift_r(word, 0u, idx << 1) & 3u;   // shift amount taken mod 32
+    return __funnelshift_l(word, word, ib) >> 30;      // shift amount taken mod 32
 }
 
 // Per-ray walk state.  T = int (rays < 2^14 voxels per axis, k_id.cu header) or long long.
@@ -40,7 +42,8 @@ struct Walk {
     T qxy, qxz, qyz;           // sign decides the next axis (see header)
     T ax, ay, az;              // |D_a| in Q16 units
     T nax;                     // -|D_x| (hot path)
-    uint32_t idx;              // padded linear index of the current voxel (in-grid walk)
+    uint32_t idx;              // linear: padded index of the current voxel (in-grid walk) << SH,
+                               // SH = 1 for the 2-bit store (idx = the code's bit offset); Morton: address
     int dX, dY, ndZ;           // linear: idx increments of a step along x, y and (negated) z
     uint32_t rx, ry, rz;       // Morton: per-axis dilated coordinates in "decrement form"
     uint32_t xinv;             // Morton: bits to flip (axes walked in + direction)

@@ -75,9 +75,24 @@ constexpr int kInt32MaxVoxels = 16000;   // |D_a| bound (voxels) for the int32 d
 constexpr int kTileW = NBT_TILE_W;       // a warp's 32 rays: a kTileW x kTileH pixel tile
 constexpr int kTileH = 32 / kTileW;
 
+// Store kinds (the VB template parameter): kStore2 = 2-bit codes, 16 per word (rows a1, a6);
+// kStoreByte = one byte per voxel holding the code alone; kStoreProb = one byte per voxel,
+// code in bits 0-1 and the Eq. 2 gain in bits 2-7 (f1).  Byte stores load the voxel's own
+// byte, so a visit needs no rotate and the code packs with one shift-add.
+constexpr int kStore2 = 2, kStoreByte = 1, kStoreProb = 8;
+
+// Scale of the walk's linear index: the 2-bit linear store walks the code's bit offset 2i
+// (its word is ib >> 5 and one left rotate by ib brings the code to bits 30-31, map_store.cuh),
+// so a visit needs no separate rotate amount; byte stores walk the byte index i.
+template <int L, int VB>
+__device__ __forceinline__ constexpr int idx_shift()
+{
+    return (L == kLayoutLinear && VB == kStore2) ? 1 : 0;
+}
+
 // Origin outside the grid (rare): step with explicit bounds checks until the walk
 // enters the grid or ends.  Returns true if the ray is finished.
-template <typename T, int L, bool RECORD>
+template <typename T, int L, bool RECORD, int SH = 0>
 __device__ bool walk_enter(Walk<T> &w, const MapView &m, int32_t *rec_ijk, uint8_t *rec_code, int max_visits)
 {
     while (!inside(m, w.vx, w.vy, w.vz)) {
@@ -100,10 +115,10 @@ __device__ bool walk_enter(Walk<T> &w, const MapView &m, int32_t *rec_ijk, uint8
         w.rz = (dz ^ w.xinv) & m.mz;
         w.idx = dx | dy | dz;
     } else {
-        w.idx = grid_index<L>(m, w.vx, w.vy, w.vz);
-        w.dX = w.sx;
-        w.dY = w.sy * m.px;
-        w.ndZ = -w.sz * m.pxy;
+        w.idx = grid_index<L>(m, w.vx, w.vy, w.vz) << SH;
+        w.dX = w.sx * (1 << SH);
+        w.dY = w.sy * m.px * (1 << SH);
+        w.ndZ = -w.sz * m.pxy * (1 << SH);
     }
     return false;
 }
@@ -146,18 +161,19 @@ __device__ __forceinline__ void walk_close_end(const Walk<T> &w, int policy, uin
     c.g += ng + 63u * u_out;
 }
 
-// A batch of K visits: the loaded map words and, per visit, the rotate amount that
-// brings its value's state bits to bits 2k..2k+1 of the packed word.
+// A batch of K visits: the loaded map words and, per visit (2-bit store), the code's bit
+// offset, the left rotate that brings the code to bits 30-31.
 template <int K>
 struct Batch {
     uint32_t wd[K];
     uint32_t rot[K];
 };
 
+// Packed codes of a batch: visit k at bits 31-2k..30-2k (visit 0 at the top).
 template <int K>
-__device__ __forceinline__ constexpr uint32_t lanes_mask(uint32_t pattern)
+__device__ __forceinline__ constexpr uint32_t batch_mask()
 {
-    return K >= 16 ? pattern : (pattern & ((1u << (2 * K)) - 1u));
+    return K >= 16 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> (2 * K));
 }
 
 #ifndef NBT_MAP_LOAD
@@ -183,12 +199,6 @@ __device__ __forceinline__ uint32_t load_map_word(const uint32_t *p)
     return __ldg(p);
 #endif
 }
-
-// Store kinds (the VB template parameter): kStore2 = 2-bit codes, 16 per word (rows a1, a6);
-// kStoreByte = one byte per voxel holding the code alone; kStoreProb = one byte per voxel,
-// code in bits 0-1 and the Eq. 2 gain in bits 2-7 (f1).  Byte stores load the voxel's own
-// byte, so a visit needs no rotate and the code packs with one shift-add.
-constexpr int kStore2 = 2, kStoreByte = 1, kStoreProb = 8;
 
 // Step table (NBT_DDA_TABLE experiment, linear layout, int32 terms): per lane, the three
 // possible updates (dq_xy, dq_xz, dq_yz, d_idx) of a step along x, y, z in shared memory,
@@ -240,8 +250,9 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         if (VB == kStore2) {
-            b.rot[k] = (w.idx << 1) - 2 * k;    // rotate amounts are taken mod 32
-            b.wd[k] = load_map_word(m.words + (w.idx >> 4));
+            const uint32_t ib = L == kLayoutLinear ? w.idx : (w.idx << 1);   // the code's bit offset
+            b.rot[k] = ib;                       // rotate amounts are taken mod 32
+            b.wd[k] = load_map_word(m.words + (ib >> 5));
         } else {
             b.wd[k] = __ldg(bytes + w.idx);
         }
@@ -252,29 +263,41 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
     }
 }
 
-// The packed 2-bit code of visit k of a batch, at bits 2k..2k+1 (stores without a gain).
+// Append the code of visit k of a batch below the codes packed so far: 2-bit store, one
+// rotate (code to bits 30-31) and one funnel shift; byte stores, one shift-add.
 template <int VB, int K>
-__device__ __forceinline__ uint32_t batch_code(const Batch<K> &b, int k)
+__device__ __forceinline__ uint32_t batch_push(uint32_t bits, const Batch<K> &b, int k)
 {
-    if (VB == kStore2) return __funnelshift_r(b.wd[k], b.wd[k], b.rot[k]) & (3u << (2 * k));
-    return b.wd[k] << (2 * k);                   // byte store: the byte is the code
+    if (VB == kStore2) return __funnelshift_l(__funnelshift_l(b.wd[k], b.wd[k], b.rot[k]), bits, 2);
+    if (VB == kStoreByte) return bits * 4u + b.wd[k];             // the byte is the code (< 4)
+    return (bits << 2) | (b.wd[k] & 3u);
+}
+
+// The packed codes of a whole batch, visit k at bits 31-2k..30-2k.
+template <int VB, int K>
+__device__ __forceinline__ uint32_t batch_bits(const Batch<K> &b)
+{
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) bits = batch_push<VB, K>(bits, b, k);
+    return K >= 16 ? bits : bits << (32 - 2 * K);
 }
 
 // Close or advance the walk after the batch holding visits s..s+K-1, whose codes are
-// packed in `bits` (and, with the 8-bit store, whose gains sum to gsum / are read from b).
-// Returns true when the ray is finished (counts added to c): first code >= 2 by one ffs
-// (Occupied: early stop; 3: left the grid), Free voxels by one popc.
+// packed in `bits` (visit k at bits 31-2k..30-2k; with the 8-bit store, whose gains sum to
+// gsum / are read from b).  Returns true when the ray is finished (counts added to c): first
+// code >= 2 by one clz (Occupied: early stop; 3: left the grid), Free voxels by one popc.
 template <typename T, int VB, int K>
 __device__ __forceinline__ bool batch_finish(Walk<T> &w, uint32_t bits, uint32_t gsum, const Batch<K> &b,
                                              int policy, Counts &c)
 {
     const int left = w.n - w.s + 1;             // visits remaining, including the current one
-    const uint32_t valid = left >= K ? lanes_mask<K>(0xFFFFFFFFu) : ((1u << (2 * left)) - 1u);
+    const uint32_t valid = left >= K ? batch_mask<K>() : ~(0xFFFFFFFFu >> (2 * left));   // 1 <= left < 16
     const uint32_t stop = bits & valid & 0xAAAAAAAAu;   // codes 2 (Occupied) and 3 (outside)
     if (stop || left <= K) {
         // last batch of the ray: only visits up to the stop (or the end) count
-        const int last = stop ? ((__ffs(stop) - 1) >> 1) : left - 1;
-        const uint32_t upto = last >= 15 ? 0xFFFFFFFFu : ((1u << (2 * last + 2)) - 1u);
+        const int last = stop ? (__clz(stop) >> 1) : left - 1;
+        const uint32_t upto = last >= 15 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> (2 * last + 2));   // visits 0..last
         uint32_t ng = w.ng;
         if (VB == kStoreProb) {
 #pragma unroll
@@ -282,8 +305,8 @@ __device__ __forceinline__ bool batch_finish(Walk<T> &w, uint32_t bits, uint32_t
                 if (k <= last) ng += b.wd[k] >> 2;
         }
         if (stop) {
-            const uint32_t nf = w.nf + __popc(bits & (upto >> 2) & 0x55555555u);
-            walk_close_stop(w, policy, (bits >> (2 * last)) & 3u, w.s + last, nf, ng, c);
+            const uint32_t nf = w.nf + __popc(bits & (upto << 2) & 0x55555555u);   // visits 0..last-1
+            walk_close_stop(w, policy, (bits >> (30 - 2 * last)) & 3u, w.s + last, nf, ng, c);
         } else {
             walk_close_end(w, policy, w.nf + __popc(bits & upto & 0x55555555u), ng, c);
         }
@@ -299,17 +322,12 @@ __device__ __forceinline__ bool batch_finish(Walk<T> &w, uint32_t bits, uint32_t
 template <typename T, int VB, int K>
 __device__ __forceinline__ bool batch_consume(Walk<T> &w, const Batch<K> &b, int policy, Counts &c)
 {
-    uint32_t bits = 0, gsum = 0;
+    uint32_t gsum = 0;
+    if (VB == kStoreProb) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        if (VB == kStoreProb) {
-            bits += (b.wd[k] & 3u) << (2 * k);
-            gsum += b.wd[k] >> 2;                // Eq. 2 gain in 1/63 units
-        } else {
-            bits |= batch_code<VB, K>(b, k);
-        }
+        for (int k = 0; k < K; ++k) gsum += b.wd[k] >> 2;      // Eq. 2 gain in 1/63 units
     }
-    return batch_finish<T, VB, K>(w, bits, gsum, b, policy, c);
+    return batch_finish<T, VB, K>(w, batch_bits<VB, K>(b), gsum, b, policy, c);
 }
 
 // In-place software pipeline (stores without a gain): extract the codes of the batch in b
@@ -323,16 +341,17 @@ __device__ __forceinline__ uint32_t batch_cycle(Walk<T> &w, const MapView &m, Ba
     uint32_t bits = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        bits |= batch_code<VB, K>(b, k);
+        bits = batch_push<VB, K>(bits, b, k);
         if (VB == kStore2) {
-            b.rot[k] = (w.idx << 1) - 2 * k;
-            b.wd[k] = __ldg(m.words + (w.idx >> 4));
+            const uint32_t ib = L == kLayoutLinear ? w.idx : (w.idx << 1);
+            b.rot[k] = ib;
+            b.wd[k] = __ldg(m.words + (ib >> 5));
         } else {
             b.wd[k] = __ldg(bytes + w.idx);
         }
         walk_step<T, L, false>(w, m);
     }
-    return bits;
+    return K >= 16 ? bits : bits << (32 - 2 * K);
 }
 
 // ------------------------------------------------------------------ frames (a4)
@@ -649,7 +668,7 @@ __device__ __noinline__ void add_unknown_shard(const TraceArgs &A, int j, uint32
     }
 }
 
-template <typename T, int L, bool SHARD, bool REC = false>
+template <typename T, int L, int VB, bool SHARD, bool REC = false>
 __device__ __forceinline__ bool prep_ray(const TraceArgs &A, int j, int slot, Walk<T> &w)
 {
     int mi = 0, mk = 0, corner = -1;
@@ -661,7 +680,7 @@ __device__ __forceinline__ bool prep_ray(const TraceArgs &A, int j, int slot, Wa
     int o[3], e[3];
     ray_segment(f, mi, mk, corner, o, e);
     walk_setup(w, o, e);
-    if (walk_enter<T, L, false>(w, A.m, nullptr, nullptr, 0)) {
+    if (walk_enter<T, L, false, idx_shift<L, VB>()>(w, A.m, nullptr, nullptr, 0)) {
         if (A.m.policy == NBT_OUTSIDE_UNKNOWN) {
             if (SHARD) {
                 add_unknown_shard(A, j, w.pre);
@@ -802,7 +821,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     }
                 }
                 Walk<T> t;
-                const bool ok = lane < valid && prep_ray<T, L, SHARD, REC>(A, q_j, slot0 + lane, t);
+                const bool ok = lane < valid && prep_ray<T, L, VB, SHARD, REC>(A, q_j, slot0 + lane, t);
                 q_next += avail;
                 const unsigned vm = __ballot_sync(full, ok);
                 if (ok) queue_put<T, L>(Q, __popc(vm & lanes_below), t, q_j);
@@ -847,9 +866,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
             if (w.n - w.s + 1 > K) {
                 bits = batch_cycle<T, L, VB, K>(w, A.m, b0);
             } else {
-                bits = 0;
-#pragma unroll
-                for (int k = 0; k < K; ++k) bits |= batch_code<VB, K>(b0, k);
+                bits = batch_bits<VB, K>(b0);
             }
             if (batch_finish<T, VB, K>(w, bits, 0u, b0, A.m.policy, c)) have = false;
         } else {
@@ -961,12 +978,13 @@ __global__ void k_debug_trace(MapView m, const int32_t *__restrict__ o, const in
     uint8_t *rc = code + (size_t)r * max_visits;
     Counts c{0, 0, 0, 0, 0};
     int visits;
-    if (walk_enter<T, L, true>(w, m, ri, rc, max_visits)) {
+    if (walk_enter<T, L, true, idx_shift<L, VB>()>(w, m, ri, rc, max_visits)) {
         if (m.policy == NBT_OUTSIDE_UNKNOWN) c.u += w.pre;
         visits = w.n + 1;
     } else {
         for (;;) {
-            const uint32_t cd = VB == kStore2 ? code_of(__ldg(m.words + (w.idx >> 4)), w.idx)
+            const uint32_t ib = L == kLayoutLinear ? w.idx : (w.idx << 1);   // 2-bit store: bit offset
+            const uint32_t cd = VB == kStore2 ? code_of(__ldg(m.words + (ib >> 5)), ib)
                                               : __ldg(reinterpret_cast<const uint8_t *>(m.words) + w.idx) & 3u;
             if (w.s < max_visits) {
                 ri[3 * w.s] = w.vx; ri[3 * w.s + 1] = w.vy; ri[3 * w.s + 2] = w.vz;

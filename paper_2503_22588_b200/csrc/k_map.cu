@@ -9,7 +9,7 @@
 // detects an Occupied voxel, and its thickness keeps look-ahead loads inside the store.
 //
 // Two value widths.  2 bits per voxel (the three states, 0 U / 1 F / 2 O, 3 = sentinel),
-// 16 voxels per word: per-state gains (reading Q15).  8 bits per voxel (f1, exact Eq. 2,
+// 16 voxels per word, the first at the top (bits 30-31): per-state gains (reading Q15).  8 bits per voxel (f1, exact Eq. 2,
 // reading Q32), 4 voxels per word: bits 0-1 the state, bits 2-7 the voxel's Eq. 2 gain in
 // units of 1/63 -- 63 for Unknown, level for Free (P = level/63), 63 - level for
 // Occupied -- so the walk reads the gain with one shift.
@@ -59,7 +59,7 @@ __global__ void k_map_pack(const uint8_t *__restrict__ codes, const uint8_t *__r
             if (lv > 63u) { bad = true; lv = 63u; }
             v = stored_value(g, c, lv);
         }
-        out |= v << (g.vbits * k);
+        out |= v << (g.vbits == 2 ? 30 - 2 * k : 8 * k);     // shift_of (map_store.cuh)
     }
     words[w] = out;
     if (bad) atomicCAS(err, 0, (int)NBT_ERR_INVALID_ARG);

@@ -25,7 +25,9 @@ __device__ __forceinline__ uint64_t store_index(const Geom &g, uint32_t x, uint3
 __device__ __forceinline__ uint32_t word_of(const Geom &g, uint64_t i) { return (uint32_t)(i >> (g.vbits == 2 ? 4 : 2)); }
 __device__ __forceinline__ uint32_t shift_of(const Geom &g, uint64_t i)
 {
-    return g.vbits == 2 ? (uint32_t)(i & 15) * 2 : (uint32_t)(i & 3) * 8;
+    // 2-bit store: voxel i % 16 of a word at bits 31-2(i%16) .. 30-2(i%16) (first voxel at the
+    // top, so the walk brings a code to bits 30-31 with one left rotate by its bit offset 2i)
+    return g.vbits == 2 ? 30u - (uint32_t)(i & 15) * 2 : (uint32_t)(i & 3) * 8;
 }
 
 // The stored value of a grid voxel: the state, or state | Eq. 2 gain (1/63 units) << 2.

@@ -637,6 +637,9 @@ static nbt_status check_desc(const nbt_map_desc *d)
         return fail(NBT_ERR_INVALID_ARG, "map extents must be in [1, 16384]");
     uint64_t pad = (uint64_t)(d->nx + 2 * kBorder) * (d->ny + 2 * kBorder) * (d->nz + 2 * kBorder);
     if (pad >= (1ull << 32)) return fail(NBT_ERR_INVALID_ARG, "(nx+32)(ny+32)(nz+32) must be < 2^32");
+    // the walk addresses the linear 2-bit store by the 32-bit bit offset 2i of a code (k_id.cu)
+    if (d->state_bits == 2 && d->layout == NBT_LAYOUT_LINEAR && pad >= (1ull << 31))
+        return fail(NBT_ERR_INVALID_ARG, "2-bit linear store: (nx+32)(ny+32)(nz+32) must be < 2^31");
     if (!(d->voxel_size > 0) || !isfinite(d->voxel_size)) return fail(NBT_ERR_INVALID_ARG, "voxel_size must be > 0");
     if (!finite3(d->origin)) return fail(NBT_ERR_INVALID_ARG, "origin must be finite");
     for (int k = 0; k < 3; ++k)
