@@ -790,10 +790,36 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
     bool have = false;
     int jl = -1;                             // perspective of this lane's accumulators
     Counts c{0, 0, 0, 0, 0};
+    int thr = A.min_refill;                  // idle lanes that end the batch loop (32 once the work is out)
     for (;;) {
-        const unsigned need = __ballot_sync(full, !have);
-        // refill once enough lanes are idle (min_refill = 1: as soon as any is)
-        if (need && (__popc(need) >= A.min_refill || q_done || need == full)) {
+        // the walk: batches until enough lanes are idle (min_refill = 1: as soon as any is)
+        unsigned need;
+        for (;;) {
+            if (have) {
+                if (CYCLE) {
+                    // b0 holds visits s..s+K-1 (issued at the ray's start or by the last cycle)
+                    uint32_t bits;
+                    if (w.n - w.s + 1 > K) {
+                        bits = batch_cycle<T, L, VB, K>(w, A.m, b0);
+                    } else {
+                        bits = batch_bits<VB, K>(b0);
+                    }
+                    if (batch_finish<T, VB, K>(w, bits, 0u, b0, A.m.policy, c)) have = false;
+                } else {
+                    batch_issue<T, L, VB, K, TAB>(w, A.m, b0, tz);
+                    const Counts before = c;
+                    if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) {
+                        have = false;
+                        if (REC)
+                            record_ray(A, jl, my_slot, c.u - before.u, c.f - before.f, c.o - before.o,
+                                       c.l - before.l);
+                    }
+                }
+            }
+            need = __ballot_sync(full, !have);
+            if (__popc(need) >= thr) break;
+        }
+        {
             // all 32 lanes prepare up to 32 rays at once, so the set-up runs converged
             while (qcount == 0 && !q_done) {
                 if (q_next >= q_end) {
@@ -858,24 +884,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                 __syncwarp();
             }
         }
-        if (q_done && qcount == 0 && !__any_sync(full, have)) break;
-        if (!have) continue;
-        if (CYCLE) {
-            // b0 holds visits s..s+K-1 (issued at the ray's start or by the last cycle)
-            uint32_t bits;
-            if (w.n - w.s + 1 > K) {
-                bits = batch_cycle<T, L, VB, K>(w, A.m, b0);
-            } else {
-                bits = batch_bits<VB, K>(b0);
-            }
-            if (batch_finish<T, VB, K>(w, bits, 0u, b0, A.m.policy, c)) have = false;
-        } else {
-            batch_issue<T, L, VB, K, TAB>(w, A.m, b0, tz);
-            const Counts before = c;
-            if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) {
-                have = false;
-                if (REC) record_ray(A, jl, my_slot, c.u - before.u, c.f - before.f, c.o - before.o, c.l - before.l);
-            }
+        if (q_done && qcount == 0) {
+            if (!__any_sync(full, have)) break;  // every lane idle and no work left
+            thr = 32;                            // let the last walks finish
         }
     }
     // residual counts, once per lane (the warp-combined form measured ~2% slower here)
