@@ -295,20 +295,27 @@ __device__ __forceinline__ bool batch_finish(Walk<T> &w, uint32_t bits, uint32_t
     const uint32_t valid = left >= K ? batch_mask<K>() : ~(0xFFFFFFFFu >> (2 * left));   // 1 <= left < 16
     const uint32_t stop = bits & valid & 0xAAAAAAAAu;   // codes 2 (Occupied) and 3 (outside)
     if (stop || left <= K) {
-        // last batch of the ray: only visits up to the stop (or the end) count
+        // last batch of the ray: only visits up to the stop (or the end) count.  The same counts
+        // as walk_close_stop / walk_close_end in branch-free form: visit `last` is the stop (code
+        // 2 Occupied: counted; 3: left the grid, Q14) or the ray's end (code 0 or 1).
         const int last = stop ? (__clz(stop) >> 1) : left - 1;
-        const uint32_t upto = last >= 15 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> (2 * last + 2));   // visits 0..last
-        uint32_t ng = w.ng;
+        const uint32_t upto = ~((0xFFFFFFFFu >> (2 * last)) >> 2);       // visits 0..last
+        const uint32_t code = (bits << (2 * last)) >> 30;
+        const uint32_t nf = w.nf + __popc(bits & ~(bits >> 1) & upto & 0x55555555u);   // codes 01 only
+        const uint32_t o = code == 2u, out = code == 3u;
+        const uint32_t l = (uint32_t)(w.s - w.s0 + last + 1) - out;      // in-grid lookups
+        uint32_t u_out = 0;                                              // Unknown visits outside (Q14)
+        if (policy == NBT_OUTSIDE_UNKNOWN) u_out = w.pre + out * (uint32_t)(w.n - w.s - last + 1);
+        c.o += o;
+        c.f += nf;
+        c.l += l;
+        c.u += l - nf - o + u_out;
         if (VB == kStoreProb) {
+            uint32_t ng = w.ng;
 #pragma unroll
             for (int k = 0; k < K; ++k)
                 if (k <= last) ng += b.wd[k] >> 2;
-        }
-        if (stop) {
-            const uint32_t nf = w.nf + __popc(bits & (upto << 2) & 0x55555555u);   // visits 0..last-1
-            walk_close_stop(w, policy, (bits >> (30 - 2 * last)) & 3u, w.s + last, nf, ng, c);
-        } else {
-            walk_close_end(w, policy, w.nf + __popc(bits & upto & 0x55555555u), ng, c);
+            c.g += ng + 63u * u_out;
         }
         return true;
     }
@@ -898,7 +905,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
             if (c.f) atomicAdd(t + 1, (unsigned long long)c.f);
             if (c.o) atomicAdd(t + 2, (unsigned long long)c.o);
             if (c.l) atomicAdd(t + 3, (unsigned long long)c.l);
-            if (c.g) atomicAdd(t + 4, (unsigned long long)c.g);
+            if (VB == kStoreProb && c.g) atomicAdd(t + 4, (unsigned long long)c.g);
         }
     } else if (jl >= 0) {
         unsigned long long *t = A.totals + kTotals * (size_t)jl;
@@ -906,7 +913,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
         if (c.f) atomicAdd(t + 1, (unsigned long long)c.f);
         if (c.o) atomicAdd(t + 2, (unsigned long long)c.o);
         if (c.l) atomicAdd(t + 3, (unsigned long long)c.l);
-        if (c.g) atomicAdd(t + 4, (unsigned long long)c.g);
+        if (VB == kStoreProb && c.g) atomicAdd(t + 4, (unsigned long long)c.g);
     }
 }
 
