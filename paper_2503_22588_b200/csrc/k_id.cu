@@ -241,6 +241,14 @@ __device__ __forceinline__ void walk_step_table(Walk<T> &w, uint32_t tz)
     w.idx = (uint32_t)mad_i32(1, di, (int)w.idx);
 }
 
+// DDA step form per store kind (walk_step): 0/1 flags for the 2-bit store, 0/-1 masks for
+// the byte stores (measured, profiles/r02_s3_mask_ab.log).
+template <int VB>
+__device__ __forceinline__ constexpr bool masks_of()
+{
+    return VB != kStore2;
+}
+
 // Issue the K loads of the next K visits (the DDA does not depend on the map, so
 // this runs ahead of the codes) and advance the DDA by K steps.
 template <typename T, int L, int VB, int K, bool TAB = false>
@@ -259,7 +267,7 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
         if constexpr (TAB)
             walk_step_table(w, tz);
         else
-            walk_step<T, L, false>(w, m);
+            walk_step<T, L, false, masks_of<VB>()>(w, m);
     }
 }
 
@@ -356,7 +364,7 @@ __device__ __forceinline__ uint32_t batch_cycle(Walk<T> &w, const MapView &m, Ba
         } else {
             b.wd[k] = __ldg(bytes + w.idx);
         }
-        walk_step<T, L, false>(w, m);
+        walk_step<T, L, false, masks_of<VB>()>(w, m);
     }
     return K >= 16 ? bits : bits << (32 - 2 * K);
 }
@@ -741,7 +749,6 @@ __device__ __forceinline__ int queue_get(const Queue &Q, int i, Walk<T> &w)
 {
     w.qxy = Q.q[0][i]; w.qxz = Q.q[1][i]; w.qyz = Q.q[2][i];
     w.ax = Q.a[0][i]; w.ay = Q.a[1][i]; w.az = Q.a[2][i];
-    w.nax = -w.ax;
     w.idx = Q.idx[i];
     if (L == kLayoutMorton) {
         w.rx = (uint32_t)Q.d[0][i]; w.ry = (uint32_t)Q.d[1][i]; w.rz = (uint32_t)Q.d[2][i];
@@ -750,6 +757,7 @@ __device__ __forceinline__ int queue_get(const Queue &Q, int i, Walk<T> &w)
         w.dX = Q.d[0][i]; w.dY = Q.d[1][i]; w.ndZ = Q.d[2][i];
     }
     w.n = Q.n[i]; w.s0 = Q.s0[i]; w.s = w.s0; w.pre = Q.pre[i]; w.nf = 0; w.ng = 0;
+    walk_hot_init(w);
     return Q.j[i];
 }
 
