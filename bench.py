@@ -104,6 +104,18 @@ def ncu_traffic(cfg_name):
         return {}
 
 
+def l1_block(tr):
+    """The kernel's L1 data-pipe and issue utilisation from the same ncu capture (the units that
+    bind it: D is L1-data-pipe bound, C' issue bound)."""
+    if "l1_data_pipe_wavefronts_pct" not in tr:
+        return {}
+    return {"l1": {"data_pipe_wavefronts_frac": tr["l1_data_pipe_wavefronts_pct"] / 100.0,
+                   "wavefronts_per_request": tr["l1_wavefronts_per_request"],
+                   "sectors_per_request": tr["l1_sectors_per_request"], "hit_rate_pct": tr.get("l1_hit_rate_pct"),
+                   "issue_active_frac": tr["issue_active_pct"] / 100.0,
+                   "source": tr.get("source_l1")}}
+
+
 def host_cpu():
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
@@ -668,6 +680,7 @@ def run_cycle(args, nbt, ndist, ctx, stream, dev, rank, world, cfg, mode, steps,
                       "frac": (l2_bytes / (tr_avg / 1e3) / 1e9 / pk["l2_gbs"]) if pk["l2_gbs"] else None,
                       "bytes_per_launch": l2_bytes,
                       "source": tr.get("source", "ncu --set full, lts__t_sectors_srcunit_tex_op_read x 32 B")}
+    roof.update(l1_block(tr))
     return {
         "value": rays_total / sec, "ms_per_step": t_dev / steps,
         "ms_per_step_p50": statistics.median(step_ms), "ms_per_step_max": max(step_ms),
@@ -879,6 +892,7 @@ def run_cprime(args, nbt, ctx, stream, dev, flush, pk, reps):
     if tr.get("l2_bytes_per_launch") and pk["l2_gbs"]:
         a = tr["l2_bytes_per_launch"] / (tr_avg / 1e3) / 1e9
         roof["l2"] = {"achieved_gbs": a, "peak_gbs": pk["l2_gbs"], "frac": a / pk["l2_gbs"]}
+    roof.update(l1_block(tr))
     # e2e: host perspectives in, host IG cloud and IDW values out, through the ABI
     hp = [nbt.sample_perspectives(ctx, cn.poi, cn.persp_radius, cn.n_persp, 99 + t, cn.persp_mode)
           for t in range(4)]

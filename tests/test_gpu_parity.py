@@ -1208,3 +1208,17 @@ def test_ctx_options_roundtrip_and_range(nbt, ctx):
         ctx.set_option(nbt.OPT_TRACE_REFILL_MIN, 6)
         ctx.set_option(nbt.OPT_TRACE_CHUNK_MIN, 64)
         ctx.set_option(nbt.OPT_TRACE_CARVEOUT, 25)
+
+
+def test_map_extent_limit_of_the_bit_offset_walk(nbt, ctx):
+    """The walk addresses the linear 2-bit store by the 32-bit bit offset 2i of a code
+    (k_id.cu idx_shift), so that store is refused from a padded extent of 2^31 voxels on
+    (NBT_ERR_INVALID_ARG from the descriptor check, before any allocation); the byte store of
+    the same extents stays within its own 2^32 limit (checked only, not created: 2.2 GB)."""
+    n = 1260                                           # (1260 + 32)^3 = 2.157e9 >= 2^31
+    assert (n + 32) ** 3 >= 2 ** 31 and (n + 32) ** 3 < 2 ** 32
+    with pytest.raises(nbt.NbtError) as ei:
+        nbt.Map(ctx, nbt.map_desc(n, n, n, 0.01))
+    assert "2^31" in str(ei.value)
+    m = nbt.Map(ctx, nbt.map_desc(1255, 1255, 8, 0.01))   # (1287^2 * 40) < 2^31: accepted
+    m.close()
