@@ -223,157 +223,6 @@ __global__ void __launch_bounds__(kThreads, NBT_IDW_LB)
     }
 }
 
-// Warp-per-unit form (default).  A unit is (32 queries, entry e, a chunk of the entry's
-// perspectives): every lane owns one query and walks the chunk's perspectives, read as warp
-// broadcasts (the 4 warps of a block take neighbouring query warps of the same chunk, so the
-// chunk is read from L1), with 4 independent (num, den) accumulators -- no cross-lane
-// reduction.  The chunk count is chosen so the units fill every SM sub-partition several
-// times over (the call is ~10 M pair evaluations, a few microseconds of the fp64 pipe).
-// Per pair: d^2 (6 fp64 operations), the reciprocal (MUFU + one cubic step, 3 fma) and the
-// two accumulations; min d^2 by its high word on the integer pipe.  Each unit stores its
-// partial sums ([e][chunk][query], ordered); the last unit of a query warp to finish (a
-// counter per query warp, reset by that unit) sums the chunks in order, applies the
-// zero-distance rule (an exact rescan only when min d^2 may lie within zero_eps), stores the
-// per-entry values and, when `out` is given, G = sum_u w_u v_u in entry order.
-constexpr int kPairWarps = 4;               // warps (units) per block
-constexpr int kPairUnroll = 4;              // independent accumulators per lane
-
-struct PairArgs {
-    const double *xyz, *gain;
-    const int32_t *meta;
-    int32_t max_persp, cap;
-    const double *q;
-    int32_t n_q, n_qw;                      // queries, query warps
-    int32_t nch, chunk;                     // perspective chunks per entry, perspectives per chunk
-    double power_p, zero_eps;
-    double *v_out;                          // [cap][n_q] per-entry values
-    double2 *part;                          // [cap][nch][n_q] (num, den)
-    int *part_h;                            // [cap][nch][n_q] high word of min d^2
-    int *done;                              // [n_qw] completion counters (zero between calls)
-    int32_t normalize;
-    double *out;                            // G per query, or null (information cost)
-};
-
-template <bool P2>        // power_p == 2 (the reciprocal) or a general power (pow)
-__global__ void __launch_bounds__(kPairWarps * 32)
-    k_idw_pairs(const __grid_constant__ PairArgs a)
-{
-    const int lane = threadIdx.x & 31;
-    const long long unit = (long long)blockIdx.x * kPairWarps + (threadIdx.x >> 5);
-    const long long units = (long long)a.cap * a.nch * a.n_qw;
-    if (unit >= units) return;
-    const int qw = (int)(unit % a.n_qw);
-    const int ec = (int)(unit / a.n_qw);              // e * nch + c
-    const int e = ec / a.nch, c = ec - e * a.nch;
-    const int pushes = a.meta[0];
-    const int m = min(pushes, a.cap);
-    const int qi = qw * 32 + lane;
-    const int qc = min(qi, a.n_q - 1);                // clamped: lanes past the end compute garbage
-    const double x0 = a.q[3 * (size_t)qc], x1 = a.q[3 * (size_t)qc + 1], x2 = a.q[3 * (size_t)qc + 2];
-    double num[kPairUnroll], den[kPairUnroll];
-    int hmin = 0x7ff00000;
-#pragma unroll
-    for (int k = 0; k < kPairUnroll; ++k) { num[k] = 0.0; den[k] = 0.0; }
-    if (e < m) {
-        const int slot = (pushes - m + e) % a.cap;    // entry e, oldest first
-        const int np = a.meta[1 + slot];
-        const double *P = a.xyz + (size_t)slot * a.max_persp * 3;
-        const double *G = a.gain + (size_t)slot * a.max_persp;
-        const int j0 = c * a.chunk, j1 = min(np, j0 + a.chunk);
-        const double hp = -0.5 * a.power_p;
-        const double *Pj = P + 3 * (size_t)j0;
-        const double *Gj = G + j0;
-        int n = j1 - j0;
-        // all loads of a group first (warp broadcasts), then the arithmetic
-        for (; n >= kPairUnroll; n -= kPairUnroll, Pj += 3 * kPairUnroll, Gj += kPairUnroll) {
-            double pv[3 * kPairUnroll], gv[kPairUnroll];
-#pragma unroll
-            for (int k = 0; k < 3 * kPairUnroll; ++k) pv[k] = __ldg(Pj + k);
-#pragma unroll
-            for (int k = 0; k < kPairUnroll; ++k) gv[k] = __ldg(Gj + k);
-#pragma unroll
-            for (int k = 0; k < kPairUnroll; ++k) {
-                const double d2 = dist2_fast(x0, x1, x2, pv[3 * k], pv[3 * k + 1], pv[3 * k + 2]);
-                hmin = min(hmin, __double2hiint(d2));
-                const double w = P2 ? rcp_nr(d2) : pow(d2, hp);
-                num[k] = fma(gv[k], w, num[k]);
-                den[k] += w;
-            }
-        }
-        for (; n > 0; --n, Pj += 3, ++Gj) {
-            const double d2 = dist2_fast(x0, x1, x2, __ldg(Pj), __ldg(Pj + 1), __ldg(Pj + 2));
-            hmin = min(hmin, __double2hiint(d2));
-            const double w = P2 ? rcp_nr(d2) : pow(d2, hp);
-            num[0] = fma(__ldg(Gj), w, num[0]);
-            den[0] += w;
-        }
-    }
-    const size_t pi = (size_t)ec * a.n_q + qi;
-    if (qi < a.n_q) {
-        a.part[pi] = make_double2((num[0] + num[1]) + (num[2] + num[3]), (den[0] + den[1]) + (den[2] + den[3]));
-        a.part_h[pi] = hmin;
-    }
-    // the last unit of this query warp combines
-    __threadfence();
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-        last = atomicAdd(a.done + qw, 1) == a.cap * a.nch - 1;
-        if (last) a.done[qw] = 0;                     // reset for the next call / graph replay
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last || qi >= a.n_q) return;
-    __threadfence();
-    double g = 0.0, wsum = 0.0;
-    double nn = 0.0, dd = 0.0;
-    int h = 0x7ff00000;
-    const int total = m * a.nch;                      // partials f = u * nch + chunk, in order
-    for (int f0 = 0; f0 < total; f0 += kCombineBatch) {
-        double2 pr[kCombineBatch];
-        int hh[kCombineBatch];
-#pragma unroll
-        for (int t = 0; t < kCombineBatch; ++t) {     // the batch's loads first (independent L2 reads)
-            if (f0 + t < total) {
-                const size_t k = (size_t)(f0 + t) * a.n_q + qi;
-                pr[t] = __ldcg(a.part + k);
-                hh[t] = __ldcg(a.part_h + k);
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < kCombineBatch; ++t) {
-            if (f0 + t >= total) break;
-            nn += pr[t].x;
-            dd += pr[t].y;
-            h = min(h, hh[t]);
-            if ((f0 + t + 1) % a.nch != 0) continue;
-            const int u = (f0 + t) / a.nch;               // entry u complete
-            double v = nn / dd;
-            const double lim = a.zero_eps * (1.0 + 1e-6);
-            if (__hiloint2double(h, 0) < lim * lim) {
-                // min d^2 (rounded down to its high word) may lie within zero_eps: the definition's
-                // nearest -- correctly rounded d, lowest j among equal d (Q23)
-                const int slot = (pushes - m + u) % a.cap;
-                const int np = a.meta[1 + slot];
-                const double *P = a.xyz + (size_t)slot * a.max_persp * 3;
-                double dmin = __longlong_as_double(0x7ff0000000000000LL);
-                int jmin = -1;
-                for (int jj = 0; jj < np; ++jj) {
-                    const double d = __dsqrt_rn(dist2(x0, x1, x2, P[3 * (size_t)jj], P[3 * (size_t)jj + 1],
-                                                      P[3 * (size_t)jj + 2]));
-                    if (d < dmin) { dmin = d; jmin = jj; }
-                }
-                if (jmin >= 0 && dmin < a.zero_eps) v = a.gain[(size_t)slot * a.max_persp + jmin];
-            }
-            a.v_out[(size_t)u * a.n_q + qi] = v;
-            const double wu = __ddiv_rn(1.0, (double)(m - u));
-            g = __dadd_rn(g, __dmul_rn(wu, v));
-            wsum = __dadd_rn(wsum, wu);
-            nn = 0.0; dd = 0.0; h = 0x7ff00000;
-            }
-    }
-    if (a.out) a.out[qi] = a.normalize ? __ddiv_rn(g, wsum) : g;
-}
-
 // Optional k-nearest Eq. 4 (reading Q22): one warp per (query, entry).  Every lane keeps the
 // 16 nearest of its perspectives (j = lane, lane + 32, ...) sorted by (d^2, j) in registers;
 // knn rounds of a warp-wide (d^2, j) argmin then take the k nearest of the entry, each
@@ -561,56 +410,6 @@ __global__ void __launch_bounds__(kPushOneBlock) k_idbuf_push_small(int32_t *met
     }
 }
 
-#ifndef NBT_IDW_PAIRS
-#define NBT_IDW_PAIRS 0           // 1: k_idw_pairs (warp per unit, measured 1.5-2x slower); 0: k_idw_entry
-#endif
-#ifndef NBT_IDW_UNITS_PER_SMSP
-#define NBT_IDW_UNITS_PER_SMSP 8
-#endif
-
-// k_idw_pairs over the buffer: chunking, scratch, counters.  out = null: per-entry values only.
-nbt_status launch_idw_pairs(nbt_ctx ctx, const nbt_idbuf_s *b, const double *d_q, int32_t n_q, double power_p,
-                            double zero_eps, int32_t normalize, double *d_out)
-{
-    PairArgs a;
-    a.xyz = b->d_xyz; a.gain = b->d_gain; a.meta = b->d_meta;
-    a.max_persp = b->max_persp; a.cap = b->capacity;
-    a.q = d_q; a.n_q = n_q; a.n_qw = (n_q + 31) / 32;
-    const long long base = (long long)a.cap * a.n_qw;
-    const long long target = (long long)ctx->num_sms * 4 * NBT_IDW_UNITS_PER_SMSP;
-    long long nch = (target + base - 1) / base;
-    const long long max_nch = (a.max_persp + kPairUnroll - 1) / kPairUnroll;
-    nch = nch < 1 ? 1 : (nch > max_nch ? max_nch : nch);
-    long long chunk = (a.max_persp + nch - 1) / nch;
-    chunk = (chunk + kPairUnroll - 1) / kPairUnroll * kPairUnroll;
-    a.chunk = (int32_t)chunk;
-    a.nch = (int32_t)((a.max_persp + chunk - 1) / chunk);
-    a.power_p = power_p; a.zero_eps = zero_eps; a.normalize = normalize; a.out = d_out;
-    const size_t nv = (size_t)a.cap * n_q, np = nv * a.nch;
-    nbt_status st;
-    if ((st = ctx->idw_tmp.ensure(nv * 8 + np * 16 + np * 4))) return st;
-    a.v_out = ctx->idw_tmp.as<double>();
-    a.part = reinterpret_cast<double2 *>(a.v_out + nv);
-    a.part_h = reinterpret_cast<int *>(a.part + np);
-    // per-query-warp completion counters in their own buffer, zero between calls (the last unit
-    // of a query warp resets its counter); zeroed once when (re)allocated
-    if ((st = ctx->idw_done.ensure((size_t)a.n_qw * 4))) return st;
-    a.done = ctx->idw_done.as<int>();
-    if (ctx->idw_done_at != (void *)a.done || ctx->idw_done_zeroed < (size_t)a.n_qw) {
-        NBT_CUDA(cudaMemsetAsync(a.done, 0, ctx->idw_done.cap, ctx->stream));
-        ctx->idw_done_zeroed = ctx->idw_done.cap / 4;
-        ctx->idw_done_at = a.done;
-    }
-    const long long units = base * a.nch;
-    const unsigned blocks = (unsigned)((units + kPairWarps - 1) / kPairWarps);
-    if (power_p == 2.0)
-        k_idw_pairs<true><<<blocks, kPairWarps * 32, 0, ctx->stream>>>(a);
-    else
-        k_idw_pairs<false><<<blocks, kPairWarps * 32, 0, ctx->stream>>>(a);
-    NBT_LAUNCHED(ctx);
-    return NBT_OK;
-}
-
 }  // namespace
 
 nbt_status launch_idbuf_push(nbt_ctx ctx, nbt_idbuf_s *b, const double *d_xyz, const double *d_gain, int32_t n)
@@ -636,16 +435,12 @@ nbt_status launch_info_cost(nbt_ctx ctx, const nbt_idbuf_s *b, const InfoCostArg
     if (n_q == 0) return NBT_OK;
     nbt_status st;
     ProfScope ps(ctx, NBT_KERNEL_IDW);
-    if (NBT_IDW_PAIRS) {
-        if ((st = launch_idw_pairs(ctx, b, a.pos, n_q, power_p, zero_eps, 0, nullptr))) return st;
-    } else {
-        if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_q * 8))) return st;
-        dim3 grid((n_q + kQueries - 1) / kQueries, b->capacity);
-        (power_p == 2.0 ? k_idw_entry<true> : k_idw_entry<false>)<<<grid, kThreads, 0, ctx->stream>>>(
-            b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, a.pos, n_q, power_p, zero_eps,
-            ctx->idw_tmp.as<double>(), nullptr, 0, nullptr);
-        NBT_LAUNCHED(ctx);
-    }
+    if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_q * 8))) return st;
+    dim3 grid((n_q + kQueries - 1) / kQueries, b->capacity);
+    (power_p == 2.0 ? k_idw_entry<true> : k_idw_entry<false>)<<<grid, kThreads, 0, ctx->stream>>>(
+        b->d_xyz, b->d_gain, b->max_persp, b->d_meta, b->capacity, a.pos, n_q, power_p, zero_eps,
+        ctx->idw_tmp.as<double>(), nullptr, 0, nullptr);
+    NBT_LAUNCHED(ctx);
     k_info_cost<<<(a.n_traj + 63) / 64, 64, 0, ctx->stream>>>(ctx->idw_tmp.as<double>(), b->d_meta, b->capacity, a,
                                                               normalize, ctx->d_err);
     NBT_LAUNCHED(ctx);
@@ -658,7 +453,6 @@ nbt_status launch_idw(nbt_ctx ctx, const nbt_idbuf_s *b, const double *d_q, int3
     if (n_q == 0) return NBT_OK;
     nbt_status st;
     ProfScope ps(ctx, NBT_KERNEL_IDW);
-    if (knn == 0 && NBT_IDW_PAIRS) return launch_idw_pairs(ctx, b, d_q, n_q, power_p, zero_eps, normalize, d_out);
     if ((st = ctx->idw_tmp.ensure((size_t)b->capacity * n_q * 8))) return st;
     if (knn > 0) {
         const long long warps = (long long)n_q * b->capacity;
