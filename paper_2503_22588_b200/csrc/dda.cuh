@@ -41,11 +41,10 @@ template <typename T>
 struct Walk {
     T qxy, qxz, qyz;           // sign decides the next axis (see header)
     T ax, ay, az;              // |D_a| in Q16 units
-    T nax, nay, naz;           // -|D_a| (hot path, set when a lane takes the walk)
+    T nax;                     // -|D_x| (hot path)
     uint32_t idx;              // linear: padded index of the current voxel (in-grid walk) << SH,
                                // SH = 1 for the 2-bit store (idx = the code's bit offset); Morton: address
     int dX, dY, ndZ;           // linear: idx increments of a step along x, y and (negated) z
-    int ndX, ndY;              // linear, hot path: -dX, -dY
     uint32_t rx, ry, rz;       // Morton: per-axis dilated coordinates in "decrement form"
     uint32_t xinv;             // Morton: bits to flip (axes walked in + direction)
     int s, n;                  // current step (0 = origin voxel) and total steps
@@ -82,7 +81,7 @@ __device__ __forceinline__ void walk_setup(Walk<T> &w, const int o[3], const int
     w.qxz = (T)(fxz >> kQShift);
     w.qyz = (T)(fyz >> kQShift);
     w.ax = (T)ad[0]; w.ay = (T)ad[1]; w.az = (T)ad[2];
-    w.nax = -w.ax; w.nay = -w.ay; w.naz = -w.az;
+    w.nax = -w.ax;
     w.sx = neg[0] ? -1 : 1;
     w.sy = neg[1] ? -1 : 1;
     w.sz = neg[2] ? -1 : 1;
@@ -101,32 +100,21 @@ __device__ __forceinline__ int mad_i32(int a, int b, int c)
     return d;
 }
 
-// Hot-path negations of a walk taken from the prepared-walk queue (walk_step's mask form).
-template <typename T>
-__device__ __forceinline__ void walk_hot_init(Walk<T> &w)
-{
-    w.nax = -w.ax; w.nay = -w.ay; w.naz = -w.az;
-    w.ndX = -w.dX; w.ndY = -w.dY;
-}
-
 // One DDA step: pick the axis, update the two decision terms that involve it, and move
 // the map address.  Linear layout: idx += step of the axis.  Morton layout: every axis
 // register holds its dilated coordinate so that a step is always a dilated DECREMENT
 // (axes walked in + direction are stored complemented within their bits), i.e.
 // r = (r - lsb) & mask, and the address is (rx | ry | rz) ^ xinv.
 //
-// Hot path (int32, no coordinates; walk_hot_init first), two equivalent forms of the axis
-// choice, picked per store kind by measurement (profiles/r02_s3_mask_ab.log):
-//  MASKS = false: 0/1 flags from the sign bits (2 LOP3 + 2 SHF) and npz = px + py - 1 (one
-//    IADD3), the updates as multiply-adds by the flags (the 2-bit store: D -1.9%, B -1.5%);
-//  MASKS = true: 0/-1 masks (2 LOP3 + 2 SHF) and mz = ~(mx | my) (one LOP3), multiply-adds by
-//    the masks with the negated magnitudes (the byte stores: C' -1.6%).
-// Either way 5 ALU ops and 9 multiply-adds per step.  (Moving one or two decision terms to
-// the ALU pipe as AND + 3-input add was measured 4-14% slower: the step is issue-bound.)
-template <typename T, int L, bool COORDS, bool MASKS = false>
+// Hot path (int32, no coordinates): the axis choice as 0/1 flags from the sign bits (2 LOP3 +
+// 2 SHF) and npz = px + py - 1 (one IADD3), the updates as multiply-adds by the flags -- 5 ALU ops
+// and 9 multiply-adds per step.  (Measured alternatives: 0/-1 masks with the
+// negated magnitudes, within +-1.6% depending on how ptxas schedules the batch; one or two decision
+// terms on the ALU pipe as AND + 3-input add, 4-14% slower: the step is issue-bound.)
+template <typename T, int L, bool COORDS>
 __device__ __forceinline__ void walk_step(Walk<T> &w, const MapView &m)
 {
-    if constexpr (sizeof(T) == 4 && !COORDS && !MASKS) {
+    if constexpr (sizeof(T) == 4 && !COORDS) {
         const int t1 = w.qxy & w.qxz;            // sign: x first
         const int t2 = w.qyz & ~t1;              // sign: y first
         const int px = (int)((unsigned)t1 >> 31);
@@ -142,24 +130,6 @@ __device__ __forceinline__ void walk_step(Walk<T> &w, const MapView &m)
             w.idx = (w.rx | w.ry | w.rz) ^ w.xinv;
         } else {
             w.idx = (uint32_t)mad_i32(px, w.dX, mad_i32(py, w.dY, mad_i32(npz, w.ndZ, (int)w.idx)));
-        }
-    } else if constexpr (sizeof(T) == 4 && !COORDS) {
-        const int t1 = w.qxy & w.qxz;            // sign: x first
-        const int t2 = w.qyz & ~t1;              // sign: y first
-        const int mx = t1 >> 31;                 // -1 if x first, else 0
-        const int my = t2 >> 31;                 // -1 if y first
-        int mz;                                  // -1 if z first: ~(mx | my) as one LOP3
-        asm("lop3.b32 %0, %1, %2, 0, 0x03;" : "=r"(mz) : "r"(mx), "r"(my));
-        w.qxy = mad_i32(mx, w.nay, mad_i32(my, w.ax, w.qxy));
-        w.qxz = mad_i32(mx, w.naz, mad_i32(mz, w.ax, w.qxz));
-        w.qyz = mad_i32(my, w.naz, mad_i32(mz, w.ay, w.qyz));
-        if (L == kLayoutMorton) {
-            w.rx = (uint32_t)((int)w.rx + mx) & m.mx;
-            w.ry = (uint32_t)mad_i32(my, 2, (int)w.ry) & m.my;
-            w.rz = (uint32_t)mad_i32(mz, 4, (int)w.rz) & m.mz;
-            w.idx = (w.rx | w.ry | w.rz) ^ w.xinv;
-        } else {
-            w.idx = (uint32_t)mad_i32(mx, w.ndX, mad_i32(my, w.ndY, mad_i32(mz, w.ndZ, (int)w.idx)));
         }
     } else {
         const bool px = (w.qxy & w.qxz) < 0;     // both negative

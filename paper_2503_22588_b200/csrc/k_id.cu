@@ -241,14 +241,6 @@ __device__ __forceinline__ void walk_step_table(Walk<T> &w, uint32_t tz)
     w.idx = (uint32_t)mad_i32(1, di, (int)w.idx);
 }
 
-// DDA step form per store kind (walk_step): 0/1 flags for the 2-bit store, 0/-1 masks for
-// the byte stores (measured, profiles/r02_s3_mask_ab.log).
-template <int VB>
-__device__ __forceinline__ constexpr bool masks_of()
-{
-    return VB != kStore2;
-}
-
 // Issue the K loads of the next K visits (the DDA does not depend on the map, so
 // this runs ahead of the codes) and advance the DDA by K steps.
 template <typename T, int L, int VB, int K, bool TAB = false>
@@ -267,7 +259,7 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
         if constexpr (TAB)
             walk_step_table(w, tz);
         else
-            walk_step<T, L, false, masks_of<VB>()>(w, m);
+            walk_step<T, L, false>(w, m);
     }
 }
 
@@ -364,7 +356,7 @@ __device__ __forceinline__ uint32_t batch_cycle(Walk<T> &w, const MapView &m, Ba
         } else {
             b.wd[k] = __ldg(bytes + w.idx);
         }
-        walk_step<T, L, false, masks_of<VB>()>(w, m);
+        walk_step<T, L, false>(w, m);
     }
     return K >= 16 ? bits : bits << (32 - 2 * K);
 }
@@ -712,6 +704,10 @@ __device__ __forceinline__ bool prep_ray(const TraceArgs &A, int j, int slot, Wa
 
 // Per-warp queue of prepared walks in shared memory (structure of arrays, one column
 // per entry, so 32 lanes touching 32 entries hit 32 banks).
+// A queue holds the rays of ONE fill (one 32-slot unit of one perspective: the warp-uniform
+// q_j), and every queued ray entered the grid, so its outside visits equal its entry step
+// (pre == s0): neither is stored.  32-bit decision terms travel in int2 columns (one 8-byte
+// shared access per pair of fields and lane: 6 + 6 instead of 14 + 14 per ray).
 template <typename T>
 struct WalkQueue {
     T q[3][32];
@@ -720,8 +716,16 @@ struct WalkQueue {
     int d[3][32];                // linear: dX, dY, ndZ; Morton: rx, ry, rz
     uint32_t xinv[32];           // Morton only
     int n[32], s0[32];
-    uint32_t pre[32];
-    int j[32];
+};
+template <>
+struct WalkQueue<int> {
+    int2 qq[32];                 // (qxy, qxz)
+    int2 qa[32];                 // (qyz, ax)
+    int2 aa[32];                 // (ay, az)
+    int2 id[32];                 // (idx, d0)
+    int2 dd[32];                 // (d1, d2); linear: dX, dY, ndZ; Morton: rx, ry, rz
+    int2 ns[32];                 // (n, s0)
+    uint32_t xinv[32];           // Morton only
 };
 // REC instance: the queue also carries each prepared ray's slot.
 template <typename T>
@@ -730,35 +734,53 @@ struct WalkQueueRec : WalkQueue<T> {
 };
 
 template <typename T, int L, typename Queue>
-__device__ __forceinline__ void queue_put(Queue &Q, int i, const Walk<T> &w, int j)
+__device__ __forceinline__ void queue_put(Queue &Q, int i, const Walk<T> &w)
 {
-    Q.q[0][i] = w.qxy; Q.q[1][i] = w.qxz; Q.q[2][i] = w.qyz;
-    Q.a[0][i] = w.ax; Q.a[1][i] = w.ay; Q.a[2][i] = w.az;
-    Q.idx[i] = w.idx;
-    if (L == kLayoutMorton) {
-        Q.d[0][i] = (int)w.rx; Q.d[1][i] = (int)w.ry; Q.d[2][i] = (int)w.rz;
-        Q.xinv[i] = w.xinv;
+    const int d0 = L == kLayoutMorton ? (int)w.rx : w.dX, d1 = L == kLayoutMorton ? (int)w.ry : w.dY,
+              d2 = L == kLayoutMorton ? (int)w.rz : w.ndZ;
+    if constexpr (sizeof(T) == 4) {
+        Q.qq[i] = make_int2(w.qxy, w.qxz);
+        Q.qa[i] = make_int2(w.qyz, w.ax);
+        Q.aa[i] = make_int2(w.ay, w.az);
+        Q.id[i] = make_int2((int)w.idx, d0);
+        Q.dd[i] = make_int2(d1, d2);
+        Q.ns[i] = make_int2(w.n, w.s0);
     } else {
-        Q.d[0][i] = w.dX; Q.d[1][i] = w.dY; Q.d[2][i] = w.ndZ;
+        Q.q[0][i] = w.qxy; Q.q[1][i] = w.qxz; Q.q[2][i] = w.qyz;
+        Q.a[0][i] = w.ax; Q.a[1][i] = w.ay; Q.a[2][i] = w.az;
+        Q.idx[i] = w.idx;
+        Q.d[0][i] = d0; Q.d[1][i] = d1; Q.d[2][i] = d2;
+        Q.n[i] = w.n; Q.s0[i] = w.s0;
     }
-    Q.n[i] = w.n; Q.s0[i] = w.s0; Q.pre[i] = w.pre; Q.j[i] = j;
+    if (L == kLayoutMorton) Q.xinv[i] = w.xinv;
 }
 
 template <typename T, int L, typename Queue>
-__device__ __forceinline__ int queue_get(const Queue &Q, int i, Walk<T> &w)
+__device__ __forceinline__ void queue_get(const Queue &Q, int i, Walk<T> &w)
 {
-    w.qxy = Q.q[0][i]; w.qxz = Q.q[1][i]; w.qyz = Q.q[2][i];
-    w.ax = Q.a[0][i]; w.ay = Q.a[1][i]; w.az = Q.a[2][i];
-    w.idx = Q.idx[i];
+    int d0, d1, d2;
+    if constexpr (sizeof(T) == 4) {
+        const int2 qq = Q.qq[i], qa = Q.qa[i], aa = Q.aa[i], id = Q.id[i], dd = Q.dd[i], ns = Q.ns[i];
+        w.qxy = qq.x; w.qxz = qq.y; w.qyz = qa.x;
+        w.ax = qa.y; w.ay = aa.x; w.az = aa.y;
+        w.idx = (uint32_t)id.x;
+        d0 = id.y; d1 = dd.x; d2 = dd.y;
+        w.n = ns.x; w.s0 = ns.y;
+    } else {
+        w.qxy = Q.q[0][i]; w.qxz = Q.q[1][i]; w.qyz = Q.q[2][i];
+        w.ax = Q.a[0][i]; w.ay = Q.a[1][i]; w.az = Q.a[2][i];
+        w.idx = Q.idx[i];
+        d0 = Q.d[0][i]; d1 = Q.d[1][i]; d2 = Q.d[2][i];
+        w.n = Q.n[i]; w.s0 = Q.s0[i];
+    }
     if (L == kLayoutMorton) {
-        w.rx = (uint32_t)Q.d[0][i]; w.ry = (uint32_t)Q.d[1][i]; w.rz = (uint32_t)Q.d[2][i];
+        w.rx = (uint32_t)d0; w.ry = (uint32_t)d1; w.rz = (uint32_t)d2;
         w.xinv = Q.xinv[i];
     } else {
-        w.dX = Q.d[0][i]; w.dY = Q.d[1][i]; w.ndZ = Q.d[2][i];
+        w.dX = d0; w.dY = d1; w.ndZ = d2;
     }
-    w.n = Q.n[i]; w.s0 = Q.s0[i]; w.s = w.s0; w.pre = Q.pre[i]; w.nf = 0; w.ng = 0;
-    walk_hot_init(w);
-    return Q.j[i];
+    w.s = w.s0; w.pre = (uint32_t)w.s0; w.nf = 0; w.ng = 0;   // queued rays entered the grid: pre == s0
+    w.nax = -w.ax;
 }
 
 // Resident blocks per SM the register allocation must allow: 4 (64 registers, 32 warps) for
@@ -800,9 +822,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
     int q_j = 0, q_next = 0, q_end = 0;      // warp-uniform chunk cursor
     bool q_done = false;
     int qhead = 0, qcount = 0;               // warp-uniform prepared-walk queue
+    int q_jq = 0;                            // ... and the perspective of its rays
     Walk<T> w;
     Batch<K> b0;
-    bool have = false;
+    int have = 0;                            // this lane walks a ray (an int: no predicate byte packing)
     int jl = -1;                             // perspective of this lane's accumulators
     Counts c{0, 0, 0, 0, 0};
     int thr = A.min_refill;                  // idle lanes that end the batch loop (32 once the work is out)
@@ -819,12 +842,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     } else {
                         bits = batch_bits<VB, K>(b0);
                     }
-                    if (batch_finish<T, VB, K>(w, bits, 0u, b0, A.m.policy, c)) have = false;
+                    if (batch_finish<T, VB, K>(w, bits, 0u, b0, A.m.policy, c)) have = 0;
                 } else {
                     batch_issue<T, L, VB, K, TAB>(w, A.m, b0, tz);
                     const Counts before = c;
                     if (batch_consume<T, VB, K>(w, b0, A.m.policy, c)) {
-                        have = false;
+                        have = 0;
                         if (REC)
                             record_ray(A, jl, my_slot, c.u - before.u, c.f - before.f, c.o - before.o,
                                        c.l - before.l);
@@ -865,7 +888,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                 const bool ok = lane < valid && prep_ray<T, L, VB, SHARD, REC>(A, q_j, slot0 + lane, t);
                 q_next += avail;
                 const unsigned vm = __ballot_sync(full, ok);
-                if (ok) queue_put<T, L>(Q, __popc(vm & lanes_below), t, q_j);
+                if (ok) queue_put<T, L>(Q, __popc(vm & lanes_below), t);
+                q_jq = q_j;                                        // the queue's perspective
                 if constexpr (REC) {
                     if (ok) Q.slot[__popc(vm & lanes_below)] = slot0 + lane;
                 }
@@ -878,7 +902,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                 const int take = min(__popc(need), qcount);
                 int j = -1;
                 if (!have && rank < take) {
-                    j = queue_get<T, L>(Q, qhead + rank, w);
+                    queue_get<T, L>(Q, qhead + rank, w);
+                    j = q_jq;
                     if constexpr (REC) my_slot = Q.slot[qhead + rank];
                 }
                 // lanes moving to another perspective flush their counts, one atomic per
@@ -890,7 +915,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     flush_counts_warp<VB == kStoreProb>(A.totals, jl, c, fl, lane);
                 if (j >= 0) {
                     jl = j;
-                    have = true;
+                    have = 1;
                     if (TAB) table_put(tz, w);
                     if (CYCLE) batch_issue<T, L, VB, K>(w, A.m, b0);
                 }

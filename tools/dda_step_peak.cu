@@ -1,9 +1,9 @@
 // Instruction-mix ceiling of the ID walk: the exact DDA step of
 // dda.cuh (walk_step, int32 decision terms, linear layout) run on registers only -- no map
 // loads, no rays to set up, every lane busy -- and the same step plus the per-visit code
-// packing of k_id_trace: MODE 1 = the 2-bit store's (0/1-flag step; rotate of a register word
-// by the code's bit offset + funnel shift into the batch word), MODE 2 = the byte stores'
-// (0/-1-mask step; shift-add of a register byte).  The visits/s it reaches is
+// packing of k_id_trace: MODE 1 = the 2-bit store's (rotate of a register word by the code's
+// bit offset + funnel shift into the batch word), MODE 2 = the byte stores' (shift-add of a
+// register byte).  The visits/s it reaches is
 // what the kernel's instruction mix alone allows on this GPU; bench.py's in-grid lookups/s
 // divided by it says how much the loads, the ray set-up, idle lanes and speculation cost.
 //
@@ -32,7 +32,6 @@ __global__ void __launch_bounds__(256) k_step_peak(int iters, uint32_t seed, uin
                       o[2] - (int)(550 << 12)};
     walk_setup(w, o, e);
     w.dX = 2; w.dY = 640; w.ndZ = 640 * 320;       // the 2-bit store's bit-offset steps
-    walk_hot_init(w);
     w.idx = t;
     MapView m{};
     uint32_t acc = 0, word = seed ^ t;
@@ -42,7 +41,7 @@ __global__ void __launch_bounds__(256) k_step_peak(int iters, uint32_t seed, uin
         for (int k = 0; k < kSteps; ++k) {
             if (MODE == 1) bits = __funnelshift_l(__funnelshift_l(word, word, w.idx), bits, 2);
             if (MODE == 2) bits = bits * 4u + ((word >> (w.idx & 24)) & 3u);
-            walk_step<int, kLayoutLinear, false, MODE == 2>(w, m);
+            walk_step<int, kLayoutLinear, false>(w, m);
         }
         acc += MODE ? __popc(bits & 0x55555555u) : w.idx;
         word = word * 1664525u + 1013904223u;
