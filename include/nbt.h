@@ -85,7 +85,7 @@ uint64_t   nbt_ctx_launch_count(nbt_ctx ctx);
  * reads no environment variable.  NBT_ERR_INVALID_ARG for an unknown option or a value
  * outside its range; get returns the current value. */
 enum {
-    NBT_OPT_TRACE_REFILL_MIN = 1,   /* idle lanes before a trace warp pops prepared rays: 1..32, default 6 */
+    NBT_OPT_TRACE_REFILL_MIN = 1,   /* idle lanes before a trace warp pops prepared rays: 1..32, default 32 (tile lockstep) */
     NBT_OPT_TRACE_CHUNK_MIN = 2,    /* smallest ray-slot chunk per work grab: 32..1024 (rounded up to 32), default 64 */
     NBT_OPT_TRACE_CARVEOUT = 3,     /* shared-memory carveout (%) of the trace kernel: -1 (driver) .. 100, default 25;
                                        a function attribute, so process-wide: applied at the ctx's next

@@ -125,7 +125,7 @@ struct ProfScope {
 
 // Tuning options of a ctx (nbt_ctx_set_option; none changes a result).
 struct NbtOptions {
-    int refill_min = 6;               // NBT_OPT_TRACE_REFILL_MIN
+    int refill_min = 32;              // NBT_OPT_TRACE_REFILL_MIN (32: a warp refills when all lanes are idle)
     int chunk_min = 64;               // NBT_OPT_TRACE_CHUNK_MIN
     int carveout = 25;                // NBT_OPT_TRACE_CARVEOUT
     int delta_sort = 0;               // NBT_OPT_DELTA_SORT

@@ -1185,7 +1185,7 @@ def test_full_size_per_ray_production_trace(nbt, ctx, name, bits, sampled):
 def test_ctx_options_roundtrip_and_range(nbt, ctx):
     """nbt_ctx_set_option / get_option: defaults, round trip, out-of-range and unknown options
     rejected; a non-default trace tuning gives the same ID bit for bit."""
-    assert ctx.get_option(nbt.OPT_TRACE_REFILL_MIN) == 6
+    assert ctx.get_option(nbt.OPT_TRACE_REFILL_MIN) == 32
     assert ctx.get_option(nbt.OPT_TRACE_CHUNK_MIN) == 64
     assert ctx.get_option(nbt.OPT_WALK_WIDTH) == 0
     for opt, bad in [(nbt.OPT_TRACE_REFILL_MIN, 0), (nbt.OPT_TRACE_REFILL_MIN, 33), (nbt.OPT_TRACE_CHUNK_MIN, 16),
@@ -1205,7 +1205,7 @@ def test_ctx_options_roundtrip_and_range(nbt, ctx):
         alt = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
         assert np.array_equal(alt.counts, ref.counts) and np.array_equal(alt.gain, ref.gain)
     finally:
-        ctx.set_option(nbt.OPT_TRACE_REFILL_MIN, 6)
+        ctx.set_option(nbt.OPT_TRACE_REFILL_MIN, 32)
         ctx.set_option(nbt.OPT_TRACE_CHUNK_MIN, 64)
         ctx.set_option(nbt.OPT_TRACE_CARVEOUT, 25)
 
