@@ -69,6 +69,12 @@ constexpr int kWarpsPerBlock = NBT_WARPS_PER_BLOCK;
 constexpr int kBatchK = NBT_BATCH_K;
 constexpr bool kPipe = NBT_PIPE;
 constexpr int kInt32MaxVoxels = 16000;   // |D_a| bound (voxels) for the int32 decision terms (< 16383)
+// Largest chunk of ray slots per work grab (8 tiles): with tile lockstep a warp's last chunk is the
+// end-of-launch tail, and 256-slot chunks cut D by 4.7% and C' by 0.7% against 1024 (128: D -5.1%,
+// C' -0.2%; 64: D -4.7%, C' +0.6%; profiles/r02_s3_cmax*.log).
+#ifndef NBT_CHUNK_MAX
+#define NBT_CHUNK_MAX 256
+#endif
 #ifndef NBT_TILE_W
 #define NBT_TILE_W 8
 #endif
@@ -1257,7 +1263,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     // smallest chunk per grab of the work counter (NBT_OPT_TRACE_CHUNK_MIN, default 64,
     // profiles/r01_chunk_flush.log)
     const int cmin = ctx->opt.chunk_min;
-    chunk = chunk < cmin ? cmin : (chunk > 1024 ? 1024 : chunk);
+    chunk = chunk < cmin ? cmin : (chunk > NBT_CHUNK_MAX ? NBT_CHUNK_MAX : chunk);
     T.chunk = chunk;
     T.chunks_per_persp = (T.slots + chunk - 1) / chunk;
     long long tc = (long long)T.chunks_per_persp * L.n;
