@@ -72,6 +72,13 @@ constexpr int kInt32MaxVoxels = 16000;   // |D_a| bound (voxels) for the int32 d
 // Largest chunk of ray slots per work grab (8 tiles): with tile lockstep a warp's last chunk is the
 // end-of-launch tail, and 256-slot chunks cut D by 4.7% and C' by 0.7% against 1024 (128: D -5.1%,
 // C' -0.2%; 64: D -4.7%, C' +0.6%; profiles/r02_s3_cmax*.log).
+// Chunk size = the launch's slots / (32 x resident warps), 64..256 slots: full-size D and C' (>= 8 k
+// slots per warp) keep 256, config B keeps 64, and the mid-size launches of one rank's strided shard
+// of D get finer chunks for a shorter tail -- 1024 perspectives (N = 4) -2.9%, 512 (N = 8) -4.2%
+// against 4 chunks per warp (profiles/r02_s3_shards.log).
+#ifndef NBT_CHUNKS_PER_WARP
+#define NBT_CHUNKS_PER_WARP 32
+#endif
 #ifndef NBT_CHUNK_MAX
 #define NBT_CHUNK_MAX 256
 #endif
@@ -1258,7 +1265,7 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     const int bps = ctx->trace_bps[fi];
     long long resident_warps = (long long)ctx->num_sms * bps * kWarpsPerBlock;
     long long total_slots = (long long)L.n * T.slots;
-    long long per = total_slots / (4 * resident_warps);           // aim for >= 4 chunks per warp
+    long long per = total_slots / (NBT_CHUNKS_PER_WARP * resident_warps);   // chunks per warp to aim for
     int chunk = (int)((per / 32) * 32);
     // smallest chunk per grab of the work counter (NBT_OPT_TRACE_CHUNK_MIN, default 64,
     // profiles/r01_chunk_flush.log)

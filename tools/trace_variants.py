@@ -19,8 +19,9 @@ import paper_2503_22588_b200 as nbt
 from nbt_inputs import CONFIGS, FOV_H, FOV_V
 
 
-def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=()):
+def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=(), persp=None, stride=1):
     cfg = CONFIGS[cfg_name]
+    n_use = persp if persp else cfg.n_persp
     dev = torch.device("cuda", 0)
     s = torch.cuda.Stream(dev)
     torch.cuda.set_stream(s)
@@ -37,9 +38,12 @@ def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=()):
     else:
         m.upload(codes)
     cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
-    persp = torch.empty((cfg.n_persp, 3), dtype=torch.float64, device=dev)
-    nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode, out=persp)
-    out = nbt.empty_cloud(cfg.n_persp, device=dev)
+    persp_all = torch.empty((cfg.n_persp, 3), dtype=torch.float64, device=dev)
+    nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode,
+                            out=persp_all)
+    # --persp N --stride S: N perspectives j = 0, S, 2S, ... (one rank's strided shard of D at S ranks)
+    persp = persp_all[::stride][:n_use].contiguous()
+    out = nbt.empty_cloud(persp.shape[0], device=dev)
     nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=out)
     ctx.sync()
     ctx.set_profiling(True)
@@ -50,8 +54,9 @@ def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=()):
     counts = out.counts.cpu().numpy()
     lookups = float(counts[:, 3].sum())
     ms /= n
+    rays = cfg.rays_per_id // cfg.n_persp * persp.shape[0]
     return {"config": cfg_name, "store": "8-bit prob" if prob else f"{bits}-bit {layout}", "trace_ms": ms,
-            "rays_per_s": cfg.rays_per_id / (ms / 1e3), "lookups_per_s": lookups / (ms / 1e3),
+            "persp": int(persp.shape[0]), "rays_per_s": rays / (ms / 1e3), "lookups_per_s": lookups / (ms / 1e3),
             "lookups": lookups, "checksum": int(counts.sum())}
 
 
@@ -64,7 +69,10 @@ if __name__ == "__main__":
     ap.add_argument("--bits", type=int, default=2)
     ap.add_argument("--opt", action="append", default=[])
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--persp", type=int, default=None, help="use N of the config's perspectives")
+    ap.add_argument("--stride", type=int, default=1, help="... taking every S-th (a strided rank shard)")
     a = ap.parse_args()
     opts = [(o.split("=")[0], int(o.split("=")[1])) for o in a.opt]
     for name in a.configs:
-        print(json.dumps(run(name, reps=a.reps, prob=a.prob, layout=a.layout, bits=a.bits, opts=opts)), flush=True)
+        print(json.dumps(run(name, reps=a.reps, prob=a.prob, layout=a.layout, bits=a.bits, opts=opts,
+                             persp=a.persp, stride=a.stride)), flush=True)
