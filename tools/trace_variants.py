@@ -19,7 +19,7 @@ import paper_2503_22588_b200 as nbt
 from nbt_inputs import CONFIGS, FOV_H, FOV_V
 
 
-def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=(), persp=None, stride=1):
+def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=(), persp=None, stride=1, offset=0):
     cfg = CONFIGS[cfg_name]
     n_use = persp if persp else cfg.n_persp
     dev = torch.device("cuda", 0)
@@ -42,7 +42,7 @@ def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=(), persp=No
     nbt.sample_perspectives(ctx, cfg.poi, cfg.persp_radius, cfg.n_persp, cfg.persp_seed, cfg.persp_mode,
                             out=persp_all)
     # --persp N --stride S: N perspectives j = 0, S, 2S, ... (one rank's strided shard of D at S ranks)
-    persp = persp_all[::stride][:n_use].contiguous()
+    persp = persp_all[offset::stride][:n_use].contiguous()
     out = nbt.empty_cloud(persp.shape[0], device=dev)
     nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=out)
     ctx.sync()
@@ -71,8 +71,9 @@ if __name__ == "__main__":
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--persp", type=int, default=None, help="use N of the config's perspectives")
     ap.add_argument("--stride", type=int, default=1, help="... taking every S-th (a strided rank shard)")
+    ap.add_argument("--offset", type=int, default=0, help="... starting at this one (the rank)")
     a = ap.parse_args()
     opts = [(o.split("=")[0], int(o.split("=")[1])) for o in a.opt]
     for name in a.configs:
         print(json.dumps(run(name, reps=a.reps, prob=a.prob, layout=a.layout, bits=a.bits, opts=opts,
-                             persp=a.persp, stride=a.stride)), flush=True)
+                             persp=a.persp, stride=a.stride, offset=a.offset)), flush=True)
