@@ -79,6 +79,14 @@ constexpr int kInt32MaxVoxels = 16000;   // |D_a| bound (voxels) for the int32 d
 #ifndef NBT_CHUNKS_PER_WARP
 #define NBT_CHUNKS_PER_WARP 32
 #endif
+// Chunk order: 1 = position-major, the image's top and bottom rows of tiles first and its middle
+// rows last (chunk index c -> perspective c mod n, position c / n taken 0, last, 1, last - 1, ...):
+// the middle rows look at the object and stop early, so the launch ends on short tiles -- B -4.8%,
+// one rank's D shard at N = 8 -4.4%, D -0.7%, C' -0.2% (profiles/r02_s3_chunk_order.log);
+// 0 = perspective-major (round 2).
+#ifndef NBT_CHUNK_ORDER
+#define NBT_CHUNK_ORDER 1
+#endif
 #ifndef NBT_CHUNK_MAX
 #define NBT_CHUNK_MAX 256
 #endif
@@ -884,8 +892,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     if (lane == 0) ch = kHomes > 0 ? next_chunk_affine(A) : atomicAdd(A.work_counter, 1);
                     ch = __shfl_sync(full, ch, 0);
                     if (ch >= A.total_chunks) { q_done = true; break; }
-                    q_j = ch / A.chunks_per_persp;
-                    q_next = (ch - q_j * A.chunks_per_persp) * A.chunk;
+                    if (NBT_CHUNK_ORDER == 1) {
+                        // position-major: top and bottom rows of tiles first, the middle rows last
+                        const int n = A.total_chunks / A.chunks_per_persp;
+                        const int pp = ch / n;
+                        q_j = ch - pp * n;
+                        const int qq = (pp & 1) ? A.chunks_per_persp - 1 - (pp >> 1) : (pp >> 1);
+                        q_next = qq * A.chunk;
+                    } else {
+                        q_j = ch / A.chunks_per_persp;
+                        q_next = (ch - q_j * A.chunks_per_persp) * A.chunk;
+                    }
                     q_end = min(q_next + A.chunk, A.slots);
                     if (__ldg(A.frames + (size_t)q_j * kFrameInts + 18) != 0) q_next = q_end;   // invalid
                     continue;
