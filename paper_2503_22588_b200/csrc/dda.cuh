@@ -59,24 +59,30 @@ struct Walk {
 template <typename T>
 __device__ __forceinline__ void walk_setup(Walk<T> &w, const int o[3], const int e[3])
 {
-    long long ad[3], N[3];
+    // 32-bit operands throughout (|D| < 2^31: both ends inside (-2^30, 2^30); N in [0, 65536];
+    // v << 16 in [-2^30, 2^30]), 64-bit only for the products N_a |D_b| < 2^47 (one 32x32->64
+    // multiply-add each)
+    uint32_t ad[3], N[3];
     int neg[3], v[3];
     int n = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        int D = e[a] - o[a];                     // |D| < 2^31: both ends inside (-2^30, 2^30)
+        const int D = e[a] - o[a];
         neg[a] = D < 0;
-        ad[a] = neg[a] ? -(long long)D : (long long)D;
+        ad[a] = neg[a] ? (uint32_t)(-D) : (uint32_t)D;
         v[a] = o[a] >> kQShift;                  // floor
-        int ve = e[a] >> kQShift;
+        const int ve = e[a] >> kQShift;
         n += (ve > v[a]) ? ve - v[a] : v[a] - ve;
-        N[a] = neg[a] ? (long long)o[a] - ((long long)v[a] << kQShift)
-                      : (((long long)v[a] + 1) << kQShift) - o[a];          // in [0, 65536]
+        N[a] = neg[a] ? (uint32_t)(o[a] - (v[a] << kQShift))
+                      : (uint32_t)(((v[a] + 1) << kQShift) - o[a]);   // in [0, 65536]
     }
     // tie favours the lower axis unless it moves negatively and the other positively
-    long long fxy = N[0] * ad[1] - N[1] * ad[0] - ((neg[0] && !neg[1]) ? 0 : 1);
-    long long fxz = N[0] * ad[2] - N[2] * ad[0] - ((neg[0] && !neg[2]) ? 0 : 1);
-    long long fyz = N[1] * ad[2] - N[2] * ad[1] - ((neg[1] && !neg[2]) ? 0 : 1);
+    const long long fxy = (long long)((unsigned long long)N[0] * ad[1]) - (long long)((unsigned long long)N[1] * ad[0]) -
+                          ((neg[0] && !neg[1]) ? 0 : 1);
+    const long long fxz = (long long)((unsigned long long)N[0] * ad[2]) - (long long)((unsigned long long)N[2] * ad[0]) -
+                          ((neg[0] && !neg[2]) ? 0 : 1);
+    const long long fyz = (long long)((unsigned long long)N[1] * ad[2]) - (long long)((unsigned long long)N[2] * ad[1]) -
+                          ((neg[1] && !neg[2]) ? 0 : 1);
     w.qxy = (T)(fxy >> kQShift);                 // arithmetic shift = floor division by S
     w.qxz = (T)(fxz >> kQShift);
     w.qyz = (T)(fyz >> kQShift);
