@@ -2,19 +2,19 @@
 //
 //   k_persp_frames  per perspective: view frame (Q4) and its Q16 quantisation
 //                   (Q19), bound checks; zeroes the per-perspective totals.
-//   k_id_trace      persistent warps with per-lane refill: every lane owns one ray at a
-//                   time; when it finishes, the warp hands it the next ray of the
-//                   current chunk (a run of one perspective's rays in 8x4 pixel tiles).
-//                   The lane builds its endpoint on the far plane in registers
-//                   (Q27) on the frame's Q16 lattice, and walks the exact
-//                   integer 3D-DDA (Q13) through the 2-bit map in batches of K = 16
-//                   voxels: the DDA does not depend on the map, so a batch computes
-//                   K voxel indices, issues K independent loads, packs the
-//                   2-bit codes into one word and finds the first Occupied / outside
-//                   voxel with one ffs (early stop) and the Free count with one
-//                   popc.  Ray set-up (frame, endpoint, 64-bit DDA init, grid entry)
-//                   runs converged for 32 rays at a time into a per-warp shared-memory
-//                   queue; lanes refill from it when their ray ends.  Per-state visit
+//   k_id_trace      persistent warps walking 8x4 pixel tiles in lockstep: a warp takes
+//                   chunks of one perspective's ray slots from a global counter (handed
+//                   out position-major, the image's middle tile rows last), prepares a
+//                   tile's 32 rays at once (frame, endpoint on the far plane in registers,
+//                   P:158-169, Q27, on the frame's Q16 lattice; DDA init; grid entry) and
+//                   walks them together until all have ended (NBT_OPT_TRACE_REFILL_MIN
+//                   < 32: per-lane refills from the prepared-ray queue instead).  Each
+//                   lane walks the exact integer 3D-DDA (Q13) through the map in batches
+//                   of K = 16 voxels: the DDA does not depend on the map, so a batch
+//                   computes K voxel indices, issues K independent loads, packs the
+//                   codes into one word (visit 0 at the top) and finds the first
+//                   Occupied / outside voxel with one clz (early stop) and the
+//                   Free count with one popc.  Per-state visit
 //                   counts (Eq. 2 as integers, Q26) accumulate in registers and are
 //                   flushed warp-combined (one u64 atomic per counter per warp and
 //                   perspective) when lanes move to another perspective.  A separate
