@@ -536,6 +536,22 @@ __device__ __forceinline__ int next_chunk_affine(const TraceArgs &A)
     return A.total_chunks;
 }
 
+// Chunk index -> (perspective, first slot) in the NBT_CHUNK_ORDER order.
+__device__ __forceinline__ void decode_chunk(const TraceArgs &A, int ch, int &q_j, int &q_next)
+{
+    if (NBT_CHUNK_ORDER == 1) {
+        // position-major: top and bottom rows of tiles first, the middle rows last
+        const int n = A.total_chunks / A.chunks_per_persp;
+        const int pp = ch / n;
+        q_j = ch - pp * n;
+        const int qq = (pp & 1) ? A.chunks_per_persp - 1 - (pp >> 1) : (pp >> 1);
+        q_next = qq * A.chunk;
+    } else {
+        q_j = ch / A.chunks_per_persp;
+        q_next = (ch - q_j * A.chunks_per_persp) * A.chunk;
+    }
+}
+
 // REC instance (nbt_debug_id_rays): the per-ray record array lives in the same buffer.
 constexpr int kRecordOffset = 64;       // ints (after the peer totals)
 static_assert(kPeerTotalsOffset * 4 + sizeof(PeerTotals) <= kRecordOffset * 4, "record after the peer totals");
@@ -822,15 +838,18 @@ constexpr int trace_min_blocks()
 // REC = per-ray record instance (nbt_debug_id_rays): the same code, which also writes every
 // closed ray's counts to the record array; a separate instance, so the production kernel's
 // code is unchanged.
-template <typename T, int L, int VB, int K, bool PIPE, bool SHARD, bool REC = false>
+// LOCK: the lockstep walk (NBT_OPT_TRACE_REFILL_MIN = 32, the default) specialised -- a tile's rays
+// prepared straight into the lanes' walks (no queue, no shared memory) and the batch loop left when
+// no lane walks (one vote).  LOCK = false: the general form with per-lane refills from a queue.
+template <typename T, int L, int VB, int K, bool PIPE, bool SHARD, bool REC = false, bool LOCK = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()) k_id_trace(TraceArgs A)
 {
     constexpr bool CYCLE = PIPE && VB != kStoreProb;     // in-place pipeline (batch_cycle)
     static_assert((CYCLE ? 2 * K : K) <= kBorder, "look-ahead must stay inside the sentinel shell");
     static_assert(!(REC && (SHARD || CYCLE)), "the record instance is the whole-ID, unpipelined walk");
-    using Queue = std::conditional_t<REC, WalkQueueRec<T>, WalkQueue<T>>;
-    __shared__ Queue queues[kWarpsPerBlock];
-    Queue &Q = queues[threadIdx.x >> 5];
+    using Queue = std::conditional_t<LOCK, char, std::conditional_t<REC, WalkQueueRec<T>, WalkQueue<T>>>;
+    __shared__ Queue queues[LOCK ? 1 : kWarpsPerBlock];
+    Queue &Q = queues[LOCK ? 0 : (threadIdx.x >> 5)];
     constexpr bool TAB = kDdaTable && sizeof(T) == 4 && L == kLayoutLinear && !CYCLE;
     __shared__ int4 step_tab[TAB ? kWarpsPerBlock * 96 : 1];
     // this lane's z-step entry: step_tab[warp][2][lane] (x, y entries 64 and 32 int4 below)
@@ -881,10 +900,57 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     }
                 }
             }
-            need = __ballot_sync(full, !have);
-            if (__popc(need) >= thr) break;
+            if constexpr (LOCK) {
+                if (!__any_sync(full, have)) break;
+            } else {
+                need = __ballot_sync(full, !have);
+                if (__popc(need) >= thr) break;
+            }
         }
-        {
+        if constexpr (LOCK) {
+            // every lane is idle: the next 32-ray unit, prepared straight into the lanes' walks
+            for (;;) {
+                if (q_next >= q_end) {
+                    int ch = 0;
+                    if (lane == 0) ch = kHomes > 0 ? next_chunk_affine(A) : atomicAdd(A.work_counter, 1);
+                    ch = __shfl_sync(full, ch, 0);
+                    if (ch >= A.total_chunks) { q_done = true; break; }
+                    decode_chunk(A, ch, q_j, q_next);
+                    q_end = min(q_next + A.chunk, A.slots);
+                    if (__ldg(A.frames + (size_t)q_j * kFrameInts + 18) != 0) q_next = q_end;   // invalid
+                    continue;
+                }
+                const int avail = min(32, q_end - q_next);
+                int slot0 = q_next, valid = avail;
+                if (SHARD) {
+                    if (q_next < A.local_tile_slots) {
+                        slot0 = ((q_next >> 5) * A.ray_world + A.ray_rank) << 5;
+                        valid = min(avail, A.n_tile_slots - slot0);
+                    } else {
+                        slot0 = q_next - A.local_tile_slots + A.n_tile_slots;
+                    }
+                }
+                const bool ok = lane < valid && prep_ray<T, L, VB, SHARD, REC>(A, q_j, slot0 + lane, w);
+                q_next += avail;
+                if (!__any_sync(full, ok)) continue;
+                // lanes moving to another perspective flush their counts (warp-combined)
+                const bool fl = ok && q_j != jl;
+                if (SHARD && peer_totals_of(A)->n > 0)
+                    flush_counts_warp_peer<VB == kStoreProb>(peer_totals_of(A), jl, c, fl, lane);
+                else
+                    flush_counts_warp<VB == kStoreProb>(A.totals, jl, c, fl, lane);
+                if (ok) {
+                    jl = q_j;
+                    have = 1;
+                    if constexpr (REC) my_slot = slot0 + lane;
+                    if (TAB) table_put(tz, w);
+                    if (CYCLE) batch_issue<T, L, VB, K>(w, A.m, b0);
+                }
+                break;
+            }
+            if (q_done) break;                   // every lane idle and no work left
+            continue;
+        } else {
             // all 32 lanes prepare up to 32 rays at once, so the set-up runs converged
             while (qcount == 0 && !q_done) {
                 if (q_next >= q_end) {
@@ -892,17 +958,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     if (lane == 0) ch = kHomes > 0 ? next_chunk_affine(A) : atomicAdd(A.work_counter, 1);
                     ch = __shfl_sync(full, ch, 0);
                     if (ch >= A.total_chunks) { q_done = true; break; }
-                    if (NBT_CHUNK_ORDER == 1) {
-                        // position-major: top and bottom rows of tiles first, the middle rows last
-                        const int n = A.total_chunks / A.chunks_per_persp;
-                        const int pp = ch / n;
-                        q_j = ch - pp * n;
-                        const int qq = (pp & 1) ? A.chunks_per_persp - 1 - (pp >> 1) : (pp >> 1);
-                        q_next = qq * A.chunk;
-                    } else {
-                        q_j = ch / A.chunks_per_persp;
-                        q_next = (ch - q_j * A.chunks_per_persp) * A.chunk;
-                    }
+                    decode_chunk(A, ch, q_j, q_next);
                     q_end = min(q_next + A.chunk, A.slots);
                     if (__ldg(A.frames + (size_t)q_j * kFrameInts + 18) != 0) q_next = q_end;   // invalid
                     continue;
@@ -1160,23 +1216,28 @@ double max_ray_voxels(const nbt_camera &cam, double range, double voxel_size)
 }
 
 // The kernel instances: [ray shard][wide][layout][store: 2-bit, byte, byte + gain].
-#define NBT_TRACE_ROW(T, L, S)                                                                        \
-    {k_id_trace<T, L, kStore2, kBatchK, kPipe, S>, k_id_trace<T, L, kStoreByte, kBatchK, kPipe, S>, \
-     k_id_trace<T, L, kStoreProb, kBatchK, kPipe, S>}
-#define NBT_TRACE_SET(S)                                                          \
-    {{NBT_TRACE_ROW(int, kLayoutLinear, S), NBT_TRACE_ROW(int, kLayoutMorton, S)}, \
-     {NBT_TRACE_ROW(long long, kLayoutLinear, S), NBT_TRACE_ROW(long long, kLayoutMorton, S)}}
+// [lock][shard][wide][layout][store]
+#define NBT_TRACE_ROW(T, L, S, LK)                                                                                 \
+    {k_id_trace<T, L, kStore2, kBatchK, kPipe, S, false, LK>, k_id_trace<T, L, kStoreByte, kBatchK, kPipe, S, false, LK>, \
+     k_id_trace<T, L, kStoreProb, kBatchK, kPipe, S, false, LK>}
+#define NBT_TRACE_SET(S, LK)                                                              \
+    {{NBT_TRACE_ROW(int, kLayoutLinear, S, LK), NBT_TRACE_ROW(int, kLayoutMorton, S, LK)}, \
+     {NBT_TRACE_ROW(long long, kLayoutLinear, S, LK), NBT_TRACE_ROW(long long, kLayoutMorton, S, LK)}}
 using TraceFn = void (*)(TraceArgs);
-const TraceFn kTraceFns[2][2][2][3] = {NBT_TRACE_SET(false), NBT_TRACE_SET(true)};
+const TraceFn kTraceFns[2][2][2][2][3] = {{NBT_TRACE_SET(false, false), NBT_TRACE_SET(true, false)},
+                                          {NBT_TRACE_SET(false, true), NBT_TRACE_SET(true, true)}};
 #undef NBT_TRACE_SET
 #undef NBT_TRACE_ROW
-// The per-ray record instances (nbt_debug_id_rays): [wide][layout][store], unpipelined.
-#define NBT_TRACE_REC_ROW(T, L)                                                                            \
-    {k_id_trace<T, L, kStore2, kBatchK, false, false, true>, k_id_trace<T, L, kStoreByte, kBatchK, false, false, true>, \
-     k_id_trace<T, L, kStoreProb, kBatchK, false, false, true>}
-const TraceFn kTraceRecFns[2][2][3] = {{NBT_TRACE_REC_ROW(int, kLayoutLinear), NBT_TRACE_REC_ROW(int, kLayoutMorton)},
-                                       {NBT_TRACE_REC_ROW(long long, kLayoutLinear),
-                                        NBT_TRACE_REC_ROW(long long, kLayoutMorton)}};
+// The per-ray record instances (nbt_debug_id_rays): [lock][wide][layout][store], unpipelined.
+#define NBT_TRACE_REC_ROW(T, L, LK)                                                                 \
+    {k_id_trace<T, L, kStore2, kBatchK, false, false, true, LK>,                                    \
+     k_id_trace<T, L, kStoreByte, kBatchK, false, false, true, LK>,                                 \
+     k_id_trace<T, L, kStoreProb, kBatchK, false, false, true, LK>}
+#define NBT_TRACE_REC_SET(LK)                                                                \
+    {{NBT_TRACE_REC_ROW(int, kLayoutLinear, LK), NBT_TRACE_REC_ROW(int, kLayoutMorton, LK)}, \
+     {NBT_TRACE_REC_ROW(long long, kLayoutLinear, LK), NBT_TRACE_REC_ROW(long long, kLayoutMorton, LK)}}
+const TraceFn kTraceRecFns[2][2][2][3] = {NBT_TRACE_REC_SET(false), NBT_TRACE_REC_SET(true)};
+#undef NBT_TRACE_REC_SET
 #undef NBT_TRACE_REC_ROW
 
 using DebugFn = void (*)(MapView, const int32_t *, const int32_t *, int, int, int32_t *, uint8_t *, int32_t *,
@@ -1247,35 +1308,39 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     if (L.d_record)   // REC instance: where it writes the per-ray counts (debug entry, never captured)
         NBT_CUDA(cudaMemcpyAsync(counter + kRecordOffset, &L.d_record, sizeof(void *), cudaMemcpyHostToDevice,
                                  ctx->stream));
-    const TraceFn fn = L.d_record ? kTraceRecFns[wide][m->layout == kLayoutMorton][sk]
-                                  : kTraceFns[L.ray_world > 1 || peer][wide][m->layout == kLayoutMorton][sk];
-    const int fi = (wide ? 6 : 0) + (m->layout == kLayoutMorton ? 3 : 0) + sk;
+    const int lock = ctx->opt.refill_min >= 32;   // the lockstep instance (default) or per-lane refills
+    const TraceFn fn = L.d_record ? kTraceRecFns[lock][wide][m->layout == kLayoutMorton][sk]
+                                  : kTraceFns[lock][L.ray_world > 1 || peer][wide][m->layout == kLayoutMorton][sk];
+    const int fi = lock * 12 + (wide ? 6 : 0) + (m->layout == kLayoutMorton ? 3 : 0) + sk;
     if (ctx->trace_blocks_per_sm == 0) {
         // smallest shared-memory carveout that holds the walk queues of the resident blocks,
         // so the rest of the SM's 256 KB stays L1 for the map lines
         // preferred shared-memory carveout (NBT_OPT_TRACE_CARVEOUT, default 25; -1 = driver)
+        // (the lockstep instances hold no queue: the carveout applies to the refill instances)
         const int carve = ctx->opt.carveout;
         if (carve >= 0) {
-            for (auto &sh : kTraceFns)
-                for (auto &a : sh)
+            for (auto &lk : kTraceFns)
+                for (auto &sh : lk)
+                    for (auto &a : sh)
+                        for (auto &b : a)
+                            for (TraceFn f : b)
+                                NBT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            for (auto &lk : kTraceRecFns)
+                for (auto &a : lk)
                     for (auto &b : a)
                         for (TraceFn f : b)
                             NBT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-            for (auto &a : kTraceRecFns)
-                for (auto &b : a)
-                    for (TraceFn f : b)
-                        NBT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
         }
-        for (int k = 0; k < 12; ++k) {
+        for (int k = 0; k < 24; ++k) {
             int b = 0;
-            NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kTraceFns[0][k / 6][(k / 3) & 1][k % 3],
-                                                                   kWarpsPerBlock * 32, 0));
+            NBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &b, kTraceFns[k / 12][0][(k / 6) & 1][(k / 3) & 1][k % 3], kWarpsPerBlock * 32, 0));
             ctx->trace_bps[k] = b > 0 ? b : 1;
         }
-        ctx->trace_blocks_per_sm = ctx->trace_bps[0];
+        ctx->trace_blocks_per_sm = ctx->trace_bps[12];
         if (ctx->opt.verbose) {
             fprintf(stderr, "libnbt: k_id_trace resident blocks/SM");
-            for (int k = 0; k < 12; ++k) fprintf(stderr, " %d", ctx->trace_bps[k]);
+            for (int k = 0; k < 24; ++k) fprintf(stderr, " %d", ctx->trace_bps[k]);
             fprintf(stderr, " (carveout %d)\n", carve);
         }
     }

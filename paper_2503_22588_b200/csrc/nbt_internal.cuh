@@ -148,7 +148,7 @@ struct nbt_ctx_s {
     int *h_err = nullptr;             // pinned mirror
     NbtOptions opt;
     int trace_blocks_per_sm = 0;      // cached occupancy of the trace kernel (0: recompute at the next launch)
-    int trace_bps[12] = {0};          // ... per instance [wide][morton][store kind]
+    int trace_bps[24] = {0};          // ... per instance [lockstep][wide][morton][store kind]
     // scratch
     nbt::DevBuf persp;                // staged perspective origins (n x 3 f64)
     nbt::DevBuf frames;               // per-perspective Q16 frames
