@@ -1222,3 +1222,25 @@ def test_map_extent_limit_of_the_bit_offset_walk(nbt, ctx):
     assert "2^31" in str(ei.value)
     m = nbt.Map(ctx, nbt.map_desc(1255, 1255, 8, 0.01))   # (1287^2 * 40) < 2^31: accepted
     m.close()
+
+
+def test_trace_schedules_agree_on_config_b(nbt, ctx):
+    """The lockstep walk (default, NBT_OPT_TRACE_REFILL_MIN = 32) and the per-lane refill forms
+    (thresholds 1 and 6, the queue instance) give the same integer totals and g_P bit for bit on
+    config B's map and camera (64 perspectives), and equal the oracle on a few of them."""
+    cfg = CONFIGS["B"]
+    m, om = make_map(nbt, ctx, cfg.map_codes(), cfg.voxel_size)
+    P = oracle.sample_perspectives(cfg.poi, cfg.persp_radius, 64, cfg.persp_seed, cfg.persp_mode)
+    cam = nbt.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    ref = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
+    try:
+        for thr in (1, 6):
+            ctx.set_option(nbt.OPT_TRACE_REFILL_MIN, thr)
+            alt = nbt.id_compute(ctx, m, cfg.poi, P, cam, cfg.range_)
+            assert np.array_equal(alt.counts, ref.counts) and np.array_equal(alt.gain, ref.gain), thr
+    finally:
+        ctx.set_option(nbt.OPT_TRACE_REFILL_MIN, 32)
+    ocam = oracle.camera_from_fov(FOV_H, FOV_V, cfg.width, cfg.height)
+    _, g, c = oracle.id_compute(om, cfg.poi, P[:4], ocam, cfg.range_)
+    assert np.array_equal(ref.counts[:4].astype(np.int64), c)
+    assert np.array_equal(ref.gain[:4], g)
