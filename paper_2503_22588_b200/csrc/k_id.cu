@@ -84,6 +84,9 @@ constexpr int kInt32MaxVoxels = 16000;   // |D_a| bound (voxels) for the int32 d
 // the middle rows look at the object and stop early, so the launch ends on short tiles -- B -4.8%,
 // one rank's D shard at N = 8 -4.4%, D -0.7%, C' -0.2% (profiles/r02_s3_chunk_order.log);
 // 0 = perspective-major (round 2).
+#ifndef NBT_SPLIT_TAIL
+#define NBT_SPLIT_TAIL 2           // chunks per resident warp handed out as halves at the launch's end
+#endif
 #ifndef NBT_CHUNK_ORDER
 #define NBT_CHUNK_ORDER 1
 #endif
@@ -498,6 +501,8 @@ struct TraceArgs {
     int min_refill;             // idle lanes needed before a warp refills (experiments)
     int ray_rank, ray_world;    // ray shard: this call walks 32-slot units u = ray_rank mod ray_world
     int local_tile_slots;       // lattice slots of this shard (its units * 32)
+    int split_from;             // chunks from this index on are handed out as two half chunks
+    int total_grabs;            // split_from + 2 * (total_chunks - split_from)
 };
 
 // SHARD instance: the peer totals of a fused ray split live in the work-counter buffer, after
@@ -550,6 +555,25 @@ __device__ __forceinline__ void decode_chunk(const TraceArgs &A, int ch, int &q_
         q_j = ch / A.chunks_per_persp;
         q_next = (ch - q_j * A.chunks_per_persp) * A.chunk;
     }
+}
+
+// Grab g of the work counter -> the slot range [q_next, q_end) of perspective q_j; false once the
+// work is out.  The launch's last chunks (from split_from on, NBT_SPLIT_TAIL per resident warp) are
+// handed out as two halves, so the end of the launch waits on half chunks.
+__device__ __forceinline__ bool take_grab(const TraceArgs &A, int g, int &q_j, int &q_next, int &q_end)
+{
+    if (g >= A.total_grabs) return false;
+    int ch = g, len = A.chunk, half = 0;
+    if (g >= A.split_from) {
+        const int h = g - A.split_from;
+        ch = A.split_from + (h >> 1);
+        len = A.chunk >> 1;
+        half = h & 1;
+    }
+    decode_chunk(A, ch, q_j, q_next);
+    q_next += half * len;
+    q_end = min(q_next + len, A.slots);
+    return true;
 }
 
 // REC instance (nbt_debug_id_rays): the per-ray record array lives in the same buffer.
@@ -914,9 +938,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     int ch = 0;
                     if (lane == 0) ch = kHomes > 0 ? next_chunk_affine(A) : atomicAdd(A.work_counter, 1);
                     ch = __shfl_sync(full, ch, 0);
-                    if (ch >= A.total_chunks) { q_done = true; break; }
-                    decode_chunk(A, ch, q_j, q_next);
-                    q_end = min(q_next + A.chunk, A.slots);
+                    if (!take_grab(A, ch, q_j, q_next, q_end)) { q_done = true; break; }
                     if (__ldg(A.frames + (size_t)q_j * kFrameInts + 18) != 0) q_next = q_end;   // invalid
                     continue;
                 }
@@ -957,9 +979,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, trace_min_blocks<T, VB>()
                     int ch = 0;
                     if (lane == 0) ch = kHomes > 0 ? next_chunk_affine(A) : atomicAdd(A.work_counter, 1);
                     ch = __shfl_sync(full, ch, 0);
-                    if (ch >= A.total_chunks) { q_done = true; break; }
-                    decode_chunk(A, ch, q_j, q_next);
-                    q_end = min(q_next + A.chunk, A.slots);
+                    if (!take_grab(A, ch, q_j, q_next, q_end)) { q_done = true; break; }
                     if (__ldg(A.frames + (size_t)q_j * kFrameInts + 18) != 0) q_next = q_end;   // invalid
                     continue;
                 }
@@ -1358,6 +1378,10 @@ nbt_status launch_id(nbt_ctx ctx, nbt_map m, const IdLaunch &L)
     long long tc = (long long)T.chunks_per_persp * L.n;
     if (tc >= (1ll << 31)) return fail(NBT_ERR_INVALID_ARG, "nbt_id_compute: too many rays in one call");
     T.total_chunks = (int)tc;
+    // the last NBT_SPLIT_TAIL chunks per resident warp as half chunks (chunks of >= 64 slots)
+    const long long tail = (long long)NBT_SPLIT_TAIL * resident_warps;
+    T.split_from = (kHomes > 0 || chunk < 64 || tail == 0) ? T.total_chunks : (int)(tc > tail ? tc - tail : 0);
+    T.total_grabs = T.split_from + 2 * (T.total_chunks - T.split_from);
     T.min_refill = ctx->opt.refill_min;   // NBT_OPT_TRACE_REFILL_MIN (profiles/r01_refill_sweep.log)
     long long want_blocks = (tc + kWarpsPerBlock - 1) / kWarpsPerBlock;
     long long max_blocks = (long long)ctx->num_sms * bps;
