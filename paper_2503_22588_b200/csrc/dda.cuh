@@ -8,6 +8,10 @@
 namespace nbt {
 namespace dda {
 
+#ifndef NBT_DDA_PRED
+#define NBT_DDA_PRED 1   // 0: the flag form of the int32 step for the linear layout too (A/B builds)
+#endif
+
 constexpr int kQShift = 16;      // walk coordinates: Q16, the frames' lattice
 
 struct MapView {
@@ -112,15 +116,41 @@ __device__ __forceinline__ int mad_i32(int a, int b, int c)
 // (axes walked in + direction are stored complemented within their bits), i.e.
 // r = (r - lsb) & mask, and the address is (rx | ry | rz) ^ xinv.
 //
-// Hot path (int32, no coordinates): the axis choice as 0/1 flags from the sign bits (2 LOP3 +
-// 2 SHF) and npz = px + py - 1 (one IADD3), the updates as multiply-adds by the flags -- 5 ALU ops
-// and 9 multiply-adds per step.  (Measured alternatives: 0/-1 masks with the
-// negated magnitudes, within +-1.6% depending on how ptxas schedules the batch; one or two decision
-// terms on the ALU pipe as AND + 3-input add, 4-14% slower: the step is issue-bound.)
+// Hot path (int32, no coordinates, linear layout): the axis choice as four predicates (4 ISETP,
+// chained on the previous results), the decision-term updates as 6 predicated adds and the new
+// index as one add and two predicated overwrites -- 13 instructions, none with more than two register sources, which ptxas
+// spreads over the ALU (IADD3) and FMA (VIADD) pipes.  The register-only ceiling of this form is
+// 2.23e12 visits/s against 1.92e12 for the earlier flag form (0/1 flags from the sign bits, 5 ALU
+// ops and 9 multiply-adds by the flags: three register sources each), same decision terms
+// (tools/dda_step_forms.cu, profiles/r02_s4_step_forms.log).  The Morton layout keeps the flag form.
+// (Measured alternatives: 0/-1 masks with the negated magnitudes; one or two
+// decision terms on the ALU pipe as AND + 3-input add, 4-14% slower.)
 template <typename T, int L, bool COORDS>
 __device__ __forceinline__ void walk_step(Walk<T> &w, const MapView &m)
 {
-    if constexpr (sizeof(T) == 4 && !COORDS) {
+    if constexpr (sizeof(T) == 4 && !COORDS && L != kLayoutMorton && NBT_DDA_PRED) {
+        // x first: q_xy < 0 and q_xz < 0; y first: not x and q_yz < 0; z first: neither
+        // the new index goes to a fresh register (the batch still reads the old one for its
+        // rotate): one unconditional add and two predicated overwrites
+        uint32_t nidx;
+        asm("{\n\t.reg .pred t, px, py, pz;\n\t"
+            "setp.lt.s32 t, %1, 0;\n\t"
+            "setp.lt.and.s32 px, %0, 0, t;\n\t"
+            "setp.lt.and.s32 py, %2, 0, !px;\n\t"
+            "setp.ge.and.s32 pz, %2, 0, !px;\n\t"
+            "sub.s32 %3, %4, %10;\n\t"
+            "@px add.s32 %0, %0, %5;\n\t"
+            "@px add.s32 %1, %1, %6;\n\t"
+            "@px add.s32 %3, %4, %8;\n\t"
+            "@py sub.s32 %0, %0, %7;\n\t"
+            "@py add.s32 %2, %2, %6;\n\t"
+            "@py add.s32 %3, %4, %9;\n\t"
+            "@pz sub.s32 %1, %1, %7;\n\t"
+            "@pz sub.s32 %2, %2, %5;\n\t}"
+            : "+r"(w.qxy), "+r"(w.qxz), "+r"(w.qyz), "=&r"(nidx)
+            : "r"(w.idx), "r"(w.ay), "r"(w.az), "r"(w.ax), "r"(w.dX), "r"(w.dY), "r"(w.ndZ));
+        w.idx = nidx;
+    } else if constexpr (sizeof(T) == 4 && !COORDS) {
         const int t1 = w.qxy & w.qxz;            // sign: x first
         const int t2 = w.qyz & ~t1;              // sign: y first
         const int px = (int)((unsigned)t1 >> 31);
