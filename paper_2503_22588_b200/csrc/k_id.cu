@@ -265,6 +265,9 @@ __device__ __forceinline__ void walk_step_table(Walk<T> &w, uint32_t tz)
     w.idx = (uint32_t)mad_i32(1, di, (int)w.idx);
 }
 
+#ifndef NBT_BYTE_ASM
+#define NBT_BYTE_ASM 1
+#endif
 // Issue the K loads of the next K visits (the DDA does not depend on the map, so
 // this runs ahead of the codes) and advance the DDA by K steps.
 template <typename T, int L, int VB, int K, bool TAB = false>
@@ -277,6 +280,10 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
             const uint32_t ib = L == kLayoutLinear ? w.idx : (w.idx << 1);   // the code's bit offset
             b.rot[k] = ib;                       // rotate amounts are taken mod 32
             b.wd[k] = load_map_word(m.words + (ib >> 5));
+        } else if (VB == kStoreByte && NBT_BYTE_ASM) {
+            // the byte lands zero-extended in a 32-bit register: the packing shift-adds need
+            // no mask (through __ldg the compiler re-masks every byte before packing)
+            asm("ld.global.nc.u8 %0, [%1];" : "=r"(b.wd[k]) : "l"(bytes + w.idx));
         } else {
             b.wd[k] = __ldg(bytes + w.idx);
         }
