@@ -227,7 +227,8 @@ __device__ __forceinline__ uint32_t load_map_word(const uint32_t *p)
 // Step table (NBT_DDA_TABLE experiment, linear layout, int32 terms): per lane, the three
 // possible updates (dq_xy, dq_xz, dq_yz, d_idx) of a step along x, y, z in shared memory,
 // written when the lane takes a ray; a step is then the axis choice (2 LOP3 + 2 SHF), one
-// 16-byte shared load and 4 adds instead of the 9 mask multiply-adds of walk_step.
+// 16-byte shared load and 4 adds instead of the 9 flag multiply-adds of the round-2 walk_step
+// (walk_step itself is now 4 compares and 9 predicated adds, dda.cuh).
 #ifndef NBT_DDA_TABLE
 #define NBT_DDA_TABLE 0
 #endif
