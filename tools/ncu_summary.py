@@ -15,6 +15,11 @@ KEYS = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
     ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe % of peak"),
     ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe % of peak"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64 pipe % of peak"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU pipe % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 data-pipe wavefronts % of peak"),
+    ("sm__cycles_active.avg", "SM active cycles (mean over SMs)"),
+    ("gpc__cycles_elapsed.max", "elapsed cycles"),
     ("smsp__thread_inst_executed_per_inst_executed.ratio", "active threads / warp instr"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("l1tex__t_sector_hit_rate.pct", "L1 sector hit rate %"),
