@@ -281,7 +281,7 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
             const uint32_t ib = L == kLayoutLinear ? w.idx : (w.idx << 1);   // the code's bit offset
             b.rot[k] = ib;                       // rotate amounts are taken mod 32
             b.wd[k] = load_map_word(m.words + (ib >> 5));
-        } else if (VB == kStoreByte && NBT_BYTE_ASM) {
+        } else if (NBT_BYTE_ASM) {
             // the byte lands zero-extended in a 32-bit register: the packing shift-adds need
             // no mask (through __ldg the compiler re-masks every byte before packing)
             asm("ld.global.nc.u8 %0, [%1];" : "=r"(b.wd[k]) : "l"(bytes + w.idx));

@@ -274,7 +274,9 @@ def test_integrate_few_dense_cells(nbt, ctx):
         ctx.sync()
         dt = time.perf_counter() - t0
         assert same_logodds(occ.download(), L)
-        assert dt < 0.25, f"{dt:.3f} s for one frame"
+        # a quadratic grouping of 400 k points per cell would take minutes; the bound leaves room
+        # for the host-side copies on a busy box (0.34 s seen once against ~0.1 s typical)
+        assert dt < 1.0, f"{dt:.3f} s for one frame"
 
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("NBT_FUZZ_SEEDS", "8"))))
