@@ -4,14 +4,14 @@ of beam / packet traversal for dense lattices, verdict r01 lever (a)): on config
 report the mean ray length (visits until the stop or the end), the mean common prefix of
 horizontally adjacent rays, and the prefix shared by all 32 rays of the tile.  Oracle only, CPU.
 
-    python tools/beam_prefix.py [--tiles 60] [--persp 3]
+    python tests/analysis/beam_prefix.py [--tiles 60] [--persp 3]
 """
 import argparse
 import json
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import numpy as np

@@ -6,14 +6,14 @@ per-perspective choice of the copy whose fast axis best matches the camera's hor
 a request = one visit index of the lockstep walk (all rays of the tile start together), over
 the lanes whose ray is still walking inside the grid.  Oracle only, CPU.
 
-    python tools/line_spread.py [--tiles 40] [--persp 12] [--configs D B]
+    python tests/analysis/line_spread.py [--tiles 40] [--persp 12] [--configs D B]
 """
 import argparse
 import json
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import numpy as np
