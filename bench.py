@@ -109,11 +109,16 @@ def l1_block(tr):
     bind it: D is L1-data-pipe bound, C' issue bound)."""
     if "l1_data_pipe_wavefronts_pct" not in tr:
         return {}
-    return {"l1": {"data_pipe_wavefronts_frac": tr["l1_data_pipe_wavefronts_pct"] / 100.0,
+    l1f, isf = tr["l1_data_pipe_wavefronts_pct"] / 100.0, tr["issue_active_pct"] / 100.0
+    return {"l1": {"data_pipe_wavefronts_frac": l1f,
                    "wavefronts_per_request": tr["l1_wavefronts_per_request"],
                    "sectors_per_request": tr["l1_sectors_per_request"], "hit_rate_pct": tr.get("l1_hit_rate_pct"),
-                   "issue_active_frac": tr["issue_active_pct"] / 100.0,
-                   "source": tr.get("source_l1")}}
+                   "issue_active_frac": isf,
+                   "source": tr.get("source_l1")},
+            # the busiest unit of the same capture: the kernel's real bound (the int32 frac above
+            # counts SURVEY's 12 algorithmic ops per lookup against the best integer mix)
+            "binding": {"unit": "l1_data_pipe" if l1f >= isf else "issue", "frac": max(l1f, isf),
+                        "source": "ncu --set full, one launch: l1tex__data_pipe_lsu_wavefronts vs smsp__issue_active"}}
 
 
 def host_cpu():
