@@ -9,7 +9,8 @@ namespace nbt {
 namespace dda {
 
 #ifndef NBT_DDA_PRED
-#define NBT_DDA_PRED 1   // 0: the flag form of the int32 step for the linear layout too (A/B builds)
+#define NBT_DDA_PRED 1   // 0: the flag form of the int32 step for the linear layout too, 3: x first from one
+                         // LOP3 with a predicate output instead of two compares (A/B builds)
 #endif
 
 constexpr int kQShift = 16;      // walk coordinates: Q16, the frames' lattice
@@ -133,10 +134,19 @@ __device__ __forceinline__ void walk_step(Walk<T> &w, const MapView &m)
         // the new index goes to a fresh register (the batch still reads the old one for its
         // rotate): one unconditional add and two predicated overwrites
         uint32_t nidx;
+#if NBT_DDA_PRED != 3
         asm("{\n\t.reg .pred t, px, py, pz;\n\t"
             "setp.lt.s32 t, %1, 0;\n\t"
             "setp.lt.and.s32 px, %0, 0, t;\n\t"
             "setp.lt.and.s32 py, %2, 0, !px;\n\t"
+#else
+        // x first from one LOP3 with a predicate output, (q_xy & q_xz & sign bit) != 0: one
+        // instruction fewer per step but C' +0.8% (profiles/r02_s4_lop3p.log), so not the default
+        asm("{\n\t.reg .pred tru, px, py, pz;\n\t.reg .b32 t;\n\t"
+            "setp.eq.u32 tru, 0, 0;\n\t"
+            "lop3.and.b32 t|px, %0, %1, 0x80000000, 0x80, tru;\n\t"
+            "setp.lt.and.s32 py, %2, 0, !px;\n\t"
+#endif
             "setp.ge.and.s32 pz, %2, 0, !px;\n\t"
             "sub.s32 %3, %4, %10;\n\t"
             "@px add.s32 %0, %0, %5;\n\t"
