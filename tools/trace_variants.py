@@ -19,7 +19,8 @@ import paper_2503_22588_b200 as nbt
 from nbt_inputs import CONFIGS, FOV_H, FOV_V
 
 
-def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=(), persp=None, stride=1, offset=0):
+def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=(), persp=None, stride=1, offset=0,
+        ray_world=1, ray_rank=0):
     cfg = CONFIGS[cfg_name]
     n_use = persp if persp else cfg.n_persp
     dev = torch.device("cuda", 0)
@@ -44,17 +45,24 @@ def run(cfg_name, reps=5, prob=False, layout="linear", bits=2, opts=(), persp=No
     # --persp N --stride S: N perspectives j = 0, S, 2S, ... (one rank's strided shard of D at S ranks)
     persp = persp_all[offset::stride][:n_use].contiguous()
     out = nbt.empty_cloud(persp.shape[0], device=dev)
-    nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=out)
+    if ray_world > 1:
+        # --ray-world W --ray-rank R: ray shard R of W of every perspective (the ray split)
+        def one():
+            return nbt.id_compute_rays(ctx, m, cfg.poi, persp, cam, cfg.range_, ray_rank, ray_world)
+    else:
+        def one():
+            return nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=out)
+    one()
     ctx.sync()
     ctx.set_profiling(True)
     ctx.profile_read(nbt.KERNEL_TRACE, reset=True)
     for _ in range(reps):
-        nbt.id_compute(ctx, m, cfg.poi, persp, cam, cfg.range_, out=out)
+        res = one()
     ms, n = ctx.profile_read(nbt.KERNEL_TRACE, reset=True)
-    counts = out.counts.cpu().numpy()
+    counts = res.cpu().numpy()[:, :4] if ray_world > 1 else out.counts.cpu().numpy()
     lookups = float(counts[:, 3].sum())
     ms /= n
-    rays = cfg.rays_per_id // cfg.n_persp * persp.shape[0]
+    rays = cfg.rays_per_id // cfg.n_persp * persp.shape[0] // ray_world
     return {"config": cfg_name, "store": "8-bit prob" if prob else f"{bits}-bit {layout}", "trace_ms": ms,
             "persp": int(persp.shape[0]), "rays_per_s": rays / (ms / 1e3), "lookups_per_s": lookups / (ms / 1e3),
             "lookups": lookups, "checksum": int(counts.sum())}
@@ -72,8 +80,11 @@ if __name__ == "__main__":
     ap.add_argument("--persp", type=int, default=None, help="use N of the config's perspectives")
     ap.add_argument("--stride", type=int, default=1, help="... taking every S-th (a strided rank shard)")
     ap.add_argument("--offset", type=int, default=0, help="... starting at this one (the rank)")
+    ap.add_argument("--ray-world", type=int, default=1, help="ray split: shards of every perspective's rays")
+    ap.add_argument("--ray-rank", type=int, default=0, help="... this shard")
     a = ap.parse_args()
     opts = [(o.split("=")[0], int(o.split("=")[1])) for o in a.opt]
     for name in a.configs:
         print(json.dumps(run(name, reps=a.reps, prob=a.prob, layout=a.layout, bits=a.bits, opts=opts,
-                             persp=a.persp, stride=a.stride, offset=a.offset)), flush=True)
+                             persp=a.persp, stride=a.stride, offset=a.offset, ray_world=a.ray_world,
+                             ray_rank=a.ray_rank)), flush=True)
