@@ -9,8 +9,10 @@ namespace nbt {
 namespace dda {
 
 #ifndef NBT_DDA_PRED
-#define NBT_DDA_PRED 1   // 0: the flag form of the int32 step for the linear layout too, 3: x first from one
-                         // LOP3 with a predicate output instead of two compares (A/B builds)
+#define NBT_DDA_PRED 1   // int32 step for the linear layout: 1 = predicated, "x first" from one LOP3 with a
+                         // predicate output where the caller asks for it (the 2-bit store) and from two
+                         // compares otherwise (the byte stores); 3 / 4 = LOP3 / two compares everywhere;
+                         // 0 = the flag form (A/B builds)
 #endif
 
 constexpr int kQShift = 16;      // walk coordinates: Q16, the frames' lattice
@@ -118,35 +120,29 @@ __device__ __forceinline__ int mad_i32(int a, int b, int c)
 // r = (r - lsb) & mask, and the address is (rx | ry | rz) ^ xinv.
 //
 // Hot path (int32, no coordinates, linear layout): the axis choice as four predicates (4 ISETP,
-// chained on the previous results), the decision-term updates as 6 predicated adds and the new
-// index as one add and two predicated overwrites -- 13 instructions, none with more than two register sources, which ptxas
+// chained on the previous results; or 1 LOP3 with a predicate output + 2 ISETP, XLOP), the
+// decision-term updates as 6 predicated adds and the new index as one add and two predicated
+// overwrites -- 13 (12) instructions, none with more than two register sources, which ptxas
 // spreads over the ALU (IADD3) and FMA (VIADD) pipes.  The register-only ceiling of this form is
 // 2.23e12 visits/s against 1.92e12 for the earlier flag form (0/1 flags from the sign bits, 5 ALU
 // ops and 9 multiply-adds by the flags: three register sources each), same decision terms
 // (tools/dda_step_forms.cu, profiles/r02_s4_step_forms.log).  The Morton layout keeps the flag form.
 // (Measured alternatives: 0/-1 masks with the negated magnitudes; one or two
 // decision terms on the ALU pipe as AND + 3-input add, 4-14% slower.)
-template <typename T, int L, bool COORDS>
+template <typename T, int L, bool COORDS, bool XLOP = false>
 __device__ __forceinline__ void walk_step(Walk<T> &w, const MapView &m)
 {
     if constexpr (sizeof(T) == 4 && !COORDS && L != kLayoutMorton && NBT_DDA_PRED) {
+        constexpr bool lop = NBT_DDA_PRED == 3 || (NBT_DDA_PRED == 1 && XLOP);
         // x first: q_xy < 0 and q_xz < 0; y first: not x and q_yz < 0; z first: neither
         // the new index goes to a fresh register (the batch still reads the old one for its
         // rotate): one unconditional add and two predicated overwrites
         uint32_t nidx;
-#if NBT_DDA_PRED != 3
-        asm("{\n\t.reg .pred t, px, py, pz;\n\t"
+        if constexpr (!lop) {
+            asm("{\n\t.reg .pred t, px, py, pz;\n\t"
             "setp.lt.s32 t, %1, 0;\n\t"
             "setp.lt.and.s32 px, %0, 0, t;\n\t"
             "setp.lt.and.s32 py, %2, 0, !px;\n\t"
-#else
-        // x first from one LOP3 with a predicate output, (q_xy & q_xz & sign bit) != 0: one
-        // instruction fewer per step but C' +0.8% (profiles/r02_s4_lop3p.log), so not the default
-        asm("{\n\t.reg .pred tru, px, py, pz;\n\t.reg .b32 t;\n\t"
-            "setp.eq.u32 tru, 0, 0;\n\t"
-            "lop3.and.b32 t|px, %0, %1, 0x80000000, 0x80, tru;\n\t"
-            "setp.lt.and.s32 py, %2, 0, !px;\n\t"
-#endif
             "setp.ge.and.s32 pz, %2, 0, !px;\n\t"
             "sub.s32 %3, %4, %10;\n\t"
             "@px add.s32 %0, %0, %5;\n\t"
@@ -159,6 +155,27 @@ __device__ __forceinline__ void walk_step(Walk<T> &w, const MapView &m)
             "@pz sub.s32 %2, %2, %5;\n\t}"
             : "+r"(w.qxy), "+r"(w.qxz), "+r"(w.qyz), "=&r"(nidx)
             : "r"(w.idx), "r"(w.ay), "r"(w.az), "r"(w.ax), "r"(w.dX), "r"(w.dY), "r"(w.ndZ));
+        } else {
+            // x first from one LOP3 with a predicate output, (q_xy & q_xz & sign bit) != 0: one
+            // instruction fewer on the ALU pipe (2-bit store: D -3.4%, B -3.5%; byte store: C'
+            // +0.8%, profiles/r02_s4_addrlea.log)
+            asm("{\n\t.reg .pred tru, px, py, pz;\n\t.reg .b32 t;\n\t"
+            "setp.eq.u32 tru, 0, 0;\n\t"
+            "lop3.and.b32 t|px, %0, %1, 0x80000000, 0x80, tru;\n\t"
+            "setp.lt.and.s32 py, %2, 0, !px;\n\t"
+            "setp.ge.and.s32 pz, %2, 0, !px;\n\t"
+            "sub.s32 %3, %4, %10;\n\t"
+            "@px add.s32 %0, %0, %5;\n\t"
+            "@px add.s32 %1, %1, %6;\n\t"
+            "@px add.s32 %3, %4, %8;\n\t"
+            "@py sub.s32 %0, %0, %7;\n\t"
+            "@py add.s32 %2, %2, %6;\n\t"
+            "@py add.s32 %3, %4, %9;\n\t"
+            "@pz sub.s32 %1, %1, %7;\n\t"
+            "@pz sub.s32 %2, %2, %5;\n\t}"
+            : "+r"(w.qxy), "+r"(w.qxz), "+r"(w.qyz), "=&r"(nidx)
+            : "r"(w.idx), "r"(w.ay), "r"(w.az), "r"(w.ax), "r"(w.dX), "r"(w.dY), "r"(w.ndZ));
+        }
         w.idx = nidx;
     } else if constexpr (sizeof(T) == 4 && !COORDS) {
         const int t1 = w.qxy & w.qxz;            // sign: x first

@@ -269,6 +269,9 @@ __device__ __forceinline__ void walk_step_table(Walk<T> &w, uint32_t tz)
 #ifndef NBT_BYTE_ASM
 #define NBT_BYTE_ASM 1
 #endif
+#ifndef NBT_ADDR_LEA
+#define NBT_ADDR_LEA 1     // 0: the 2-bit word address by SHF + IMAD.WIDE (A/B builds)
+#endif
 // Issue the K loads of the next K visits (the DDA does not depend on the map, so
 // this runs ahead of the codes) and advance the DDA by K steps.
 template <typename T, int L, int VB, int K, bool TAB = false>
@@ -280,7 +283,16 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
         if (VB == kStore2) {
             const uint32_t ib = L == kLayoutLinear ? w.idx : (w.idx << 1);   // the code's bit offset
             b.rot[k] = ib;                       // rotate amounts are taken mod 32
+#if NBT_ADDR_LEA
+            // the word address by a 64-bit shift and add: ptxas emits SHF + LEA + LEA.HI.X (ALU
+            // pipe) instead of SHF + IMAD.WIDE (FMA pipe, which the predicated step already fills)
+            const uint32_t *a;
+            asm("{\n\t.reg .u64 t;\n\tcvt.u64.u32 t, %1;\n\tshr.u64 t, t, 5;\n\tshl.b64 t, t, 2;\n\t"
+                "add.s64 %0, %2, t;\n\t}" : "=l"(a) : "r"(ib), "l"(m.words));
+            b.wd[k] = load_map_word(a);
+#else
             b.wd[k] = load_map_word(m.words + (ib >> 5));
+#endif
         } else if (NBT_BYTE_ASM) {
             // the byte lands zero-extended in a 32-bit register: the packing shift-adds need
             // no mask (through __ldg the compiler re-masks every byte before packing)
@@ -291,7 +303,7 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
         if constexpr (TAB)
             walk_step_table(w, tz);
         else
-            walk_step<T, L, false>(w, m);
+            walk_step<T, L, false, VB == kStore2>(w, m);
     }
 }
 
@@ -388,7 +400,7 @@ __device__ __forceinline__ uint32_t batch_cycle(Walk<T> &w, const MapView &m, Ba
         } else {
             b.wd[k] = __ldg(bytes + w.idx);
         }
-        walk_step<T, L, false>(w, m);
+        walk_step<T, L, false, VB == kStore2>(w, m);
     }
     return K >= 16 ? bits : bits << (32 - 2 * K);
 }

@@ -652,6 +652,9 @@ static nbt_status check_desc(const nbt_map_desc *d)
     return NBT_OK;
 }
 
+#ifndef NBT_BANK_PAD
+#define NBT_BANK_PAD 1     // 0: rows of nx + 2 kBorder voxels, planes of (nx + 2B)(ny + 2B) (A/B builds)
+#endif
 static nbt_status map_create(nbt_ctx ctx, const nbt_map_desc *desc, int vbits, bool prob, nbt_map *out)
 {
     nbt_status s;
@@ -666,6 +669,25 @@ static nbt_status map_create(nbt_ctx ctx, const nbt_map_desc *desc, int vbits, b
     m->vbits = vbits;
     m->prob = prob;
     m->px = desc->nx + 2 * kBorder; m->py = desc->ny + 2 * kBorder; m->pz = desc->nz + 2 * kBorder;
+#if NBT_BANK_PAD
+    if (desc->layout != NBT_LAYOUT_MORTON) {
+        // Extra sentinel columns / rows so that neighbouring rows fall into different L1 banks
+        // (4-byte banks, 32 of them): a row is an odd number of words (y step = sy words) and a
+        // plane is 17 words mod 32 (z step), so a warp's rays spread over a few rows and planes
+        // hit distinct banks instead of the plane-aligned same bank (D: px = 544 = 34 words,
+        // a plane 18496 words = 0 mod 32).  Skipped when it would break the 2^31 / 2^32 bound.
+        const uint32_t per = vbits == 2 ? 16 : 4;
+        uint32_t px = (m->px + per - 1) / per * per;
+        if (((px / per) & 1u) == 0) px += per;
+        const uint32_t sy = (px / per) & 31u;                      // odd
+        uint32_t inv = 1;
+        while ((sy * inv & 31u) != 1u) inv += 2;                   // sy^-1 mod 32
+        const uint32_t want = (17u * inv) & 31u;                   // py = want (mod 32)
+        const uint32_t py = m->py + ((want - (m->py & 31u)) & 31u);
+        const uint64_t nv = (uint64_t)px * py * m->pz;
+        if (nv < (vbits == 2 ? (1ull << 31) : (1ull << 32))) { m->px = px; m->py = py; }
+    }
+#endif
     m->nvox_pad = (uint64_t)m->px * m->py * m->pz;
     // Store layout (desc->layout): linear by default (fewest instructions per voxel step,
     // fastest on configs C' and D, profiles/r01_layouts.md), or the Morton cube (side >= max
