@@ -309,21 +309,32 @@ __device__ __forceinline__ void batch_issue(Walk<T> &w, const MapView &m, Batch<
 
 // Append the code of visit k of a batch below the codes packed so far: 2-bit store, one
 // rotate (code to bits 30-31) and one funnel shift; byte stores, one shift-add.
+#ifndef NBT_BYTE_REV
+#define NBT_BYTE_REV 0
+#endif
+// NBT_BYTE_REV = 1 (experiment): the byte store's batch word packed bottom-up (visit k at bits
+// 2k+1..2k), each code entering at the top by one funnel shift right -- an ALU instruction where
+// the top-down shift-add is an FMA-pipe IMAD; C' +0.5% (profiles/r02_s4_revpack.log), not the default.
+template <int VB>
+constexpr bool rev_pack() { return VB == kStoreByte && NBT_BYTE_REV; }
+
 template <int VB, int K>
 __device__ __forceinline__ uint32_t batch_push(uint32_t bits, const Batch<K> &b, int k)
 {
     if (VB == kStore2) return __funnelshift_l(__funnelshift_l(b.wd[k], b.wd[k], b.rot[k]), bits, 2);
+    if (rev_pack<VB>()) return __funnelshift_r(bits, b.wd[k], 2);  // (bits >> 2) | code << 30
     if (VB == kStoreByte) return bits * 4u + b.wd[k];             // the byte is the code (< 4)
     return (bits << 2) | (b.wd[k] & 3u);
 }
 
-// The packed codes of a whole batch, visit k at bits 31-2k..30-2k.
+// The packed codes of a whole batch, visit k at bits 31-2k..30-2k (bottom-up stores: 2k+1..2k).
 template <int VB, int K>
 __device__ __forceinline__ uint32_t batch_bits(const Batch<K> &b)
 {
     uint32_t bits = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) bits = batch_push<VB, K>(bits, b, k);
+    if (rev_pack<VB>()) return K >= 16 ? bits : bits >> (32 - 2 * K);
     return K >= 16 ? bits : bits << (32 - 2 * K);
 }
 
@@ -335,16 +346,20 @@ template <typename T, int VB, int K>
 __device__ __forceinline__ bool batch_finish(Walk<T> &w, uint32_t bits, uint32_t gsum, const Batch<K> &b,
                                              int policy, Counts &c)
 {
+    constexpr bool REV = rev_pack<VB>();        // visit k at bits 2k+1..2k
     const int left = w.n - w.s + 1;             // visits remaining, including the current one
-    const uint32_t valid = left >= K ? batch_mask<K>() : ~(0xFFFFFFFFu >> (2 * left));   // 1 <= left < 16
+    const uint32_t valid = REV ? (left >= K ? (K >= 16 ? 0xFFFFFFFFu : (1u << (2 * K)) - 1u)
+                                            : 0xFFFFFFFFu >> (32 - 2 * left))
+                               : (left >= K ? batch_mask<K>() : ~(0xFFFFFFFFu >> (2 * left)));   // 1 <= left < 16
     const uint32_t stop = bits & valid & 0xAAAAAAAAu;   // codes 2 (Occupied) and 3 (outside)
     if (stop || left <= K) {
         // last batch of the ray: only visits up to the stop (or the end) count.  The same counts
         // as walk_close_stop / walk_close_end in branch-free form: visit `last` is the stop (code
         // 2 Occupied: counted; 3: left the grid, Q14) or the ray's end (code 0 or 1).
-        const int last = stop ? (__clz(stop) >> 1) : left - 1;
-        const uint32_t upto = ~((0xFFFFFFFFu >> (2 * last)) >> 2);       // visits 0..last
-        const uint32_t code = (bits << (2 * last)) >> 30;
+        const int last = stop ? (REV ? (__ffs(stop) - 1) >> 1 : __clz(stop) >> 1) : left - 1;
+        const uint32_t upto = REV ? 0xFFFFFFFFu >> (30 - 2 * last)              // visits 0..last
+                                  : ~((0xFFFFFFFFu >> (2 * last)) >> 2);
+        const uint32_t code = REV ? (bits >> (2 * last)) & 3u : (bits << (2 * last)) >> 30;
         const uint32_t nf = w.nf + __popc(bits & ~(bits >> 1) & upto & 0x55555555u);   // codes 01 only
         const uint32_t o = code == 2u, out = code == 3u;
         const uint32_t l = (uint32_t)(w.s - w.s0 + last + 1) - out;      // in-grid lookups
